@@ -1,0 +1,1477 @@
+// engine.cpp -- host orchestration of the B200 tmatch hot path behind the C ABI
+// (include/tmatch_cuda.h).  C++ host code; all arithmetic on images runs in the sm_100a
+// kernels of k_*.cu, the host only sequences them and runs the scalar decisions the
+// reference makes between passes (EGS accept/stop, OptA accept, repair fixed point).
+//
+// Reference control flow mirrored here (file:line in /root/reference/proj/src):
+//   window_stats            stats.cpp:55-94        -> WS cache per (image, m, n)
+//   efficient_group_size    egs.cpp:39-91          -> run_egs_search()
+//   optimize_autocorrelation blur.cpp:243-278      -> run_opta_prep()
+//   repair_to_fixed_point   blur.cpp:208-239       -> repair()
+//   transitive_search_impl  matcher.cpp:95-177     -> search()
+//   refine_impl             matcher.cpp:80-93      -> refine()
+//   match / prepare / run   matcher.cpp:205-307    -> tm_prepare / tm_run / tm_match
+//
+// Compile with -ffp-contract=off: the few host-side FP64 expressions (template stats,
+// thresholds, costs) follow the reference's evaluation order.
+#include <algorithm>
+#include <chrono>
+#include <climits>
+#include <cmath>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "kernels.hpp"
+#include "tmatch_cuda.h"
+
+namespace {
+
+thread_local std::string g_err;
+
+struct TmError {
+    int code;
+    std::string msg;
+};
+
+[[noreturn]] void invalid(const std::string& msg) { throw TmError{TM_EINVAL, msg}; }
+
+void ck(cudaError_t e, const char* what) {
+    if (e != cudaSuccess) throw TmError{TM_ECUDA, std::string(what) + ": " + cudaGetErrorString(e)};
+}
+#define CK(x) ck((x), #x)
+
+constexpr double kEps = 2.220446049250313e-16;
+
+template <class T>
+struct DBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    DBuf() = default;
+    DBuf(const DBuf&) = delete;
+    DBuf& operator=(const DBuf&) = delete;
+    ~DBuf() { release(); }
+    void ensure(size_t n) {
+        if (n <= cap && p) return;
+        release();
+        CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+        cap = std::max<size_t>(n, 1);
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    void swap(DBuf& o) {
+        std::swap(p, o.p);
+        std::swap(cap, o.cap);
+    }
+};
+
+// detail.hpp:18-22
+bool variance_is_flat_h(double var_sum, double q_sum, long long mn) {
+    const double abs_tol = 1e-9 * double(mn);
+    const double rel = std::max(1e-13, 4.0 * kEps * double(mn));
+    return var_sum <= std::max(abs_tol * abs_tol, rel * q_sum);
+}
+
+double clampd(double v, double lo, double hi) { return std::clamp(v, lo, hi); }
+
+// bounds.cpp:13-17
+double checked(double rho, const char* name) {
+    if (std::abs(rho) > 1.0 + 1e-9) invalid(std::string("correlation out of [-1,1]: ") + name);
+    return clampd(rho, -1.0, 1.0);
+}
+
+// bounds.cpp:48-59
+double elimination_autocorr_threshold_h(double rho_tb, double rho_tc) {
+    const double tb = checked(rho_tb, "rho_tb");
+    const double tc = checked(rho_tc, "rho_tc");
+    const double radicand = 1.0 + tc * tc * tb * tb - (tc * tc + tb * tb);
+    return tb * tc + std::sqrt(std::max(0.0, radicand));
+}
+double expected_elimination_threshold_h(double rho_tb) {
+    const double tb = checked(rho_tb, "rho_tb");
+    return std::sqrt(std::max(0.0, 1.0 - tb * tb));
+}
+
+bool better_h(const tmk::CellH& a, const tmk::CellH& b) {
+    if (!(a.flags & 1)) return false;
+    if (!(b.flags & 1)) return true;
+    const bool da = a.flags & 2, db = b.flags & 2;
+    if (da != db) return !da;
+    if (a.rho != b.rho) return a.rho > b.rho;
+    if (a.row != b.row) return a.row < b.row;
+    return a.col < b.col;
+}
+
+double ms_between(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+// ==== context ========================================================================
+struct WS {
+    DBuf<double> mu, om;
+    DBuf<uint8_t> fl;
+    int er = 0, ec = 0, m = 0, n = 0;
+    tmk::DevStats dev() const { return tmk::DevStats{mu.p, om.p, fl.p, er, ec, m, n}; }
+};
+
+struct tm_ctx {
+    int device = 0;
+    cudaStream_t s = nullptr;
+    std::mutex mu;
+    int64_t launches = 0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+    // scratch (grow-only)
+    DBuf<int> hs, hq, markP;
+    DBuf<double> rowacc, prefix, S, Q, fid, cross, inwin, dtmp;
+    DBuf<uint8_t> u8tmp, marks;
+    DBuf<tmk::CellH> partials, cells;
+    DBuf<double> thr, seq_rho, rec_T, prof;
+    DBuf<tmk::Tally> tally;
+    DBuf<unsigned long long> counters, rec_key;
+    DBuf<int2> locs, seed_locs;
+    DBuf<uint8_t> seq_deg, seeded, deg_c, visits;
+    DBuf<double> rho_c, surface;
+    DBuf<float> tf;
+    DBuf<double> td;
+    DBuf<int> rows_list;
+    DBuf<double> map_tmp, map_user;
+    unsigned long long* h_pinned = nullptr;  // small pinned staging
+    void add(int k) { launches += k; }
+};
+
+struct tm_image {
+    tm_ctx* ctx = nullptr;
+    int p = 0, q = 0;
+    bool integer = false;
+    DBuf<uint8_t> u8;
+    DBuf<float> f32;
+    int pitch = 0;
+    DBuf<double> f64;
+    bool have_f64 = false;
+    bool have_qtotal = false;
+    double q_total = 0.0;
+    std::map<std::pair<int, int>, std::unique_ptr<WS>> ws_cache;
+};
+
+struct tm_prep {
+    tm_match_params params{};
+    std::vector<double> profile;
+    int mode = TM_MODE_EGS;
+    int m = 0, n = 0, h = 0, w = 0;
+    tmk::GridDesc g{};
+    DBuf<double> map;
+    std::unique_ptr<tm_image> search_img;  // OptA: optimised image (owned)
+    std::unique_ptr<WS> search_ws;          // OptA: window stats of the optimised image
+    int kappa = 0, radius = 0;
+    double lambda = 1.0;
+    tm_egs_iter cost{};
+    std::vector<tm_egs_iter> egs_trace;
+    std::vector<tm_opta_iter> opta_trace;
+    double prep_ms = 0.0;
+    tm_image* source = nullptr;  // not owned
+};
+
+namespace {
+
+tmk::GridDesc make_grid(int er, int ec, int h, int w) {
+    if (er < 1 || ec < 1) invalid("group grid: empty search extent");
+    if (h < 1 || w < 1 || h % 2 == 0 || w % 2 == 0)
+        invalid("group grid: group size must be odd and >= 1");
+    return tmk::GridDesc{er, ec, h, w, (er + h - 1) / h, (ec + w - 1) / w};
+}
+
+int centre_row_h(const tmk::GridDesc& g, int ti) {
+    const int r0 = ti * g.h, r1 = std::min(r0 + g.h, g.er) - 1;
+    return (r0 + r1) / 2;
+}
+int centre_col_h(const tmk::GridDesc& g, int tj) {
+    const int c0 = tj * g.w, c1 = std::min(c0 + g.w, g.ec) - 1;
+    return (c0 + c1) / 2;
+}
+
+// ---- images ----------------------------------------------------------------------------
+void finish_integer_image(tm_ctx* ctx, tm_image* img) {
+    img->pitch = ((img->q + 3) & ~3) + 128;  // zero pad: vector loads past the last column
+    img->f32.ensure(size_t(img->p) * img->pitch);
+    CK(tmk::u8_to_f32_pitched(img->u8.p, img->p, img->q, img->f32.p, img->pitch, ctx->s));
+    ctx->add(1);
+}
+
+void ensure_f64(tm_ctx* ctx, tm_image* img) {
+    if (img->have_f64) return;
+    img->f64.ensure(size_t(img->p) * img->q);
+    CK(tmk::u8_to_f64(img->u8.p, size_t(img->p) * img->q, img->f64.p, ctx->s));
+    ctx->add(1);
+    img->have_f64 = true;
+}
+
+// Adopt a device FP64 raster (already in img->f64); classify and derive the u8/f32 views.
+void classify_device_image(tm_ctx* ctx, tm_image* img) {
+    const size_t N = size_t(img->p) * img->q;
+    int* bad = reinterpret_cast<int*>(ctx->counters.p);
+    CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->s));
+    CK(tmk::check_u8_domain(img->f64.p, N, bad, ctx->s));
+    int hbad = 0;
+    CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    ctx->add(1);
+    img->have_f64 = true;
+    img->integer = hbad == 0;
+    if (img->integer) {
+        img->u8.ensure(N);
+        CK(tmk::f64_to_u8(img->f64.p, N, img->u8.p, ctx->s));
+        ctx->add(1);
+        finish_integer_image(ctx, img);
+    }
+}
+
+double image_q_total(tm_ctx* ctx, tm_image* img) {
+    if (img->have_qtotal) return img->q_total;
+    const size_t N = size_t(img->p) * img->q;
+    if (img->integer) {
+        CK(tmk::sum_sq_u8(img->u8.p, N, ctx->counters.p + 1, ctx->s));
+        unsigned long long v = 0;
+        CK(cudaMemcpyAsync(&v, ctx->counters.p + 1, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        img->q_total = double(v);  // exact: the reference's sequential sum of integers
+    } else {
+        double* d = reinterpret_cast<double*>(ctx->counters.p + 1);
+        CK(tmk::sum_sq_f64(img->f64.p, N, d, ctx->s));
+        double v = 0;
+        CK(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        img->q_total = v;
+    }
+    ctx->add(1);
+    img->have_qtotal = true;
+    return img->q_total;
+}
+
+// Replica prefix over a product source; the full window-sum table lands in `out`.
+void replica_sums(tm_ctx* ctx, tmk::ProdSrc src, int rows, int cols, int m, int n, double* out) {
+    ctx->rowacc.ensure(size_t(rows) * cols);
+    ctx->prefix.ensure(size_t(rows + 1) * (cols + 1));
+    CK(tmk::replica_prefix(src, rows, cols, ctx->rowacc.p, ctx->prefix.p, ctx->s));
+    CK(tmk::replica_window_diff(ctx->prefix.p, rows, cols, m, n, out, ctx->s));
+    ctx->add(3);
+}
+
+// window_stats (stats.cpp:55-94) into `ws`.
+void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
+    const int p = img->p, q = img->q;
+    if (m < 1 || n < 1 || m > p || n > q) invalid("running_sum: window does not fit the source");
+    const int er = p - m + 1, ec = q - n + 1;
+    const size_t E = size_t(er) * ec;
+    ws.mu.ensure(E);
+    ws.om.ensure(E);
+    ws.fl.ensure(E);
+    ws.er = er;
+    ws.ec = ec;
+    ws.m = m;
+    ws.n = n;
+    const double prefix_noise = double(p + q) * kEps * image_q_total(ctx, img);
+    if (img->integer) {
+        ctx->hs.ensure(size_t(p) * ec);
+        ctx->hq.ensure(size_t(p) * ec);
+        CK(tmk::window_stats_u8(img->u8.p, p, q, m, n, prefix_noise, ctx->hs.p, ctx->hq.p, ws.dev(),
+                                ctx->s));
+        ctx->add(2);
+    } else {
+        ctx->S.ensure(E);
+        ctx->Q.ensure(E);
+        replica_sums(ctx, tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 0}, p, q, m, n,
+                     ctx->S.p);
+        replica_sums(ctx, tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 1}, p, q, m, n,
+                     ctx->Q.p);
+        CK(tmk::stats_from_sums(ctx->S.p, ctx->Q.p, E, m, n, prefix_noise, ws.dev(), ctx->s));
+        ctx->add(1);
+    }
+}
+
+WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
+    auto key = std::make_pair(m, n);
+    auto it = img->ws_cache.find(key);
+    if (it != img->ws_cache.end()) return *it->second;
+    auto ws = std::make_unique<WS>();
+    compute_ws(ctx, img, m, n, *ws);
+    WS& ref = *ws;
+    img->ws_cache[key] = std::move(ws);
+    return ref;
+}
+
+// ---- templates ---------------------------------------------------------------------------
+struct Tmpl {
+    int m = 0, n = 0, npad = 0;
+    bool integer = false;
+    tmk::TStatsH ts{};
+    int flush_rows = 0;
+};
+
+// template_stats (stats.cpp:98-111) in reference order, then upload.
+Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n) {
+    Tmpl T;
+    T.m = m;
+    T.n = n;
+    T.npad = (n + 15) & ~15;
+    double sum = 0.0, sq = 0.0;
+    bool integer = true;
+    for (size_t i = 0; i < size_t(m) * n; ++i) {
+        sum += t[i];
+        sq += t[i] * t[i];
+        if (!(t[i] >= 0.0 && t[i] <= 255.0) || t[i] != std::rint(t[i])) integer = false;
+    }
+    const long long mn = (long long)m * n;
+    const double var_sum = sq - sum * sum / double(mn);
+    T.ts.mu = sum / double(mn);
+    T.ts.omega = std::sqrt(std::max(0.0, var_sum));
+    T.ts.flat = variance_is_flat_h(var_sum, sq, mn);
+    T.ts.mn = double(m) * double(n);
+    T.integer = integer;
+    T.flush_rows = int(16777216LL / (65025LL * n));
+    std::vector<float> tf(size_t(m) * T.npad, 0.f);
+    for (int i = 0; i < m; ++i)
+        for (int j = 0; j < n; ++j) tf[size_t(i) * T.npad + j] = float(t[size_t(i) * n + j]);
+    ctx->tf.ensure(tf.size());
+    ctx->td.ensure(size_t(m) * n);
+    CK(cudaMemcpyAsync(ctx->tf.p, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaMemcpyAsync(ctx->td.p, t, size_t(m) * n * 8, cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));  // host vectors go out of scope
+    return T;
+}
+
+bool fp32_path(const tm_image* img, const Tmpl& T) {
+    return img->integer && T.integer && T.flush_rows >= 1;
+}
+
+tmk::CorrJob make_job(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
+    tmk::CorrJob j{};
+    const bool fp32 = fp32_path(img, T);
+    if (!fp32) ensure_f64(ctx, img);
+    j.imgf = img->f32.p;
+    j.pitch = img->pitch;
+    j.imgd = img->f64.p;
+    j.q = img->q;
+    j.tf = ctx->tf.p;
+    j.npad = T.npad;
+    j.td = ctx->td.p;
+    j.m = T.m;
+    j.n = T.n;
+    j.flush_rows = std::max(1, T.flush_rows);
+    j.ts = T.ts;
+    j.st = ws.dev();
+    return j;
+}
+
+int nw_for(int sw) { return sw == 1 ? 4 : (sw == 3 ? 2 : 1); }
+
+int band_partials(int nrows, int nc, int sw) {
+    const int nw = nw_for(sw);
+    return ((nc + nw * 32 - 1) / (nw * 32)) * ((nrows + 7) / 8);
+}
+
+int row_span(const std::vector<int>& rows) {
+    int span = 0;
+    for (size_t yb = 0; yb < rows.size(); yb += 8) {
+        const size_t yl = std::min(rows.size() - 1, yb + 7);
+        span = std::max(span, rows[yl] - rows[yb]);
+    }
+    return span;
+}
+
+void upload_rows(tm_ctx* ctx, const std::vector<int>& rows) {
+    ctx->rows_list.ensure(rows.size());
+    CK(cudaMemcpyAsync(ctx->rows_list.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice,
+                       ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+}
+
+constexpr int kListBlocks = 148 * 4;
+
+// Reduce `n` partial cells to ctx->cells[slot].
+void reduce_to(tm_ctx* ctx, int n, int slot) {
+    if (n <= 0) {
+        tmk::CellH none{0.0, -1, -1, 2};
+        CK(cudaMemcpyAsync(ctx->cells.p + slot, &none, sizeof none, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        return;
+    }
+    CK(tmk::reduce_cells(ctx->partials.p, n, ctx->cells.p + slot, ctx->s));
+    ctx->add(1);
+}
+
+// Evaluate a device location list (count on device) -> cells[slot].
+void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const int2* locs,
+               const unsigned long long* count, int max_count, double* out_rho,
+               uint8_t* out_deg, int slot) {
+    const tmk::CorrJob job = make_job(ctx, img, ws, T);
+    ctx->partials.ensure(kListBlocks);
+    if (fp32_path(img, T))
+        CK(tmk::corr_list(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
+                          kListBlocks, ctx->s));
+    else
+        CK(tmk::corr_list_f64(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
+                              kListBlocks, ctx->s));
+    ctx->add(1);
+    reduce_to(ctx, kListBlocks, slot);
+}
+
+// ---- scan 1: every group centre (matcher.cpp:23-37) -> rho_c, deg_c, cells[0] --------
+void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                 const tmk::GridDesc& g) {
+    const size_t G = size_t(g.tr) * g.tc;
+    ctx->rho_c.ensure(G);
+    ctx->deg_c.ensure(G);
+    const tmk::CorrJob job = make_job(ctx, img, ws, T);
+    const int wr = g.w / 2;
+    if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
+        std::vector<int> rows(g.tr);
+        for (int ti = 0; ti < g.tr; ++ti) rows[ti] = centre_row_h(g, ti);
+        upload_rows(ctx, rows);
+        const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
+        const int nc_reg = clipped ? g.tc - 1 : g.tc;
+        const int np_main = nc_reg > 0 ? band_partials(g.tr, nc_reg, g.w) : 0;
+        const int np_last = clipped ? band_partials(g.tr, 1, 1) : 0;
+        ctx->partials.ensure(size_t(np_main + np_last) + 1);
+        int n1 = 0, n2 = 0;
+        tmk::BandTask t{};
+        t.rows = ctx->rows_list.p;
+        t.nrows = g.tr;
+        t.mode = 1;
+        t.row_span = row_span(rows);
+        t.tc = g.tc;
+        t.out_rho = ctx->rho_c.p;
+        t.out_deg = ctx->deg_c.p;
+        if (nc_reg > 0) {
+            t.cbase = wr;
+            t.sw = g.w;
+            t.nc = nc_reg;
+            t.col0 = 0;
+            CK(tmk::corr_band(job, t, ctx->partials.p, &n1, ctx->s));
+            ctx->add(1);
+        }
+        if (clipped) {
+            t.cbase = centre_col_h(g, g.tc - 1);
+            t.sw = 1;
+            t.nc = 1;
+            t.col0 = g.tc - 1;
+            CK(tmk::corr_band(job, t, ctx->partials.p + n1, &n2, ctx->s));
+            ctx->add(1);
+        }
+        reduce_to(ctx, n1 + n2, 0);
+        return;
+    }
+    // general path: explicit centre list in grid order
+    std::vector<int2> locs(G);
+    for (int ti = 0; ti < g.tr; ++ti)
+        for (int tj = 0; tj < g.tc; ++tj)
+            locs[size_t(ti) * g.tc + tj] = make_int2(centre_row_h(g, ti), centre_col_h(g, tj));
+    ctx->seed_locs.ensure(G);
+    CK(cudaMemcpyAsync(ctx->seed_locs.p, locs.data(), G * sizeof(int2), cudaMemcpyHostToDevice,
+                       ctx->s));
+    unsigned long long cnt = G;
+    CK(cudaMemcpyAsync(ctx->counters.p + 4, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(G), ctx->rho_c.p,
+              ctx->deg_c.p, 0);
+}
+
+// ---- EGS: local auto-correlation + retained count ----------------------------------------
+long long autocorr_map(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
+                       double thr, double* map) {
+    const int m = ws.m, n = ws.n, p = img->p, q = img->q;
+    unsigned long long* nr = ctx->counters.p + 2;
+    CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
+    if (img->integer) {
+        CK(tmk::autocorr_u8(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
+        ctx->add(1);
+    } else {
+        CK(tmk::autocorr_init(map, g, ctx->s));
+        ctx->add(1);
+        const int hr = g.h / 2, wr = g.w / 2;
+        for (int di = -hr; di <= hr; ++di)
+            for (int dj = -wr; dj <= wr; ++dj) {
+                if (di == 0 && dj == 0) continue;
+                const int orr = std::max(0, -di), occ = std::max(0, -dj);
+                const int ph = p - std::abs(di), pw = q - std::abs(dj);
+                if (ph < m || pw < n) continue;
+                ctx->rowacc.ensure(size_t(ph) * pw);
+                ctx->prefix.ensure(size_t(ph + 1) * (pw + 1));
+                tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0};
+                CK(tmk::replica_prefix(src, ph, pw, ctx->rowacc.p, ctx->prefix.p, ctx->s));
+                CK(tmk::autocorr_offset_epilogue(ctx->prefix.p, ph, pw, m, n, g, ws.dev(), di, dj,
+                                                 map, ctx->s));
+                ctx->add(3);
+            }
+        CK(tmk::retained_count(map, g, thr, nr, ctx->s));
+        ctx->add(1);
+    }
+    unsigned long long v = 0;
+    CK(cudaMemcpyAsync(&v, nr, 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return (long long)v;
+}
+
+// total_cost (egs.cpp:27-37)
+tm_egs_iter total_cost_h(int er, int ec, int h, int w, long long n_r, double amortized) {
+    if (h < 1 || w < 1) invalid("total_cost: group size must be >= 1");
+    tm_egs_iter it{};
+    it.h = h;
+    it.w = w;
+    it.central = double((er + h - 1) / h) * double((ec + w - 1) / w);
+    it.retained = n_r;
+    it.retained_cost = double(n_r);
+    it.amortized = amortized;
+    it.total = it.central + it.retained_cost + it.amortized;
+    return it;
+}
+
+struct EgsOut {
+    int h = 0, w = 0;
+    tm_egs_iter cost{};
+    std::vector<tm_egs_iter> trace;
+};
+
+// efficient_group_size (egs.cpp:39-91); best map ends in `best`.
+EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, int h0, int w0,
+                      double rho_tb, double xi, int max_group, DBuf<double>& best) {
+    if (h0 < 1 || w0 < 1 || h0 % 2 == 0 || w0 % 2 == 0)
+        invalid("efficient_group_size: initial group size must be odd");
+    if (rho_tb <= 0.0 || rho_tb >= 1.0)
+        invalid("efficient_group_size: rho_tb must be in (0,1)");
+    const int er = img->p - m + 1, ec = img->q - n + 1;
+    if (er < 1 || ec < 1) invalid("efficient_group_size: template does not fit");
+    if (rho_tb < 0.0 || rho_tb > 1.0) invalid("retained_count: rho_tb must be in [0,1]");
+    const double thr = expected_elimination_threshold_h(rho_tb);
+    int cap = max_group > 0 ? max_group : INT_MAX;
+    if (cap % 2 == 0) ++cap;
+    const size_t E = size_t(er) * ec;
+    best.ensure(E);
+    ctx->map_tmp.ensure(E);
+    EgsOut out;
+    double prev_cost = std::numeric_limits<double>::infinity();
+    int h = h0, w = w0;
+    for (;;) {
+        const tmk::GridDesc g = make_grid(er, ec, h, w);
+        const long long n_r = autocorr_map(ctx, img, ws, g, thr, ctx->map_tmp.p);
+        const tm_egs_iter cost = total_cost_h(er, ec, h, w, n_r, 0.0);
+        const bool accepted =
+            !std::isfinite(prev_cost) || prev_cost - cost.total > xi * prev_cost;
+        if (!accepted) break;
+        out.h = h;
+        out.w = w;
+        out.cost = cost;
+        out.trace.push_back(cost);
+        best.swap(ctx->map_tmp);
+        ctx->map_tmp.ensure(E);
+        prev_cost = cost.total;
+        if ((h >= er && w >= ec) || (h >= cap && w >= cap)) break;
+        h = std::min(h + 2, cap);
+        w = std::min(w + 2, cap);
+    }
+    return out;
+}
+
+// ---- OptA -----------------------------------------------------------------------------
+double quality_threshold_h(double rho_th, double rho_max) {
+    if (rho_th < 0.0 || rho_th > 1.0 || rho_max < 0.0 || rho_max > 1.0)
+        invalid("quality_threshold: inputs must be in [0,1]");
+    if (rho_max < rho_th) invalid("quality_threshold: rho_max must be >= rho_th");
+    return elimination_autocorr_threshold_h(rho_th, rho_max);
+}
+
+std::unique_ptr<tm_image> device_image_like(tm_ctx* ctx, int p, int q) {
+    auto img = std::make_unique<tm_image>();
+    img->ctx = ctx;
+    img->p = p;
+    img->q = q;
+    img->f64.ensure(size_t(p) * q);
+    img->have_f64 = true;
+    return img;
+}
+
+void fidelity(tm_ctx* ctx, tm_image* orig, const WS& ws_orig, tm_image* blurred, WS& ws_b,
+              double* fid) {
+    const int p = orig->p, q = orig->q, m = ws_orig.m, n = ws_orig.n;
+    const size_t E = size_t(ws_orig.er) * ws_orig.ec;
+    ctx->cross.ensure(E);
+    // product = I_blur * I (blur.cpp:101-103)
+    replica_sums(ctx, tmk::ProdSrc{blurred->f64.p, q, 0, 0, orig->f64.p, q, 0, 0, 0}, p, q, m, n,
+                 ctx->cross.p);
+    blurred->have_qtotal = false;
+    compute_ws(ctx, blurred, m, n, ws_b);
+    CK(tmk::fidelity_epilogue(ctx->cross.p, ws_orig.dev(), ws_b.dev(), fid, ctx->s));
+    ctx->add(1);
+}
+
+// repair_to_fixed_point (blur.cpp:208-239); leaves ws_b = window_stats(final blurred).
+long long repair(tm_ctx* ctx, tm_image* blurred, tm_image* orig, const WS& ws_orig, double lambda,
+                 WS& ws_b) {
+    const int p = orig->p, q = orig->q, m = ws_orig.m, n = ws_orig.n;
+    const int er = ws_orig.er, ec = ws_orig.ec;
+    const size_t E = size_t(er) * ec, N = size_t(p) * q;
+    ctx->fid.ensure(E);
+    ctx->inwin.ensure(E);
+    ctx->u8tmp.ensure(N);
+    ctx->marks.ensure(E);
+    ctx->markP.ensure(size_t(er + 1) * (ec + 1));
+    ctx->hs.ensure(size_t(p) * ec);
+    long long total = 0;
+    for (;;) {
+        fidelity(ctx, orig, ws_orig, blurred, ws_b, ctx->fid.p);
+        CK(tmk::changed_mask(blurred->f64.p, orig->f64.p, N, ctx->u8tmp.p, ctx->s));
+        CK(tmk::window_sums_u8(ctx->u8tmp.p, p, q, m, n, ctx->hs.p, ctx->inwin.p, ctx->s));
+        CK(tmk::mark_violations(ctx->fid.p, ctx->inwin.p, E, lambda, ctx->marks.p,
+                                ctx->counters.p + 3, ctx->s));
+        ctx->add(4);
+        unsigned long long count = 0;
+        CK(cudaMemcpyAsync(&count, ctx->counters.p + 3, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        if (count == 0) break;
+        CK(tmk::restore_covered(blurred->f64.p, orig->f64.p, ctx->marks.p, er, ec, m, n, p, q,
+                                ctx->markP.p, ctx->s));
+        ctx->add(3);
+        total += (long long)count;
+    }
+    return total;
+}
+
+// optimize_autocorrelation (blur.cpp:243-278) + prepare_opta (matcher.cpp:217-233).
+void run_opta_prep(tm_ctx* ctx, tm_image* img, tm_prep* prep) {
+    const tm_match_params& P = prep->params;
+    const int m = prep->m, n = prep->n, p = img->p, q = img->q;
+    const double lambda = quality_threshold_h(P.rho_th, P.rho_max);
+    WS& ws_orig = get_ws(ctx, img, m, n);
+    ensure_f64(ctx, img);
+    EgsOut e0 = run_egs_search(ctx, img, ws_orig, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
+                               P.max_group, prep->map);
+    prep->lambda = lambda;
+    prep->kappa = 0;
+    prep->opta_trace.clear();
+    prep->opta_trace.push_back(tm_opta_iter{e0.h, e0.w, e0.cost.total, 0});
+    double prev_cost = e0.cost.total;
+    int h = e0.h, w = e0.w;
+    prep->h = h;
+    prep->w = w;
+    prep->cost = e0.cost;
+    prep->egs_trace = e0.trace;
+
+    const size_t N = size_t(p) * q;
+    ctx->prof.ensure(prep->profile.size());
+    CK(cudaMemcpyAsync(ctx->prof.p, prep->profile.data(), prep->profile.size() * 8,
+                       cudaMemcpyHostToDevice, ctx->s));
+    const int len = int(prep->profile.size());
+    const bool identity = (len == 1);  // blur.cpp:59: radius 0 and one tap returns img
+    auto current = device_image_like(ctx, p, q);
+    CK(cudaMemcpyAsync(current->f64.p, img->f64.p, N * 8, cudaMemcpyDeviceToDevice, ctx->s));
+    std::unique_ptr<tm_image> accepted;  // optimised image (nullptr: the original)
+    std::unique_ptr<WS> accepted_ws;
+    DBuf<double> map_k;
+    ctx->dtmp.ensure(N);
+    for (int iter = 1; iter <= 64; ++iter) {
+        auto blurred = device_image_like(ctx, p, q);
+        if (identity) {
+            CK(cudaMemcpyAsync(blurred->f64.p, current->f64.p, N * 8, cudaMemcpyDeviceToDevice,
+                               ctx->s));
+        } else {
+            CK(tmk::blur_replica(current->f64.p, p, q, ctx->prof.p, len, ctx->dtmp.p,
+                                 blurred->f64.p, ctx->s));
+            ctx->add(2);
+        }
+        auto ws_b = std::make_unique<WS>();
+        const long long restored = repair(ctx, blurred.get(), img, ws_orig, lambda, *ws_b);
+        // efficient_group_size(blurred) recomputes window_stats(blurred) == ws_b
+        blurred->integer = false;
+        EgsOut ek = run_egs_search(ctx, blurred.get(), *ws_b, m, n, h, w, P.rho_th, P.xi_fraction,
+                                   P.max_group, map_k);
+        const double improvement = prev_cost - ek.cost.total;
+        if (!(improvement >= P.opta_margin * ek.cost.total)) break;
+        prep->opta_trace.push_back(tm_opta_iter{ek.h, ek.w, ek.cost.total, restored});
+        prep->kappa = iter;
+        prev_cost = ek.cost.total;
+        h = ek.h;
+        w = ek.w;
+        prep->h = h;
+        prep->w = w;
+        prep->cost = ek.cost;
+        prep->egs_trace = ek.trace;
+        prep->map.swap(map_k);
+        // the accepted image becomes the next iteration's input
+        auto cur_copy = device_image_like(ctx, p, q);
+        CK(cudaMemcpyAsync(cur_copy->f64.p, blurred->f64.p, N * 8, cudaMemcpyDeviceToDevice,
+                           ctx->s));
+        current = std::move(cur_copy);
+        accepted = std::move(blurred);
+        accepted_ws = std::move(ws_b);
+    }
+    if (accepted) {
+        // classify (an exact-integer optimised image would take the integer kernels)
+        accepted->have_qtotal = false;
+        classify_device_image(ctx, accepted.get());
+        if (accepted->integer) accepted_ws.reset();  // recompute through the integer path
+        prep->search_img = std::move(accepted);
+        if (accepted_ws) {
+            prep->search_ws = std::move(accepted_ws);
+        } else {
+            prep->search_ws = std::make_unique<WS>();
+            compute_ws(ctx, prep->search_img.get(), m, n, *prep->search_ws);
+        }
+    }
+    prep->radius = len / 2;
+    CK(cudaStreamSynchronize(ctx->s));
+}
+
+// ---- scan 2 / transitive search (matcher.cpp:95-177) -----------------------------------
+struct SearchIn {
+    tm_image* img;
+    const WS* ws;
+    tmk::GridDesc g;
+    const double* map;  // device
+};
+
+tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
+                       const tm_match_params& P, uint8_t* visits_host) {
+    const tmk::GridDesc& g = in.g;
+    if (T.ts.flat) invalid("transitive_search: constant template has no defined correlation");
+    if (P.has_init_threshold && std::abs(P.init_threshold) > 1.0 + 1e-9)
+        invalid("transitive_search: init threshold out of [-1,1]");
+    const size_t E = size_t(g.er) * g.ec, G = size_t(g.tr) * g.tc;
+    tm_image* img = in.img;
+    const WS& ws = *in.ws;
+    cudaStream_t s = ctx->s;
+
+    int policy = P.policy;
+    if (policy == TM_POLICY_REFERENCE)
+        policy = (P.parallel && P.threads > 1 && G > 1) ? TM_POLICY_FROZEN : TM_POLICY_SEQUENTIAL;
+
+    centre_scan(ctx, img, ws, T, g);
+    CK(tmk::threshold_init(ctx->cells.p + 0, P.has_init_threshold, P.init_threshold,
+                           ctx->thr.p, s));
+    ctx->add(1);
+    double T0 = 0.0;
+    CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+
+    const uint8_t* seeded = nullptr;
+    if (policy == TM_POLICY_SEEDED) {
+        const unsigned long long max_groups = 256;
+        const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
+        ctx->seed_locs.ensure(max_locs);
+        ctx->seeded.ensure(G);
+        CK(cudaMemsetAsync(ctx->counters.p + 4, 0, 16, s));
+        CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, P.seed_margin,
+                             ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
+                             ctx->counters.p + 5, max_groups, s));
+        ctx->add(1);
+        eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs), nullptr,
+                  nullptr, 1);
+        CK(tmk::threshold_raise(ctx->cells.p + 1, ctx->thr.p, s));
+        ctx->add(1);
+        seeded = ctx->seeded.p;
+    }
+
+    uint8_t* visits = nullptr;
+    if (visits_host) {
+        ctx->visits.ensure(E);
+        visits = ctx->visits.p;
+    }
+    ctx->locs.ensure(E);
+    CK(cudaMemsetAsync(ctx->tally.p, 0, sizeof(tmk::Tally), s));
+    CK(tmk::sec_compact(g, in.map, ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, ctx->thr.p,
+                        seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
+    ctx->add(1);
+    const unsigned long long* count = &ctx->tally.p->survivors;
+    const bool seq = policy == TM_POLICY_SEQUENTIAL;
+    if (seq) {
+        ctx->seq_rho.ensure(E);
+        ctx->seq_deg.ensure(E);
+    }
+    eval_list(ctx, img, ws, T, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
+              seq ? ctx->seq_rho.p : nullptr, seq ? ctx->seq_deg.p : nullptr, 2);
+
+    double final_T = T0;
+    tmk::Tally tally{};
+    if (seq) {
+        // Replay the running threshold: records in scan order (see k_first_record).
+        std::vector<unsigned long long> rk;
+        std::vector<double> rt;
+        double Tcur = T0;
+        unsigned long long after = ~0ull;
+        for (;;) {
+            CK(tmk::first_record(g, ctx->locs.p, count, ctx->seq_rho.p, ctx->seq_deg.p, in.map,
+                                 ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, Tcur, after,
+                                 ctx->counters.p + 6, s));
+            ctx->add(1);
+            unsigned long long key = 0;
+            CK(cudaMemcpyAsync(&key, ctx->counters.p + 6, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (key == ~0ull) break;
+            double rho = 0.0;
+            CK(tmk::fetch_record_rho(g, ctx->locs.p, count, ctx->seq_rho.p, key,
+                                     ctx->thr.p + 1, s));
+            ctx->add(1);
+            CK(cudaMemcpyAsync(&rho, ctx->thr.p + 1, 8, cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            rk.push_back(key);
+            rt.push_back(rho);
+            Tcur = rho;
+            after = key;
+        }
+        ctx->rec_key.ensure(rk.size() + 1);
+        ctx->rec_T.ensure(rk.size() + 1);
+        if (!rk.empty()) {
+            CK(cudaMemcpyAsync(ctx->rec_key.p, rk.data(), rk.size() * 8, cudaMemcpyHostToDevice, s));
+            CK(cudaMemcpyAsync(ctx->rec_T.p, rt.data(), rt.size() * 8, cudaMemcpyHostToDevice, s));
+        }
+        ctx->partials.ensure(kListBlocks);
+        CK(tmk::seq_final(g, ctx->locs.p, count, ctx->seq_rho.p, ctx->seq_deg.p, in.map,
+                          ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, T0, ctx->rec_key.p,
+                          ctx->rec_T.p, int(rk.size()), ctx->tally.p, visits, ctx->partials.p,
+                          kListBlocks, s));
+        ctx->add(1);
+        reduce_to(ctx, kListBlocks, 2);
+        final_T = Tcur;
+    }
+    tmk::CellH cells[3];
+    CK(cudaMemcpyAsync(cells, ctx->cells.p, sizeof cells, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
+    double thr_after = 0.0;
+    CK(cudaMemcpyAsync(&thr_after, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+    if (visits_host) CK(cudaMemcpyAsync(visits_host, visits, E, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+
+    tmk::CellH best = cells[0];
+    if (policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
+    if (better_h(cells[2], best)) best = cells[2];
+
+    long long eliminated = (long long)tally.eliminated;
+    long long retained = (long long)tally.retained;
+    if (seq) retained = (long long)tally.pad;  // alive candidates; dead ones were added
+                                                // to eliminated by seq_final
+    if (policy == TM_POLICY_SEEDED) {
+        final_T = thr_after;
+        if (better_h(cells[2], cells[1]) && (cells[2].flags & 1) && !(cells[2].flags & 2))
+            final_T = std::max(final_T, cells[2].rho);
+    }
+    tm_match_result r{};
+    r.mode = TM_MODE_EGS;
+    r.extent_rows = g.er;
+    r.extent_cols = g.ec;
+    r.best_row = r.refined_row = best.row;
+    r.best_col = r.refined_col = best.col;
+    r.best_rho = r.refined_rho = best.rho;
+    r.best_degenerate = (best.flags & 2) != 0;
+    r.final_threshold = std::isfinite(final_T) ? final_T : 0.0;
+    r.below_threshold =
+        P.has_init_threshold && (r.best_degenerate || best.rho < P.init_threshold);
+    r.centers = (long long)G;
+    r.eliminated = eliminated;
+    r.retained = retained;
+    r.elim_pct = 100.0 * double(eliminated) / (double(g.er) * double(g.ec));
+    r.ops = (long long)G + retained;
+    return r;
+}
+
+// refine_impl (matcher.cpp:80-93) on the original image.
+tmk::CellH refine(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, int lr, int lc, int d,
+                  long long* ops) {
+    const int r0 = std::max(0, lr - d), r1 = std::min(ws.er - 1, lr + d);
+    const int c0 = std::max(0, lc - d), c1 = std::min(ws.ec - 1, lc + d);
+    std::vector<int2> locs;
+    for (int r = r0; r <= r1; ++r)
+        for (int c = c0; c <= c1; ++c) locs.push_back(make_int2(r, c));
+    *ops += (long long)locs.size();
+    ctx->seed_locs.ensure(locs.size());
+    CK(cudaMemcpyAsync(ctx->seed_locs.p, locs.data(), locs.size() * sizeof(int2),
+                       cudaMemcpyHostToDevice, ctx->s));
+    unsigned long long cnt = locs.size();
+    CK(cudaMemcpyAsync(ctx->counters.p + 7, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
+    eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 7, int(locs.size()), nullptr,
+              nullptr, 3);
+    tmk::CellH c;
+    CK(cudaMemcpyAsync(&c, ctx->cells.p + 3, sizeof c, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    return c;
+}
+
+// brute_force_match (stats.cpp:156-213)
+tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface_host) {
+    const int m = T.m, n = T.n;
+    if (m > img->p || n > img->q)
+        invalid("brute_force_match: template larger than search image");
+    WS& ws = get_ws(ctx, img, m, n);
+    const int er = ws.er, ec = ws.ec;
+    const size_t E = size_t(er) * ec;
+    double* surface = nullptr;
+    if (surface_host) {
+        ctx->surface.ensure(E);
+        surface = ctx->surface.p;
+    }
+    const tmk::CorrJob job = make_job(ctx, img, ws, T);
+    if (fp32_path(img, T)) {
+        std::vector<int> rows(er);
+        for (int r = 0; r < er; ++r) rows[r] = r;
+        upload_rows(ctx, rows);
+        tmk::BandTask t{};
+        t.rows = ctx->rows_list.p;
+        t.nrows = er;
+        t.cbase = 0;
+        t.sw = 1;
+        t.nc = ec;
+        t.mode = 0;
+        t.row_span = 7;
+        t.out_rho = surface;
+        ctx->partials.ensure(size_t(band_partials(er, ec, 1)));
+        int np = 0;
+        CK(tmk::corr_band(job, t, ctx->partials.p, &np, ctx->s));
+        ctx->add(1);
+        reduce_to(ctx, np, 2);
+    } else {
+        ctx->partials.ensure(kListBlocks);
+        CK(tmk::corr_dense_f64(job, surface, ctx->partials.p, kListBlocks, ctx->s));
+        ctx->add(1);
+        reduce_to(ctx, kListBlocks, 2);
+    }
+    tmk::CellH best;
+    CK(cudaMemcpyAsync(&best, ctx->cells.p + 2, sizeof best, cudaMemcpyDeviceToHost, ctx->s));
+    if (surface_host)
+        CK(cudaMemcpyAsync(surface_host, surface, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    tm_match_result r{};
+    r.mode = TM_MODE_BRUTE;
+    r.extent_rows = er;
+    r.extent_cols = ec;
+    r.best_row = r.refined_row = best.row;
+    r.best_col = r.refined_col = best.col;
+    r.best_rho = r.refined_rho = best.rho;
+    r.best_degenerate = (best.flags & 2) != 0;
+    r.final_threshold = r.best_degenerate ? 0.0 : best.rho;
+    r.retained = (long long)er * ec;
+    r.ops = (long long)er * ec;
+    return r;
+}
+
+std::vector<double> params_profile(const tm_match_params& P) {
+    if (!P.kernel_profile || P.kernel_len < 1) return {0.05, 0.20, 0.50, 0.20, 0.05};
+    if (P.kernel_len % 2 == 0) invalid("blur kernel profile must have odd length");
+    return std::vector<double>(P.kernel_profile, P.kernel_profile + P.kernel_len);
+}
+
+tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params& P) {
+    auto prep = std::make_unique<tm_prep>();
+    prep->params = P;
+    prep->profile = params_profile(P);
+    prep->params.kernel_profile = nullptr;
+    prep->m = m;
+    prep->n = n;
+    prep->source = img;
+    prep->mode = P.mode == TM_MODE_OPTA ? TM_MODE_OPTA : TM_MODE_EGS;
+    if (m > img->p || n > img->q) invalid("match: template larger than search image");
+    CK(cudaEventRecord(ctx->ev0, ctx->s));
+    if (prep->mode == TM_MODE_EGS) {
+        WS& ws = get_ws(ctx, img, m, n);
+        EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
+                                  P.max_group, prep->map);
+        prep->h = e.h;
+        prep->w = e.w;
+        prep->cost = e.cost;
+        prep->egs_trace = e.trace;
+    } else {
+        run_opta_prep(ctx, img, prep.get());
+    }
+    CK(cudaEventRecord(ctx->ev1, ctx->s));
+    CK(cudaEventSynchronize(ctx->ev1));
+    prep->prep_ms = ms_between(ctx->ev0, ctx->ev1);
+    prep->g = make_grid(img->p - m + 1, img->q - n + 1, prep->h, prep->w);
+    return prep.release();
+}
+
+tm_match_result run_one(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* t,
+                        const tm_match_params& P, uint8_t* visits) {
+    const int m = prep->m, n = prep->n;
+    const Tmpl T = upload_template(ctx, t, m, n);
+    tm_image* search_img = prep->search_img ? prep->search_img.get() : img;
+    const WS* ws = prep->search_img ? prep->search_ws.get() : &get_ws(ctx, img, m, n);
+    SearchIn in{search_img, ws, prep->g, prep->map.p};
+    tm_match_result r = search(ctx, in, T, P, visits);
+    if (prep->mode == TM_MODE_OPTA) {
+        r.mode = TM_MODE_OPTA;
+        const int d = prep->kappa * prep->radius;
+        long long rops = 0;
+        WS& ws_orig = get_ws(ctx, img, m, n);
+        const tmk::CellH c = refine(ctx, img, ws_orig, T, r.best_row, r.best_col, d, &rops);
+        r.refined_row = c.row;
+        r.refined_col = c.col;
+        r.refined_rho = c.rho;
+        r.ops += rops;
+        if (P.has_init_threshold)
+            r.below_threshold = (c.flags & 2) || c.rho < P.init_threshold;
+    }
+    return r;
+}
+
+template <class F>
+int guard(tm_ctx* ctx, F&& f) {
+    try {
+        if (ctx) {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            CK(cudaSetDevice(ctx->device));
+            f();
+        } else {
+            f();
+        }
+        return TM_OK;
+    } catch (const TmError& e) {
+        g_err = e.msg;
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "out of host memory";
+        return TM_ENOMEM;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return TM_EINVAL;
+    }
+}
+
+}  // namespace
+
+// ==== C ABI ===========================================================================
+extern "C" {
+
+const char* tm_last_error(void) { return g_err.c_str(); }
+
+void tm_default_params(tm_match_params* p) {
+    std::memset(p, 0, sizeof *p);
+    p->mode = TM_MODE_EGS;
+    p->h0 = 3;
+    p->w0 = 3;
+    p->rho_th = 0.8;
+    p->rho_max = 0.95;
+    p->xi_fraction = 0.005;
+    p->opta_margin = 0.005;
+    p->kernel_profile = nullptr;  // default {.05,.2,.5,.2,.05}
+    p->kernel_len = 0;
+    p->parallel = 0;
+    p->threads = 2;
+    p->policy = TM_POLICY_REFERENCE;
+    p->max_group = 127;
+    p->seed_margin = 0.02;
+}
+
+int tm_ctx_create(int device, tm_ctx** out) {
+    return guard(nullptr, [&] {
+        int ndev = 0;
+        if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+            throw TmError{TM_ENODEV, "no CUDA device available (the tmatch path is GPU-only)"};
+        if (device < 0 || device >= ndev) invalid("tm_ctx_create: bad device index");
+        cudaDeviceProp prop;
+        CK(cudaGetDeviceProperties(&prop, device));
+        if (prop.major < 10)
+            throw TmError{TM_ENODEV, "tmatch kernels are built for sm_100a (Blackwell)"};
+        auto ctx = std::make_unique<tm_ctx>();
+        ctx->device = device;
+        CK(cudaSetDevice(device));
+        CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
+        CK(cudaEventCreate(&ctx->ev0));
+        CK(cudaEventCreate(&ctx->ev1));
+        ctx->counters.ensure(16);
+        ctx->cells.ensure(8);
+        ctx->thr.ensure(2);
+        ctx->tally.ensure(1);
+        *out = ctx.release();
+    });
+}
+
+void tm_ctx_destroy(tm_ctx* ctx) {
+    if (!ctx) return;
+    cudaSetDevice(ctx->device);
+    cudaStreamSynchronize(ctx->s);
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    cudaStreamDestroy(ctx->s);
+    delete ctx;
+}
+
+int tm_ctx_synchronize(tm_ctx* ctx) {
+    return guard(ctx, [&] { CK(cudaStreamSynchronize(ctx->s)); });
+}
+
+int64_t tm_ctx_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int tm_image_create(tm_ctx* ctx, const double* pixels, int rows, int cols, tm_image** out) {
+    return guard(ctx, [&] {
+        if (rows < 1 || cols < 1) invalid("image dimensions must be at least 1x1");
+        auto img = std::make_unique<tm_image>();
+        img->ctx = ctx;
+        img->p = rows;
+        img->q = cols;
+        const size_t N = size_t(rows) * cols;
+        img->f64.ensure(N);
+        CK(cudaMemcpyAsync(img->f64.p, pixels, N * 8, cudaMemcpyHostToDevice, ctx->s));
+        classify_device_image(ctx, img.get());
+        *out = img.release();
+    });
+}
+
+int tm_image_create_u8(tm_ctx* ctx, const uint8_t* pixels, int rows, int cols, tm_image** out) {
+    return guard(ctx, [&] {
+        if (rows < 1 || cols < 1) invalid("image dimensions must be at least 1x1");
+        auto img = std::make_unique<tm_image>();
+        img->ctx = ctx;
+        img->p = rows;
+        img->q = cols;
+        img->integer = true;
+        const size_t N = size_t(rows) * cols;
+        img->u8.ensure(N);
+        CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
+        finish_integer_image(ctx, img.get());
+        CK(cudaStreamSynchronize(ctx->s));
+        *out = img.release();
+    });
+}
+
+int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
+    return guard(ctx, [&] {
+        if (!img->integer) invalid("tm_image_upload_u8: image is not an 8-bit image");
+        const size_t N = size_t(img->p) * img->q;
+        CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
+        CK(tmk::u8_to_f32_pitched(img->u8.p, img->p, img->q, img->f32.p, img->pitch, ctx->s));
+        ctx->add(1);
+        img->have_f64 = false;
+        img->have_qtotal = false;
+        img->ws_cache.clear();
+    });
+}
+
+int tm_image_download(tm_ctx* ctx, const tm_image* cimg, double* out) {
+    tm_image* img = const_cast<tm_image*>(cimg);
+    return guard(ctx, [&] {
+        const size_t N = size_t(img->p) * img->q;
+        if (!img->have_f64) ensure_f64(ctx, img);
+        CK(cudaMemcpyAsync(out, img->f64.p, N * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_image_is_integer(const tm_image* img) { return img && img->integer ? 1 : 0; }
+
+void tm_image_destroy(tm_image* img) {
+    if (!img) return;
+    if (img->ctx) {
+        std::lock_guard<std::mutex> lk(img->ctx->mu);
+        cudaSetDevice(img->ctx->device);
+        cudaStreamSynchronize(img->ctx->s);
+        delete img;
+    } else {
+        delete img;
+    }
+}
+
+int tm_running_sum(tm_ctx* ctx, tm_image* img, int m, int n, double* out) {
+    return guard(ctx, [&] {
+        const int p = img->p, q = img->q;
+        if (m < 1 || n < 1 || m > p || n > q) invalid("running_sum: window does not fit the source");
+        const size_t E = size_t(p - m + 1) * (q - n + 1);
+        ctx->S.ensure(E);
+        if (img->integer) {
+            ctx->hs.ensure(size_t(p) * (q - n + 1));
+            CK(tmk::window_sums_u8(img->u8.p, p, q, m, n, ctx->hs.p, ctx->S.p, ctx->s));
+            ctx->add(2);
+        } else {
+            replica_sums(ctx, tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 0}, p, q, m, n,
+                         ctx->S.p);
+        }
+        CK(cudaMemcpyAsync(out, ctx->S.p, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_window_stats(tm_ctx* ctx, tm_image* img, int m, int n, double* mu, double* omega,
+                    uint8_t* flat) {
+    return guard(ctx, [&] {
+        WS& ws = get_ws(ctx, img, m, n);
+        const size_t E = size_t(ws.er) * ws.ec;
+        if (mu) CK(cudaMemcpyAsync(mu, ws.mu.p, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+        if (omega) CK(cudaMemcpyAsync(omega, ws.om.p, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+        if (flat) CK(cudaMemcpyAsync(flat, ws.fl.p, E, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_brute_force_match(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
+                         tm_match_result* out, double* surface) {
+    return guard(ctx, [&] {
+        if (m > img->p || n > img->q)
+            invalid("brute_force_match: template larger than search image");
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        const Tmpl T = upload_template(ctx, tmpl, m, n);
+        *out = brute(ctx, img, T, surface);
+        CK(cudaEventRecord(ctx->ev1, ctx->s));
+        CK(cudaEventSynchronize(ctx->ev1));
+        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+    });
+}
+
+int tm_local_autocorrelation(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w,
+                             double* map) {
+    return guard(ctx, [&] {
+        if (m > img->p || n > img->q) invalid("group grid: template does not fit the image");
+        const tmk::GridDesc g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        WS& ws = get_ws(ctx, img, m, n);
+        const size_t E = size_t(g.er) * g.ec;
+        ctx->map_user.ensure(E);
+        autocorr_map(ctx, img, ws, g, 0.6, ctx->map_user.p);
+        CK(cudaMemcpyAsync(map, ctx->map_user.p, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_autocorr_retained(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w, double rho_tb,
+                         int64_t* n_r) {
+    return guard(ctx, [&] {
+        if (rho_tb < 0.0 || rho_tb > 1.0) invalid("retained_count: rho_tb must be in [0,1]");
+        if (m > img->p || n > img->q) invalid("group grid: template does not fit the image");
+        const tmk::GridDesc g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        WS& ws = get_ws(ctx, img, m, n);
+        ctx->map_user.ensure(size_t(g.er) * g.ec);
+        *n_r = autocorr_map(ctx, img, ws, g, expected_elimination_threshold_h(rho_tb),
+                            ctx->map_user.p);
+    });
+}
+
+int tm_efficient_group_size(tm_ctx* ctx, tm_image* img, int m, int n, int h0, int w0,
+                            double rho_tb, double xi_fraction, int max_group, int* h, int* w,
+                            tm_egs_iter* trace, int* trace_len, double* map) {
+    return guard(ctx, [&] {
+        if (m > img->p || n > img->q) invalid("efficient_group_size: template does not fit");
+        WS& ws = get_ws(ctx, img, m, n);
+        DBuf<double> best;
+        EgsOut e = run_egs_search(ctx, img, ws, m, n, h0, w0, rho_tb, xi_fraction, max_group, best);
+        *h = e.h;
+        *w = e.w;
+        *trace_len = int(e.trace.size());
+        for (size_t k = 0; k < e.trace.size() && k < TM_MAX_TRACE; ++k) trace[k] = e.trace[k];
+        if (map)
+            CK(cudaMemcpyAsync(map, best.p, size_t(ws.er) * ws.ec * 8, cudaMemcpyDeviceToHost,
+                               ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_blur(tm_ctx* ctx, tm_image* img, const double* profile, int len, double* out) {
+    return guard(ctx, [&] {
+        if (len < 1 || len % 2 == 0) invalid("blur kernel profile must have odd length");
+        ensure_f64(ctx, img);
+        const size_t N = size_t(img->p) * img->q;
+        if (len == 1) {
+            CK(cudaMemcpyAsync(out, img->f64.p, N * 8, cudaMemcpyDeviceToHost, ctx->s));
+        } else {
+            ctx->prof.ensure(len);
+            ctx->dtmp.ensure(N);
+            ctx->rowacc.ensure(N);
+            CK(cudaMemcpyAsync(ctx->prof.p, profile, len * 8, cudaMemcpyHostToDevice, ctx->s));
+            CK(tmk::blur_replica(img->f64.p, img->p, img->q, ctx->prof.p, len, ctx->dtmp.p,
+                                 ctx->rowacc.p, ctx->s));
+            ctx->add(2);
+            CK(cudaMemcpyAsync(out, ctx->rowacc.p, N * 8, cudaMemcpyDeviceToHost, ctx->s));
+        }
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_blur_fidelity_map(tm_ctx* ctx, tm_image* img, tm_image* blurred, int m, int n,
+                         double* fid) {
+    return guard(ctx, [&] {
+        if (img->p != blurred->p || img->q != blurred->q)
+            invalid("blur_fidelity_map: dimension mismatch");
+        WS& ws_o = get_ws(ctx, img, m, n);
+        ensure_f64(ctx, img);
+        ensure_f64(ctx, blurred);
+        WS ws_b;
+        ctx->fid.ensure(size_t(ws_o.er) * ws_o.ec);
+        // the blurred image's stats must come from the FP64 replica (window_stats on I_blur)
+        const bool was_int = blurred->integer;
+        blurred->integer = false;
+        fidelity(ctx, img, ws_o, blurred, ws_b, ctx->fid.p);
+        blurred->integer = was_int;
+        blurred->have_qtotal = false;
+        CK(cudaMemcpyAsync(fid, ctx->fid.p, size_t(ws_o.er) * ws_o.ec * 8, cudaMemcpyDeviceToHost,
+                           ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params* params,
+               tm_prep** out) {
+    return guard(ctx, [&] { *out = prepare(ctx, img, m, n, *params); });
+}
+
+int tm_prep_get_info(const tm_prep* prep, tm_prep_info* info) {
+    return guard(nullptr, [&] {
+        std::memset(info, 0, sizeof *info);
+        info->mode = prep->mode;
+        info->m = prep->m;
+        info->n = prep->n;
+        info->h = prep->h;
+        info->w = prep->w;
+        info->extent_rows = prep->g.er;
+        info->extent_cols = prep->g.ec;
+        info->kappa = prep->kappa;
+        info->lambda = prep->lambda;
+        info->cost = prep->cost;
+        info->egs_trace_len = int(prep->egs_trace.size());
+        for (size_t k = 0; k < prep->egs_trace.size() && k < TM_MAX_TRACE; ++k)
+            info->egs_trace[k] = prep->egs_trace[k];
+        info->opta_trace_len = int(prep->opta_trace.size());
+        for (size_t k = 0; k < prep->opta_trace.size() && k < TM_MAX_TRACE + 1; ++k)
+            info->opta_trace[k] = prep->opta_trace[k];
+        info->prep_ms = prep->prep_ms;
+    });
+}
+
+int tm_prep_download(tm_ctx* ctx, const tm_prep* prep, double* map, double* image) {
+    return guard(ctx, [&] {
+        const size_t E = size_t(prep->g.er) * prep->g.ec;
+        if (map) CK(cudaMemcpyAsync(map, prep->map.p, E * 8, cudaMemcpyDeviceToHost, ctx->s));
+        if (image) {
+            tm_image* src = prep->search_img ? prep->search_img.get() : prep->source;
+            ensure_f64(ctx, src);
+            CK(cudaMemcpyAsync(image, src->f64.p, size_t(src->p) * src->q * 8,
+                               cudaMemcpyDeviceToHost, ctx->s));
+        }
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+void tm_prep_destroy(tm_prep* prep) {
+    if (!prep) return;
+    tm_ctx* ctx = prep->source ? prep->source->ctx : nullptr;
+    if (ctx) {
+        std::lock_guard<std::mutex> lk(ctx->mu);
+        cudaStreamSynchronize(ctx->s);
+        delete prep;
+    } else {
+        delete prep;
+    }
+}
+
+int tm_run(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, int ntmpl,
+           const tm_match_params* params, tm_match_result* out, uint8_t* visits) {
+    return guard(ctx, [&] {
+        const size_t mn = size_t(prep->m) * prep->n;
+        const size_t E = size_t(prep->g.er) * prep->g.ec;
+        for (int k = 0; k < ntmpl; ++k) {
+            CK(cudaEventRecord(ctx->ev0, ctx->s));
+            out[k] = run_one(ctx, prep, img, tmpls + k * mn, *params, visits ? visits + k * E : nullptr);
+            CK(cudaEventRecord(ctx->ev1, ctx->s));
+            CK(cudaEventSynchronize(ctx->ev1));
+            out[k].wall_ms = ms_between(ctx->ev0, ctx->ev1);
+        }
+    });
+}
+
+int tm_run_u8(tm_ctx* ctx, tm_prep* prep, tm_image* img, const uint8_t* tmpls, int ntmpl,
+              const tm_match_params* params, tm_match_result* out, uint8_t* visits) {
+    const size_t mn = size_t(prep->m) * prep->n;
+    std::vector<double> t(mn * size_t(ntmpl));
+    for (size_t i = 0; i < t.size(); ++i) t[i] = tmpls[i];
+    return tm_run(ctx, prep, img, t.data(), ntmpl, params, out, visits);
+}
+
+int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
+                         const double* map, int h, int w, const tm_match_params* params,
+                         tm_match_result* out, uint8_t* visits) {
+    return guard(ctx, [&] {
+        if (m > img->p || n > img->q) invalid("group grid: template does not fit the image");
+        const tmk::GridDesc g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        WS& ws = get_ws(ctx, img, m, n);
+        const size_t E = size_t(g.er) * g.ec;
+        ctx->map_user.ensure(E);
+        CK(cudaMemcpyAsync(ctx->map_user.p, map, E * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        const Tmpl T = upload_template(ctx, tmpl, m, n);
+        *out = search(ctx, SearchIn{img, &ws, g, ctx->map_user.p}, T, *params, visits);
+        CK(cudaEventRecord(ctx->ev1, ctx->s));
+        CK(cudaEventSynchronize(ctx->ev1));
+        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+    });
+}
+
+int tm_center_scan(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img, int h, int w,
+                   double* rho, uint8_t* degenerate, int* best_row, int* best_col,
+                   double* best_rho, int* best_degenerate) {
+    return guard(ctx, [&] {
+        if (m > img->p || n > img->q) invalid("center_scan: grid extent mismatch");
+        const tmk::GridDesc g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        WS& ws = get_ws(ctx, img, m, n);
+        const Tmpl T = upload_template(ctx, tmpl, m, n);
+        centre_scan(ctx, img, ws, T, g);
+        const size_t G = size_t(g.tr) * g.tc;
+        tmk::CellH c;
+        CK(cudaMemcpyAsync(&c, ctx->cells.p, sizeof c, cudaMemcpyDeviceToHost, ctx->s));
+        if (rho) CK(cudaMemcpyAsync(rho, ctx->rho_c.p, G * 8, cudaMemcpyDeviceToHost, ctx->s));
+        if (degenerate)
+            CK(cudaMemcpyAsync(degenerate, ctx->deg_c.p, G, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        *best_row = c.row;
+        *best_col = c.col;
+        *best_rho = c.rho;
+        *best_degenerate = (c.flags & 2) != 0;
+    });
+}
+
+int tm_refine_localization(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* original,
+                           int loc_row, int loc_col, int d, int* row, int* col, double* rho,
+                           int* degenerate) {
+    return guard(ctx, [&] {
+        if (d < 0) invalid("refine_localization: d must be >= 0");
+        WS& ws = get_ws(ctx, original, m, n);
+        if (loc_row < 0 || loc_row >= ws.er || loc_col < 0 || loc_col >= ws.ec)
+            invalid("refine_localization: location outside the extent");
+        const Tmpl T = upload_template(ctx, tmpl, m, n);
+        long long ops = 0;
+        const tmk::CellH c = refine(ctx, original, ws, T, loc_row, loc_col, d, &ops);
+        *row = c.row;
+        *col = c.col;
+        *rho = c.rho;
+        *degenerate = (c.flags & 2) != 0;
+    });
+}
+
+int tm_match(tm_ctx* ctx, const double* tmpl, int m, int n, const double* image, int rows,
+             int cols, const tm_match_params* params, tm_match_result* out, uint8_t* visits) {
+    tm_image* img = nullptr;
+    int rc = tm_image_create(ctx, image, rows, cols, &img);
+    if (rc != TM_OK) return rc;
+    rc = guard(ctx, [&] {
+        if (m > rows || n > cols) invalid("match: template larger than search image");
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        const auto t0 = std::chrono::steady_clock::now();
+        if (params->mode == TM_MODE_BRUTE) {
+            const Tmpl T = upload_template(ctx, tmpl, m, n);
+            *out = brute(ctx, img, T, nullptr);
+            if (visits) std::memset(visits, TM_VISIT_RETAINED, size_t(out->extent_rows) * out->extent_cols);
+        } else {
+            const Tmpl T = upload_template(ctx, tmpl, m, n);
+            if (T.ts.flat) invalid("match: constant template has no defined correlation");
+            std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params));
+            *out = run_one(ctx, prep.get(), img, tmpl, *params, visits);
+            prep.reset();
+        }
+        out->wall_ms =
+            std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+    });
+    tm_image_destroy(img);
+    return rc;
+}
+
+}  // extern "C"

@@ -1,0 +1,280 @@
+// k_autocorr.cu -- local auto-correlation map R_co and the EGS retained count (sm_100a).
+//
+// Reference: local_autocorrelation (autocorr.cpp:40-96) builds, for each of the hw-1
+// offsets, a full-image product table and its FP64 prefix sums, then reads one window
+// sum per group centre.  On 8-bit data those cross sums are exact integers, so here one
+// fused pass computes them directly, and only at the centres:
+//
+//   S_d(c) = sum_{a<m, b<n} I(cr+a, cc+b) * I(cr+di+a, cc+dj+b)
+//
+// A CTA owns a tile of GTR x GTC groups, stages the image region it needs in shared
+// memory once, and loops over all offsets: a row pass slides an n-wide window along the
+// centre columns (H), a column pass slides an m-tall window along the centre rows, and the
+// FP64 epilogue replays autocorr.cpp:84-88 op for op.  The retained count (egs.cpp:12-25,
+// members with R_co < sqrt(1 - rho_tb^2)) is reduced in the same kernel.  Algorithmic
+// work is O((hw-1) * p * q) integer MACs per candidate size instead of the reference's
+// (hw-1) full-image FP64 prefix passes.
+#include <algorithm>
+
+#include "kernels.hpp"
+#include "tm_common.cuh"
+
+namespace tmk {
+
+namespace {
+
+struct ACParams {
+    const uint8_t* img;
+    int p, q, m, n;
+    Grid g;
+    DevStats st;
+    double thr;
+    double* map;
+    unsigned long long* n_r;
+    int gtr, gtc;   // groups per CTA tile
+    int nx_max;     // H rows per tile
+    int spitch;     // staged image pitch (bytes)
+    int srows;
+};
+
+__device__ __forceinline__ int ccol(const Grid& g, int tj) { return g.center_col(tj); }
+__device__ __forceinline__ int crow(const Grid& g, int ti) { return g.center_row(ti); }
+
+__global__ void k_autocorr_u8(ACParams P) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const Grid& g = P.g;
+    const int ti0 = blockIdx.y * P.gtr, tj0 = blockIdx.x * P.gtc;
+    const int nti = min(P.gtr, g.tr - ti0), ntj = min(P.gtc, g.tc - tj0);
+    const int hr = g.h >> 1, wr = g.w >> 1;
+    const int crA = crow(g, ti0), crB = crow(g, ti0 + nti - 1);
+    const int ccA = ccol(g, tj0), ccB = ccol(g, tj0 + ntj - 1);
+    const int R0 = crA - hr, C0 = ccA - wr;  // staged region origin (may be < 0: zeros)
+    const int nrows = (crB + hr + P.m) - R0;
+    const int ncols = (ccB + wr + P.n) - C0;
+
+    uint8_t* simg = smem;
+    int* H = reinterpret_cast<int*>(smem + ((size_t(P.srows) * P.spitch + 15) & ~size_t(15)));
+    int* scc = H + size_t(P.nx_max) * P.gtc;
+    int* scr = scc + P.gtc;
+    __shared__ unsigned long long blk_nr;
+
+    if (threadIdx.x == 0) blk_nr = 0;
+    for (int k = threadIdx.x; k < ntj; k += blockDim.x) scc[k] = ccol(g, tj0 + k);
+    for (int k = threadIdx.x; k < nti; k += blockDim.x) scr[k] = crow(g, ti0 + k);
+    for (int idx = threadIdx.x; idx < nrows * ncols; idx += blockDim.x) {
+        const int a = idx / ncols, b = idx % ncols;
+        const int r = R0 + a, c = C0 + b;
+        simg[size_t(a) * P.spitch + b] =
+            (r >= 0 && r < P.p && c >= 0 && c < P.q) ? P.img[size_t(r) * P.q + c] : 0;
+    }
+    __syncthreads();
+
+    const int nx = crB - crA + P.m;  // H rows: x = crA + xi
+    constexpr int kTJ = 8;           // centre columns per row-pass item
+    constexpr int kTI = 4;           // centre rows per column-pass item
+    const int nch = (ntj + kTJ - 1) / kTJ;
+    const double mn = double(P.m) * double(P.n);
+    unsigned long long local_nr = 0;
+
+    for (int di = -hr; di <= hr; ++di) {
+        for (int dj = -wr; dj <= wr; ++dj) {
+            if (di == 0 && dj == 0) continue;
+            // ---- row pass: H[xi][tj] = sum_b I(x, cc+b) * I(x+di, cc+dj+b) ----------
+            for (int item = threadIdx.x; item < nx * nch; item += blockDim.x) {
+                const int xi = item / nch, ch = item % nch;
+                const int x = crA + xi;
+                const uint8_t* ra = simg + size_t(x - R0) * P.spitch - C0;
+                const uint8_t* rb = simg + size_t(x + di - R0) * P.spitch - C0 + dj;
+                const int k0 = ch * kTJ, k1 = min(k0 + kTJ, ntj);
+                int cc = scc[k0];
+                int s = 0;
+                for (int b = 0; b < P.n; ++b) s += int(ra[cc + b]) * int(rb[cc + b]);
+                H[size_t(xi) * P.gtc + k0] = s;
+                for (int k = k0 + 1; k < k1; ++k) {
+                    const int nc = scc[k];
+                    for (int c = cc; c < nc; ++c)
+                        s += int(ra[c + P.n]) * int(rb[c + P.n]) - int(ra[c]) * int(rb[c]);
+                    cc = nc;
+                    H[size_t(xi) * P.gtc + k] = s;
+                }
+            }
+            __syncthreads();
+            // ---- column pass + epilogue --------------------------------------------
+            const int nic = (nti + kTI - 1) / kTI;
+            for (int item = threadIdx.x; item < ntj * nic; item += blockDim.x) {
+                const int k = item % ntj, ic = item / ntj;
+                const int i0 = ic * kTI, i1 = min(i0 + kTI, nti);
+                int cr = scr[i0];
+                long long S = 0;
+                for (int a = 0; a < P.m; ++a) S += H[size_t(cr - crA + a) * P.gtc + k];
+                const int cc = scc[k];
+                const int tj = tj0 + k;
+                const int c0 = tj * g.w, c1 = min(c0 + g.w, g.ec) - 1;
+                const int mc = cc + dj;
+                for (int i = i0; i < i1; ++i) {
+                    if (i > i0) {
+                        const int ncr = scr[i];
+                        for (int x = cr; x < ncr; ++x)
+                            S += (long long)H[size_t(x + P.m - crA) * P.gtc + k] -
+                                 H[size_t(x - crA) * P.gtc + k];
+                        cr = ncr;
+                    }
+                    const int ti = ti0 + i;
+                    const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+                    const int mr = cr + di;
+                    if (mr < r0 || mr > r1 || mc < c0 || mc > c1) continue;
+                    const size_t kc = size_t(cr) * g.ec + cc, km = size_t(mr) * g.ec + mc;
+                    double v = 0.0;
+                    if (!P.st.flat[kc] && !P.st.flat[km]) {
+                        const double num =
+                            __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, P.st.mu[kc]), P.st.mu[km]));
+                        v = dclamp(__ddiv_rn(num, __dmul_rn(P.st.omega[kc], P.st.omega[km])), -1.0,
+                                   1.0);
+                    }
+                    P.map[km] = v;
+                    if (v < P.thr) ++local_nr;
+                }
+            }
+            __syncthreads();
+        }
+    }
+    // centres carry exactly 1 (autocorr.cpp:92-93)
+    for (int idx = threadIdx.x; idx < nti * ntj; idx += blockDim.x) {
+        const int i = idx / ntj, k = idx % ntj;
+        P.map[size_t(scr[i]) * g.ec + scc[k]] = 1.0;
+    }
+    local_nr = warp_sum(local_nr);
+    if ((threadIdx.x & 31) == 0 && local_nr) atomicAdd(&blk_nr, local_nr);
+    __syncthreads();
+    if (threadIdx.x == 0 && blk_nr) atomicAdd(P.n_r, blk_nr);
+}
+
+// ---- replica path helpers ---------------------------------------------------------------
+
+__global__ void k_autocorr_init(double* map, Grid g) {
+    const size_t E = size_t(g.er) * g.ec;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+         k += size_t(gridDim.x) * blockDim.x) {
+        const int r = int(k / g.ec), c = int(k % g.ec);
+        const int ti = g.tile_r(r), tj = g.tile_c(c);
+        map[k] = (g.center_row(ti) == r && g.center_col(tj) == c) ? 1.0 : 0.0;
+    }
+}
+
+// One offset: prefix is the (ph+1) x (pw+1) replica prefix table of the product image
+// whose origin is (orr, occ) (autocorr.cpp:64-76); cross sum at the centre is the window
+// difference at (cr - orr, cc - occ) in stats.cpp:50 order.
+__global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int pw, int m, int n,
+                                  Grid g, DevStats st, int di, int dj, double* __restrict__ map) {
+    const long long G = (long long)g.tr * g.tc;
+    const int orr = max(0, -di), occ = max(0, -dj);
+    const size_t ppw = size_t(pw) + 1;
+    const double mn = double(m) * double(n);
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
+         gi += (long long)gridDim.x * blockDim.x) {
+        const int ti = int(gi / g.tc), tj = int(gi % g.tc);
+        const int cr = g.center_row(ti), cc = g.center_col(tj);
+        const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        const int c0 = tj * g.w, c1 = min(c0 + g.w, g.ec) - 1;
+        const int mr = cr + di, mc = cc + dj;
+        if (mr < r0 || mr > r1 || mc < c0 || mc > c1) continue;
+        const size_t kc = size_t(cr) * g.ec + cc, km = size_t(mr) * g.ec + mc;
+        if (st.flat[kc] || st.flat[km]) continue;
+        const int r = cr - orr, c = cc - occ;
+        const double* top = prefix + size_t(r) * ppw;
+        const double* bot = prefix + size_t(r + m) * ppw;
+        const double cross = __dadd_rn(__dsub_rn(__dsub_rn(bot[c + n], top[c + n]), bot[c]), top[c]);
+        const double num = __dsub_rn(cross, __dmul_rn(__dmul_rn(mn, st.mu[kc]), st.mu[km]));
+        map[km] = dclamp(__ddiv_rn(num, __dmul_rn(st.omega[kc], st.omega[km])), -1.0, 1.0);
+    }
+}
+
+__global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
+                           unsigned long long* n_r) {
+    const size_t E = size_t(g.er) * g.ec;
+    unsigned long long local = 0;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+         k += size_t(gridDim.x) * blockDim.x) {
+        const int r = int(k / g.ec), c = int(k % g.ec);
+        const int ti = g.tile_r(r), tj = g.tile_c(c);
+        if (g.center_row(ti) == r && g.center_col(tj) == c) continue;
+        if (map[k] < thr) ++local;
+    }
+    local = warp_sum(local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_r, local);
+}
+
+Grid to_grid(GridDesc d) { return Grid{d.er, d.ec, d.h, d.w, d.tr, d.tc}; }
+
+}  // namespace
+
+cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc gd, DevStats st,
+                        double retain_threshold, double* map, unsigned long long* n_r,
+                        cudaStream_t s) {
+    ACParams P;
+    P.img = img;
+    P.p = p;
+    P.q = q;
+    P.m = m;
+    P.n = n;
+    P.g = to_grid(gd);
+    P.st = st;
+    P.thr = retain_threshold;
+    P.map = map;
+    P.n_r = n_r;
+    const int hr = gd.h / 2, wr = gd.w / 2;
+    // Choose the group tile so the staged image + H fit in ~96 KB of shared memory.
+    int gtr = 16, gtc = 32;
+    size_t bytes = 0;
+    for (;;) {
+        const int srows = (gtr - 1) * gd.h + 2 * hr + m + 1;
+        const int scols = (gtc - 1) * gd.w + 2 * wr + n + 1;
+        const int spitch = (scols + 15) & ~15;
+        const int nx = (gtr - 1) * gd.h + m + 1;
+        bytes = ((size_t(srows) * spitch + 15) & ~size_t(15)) + size_t(nx) * gtc * 4 +
+                size_t(gtc + gtr) * 4;
+        P.srows = srows;
+        P.spitch = spitch;
+        P.nx_max = nx;
+        if (bytes <= 96 * 1024 || (gtr == 1 && gtc == 1)) break;
+        if (gtc >= gtr && gtc > 1) gtc /= 2;
+        else if (gtr > 1) gtr /= 2;
+    }
+    P.gtr = gtr;
+    P.gtc = gtc;
+    if (bytes > 200 * 1024) return cudaErrorInvalidValue;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_autocorr_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr_set = true;
+    }
+    dim3 grid((gd.tc + gtc - 1) / gtc, (gd.tr + gtr - 1) / gtr);
+    k_autocorr_u8<<<grid, 256, bytes, s>>>(P);
+    return cudaGetLastError();
+}
+
+cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s) {
+    const size_t E = size_t(g.er) * g.ec;
+    const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 16));
+    k_autocorr_init<<<blocks, 256, 0, s>>>(map, to_grid(g));
+    return cudaGetLastError();
+}
+
+cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
+                                     GridDesc g, DevStats st, int di, int dj, double* map,
+                                     cudaStream_t s) {
+    const long long G = (long long)g.tr * g.tc;
+    const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 16));
+    k_autocorr_offset<<<blocks, 256, 0, s>>>(prefix, ph, pw, m, n, to_grid(g), st, di, dj, map);
+    return cudaGetLastError();
+}
+
+cudaError_t retained_count(const double* map, GridDesc g, double threshold,
+                           unsigned long long* n_r, cudaStream_t s) {
+    const size_t E = size_t(g.er) * g.ec;
+    const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 16));
+    k_retained<<<blocks, 256, 0, s>>>(map, to_grid(g), threshold, n_r);
+    return cudaGetLastError();
+}
+
+}  // namespace tmk

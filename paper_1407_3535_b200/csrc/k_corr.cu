@@ -1,0 +1,643 @@
+// k_corr.cu -- template correlation, scan-2 elimination and argmax (sm_100a).
+//
+// window_dot (detail.hpp:32-41) on 8-bit data is an exact integer <= 255^2*m*n, so the
+// CUDA-core kernels accumulate u8*u8 products in FP32 FMA -- exact while a partial stays
+// below 2^24, i.e. for flush_rows*n*255^2 < 2^24 -- and flush into FP64 every flush_rows
+// template rows.  The dot therefore equals the reference's FP64 sum bit for bit, and the
+// zncc_at epilogue (detail.hpp:45-51) is replayed with _rn intrinsics.
+//
+// corr_band: the dense engine.  A CTA owns a band of 8 output rows (taken from a row
+// list, so centre rows at stride h work the same as consecutive rows) times NW*32 column
+// indices at column stride SW.  Lane (ry, sx) = (lane/4, lane%4) owns 8 outputs of one row;
+// it keeps a register window of (8-1)*SW+16 image values per 16-column template block so
+// every staged float feeds 8 FMAs.  Template rows are staged IC at a time with the image
+// rows they touch; the staged pitch is 4 mod 8 words so the 8 lanes of each LDS.128 phase
+// hit 8 distinct bank groups (row strides are odd).
+#include <algorithm>
+
+#include "kernels.hpp"
+#include "tm_common.cuh"
+
+namespace tmk {
+
+namespace {
+
+constexpr int kRX = 8;   // outputs per lane
+constexpr int kJB = 16;  // template columns per register block
+constexpr int kIC = 8;   // template rows per shared-memory stage
+
+__host__ __device__ constexpr int win_floats(int sw) { return (((kRX - 1) * sw + kJB) + 3) & ~3; }
+
+__device__ __forceinline__ TStats to_ts(const TStatsH& h) {
+    return TStats{h.mu, h.omega, h.mn, h.flat};
+}
+
+__device__ __forceinline__ void store_partial(const Cell& c, CellH* partials, int idx) {
+    partials[idx] = CellH{c.rho, c.row, c.col, c.flags};
+}
+
+struct BandGeom {
+    int spitch;  // staged floats per row (4 mod 8)
+    int srows;   // staged rows
+    size_t smem;
+};
+
+template <int SW, int NW>
+__host__ BandGeom band_geom(int span_rows, int npad) {
+    BandGeom g;
+    const int width = (NW * 32 - 1) * SW + npad + 4;
+    int pitch = (width + 3) & ~3;
+    if (((pitch / 4) & 1) == 0) pitch += 4;
+    g.spitch = pitch;
+    g.srows = span_rows;
+    g.smem = size_t(span_rows) * pitch * 4 + size_t(kIC) * npad * 4;
+    return g;
+}
+
+template <int SW, int NW>
+__global__ void __launch_bounds__(NW * 32)
+    k_corr_band(CorrJob job, BandTask task, int spitch, int srows, CellH* partials) {
+    extern __shared__ __align__(16) float sm[];
+    float* simg = sm;
+    float* stp = sm + size_t(srows) * spitch;
+    __shared__ Cell scratch[NW];
+
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ry = lane >> 2, sx = lane & 3;
+    const int yb = blockIdx.y * 8;
+    const int ylast = min(yb + 7, task.nrows - 1);
+    const int yi = yb + ry;
+    const bool row_ok = yi < task.nrows;
+    const int r = task.rows[row_ok ? yi : ylast];
+    const int r_first = task.rows[yb];
+    const int span = task.rows[ylast] - r_first + kIC;
+    const int kb = blockIdx.x * (NW * 32);
+    const int cstart = task.cbase + kb * SW;
+    const int width = (NW * 32 - 1) * SW + job.npad;
+    const int lane_col = (wid * 32 + sx * kRX) * SW;  // staged column of output x=0
+    const int yo = r - r_first;
+
+    float acc[kRX];
+    double dacc[kRX];
+#pragma unroll
+    for (int x = 0; x < kRX; ++x) {
+        acc[x] = 0.f;
+        dacc[x] = 0.0;
+    }
+    constexpr int W = win_floats(SW);
+    const int p_rows = job.st.er + job.m - 1;  // image rows
+    const int q_cols = job.st.ec + job.n - 1;
+
+    for (int i0 = 0; i0 < job.m; i0 += kIC) {
+        __syncthreads();
+        // stage image rows [r_first + i0, r_first + i0 + span), columns [cstart, +width)
+        const int total = span * width;
+        for (int idx = threadIdx.x; idx < total; idx += NW * 32) {
+            const int a = idx / width, b = idx - a * width;
+            const int gr = r_first + i0 + a, gc = cstart + b;
+            simg[a * spitch + b] =
+                (gr < p_rows && gc < q_cols) ? job.imgf[size_t(gr) * job.pitch + gc] : 0.f;
+        }
+        for (int idx = threadIdx.x; idx < kIC * job.npad; idx += NW * 32) {
+            const int a = idx / job.npad, b = idx - a * job.npad;
+            stp[idx] = (i0 + a < job.m) ? job.tf[size_t(i0 + a) * job.npad + b] : 0.f;
+        }
+        __syncthreads();
+        const int nii = min(kIC, job.m - i0);
+        for (int ii = 0; ii < nii; ++ii) {
+            const float* irow = simg + (yo + ii) * spitch + lane_col;
+            const float* trow = stp + ii * job.npad;
+            for (int jb = 0; jb < job.npad; jb += kJB) {
+                float win[W];
+#pragma unroll
+                for (int v = 0; v < W / 4; ++v) {
+                    const float4 t4 = *reinterpret_cast<const float4*>(irow + jb + 4 * v);
+                    win[4 * v + 0] = t4.x;
+                    win[4 * v + 1] = t4.y;
+                    win[4 * v + 2] = t4.z;
+                    win[4 * v + 3] = t4.w;
+                }
+                float tv[kJB];
+#pragma unroll
+                for (int v = 0; v < kJB / 4; ++v) {
+                    const float4 t4 = *reinterpret_cast<const float4*>(trow + jb + 4 * v);
+                    tv[4 * v + 0] = t4.x;
+                    tv[4 * v + 1] = t4.y;
+                    tv[4 * v + 2] = t4.z;
+                    tv[4 * v + 3] = t4.w;
+                }
+#pragma unroll
+                for (int j = 0; j < kJB; ++j)
+#pragma unroll
+                    for (int x = 0; x < kRX; ++x) acc[x] = fmaf(tv[j], win[x * SW + j], acc[x]);
+            }
+            if ((i0 + ii + 1) % job.flush_rows == 0) {
+#pragma unroll
+                for (int x = 0; x < kRX; ++x) {
+                    dacc[x] += double(acc[x]);
+                    acc[x] = 0.f;
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int x = 0; x < kRX; ++x) dacc[x] += double(acc[x]);
+
+    // ---- epilogue ---------------------------------------------------------------------
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    const int k0 = kb + wid * 32 + sx * kRX;
+#pragma unroll
+    for (int x = 0; x < kRX; ++x) {
+        const int k = k0 + x;
+        if (!row_ok || k >= task.nc) continue;
+        const int c = task.cbase + k * SW;
+        const size_t kk = size_t(r) * job.st.ec + c;
+        if (task.mode == 2 && task.mask[kk] != 2) continue;
+        const bool wflat = job.st.flat[kk];
+        const double rho = zncc_epilogue(dacc[x], ts, job.st.mu[kk], job.st.omega[kk], wflat);
+        const bool deg = ts.flat || wflat;
+        if (task.mode == 1) {
+            const size_t gi = size_t(yi) * task.tc + task.col0 + k;
+            task.out_rho[gi] = rho;
+            task.out_deg[gi] = deg;
+        } else if (task.out_rho) {
+            task.out_rho[kk] = rho;
+        }
+        const Cell cand = make_cell(r, c, rho, deg);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.y * gridDim.x + blockIdx.x);
+}
+
+// ---- sparse: one warp per location ----------------------------------------------------
+__global__ void __launch_bounds__(256)
+    k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
+                int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+                int lane_flush) {
+    __shared__ Cell scratch[8];
+    const int lane = threadIdx.x & 31;
+    const long long nloc = min((long long)*count, (long long)max_count);
+    const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    for (long long li = warp0; li < nloc; li += nwarps) {
+        const int2 rc = locs[li];
+        float acc = 0.f;
+        double dacc = 0.0;
+        for (int i = 0; i < job.m; ++i) {
+            const float* ir = job.imgf + size_t(rc.x + i) * job.pitch + rc.y;
+            const float* tr = job.tf + size_t(i) * job.npad;
+            for (int j = lane; j < job.n; j += 32) acc = fmaf(tr[j], ir[j], acc);
+            if ((i + 1) % lane_flush == 0) {
+                dacc += double(acc);
+                acc = 0.f;
+            }
+        }
+        dacc += double(acc);
+        dacc = warp_sum(dacc);
+        if (lane == 0) {
+            const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
+            const bool wflat = job.st.flat[kk];
+            const double rho = zncc_epilogue(dacc, ts, job.st.mu[kk], job.st.omega[kk], wflat);
+            if (out_rho) out_rho[li] = rho;
+            if (out_deg) out_deg[li] = ts.flat || wflat;
+            const Cell cand = make_cell(rc.x, rc.y, rho, ts.flat || wflat);
+            if (better(cand, best)) best = cand;
+        }
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
+// ---- FP64 replica (non-integer images / templates) --------------------------------------
+__device__ __forceinline__ double dot_f64(const CorrJob& job, int r, int c) {
+    double acc = 0.0;
+    for (int i = 0; i < job.m; ++i) {
+        const double* pt = job.td + size_t(i) * job.n;
+        const double* pi = job.imgd + size_t(r + i) * job.q + c;
+        for (int j = 0; j < job.n; ++j) acc = __dadd_rn(acc, __dmul_rn(pt[j], pi[j]));
+    }
+    return acc;
+}
+
+__global__ void __launch_bounds__(256)
+    k_list_f64(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
+               int max_count, double* out_rho, uint8_t* out_deg, CellH* partials) {
+    __shared__ Cell scratch[8];
+    const long long nloc = min((long long)*count, (long long)max_count);
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < nloc;
+         li += (long long)gridDim.x * blockDim.x) {
+        const int2 rc = locs[li];
+        const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
+        const bool wflat = job.st.flat[kk];
+        const double rho = (ts.flat || wflat)
+                               ? 0.0
+                               : zncc_epilogue(dot_f64(job, rc.x, rc.y), ts, job.st.mu[kk],
+                                               job.st.omega[kk], wflat);
+        if (out_rho) out_rho[li] = rho;
+        if (out_deg) out_deg[li] = ts.flat || wflat;
+        const Cell cand = make_cell(rc.x, rc.y, rho, ts.flat || wflat);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(256)
+    k_centres_f64(CorrJob job, Grid g, double* rho_c, uint8_t* deg_c, CellH* partials) {
+    __shared__ Cell scratch[8];
+    const long long G = (long long)g.tr * g.tc;
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
+         gi += (long long)gridDim.x * blockDim.x) {
+        const int ti = int(gi / g.tc), tj = int(gi % g.tc);
+        const int r = g.center_row(ti), c = g.center_col(tj);
+        const size_t kk = size_t(r) * job.st.ec + c;
+        const bool wflat = job.st.flat[kk];
+        const double rho = (ts.flat || wflat) ? 0.0
+                                              : zncc_epilogue(dot_f64(job, r, c), ts, job.st.mu[kk],
+                                                              job.st.omega[kk], wflat);
+        rho_c[gi] = rho;
+        deg_c[gi] = ts.flat || wflat;
+        const Cell cand = make_cell(r, c, rho, ts.flat || wflat);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
+__global__ void __launch_bounds__(256)
+    k_dense_f64(CorrJob job, double* surface, CellH* partials) {
+    __shared__ Cell scratch[8];
+    const long long E = (long long)job.st.er * job.st.ec;
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    for (long long k = blockIdx.x * (long long)blockDim.x + threadIdx.x; k < E;
+         k += (long long)gridDim.x * blockDim.x) {
+        const int r = int(k / job.st.ec), c = int(k % job.st.ec);
+        const bool wflat = job.st.flat[k];
+        const double rho = (ts.flat || wflat) ? 0.0
+                                              : zncc_epilogue(dot_f64(job, r, c), ts, job.st.mu[k],
+                                                              job.st.omega[k], wflat);
+        if (surface) surface[k] = rho;
+        const Cell cand = make_cell(r, c, rho, ts.flat || wflat);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
+// ---- reductions -----------------------------------------------------------------------
+__global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH* out) {
+    __shared__ Cell scratch[32];
+    Cell best = no_cell();
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+        const CellH h = partials[i];
+        const Cell c{h.rho, h.row, h.col, h.flags};
+        if (better(c, best)) best = c;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) out[0] = CellH{best.rho, best.row, best.col, best.flags};
+}
+
+// ---- scan 2: SEC test + survivor compaction (matcher.cpp:48-78, bounds.cpp:41-46) -------
+__global__ void __launch_bounds__(256)
+    k_sec_compact(Grid g, const double* __restrict__ map, const double* __restrict__ rho_c,
+                  const uint8_t* __restrict__ deg_c, const uint8_t* __restrict__ flat, int tflat,
+                  const double* __restrict__ thr_ptr, const uint8_t* __restrict__ seeded,
+                  int2* locs, unsigned long long max_locs, Tally* tally, uint8_t* visits) {
+    const double T = *thr_ptr;
+    const double tb = dmin(T, 1.0);
+    const size_t E = size_t(g.er) * g.ec;
+    const int lane = threadIdx.x & 31;
+    unsigned long long n_elim = 0, n_keep = 0;
+    for (size_t base = blockIdx.x * size_t(blockDim.x); base < E;
+         base += size_t(gridDim.x) * blockDim.x) {
+        const size_t k = base + threadIdx.x;
+        bool survivor = false;
+        if (k < E) {
+            const int r = int(k / g.ec), c = int(k % g.ec);
+            const int ti = g.tile_r(r), tj = g.tile_c(c);
+            const bool centre = g.center_row(ti) == r && g.center_col(tj) == c;
+            if (centre) {
+                if (visits) visits[k] = 0;
+            } else {
+                const size_t gi = size_t(ti) * g.tc + tj;
+                if (seeded && seeded[gi]) {
+                    ++n_keep;  // evaluated by the seeding pass
+                    if (visits) visits[k] = 2;
+                } else {
+                    const bool mflat = tflat || flat[k];
+                    const bool elim =
+                        !deg_c[gi] && !mflat && T >= -1.0 && sec_holds(tb, rho_c[gi], map[k]);
+                    if (elim) {
+                        ++n_elim;
+                        if (visits) visits[k] = 1;
+                    } else {
+                        ++n_keep;
+                        survivor = true;
+                        if (visits) visits[k] = 2;
+                    }
+                }
+            }
+        }
+        const unsigned ballot = __ballot_sync(0xffffffffu, survivor);
+        if (ballot) {
+            unsigned long long basepos = 0;
+            if (lane == 0) basepos = atomicAdd(&tally->survivors, (unsigned long long)__popc(ballot));
+            basepos = __shfl_sync(0xffffffffu, basepos, 0);
+            if (survivor) {
+                const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
+                if (pos < max_locs) locs[pos] = make_int2(int(k / g.ec), int(k % g.ec));
+            }
+        }
+    }
+    n_elim = warp_sum(n_elim);
+    n_keep = warp_sum(n_keep);
+    if (lane == 0) {
+        if (n_elim) atomicAdd(&tally->eliminated, n_elim);
+        if (n_keep) atomicAdd(&tally->retained, n_keep);
+    }
+}
+
+__global__ void k_threshold_init(const CellH* best, int has_init, double init, double* thr) {
+    double t = -INFINITY;
+    const CellH b = *best;
+    if ((b.flags & 1) && !(b.flags & 2)) t = b.rho;
+    if (has_init) t = dmax(t, dclamp(init, -1.0, 1.0));
+    *thr = t;
+}
+
+__global__ void k_threshold_raise(const CellH* best, double* thr) {
+    const CellH b = *best;
+    if ((b.flags & 1) && !(b.flags & 2) && b.rho > *thr) *thr = b.rho;
+}
+
+// Seeded policy: every group whose centre rho is within `margin` of the best centre is
+// searched exhaustively first; its best member raises the threshold before scan 2.
+__global__ void k_seed_members(Grid g, const double* __restrict__ rho_c,
+                               const uint8_t* __restrict__ deg_c, const double* thr,
+                               double margin, uint8_t* seeded, int2* locs,
+                               unsigned long long* count, unsigned long long max_locs,
+                               unsigned long long* n_groups, unsigned long long max_groups) {
+    const long long G = (long long)g.tr * g.tc;
+    const double T = *thr;
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
+         gi += (long long)gridDim.x * blockDim.x) {
+        seeded[gi] = 0;
+        if (deg_c[gi] || !(rho_c[gi] >= T - margin)) continue;
+        const unsigned long long slot = atomicAdd(n_groups, 1ull);
+        if (slot >= max_groups) continue;
+        const int ti = int(gi / g.tc), tj = int(gi % g.tc);
+        const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        const int c0 = tj * g.w, c1 = min(c0 + g.w, g.ec) - 1;
+        const int cr = (r0 + r1) >> 1, cc = (c0 + c1) >> 1;
+        const unsigned long long nm = (unsigned long long)(r1 - r0 + 1) * (c1 - c0 + 1) - 1;
+        const unsigned long long pos = atomicAdd(count, nm);
+        if (pos + nm > max_locs) continue;
+        seeded[gi] = 1;
+        unsigned long long o = pos;
+        for (int r = r0; r <= r1; ++r)
+            for (int c = c0; c <= c1; ++c)
+                if (r != cr || c != cc) locs[o++] = make_int2(r, c);
+    }
+}
+
+// ---- sequential policy (matcher.cpp:48-78 with running_update): exact replay ----------
+// Scan order key of a member: group index * (h*w) + row-major offset inside its tile.
+__device__ __forceinline__ unsigned long long scan_key(const Grid& g, int r, int c) {
+    const int ti = g.tile_r(r), tj = g.tile_c(c);
+    return ((unsigned long long)ti * g.tc + tj) * (unsigned long long)(g.h * g.w) +
+           (unsigned long long)((r - ti * g.h) * g.w + (c - tj * g.w));
+}
+
+__device__ __forceinline__ bool alive_at(const Grid& g, int r, int c, double T,
+                                         const double* map, const double* rho_c,
+                                         const uint8_t* deg_c, const uint8_t* flat, int tflat) {
+    const size_t k = size_t(r) * g.ec + c;
+    const size_t gi = size_t(g.tile_r(r)) * g.tc + g.tile_c(c);
+    const bool mflat = tflat || flat[k];
+    if (deg_c[gi] || mflat || !(T >= -1.0)) return true;
+    return !sec_holds(dmin(T, 1.0), rho_c[gi], map[k]);
+}
+
+// First (in scan order, key > after) candidate that is alive at T and sets a new record.
+__global__ void k_first_record(Grid g, const int2* __restrict__ locs,
+                               const unsigned long long* count, const double* __restrict__ rho,
+                               const uint8_t* __restrict__ deg, const double* map,
+                               const double* rho_c, const uint8_t* deg_c, const uint8_t* flat,
+                               int tflat, double T, unsigned long long after,
+                               unsigned long long* best_key) {
+    const unsigned long long n = *count;
+    unsigned long long mine = ~0ull;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        if (deg[i] || !(rho[i] > T)) continue;
+        const int2 rc = locs[i];
+        const unsigned long long key = scan_key(g, rc.x, rc.y);
+        if ((after != ~0ull && key <= after) || key >= mine) continue;
+        if (alive_at(g, rc.x, rc.y, T, map, rho_c, deg_c, flat, tflat)) mine = key;
+    }
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) mine = min(mine, __shfl_xor_sync(0xffffffffu, mine, s));
+    if ((threadIdx.x & 31) == 0 && mine != ~0ull) atomicMin(best_key, mine);
+}
+
+__global__ void k_fetch_rho(Grid g, const int2* __restrict__ locs, const unsigned long long* count,
+                            const double* __restrict__ rho, unsigned long long key, double* out) {
+    const unsigned long long n = *count;
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int2 rc = locs[i];
+        if (scan_key(g, rc.x, rc.y) == key) *out = rho[i];
+    }
+}
+
+// Final pass: each candidate sees the threshold of the last record before it.
+__global__ void k_seq_final(Grid g, const int2* __restrict__ locs, const unsigned long long* count,
+                            const double* __restrict__ rho, const uint8_t* __restrict__ deg,
+                            const double* map, const double* rho_c, const uint8_t* deg_c,
+                            const uint8_t* flat, int tflat, double T0,
+                            const unsigned long long* __restrict__ rec_key,
+                            const double* __restrict__ rec_T, int n_rec, Tally* tally,
+                            uint8_t* visits, CellH* partials) {
+    __shared__ Cell scratch[8];
+    const unsigned long long n = *count;
+    unsigned long long dead = 0, alive = 0;
+    Cell best = no_cell();
+    for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
+         i += (unsigned long long)gridDim.x * blockDim.x) {
+        const int2 rc = locs[i];
+        const unsigned long long key = scan_key(g, rc.x, rc.y);
+        // threshold in effect: last record with rec_key < key (records sorted ascending)
+        int lo = 0, hi = n_rec;
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (rec_key[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        const double T = lo == 0 ? T0 : rec_T[lo - 1];
+        if (alive_at(g, rc.x, rc.y, T, map, rho_c, deg_c, flat, tflat)) {
+            ++alive;
+            const Cell cand = make_cell(rc.x, rc.y, rho[i], deg[i] != 0);
+            if (better(cand, best)) best = cand;
+        } else {
+            ++dead;
+            if (visits) visits[size_t(rc.x) * g.ec + rc.y] = 1;
+        }
+    }
+    dead = warp_sum(dead);
+    alive = warp_sum(alive);
+    if ((threadIdx.x & 31) == 0) {
+        if (dead) atomicAdd(&tally->eliminated, dead);
+        if (alive) atomicAdd(&tally->pad, alive);
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
+Grid to_grid(GridDesc d) { return Grid{d.er, d.ec, d.h, d.w, d.tr, d.tc}; }
+
+template <int SW, int NW>
+cudaError_t launch_band(const CorrJob& job, const BandTask& task, CellH* partials, int* n_partials,
+                        cudaStream_t s) {
+    const int bands = (task.nrows + 7) / 8;
+    // span of staged rows: max over bands of (rows[yb+7] - rows[yb]) + kIC; rows are
+    // increasing with the largest step at most the row stride, bounded by the caller.
+    const int span = task.row_span + kIC;
+    const BandGeom geo = band_geom<SW, NW>(span, job.npad);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_corr_band<SW, NW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    if (geo.smem > 200 * 1024) return cudaErrorInvalidValue;
+    dim3 grid((task.nc + NW * 32 - 1) / (NW * 32), bands);
+    k_corr_band<SW, NW><<<grid, NW * 32, geo.smem, s>>>(job, task, geo.spitch, geo.srows, partials);
+    *n_partials = int(grid.x * grid.y);
+    return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials, int* n_partials,
+                      cudaStream_t s) {
+    if (task.nrows <= 0 || task.nc <= 0) {
+        *n_partials = 0;
+        return cudaSuccess;
+    }
+    switch (task.sw) {
+        case 1: return launch_band<1, 4>(job, task, partials, n_partials, s);
+        case 3: return launch_band<3, 2>(job, task, partials, n_partials, s);
+        case 5: return launch_band<5, 1>(job, task, partials, n_partials, s);
+        case 7: return launch_band<7, 1>(job, task, partials, n_partials, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
+
+cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
+                      int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+                      int n_partials, cudaStream_t s) {
+    const int per_lane = (job.n + 31) / 32;
+    int lane_flush = int(16777216LL / (65025LL * per_lane));
+    if (lane_flush < 1) lane_flush = 1;
+    k_corr_list<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
+                                           partials, lane_flush);
+    return cudaGetLastError();
+}
+
+cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
+                          int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+                          int n_partials, cudaStream_t s) {
+    k_list_f64<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
+                                          partials);
+    return cudaGetLastError();
+}
+
+cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint8_t* deg_c,
+                             CellH* partials, int n_partials, cudaStream_t s) {
+    k_centres_f64<<<n_partials, 256, 0, s>>>(job, to_grid(g), rho_c, deg_c, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
+                           cudaStream_t s) {
+    k_dense_f64<<<n_partials, 256, 0, s>>>(job, surface, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s) {
+    k_reduce_cells<<<1, 1024, 0, s>>>(partials, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c, const uint8_t* deg_c,
+                        const uint8_t* flat, int tflat, const double* thr, const uint8_t* seeded,
+                        int2* locs, unsigned long long max_locs, Tally* tally, uint8_t* visits,
+                        cudaStream_t s) {
+    const size_t E = size_t(g.er) * g.ec;
+    const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 8));
+    k_sec_compact<<<blocks, 256, 0, s>>>(to_grid(g), map, rho_c, deg_c, flat, tflat, thr, seeded,
+                                         locs, max_locs, tally, visits);
+    return cudaGetLastError();
+}
+
+cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, double* thr,
+                           cudaStream_t s) {
+    k_threshold_init<<<1, 1, 0, s>>>(centre_best, has_init, init, thr);
+    return cudaGetLastError();
+}
+
+cudaError_t threshold_raise(const CellH* best, double* thr, cudaStream_t s) {
+    k_threshold_raise<<<1, 1, 0, s>>>(best, thr);
+    return cudaGetLastError();
+}
+
+cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, const double* thr,
+                         double margin, uint8_t* seeded, int2* locs, unsigned long long* count,
+                         unsigned long long max_locs, unsigned long long* n_groups,
+                         unsigned long long max_groups, cudaStream_t s) {
+    const long long G = (long long)g.tr * g.tc;
+    const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 8));
+    k_seed_members<<<blocks, 256, 0, s>>>(to_grid(g), rho_c, deg_c, thr, margin, seeded, locs, count,
+                                          max_locs, n_groups, max_groups);
+    return cudaGetLastError();
+}
+
+cudaError_t first_record(GridDesc g, const int2* locs, const unsigned long long* count,
+                         const double* rho, const uint8_t* deg, const double* map,
+                         const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
+                         double T, unsigned long long after, unsigned long long* best_key,
+                         cudaStream_t s) {
+    cudaMemsetAsync(best_key, 0xff, sizeof(*best_key), s);
+    k_first_record<<<148 * 4, 256, 0, s>>>(to_grid(g), locs, count, rho, deg, map, rho_c, deg_c,
+                                           flat, tflat, T, after, best_key);
+    return cudaGetLastError();
+}
+
+cudaError_t fetch_record_rho(GridDesc g, const int2* locs, const unsigned long long* count,
+                             const double* rho, unsigned long long key, double* out,
+                             cudaStream_t s) {
+    k_fetch_rho<<<148 * 4, 256, 0, s>>>(to_grid(g), locs, count, rho, key, out);
+    return cudaGetLastError();
+}
+
+cudaError_t seq_final(GridDesc g, const int2* locs, const unsigned long long* count,
+                      const double* rho, const uint8_t* deg, const double* map,
+                      const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
+                      double T0, const unsigned long long* rec_key, const double* rec_T, int n_rec,
+                      Tally* tally, uint8_t* visits, CellH* partials, int n_partials,
+                      cudaStream_t s) {
+    k_seq_final<<<n_partials, 256, 0, s>>>(to_grid(g), locs, count, rho, deg, map, rho_c, deg_c,
+                                           flat, tflat, T0, rec_key, rec_T, n_rec, tally, visits,
+                                           partials);
+    return cudaGetLastError();
+}
+
+}  // namespace tmk

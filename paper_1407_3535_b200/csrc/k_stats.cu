@@ -1,0 +1,316 @@
+// k_stats.cu -- image preparation, window statistics and running sums (sm_100a).
+//
+// Integer path (8-bit images, the reference's input domain): window sums S and Q are
+// exact integers, accumulated with a row-sliding pass then a column-sliding pass; the
+// FP64 epilogue replays stats.cpp:83-92 with _rn intrinsics, so mu/omega/flat are bit
+// identical to the reference.
+//
+// Replica path (non-integer images, e.g. OptA's blurred image): the reference's FP64
+// prefix table (stats.cpp:26-37: sequential row accumulation, then prefix[r+1] =
+// prefix[r] + row_acc) is rebuilt in the same operation order -- one thread scans one
+// row (through a shared-memory transpose for coalescing), one thread accumulates one
+// column -- and window sums use the reference's difference order (stats.cpp:50).
+#include "kernels.hpp"
+#include "tm_common.cuh"
+
+namespace tmk {
+
+namespace {
+
+__global__ void k_check_u8(const double* __restrict__ img, size_t n, int* bad) {
+    int local = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const double v = img[i];
+        if (!(v >= 0.0 && v <= 255.0) || v != rint(v)) local = 1;
+    }
+    if (__syncthreads_or(local) && threadIdx.x == 0) atomicOr(bad, 1);
+}
+
+__global__ void k_f64_to_u8(const double* __restrict__ img, size_t n, uint8_t* __restrict__ out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        out[i] = uint8_t(img[i]);
+}
+
+__global__ void k_u8_to_f64(const uint8_t* __restrict__ img, size_t n, double* __restrict__ out) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        out[i] = double(img[i]);
+}
+
+// Float copy with a padded pitch; the pad columns are zero so vector loads past the last
+// column read zeros.
+__global__ void k_u8_to_f32(const uint8_t* __restrict__ img, int p, int q, float* __restrict__ out,
+                            int pitch) {
+    const int r = blockIdx.y;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x)
+        out[size_t(r) * pitch + c] = c < q ? float(img[size_t(r) * q + c]) : 0.0f;
+}
+
+__global__ void k_sum_sq_u8(const uint8_t* __restrict__ img, size_t n,
+                            unsigned long long* out) {
+    unsigned long long acc = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const unsigned v = img[i];
+        acc += v * v;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+// q_total for non-integer images.  The reference sums sequentially (stats.cpp:79); a
+// parallel tree sum differs in the last bits, which only matters for windows whose
+// variance sits exactly on the prefix-noise floor (documented in DESIGN.md).
+__global__ void k_sum_sq_f64(const double* __restrict__ img, size_t n, double* out) {
+    double acc = 0.0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x)
+        acc += img[i] * img[i];
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+}
+
+constexpr int kChunk = 32;
+
+// Row pass: hs[r][c] = sum_{j<n} I(r, c+j), hq likewise for I^2; one thread owns kChunk
+// consecutive output columns of one row and slides the window.
+__global__ void k_hsum_u8(const uint8_t* __restrict__ img, int p, int q, int n,
+                          int* __restrict__ hs, int* __restrict__ hq) {
+    const int ec = q - n + 1;
+    const int r = blockIdx.y;
+    const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * kChunk;
+    if (c0 >= ec) return;
+    const uint8_t* row = img + size_t(r) * q;
+    int s = 0, sq = 0;
+    for (int j = 0; j < n; ++j) {
+        const int v = row[c0 + j];
+        s += v;
+        sq += v * v;
+    }
+    const int c1 = min(c0 + kChunk, ec);
+    int* os = hs + size_t(r) * ec;
+    int* oq = hq ? hq + size_t(r) * ec : nullptr;
+    for (int c = c0; c < c1; ++c) {
+        os[c] = s;
+        if (oq) oq[c] = sq;
+        if (c + 1 < c1) {
+            const int vin = row[c + n], vout = row[c];
+            s += vin - vout;
+            sq += vin * vin - vout * vout;
+        }
+    }
+}
+
+// Column pass + FP64 epilogue: S, Q over m rows of the row sums; one thread owns kChunk
+// consecutive output rows of one column (coalesced across the warp).
+__global__ void k_vsum_stats(const int* __restrict__ hs, const int* __restrict__ hq, int p,
+                             int ec, int m, int n, double prefix_noise, DevStats st) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int er = p - m + 1;
+    const int r0 = blockIdx.y * kChunk;
+    if (c >= ec || r0 >= er) return;
+    long long s = 0, sq = 0;
+    for (int i = 0; i < m; ++i) {
+        s += hs[size_t(r0 + i) * ec + c];
+        sq += hq[size_t(r0 + i) * ec + c];
+    }
+    const double inv_mn = 1.0 / (double(m) * double(n));
+    const long long mn = (long long)m * n;
+    const int r1 = min(r0 + kChunk, er);
+    for (int r = r0; r < r1; ++r) {
+        const size_t k = size_t(r) * ec + c;
+        double mu, om;
+        uint8_t fl;
+        window_epilogue(double(s), double(sq), inv_mn, mn, prefix_noise, mu, om, fl);
+        st.mu[k] = mu;
+        st.omega[k] = om;
+        st.flat[k] = fl;
+        if (r + 1 < r1) {
+            s += hs[size_t(r + m) * ec + c] - hs[size_t(r) * ec + c];
+            sq += hq[size_t(r + m) * ec + c] - hq[size_t(r) * ec + c];
+        }
+    }
+}
+
+__global__ void k_vsum_only(const int* __restrict__ hs, int p, int ec, int m,
+                            double* __restrict__ out) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const int er = p - m + 1;
+    const int r0 = blockIdx.y * kChunk;
+    if (c >= ec || r0 >= er) return;
+    long long s = 0;
+    for (int i = 0; i < m; ++i) s += hs[size_t(r0 + i) * ec + c];
+    const int r1 = min(r0 + kChunk, er);
+    for (int r = r0; r < r1; ++r) {
+        out[size_t(r) * ec + c] = double(s);
+        if (r + 1 < r1) s += hs[size_t(r + m) * ec + c] - hs[size_t(r) * ec + c];
+    }
+}
+
+// ---- replica prefix ------------------------------------------------------------------
+__device__ __forceinline__ double src_value(const ProdSrc& s, int a, int b) {
+    const double x = s.X[size_t(a + s.xr) * s.xq + (b + s.xc)];
+    if (s.square) return __dmul_rn(x, x);
+    if (s.Y) return __dmul_rn(x, s.Y[size_t(a + s.yr) * s.yq + (b + s.yc)]);
+    return x;
+}
+
+// One warp = 32 rows.  Tiles of 32 columns are staged through shared memory so global
+// reads/writes stay coalesced while each lane scans its own row sequentially
+// (row_acc += v, stats.cpp:34).
+__global__ void k_rowscan(ProdSrc src, int rows, int cols, double* __restrict__ rowacc) {
+    __shared__ double tile[4][32][33];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r0 = (blockIdx.x * 4 + wid) * 32;
+    if (r0 >= rows) return;
+    double acc = 0.0;
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+        const int c = c0 + lane;
+        for (int k = 0; k < 32; ++k) {
+            const int r = r0 + k;
+            tile[wid][k][lane] = (r < rows && c < cols) ? src_value(src, r, c) : 0.0;
+        }
+        __syncwarp();
+        const int cn = min(32, cols - c0);
+        for (int j = 0; j < cn; ++j) {
+            acc = __dadd_rn(acc, tile[wid][lane][j]);
+            tile[wid][lane][j] = acc;
+        }
+        __syncwarp();
+        for (int k = 0; k < 32; ++k) {
+            const int r = r0 + k;
+            if (r < rows && c < cols) rowacc[size_t(r) * cols + c] = tile[wid][k][lane];
+        }
+        __syncwarp();
+    }
+}
+
+// prefix[(r+1)][c+1] = prefix[r][c+1] + rowacc[r][c]  (stats.cpp:35), one thread per column.
+__global__ void k_colacc(const double* __restrict__ rowacc, int rows, int cols,
+                         double* __restrict__ prefix) {
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t pw = size_t(cols) + 1;
+    if (c > cols) return;
+    prefix[c] = 0.0;  // zero top row
+    if (c == cols) {
+        for (int r = 0; r < rows; ++r) prefix[size_t(r + 1) * pw] = 0.0;  // zero first col
+        return;
+    }
+    double acc = 0.0;
+    for (int r = 0; r < rows; ++r) {
+        acc = __dadd_rn(acc, rowacc[size_t(r) * cols + c]);
+        prefix[size_t(r + 1) * pw + c + 1] = acc;
+    }
+}
+
+__global__ void k_window_diff(const double* __restrict__ prefix, int rows, int cols, int m, int n,
+                              double* __restrict__ out) {
+    const int er = rows - m + 1, ec = cols - n + 1;
+    const size_t pw = size_t(cols) + 1;
+    const size_t total = size_t(er) * ec;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < total;
+         k += size_t(gridDim.x) * blockDim.x) {
+        const int r = int(k / ec), c = int(k % ec);
+        const double* top = prefix + size_t(r) * pw;
+        const double* bot = prefix + size_t(r + m) * pw;
+        out[k] = __dadd_rn(__dsub_rn(__dsub_rn(bot[c + n], top[c + n]), bot[c]), top[c]);
+    }
+}
+
+__global__ void k_stats_from_sums(const double* __restrict__ S, const double* __restrict__ Q,
+                                  size_t E, int m, int n, double prefix_noise, DevStats st) {
+    const double inv_mn = 1.0 / (double(m) * double(n));
+    const long long mn = (long long)m * n;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+         k += size_t(gridDim.x) * blockDim.x) {
+        double mu, om;
+        uint8_t fl;
+        window_epilogue(S[k], Q[k], inv_mn, mn, prefix_noise, mu, om, fl);
+        st.mu[k] = mu;
+        st.omega[k] = om;
+        st.flat[k] = fl;
+    }
+}
+
+int grid_for(size_t n, int threads) {
+    const size_t b = (n + threads - 1) / threads;
+    return int(b < 148 * 16 ? (b ? b : 1) : 148 * 16);
+}
+
+}  // namespace
+
+cudaError_t check_u8_domain(const double* img, size_t n, int* bad, cudaStream_t s) {
+    k_check_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, bad);
+    return cudaGetLastError();
+}
+cudaError_t f64_to_u8(const double* img, size_t n, uint8_t* out, cudaStream_t s) {
+    k_f64_to_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+    return cudaGetLastError();
+}
+cudaError_t u8_to_f64(const uint8_t* img, size_t n, double* out, cudaStream_t s) {
+    k_u8_to_f64<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+    return cudaGetLastError();
+}
+cudaError_t u8_to_f32_pitched(const uint8_t* img, int p, int q, float* out, int pitch,
+                              cudaStream_t s) {
+    dim3 grid((pitch + 255) / 256, p);
+    k_u8_to_f32<<<grid, 256, 0, s>>>(img, p, q, out, pitch);
+    return cudaGetLastError();
+}
+cudaError_t sum_sq_u8(const uint8_t* img, size_t n, unsigned long long* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(*out), s);
+    k_sum_sq_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+    return cudaGetLastError();
+}
+cudaError_t sum_sq_f64(const double* img, size_t n, double* out, cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof(*out), s);
+    k_sum_sq_f64<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, double prefix_noise,
+                            int* hs, int* hq, DevStats st, cudaStream_t s) {
+    const int ec = q - n + 1, er = p - m + 1;
+    const int tpr = (ec + kChunk - 1) / kChunk;
+    dim3 g1((tpr + 127) / 128, p);
+    k_hsum_u8<<<g1, 128, 0, s>>>(img, p, q, n, hs, hq);
+    dim3 g2((ec + 127) / 128, (er + kChunk - 1) / kChunk);
+    k_vsum_stats<<<g2, 128, 0, s>>>(hs, hq, p, ec, m, n, prefix_noise, st);
+    return cudaGetLastError();
+}
+
+cudaError_t window_sums_u8(const uint8_t* img, int p, int q, int m, int n, int* hs, double* out,
+                           cudaStream_t s) {
+    const int ec = q - n + 1, er = p - m + 1;
+    const int tpr = (ec + kChunk - 1) / kChunk;
+    dim3 g1((tpr + 127) / 128, p);
+    k_hsum_u8<<<g1, 128, 0, s>>>(img, p, q, n, hs, nullptr);
+    dim3 g2((ec + 127) / 128, (er + kChunk - 1) / kChunk);
+    k_vsum_only<<<g2, 128, 0, s>>>(hs, p, ec, m, out);
+    return cudaGetLastError();
+}
+
+cudaError_t replica_prefix(ProdSrc src, int rows, int cols, double* rowacc, double* prefix,
+                           cudaStream_t s) {
+    const int warps = (rows + 31) / 32;
+    k_rowscan<<<(warps + 3) / 4, 128, 0, s>>>(src, rows, cols, rowacc);
+    k_colacc<<<(cols + 1 + 127) / 128, 128, 0, s>>>(rowacc, rows, cols, prefix);
+    return cudaGetLastError();
+}
+
+cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m, int n,
+                                double* out, cudaStream_t s) {
+    const size_t E = size_t(rows - m + 1) * (cols - n + 1);
+    k_window_diff<<<grid_for(E, 256), 256, 0, s>>>(prefix, rows, cols, m, n, out);
+    return cudaGetLastError();
+}
+
+cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
+                            double prefix_noise, DevStats st, cudaStream_t s) {
+    k_stats_from_sums<<<grid_for(E, 256), 256, 0, s>>>(S, Q, E, m, n, prefix_noise, st);
+    return cudaGetLastError();
+}
+
+}  // namespace tmk

@@ -1,0 +1,187 @@
+// kernels.hpp -- host-callable launchers for the tmatch sm_100a kernels.
+//
+// Every launcher is asynchronous on the given stream and returns the launch error.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmk {
+
+struct DevStats {  // WindowStats (stats.hpp:35-47) resident in HBM
+    double* mu = nullptr;
+    double* omega = nullptr;
+    uint8_t* flat = nullptr;
+    int er = 0, ec = 0, m = 0, n = 0;
+};
+
+struct GridDesc {  // GroupGrid (autocorr.hpp:24-52)
+    int er, ec, h, w, tr, tc;
+};
+
+struct TStatsH {  // TemplateStats (detail.hpp:24-28) + mn
+    double mu, omega, mn;
+    int flat;
+};
+
+struct CellH {  // BestCell, device layout of tmk::Cell
+    double rho;
+    int row, col;
+    int flags;  // bit0 valid, bit1 degenerate
+};
+
+struct Tally {  // accumulated on device by the search kernels
+    unsigned long long eliminated;
+    unsigned long long retained;
+    unsigned long long survivors;  // entries appended to the survivor list
+    unsigned long long pad;
+};
+
+// ---- image preparation ---------------------------------------------------------------
+cudaError_t check_u8_domain(const double* img, size_t n, int* bad, cudaStream_t s);
+cudaError_t f64_to_u8(const double* img, size_t n, uint8_t* out, cudaStream_t s);
+cudaError_t u8_to_f32_pitched(const uint8_t* img, int p, int q, float* out, int pitch,
+                              cudaStream_t s);
+cudaError_t u8_to_f64(const uint8_t* img, size_t n, double* out, cudaStream_t s);
+cudaError_t sum_sq_u8(const uint8_t* img, size_t n, unsigned long long* out, cudaStream_t s);
+cudaError_t sum_sq_f64(const double* img, size_t n, double* out, cudaStream_t s);
+
+// ---- window statistics, exact integer path (stats.cpp:55-94) ---------------------------
+// hs/hq scratch: p * ec int32 each.
+cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, double prefix_noise,
+                            int* hs, int* hq, DevStats st, cudaStream_t s);
+// Window sums of an 8-bit image as exact doubles (running_sum on integer data).
+cudaError_t window_sums_u8(const uint8_t* img, int p, int q, int m, int n, int* hs,
+                           double* out, cudaStream_t s);
+
+// ---- FP64 replica running sums (stats.cpp:19-53 operation order) -----------------------
+// Source of the prefix table: value(a,b) = X[(a+xo_r)*xq + b+xo_c] (* Y[...] when Y != 0,
+// or squared when square != 0), over a rows x cols region.
+struct ProdSrc {
+    const double* X;
+    int xq, xr, xc;
+    const double* Y;
+    int yq, yr, yc;
+    int square;
+};
+// rowacc: rows*cols; prefix: (rows+1)*(cols+1) with zero first row/col.
+cudaError_t replica_prefix(ProdSrc src, int rows, int cols, double* rowacc, double* prefix,
+                           cudaStream_t s);
+// out[r][c] = bot[c+n] - top[c+n] - bot[c] + top[c] for the full (rows-m+1)x(cols-n+1).
+cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m, int n,
+                                double* out, cudaStream_t s);
+// stats epilogue from FP64 window sums S, Q (E entries).
+cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
+                            double prefix_noise, DevStats st, cudaStream_t s);
+
+// ---- local auto-correlation + retained count (autocorr.cpp:40-96, egs.cpp:12-25) -------
+cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc g, DevStats st,
+                        double retain_threshold, double* map, unsigned long long* n_r,
+                        cudaStream_t s);
+// replica path, one offset: cross-sum prefix table of the product image for (di,dj).
+cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
+                                     GridDesc g, DevStats st, int di, int dj, double* map,
+                                     cudaStream_t s);
+cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s);  // zeros + centres=1
+cudaError_t retained_count(const double* map, GridDesc g, double threshold,
+                           unsigned long long* n_r, cudaStream_t s);
+
+// ---- correlation -----------------------------------------------------------------------
+struct CorrJob {
+    // image (integer path uses imgf, FP64 path uses imgd)
+    const float* imgf;
+    int pitch;  // floats per row of imgf
+    const double* imgd;
+    int q;  // columns of imgd
+    // template
+    const float* tf;  // m x npad, zero padded
+    int npad;
+    const double* td;  // m x n
+    int m, n;
+    int flush_rows;  // FP32-exact flush period in template rows
+    TStatsH ts;
+    DevStats st;
+};
+
+// Dense band evaluation over rows[] x {cbase + k*sw : k < nc}.  mode 0: argmax (+surface
+// if out_rho != 0, indexed r*ec + c); mode 1: centre scan (out_rho/out_deg indexed
+// yi*tc + k + col0); mode 2: masked by visits == 2 (survivor tiles).
+struct BandTask {
+    const int* rows;
+    int nrows;
+    int cbase, sw, nc;
+    int mode;
+    int row_span;  // max over 8-row bands of rows[yb+7]-rows[yb] (staging height - kIC)
+    int col0;  // column-index offset for mode 1 group indexing
+    int tc;    // groups per grid row (mode 1)
+    double* out_rho;
+    uint8_t* out_deg;
+    const uint8_t* mask;  // mode 2
+};
+cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
+                      int* n_partials, cudaStream_t s);
+// Warp-per-location evaluation of a location list (int2 row,col), argmax into partials.
+// out_rho/out_deg (optional) are indexed by list position.
+cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
+                      int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+                      int n_partials, cudaStream_t s);
+// FP64 replica (window_dot order, detail.hpp:32-41) over a location list or a dense range.
+cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
+                          int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+                          int n_partials, cudaStream_t s);
+cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint8_t* deg_c,
+                             CellH* partials, int n_partials, cudaStream_t s);
+cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
+                           cudaStream_t s);
+
+// Reduce partial cells -> out[0] (better_candidate order).
+cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s);
+
+// ---- scan 2 (matcher.cpp:48-78) ---------------------------------------------------------
+// threshold read from *thr (device).  Survivors appended to locs (int2) with counters in
+// tally.  visits (optional, E bytes) receives kVisit codes.
+cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c,
+                        const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
+                        const uint8_t* seeded, int2* locs, unsigned long long max_locs,
+                        Tally* tally, uint8_t* visits, cudaStream_t s);
+// Threshold bootstrap: thr = max(best non-degenerate centre rho, init) (matcher.cpp:121-125)
+cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, double* thr,
+                           cudaStream_t s);
+// Seeded policy: members of every group whose centre rho >= thr - margin -> list.
+cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, const double* thr,
+                         double margin, uint8_t* seeded, int2* locs, unsigned long long* count,
+                         unsigned long long max_locs, unsigned long long* n_groups,
+                         unsigned long long max_groups, cudaStream_t s);
+cudaError_t threshold_raise(const CellH* best, double* thr, cudaStream_t s);
+// Sequential policy replay: candidates = scan-2 survivors at T0 with their rho.
+cudaError_t first_record(GridDesc g, const int2* locs, const unsigned long long* count,
+                         const double* rho, const uint8_t* deg, const double* map,
+                         const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
+                         double T, unsigned long long after, unsigned long long* best_key,
+                         cudaStream_t s);
+cudaError_t fetch_record_rho(GridDesc g, const int2* locs, const unsigned long long* count,
+                             const double* rho, unsigned long long key, double* out,
+                             cudaStream_t s);
+cudaError_t seq_final(GridDesc g, const int2* locs, const unsigned long long* count,
+                      const double* rho, const uint8_t* deg, const double* map,
+                      const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
+                      double T0, const unsigned long long* rec_key, const double* rec_T, int n_rec,
+                      Tally* tally, uint8_t* visits, CellH* partials, int n_partials,
+                      cudaStream_t s);
+
+// ---- blur / OptA (blur.cpp) -----------------------------------------------------------
+cudaError_t blur_replica(const double* img, int p, int q, const double* prof_dev, int len,
+                         double* tmp, double* out, cudaStream_t s);
+cudaError_t fidelity_epilogue(const double* cross, DevStats orig, DevStats blur, double* fid,
+                              cudaStream_t s);
+cudaError_t changed_mask(const double* a, const double* b, size_t n, uint8_t* out,
+                         cudaStream_t s);
+cudaError_t mark_violations(const double* fid, const double* changed_in_window, size_t E,
+                            double lambda, uint8_t* marks, unsigned long long* count,
+                            cudaStream_t s);
+cudaError_t restore_covered(double* blurred, const double* original, const uint8_t* marks,
+                            int er, int ec, int m, int n, int p, int q, int* scratch,
+                            cudaStream_t s);
+
+}  // namespace tmk

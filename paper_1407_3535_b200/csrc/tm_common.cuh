@@ -1,0 +1,147 @@
+// tm_common.cuh -- device helpers shared by the tmatch sm_100a kernels.
+//
+// Bit-exactness discipline: every FP64 expression that the reference evaluates in a
+// fixed order is written with explicit _rn intrinsics (no FMA contraction), mirroring
+// the cited reference line.  Integer work (window sums, dot products on u8 data) is
+// exact in any order and is free to be re-associated.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace tmk {
+
+constexpr double kEps = 2.220446049250313e-16;
+
+__device__ __forceinline__ double dmax(double a, double b) { return (a < b) ? b : a; }
+__device__ __forceinline__ double dmin(double a, double b) { return (b < a) ? b : a; }
+// std::clamp(v, lo, hi)
+__device__ __forceinline__ double dclamp(double v, double lo, double hi) {
+    return (v < lo) ? lo : ((hi < v) ? hi : v);
+}
+
+// detail.hpp:18-22 variance_is_flat
+__device__ __forceinline__ bool variance_is_flat(double var_sum, double q_sum, long long mn) {
+    const double abs_tol = __dmul_rn(1e-9, double(mn));
+    const double rel = dmax(1e-13, __dmul_rn(__dmul_rn(4.0, kEps), double(mn)));
+    return var_sum <= dmax(__dmul_rn(abs_tol, abs_tol), __dmul_rn(rel, q_sum));
+}
+
+// stats.cpp:84-91: per-window epilogue from exact sums S, Q.
+__device__ __forceinline__ void window_epilogue(double sum, double sq, double inv_mn,
+                                                long long mn, double prefix_noise, double& mu,
+                                                double& omega, uint8_t& flat) {
+    const double var_sum = __dsub_rn(sq, __dmul_rn(__dmul_rn(sum, sum), inv_mn));
+    const bool f = variance_is_flat(var_sum, sq, mn) || var_sum <= prefix_noise;
+    mu = __dmul_rn(sum, inv_mn);
+    omega = f ? 0.0 : __dsqrt_rn(dmax(0.0, var_sum));
+    flat = f ? 1 : 0;
+}
+
+// Template statistics shared by every correlation launch (stats.cpp:98-111, computed on
+// the host in reference order).
+struct TStats {
+    double mu, omega;
+    double mn;  // double(m) * double(n)
+    int flat;
+};
+
+// detail.hpp:45-51 zncc_at epilogue given the window dot product.
+__device__ __forceinline__ double zncc_epilogue(double dot, const TStats& ts, double mu_w,
+                                                double omega_w, bool flat_w) {
+    if (ts.flat || flat_w) return 0.0;
+    const double num = __dsub_rn(dot, __dmul_rn(__dmul_rn(ts.mn, ts.mu), mu_w));
+    return dclamp(__ddiv_rn(num, __dmul_rn(ts.omega, omega_w)), -1.0, 1.0);
+}
+
+// bounds.cpp:21-23, 41-46 (inputs already clamped, so `checked` never throws here).
+__device__ __forceinline__ double half_gap(double a, double b) {
+    return __dmul_rn(__dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(a, a)))),
+                     __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b)))));
+}
+__device__ __forceinline__ bool sec_holds(double tb, double a, double b) {
+    tb = dclamp(tb, -1.0, 1.0);
+    a = dclamp(a, -1.0, 1.0);
+    b = dclamp(b, -1.0, 1.0);
+    return tb >= __dadd_rn(__dmul_rn(a, b), half_gap(a, b));
+}
+
+// ---- BestCell (stats.hpp:71-79) and better_candidate (stats.cpp:147-154) ----------
+struct Cell {
+    double rho;
+    int row, col;
+    int flags;  // bit0 valid, bit1 degenerate
+};
+
+__device__ __forceinline__ Cell no_cell() { return Cell{0.0, -1, -1, 2}; }
+__device__ __forceinline__ Cell make_cell(int r, int c, double rho, bool degenerate) {
+    return Cell{rho, r, c, 1 | (degenerate ? 2 : 0)};
+}
+
+__device__ __forceinline__ bool better(const Cell& a, const Cell& b) {
+    if (!(a.flags & 1)) return false;
+    if (!(b.flags & 1)) return true;
+    const bool da = a.flags & 2, db = b.flags & 2;
+    if (da != db) return !da;
+    if (a.rho != b.rho) return a.rho > b.rho;
+    if (a.row != b.row) return a.row < b.row;
+    return a.col < b.col;
+}
+
+__device__ __forceinline__ Cell shfl_cell(const Cell& c, int src_lane_xor) {
+    Cell o;
+    o.rho = __shfl_xor_sync(0xffffffffu, c.rho, src_lane_xor);
+    o.row = __shfl_xor_sync(0xffffffffu, c.row, src_lane_xor);
+    o.col = __shfl_xor_sync(0xffffffffu, c.col, src_lane_xor);
+    o.flags = __shfl_xor_sync(0xffffffffu, c.flags, src_lane_xor);
+    return o;
+}
+
+__device__ __forceinline__ Cell warp_best(Cell c) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const Cell o = shfl_cell(c, s);
+        if (better(o, c)) c = o;
+    }
+    return c;
+}
+
+// Block-wide best; result valid in thread 0.  `scratch` needs blockDim/32 Cells.
+__device__ __forceinline__ Cell block_best(Cell c, Cell* scratch) {
+    c = warp_best(c);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    if (lane == 0) scratch[wid] = c;
+    __syncthreads();
+    if (wid == 0) {
+        const int nw = (blockDim.x + 31) >> 5;
+        c = lane < nw ? scratch[lane] : no_cell();
+        c = warp_best(c);
+    }
+    __syncthreads();
+    return c;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) v += __shfl_xor_sync(0xffffffffu, v, s);
+    return v;
+}
+
+// Group geometry (autocorr.cpp:12-32): tiles anchored at (0,0), clipped edge tiles,
+// centre = (r0 + r1) / 2.
+struct Grid {
+    int er, ec, h, w, tr, tc;
+    __device__ __forceinline__ int tile_r(int r) const { return min(r / h, tr - 1); }
+    __device__ __forceinline__ int tile_c(int c) const { return min(c / w, tc - 1); }
+    __device__ __forceinline__ int center_row(int ti) const {
+        const int r0 = ti * h, r1 = min(r0 + h, er) - 1;
+        return (r0 + r1) >> 1;
+    }
+    __device__ __forceinline__ int center_col(int tj) const {
+        const int c0 = tj * w, c1 = min(c0 + w, ec) - 1;
+        return (c0 + c1) >> 1;
+    }
+};
+
+}  // namespace tmk
