@@ -1,0 +1,332 @@
+#!/usr/bin/env python3
+"""Benchmark: ZNCC-equivalent search locations/s and ms/search (BASELINE.json metric).
+
+One step = one full exhaustive-accuracy search of one template through the B200 path:
+window statistics + EGS group sizing (prepare_egs) + centre scan + transitive-bound
+elimination + survivor ZNCC + argmax (run_egs), on BASELINE config 2 (2048x2048 1/f^1.8
+image with half the tiles blurred, one 64x64 template; seeded synthetic data).
+
+  value : extent locations per second of device time, image resident in HBM, L2 flushed
+          between steps (the device-timed step excludes the flush).
+  e2e   : the same metric through the reference-facing call tm_match() (host FP64 image
+          in pinned memory -> device -> result back to the host), wall-clock per step.
+
+--impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
+/root/reference) on the same workload with all host threads.
+
+Multi-GPU (torchrun): each rank searches its own seeded C2 replica (weak scaling); the
+best cells are all-gathered over NCCL and merged in better_candidate order.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "ZNCC-equivalent search locations/sec"
+UNIT = "locations/s"
+
+
+def _peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def cpu_baseline(workload, threads=None, kind=None):
+    """Reference CPU path on the same C2 search (prepare_egs + run_egs, frozen policy)."""
+    from oracle import binding as ob
+    threads = threads or os.cpu_count()
+    t = workload.templates[0].pixels.astype(np.float64)
+    img = workload.image.astype(np.float64)
+    if kind in (None, "reference") and ob.available("ref"):
+        ref = ob.Oracle("ref", autobuild=False)
+        t0 = time.perf_counter()
+        res, prep_ms, run_ms = ref.prepare_run_egs(t, img, parallel=True, threads=threads)
+        wall = time.perf_counter() - t0
+        return {"value": workload.extent / wall, "unit": UNIT, "cores": threads,
+                "kind": "reference",
+                "sample": f"1 full {workload.name} search (reference prepare_egs {prep_ms:.0f} ms "
+                          f"1 thread + run_egs frozen policy {run_ms:.0f} ms on {threads} "
+                          f"threads)", "ms_per_search": wall * 1e3,
+                "best": [res.best_row, res.best_col, res.best_rho],
+                "elim_pct": res.elim_pct}
+    port = ob.Oracle("port")
+    t0 = time.perf_counter()
+    res = port.match(t, img, mode="egs", parallel=True, threads=2)
+    wall = time.perf_counter() - t0
+    return {"value": workload.extent / wall, "unit": UNIT, "cores": 1, "kind": "port",
+            "sample": f"1 full {workload.name} search (C restatement, frozen policy, 1 thread)",
+            "ms_per_search": wall * 1e3, "best": [res.best_row, res.best_col, res.best_rho],
+            "elim_pct": res.elim_pct}
+
+
+def run_reference(args):
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    from paper_1407_3535_b200 import workloads as W
+    wl = W.make(args.config)
+    # bounded: each step is one full reference search (~seconds); cap the run time
+    per = []
+    t_start = time.perf_counter()
+    steps_done = 0
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(wl)
+        if i >= args.warmup:
+            per.append(cb["ms_per_search"])
+            steps_done += 1
+        if time.perf_counter() - t_start > args.reference_budget_s and steps_done >= 1:
+            break
+    ms = statistics.mean(per)
+    value = wl.extent / (ms / 1e3)
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps_done, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded 1/f^beta, SURVEY 8d)",
+            "config": {"workload": f"{wl.name}: {wl.description}", "extent": wl.extent,
+                       "templates": 1, "mode": "egs", "policy": "reference frozen (--parallel)"},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cb["cores"],
+                             "kind": cb["kind"], "sample": cb["sample"]},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    if steps_done < args.steps:
+        line["note"] = f"bounded: {steps_done} of {args.steps} steps within the time budget"
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def run_b200(args):
+    import torch
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    torch.cuda.set_device(local)
+    from paper_1407_3535_b200 import api, workloads as W
+
+    wl = W.make(args.config, seed=W.CONFIGS[args.config].__defaults__[0] + 1000 * rank) \
+        if ws > 1 else W.make(args.config)
+    tmpl = wl.templates[0].pixels
+    m, n = tmpl.shape
+    ctx = api.Context(local)
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device(f"cuda:{local}"))
+    img = ctx.image(wl.image)  # resident in HBM for the device-timed value
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+
+    def step():
+        img.reset_cache()  # recompute window statistics: nothing cached across steps
+        prep = ctx.prepare(img, m, n, mode="egs")
+        res = ctx.run(prep, tmpl, policy=args.policy)
+        info = prep.info
+        prep.close()
+        return res, info
+
+    for _ in range(args.warmup):
+        step()
+    ctx.synchronize()
+    if ws > 1:
+        torch.distributed.barrier()
+    ctx.set_profiling(True)
+    launches0 = ctx.launches
+    clocks = ClockSampler(local)
+    clocks.start()
+    times = []
+    res = info = None
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()  # L2 flush (512 MB > 126 MB L2), outside the timed span
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            e0.record(stream)
+        res, info = step()
+        e1.record(stream)
+        e1.synchronize()
+        times.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    launches = (ctx.launches - launches0) / args.steps
+    phases = ctx.phase_times()
+    ctx.set_profiling(False)
+    ms = statistics.mean(times)
+    if ws > 1:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+        torch.distributed.barrier()
+    value = ws * wl.extent / (ms / 1e3)
+
+    # ---- e2e through the reference-facing C ABI call (host FP64 buffers) -------------
+    img_host = torch.empty(wl.image.shape, dtype=torch.float64, pin_memory=True)
+    img_host.numpy()[:] = wl.image
+    t_host = tmpl.astype(np.float64)
+    for _ in range(max(1, args.warmup)):
+        ctx.match(t_host, img_host.numpy(), mode="egs", policy=args.policy)
+    e2e_ms = []
+    for _ in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        r2 = ctx.match(t_host, img_host.numpy(), mode="egs", policy=args.policy)
+        e2e_ms.append((time.perf_counter() - t0) * 1e3)
+    e2e = statistics.mean(e2e_ms)
+    if ws > 1:
+        t = torch.tensor([e2e], device=f"cuda:{local}")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        e2e = float(t.item())
+    assert (r2.best_row, r2.best_col) == (res.best_row, res.best_col)
+
+    if rank != 0:
+        if ws > 1:
+            torch.distributed.destroy_process_group()
+        return 0
+
+    # ---- roofline of the dominant kernel ---------------------------------------------
+    peaks = _peaks()
+    G = res.centers
+    cs = phases.get("centre_scan", {"count": 1, "ms": float("nan")})
+    cs_ms = cs["ms"] / max(cs["count"], 1)
+    flops = 2.0 * m * n * G
+    sm_max = peaks.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
+    achieved = flops / (cs_ms / 1e3) / 1e12
+    share = cs["ms"] / max(sum(p["ms"] for p in phases.values()), 1e-9)
+    roofline = {"bound": "fp32", "kernel": "k_corr_band (centre scan, FP32-exact FFMA)",
+                "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
+                "frac": achieved / fp32_peak, "traffic": None,
+                "peak_source": f"nominal FP32 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
+                               "(MEASURED_PEAKS.json has no FP32 entry)",
+                "algorithmic": f"2*m*n FLOP per centre x {G} centres per launch",
+                "kernel_ms": cs_ms, "share_of_step": share}
+
+    cpu = None
+    if not args.no_cpu_baseline:
+        try:
+            cb = cpu_baseline(wl)
+            cpu = {k: cb[k] for k in ("value", "unit", "cores", "kind", "sample")}
+        except Exception as e:  # the oracle may be absent on a foreign box
+            cpu = {"value": None, "unit": UNIT, "cores": 0, "kind": "port",
+                   "sample": f"unavailable: {e}"}
+
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "u8->fp32-exact (int dot), f64 epilogue",
+        "data": "synthetic (seeded 1/f^beta generator, SURVEY 8d; BASELINE config 2)",
+        "config": {"workload": f"{wl.name}: {wl.description}", "extent": wl.extent,
+                   "templates": 1, "mode": "egs", "policy": args.policy,
+                   "l2": "flushed between steps (512 MB write, untimed)",
+                   "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+        "result": {"best_row": res.best_row, "best_col": res.best_col, "best_rho": res.best_rho,
+                   "elim_pct": res.elim_pct, "eliminated": res.eliminated,
+                   "retained": res.retained, "centers": res.centers, "h_e": info["h"],
+                   "prep_ms": info["prep_ms"]},
+        "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in phases.items()},
+        "gpu_launches": launches,
+        "e2e": {"value": ws * wl.extent / (e2e / 1e3), "unit": UNIT,
+                "h2d_bytes_per_step": int(wl.image.size * 8 + tmpl.size * 8),
+                "d2h_bytes_per_step": 128, "ms_per_step": e2e},
+        "roofline": roofline,
+        "cpu_baseline": cpu,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    if ws > 1:
+        torch.distributed.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--policy", default="seeded",
+                    choices=["seeded", "frozen", "sequential", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--reference-budget-s", type=float, default=150.0)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "b200" else args.warmup
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

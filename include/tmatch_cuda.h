@@ -215,6 +215,14 @@ int tm_match(tm_ctx* ctx, const double* tmpl, int m, int n, const double* image,
 
 /* Instrumentation: number of kernels this context launched (bench gpu_launches). */
 int64_t tm_ctx_launch_count(const tm_ctx* ctx);
+/* The context's CUDA stream (cudaStream_t) for callers that time or order work on it. */
+void* tm_ctx_stream(tm_ctx* ctx);
+/* Per-phase device timing with CUDA events on the context stream (off by default). */
+int tm_ctx_set_profiling(tm_ctx* ctx, int enable);
+/* JSON {"phase": [launch_groups, total_ms], ...} accumulated since profiling was enabled. */
+int tm_ctx_phase_times(tm_ctx* ctx, char* buf, size_t len);
+/* Drop the cached window statistics so the next call recomputes them (benchmarks). */
+int tm_image_reset_cache(tm_image* img);
 
 #ifdef __cplusplus
 }

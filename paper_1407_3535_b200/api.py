@@ -75,6 +75,9 @@ class Image:
     def is_integer(self) -> bool:
         return bool(N.lib().tm_image_is_integer(self.h))
 
+    def reset_cache(self):
+        N.check(N.lib().tm_image_reset_cache(self.h))
+
     def upload_u8(self, pixels):
         a = np.ascontiguousarray(pixels, dtype=np.uint8)
         N.check(N.lib().tm_image_upload_u8(self.ctx.h, self.h, _u8ptr(a)))
@@ -164,6 +167,19 @@ class Context:
     @property
     def launches(self) -> int:
         return int(N.lib().tm_ctx_launch_count(self.h))
+
+    @property
+    def stream_ptr(self) -> int:
+        return int(N.lib().tm_ctx_stream(self.h) or 0)
+
+    def set_profiling(self, enable=True):
+        N.check(N.lib().tm_ctx_set_profiling(self.h, int(bool(enable))))
+
+    def phase_times(self) -> dict:
+        import json
+        buf = C.create_string_buffer(1 << 16)
+        N.check(N.lib().tm_ctx_phase_times(self.h, buf, len(buf)))
+        return {k: {"count": v[0], "ms": v[1]} for k, v in json.loads(buf.value.decode()).items()}
 
     def synchronize(self):
         N.check(N.lib().tm_ctx_synchronize(self.h))

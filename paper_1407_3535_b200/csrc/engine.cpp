@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <chrono>
 #include <climits>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <map>
@@ -47,10 +48,15 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr double kEps = 2.220446049250313e-16;
 
+// Stream the current API call runs on (set by guard()); device buffers are allocated and
+// freed stream-ordered from the device's memory pool, so buffer churn never synchronises.
+thread_local cudaStream_t g_stream = nullptr;
+
 template <class T>
 struct DBuf {
     T* p = nullptr;
     size_t cap = 0;
+    cudaStream_t s = nullptr;
     DBuf() = default;
     DBuf(const DBuf&) = delete;
     DBuf& operator=(const DBuf&) = delete;
@@ -58,17 +64,47 @@ struct DBuf {
     void ensure(size_t n) {
         if (n <= cap && p) return;
         release();
-        CK(cudaMalloc(&p, std::max<size_t>(n, 1) * sizeof(T)));
+        s = g_stream;
+        CK(cudaMallocAsync(reinterpret_cast<void**>(&p), std::max<size_t>(n, 1) * sizeof(T), s));
         cap = std::max<size_t>(n, 1);
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) cudaFreeAsync(p, s);
         p = nullptr;
         cap = 0;
     }
     void swap(DBuf& o) {
         std::swap(p, o.p);
         std::swap(cap, o.cap);
+        std::swap(s, o.s);
+    }
+};
+
+// Pinned host staging for small uploads (templates, row lists): a copy from it is truly
+// asynchronous; the event guards reuse of the buffer.
+struct Pinned {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaEvent_t done = nullptr;
+    ~Pinned() {
+        if (p) cudaFreeHost(p);
+        if (done) cudaEventDestroy(done);
+    }
+    void* get(size_t n) {
+        if (!done) CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+        CK(cudaEventSynchronize(done));  // previous copy out of this buffer finished
+        if (n > cap) {
+            if (p) cudaFreeHost(p);
+            CK(cudaMallocHost(&p, n));
+            cap = n;
+        }
+        return p;
+    }
+    void upload(void* dst, const void* src, size_t n, cudaStream_t st) {
+        void* h = get(n);
+        std::memcpy(h, src, n);
+        CK(cudaMemcpyAsync(dst, h, n, cudaMemcpyHostToDevice, st));
+        CK(cudaEventRecord(done, st));
     }
 };
 
@@ -146,8 +182,60 @@ struct tm_ctx {
     DBuf<double> td;
     DBuf<int> rows_list;
     DBuf<double> map_tmp, map_user;
-    unsigned long long* h_pinned = nullptr;  // small pinned staging
+    DBuf<double> egs_maps[3];
+    Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt;
     void add(int k) { launches += k; }
+    // optional per-phase device timing (CUDA events on the context stream)
+    bool profiling = false;
+    struct Mark {
+        const char* name;
+        cudaEvent_t a, b;
+    };
+    std::vector<Mark> pending;
+    std::vector<cudaEvent_t> pool;
+    std::map<std::string, std::pair<long long, double>> phase_ms;  // name -> (count, ms)
+    cudaEvent_t get_event() {
+        if (!pool.empty()) {
+            cudaEvent_t e = pool.back();
+            pool.pop_back();
+            return e;
+        }
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        return e;
+    }
+    void resolve() {  // call after a stream synchronisation
+        for (auto& mk : pending) {
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, mk.a, mk.b);
+            auto& slot = phase_ms[mk.name];
+            slot.first += 1;
+            slot.second += ms;
+            pool.push_back(mk.a);
+            pool.push_back(mk.b);
+        }
+        pending.clear();
+    }
+};
+
+// RAII phase timer: brackets the launches issued in its scope with two events.
+struct Phase {
+    tm_ctx* ctx;
+    const char* name;
+    cudaEvent_t a = nullptr;
+    Phase(tm_ctx* c, const char* n) : ctx(c), name(n) {
+        if (ctx->profiling) {
+            a = ctx->get_event();
+            cudaEventRecord(a, ctx->s);
+        }
+    }
+    ~Phase() {
+        if (ctx->profiling) {
+            cudaEvent_t b = ctx->get_event();
+            cudaEventRecord(b, ctx->s);
+            ctx->pending.push_back(tm_ctx::Mark{name, a, b});
+        }
+    }
 };
 
 struct tm_image {
@@ -159,8 +247,9 @@ struct tm_image {
     int pitch = 0;
     DBuf<double> f64;
     bool have_f64 = false;
-    bool have_qtotal = false;
-    double q_total = 0.0;
+    bool have_qtotal = false;  // prefix_noise computed on the device
+    DBuf<double> pn;           // [0] q_total (FP64 path) / [1] prefix_noise
+    DBuf<unsigned long long> qt;
     std::map<std::pair<int, int>, std::unique_ptr<WS>> ws_cache;
 };
 
@@ -178,8 +267,13 @@ struct tm_prep {
     tm_egs_iter cost{};
     std::vector<tm_egs_iter> egs_trace;
     std::vector<tm_opta_iter> opta_trace;
-    double prep_ms = 0.0;
+    double prep_ms = -1.0;
+    cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     tm_image* source = nullptr;  // not owned
+    ~tm_prep() {
+        if (ev0) cudaEventDestroy(ev0);
+        if (ev1) cudaEventDestroy(ev1);
+    }
 };
 
 namespace {
@@ -236,26 +330,20 @@ void classify_device_image(tm_ctx* ctx, tm_image* img) {
     }
 }
 
-double image_q_total(tm_ctx* ctx, tm_image* img) {
-    if (img->have_qtotal) return img->q_total;
-    const size_t N = size_t(img->p) * img->q;
-    if (img->integer) {
-        CK(tmk::sum_sq_u8(img->u8.p, N, ctx->counters.p + 1, ctx->s));
-        unsigned long long v = 0;
-        CK(cudaMemcpyAsync(&v, ctx->counters.p + 1, 8, cudaMemcpyDeviceToHost, ctx->s));
-        CK(cudaStreamSynchronize(ctx->s));
-        img->q_total = double(v);  // exact: the reference's sequential sum of integers
-    } else {
-        double* d = reinterpret_cast<double*>(ctx->counters.p + 1);
-        CK(tmk::sum_sq_f64(img->f64.p, N, d, ctx->s));
-        double v = 0;
-        CK(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, ctx->s));
-        CK(cudaStreamSynchronize(ctx->s));
-        img->q_total = v;
+// prefix_noise (stats.cpp:78-81) on the device; returns a device pointer.
+const double* image_prefix_noise(tm_ctx* ctx, tm_image* img) {
+    if (!img->have_qtotal) {
+        img->pn.ensure(2);
+        if (img->integer) {
+            img->qt.ensure(1);
+            CK(tmk::prefix_noise_u8(img->u8.p, img->p, img->q, img->qt.p, img->pn.p + 1, ctx->s));
+        } else {
+            CK(tmk::prefix_noise_f64(img->f64.p, img->p, img->q, img->pn.p, img->pn.p + 1, ctx->s));
+        }
+        ctx->add(2);
+        img->have_qtotal = true;
     }
-    ctx->add(1);
-    img->have_qtotal = true;
-    return img->q_total;
+    return img->pn.p + 1;
 }
 
 // Replica prefix over a product source; the full window-sum table lands in `out`.
@@ -280,7 +368,8 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
     ws.ec = ec;
     ws.m = m;
     ws.n = n;
-    const double prefix_noise = double(p + q) * kEps * image_q_total(ctx, img);
+    const double* prefix_noise = image_prefix_noise(ctx, img);
+    Phase ph(ctx, "window_stats");
     if (img->integer) {
         ctx->hs.ensure(size_t(p) * ec);
         ctx->hq.ensure(size_t(p) * ec);
@@ -344,9 +433,8 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n) {
         for (int j = 0; j < n; ++j) tf[size_t(i) * T.npad + j] = float(t[size_t(i) * n + j]);
     ctx->tf.ensure(tf.size());
     ctx->td.ensure(size_t(m) * n);
-    CK(cudaMemcpyAsync(ctx->tf.p, tf.data(), tf.size() * 4, cudaMemcpyHostToDevice, ctx->s));
-    CK(cudaMemcpyAsync(ctx->td.p, t, size_t(m) * n * 8, cudaMemcpyHostToDevice, ctx->s));
-    CK(cudaStreamSynchronize(ctx->s));  // host vectors go out of scope
+    ctx->pin_tf.upload(ctx->tf.p, tf.data(), tf.size() * 4, ctx->s);
+    ctx->pin_td.upload(ctx->td.p, t, size_t(m) * n * 8, ctx->s);
     return T;
 }
 
@@ -391,9 +479,7 @@ int row_span(const std::vector<int>& rows) {
 
 void upload_rows(tm_ctx* ctx, const std::vector<int>& rows) {
     ctx->rows_list.ensure(rows.size());
-    CK(cudaMemcpyAsync(ctx->rows_list.p, rows.data(), rows.size() * 4, cudaMemcpyHostToDevice,
-                       ctx->s));
-    CK(cudaStreamSynchronize(ctx->s));
+    ctx->pin_rows.upload(ctx->rows_list.p, rows.data(), rows.size() * 4, ctx->s);
 }
 
 constexpr int kListBlocks = 148 * 4;
@@ -416,6 +502,7 @@ void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const in
                uint8_t* out_deg, int slot) {
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     ctx->partials.ensure(kListBlocks);
+    Phase ph(ctx, slot == 1 ? "seed_eval" : (slot == 2 ? "survivor_eval" : "list_eval"));
     if (fp32_path(img, T))
         CK(tmk::corr_list(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
                           kListBlocks, ctx->s));
@@ -434,6 +521,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     ctx->deg_c.ensure(G);
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     const int wr = g.w / 2;
+    Phase ph(ctx, "centre_scan");
     if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
         std::vector<int> rows(g.tr);
         for (int ti = 0; ti < g.tr; ++ti) rows[ti] = centre_row_h(g, ti);
@@ -461,12 +549,23 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             ctx->add(1);
         }
         if (clipped) {
-            t.cbase = centre_col_h(g, g.tc - 1);
-            t.sw = 1;
-            t.nc = 1;
-            t.col0 = g.tc - 1;
-            CK(tmk::corr_band(job, t, ctx->partials.p + n1, &n2, ctx->s));
-            ctx->add(1);
+            // the clipped last group column: one centre per group row, list kernel
+            std::vector<int2> last(g.tr);
+            const int cc = centre_col_h(g, g.tc - 1);
+            for (int ti = 0; ti < g.tr; ++ti) last[ti] = make_int2(rows[ti], cc);
+            ctx->seed_locs.ensure(size_t(g.tr));
+            ctx->pin_locs.upload(ctx->seed_locs.p, last.data(), last.size() * sizeof(int2), ctx->s);
+            const unsigned long long cnt = g.tr;
+            ctx->pin_cnt.upload(ctx->counters.p + 12, &cnt, 8, ctx->s);
+            ctx->seq_rho.ensure(size_t(g.tr));
+            ctx->seq_deg.ensure(size_t(g.tr));
+            n2 = std::min(kListBlocks, (g.tr + 7) / 8);
+            ctx->partials.ensure(size_t(n1 + n2) + 1);
+            CK(tmk::corr_list(job, ctx->seed_locs.p, ctx->counters.p + 12, g.tr, ctx->seq_rho.p,
+                              ctx->seq_deg.p, ctx->partials.p + n1, n2, ctx->s));
+            CK(tmk::scatter_column(ctx->seq_rho.p, ctx->seq_deg.p, g.tr, g.tc, g.tc - 1,
+                                   ctx->rho_c.p, ctx->deg_c.p, ctx->s));
+            ctx->add(2);
         }
         reduce_to(ctx, n1 + n2, 0);
         return;
@@ -477,8 +576,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         for (int tj = 0; tj < g.tc; ++tj)
             locs[size_t(ti) * g.tc + tj] = make_int2(centre_row_h(g, ti), centre_col_h(g, tj));
     ctx->seed_locs.ensure(G);
-    CK(cudaMemcpyAsync(ctx->seed_locs.p, locs.data(), G * sizeof(int2), cudaMemcpyHostToDevice,
-                       ctx->s));
+    ctx->pin_locs.upload(ctx->seed_locs.p, locs.data(), G * sizeof(int2), ctx->s);
     unsigned long long cnt = G;
     CK(cudaMemcpyAsync(ctx->counters.p + 4, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
@@ -487,35 +585,42 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 }
 
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
-long long autocorr_map(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
-                       double thr, double* map) {
+// Launch the R_co map + retained count for one group size; n_r lands in *nr (device).
+void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
+                     double thr, double* map, unsigned long long* nr) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
-    unsigned long long* nr = ctx->counters.p + 2;
     CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
+    Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
     if (img->integer) {
         CK(tmk::autocorr_u8(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
         ctx->add(1);
-    } else {
-        CK(tmk::autocorr_init(map, g, ctx->s));
-        ctx->add(1);
-        const int hr = g.h / 2, wr = g.w / 2;
-        for (int di = -hr; di <= hr; ++di)
-            for (int dj = -wr; dj <= wr; ++dj) {
-                if (di == 0 && dj == 0) continue;
-                const int orr = std::max(0, -di), occ = std::max(0, -dj);
-                const int ph = p - std::abs(di), pw = q - std::abs(dj);
-                if (ph < m || pw < n) continue;
-                ctx->rowacc.ensure(size_t(ph) * pw);
-                ctx->prefix.ensure(size_t(ph + 1) * (pw + 1));
-                tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0};
-                CK(tmk::replica_prefix(src, ph, pw, ctx->rowacc.p, ctx->prefix.p, ctx->s));
-                CK(tmk::autocorr_offset_epilogue(ctx->prefix.p, ph, pw, m, n, g, ws.dev(), di, dj,
-                                                 map, ctx->s));
-                ctx->add(3);
-            }
-        CK(tmk::retained_count(map, g, thr, nr, ctx->s));
-        ctx->add(1);
+        return;
     }
+    CK(tmk::autocorr_init(map, g, ctx->s));
+    ctx->add(1);
+    const int hr = g.h / 2, wr = g.w / 2;
+    for (int di = -hr; di <= hr; ++di)
+        for (int dj = -wr; dj <= wr; ++dj) {
+            if (di == 0 && dj == 0) continue;
+            const int orr = std::max(0, -di), occ = std::max(0, -dj);
+            const int ph_ = p - std::abs(di), pw = q - std::abs(dj);
+            if (ph_ < m || pw < n) continue;
+            ctx->rowacc.ensure(size_t(ph_) * pw);
+            ctx->prefix.ensure(size_t(ph_ + 1) * (pw + 1));
+            tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0};
+            CK(tmk::replica_prefix(src, ph_, pw, ctx->rowacc.p, ctx->prefix.p, ctx->s));
+            CK(tmk::autocorr_offset_epilogue(ctx->prefix.p, ph_, pw, m, n, g, ws.dev(), di, dj,
+                                             map, ctx->s));
+            ctx->add(3);
+        }
+    CK(tmk::retained_count(map, g, thr, nr, ctx->s));
+    ctx->add(1);
+}
+
+long long autocorr_map(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
+                       double thr, double* map) {
+    unsigned long long* nr = ctx->counters.p + 2;
+    autocorr_launch(ctx, img, ws, g, thr, map, nr);
     unsigned long long v = 0;
     CK(cudaMemcpyAsync(&v, nr, 8, cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
@@ -557,27 +662,54 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     if (cap % 2 == 0) ++cap;
     const size_t E = size_t(er) * ec;
     best.ensure(E);
-    ctx->map_tmp.ensure(E);
     EgsOut out;
     double prev_cost = std::numeric_limits<double>::infinity();
     int h = h0, w = w0;
-    for (;;) {
-        const tmk::GridDesc g = make_grid(er, ec, h, w);
-        const long long n_r = autocorr_map(ctx, img, ws, g, thr, ctx->map_tmp.p);
-        const tm_egs_iter cost = total_cost_h(er, ec, h, w, n_r, 0.0);
-        const bool accepted =
-            !std::isfinite(prev_cost) || prev_cost - cost.total > xi * prev_cost;
-        if (!accepted) break;
-        out.h = h;
-        out.w = w;
-        out.cost = cost;
-        out.trace.push_back(cost);
-        best.swap(ctx->map_tmp);
-        ctx->map_tmp.ensure(E);
-        prev_cost = cost.total;
-        if ((h >= er && w >= ec) || (h >= cap && w >= cap)) break;
-        h = std::min(h + 2, cap);
-        w = std::min(w + 2, cap);
+    bool done = false;
+    // Candidates are launched in batches of up to three group sizes and decided after one
+    // readback; the accept/stop sequence is exactly egs.cpp:61-88 (a candidate after the
+    // first rejection is computed but ignored).
+    while (!done) {
+        struct Cand {
+            int h, w;
+        } cand[3];
+        int nc = 0;
+        int hh = h, ww = w;
+        for (; nc < 3;) {
+            cand[nc++] = Cand{hh, ww};
+            if ((hh >= er && ww >= ec) || (hh >= cap && ww >= cap)) break;
+            hh = std::min(hh + 2, cap);
+            ww = std::min(ww + 2, cap);
+        }
+        for (int k = 0; k < nc; ++k) {
+            const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
+            ctx->egs_maps[k].ensure(E);
+            autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p, ctx->counters.p + 8 + k);
+        }
+        unsigned long long nr[3] = {0, 0, 0};
+        CK(cudaMemcpyAsync(nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        for (int k = 0; k < nc; ++k) {
+            const tm_egs_iter cost = total_cost_h(er, ec, cand[k].h, cand[k].w, (long long)nr[k], 0.0);
+            const bool accepted =
+                !std::isfinite(prev_cost) || prev_cost - cost.total > xi * prev_cost;
+            if (!accepted) {
+                done = true;
+                break;
+            }
+            out.h = cand[k].h;
+            out.w = cand[k].w;
+            out.cost = cost;
+            out.trace.push_back(cost);
+            best.swap(ctx->egs_maps[k]);
+            prev_cost = cost.total;
+            if ((cand[k].h >= er && cand[k].w >= ec) || (cand[k].h >= cap && cand[k].w >= cap)) {
+                done = true;
+                break;
+            }
+            h = std::min(cand[k].h + 2, cap);
+            w = std::min(cand[k].w + 2, cap);
+        }
     }
     return out;
 }
@@ -753,13 +885,13 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     int policy = P.policy;
     if (policy == TM_POLICY_REFERENCE)
         policy = (P.parallel && P.threads > 1 && G > 1) ? TM_POLICY_FROZEN : TM_POLICY_SEQUENTIAL;
+    const bool seq = policy == TM_POLICY_SEQUENTIAL;
 
+    // ---- scan 1 + threshold bootstrap (matcher.cpp:116-125) ---------------------------
     centre_scan(ctx, img, ws, T, g);
     CK(tmk::threshold_init(ctx->cells.p + 0, P.has_init_threshold, P.init_threshold,
                            ctx->thr.p, s));
     ctx->add(1);
-    double T0 = 0.0;
-    CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
 
     const uint8_t* seeded = nullptr;
     if (policy == TM_POLICY_SEEDED) {
@@ -779,36 +911,83 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         seeded = ctx->seeded.p;
     }
 
-    uint8_t* visits = nullptr;
-    if (visits_host) {
-        ctx->visits.ensure(E);
-        visits = ctx->visits.p;
-    }
+    // ---- scan 2: bound test + survivor compaction -------------------------------------
+    ctx->visits.ensure(E);
+    uint8_t* visits = ctx->visits.p;
     ctx->locs.ensure(E);
     CK(cudaMemsetAsync(ctx->tally.p, 0, sizeof(tmk::Tally), s));
-    CK(tmk::sec_compact(g, in.map, ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, ctx->thr.p,
-                        seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
-    ctx->add(1);
+    {
+        Phase ph(ctx, "sec_compact");
+        CK(tmk::sec_compact(g, in.map, ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
+                            ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
+        ctx->add(1);
+    }
+    double T0 = 0.0;
+    tmk::Tally tally{};
+    CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
     const unsigned long long* count = &ctx->tally.p->survivors;
-    const bool seq = policy == TM_POLICY_SEQUENTIAL;
+    double* rho_loc = nullptr;
     if (seq) {
         ctx->seq_rho.ensure(E);
-        ctx->seq_deg.ensure(E);
+        rho_loc = ctx->seq_rho.p;
     }
-    eval_list(ctx, img, ws, T, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
-              seq ? ctx->seq_rho.p : nullptr, seq ? ctx->seq_deg.p : nullptr, 2);
+    // Dense survivors: evaluate whole tiles masked by the visit map (band kernel);
+    // sparse survivors: one warp per listed location.
+    const bool dense = tally.survivors * 16 > E && fp32_path(img, T);
+    if (dense) {
+        const tmk::CorrJob job = make_job(ctx, img, ws, T);
+        std::vector<int> rows(g.er);
+        for (int r = 0; r < g.er; ++r) rows[r] = r;
+        upload_rows(ctx, rows);
+        tmk::BandTask t{};
+        t.rows = ctx->rows_list.p;
+        t.nrows = g.er;
+        t.cbase = 0;
+        t.sw = 1;
+        t.nc = g.ec;
+        t.mode = 2;
+        t.row_span = 7;
+        t.out_rho = rho_loc;
+        t.mask = visits;
+        ctx->partials.ensure(size_t(band_partials(g.er, g.ec, 1)));
+        int np = 0;
+        {
+            Phase ph(ctx, "survivor_dense");
+            CK(tmk::corr_band(job, t, ctx->partials.p, &np, s));
+            ctx->add(1);
+        }
+        reduce_to(ctx, np, 2);
+    } else if (tally.survivors > 0) {
+        const tmk::CorrJob job = make_job(ctx, img, ws, T);
+        ctx->partials.ensure(kListBlocks);
+        {
+            Phase ph(ctx, "survivor_eval");
+            if (fp32_path(img, T))
+                CK(tmk::corr_list(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
+                                  rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
+            else
+                CK(tmk::corr_list_f64(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
+                                      rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
+            ctx->add(1);
+        }
+        reduce_to(ctx, kListBlocks, 2);
+    } else {
+        reduce_to(ctx, 0, 2);
+    }
 
     double final_T = T0;
-    tmk::Tally tally{};
     if (seq) {
-        // Replay the running threshold: records in scan order (see k_first_record).
+        // Replay the running threshold (matcher.cpp:73-74): records in scan order.
+        Phase ph(ctx, "sequential_replay");
         std::vector<unsigned long long> rk;
         std::vector<double> rt;
         double Tcur = T0;
         unsigned long long after = ~0ull;
         for (;;) {
-            CK(tmk::first_record(g, ctx->locs.p, count, ctx->seq_rho.p, ctx->seq_deg.p, in.map,
-                                 ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, Tcur, after,
+            CK(tmk::first_record(g, ctx->locs.p, count, rho_loc, in.map, ctx->rho_c.p,
+                                 ctx->deg_c.p, ws.fl.p, T.ts.flat, Tcur, after,
                                  ctx->counters.p + 6, s));
             ctx->add(1);
             unsigned long long key = 0;
@@ -816,8 +995,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
             CK(cudaStreamSynchronize(s));
             if (key == ~0ull) break;
             double rho = 0.0;
-            CK(tmk::fetch_record_rho(g, ctx->locs.p, count, ctx->seq_rho.p, key,
-                                     ctx->thr.p + 1, s));
+            CK(tmk::fetch_record_rho(g, ctx->locs.p, count, rho_loc, key, ctx->thr.p + 1, s));
             ctx->add(1);
             CK(cudaMemcpyAsync(&rho, ctx->thr.p + 1, 8, cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -833,10 +1011,9 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
             CK(cudaMemcpyAsync(ctx->rec_T.p, rt.data(), rt.size() * 8, cudaMemcpyHostToDevice, s));
         }
         ctx->partials.ensure(kListBlocks);
-        CK(tmk::seq_final(g, ctx->locs.p, count, ctx->seq_rho.p, ctx->seq_deg.p, in.map,
-                          ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat, T0, ctx->rec_key.p,
-                          ctx->rec_T.p, int(rk.size()), ctx->tally.p, visits, ctx->partials.p,
-                          kListBlocks, s));
+        CK(tmk::seq_final(g, ctx->locs.p, count, rho_loc, in.map, ctx->rho_c.p, ctx->deg_c.p,
+                          ws.fl.p, T.ts.flat, T0, ctx->rec_key.p, ctx->rec_T.p, int(rk.size()),
+                          ctx->tally.p, visits, ctx->partials.p, kListBlocks, s));
         ctx->add(1);
         reduce_to(ctx, kListBlocks, 2);
         final_T = Tcur;
@@ -853,14 +1030,12 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     if (policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
     if (better_h(cells[2], best)) best = cells[2];
 
-    long long eliminated = (long long)tally.eliminated;
-    long long retained = (long long)tally.retained;
-    if (seq) retained = (long long)tally.pad;  // alive candidates; dead ones were added
-                                                // to eliminated by seq_final
+    const long long eliminated = (long long)tally.eliminated;
+    // sequential: alive candidates (dead ones were moved to `eliminated` by seq_final)
+    const long long retained = seq ? (long long)tally.pad : (long long)tally.retained;
     if (policy == TM_POLICY_SEEDED) {
         final_T = thr_after;
-        if (better_h(cells[2], cells[1]) && (cells[2].flags & 1) && !(cells[2].flags & 2))
-            final_T = std::max(final_T, cells[2].rho);
+        if ((cells[2].flags & 1) && !(cells[2].flags & 2)) final_T = std::max(final_T, cells[2].rho);
     }
     tm_match_result r{};
     r.mode = TM_MODE_EGS;
@@ -891,8 +1066,7 @@ tmk::CellH refine(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, int l
         for (int c = c0; c <= c1; ++c) locs.push_back(make_int2(r, c));
     *ops += (long long)locs.size();
     ctx->seed_locs.ensure(locs.size());
-    CK(cudaMemcpyAsync(ctx->seed_locs.p, locs.data(), locs.size() * sizeof(int2),
-                       cudaMemcpyHostToDevice, ctx->s));
+    ctx->pin_locs.upload(ctx->seed_locs.p, locs.data(), locs.size() * sizeof(int2), ctx->s);
     unsigned long long cnt = locs.size();
     CK(cudaMemcpyAsync(ctx->counters.p + 7, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
     eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 7, int(locs.size()), nullptr,
@@ -917,6 +1091,7 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
         surface = ctx->surface.p;
     }
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
+    Phase ph(ctx, "brute_dense");
     if (fp32_path(img, T)) {
         std::vector<int> rows(er);
         for (int r = 0; r < er; ++r) rows[r] = r;
@@ -976,7 +1151,9 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     prep->source = img;
     prep->mode = P.mode == TM_MODE_OPTA ? TM_MODE_OPTA : TM_MODE_EGS;
     if (m > img->p || n > img->q) invalid("match: template larger than search image");
-    CK(cudaEventRecord(ctx->ev0, ctx->s));
+    CK(cudaEventCreate(&prep->ev0));
+    CK(cudaEventCreate(&prep->ev1));
+    CK(cudaEventRecord(prep->ev0, ctx->s));
     if (prep->mode == TM_MODE_EGS) {
         WS& ws = get_ws(ctx, img, m, n);
         EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
@@ -988,9 +1165,7 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     } else {
         run_opta_prep(ctx, img, prep.get());
     }
-    CK(cudaEventRecord(ctx->ev1, ctx->s));
-    CK(cudaEventSynchronize(ctx->ev1));
-    prep->prep_ms = ms_between(ctx->ev0, ctx->ev1);
+    CK(cudaEventRecord(prep->ev1, ctx->s));
     prep->g = make_grid(img->p - m + 1, img->q - n + 1, prep->h, prep->w);
     return prep.release();
 }
@@ -1025,7 +1200,12 @@ int guard(tm_ctx* ctx, F&& f) {
         if (ctx) {
             std::lock_guard<std::mutex> lk(ctx->mu);
             CK(cudaSetDevice(ctx->device));
+            g_stream = ctx->s;
             f();
+            if (ctx->profiling) {
+                CK(cudaStreamSynchronize(ctx->s));
+                ctx->resolve();
+            }
         } else {
             f();
         }
@@ -1081,9 +1261,14 @@ int tm_ctx_create(int device, tm_ctx** out) {
         ctx->device = device;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
+        cudaMemPool_t pool;
+        CK(cudaDeviceGetDefaultMemPool(&pool, device));
+        uint64_t keep = UINT64_MAX;  // keep freed blocks cached in the pool
+        CK(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
+        g_stream = ctx->s;
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
-        ctx->counters.ensure(16);
+        ctx->counters.ensure(32);
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
         ctx->tally.ensure(1);
@@ -1094,11 +1279,15 @@ int tm_ctx_create(int device, tm_ctx** out) {
 void tm_ctx_destroy(tm_ctx* ctx) {
     if (!ctx) return;
     cudaSetDevice(ctx->device);
-    cudaStreamSynchronize(ctx->s);
+    cudaStream_t st = ctx->s;
+    cudaStreamSynchronize(st);
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
-    cudaStreamDestroy(ctx->s);
-    delete ctx;
+    for (auto& kv : ctx->phase_ms) (void)kv;
+    for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
+    delete ctx;  // stream-ordered frees of the scratch buffers
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
 }
 
 int tm_ctx_synchronize(tm_ctx* ctx) {
@@ -1106,6 +1295,41 @@ int tm_ctx_synchronize(tm_ctx* ctx) {
 }
 
 int64_t tm_ctx_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+void* tm_ctx_stream(tm_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->s) : nullptr; }
+
+int tm_ctx_set_profiling(tm_ctx* ctx, int enable) {
+    return guard(ctx, [&] {
+        ctx->profiling = enable != 0;
+        ctx->phase_ms.clear();
+    });
+}
+
+int tm_ctx_phase_times(tm_ctx* ctx, char* buf, size_t len) {
+    return guard(ctx, [&] {
+        std::string js = "{";
+        bool first = true;
+        for (auto& kv : ctx->phase_ms) {
+            char item[160];
+            std::snprintf(item, sizeof item, "%s\"%s\": [%lld, %.6f]", first ? "" : ", ",
+                          kv.first.c_str(), kv.second.first, kv.second.second);
+            js += item;
+            first = false;
+        }
+        js += "}";
+        if (js.size() + 1 > len) invalid("tm_ctx_phase_times: buffer too small");
+        std::memcpy(buf, js.c_str(), js.size() + 1);
+    });
+}
+
+int tm_image_reset_cache(tm_image* img) {
+    if (!img) return TM_EINVAL;
+    tm_ctx* ctx = img->ctx;
+    return guard(ctx, [&] {
+        img->ws_cache.clear();
+        img->have_qtotal = false;
+    });
+}
 
 int tm_image_create(tm_ctx* ctx, const double* pixels, int rows, int cols, tm_image** out) {
     return guard(ctx, [&] {
@@ -1334,6 +1558,10 @@ int tm_prep_get_info(const tm_prep* prep, tm_prep_info* info) {
         info->opta_trace_len = int(prep->opta_trace.size());
         for (size_t k = 0; k < prep->opta_trace.size() && k < TM_MAX_TRACE + 1; ++k)
             info->opta_trace[k] = prep->opta_trace[k];
+        if (prep->prep_ms < 0 && prep->ev1) {
+            cudaEventSynchronize(prep->ev1);
+            const_cast<tm_prep*>(prep)->prep_ms = ms_between(prep->ev0, prep->ev1);
+        }
         info->prep_ms = prep->prep_ms;
     });
 }
@@ -1475,3 +1703,5 @@ int tm_match(tm_ctx* ctx, const double* tmpl, int m, int n, const double* image,
 }
 
 }  // extern "C"
+static_assert(sizeof(tm_match_result) == 112, "tm_match_result layout is part of the ABI");
+static_assert(sizeof(tm_egs_iter) == 48, "tm_egs_iter layout is part of the ABI");

@@ -35,6 +35,7 @@ struct ACParams {
     int nx_max;     // H rows per tile
     int spitch;     // staged image pitch (bytes)
     int srows;
+    int noff_per;   // offsets handled per CTA (blockIdx.z selects the slice)
 };
 
 __device__ __forceinline__ int ccol(const Grid& g, int tj) { return g.center_col(tj); }
@@ -76,9 +77,13 @@ __global__ void k_autocorr_u8(ACParams P) {
     const double mn = double(P.m) * double(P.n);
     unsigned long long local_nr = 0;
 
-    for (int di = -hr; di <= hr; ++di) {
-        for (int dj = -wr; dj <= wr; ++dj) {
-            if (di == 0 && dj == 0) continue;
+    // offsets in raster order, centre (0,0) skipped; this CTA takes a contiguous slice
+    const int noff = g.h * g.w - 1;
+    const int o0 = blockIdx.z * P.noff_per, o1 = min(noff, o0 + P.noff_per);
+    for (int oi = o0; oi < o1; ++oi) {
+        {
+            const int ro = oi < (noff / 2) ? oi : oi + 1;  // skip the centre slot
+            const int di = ro / g.w - hr, dj = ro % g.w - wr;
             // ---- row pass: H[xi][tj] = sum_b I(x, cc+b) * I(x+di, cc+dj+b) ----------
             for (int item = threadIdx.x; item < nx * nch; item += blockDim.x) {
                 const int xi = item / nch, ch = item % nch;
@@ -139,7 +144,7 @@ __global__ void k_autocorr_u8(ACParams P) {
         }
     }
     // centres carry exactly 1 (autocorr.cpp:92-93)
-    for (int idx = threadIdx.x; idx < nti * ntj; idx += blockDim.x) {
+    for (int idx = threadIdx.x; blockIdx.z == 0 && idx < nti * ntj; idx += blockDim.x) {
         const int i = idx / ntj, k = idx % ntj;
         P.map[size_t(scr[i]) * g.ec + scc[k]] = 1.0;
     }
@@ -229,7 +234,9 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
     for (;;) {
         const int srows = (gtr - 1) * gd.h + 2 * hr + m + 1;
         const int scols = (gtc - 1) * gd.w + 2 * wr + n + 1;
-        const int spitch = (scols + 15) & ~15;
+        // bytes per staged row = 4 mod 8: lanes on consecutive rows hit distinct banks
+        int spitch = (scols + 3) & ~3;
+        if (((spitch / 4) & 1) == 0) spitch += 4;
         const int nx = (gtr - 1) * gd.h + m + 1;
         bytes = ((size_t(srows) * spitch + 15) & ~size_t(15)) + size_t(nx) * gtc * 4 +
                 size_t(gtc + gtr) * 4;
@@ -248,7 +255,12 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
         cudaFuncSetAttribute(k_autocorr_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    dim3 grid((gd.tc + gtc - 1) / gtc, (gd.tr + gtr - 1) / gtr);
+    const int base = ((gd.tc + gtc - 1) / gtc) * ((gd.tr + gtr - 1) / gtr);
+    const int noff = gd.h * gd.w - 1;
+    int splits = std::max(1, std::min(noff, (148 * 6 + base - 1) / base));
+    P.noff_per = (noff + splits - 1) / splits;
+    splits = (noff + P.noff_per - 1) / P.noff_per;
+    dim3 grid((gd.tc + gtc - 1) / gtc, (gd.tr + gtr - 1) / gtr, std::max(splits, 1));
     k_autocorr_u8<<<grid, 256, bytes, s>>>(P);
     return cudaGetLastError();
 }

@@ -175,7 +175,7 @@ __global__ void __launch_bounds__(NW * 32)
 __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                int lane_flush) {
+                int lane_flush, int rho_by_loc) {
     __shared__ Cell scratch[8];
     const int lane = threadIdx.x & 31;
     const long long nloc = min((long long)*count, (long long)max_count);
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(256)
             const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
             const bool wflat = job.st.flat[kk];
             const double rho = zncc_epilogue(dacc, ts, job.st.mu[kk], job.st.omega[kk], wflat);
-            if (out_rho) out_rho[li] = rho;
+            if (out_rho) out_rho[rho_by_loc ? kk : li] = rho;
             if (out_deg) out_deg[li] = ts.flat || wflat;
             const Cell cand = make_cell(rc.x, rc.y, rho, ts.flat || wflat);
             if (better(cand, best)) best = cand;
@@ -225,7 +225,8 @@ __device__ __forceinline__ double dot_f64(const CorrJob& job, int r, int c) {
 
 __global__ void __launch_bounds__(256)
     k_list_f64(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
-               int max_count, double* out_rho, uint8_t* out_deg, CellH* partials) {
+               int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
+               int rho_by_loc) {
     __shared__ Cell scratch[8];
     const long long nloc = min((long long)*count, (long long)max_count);
     const TStats ts = to_ts(job.ts);
@@ -239,7 +240,7 @@ __global__ void __launch_bounds__(256)
                                ? 0.0
                                : zncc_epilogue(dot_f64(job, rc.x, rc.y), ts, job.st.mu[kk],
                                                job.st.omega[kk], wflat);
-        if (out_rho) out_rho[li] = rho;
+        if (out_rho) out_rho[rho_by_loc ? kk : li] = rho;
         if (out_deg) out_deg[li] = ts.flat || wflat;
         const Cell cand = make_cell(rc.x, rc.y, rho, ts.flat || wflat);
         if (better(cand, best)) best = cand;
@@ -430,7 +431,7 @@ __device__ __forceinline__ bool alive_at(const Grid& g, int r, int c, double T,
 // First (in scan order, key > after) candidate that is alive at T and sets a new record.
 __global__ void k_first_record(Grid g, const int2* __restrict__ locs,
                                const unsigned long long* count, const double* __restrict__ rho,
-                               const uint8_t* __restrict__ deg, const double* map,
+                               const double* map,
                                const double* rho_c, const uint8_t* deg_c, const uint8_t* flat,
                                int tflat, double T, unsigned long long after,
                                unsigned long long* best_key) {
@@ -438,8 +439,9 @@ __global__ void k_first_record(Grid g, const int2* __restrict__ locs,
     unsigned long long mine = ~0ull;
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
-        if (deg[i] || !(rho[i] > T)) continue;
         const int2 rc = locs[i];
+        const size_t kk = size_t(rc.x) * g.ec + rc.y;
+        if (tflat || flat[kk] || !(rho[kk] > T)) continue;
         const unsigned long long key = scan_key(g, rc.x, rc.y);
         if ((after != ~0ull && key <= after) || key >= mine) continue;
         if (alive_at(g, rc.x, rc.y, T, map, rho_c, deg_c, flat, tflat)) mine = key;
@@ -455,14 +457,13 @@ __global__ void k_fetch_rho(Grid g, const int2* __restrict__ locs, const unsigne
     for (unsigned long long i = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; i < n;
          i += (unsigned long long)gridDim.x * blockDim.x) {
         const int2 rc = locs[i];
-        if (scan_key(g, rc.x, rc.y) == key) *out = rho[i];
+        if (scan_key(g, rc.x, rc.y) == key) *out = rho[size_t(rc.x) * g.ec + rc.y];
     }
 }
 
 // Final pass: each candidate sees the threshold of the last record before it.
 __global__ void k_seq_final(Grid g, const int2* __restrict__ locs, const unsigned long long* count,
-                            const double* __restrict__ rho, const uint8_t* __restrict__ deg,
-                            const double* map, const double* rho_c, const uint8_t* deg_c,
+                            const double* __restrict__ rho, const double* map, const double* rho_c, const uint8_t* deg_c,
                             const uint8_t* flat, int tflat, double T0,
                             const unsigned long long* __restrict__ rec_key,
                             const double* __restrict__ rec_T, int n_rec, Tally* tally,
@@ -484,7 +485,8 @@ __global__ void k_seq_final(Grid g, const int2* __restrict__ locs, const unsigne
         const double T = lo == 0 ? T0 : rec_T[lo - 1];
         if (alive_at(g, rc.x, rc.y, T, map, rho_c, deg_c, flat, tflat)) {
             ++alive;
-            const Cell cand = make_cell(rc.x, rc.y, rho[i], deg[i] != 0);
+            const size_t kk = size_t(rc.x) * g.ec + rc.y;
+            const Cell cand = make_cell(rc.x, rc.y, rho[kk], tflat || flat[kk]);
             if (better(cand, best)) best = cand;
         } else {
             ++dead;
@@ -543,20 +545,20 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
 
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                      int n_partials, cudaStream_t s) {
+                      int n_partials, cudaStream_t s, int rho_by_loc) {
     const int per_lane = (job.n + 31) / 32;
     int lane_flush = int(16777216LL / (65025LL * per_lane));
     if (lane_flush < 1) lane_flush = 1;
     k_corr_list<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
-                                           partials, lane_flush);
+                                           partials, lane_flush, rho_by_loc);
     return cudaGetLastError();
 }
 
 cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
                           int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                          int n_partials, cudaStream_t s) {
+                          int n_partials, cudaStream_t s, int rho_by_loc) {
     k_list_f64<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
-                                          partials);
+                                          partials, rho_by_loc);
     return cudaGetLastError();
 }
 
@@ -569,6 +571,21 @@ cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint
 cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
                            cudaStream_t s) {
     k_dense_f64<<<n_partials, 256, 0, s>>>(job, surface, partials);
+    return cudaGetLastError();
+}
+
+__global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
+                                 double* rho_c, uint8_t* deg_c) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < n) {
+        rho_c[size_t(i) * tc + col] = rho[i];
+        deg_c[size_t(i) * tc + col] = deg[i];
+    }
+}
+
+cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
+                           double* rho_c, uint8_t* deg_c, cudaStream_t s) {
+    k_scatter_column<<<(n + 255) / 256, 256, 0, s>>>(rho, deg, n, tc, col, rho_c, deg_c);
     return cudaGetLastError();
 }
 
@@ -611,12 +628,12 @@ cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, 
 }
 
 cudaError_t first_record(GridDesc g, const int2* locs, const unsigned long long* count,
-                         const double* rho, const uint8_t* deg, const double* map,
+                         const double* rho, const double* map,
                          const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
                          double T, unsigned long long after, unsigned long long* best_key,
                          cudaStream_t s) {
     cudaMemsetAsync(best_key, 0xff, sizeof(*best_key), s);
-    k_first_record<<<148 * 4, 256, 0, s>>>(to_grid(g), locs, count, rho, deg, map, rho_c, deg_c,
+    k_first_record<<<148 * 4, 256, 0, s>>>(to_grid(g), locs, count, rho, map, rho_c, deg_c,
                                            flat, tflat, T, after, best_key);
     return cudaGetLastError();
 }
@@ -629,12 +646,12 @@ cudaError_t fetch_record_rho(GridDesc g, const int2* locs, const unsigned long l
 }
 
 cudaError_t seq_final(GridDesc g, const int2* locs, const unsigned long long* count,
-                      const double* rho, const uint8_t* deg, const double* map,
+                      const double* rho, const double* map,
                       const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
                       double T0, const unsigned long long* rec_key, const double* rec_T, int n_rec,
                       Tally* tally, uint8_t* visits, CellH* partials, int n_partials,
                       cudaStream_t s) {
-    k_seq_final<<<n_partials, 256, 0, s>>>(to_grid(g), locs, count, rho, deg, map, rho_c, deg_c,
+    k_seq_final<<<n_partials, 256, 0, s>>>(to_grid(g), locs, count, rho, map, rho_c, deg_c,
                                            flat, tflat, T0, rec_key, rec_T, n_rec, tally, visits,
                                            partials);
     return cudaGetLastError();

@@ -106,7 +106,7 @@ __global__ void k_hsum_u8(const uint8_t* __restrict__ img, int p, int q, int n,
 // Column pass + FP64 epilogue: S, Q over m rows of the row sums; one thread owns kChunk
 // consecutive output rows of one column (coalesced across the warp).
 __global__ void k_vsum_stats(const int* __restrict__ hs, const int* __restrict__ hq, int p,
-                             int ec, int m, int n, double prefix_noise, DevStats st) {
+                             int ec, int m, int n, const double* __restrict__ pn, DevStats st) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const int er = p - m + 1;
     const int r0 = blockIdx.y * kChunk;
@@ -118,6 +118,7 @@ __global__ void k_vsum_stats(const int* __restrict__ hs, const int* __restrict__
     }
     const double inv_mn = 1.0 / (double(m) * double(n));
     const long long mn = (long long)m * n;
+    const double prefix_noise = *pn;
     const int r1 = min(r0 + kChunk, er);
     for (int r = r0; r < r1; ++r) {
         const size_t k = size_t(r) * ec + c;
@@ -220,7 +221,9 @@ __global__ void k_window_diff(const double* __restrict__ prefix, int rows, int c
 }
 
 __global__ void k_stats_from_sums(const double* __restrict__ S, const double* __restrict__ Q,
-                                  size_t E, int m, int n, double prefix_noise, DevStats st) {
+                                  size_t E, int m, int n, const double* __restrict__ pn,
+                                  DevStats st) {
+    const double prefix_noise = *pn;
     const double inv_mn = 1.0 / (double(m) * double(n));
     const long long mn = (long long)m * n;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
@@ -232,6 +235,15 @@ __global__ void k_stats_from_sums(const double* __restrict__ S, const double* __
         st.omega[k] = om;
         st.flat[k] = fl;
     }
+}
+
+// stats.cpp:80-81: prefix_noise = double(rows + cols) * eps * q_total
+__global__ void k_prefix_noise_u64(const unsigned long long* q_total, int rows, int cols,
+                                   double* out) {
+    *out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), double(*q_total));
+}
+__global__ void k_prefix_noise_f64(const double* q_total, int rows, int cols, double* out) {
+    *out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), *q_total);
 }
 
 int grid_for(size_t n, int threads) {
@@ -259,18 +271,24 @@ cudaError_t u8_to_f32_pitched(const uint8_t* img, int p, int q, float* out, int 
     k_u8_to_f32<<<grid, 256, 0, s>>>(img, p, q, out, pitch);
     return cudaGetLastError();
 }
-cudaError_t sum_sq_u8(const uint8_t* img, size_t n, unsigned long long* out, cudaStream_t s) {
-    cudaMemsetAsync(out, 0, sizeof(*out), s);
-    k_sum_sq_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long* q_total,
+                            double* out, cudaStream_t s) {
+    const size_t n = size_t(p) * q;
+    cudaMemsetAsync(q_total, 0, sizeof(*q_total), s);
+    k_sum_sq_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, q_total);
+    k_prefix_noise_u64<<<1, 1, 0, s>>>(q_total, p, q, out);
     return cudaGetLastError();
 }
-cudaError_t sum_sq_f64(const double* img, size_t n, double* out, cudaStream_t s) {
-    cudaMemsetAsync(out, 0, sizeof(*out), s);
-    k_sum_sq_f64<<<grid_for(n, 256), 256, 0, s>>>(img, n, out);
+cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,
+                             cudaStream_t s) {
+    const size_t n = size_t(p) * q;
+    cudaMemsetAsync(q_total, 0, sizeof(*q_total), s);
+    k_sum_sq_f64<<<grid_for(n, 256), 256, 0, s>>>(img, n, q_total);
+    k_prefix_noise_f64<<<1, 1, 0, s>>>(q_total, p, q, out);
     return cudaGetLastError();
 }
 
-cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, double prefix_noise,
+cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s) {
     const int ec = q - n + 1, er = p - m + 1;
     const int tpr = (ec + kChunk - 1) / kChunk;
@@ -308,7 +326,7 @@ cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m,
 }
 
 cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
-                            double prefix_noise, DevStats st, cudaStream_t s) {
+                            const double* prefix_noise, DevStats st, cudaStream_t s) {
     k_stats_from_sums<<<grid_for(E, 256), 256, 0, s>>>(S, Q, E, m, n, prefix_noise, st);
     return cudaGetLastError();
 }

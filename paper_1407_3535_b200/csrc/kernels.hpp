@@ -44,12 +44,17 @@ cudaError_t f64_to_u8(const double* img, size_t n, uint8_t* out, cudaStream_t s)
 cudaError_t u8_to_f32_pitched(const uint8_t* img, int p, int q, float* out, int pitch,
                               cudaStream_t s);
 cudaError_t u8_to_f64(const uint8_t* img, size_t n, double* out, cudaStream_t s);
-cudaError_t sum_sq_u8(const uint8_t* img, size_t n, unsigned long long* out, cudaStream_t s);
-cudaError_t sum_sq_f64(const double* img, size_t n, double* out, cudaStream_t s);
+// q_total (stats.cpp:78-79) and prefix_noise (stats.cpp:80-81) on the device.  The 8-bit
+// sum is exact; the FP64 sum is a parallel tree sum (parity notes).
+cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long* q_total,
+                            double* out, cudaStream_t s);
+cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,
+                             cudaStream_t s);
 
 // ---- window statistics, exact integer path (stats.cpp:55-94) ---------------------------
 // hs/hq scratch: p * ec int32 each.
-cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, double prefix_noise,
+cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n,
+                            const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s);
 // Window sums of an 8-bit image as exact doubles (running_sum on integer data).
 cudaError_t window_sums_u8(const uint8_t* img, int p, int q, int m, int n, int* hs,
@@ -73,7 +78,7 @@ cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m,
                                 double* out, cudaStream_t s);
 // stats epilogue from FP64 window sums S, Q (E entries).
 cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
-                            double prefix_noise, DevStats st, cudaStream_t s);
+                            const double* prefix_noise, DevStats st, cudaStream_t s);
 
 // ---- local auto-correlation + retained count (autocorr.cpp:40-96, egs.cpp:12-25) -------
 cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc g, DevStats st,
@@ -123,18 +128,22 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
                       int* n_partials, cudaStream_t s);
 // Warp-per-location evaluation of a location list (int2 row,col), argmax into partials.
 // out_rho/out_deg (optional) are indexed by list position.
+// out_rho indexed by list position, or by location (r*ec+c) when rho_by_loc.
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                      int n_partials, cudaStream_t s);
+                      int n_partials, cudaStream_t s, int rho_by_loc = 0);
 // FP64 replica (window_dot order, detail.hpp:32-41) over a location list or a dense range.
 cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
                           int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                          int n_partials, cudaStream_t s);
+                          int n_partials, cudaStream_t s, int rho_by_loc = 0);
 cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint8_t* deg_c,
                              CellH* partials, int n_partials, cudaStream_t s);
 cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
                            cudaStream_t s);
 
+// rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
+cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
+                           double* rho_c, uint8_t* deg_c, cudaStream_t s);
 // Reduce partial cells -> out[0] (better_candidate order).
 cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s);
 
@@ -155,8 +164,9 @@ cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, 
                          unsigned long long max_groups, cudaStream_t s);
 cudaError_t threshold_raise(const CellH* best, double* thr, cudaStream_t s);
 // Sequential policy replay: candidates = scan-2 survivors at T0 with their rho.
+// rho: extent-sized, indexed by location.
 cudaError_t first_record(GridDesc g, const int2* locs, const unsigned long long* count,
-                         const double* rho, const uint8_t* deg, const double* map,
+                         const double* rho, const double* map,
                          const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
                          double T, unsigned long long after, unsigned long long* best_key,
                          cudaStream_t s);
@@ -164,7 +174,7 @@ cudaError_t fetch_record_rho(GridDesc g, const int2* locs, const unsigned long l
                              const double* rho, unsigned long long key, double* out,
                              cudaStream_t s);
 cudaError_t seq_final(GridDesc g, const int2* locs, const unsigned long long* count,
-                      const double* rho, const uint8_t* deg, const double* map,
+                      const double* rho, const double* map,
                       const double* rho_c, const uint8_t* deg_c, const uint8_t* flat, int tflat,
                       double T0, const unsigned long long* rec_key, const double* rec_T, int n_rec,
                       Tally* tally, uint8_t* visits, CellH* partials, int n_partials,

@@ -99,6 +99,10 @@ SIGNATURES = {
     "tm_ctx_destroy": (None, [_P]),
     "tm_ctx_synchronize": (C.c_int, [_P]),
     "tm_ctx_launch_count": (C.c_int64, [_P]),
+    "tm_ctx_stream": (C.c_void_p, [_P]),
+    "tm_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
+    "tm_ctx_phase_times": (C.c_int, [_P, C.c_char_p, C.c_size_t]),
+    "tm_image_reset_cache": (C.c_int, [_P]),
     "tm_image_create": (C.c_int, [_P, _D, C.c_int, C.c_int, C.POINTER(_P)]),
     "tm_image_create_u8": (C.c_int, [_P, _U8, C.c_int, C.c_int, C.POINTER(_P)]),
     "tm_image_upload_u8": (C.c_int, [_P, _P, _U8]),

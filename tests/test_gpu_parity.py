@@ -1,0 +1,232 @@
+"""GPU parity: the sm_100a path through the C ABI vs the oracle, bit for bit.
+
+Integer (8-bit) inputs take the exact-integer kernels; non-integer inputs (OptA's blurred
+image) take the FP64 replica kernels.  Both must reproduce the reference's results exactly:
+locations, rho bits, skip counts, visit maps, EGS traces, OptA kappa/traces.  (The
+north-star tolerance is rho within 1e-5; we assert equality.)
+"""
+import numpy as np
+import pytest
+
+from conftest import RESULT_KEYS, assert_same_result, golden, golden_names, res_vec
+
+pytestmark = pytest.mark.gpu
+
+
+def _ws_equal(a, b):
+    for x, y in zip(a, b):
+        np.testing.assert_array_equal(x, y)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_fixtures(ctx, name):
+    g = golden(name)
+    img, t = g["image"], g["template"]
+    m, n = t.shape
+    gi = ctx.image(img)
+    mu, om, fl = ctx.window_stats(gi, m, n)
+    np.testing.assert_array_equal(fl, g["ws_flat"])
+    if "ws_mu" in g:
+        np.testing.assert_array_equal(mu, g["ws_mu"])
+        np.testing.assert_array_equal(om, g["ws_omega"])
+    b, surf = ctx.brute_force_match(t, gi, record_surface=True)
+    np.testing.assert_array_equal(res_vec(b)[:-1], g["brute"][:-1])
+    if "surface" in g:
+        np.testing.assert_array_equal(surf, g["surface"])
+    e = ctx.efficient_group_size(gi, m, n)
+    assert [e["h"], e["w"]] == list(g["egs_h"])
+    np.testing.assert_array_equal(
+        np.array([[x["h"], x["w"], x["central"], x["retained"], x["total"]] for x in e["trace"]]),
+        g["egs_trace"])
+    if "egs_map" in g:
+        np.testing.assert_array_equal(e["map"], g["egs_map"])
+    init = 0.8 if name == "acceptance256" else None
+    for mode in ("egs", "opta"):
+        for pol, par in (("seq", False), ("frozen", True)):
+            r, vis = ctx.match(t, img, mode=mode, parallel=par, threads=4, record_visits=True,
+                               init_threshold=init)
+            np.testing.assert_array_equal(res_vec(r), g[f"{mode}_{pol}"], err_msg=f"{mode} {pol}")
+            np.testing.assert_array_equal(vis, g[f"{mode}_{pol}_visits"])
+    prep = ctx.prepare(gi, m, n, mode="opta")
+    assert prep.info["kappa"] == int(g["opta_kappa"][0])
+    np.testing.assert_array_equal(
+        np.array([[x["h"], x["w"], x["cost"], x["restored"]] for x in prep.info["opta_trace"]]),
+        g["opta_trace"])
+    if "opta_image" in g:
+        np.testing.assert_array_equal(prep.search_image(), g["opta_image"])
+        np.testing.assert_array_equal(prep.map(), g["opta_map"])
+        np.testing.assert_array_equal(ctx.blur(gi), g["blur"])
+        np.testing.assert_array_equal(ctx.blur_fidelity_map(gi, g["blur"], m, n), g["fidelity"])
+
+
+def test_config1_all_modes(ctx, port):
+    from paper_1407_3535_b200 import workloads as W
+    g = golden("config1")
+    w = W.config1()
+    t = w.templates[0].pixels.astype(np.float64)
+    for mode in ("brute", "egs", "opta"):
+        for pol, par in (("seq", False), ("frozen", True)):
+            r = ctx.match(t, w.image.astype(np.float64), mode=mode, parallel=par, threads=4)
+            np.testing.assert_array_equal(res_vec(r), g[f"{mode}_{pol}"], err_msg=f"{mode} {pol}")
+
+
+def _cases():
+    rng = np.random.default_rng(7)
+    out = []
+    shapes = [(40, 40, 5, 5), (37, 53, 7, 4), (64, 48, 16, 16), (30, 90, 3, 11), (70, 70, 33, 31),
+              (25, 25, 25, 25), (20, 64, 1, 1), (128, 96, 17, 64)]
+    for k, (p, q, m, n) in enumerate(shapes):
+        base = np.cumsum(np.cumsum(rng.normal(size=(p, q)), 0), 1)
+        img = np.clip(np.rint((base - base.min()) / (np.ptp(base) + 1e-9) * 255), 0, 255)
+        if k % 3 == 1:
+            img = rng.integers(0, 256, size=(p, q)).astype(np.float64)
+        if k == 2:
+            img[10:40, 5:30] = 77.0  # flat region: flat windows, degenerate centres
+        r0, c0 = rng.integers(0, p - m + 1), rng.integers(0, q - n + 1)
+        t = np.clip(np.rint(img[r0:r0 + m, c0:c0 + n] * 1.1 - 5 + rng.normal(0, 3, (m, n))),
+                    0, 255)
+        out.append((img, t))
+    return out
+
+
+@pytest.mark.parametrize("idx", range(8))
+def test_match_vs_oracle_edge_shapes(ctx, port, idx):
+    img, t = _cases()[idx]
+    for mode in ("brute", "egs", "opta"):
+        for par in (False, True):
+            if np.ptp(t) == 0 and mode != "brute":
+                continue
+            a, va = ctx.match(t, img, mode=mode, parallel=par, threads=3, record_visits=True)
+            b, vb = port.match(t, img, mode=mode, parallel=par, threads=3, visits=True)
+            np.testing.assert_array_equal(res_vec(a), res_vec(b), err_msg=f"{mode} par={par}")
+            if mode != "brute":
+                np.testing.assert_array_equal(va, vb)
+
+
+@pytest.mark.parametrize("h", [1, 3, 5, 7, 9, 11])
+def test_autocorrelation_and_retained(ctx, port, h):
+    img, t = _cases()[0]
+    m, n = t.shape
+    np.testing.assert_array_equal(ctx.local_autocorrelation(img, m, n, h, h),
+                                  port.local_autocorrelation(img, m, n, h, h))
+    amap = port.local_autocorrelation(img, m, n, h, h)
+    assert ctx.autocorr_retained(img, m, n, h, h, 0.8) == port.retained_count(amap, h, h, 0.8)
+
+
+def test_nonsquare_groups_and_transitive_search(ctx, port):
+    img, t = _cases()[3]
+    m, n = t.shape
+    for h, w in ((3, 5), (5, 1), (7, 3)):
+        amap = port.local_autocorrelation(img, m, n, h, w)
+        np.testing.assert_array_equal(ctx.local_autocorrelation(img, m, n, h, w), amap)
+        for par in (False, True):
+            a, va = ctx.transitive_search(t, img, amap, h, w, parallel=par, threads=2,
+                                          record_visits=True)
+            b, vb = port.transitive_search(t, img, amap, h, w, parallel=par, threads=2,
+                                           visits=True)
+            np.testing.assert_array_equal(res_vec(a)[:-1], res_vec(b)[:-1])
+            np.testing.assert_array_equal(va, vb)
+
+
+def test_center_scan_and_refine(ctx, port):
+    img, t = _cases()[4]
+    m, n = t.shape
+    cs = ctx.center_scan(t, img, 5, 5)
+    b, surface = port.brute(t, img, surface=True)  # zncc_at at every location
+    _, _, fl = port.window_stats(img, m, n)
+    er, ec = img.shape[0] - m + 1, img.shape[1] - n + 1
+    want_rho, want_deg, best = [], [], None
+    for ti in range((er + 4) // 5):
+        r0, r1 = ti * 5, min(ti * 5 + 5, er) - 1
+        for tj in range((ec + 4) // 5):
+            c0, c1 = tj * 5, min(tj * 5 + 5, ec) - 1
+            cr, cc = (r0 + r1) // 2, (c0 + c1) // 2  # autocorr.cpp:26-30
+            want_rho.append(surface[cr, cc])
+            want_deg.append(fl[cr, cc])
+            key = (not fl[cr, cc], surface[cr, cc], -cr, -cc)  # better_candidate order
+            if best is None or key > best[0]:
+                best = (key, (cr, cc, surface[cr, cc], bool(fl[cr, cc])))
+    np.testing.assert_array_equal(cs["rho"], np.array(want_rho))
+    np.testing.assert_array_equal(cs["degenerate"], np.array(want_deg, np.uint8))
+    assert cs["best"] == best[1]
+    r, c, rho, deg = ctx.refine_localization(t, img, b.best_row, b.best_col, 3)
+    assert (r, c, rho) == (b.best_row, b.best_col, b.best_rho)
+    assert port.refine(t, img, 5, 7, 4) == ctx.refine_localization(t, img, 5, 7, 4)
+
+
+def test_nonintegral_image_replica_path(ctx, port):
+    img, t = _cases()[0]
+    m, n = t.shape
+    blurred = port.blur(img)
+    gb = ctx.image(blurred)
+    assert not gb.is_integer
+    _ws_equal(ctx.window_stats(gb, m, n), port.window_stats(blurred, m, n))
+    np.testing.assert_array_equal(ctx.running_sum(gb, m, n), port.running_sum(blurred, m, n))
+    for h in (3, 5):
+        np.testing.assert_array_equal(ctx.local_autocorrelation(gb, m, n, h, h),
+                                      port.local_autocorrelation(blurred, m, n, h, h))
+    a, sa = ctx.brute_force_match(t, gb, record_surface=True)
+    b, sb = port.brute(t, blurred, surface=True)
+    np.testing.assert_array_equal(sa, sb)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+    # non-integer template on an integer image also takes the FP64 path
+    tf = t * 0.5 + 0.25
+    a = ctx.brute_force_match(tf, img)
+    b = port.brute(tf, img)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+
+
+def test_seeded_policy_same_argmax_and_sound(ctx, port):
+    img, t = _cases()[0]
+    b, surface = port.brute(t, img, surface=True)
+    for mode in ("egs", "opta"):
+        r, vis = ctx.match(t, img, mode=mode, policy="seeded", record_visits=True)
+        if mode == "egs":
+            assert (r.best_row, r.best_col, r.best_rho) == (b.best_row, b.best_col, b.best_rho)
+            # soundness: every eliminated member is <= the final threshold (acceptance c4)
+            assert np.all(surface[vis == 1] <= r.final_threshold + 1e-9)
+        else:
+            assert (r.refined_row, r.refined_col, r.refined_rho) == \
+                (b.best_row, b.best_col, b.best_rho)
+        assert r.eliminated + r.retained + r.centers == b.ops
+
+
+def test_batch_run_matches_individual(ctx, port):
+    from paper_1407_3535_b200 import workloads as W
+    w = W.config1()
+    rng = np.random.default_rng(3)
+    ts = [W.cut_template(rng, w.image, 32, 32, 1.0, 0.0, 4.0).pixels for _ in range(4)]
+    gi = ctx.image(w.image)
+    for mode in ("egs", "opta"):
+        prep = ctx.prepare(gi, 32, 32, mode=mode)
+        batch = ctx.run(prep, np.stack(ts), parallel=True, threads=4)
+        for t, r in zip(ts, batch):
+            o = port.match(t.astype(float), w.image.astype(float), mode=mode, parallel=True,
+                           threads=4)
+            np.testing.assert_array_equal(res_vec(r)[:-1], res_vec(o)[:-1])
+
+
+def test_errors_match_reference_messages(ctx):
+    from paper_1407_3535_b200.api import InvalidArgument
+    img = np.random.default_rng(1).integers(0, 256, (32, 32)).astype(np.float64)
+    with pytest.raises(InvalidArgument, match="constant template"):
+        ctx.match(np.full((5, 5), 3.0), img, mode="egs")
+    with pytest.raises(InvalidArgument, match="template larger than search image"):
+        ctx.match(np.ones((40, 5)), img, mode="egs")
+    with pytest.raises(InvalidArgument, match="odd"):
+        ctx.local_autocorrelation(img, 5, 5, 4, 3)
+    with pytest.raises(InvalidArgument, match="init threshold"):
+        ctx.match(img[:5, :5], img, mode="egs", init_threshold=1.5)
+    with pytest.raises(InvalidArgument, match="rho_tb"):
+        ctx.efficient_group_size(img, 5, 5, rho_tb=1.0)
+    r = ctx.match(np.full((5, 5), 3.0), img, mode="brute")  # brute accepts flat templates
+    assert r.best_degenerate and r.best_rho == 0.0
+
+
+def test_below_threshold_flag(ctx, port):
+    img, t = _cases()[0]
+    for mode in ("egs", "opta"):
+        a = ctx.match(t, img, mode=mode, init_threshold=0.9999)
+        b = port.match(t, img, mode=mode, init_threshold=0.9999)
+        np.testing.assert_array_equal(res_vec(a), res_vec(b))
+        assert a.below_threshold
