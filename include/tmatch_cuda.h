@@ -178,6 +178,11 @@ int tm_blur(tm_ctx* ctx, tm_image* img, const double* profile, int len, double* 
 int tm_blur_fidelity_map(tm_ctx* ctx, tm_image* img, tm_image* blurred, int m, int n,
                          double* fid);
 
+/* unblur_violations (blur.hpp:70-71): restore the window of every location whose fidelity
+ * (fid, extent doubles) is below lambda; out = restored image, count = marked windows. */
+int tm_unblur_violations(tm_ctx* ctx, tm_image* blurred, tm_image* original, const double* fid,
+                         int m, int n, double lambda, double* out, int64_t* count);
+
 /* ---- matcher.hpp ------------------------------------------------------------------- */
 /* prepare_egs / prepare_opta (matcher.hpp:71-72): device-resident PreparedEgs/PreparedOptA
  * (window statistics, R_co map, OptA image) reusable across templates of size m x n. */

@@ -79,6 +79,12 @@ def build(verbose: bool = False) -> dict:
             _run(["g++"] + CXX_FLAGS + ["-shared", "-o", api_so] + api_srcs +
                  ["-L" + LIB, "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
         out["api"] = api_so
+        check_src = os.path.join(ROOT, "tests", "cpp", "api_check.cpp")
+        check_bin = os.path.join(LIB, "api_check")
+        if os.path.exists(check_src) and _newer(check_bin, [check_src, api_so] + api_hdrs):
+            _run(["g++"] + CXX_FLAGS + ["-o", check_bin, check_src, "-L" + LIB, "-ltmatch",
+                                        "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+        out["api_check"] = check_bin
     return out
 
 

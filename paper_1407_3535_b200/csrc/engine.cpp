@@ -168,7 +168,7 @@ struct tm_ctx {
     int64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // scratch (grow-only)
-    DBuf<int> hs, hq, markP;
+    DBuf<int> hs, hq, markP, acH;
     DBuf<double> rowacc, prefix, S, Q, fid, cross, inwin, dtmp;
     DBuf<uint8_t> u8tmp, marks;
     DBuf<tmk::CellH> partials, cells;
@@ -592,8 +592,16 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
     CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
     if (img->integer) {
-        CK(tmk::autocorr_u8(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
-        ctx->add(1);
+        const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
+        if (tmk::autocorr_two_pass_supported(n, g) && hbytes <= (size_t(16) << 30)) {
+            ctx->acH.ensure(hbytes / sizeof(int));
+            CK(tmk::autocorr_u8_two_pass(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
+                                         ctx->acH.p, ctx->s));
+            ctx->add(3);
+        } else {
+            CK(tmk::autocorr_u8(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
+            ctx->add(1);
+        }
         return;
     }
     CK(tmk::autocorr_init(map, g, ctx->s));
@@ -1531,6 +1539,37 @@ int tm_blur_fidelity_map(tm_ctx* ctx, tm_image* img, tm_image* blurred, int m, i
         CK(cudaMemcpyAsync(fid, ctx->fid.p, size_t(ws_o.er) * ws_o.ec * 8, cudaMemcpyDeviceToHost,
                            ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_unblur_violations(tm_ctx* ctx, tm_image* blurred, tm_image* original, const double* fid,
+                         int m, int n, double lambda, double* out, int64_t* count) {
+    return guard(ctx, [&] {
+        if (blurred->p != original->p || blurred->q != original->q)
+            invalid("unblur_violations: shape mismatch");
+        const int p = original->p, q = original->q;
+        const int er = p - m + 1, ec = q - n + 1;
+        if (er < 1 || ec < 1) invalid("unblur_violations: window does not fit");
+        const size_t E = size_t(er) * ec, N = size_t(p) * q;
+        ensure_f64(ctx, blurred);
+        ensure_f64(ctx, original);
+        ctx->fid.ensure(E);
+        ctx->marks.ensure(E);
+        ctx->markP.ensure(size_t(er + 1) * (ec + 1));
+        ctx->dtmp.ensure(N);
+        CK(cudaMemcpyAsync(ctx->fid.p, fid, E * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaMemcpyAsync(ctx->dtmp.p, blurred->f64.p, N * 8, cudaMemcpyDeviceToDevice, ctx->s));
+        // blur.cpp:188-199: mark every location below lambda, then restore their windows
+        CK(tmk::mark_violations(ctx->fid.p, nullptr, E, lambda, ctx->marks.p,
+                                ctx->counters.p + 3, ctx->s));
+        CK(tmk::restore_covered(ctx->dtmp.p, original->f64.p, ctx->marks.p, er, ec, m, n, p, q,
+                                ctx->markP.p, ctx->s));
+        ctx->add(4);
+        unsigned long long c = 0;
+        CK(cudaMemcpyAsync(&c, ctx->counters.p + 3, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaMemcpyAsync(out, ctx->dtmp.p, N * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        *count = (int64_t)c;
     });
 }
 

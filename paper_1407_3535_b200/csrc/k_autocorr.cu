@@ -154,6 +154,231 @@ __global__ void k_autocorr_u8(ACParams P) {
     if (threadIdx.x == 0 && blk_nr) atomicAdd(P.n_r, blk_nr);
 }
 
+// ---- three-pass R_co (row walk, column prefix, epilogue), for w in {1,3,...,11} -----
+//
+// Pass 1 (k_ac_rows): a CTA owns 128 consecutive image rows x for one row offset di and one
+// segment of centre columns; it stages rows x and x+di of that segment in shared memory
+// (coalesced), then each thread walks its row once.  A W-entry register ring holds
+// I(x+di, y-wr .. y+wr), so a pixel costs two shared-memory byte loads and W integer MACs
+// -- one per column offset dj -- accumulated as running prefixes R_dj(y).  At a centre
+// column cc (y = cc) the prefixes are recorded (shared-memory ring), at y = cc + n the
+// row-window sum  H[di,dj](k, x) = sum_b I(x, cc+b) I(x+di, cc+dj+b)  is emitted.  Centre
+// columns are cc_k = wr + k*w, so with the walk aligned to multiples of W every ring
+// index and event position is static inside a W-step unrolled block.
+// Pass 2 (k_ac_scan): one warp per (offset, centre column) line turns H into its inclusive
+// prefix over rows, in place, in wrapping 32-bit arithmetic (window sums < 2^31 are then
+// exact differences).
+// Pass 3 (k_ac_epi): S = P[cr+m-1] - P[cr-1] per (offset, centre), FP64 epilogue of
+// autocorr.cpp:84-88, map write and the retained count of egs.cpp:12-25.
+// H layout [di][dj][k][x] (x fastest).
+constexpr int kAcRows = 128;
+
+template <int W>
+__global__ void __launch_bounds__(kAcRows)
+    k_ac_rows(const uint8_t* __restrict__ img, int p, int q, int n, int tcr, int tc, int seg,
+              int ring, int spitch, unsigned* __restrict__ H) {
+    extern __shared__ __align__(16) unsigned char sm[];
+    constexpr int wr = W / 2;
+    const int x0 = blockIdx.x * kAcRows;
+    const int dii = blockIdx.y;
+    const int hr = gridDim.y / 2;
+    const int di = dii - hr;
+    const int k0 = blockIdx.z * seg, k1 = min(k0 + seg, tcr);
+    if (k0 >= k1) return;
+    const int y_s = k0 * W;                   // walk start (multiple of W)
+    const int y_e = wr + (k1 - 1) * W + n;    // last window-end event
+    const int c_lo = y_s - wr;                // staged columns [c_lo, c_lo + swid)
+    const int swid = (y_e + W) - c_lo + wr + 1;
+    const int r_lo = x0 + min(0, di);         // staged rows [r_lo, r_lo + srow)
+    const int srow = kAcRows + abs(di);
+    uint8_t* simg = sm;
+    int* rec = reinterpret_cast<int*>(sm + ((size_t(srow) * spitch + 15) & ~size_t(15)));
+    for (int idx = threadIdx.x; idx < srow * swid; idx += kAcRows) {
+        const int a = idx / swid, b = idx - a * swid;
+        const int r = r_lo + a, c = c_lo + b;
+        simg[a * spitch + b] = (r >= 0 && r < p && c >= 0 && c < q) ? img[size_t(r) * q + c] : 0;
+    }
+    __syncthreads();
+    const int x = x0 + threadIdx.x;
+    const bool row_ok = x < p && x + di >= 0 && x + di < p;
+    // local column index of image column c is c - c_lo
+    const uint8_t* ra = simg + (x - r_lo) * spitch - c_lo;
+    const uint8_t* rb = simg + (x + di - r_lo) * spitch - c_lo;
+    // ring slot of column c is (c - y_s + wr) mod W: static (s + t) % W inside a block
+    int acc[W];
+    int rg[W];
+#pragma unroll
+    for (int t = 0; t < W; ++t) {
+        acc[t] = 0;
+        rg[t] = (t < W - 1 && row_ok) ? int(rb[y_s - wr + t]) : 0;
+    }
+    const size_t plane = size_t(tc) * p;  // one (di,dj) plane of H
+    for (int y0 = y_s; y0 <= y_e; y0 += W) {
+#pragma unroll
+        for (int s = 0; s < W; ++s) {
+            const int y = y0 + s;
+            // events use the prefix before P(y) is added
+            if (s == wr) {  // window start of centre k = (y - wr) / W
+                const int k = (y - wr) / W;
+                if (k < k1) {
+                    const int slot = k % ring;
+#pragma unroll
+                    for (int t = 0; t < W; ++t) rec[(slot * W + t) * kAcRows + threadIdx.x] = acc[t];
+                }
+            }
+            if (s == (wr + n) % W) {  // window end of centre k = (y - n - wr) / W
+                const int kk = y - n - wr;
+                if (kk >= k0 * W && kk < k1 * W) {
+                    const int k = kk / W;
+                    const int slot = k % ring;
+                    if (x < p) {
+#pragma unroll
+                        for (int t = 0; t < W; ++t)
+                            H[(size_t(dii) * W + t) * plane + size_t(k) * p + x] =
+                                unsigned(acc[t] - rec[(slot * W + t) * kAcRows + threadIdx.x]);
+                    }
+                }
+            }
+            rg[(s + W - 1) % W] = row_ok ? int(rb[y + wr]) : 0;  // I(x+di, y+wr)
+            const int a = row_ok ? int(ra[y]) : 0;
+#pragma unroll
+            for (int t = 0; t < W; ++t) acc[t] += a * rg[(s + t) % W];  // dj = t - wr
+        }
+    }
+}
+
+// Clipped last centre column (irregular position): direct n-wide sums.
+__global__ void k_ac_rows_last(const uint8_t* __restrict__ img, int p, int q, int n, int h, int w,
+                               int cc, int kcol, int tc, unsigned* __restrict__ H) {
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int oi = blockIdx.y;  // (di, dj) raster index in [0, h*w)
+    const int di = oi / w - h / 2, dj = oi % w - w / 2;
+    if (x >= p) return;
+    int s = 0;
+    if (x + di >= 0 && x + di < p) {
+        const uint8_t* ra = img + size_t(x) * q + cc;
+        const uint8_t* rb = img + size_t(x + di) * q + cc + dj;
+        for (int b = 0; b < n; ++b) {
+            const int cb = cc + dj + b;
+            s += int(ra[b]) * ((cb >= 0 && cb < q) ? int(rb[b]) : 0);
+        }
+    }
+    H[size_t(oi) * tc * p + size_t(kcol) * p + x] = unsigned(s);
+}
+
+// In-place inclusive prefix along x of every (offset, centre column) line (wrapping u32).
+__global__ void k_ac_scan(unsigned* __restrict__ H, int p, long long lines) {
+    const int lane = threadIdx.x & 31;
+    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long li = warp; li < lines; li += nwarps) {
+        unsigned* L = H + li * p;
+        unsigned carry = 0;
+        for (int x0 = 0; x0 < p; x0 += 32) {
+            const int x = x0 + lane;
+            unsigned v = x < p ? L[x] : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += u;
+            }
+            v += carry;
+            if (x < p) L[x] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+}
+
+// Epilogue: thread = (offset, centre row ti, centre column k), lanes over k.
+__global__ void __launch_bounds__(256)
+    k_ac_epi(const unsigned* __restrict__ P, int p, int m, int n, Grid g, DevStats st, double thr,
+             double* __restrict__ map, unsigned long long* n_r) {
+    const int hw = g.h * g.w;
+    const long long items = (long long)hw * g.tr * g.tc;
+    const double mn = double(m) * double(n);
+    const int hr = g.h / 2, wr = g.w / 2;
+    unsigned long long local = 0;
+    for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < items;
+         it += (long long)gridDim.x * blockDim.x) {
+        const int k = int(it % g.tc);
+        const long long rest = it / g.tc;
+        const int ti = int(rest % g.tr);
+        const int oi = int(rest / g.tr);
+        const int di = oi / g.w - hr, dj = oi % g.w - wr;
+        const int cc = g.center_col(k), cr = g.center_row(ti);
+        if (di == 0 && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
+            map[size_t(cr) * g.ec + cc] = 1.0;
+            continue;
+        }
+        const int c0 = k * g.w, c1 = min(c0 + g.w, g.ec) - 1;
+        const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        const int mr = cr + di, mc = cc + dj;
+        if (mr < r0 || mr > r1 || mc < c0 || mc > c1) continue;  // not this group's member
+        const unsigned* L = P + (size_t(oi) * g.tc + k) * p;
+        const unsigned S = L[cr + m - 1] - (cr > 0 ? L[cr - 1] : 0u);
+        const size_t kc = size_t(cr) * g.ec + cc, km = size_t(mr) * g.ec + mc;
+        double v = 0.0;
+        if (!st.flat[kc] && !st.flat[km]) {
+            const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, st.mu[kc]), st.mu[km]));
+            v = dclamp(__ddiv_rn(num, __dmul_rn(st.omega[kc], st.omega[km])), -1.0, 1.0);
+        }
+        map[km] = v;
+        if (v < thr) ++local;
+    }
+    local = warp_sum(local);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_r, local);
+}
+
+struct AcRowsGeom {
+    int seg, ring, spitch;
+    size_t smem;
+};
+
+template <int W>
+AcRowsGeom ac_rows_geom(int n, int h) {
+    AcRowsGeom g;
+    g.seg = std::max(4, 256 / W);
+    g.ring = (n + W - 1) / W + 2;
+    const int swid = g.seg * W + n + 2 * W + 2;
+    int pitch = (swid + 3) & ~3;
+    if (((pitch / 4) & 1) == 0) pitch += 4;  // rows 4 mod 8 bytes apart: no bank conflicts
+    g.spitch = pitch;
+    const int srow = kAcRows + h / 2;
+    g.smem = ((size_t(srow) * pitch + 15) & ~size_t(15)) + size_t(g.ring) * W * kAcRows * 4;
+    return g;
+}
+
+template <int W>
+cudaError_t launch_ac_rows(const uint8_t* img, int p, int q, int n, int h, int tcr, int tc,
+                           unsigned* H, cudaStream_t s) {
+    const AcRowsGeom geo = ac_rows_geom<W>(n, h);
+    if (geo.smem > 200 * 1024) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ac_rows<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    dim3 grid((p + kAcRows - 1) / kAcRows, h, (tcr + geo.seg - 1) / geo.seg);
+    if (tcr > 0)
+        k_ac_rows<W><<<grid, kAcRows, geo.smem, s>>>(img, p, q, n, tcr, tc, geo.seg, geo.ring,
+                                                      geo.spitch, H);
+    return cudaGetLastError();
+}
+
+bool ac_supported(int n, int h, int w) {
+    size_t smem = 0;
+    switch (w) {
+        case 1: smem = ac_rows_geom<1>(n, h).smem; break;
+        case 3: smem = ac_rows_geom<3>(n, h).smem; break;
+        case 5: smem = ac_rows_geom<5>(n, h).smem; break;
+        case 7: smem = ac_rows_geom<7>(n, h).smem; break;
+        case 9: smem = ac_rows_geom<9>(n, h).smem; break;
+        case 11: smem = ac_rows_geom<11>(n, h).smem; break;
+        default: return false;
+    }
+    return smem <= 200 * 1024;
+}
+
 // ---- replica path helpers ---------------------------------------------------------------
 
 __global__ void k_autocorr_init(double* map, Grid g) {
@@ -258,10 +483,47 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
     const int base = ((gd.tc + gtc - 1) / gtc) * ((gd.tr + gtr - 1) / gtr);
     const int noff = gd.h * gd.w - 1;
     int splits = std::max(1, std::min(noff, (148 * 6 + base - 1) / base));
-    P.noff_per = (noff + splits - 1) / splits;
-    splits = (noff + P.noff_per - 1) / P.noff_per;
+    P.noff_per = std::max(1, (noff + splits - 1) / splits);
+    splits = std::max(1, (noff + P.noff_per - 1) / P.noff_per);
     dim3 grid((gd.tc + gtc - 1) / gtc, (gd.tr + gtr - 1) / gtr, std::max(splits, 1));
     k_autocorr_u8<<<grid, 256, bytes, s>>>(P);
+    return cudaGetLastError();
+}
+
+size_t autocorr_rowsum_bytes(int p, GridDesc g) {
+    return size_t(g.h) * g.w * g.tc * p * sizeof(unsigned);
+}
+
+bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h, g.w); }
+
+cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
+                                 DevStats st, double retain_threshold, double* map,
+                                 unsigned long long* n_r, int* Hraw, cudaStream_t s) {
+    unsigned* H = reinterpret_cast<unsigned*>(Hraw);
+    const bool clipped = size_t(gd.tc) * gd.w > size_t(gd.ec);
+    const int tcr = clipped ? gd.tc - 1 : gd.tc;
+    cudaError_t e = cudaSuccess;
+    switch (gd.w) {
+        case 1: e = launch_ac_rows<1>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        case 3: e = launch_ac_rows<3>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        case 5: e = launch_ac_rows<5>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        case 7: e = launch_ac_rows<7>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        case 9: e = launch_ac_rows<9>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        case 11: e = launch_ac_rows<11>(img, p, q, n, gd.h, tcr, gd.tc, H, s); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    const Grid g = to_grid(gd);
+    if (clipped) {
+        dim3 grid((p + 127) / 128, gd.h * gd.w);
+        k_ac_rows_last<<<grid, 128, 0, s>>>(img, p, q, n, gd.h, gd.w, g.center_col(gd.tc - 1),
+                                            gd.tc - 1, gd.tc, H);
+    }
+    const long long lines = (long long)gd.h * gd.w * gd.tc;
+    k_ac_scan<<<int(std::min<long long>((lines + 7) / 8, 148 * 32)), 256, 0, s>>>(H, p, lines);
+    const long long items = (long long)gd.h * gd.w * gd.tr * gd.tc;
+    const int blocks = int(std::min<long long>((items + 255) / 256, 148 * 32));
+    k_ac_epi<<<blocks, 256, 0, s>>>(H, p, m, n, g, st, retain_threshold, map, n_r);
     return cudaGetLastError();
 }
 

@@ -172,12 +172,17 @@ __global__ void __launch_bounds__(NW * 32)
 }
 
 // ---- sparse: one warp per location ----------------------------------------------------
+// The template is staged once per CTA in shared memory; lanes own template columns
+// j = lane, lane+32, ...; the row loop is unrolled for memory-level parallelism.
 __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                 int lane_flush, int rho_by_loc) {
+    extern __shared__ __align__(16) float stmp[];  // m x npad template
     __shared__ Cell scratch[8];
     const int lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < job.m * job.npad; i += blockDim.x) stmp[i] = job.tf[i];
+    __syncthreads();
     const long long nloc = min((long long)*count, (long long)max_count);
     const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -185,15 +190,19 @@ __global__ void __launch_bounds__(256)
     Cell best = no_cell();
     for (long long li = warp0; li < nloc; li += nwarps) {
         const int2 rc = locs[li];
-        float acc = 0.f;
         double dacc = 0.0;
-        for (int i = 0; i < job.m; ++i) {
-            const float* ir = job.imgf + size_t(rc.x + i) * job.pitch + rc.y;
-            const float* tr = job.tf + size_t(i) * job.npad;
-            for (int j = lane; j < job.n; j += 32) acc = fmaf(tr[j], ir[j], acc);
-            if ((i + 1) % lane_flush == 0) {
-                dacc += double(acc);
-                acc = 0.f;
+        float acc = 0.f;
+        const float* ib = job.imgf + size_t(rc.x) * job.pitch + rc.y;
+        for (int j = lane; j < job.n; j += 32) {
+            int since = 0;
+#pragma unroll 8
+            for (int i = 0; i < job.m; ++i) {
+                acc = fmaf(stmp[i * job.npad + j], __ldg(ib + size_t(i) * job.pitch + j), acc);
+                if (++since == lane_flush) {
+                    dacc += double(acc);
+                    acc = 0.f;
+                    since = 0;
+                }
             }
         }
         dacc += double(acc);
@@ -546,11 +555,17 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                       int n_partials, cudaStream_t s, int rho_by_loc) {
-    const int per_lane = (job.n + 31) / 32;
-    int lane_flush = int(16777216LL / (65025LL * per_lane));
-    if (lane_flush < 1) lane_flush = 1;
-    k_corr_list<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
-                                           partials, lane_flush, rho_by_loc);
+    // one lane accumulates one template column at a time: flush before 2^24
+    int lane_flush = int(16777216LL / 65025LL);
+    const size_t smem = size_t(job.m) * job.npad * sizeof(float);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_corr_list, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    k_corr_list<<<n_partials, 256, smem, s>>>(job, locs, count, max_count, out_rho, out_deg,
+                                              partials, lane_flush, rho_by_loc);
     return cudaGetLastError();
 }
 

@@ -75,7 +75,7 @@ __global__ void k_marks(const double* __restrict__ fid, const double* __restrict
     unsigned long long local = 0;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
          k += size_t(gridDim.x) * blockDim.x) {
-        const bool mk = !(fid[k] >= lambda) && in_win[k] != 0.0;
+        const bool mk = !(fid[k] >= lambda) && (in_win == nullptr || in_win[k] != 0.0);
         marks[k] = mk;
         local += mk;
     }

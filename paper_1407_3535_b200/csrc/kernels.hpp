@@ -84,6 +84,13 @@ cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, i
 cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc g, DevStats st,
                         double retain_threshold, double* map, unsigned long long* n_r,
                         cudaStream_t s);
+// Two-pass variant (row walk + column slide) for w in {1,3,...,11}; H scratch of
+// autocorr_rowsum_bytes(p, g) bytes.
+size_t autocorr_rowsum_bytes(int p, GridDesc g);
+bool autocorr_two_pass_supported(int n, GridDesc g);
+cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
+                                 DevStats st, double retain_threshold, double* map,
+                                 unsigned long long* n_r, int* H, cudaStream_t s);
 // replica path, one offset: cross-sum prefix table of the product image for (di,dj).
 cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
                                      GridDesc g, DevStats st, int di, int dj, double* map,

@@ -132,13 +132,13 @@ __device__ __forceinline__ T warp_sum(T v) {
 // centre = (r0 + r1) / 2.
 struct Grid {
     int er, ec, h, w, tr, tc;
-    __device__ __forceinline__ int tile_r(int r) const { return min(r / h, tr - 1); }
-    __device__ __forceinline__ int tile_c(int c) const { return min(c / w, tc - 1); }
-    __device__ __forceinline__ int center_row(int ti) const {
+    __host__ __device__ __forceinline__ int tile_r(int r) const { return min(r / h, tr - 1); }
+    __host__ __device__ __forceinline__ int tile_c(int c) const { return min(c / w, tc - 1); }
+    __host__ __device__ __forceinline__ int center_row(int ti) const {
         const int r0 = ti * h, r1 = min(r0 + h, er) - 1;
         return (r0 + r1) >> 1;
     }
-    __device__ __forceinline__ int center_col(int tj) const {
+    __host__ __device__ __forceinline__ int center_col(int tj) const {
         const int c0 = tj * w, c1 = min(c0 + w, ec) - 1;
         return (c0 + c1) >> 1;
     }

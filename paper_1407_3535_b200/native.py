@@ -121,6 +121,8 @@ SIGNATURES = {
                                           C.POINTER(EgsIter), _I, _D]),
     "tm_blur": (C.c_int, [_P, _P, _D, C.c_int, _D]),
     "tm_blur_fidelity_map": (C.c_int, [_P, _P, _P, C.c_int, C.c_int, _D]),
+    "tm_unblur_violations": (C.c_int, [_P, _P, _P, _D, C.c_int, C.c_int, C.c_double, _D,
+                                       C.POINTER(C.c_int64)]),
     "tm_prepare": (C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(MatchParams), C.POINTER(_P)]),
     "tm_prep_get_info": (C.c_int, [_P, C.POINTER(PrepInfo)]),
     "tm_prep_download": (C.c_int, [_P, _P, _D, _D]),
