@@ -592,8 +592,14 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
     CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
     if (img->integer) {
+        const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
-        if (tmk::autocorr_two_pass_supported(n, g) && hbytes <= (size_t(16) << 30)) {
+        if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
+            ctx->acH.ensure(vbytes / sizeof(int));
+            CK(tmk::autocorr_u8_colwalk(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
+                                        reinterpret_cast<unsigned*>(ctx->acH.p), ctx->s));
+            ctx->add(3);
+        } else if (tmk::autocorr_two_pass_supported(n, g) && hbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(hbytes / sizeof(int));
             CK(tmk::autocorr_u8_two_pass(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
                                          ctx->acH.p, ctx->s));

@@ -189,107 +189,141 @@ __global__ void __launch_bounds__(kAcRows)
     const int y_e = wr + (k1 - 1) * W + n;    // last window-end event
     const int c_lo = y_s - wr;                // staged columns [c_lo, c_lo + swid)
     const int swid = (y_e + W) - c_lo + wr + 1;
-    const int r_lo = x0 + min(0, di);         // staged rows [r_lo, r_lo + srow)
+    const int r_lo = x0 + min(0, di);         // staged rows [r_lo, r_lo + srow); row srow = 0s
     const int srow = kAcRows + abs(di);
     uint8_t* simg = sm;
-    int* rec = reinterpret_cast<int*>(sm + ((size_t(srow) * spitch + 15) & ~size_t(15)));
-    for (int idx = threadIdx.x; idx < srow * swid; idx += kAcRows) {
-        const int a = idx / swid, b = idx - a * swid;
-        const int r = r_lo + a, c = c_lo + b;
-        simg[a * spitch + b] = (r >= 0 && r < p && c >= 0 && c < q) ? img[size_t(r) * q + c] : 0;
+    int* rec = reinterpret_cast<int*>(sm + ((size_t(srow + 1) * spitch + 15) & ~size_t(15)));
+    // staging: one warp per staged row, 8 independent loads in flight per lane
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int a = wid; a <= srow; a += kAcRows / 32) {
+        const int r = r_lo + a;
+        uint8_t* dst = simg + a * spitch;
+        const bool rok = a < srow && r >= 0 && r < p;
+        const uint8_t* src = img + size_t(rok ? r : 0) * q;
+        for (int b0 = 0; b0 < swid; b0 += 32 * 8) {
+            uint8_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int c = c_lo + b0 + u * 32 + lane;
+                v[u] = (rok && c >= 0 && c < q) ? __ldg(src + c) : uint8_t(0);
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const int b = b0 + u * 32 + lane;
+                if (b < swid) dst[b] = v[u];
+            }
+        }
     }
     __syncthreads();
     const int x = x0 + threadIdx.x;
     const bool row_ok = x < p && x + di >= 0 && x + di < p;
-    // local column index of image column c is c - c_lo
-    const uint8_t* ra = simg + (x - r_lo) * spitch - c_lo;
-    const uint8_t* rb = simg + (x + di - r_lo) * spitch - c_lo;
-    // ring slot of column c is (c - y_s + wr) mod W: static (s + t) % W inside a block
+    // invalid rows read the zero row, so the walk needs no per-pixel guards
+    const uint8_t* ra = simg + (row_ok ? (x - r_lo) : srow) * spitch - c_lo;
+    const uint8_t* rb = simg + (row_ok ? (x + di - r_lo) : srow) * spitch - c_lo;
     int acc[W];
     int rg[W];
 #pragma unroll
     for (int t = 0; t < W; ++t) {
         acc[t] = 0;
-        rg[t] = (t < W - 1 && row_ok) ? int(rb[y_s - wr + t]) : 0;
+        rg[t] = (t < W - 1) ? int(rb[y_s - wr + t]) : 0;
     }
-    const size_t plane = size_t(tc) * p;  // one (di,dj) plane of H
+    const size_t plane = size_t(tc) * p;
+    unsigned* hout = H + size_t(dii) * W * plane + size_t(x);
+    int* recp = rec + threadIdx.x;
+    constexpr int kEndS = (wr + (W > 0 ? 0 : 0)) + 0;  // placeholder to keep W-dependent names
+    (void)kEndS;
+    const int end_s = (wr + n) % W;
+    // centre k opens at y = wr + k*W (slot k % ring) and closes at y = wr + k*W + n
+    int open_k = k0, open_slot = k0 % ring;
+    int close_k = k0, close_slot = k0 % ring;
+    const int first_close = wr + k0 * W + n;
     for (int y0 = y_s; y0 <= y_e; y0 += W) {
 #pragma unroll
         for (int s = 0; s < W; ++s) {
             const int y = y0 + s;
-            // events use the prefix before P(y) is added
-            if (s == wr) {  // window start of centre k = (y - wr) / W
-                const int k = (y - wr) / W;
-                if (k < k1) {
-                    const int slot = k % ring;
+            if (s == wr && open_k < k1) {  // window start: record the prefix before P(y)
 #pragma unroll
-                    for (int t = 0; t < W; ++t) rec[(slot * W + t) * kAcRows + threadIdx.x] = acc[t];
-                }
+                for (int t = 0; t < W; ++t) recp[(open_slot * W + t) * kAcRows] = acc[t];
+                ++open_k;
+                if (++open_slot == ring) open_slot = 0;
             }
-            if (s == (wr + n) % W) {  // window end of centre k = (y - n - wr) / W
-                const int kk = y - n - wr;
-                if (kk >= k0 * W && kk < k1 * W) {
-                    const int k = kk / W;
-                    const int slot = k % ring;
-                    if (x < p) {
+            if (s == end_s && y >= first_close && close_k < k1) {  // window end
+                if (x < p) {
 #pragma unroll
-                        for (int t = 0; t < W; ++t)
-                            H[(size_t(dii) * W + t) * plane + size_t(k) * p + x] =
-                                unsigned(acc[t] - rec[(slot * W + t) * kAcRows + threadIdx.x]);
-                    }
+                    for (int t = 0; t < W; ++t)
+                        hout[size_t(t) * plane + size_t(close_k) * p] =
+                            unsigned(acc[t] - recp[(close_slot * W + t) * kAcRows]);
                 }
+                ++close_k;
+                if (++close_slot == ring) close_slot = 0;
             }
-            rg[(s + W - 1) % W] = row_ok ? int(rb[y + wr]) : 0;  // I(x+di, y+wr)
-            const int a = row_ok ? int(ra[y]) : 0;
+            rg[(s + W - 1) % W] = int(rb[y + wr]);  // I(x+di, y+wr)
+            const int a = int(ra[y]);
 #pragma unroll
             for (int t = 0; t < W; ++t) acc[t] += a * rg[(s + t) % W];  // dj = t - wr
         }
     }
 }
 
-// Clipped last centre column (irregular position): direct n-wide sums.
+// Clipped last centre column (irregular position): one warp per (offset, row), lanes
+// over the n template columns, exact integer warp reduction.
 __global__ void k_ac_rows_last(const uint8_t* __restrict__ img, int p, int q, int n, int h, int w,
                                int cc, int kcol, int tc, unsigned* __restrict__ H) {
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
-    const int oi = blockIdx.y;  // (di, dj) raster index in [0, h*w)
-    const int di = oi / w - h / 2, dj = oi % w - w / 2;
-    if (x >= p) return;
-    int s = 0;
-    if (x + di >= 0 && x + di < p) {
-        const uint8_t* ra = img + size_t(x) * q + cc;
-        const uint8_t* rb = img + size_t(x + di) * q + cc + dj;
-        for (int b = 0; b < n; ++b) {
-            const int cb = cc + dj + b;
-            s += int(ra[b]) * ((cb >= 0 && cb < q) ? int(rb[b]) : 0);
-        }
-    }
-    H[size_t(oi) * tc * p + size_t(kcol) * p + x] = unsigned(s);
-}
-
-// In-place inclusive prefix along x of every (offset, centre column) line (wrapping u32).
-__global__ void k_ac_scan(unsigned* __restrict__ H, int p, long long lines) {
     const int lane = threadIdx.x & 31;
-    const long long warp = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
-    for (long long li = warp; li < lines; li += nwarps) {
-        unsigned* L = H + li * p;
-        unsigned carry = 0;
-        for (int x0 = 0; x0 < p; x0 += 32) {
-            const int x = x0 + lane;
-            unsigned v = x < p ? L[x] : 0u;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
-                if (lane >= o) v += u;
+    const long long wg = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
+    const long long items = (long long)h * w * p;
+    const long long nw = (gridDim.x * (long long)blockDim.x) >> 5;
+    for (long long it = wg; it < items; it += nw) {
+        const int oi = int(it / p), x = int(it % p);
+        const int di = oi / w - h / 2, dj = oi % w - w / 2;
+        int s = 0;
+        if (x + di >= 0 && x + di < p) {
+            const uint8_t* ra = img + size_t(x) * q + cc;
+            const uint8_t* rb = img + size_t(x + di) * q;
+            for (int b = lane; b < n; b += 32) {
+                const int cb = cc + dj + b;
+                s += int(ra[b]) * ((cb >= 0 && cb < q) ? int(rb[cb]) : 0);
             }
-            v += carry;
-            if (x < p) L[x] = v;
-            carry = __shfl_sync(0xffffffffu, v, 31);
         }
+        s = warp_sum(s);
+        if (lane == 0) H[(size_t(oi) * tc + kcol) * p + x] = unsigned(s);
     }
 }
 
-// Epilogue: thread = (offset, centre row ti, centre column k), lanes over k.
+// Inclusive prefix over rows of 32 consecutive (offset, centre column) lines per CTA,
+// transposed on the way out: H[oi][k][x] -> P[oi][x][k] (k fastest), wrapping u32.
+__global__ void __launch_bounds__(1024)
+    k_ac_scan(const unsigned* __restrict__ H, unsigned* __restrict__ P, int p, int tc, int hw) {
+    __shared__ unsigned tile[32][33];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int kblocks = (tc + 31) / 32;
+    const int oi = blockIdx.x / kblocks, k0 = (blockIdx.x % kblocks) * 32;
+    if (oi >= hw) return;
+    const int k = k0 + wid;  // this warp's line
+    const unsigned* L = H + (size_t(oi) * tc + min(k, tc - 1)) * p;
+    unsigned* out = P + size_t(oi) * p * tc;
+    unsigned carry = 0;
+    for (int x0 = 0; x0 < p; x0 += 32) {
+        const int x = x0 + lane;
+        unsigned v = (x < p && k < tc) ? L[x] : 0u;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        v += carry;
+        carry = __shfl_sync(0xffffffffu, v, 31);
+        tile[wid][lane] = v;
+        __syncthreads();
+        // warp wid writes row x0+wid: 32 consecutive k
+        const int xr = x0 + wid, kk = k0 + lane;
+        if (xr < p && kk < tc) out[size_t(xr) * tc + kk] = tile[lane][wid];
+        __syncthreads();
+    }
+}
+
+// Epilogue: thread = (offset, centre row ti, centre column k), lanes over k; reads the
+// transposed prefix P[oi][x][k] coalesced.
 __global__ void __launch_bounds__(256)
     k_ac_epi(const unsigned* __restrict__ P, int p, int m, int n, Grid g, DevStats st, double thr,
              double* __restrict__ map, unsigned long long* n_r) {
@@ -314,8 +348,8 @@ __global__ void __launch_bounds__(256)
         const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
         const int mr = cr + di, mc = cc + dj;
         if (mr < r0 || mr > r1 || mc < c0 || mc > c1) continue;  // not this group's member
-        const unsigned* L = P + (size_t(oi) * g.tc + k) * p;
-        const unsigned S = L[cr + m - 1] - (cr > 0 ? L[cr - 1] : 0u);
+        const unsigned* L = P + size_t(oi) * p * g.tc + k;
+        const unsigned S = L[size_t(cr + m - 1) * g.tc] - (cr > 0 ? L[size_t(cr - 1) * g.tc] : 0u);
         const size_t kc = size_t(cr) * g.ec + cc, km = size_t(mr) * g.ec + mc;
         double v = 0.0;
         if (!st.flat[kc] && !st.flat[km]) {
@@ -327,6 +361,206 @@ __global__ void __launch_bounds__(256)
     }
     local = warp_sum(local);
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_r, local);
+}
+
+// ---- column-walk R_co (preferred path) -----------------------------------------------
+//
+// Pass 1 (k_acv<H>): thread = (image column y, column offset dj, segment of centre rows).
+// It walks down the rows once; lanes are consecutive columns, so every load is coalesced
+// and no staging is needed.  A register ring holds I(x+di, y+dj) for the h row offsets
+// di, so a row step costs two byte loads and h integer MACs accumulated as running
+// prefixes R_di(x).  At a centre row cr the prefixes are recorded (shared-memory ring);
+// at x = cr + m the vertical window sums V[di,dj](ti, y) = R_di(cr+m) - R_di(cr) are
+// written (coalesced).  Centre rows are cr_ti = hr + ti*h, so with the walk aligned to
+// multiples of H every ring index and event position is static in an H-step block.
+// Pass 2 (k_ac_hline): one warp per (offset, centre row): the V line is scanned along y in
+// shared memory (per-lane chunks + warp scan), then S = P[cc+n-1] - P[cc-1] for every
+// centre column and the FP64 epilogue / retained count.  V layout [di][dj][ti][y].
+constexpr int kAcvThreads = 128;
+
+template <int H, int D>
+__global__ void __launch_bounds__(kAcvThreads)
+    k_acv(const uint8_t* __restrict__ img, int p, int q, int m, int W, int trr, int tr,
+          int seg, unsigned* __restrict__ V) {
+    constexpr int hr = H / 2;
+    constexpr int P = D * H;  // prefetch distance in rows (a multiple of H)
+    const int y = blockIdx.x * kAcvThreads + threadIdx.x;
+    const int t = blockIdx.y;  // dj index
+    const int dj = t - W / 2;
+    const int ti0 = blockIdx.z * seg, ti1 = min(ti0 + seg, trr);
+    if (ti0 >= ti1) return;
+    const int yb = y + dj;
+    const bool col_ok = y < q && yb >= 0 && yb < q;
+    const bool a_ok = y < q;
+    const uint8_t* ca = img + (a_ok ? y : 0);
+    const uint8_t* cb = img + (col_ok ? yb : 0);
+    auto A = [&](int x) -> int { return (a_ok && x < p) ? int(__ldg(ca + size_t(x) * q)) : 0; };
+    auto B = [&](int x) -> int {
+        return (col_ok && x >= 0 && x < p) ? int(__ldg(cb + size_t(x) * q)) : 0;
+    };
+    const int x_s = ti0 * H;
+    const int x_e = hr + (ti1 - 1) * H + m;
+    int acc[H];
+    int rg[H];
+#pragma unroll
+    for (int d = 0; d < H; ++d) {
+        acc[d] = 0;
+        rg[d] = (d < H - 1) ? B(x_s - hr + d) : 0;  // rows x_s-hr .. x_s+hr-1 in slots 0..H-2
+    }
+    int pa[P], pb[P];  // loads for the next P rows, issued one superblock ahead
+#pragma unroll
+    for (int j = 0; j < P; ++j) {
+        pa[j] = A(x_s + j);
+        pb[j] = B(x_s + j + hr);
+    }
+    const size_t plane = size_t(tr) * q;
+    // window-start prefixes are parked in the output slot and turned into the window sum
+    // at the window end (same thread, same address)
+    unsigned* vout = V + size_t(t) * plane + (a_ok ? y : 0);
+    const size_t dplane = size_t(W) * plane;
+    const int end_s = (hr + m) % H;
+    const int first_close = hr + ti0 * H + m;
+    int open_t = ti0, close_t = ti0;
+    for (int x0 = x_s; x0 <= x_e; x0 += P) {
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            constexpr int dummy = 0;
+            (void)dummy;
+            const int s = j % H;
+            const int x = x0 + j;
+            if (s == hr && open_t < ti1) {  // window start (prefix before row x)
+                if (a_ok) {
+#pragma unroll
+                    for (int d = 0; d < H; ++d)
+                        vout[size_t(d) * dplane + size_t(open_t) * q] = unsigned(acc[d]);
+                }
+                ++open_t;
+            }
+            if (s == end_s && x >= first_close && close_t < ti1) {  // window end
+                if (a_ok) {
+#pragma unroll
+                    for (int d = 0; d < H; ++d) {
+                        unsigned* slot = vout + size_t(d) * dplane + size_t(close_t) * q;
+                        *slot = unsigned(acc[d]) - *slot;
+                    }
+                }
+                ++close_t;
+            }
+            rg[(s + H - 1) % H] = pb[j];  // I(x+hr, y+dj)
+            const int a = pa[j];
+            pa[j] = A(x + P);
+            pb[j] = B(x + P + hr);
+#pragma unroll
+            for (int d = 0; d < H; ++d) acc[d] += a * rg[(s + d) % H];  // di = d - hr
+        }
+    }
+}
+
+// Clipped last centre row (irregular position): thread = (column y, dj, di).
+__global__ void k_acv_last(const uint8_t* __restrict__ img, int p, int q, int m, int h, int w,
+                           int cr, int tlast, int tr, unsigned* __restrict__ V) {
+    const int y = blockIdx.x * blockDim.x + threadIdx.x;
+    const int t = blockIdx.y, d = blockIdx.z;
+    const int dj = t - w / 2, di = d - h / 2;
+    if (y >= q) return;
+    const int yb = y + dj;
+    unsigned acc = 0;
+    if (yb >= 0 && yb < q) {
+        const int a0 = max(0, -(cr + di)), a1 = min(m, p - (cr + di));
+        const uint8_t* ca = img + size_t(cr) * q + y;
+        const uint8_t* cb = img + size_t(cr + di) * q + yb;
+#pragma unroll 8
+        for (int a = a0; a < a1; ++a)
+            acc += unsigned(__ldg(ca + size_t(a) * q)) * unsigned(__ldg(cb + size_t(a) * q));
+    }
+    V[((size_t(d) * w + t) * tr + tlast) * q + y] = acc;
+}
+
+// Pass 2: CTA per (centre row ti, row offset di, column tile [c0, c0+tw)).  For fixed
+// (ti, di) the members of all groups in the tile row form one contiguous extent row
+// mr = cr + di, so statistics loads and map writes are coalesced.  The W lines
+// V[di,dj](ti, .) over [c0-1, c0+tw+n-1) are first prefix-summed (one warp per line,
+// warp scans) into shared memory; then S = L_dj[cc+n-1] - L_dj[cc-1] and the FP64
+// epilogue (autocorr.cpp:84-88) + retained count (egs.cpp:12-25) per member.
+__global__ void __launch_bounds__(128)
+    k_ac_hrow(const unsigned* __restrict__ V, int q, int m, int n, Grid g, DevStats st,
+              double thr, double* __restrict__ map, unsigned long long* n_r, int tw, int lpitch) {
+    extern __shared__ __align__(16) unsigned lines[];  // W lines x lpitch
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int ti = blockIdx.x, dii = blockIdx.y;
+    const int c0 = blockIdx.z * tw;  // multiple of w: every tile here starts at or after c0
+    const int hr = g.h / 2, wr = g.w / 2;
+    const int di = dii - hr;
+    const int cr = g.center_row(ti);
+    const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+    const int mr = cr + di;
+    if (mr < r0 || mr > r1 || c0 >= g.ec) return;  // uniform across the CTA
+    const int c1 = min(c0 + tw, g.ec);
+    const int len = (c1 - c0) + n;  // local index u <-> column c0 - 1 + u
+    // 1. prefix of each dj line over the tile (+ one column before, n-1 after)
+    for (int t = wid; t < g.w; t += blockDim.x / 32) {
+        const unsigned* src = V + ((size_t(dii) * g.w + t) * g.tr + ti) * q;
+        unsigned* L = lines + size_t(t) * lpitch;
+        unsigned carry = 0;
+        for (int u0 = 0; u0 < len; u0 += 32) {
+            const int u = u0 + lane;
+            const int c = c0 - 1 + u;
+            unsigned v = (u < len && c >= 0 && c < q) ? __ldg(src + c) : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned x = __shfl_up_sync(0xffffffffu, v, o);
+                if (lane >= o) v += x;
+            }
+            v += carry;
+            if (u < len) L[u] = v;
+            carry = __shfl_sync(0xffffffffu, v, 31);
+        }
+    }
+    __syncthreads();
+    // 2. members of row mr in [c0, c1)
+    const double mn = double(m) * double(n);
+    unsigned long long local = 0;
+    for (int c = c0 + threadIdx.x; c < c1; c += blockDim.x) {
+        const int k = g.tile_c(c);
+        const int cc = g.center_col(k);
+        const int dj = c - cc;
+        const size_t km = size_t(mr) * g.ec + c;
+        if (di == 0 && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
+            map[km] = 1.0;
+            continue;
+        }
+        const unsigned* L = lines + size_t(dj + wr) * lpitch;
+        const unsigned S = L[cc + n - c0] - L[cc - c0];  // P[cc+n-1] - P[cc-1]
+        const size_t kc = size_t(cr) * g.ec + cc;
+        double v = 0.0;
+        if (!st.flat[kc] && !st.flat[km]) {
+            const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, st.mu[kc]), st.mu[km]));
+            v = dclamp(__ddiv_rn(num, __dmul_rn(st.omega[kc], st.omega[km])), -1.0, 1.0);
+        }
+        map[km] = v;
+        if (v < thr) ++local;
+    }
+    local = warp_sum(local);
+    if (lane == 0 && local) atomicAdd(n_r, local);
+}
+
+template <int H>
+cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int trr, int tr,
+                       unsigned* V, cudaStream_t s) {
+    constexpr int D = H == 1 ? 16 : (H == 3 ? 8 : (H == 5 ? 4 : (H == 7 ? 3 : 2)));
+    // segments of centre rows: enough CTAs for ~4 waves, at least 2*m rows of walk each
+    const int colblocks = (q + kAcvThreads - 1) / kAcvThreads;
+    int nseg = std::max(1, (148 * 16) / std::max(1, colblocks * w));
+    int seg = std::max((2 * m) / H + 1, (trr + nseg - 1) / nseg);
+    nseg = (trr + seg - 1) / seg;
+    dim3 grid(colblocks, w, nseg);
+    if (trr > 0) k_acv<H, D><<<grid, kAcvThreads, 0, s>>>(img, p, q, m, w, trr, tr, seg, V);
+    return cudaGetLastError();
+}
+
+bool acv_supported(int m, int h) {
+    (void)m;
+    return h <= 11 && h % 2 == 1;
 }
 
 struct AcRowsGeom {
@@ -343,7 +577,7 @@ AcRowsGeom ac_rows_geom(int n, int h) {
     int pitch = (swid + 3) & ~3;
     if (((pitch / 4) & 1) == 0) pitch += 4;  // rows 4 mod 8 bytes apart: no bank conflicts
     g.spitch = pitch;
-    const int srow = kAcRows + h / 2;
+    const int srow = kAcRows + h / 2 + 1;  // + the zero row
     g.smem = ((size_t(srow) * pitch + 15) & ~size_t(15)) + size_t(g.ring) * W * kAcRows * 4;
     return g;
 }
@@ -385,7 +619,8 @@ __global__ void k_autocorr_init(double* map, Grid g) {
     const size_t E = size_t(g.er) * g.ec;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
          k += size_t(gridDim.x) * blockDim.x) {
-        const int r = int(k / g.ec), c = int(k % g.ec);
+        int r, c;
+        g.rc(k, r, c);
         const int ti = g.tile_r(r), tj = g.tile_c(c);
         map[k] = (g.center_row(ti) == r && g.center_col(tj) == c) ? 1.0 : 0.0;
     }
@@ -425,7 +660,8 @@ __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
     unsigned long long local = 0;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
          k += size_t(gridDim.x) * blockDim.x) {
-        const int r = int(k / g.ec), c = int(k % g.ec);
+        int r, c;
+        g.rc(k, r, c);
         const int ti = g.tile_r(r), tj = g.tile_c(c);
         if (g.center_row(ti) == r && g.center_col(tj) == c) continue;
         if (map[k] < thr) ++local;
@@ -434,7 +670,7 @@ __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_r, local);
 }
 
-Grid to_grid(GridDesc d) { return Grid{d.er, d.ec, d.h, d.w, d.tr, d.tc}; }
+Grid to_grid(GridDesc d) { return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc); }
 
 }  // namespace
 
@@ -490,11 +726,58 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
     return cudaGetLastError();
 }
 
-size_t autocorr_rowsum_bytes(int p, GridDesc g) {
-    return size_t(g.h) * g.w * g.tc * p * sizeof(unsigned);
+size_t autocorr_rowsum_bytes(int p, GridDesc g) {  // H and its transposed prefix P
+    return 2 * size_t(g.h) * g.w * g.tc * p * sizeof(unsigned);
 }
 
 bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h, g.w); }
+
+size_t autocorr_colwalk_bytes(int q, GridDesc g) {
+    return size_t(g.h) * g.w * g.tr * q * sizeof(unsigned);
+}
+
+bool autocorr_colwalk_supported(int m, int q, GridDesc g) {
+    (void)q;
+    return acv_supported(m, g.h) && g.w <= 11;
+}
+
+cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
+                                DevStats st, double retain_threshold, double* map,
+                                unsigned long long* n_r, unsigned* V, cudaStream_t s) {
+    const bool clipped = size_t(gd.tr) * gd.h > size_t(gd.er);
+    const int trr = clipped ? gd.tr - 1 : gd.tr;
+    cudaError_t e = cudaSuccess;
+    switch (gd.h) {
+        case 1: e = launch_acv<1>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 3: e = launch_acv<3>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 5: e = launch_acv<5>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 7: e = launch_acv<7>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 9: e = launch_acv<9>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 11: e = launch_acv<11>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        default: return cudaErrorInvalidValue;
+    }
+    if (e != cudaSuccess) return e;
+    const Grid g = to_grid(gd);
+    if (clipped) {
+        dim3 grid((q + 127) / 128, gd.w, gd.h);
+        k_acv_last<<<grid, 128, 0, s>>>(img, p, q, m, gd.h, gd.w, g.center_row(gd.tr - 1),
+                                        gd.tr - 1, gd.tr, V);
+    }
+    // column tiles: a multiple of w, sized so the W prefix lines fit in ~64 KB
+    int tw = std::max(gd.w, (384 / gd.w) * gd.w);
+    tw = std::min(tw, (gd.ec + gd.w - 1) / gd.w * gd.w);
+    const int lpitch = ((tw + n + 1) + 3) & ~3;
+    const size_t smem = size_t(gd.w) * lpitch * sizeof(unsigned);
+    if (smem > 200 * 1024) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_ac_hrow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    dim3 grid(gd.tr, gd.h, (gd.ec + tw - 1) / tw);
+    k_ac_hrow<<<grid, 128, smem, s>>>(V, q, m, n, g, st, retain_threshold, map, n_r, tw, lpitch);
+    return cudaGetLastError();
+}
 
 cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
                                  DevStats st, double retain_threshold, double* map,
@@ -515,15 +798,17 @@ cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n,
     if (e != cudaSuccess) return e;
     const Grid g = to_grid(gd);
     if (clipped) {
-        dim3 grid((p + 127) / 128, gd.h * gd.w);
-        k_ac_rows_last<<<grid, 128, 0, s>>>(img, p, q, n, gd.h, gd.w, g.center_col(gd.tc - 1),
-                                            gd.tc - 1, gd.tc, H);
+        const long long items = (long long)gd.h * gd.w * p;
+        const int blocks = int(std::min<long long>((items * 32 + 255) / 256, 148 * 32));
+        k_ac_rows_last<<<blocks, 256, 0, s>>>(img, p, q, n, gd.h, gd.w, g.center_col(gd.tc - 1),
+                                              gd.tc - 1, gd.tc, H);
     }
-    const long long lines = (long long)gd.h * gd.w * gd.tc;
-    k_ac_scan<<<int(std::min<long long>((lines + 7) / 8, 148 * 32)), 256, 0, s>>>(H, p, lines);
-    const long long items = (long long)gd.h * gd.w * gd.tr * gd.tc;
+    const int hw = gd.h * gd.w;
+    unsigned* P = H + size_t(hw) * gd.tc * p;  // second half of the scratch
+    k_ac_scan<<<hw * ((gd.tc + 31) / 32), 1024, 0, s>>>(H, P, p, gd.tc, hw);
+    const long long items = (long long)hw * gd.tr * gd.tc;
     const int blocks = int(std::min<long long>((items + 255) / 256, 148 * 32));
-    k_ac_epi<<<blocks, 256, 0, s>>>(H, p, m, n, g, st, retain_threshold, map, n_r);
+    k_ac_epi<<<blocks, 256, 0, s>>>(P, p, m, n, g, st, retain_threshold, map, n_r);
     return cudaGetLastError();
 }
 

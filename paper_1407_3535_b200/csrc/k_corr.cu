@@ -90,13 +90,26 @@ __global__ void __launch_bounds__(NW * 32)
 
     for (int i0 = 0; i0 < job.m; i0 += kIC) {
         __syncthreads();
-        // stage image rows [r_first + i0, r_first + i0 + span), columns [cstart, +width)
-        const int total = span * width;
-        for (int idx = threadIdx.x; idx < total; idx += NW * 32) {
-            const int a = idx / width, b = idx - a * width;
-            const int gr = r_first + i0 + a, gc = cstart + b;
-            simg[a * spitch + b] =
-                (gr < p_rows && gc < q_cols) ? job.imgf[size_t(gr) * job.pitch + gc] : 0.f;
+        // stage image rows [r_first + i0, r_first + i0 + span), columns [cstart, +width):
+        // one warp per row, 8 independent coalesced loads in flight per lane
+        for (int a = wid; a < span; a += NW) {
+            const int gr = r_first + i0 + a;
+            const bool rok = gr < p_rows;
+            const float* src = job.imgf + size_t(rok ? gr : 0) * job.pitch;
+            float* dst = simg + a * spitch;
+            for (int b0 = 0; b0 < width; b0 += 32 * 8) {
+                float v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int gc = cstart + b0 + u * 32 + lane;
+                    v[u] = (rok && gc < q_cols) ? __ldg(src + gc) : 0.f;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const int b = b0 + u * 32 + lane;
+                    if (b < width) dst[b] = v[u];
+                }
+            }
         }
         for (int idx = threadIdx.x; idx < kIC * job.npad; idx += NW * 32) {
             const int a = idx / job.npad, b = idx - a * job.npad;
@@ -331,8 +344,9 @@ __global__ void __launch_bounds__(256)
          base += size_t(gridDim.x) * blockDim.x) {
         const size_t k = base + threadIdx.x;
         bool survivor = false;
+        int r = 0, c = 0;
         if (k < E) {
-            const int r = int(k / g.ec), c = int(k % g.ec);
+            g.rc(k, r, c);
             const int ti = g.tile_r(r), tj = g.tile_c(c);
             const bool centre = g.center_row(ti) == r && g.center_col(tj) == c;
             if (centre) {
@@ -364,7 +378,7 @@ __global__ void __launch_bounds__(256)
             basepos = __shfl_sync(0xffffffffu, basepos, 0);
             if (survivor) {
                 const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
-                if (pos < max_locs) locs[pos] = make_int2(int(k / g.ec), int(k % g.ec));
+                if (pos < max_locs) locs[pos] = make_int2(r, c);
             }
         }
     }
@@ -512,7 +526,7 @@ __global__ void k_seq_final(Grid g, const int2* __restrict__ locs, const unsigne
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
 }
 
-Grid to_grid(GridDesc d) { return Grid{d.er, d.ec, d.h, d.w, d.tr, d.tc}; }
+Grid to_grid(GridDesc d) { return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc); }
 
 template <int SW, int NW>
 cudaError_t launch_band(const CorrJob& job, const BandTask& task, CellH* partials, int* n_partials,

@@ -91,6 +91,12 @@ bool autocorr_two_pass_supported(int n, GridDesc g);
 cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
                                  DevStats st, double retain_threshold, double* map,
                                  unsigned long long* n_r, int* H, cudaStream_t s);
+// Column-walk variant (preferred): V scratch of autocorr_colwalk_bytes(q, g) bytes.
+size_t autocorr_colwalk_bytes(int q, GridDesc g);
+bool autocorr_colwalk_supported(int m, int q, GridDesc g);
+cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
+                                DevStats st, double retain_threshold, double* map,
+                                unsigned long long* n_r, unsigned* V, cudaStream_t s);
 // replica path, one offset: cross-sum prefix table of the product image for (di,dj).
 cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
                                      GridDesc g, DevStats st, int di, int dj, double* map,

@@ -128,12 +128,56 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+// Exact unsigned division by a runtime constant without the XU pipe: floor(x / d) =
+// umulhi64(x, ceil(2^64 / d)) for every 32-bit x (the error term x*eps/2^64 < 1/d).
+struct FastDiv {
+    unsigned long long magic;  // 0 encodes d == 1
+    __host__ __device__ static FastDiv make(unsigned d) {
+        FastDiv f;
+        f.magic = d <= 1 ? 0ull : (~0ull) / d + 1ull;
+        return f;
+    }
+    __host__ __device__ __forceinline__ unsigned div(unsigned x) const {
+#ifdef __CUDA_ARCH__
+        return magic ? unsigned(__umul64hi((unsigned long long)x, magic)) : x;
+#else
+        return magic ? unsigned(((unsigned __int128)x * magic) >> 64) : x;
+#endif
+    }
+};
+
 // Group geometry (autocorr.cpp:12-32): tiles anchored at (0,0), clipped edge tiles,
-// centre = (r0 + r1) / 2.
+// centre = (r0 + r1) / 2.  fh/fw/fec divide by h, w and ec on the fast path.
 struct Grid {
     int er, ec, h, w, tr, tc;
-    __host__ __device__ __forceinline__ int tile_r(int r) const { return min(r / h, tr - 1); }
-    __host__ __device__ __forceinline__ int tile_c(int c) const { return min(c / w, tc - 1); }
+    FastDiv fh, fw, fec;
+    __host__ static Grid make(int er, int ec, int h, int w, int tr, int tc) {
+        return Grid{er, ec, h, w, tr, tc, FastDiv::make(unsigned(h)), FastDiv::make(unsigned(w)),
+                    FastDiv::make(unsigned(ec))};
+    }
+    __host__ __device__ __forceinline__ int tile_r(int r) const {
+#ifdef __CUDA_ARCH__
+        return min(int(fh.div(r)), tr - 1);
+#else
+        return r / h < tr - 1 ? r / h : tr - 1;
+#endif
+    }
+    __host__ __device__ __forceinline__ int tile_c(int c) const {
+#ifdef __CUDA_ARCH__
+        return min(int(fw.div(c)), tc - 1);
+#else
+        return c / w < tc - 1 ? c / w : tc - 1;
+#endif
+    }
+    // linear extent index -> (row, col)
+    __host__ __device__ __forceinline__ void rc(size_t k, int& r, int& c) const {
+#ifdef __CUDA_ARCH__
+        r = int(fec.div(unsigned(k)));
+#else
+        r = int(k / size_t(ec));
+#endif
+        c = int(k) - r * ec;
+    }
     __host__ __device__ __forceinline__ int center_row(int ti) const {
         const int r0 = ti * h, r1 = min(r0 + h, er) - 1;
         return (r0 + r1) >> 1;
