@@ -218,6 +218,33 @@ int tm_refine_localization(tm_ctx* ctx, const double* tmpl, int m, int n, tm_ima
 int tm_match(tm_ctx* ctx, const double* tmpl, int m, int n, const double* image, int rows,
              int cols, const tm_match_params* params, tm_match_result* out, uint8_t* visits);
 
+/* ---- row-strip sharding (multi-GPU) ------------------------------------
+ * Rank r of W processes the group rows [floor(r*tr/W), floor((r+1)*tr/W)) of the grid; the
+ * host exchanges the few scalars between the phases (paper_1407_3535_b200/distributed.py):
+ *   EGS:    tm_strip_autocorr per candidate -> allreduce SUM n_r -> egs.cpp:61-88 decision
+ *           -> tm_strip_commit of the accepted candidate;
+ *   search: tm_strip_search_begin (scan 1, local threshold) -> allreduce MAX ->
+ *           [seeded: tm_strip_search_seed -> allreduce MAX] -> tm_strip_search_finish ->
+ *           allgather of tm_strip_part -> better_candidate merge, sums of the counts.
+ * Frozen and seeded policies only (the sequential threshold is a single global scan). */
+typedef struct {
+    double best_rho;
+    int32_t best_row, best_col, best_flags; /* flags: bit0 valid, bit1 degenerate */
+    int32_t _pad0;
+    int64_t centers, eliminated, retained;
+    double final_threshold; /* max(threshold used, best non-degenerate survivor rho) */
+} tm_strip_part;
+
+int tm_strip_autocorr(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w, int rank, int world,
+                      double rho_tb, int slot, int64_t* n_r);
+int tm_strip_commit(tm_ctx* ctx, tm_image* img, int m, int n, int slot, int h, int w,
+                    const tm_match_params* params, const tm_egs_iter* trace, int trace_len,
+                    tm_prep** out);
+int tm_strip_search_begin(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpl,
+                          const tm_match_params* params, int rank, int world, double* T0);
+int tm_strip_search_seed(tm_ctx* ctx, double T, double* T1);
+int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out);
+
 /* Instrumentation: number of kernels this context launched (bench gpu_launches). */
 int64_t tm_ctx_launch_count(const tm_ctx* ctx);
 /* The context's CUDA stream (cudaStream_t) for callers that time or order work on it. */

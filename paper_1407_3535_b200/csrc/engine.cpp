@@ -153,6 +153,13 @@ double ms_between(cudaEvent_t a, cudaEvent_t b) {
 
 }  // namespace
 
+struct Tmpl {
+    int m = 0, n = 0, npad = 0;
+    bool integer = false;
+    tmk::TStatsH ts{};
+    int flush_rows = 0;
+};
+
 // ==== context ========================================================================
 struct WS {
     DBuf<double> mu, om;
@@ -177,13 +184,24 @@ struct tm_ctx {
     DBuf<unsigned long long> counters, rec_key;
     DBuf<int2> locs, seed_locs;
     DBuf<uint8_t> seq_deg, seeded, deg_c, visits;
-    DBuf<double> rho_c, surface;
+    DBuf<double> rho_c, surface, dotbuf;
     DBuf<float> tf;
     DBuf<double> td;
     DBuf<int> rows_list;
     DBuf<double> map_tmp, map_user;
     DBuf<double> egs_maps[3];
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt;
+    // row-strip search protocol state (tm_strip_search_*)
+    struct StripState {
+        bool active = false;
+        tm_prep* prep = nullptr;
+        tm_image* img = nullptr;
+        tmk::GridDesc g{};
+        tm_match_params P{};
+        int policy = TM_POLICY_FROZEN;
+        int m = 0, n = 0;
+        Tmpl T{};
+    } strip;
     void add(int k) { launches += k; }
     // optional per-phase device timing (CUDA events on the context stream)
     bool profiling = false;
@@ -282,7 +300,16 @@ tmk::GridDesc make_grid(int er, int ec, int h, int w) {
     if (er < 1 || ec < 1) invalid("group grid: empty search extent");
     if (h < 1 || w < 1 || h % 2 == 0 || w % 2 == 0)
         invalid("group grid: group size must be odd and >= 1");
-    return tmk::GridDesc{er, ec, h, w, (er + h - 1) / h, (ec + w - 1) / w};
+    const int tr = (er + h - 1) / h, tc = (ec + w - 1) / w;
+    return tmk::GridDesc{er, ec, h, w, tr, tc, 0, tr};
+}
+
+// Row strip `rank` of `world`: an even split of the group rows.
+tmk::GridDesc strip_of(tmk::GridDesc g, int rank, int world) {
+    if (world < 1 || rank < 0 || rank >= world) invalid("strip: bad rank/world");
+    g.ti_lo = int((long long)g.tr * rank / world);
+    g.ti_hi = int((long long)g.tr * (rank + 1) / world);
+    return g;
 }
 
 int centre_row_h(const tmk::GridDesc& g, int ti) {
@@ -400,12 +427,6 @@ WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
 }
 
 // ---- templates ---------------------------------------------------------------------------
-struct Tmpl {
-    int m = 0, n = 0, npad = 0;
-    bool integer = false;
-    tmk::TStatsH ts{};
-    int flush_rows = 0;
-};
 
 // template_stats (stats.cpp:98-111) in reference order, then upload.
 Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n) {
@@ -523,20 +544,28 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const int wr = g.w / 2;
     Phase ph(ctx, "centre_scan");
     if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
-        std::vector<int> rows(g.tr);
-        for (int ti = 0; ti < g.tr; ++ti) rows[ti] = centre_row_h(g, ti);
+        const int nstrip = g.ti_hi - g.ti_lo;
+        if (nstrip <= 0) {
+            reduce_to(ctx, 0, 0);
+            return;
+        }
+        std::vector<int> rows(nstrip);
+        for (int ti = g.ti_lo; ti < g.ti_hi; ++ti) rows[ti - g.ti_lo] = centre_row_h(g, ti);
         upload_rows(ctx, rows);
         const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
         const int nc_reg = clipped ? g.tc - 1 : g.tc;
-        const int np_main = nc_reg > 0 ? band_partials(g.tr, nc_reg, g.w) : 0;
-        const int np_last = clipped ? band_partials(g.tr, 1, 1) : 0;
+        const int np_main = nc_reg > 0 ? band_partials(nstrip, nc_reg, g.w) : 0;
+        const int np_last = clipped ? band_partials(nstrip, 1, 1) : 0;
         ctx->partials.ensure(size_t(np_main + np_last) + 1);
         int n1 = 0, n2 = 0;
         tmk::BandTask t{};
         t.rows = ctx->rows_list.p;
-        t.nrows = g.tr;
+        t.nrows = nstrip;
+        t.yi_base = g.ti_lo;
         t.mode = 1;
         t.row_span = row_span(rows);
+        t.ksplit = 1;
+        t.ms = T.m;
         t.tc = g.tc;
         t.out_rho = ctx->rho_c.p;
         t.out_deg = ctx->deg_c.p;
@@ -545,43 +574,75 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             t.sw = g.w;
             t.nc = nc_reg;
             t.col0 = 0;
-            CK(tmk::corr_band(job, t, ctx->partials.p, &n1, ctx->s));
-            ctx->add(1);
+            // split the template rows across CTAs until the grid covers ~3 waves
+            const int tiles = band_partials(nstrip, nc_reg, g.w);
+            int ks = std::max(1, std::min(8, (148 * 6 * 3) / std::max(1, tiles)));
+            ks = std::min(ks, std::max(1, T.m / 8));
+            if (ks > 1) {
+                t.ksplit = ks;
+                t.ms = ((T.m + ks - 1) / ks + 7) & ~7;
+                t.ksplit = (T.m + t.ms - 1) / t.ms;
+                ctx->dotbuf.ensure(G);
+                CK(cudaMemsetAsync(ctx->dotbuf.p, 0, G * sizeof(double), ctx->s));
+                t.dot = ctx->dotbuf.p;
+                int dummy = 0;
+                CK(tmk::corr_band(job, t, ctx->partials.p, &dummy, ctx->s));
+                n1 = std::min(kListBlocks, int((size_t(nstrip) * nc_reg + 255) / 256));
+                CK(tmk::centre_epilogue(job, g, ctx->rows_list.p, wr, g.w, nc_reg, 0, ctx->dotbuf.p,
+                                        ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s));
+                ctx->add(2);
+                t.ksplit = 1;
+                t.ms = T.m;
+                t.dot = nullptr;
+            } else {
+                t.ksplit = 1;
+                t.ms = T.m;
+                CK(tmk::corr_band(job, t, ctx->partials.p, &n1, ctx->s));
+                ctx->add(1);
+            }
         }
         if (clipped) {
             // the clipped last group column: one centre per group row, list kernel
-            std::vector<int2> last(g.tr);
+            std::vector<int2> last(nstrip);
             const int cc = centre_col_h(g, g.tc - 1);
-            for (int ti = 0; ti < g.tr; ++ti) last[ti] = make_int2(rows[ti], cc);
-            ctx->seed_locs.ensure(size_t(g.tr));
+            for (int i = 0; i < nstrip; ++i) last[i] = make_int2(rows[i], cc);
+            ctx->seed_locs.ensure(size_t(nstrip));
             ctx->pin_locs.upload(ctx->seed_locs.p, last.data(), last.size() * sizeof(int2), ctx->s);
-            const unsigned long long cnt = g.tr;
+            const unsigned long long cnt = nstrip;
             ctx->pin_cnt.upload(ctx->counters.p + 12, &cnt, 8, ctx->s);
-            ctx->seq_rho.ensure(size_t(g.tr));
-            ctx->seq_deg.ensure(size_t(g.tr));
-            n2 = std::min(kListBlocks, (g.tr + 7) / 8);
+            ctx->seq_rho.ensure(size_t(nstrip));
+            ctx->seq_deg.ensure(size_t(nstrip));
+            n2 = std::min(kListBlocks, (nstrip + 7) / 8);
             ctx->partials.ensure(size_t(n1 + n2) + 1);
-            CK(tmk::corr_list(job, ctx->seed_locs.p, ctx->counters.p + 12, g.tr, ctx->seq_rho.p,
+            CK(tmk::corr_list(job, ctx->seed_locs.p, ctx->counters.p + 12, nstrip, ctx->seq_rho.p,
                               ctx->seq_deg.p, ctx->partials.p + n1, n2, ctx->s));
-            CK(tmk::scatter_column(ctx->seq_rho.p, ctx->seq_deg.p, g.tr, g.tc, g.tc - 1,
-                                   ctx->rho_c.p, ctx->deg_c.p, ctx->s));
+            const size_t off = size_t(g.ti_lo) * g.tc;
+            CK(tmk::scatter_column(ctx->seq_rho.p, ctx->seq_deg.p, nstrip, g.tc, g.tc - 1,
+                                   ctx->rho_c.p + off, ctx->deg_c.p + off, ctx->s));
             ctx->add(2);
         }
         reduce_to(ctx, n1 + n2, 0);
         return;
     }
     // general path: explicit centre list in grid order
-    std::vector<int2> locs(G);
-    for (int ti = 0; ti < g.tr; ++ti)
+    const size_t off = size_t(g.ti_lo) * g.tc;
+    const size_t GS = size_t(g.ti_hi - g.ti_lo) * g.tc;
+    std::vector<int2> locs(GS);
+    for (int ti = g.ti_lo; ti < g.ti_hi; ++ti)
         for (int tj = 0; tj < g.tc; ++tj)
-            locs[size_t(ti) * g.tc + tj] = make_int2(centre_row_h(g, ti), centre_col_h(g, tj));
-    ctx->seed_locs.ensure(G);
-    ctx->pin_locs.upload(ctx->seed_locs.p, locs.data(), G * sizeof(int2), ctx->s);
-    unsigned long long cnt = G;
+            locs[size_t(ti - g.ti_lo) * g.tc + tj] =
+                make_int2(centre_row_h(g, ti), centre_col_h(g, tj));
+    if (GS == 0) {
+        reduce_to(ctx, 0, 0);
+        return;
+    }
+    ctx->seed_locs.ensure(GS);
+    ctx->pin_locs.upload(ctx->seed_locs.p, locs.data(), GS * sizeof(int2), ctx->s);
+    unsigned long long cnt = GS;
     CK(cudaMemcpyAsync(ctx->counters.p + 4, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
-    eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(G), ctx->rho_c.p,
-              ctx->deg_c.p, 0);
+    eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(GS), ctx->rho_c.p + off,
+              ctx->deg_c.p + off, 0);
 }
 
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
@@ -885,6 +946,62 @@ struct SearchIn {
     const double* map;  // device
 };
 
+// Scan-2 survivors (listed in ctx->locs, marked 2 in ctx->visits) -> cells[2].  Dense
+// survivor sets run the band kernel masked by the visit map; sparse ones one warp per
+// location.  rho_loc (optional, extent-sized) receives rho by location.
+void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                    const tmk::GridDesc& g, unsigned long long survivors, double* rho_loc) {
+    cudaStream_t s = ctx->s;
+    const size_t E = size_t(g.er) * g.ec;
+    const unsigned long long* count = &ctx->tally.p->survivors;
+    uint8_t* visits = ctx->visits.p;
+    const bool dense = survivors * 16 > E && fp32_path(img, T);
+    if (dense) {
+        const tmk::CorrJob job = make_job(ctx, img, ws, T);
+        const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
+        std::vector<int> rows(std::max(0, rhi - rlo));
+        for (int r = rlo; r < rhi; ++r) rows[r - rlo] = r;
+        upload_rows(ctx, rows);
+        tmk::BandTask t{};
+        t.rows = ctx->rows_list.p;
+        t.nrows = int(rows.size());
+        t.cbase = 0;
+        t.sw = 1;
+        t.nc = g.ec;
+        t.mode = 2;
+        t.row_span = 7;
+        t.ksplit = 1;
+        t.ms = T.m;
+        t.out_rho = rho_loc;
+        t.mask = visits;
+        ctx->partials.ensure(size_t(band_partials(std::max(1, int(rows.size())), g.ec, 1)));
+        int np = 0;
+        {
+            Phase ph(ctx, "survivor_dense");
+            CK(tmk::corr_band(job, t, ctx->partials.p, &np, s));
+            ctx->add(1);
+        }
+        reduce_to(ctx, np, 2);
+    } else if (survivors > 0) {
+        const tmk::CorrJob job = make_job(ctx, img, ws, T);
+        ctx->partials.ensure(kListBlocks);
+        {
+            Phase ph(ctx, "survivor_eval");
+            if (fp32_path(img, T))
+                CK(tmk::corr_list(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
+                                  rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
+            else
+                CK(tmk::corr_list_f64(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
+                                      rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
+            ctx->add(1);
+        }
+        reduce_to(ctx, kListBlocks, 2);
+    } else {
+        reduce_to(ctx, 0, 2);
+    }
+
+}
+
 tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
                        const tm_match_params& P, uint8_t* visits_host) {
     const tmk::GridDesc& g = in.g;
@@ -947,49 +1064,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         ctx->seq_rho.ensure(E);
         rho_loc = ctx->seq_rho.p;
     }
-    // Dense survivors: evaluate whole tiles masked by the visit map (band kernel);
-    // sparse survivors: one warp per listed location.
-    const bool dense = tally.survivors * 16 > E && fp32_path(img, T);
-    if (dense) {
-        const tmk::CorrJob job = make_job(ctx, img, ws, T);
-        std::vector<int> rows(g.er);
-        for (int r = 0; r < g.er; ++r) rows[r] = r;
-        upload_rows(ctx, rows);
-        tmk::BandTask t{};
-        t.rows = ctx->rows_list.p;
-        t.nrows = g.er;
-        t.cbase = 0;
-        t.sw = 1;
-        t.nc = g.ec;
-        t.mode = 2;
-        t.row_span = 7;
-        t.out_rho = rho_loc;
-        t.mask = visits;
-        ctx->partials.ensure(size_t(band_partials(g.er, g.ec, 1)));
-        int np = 0;
-        {
-            Phase ph(ctx, "survivor_dense");
-            CK(tmk::corr_band(job, t, ctx->partials.p, &np, s));
-            ctx->add(1);
-        }
-        reduce_to(ctx, np, 2);
-    } else if (tally.survivors > 0) {
-        const tmk::CorrJob job = make_job(ctx, img, ws, T);
-        ctx->partials.ensure(kListBlocks);
-        {
-            Phase ph(ctx, "survivor_eval");
-            if (fp32_path(img, T))
-                CK(tmk::corr_list(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
-                                  rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
-            else
-                CK(tmk::corr_list_f64(job, ctx->locs.p, count, int(std::min<size_t>(E, INT_MAX)),
-                                      rho_loc, nullptr, ctx->partials.p, kListBlocks, s, 1));
-            ctx->add(1);
-        }
-        reduce_to(ctx, kListBlocks, 2);
-    } else {
-        reduce_to(ctx, 0, 2);
-    }
+    eval_survivors(ctx, img, ws, T, g, tally.survivors, rho_loc);
 
     double final_T = T0;
     if (seq) {
@@ -1118,6 +1193,10 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
         t.nc = ec;
         t.mode = 0;
         t.row_span = 7;
+        t.ksplit = 1;
+        t.ms = T.m;
+        t.ksplit = 1;
+        t.ms = T.m;
         t.out_rho = surface;
         ctx->partials.ensure(size_t(band_partials(er, ec, 1)));
         int np = 0;
@@ -1717,6 +1796,153 @@ int tm_refine_localization(tm_ctx* ctx, const double* tmpl, int m, int n, tm_ima
         *col = c.col;
         *rho = c.rho;
         *degenerate = (c.flags & 2) != 0;
+    });
+}
+
+// ---- row-strip protocol (multi-GPU; orchestrated by paper_1407_3535_b200/distributed.py) ----
+int tm_strip_autocorr(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w, int rank, int world,
+                      double rho_tb, int slot, int64_t* n_r) {
+    return guard(ctx, [&] {
+        if (slot < 0 || slot > 2) invalid("tm_strip_autocorr: slot must be 0..2");
+        if (m > img->p || n > img->q) invalid("efficient_group_size: template does not fit");
+        if (rho_tb < 0.0 || rho_tb > 1.0) invalid("retained_count: rho_tb must be in [0,1]");
+        const tmk::GridDesc g =
+            strip_of(make_grid(img->p - m + 1, img->q - n + 1, h, w), rank, world);
+        WS& ws = get_ws(ctx, img, m, n);
+        ctx->egs_maps[slot].ensure(size_t(g.er) * g.ec);
+        *n_r = autocorr_map(ctx, img, ws, g, expected_elimination_threshold_h(rho_tb),
+                            ctx->egs_maps[slot].p);
+    });
+}
+
+int tm_strip_commit(tm_ctx* ctx, tm_image* img, int m, int n, int slot, int h, int w,
+                    const tm_match_params* params, const tm_egs_iter* trace, int trace_len,
+                    tm_prep** out) {
+    return guard(ctx, [&] {
+        if (slot < 0 || slot > 2) invalid("tm_strip_commit: slot must be 0..2");
+        auto prep = std::make_unique<tm_prep>();
+        prep->params = *params;
+        prep->profile = params_profile(*params);
+        prep->params.kernel_profile = nullptr;
+        prep->mode = TM_MODE_EGS;
+        prep->m = m;
+        prep->n = n;
+        prep->h = h;
+        prep->w = w;
+        prep->source = img;
+        prep->g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        prep->map.swap(ctx->egs_maps[slot]);
+        prep->egs_trace.assign(trace, trace + std::max(0, trace_len));
+        if (trace_len > 0) prep->cost = trace[trace_len - 1];
+        prep->prep_ms = 0.0;
+        *out = prep.release();
+    });
+}
+
+int tm_strip_search_begin(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpl,
+                          const tm_match_params* params, int rank, int world, double* T0) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        S = tm_ctx::StripState{};
+        S.prep = prep;
+        S.img = img;
+        S.P = *params;
+        S.m = prep->m;
+        S.n = prep->n;
+        S.g = strip_of(prep->g, rank, world);
+        S.policy = params->policy == TM_POLICY_SEEDED ? TM_POLICY_SEEDED : TM_POLICY_FROZEN;
+        if (params->policy == TM_POLICY_SEQUENTIAL ||
+            (params->policy == TM_POLICY_REFERENCE && !(params->parallel && params->threads > 1)))
+            invalid("row strips support the frozen and seeded policies (the sequential running "
+                    "threshold is defined by a single global scan order)");
+        S.T = upload_template(ctx, tmpl, S.m, S.n);
+        const Tmpl& T = S.T;
+        if (T.ts.flat) invalid("transitive_search: constant template has no defined correlation");
+        if (params->has_init_threshold && std::abs(params->init_threshold) > 1.0 + 1e-9)
+            invalid("transitive_search: init threshold out of [-1,1]");
+        tm_image* simg = prep->search_img ? prep->search_img.get() : img;
+        const WS* ws = prep->search_img ? prep->search_ws.get() : &get_ws(ctx, img, S.m, S.n);
+        const size_t G = size_t(S.g.tr) * S.g.tc;
+        ctx->rho_c.ensure(G);
+        ctx->deg_c.ensure(G);
+        centre_scan(ctx, simg, *ws, T, S.g);
+        CK(tmk::threshold_init(ctx->cells.p + 0, params->has_init_threshold,
+                               params->init_threshold, ctx->thr.p, ctx->s));
+        ctx->add(1);
+        CK(cudaMemcpyAsync(T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        S.active = true;
+    });
+}
+
+int tm_strip_search_seed(tm_ctx* ctx, double T, double* T1) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        if (!S.active) invalid("tm_strip_search_seed: no strip search in progress");
+        tm_image* simg = S.prep->search_img ? S.prep->search_img.get() : S.img;
+        const WS* ws = S.prep->search_img ? S.prep->search_ws.get() : &get_ws(ctx, S.img, S.m, S.n);
+        const Tmpl& Tm = S.T;
+        const tmk::GridDesc& g = S.g;
+        const size_t G = size_t(g.tr) * g.tc;
+        CK(cudaMemcpyAsync(ctx->thr.p, &T, 8, cudaMemcpyHostToDevice, ctx->s));
+        const unsigned long long max_groups = 256;
+        const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
+        ctx->seed_locs.ensure(max_locs);
+        ctx->seeded.ensure(G);
+        CK(cudaMemsetAsync(ctx->counters.p + 4, 0, 16, ctx->s));
+        CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, S.P.seed_margin,
+                             ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
+                             ctx->counters.p + 5, max_groups, ctx->s));
+        ctx->add(1);
+        eval_list(ctx, simg, *ws, Tm, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs), nullptr,
+                  nullptr, 1);
+        CK(tmk::threshold_raise(ctx->cells.p + 1, ctx->thr.p, ctx->s));
+        ctx->add(1);
+        CK(cudaMemcpyAsync(T1, ctx->thr.p, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        if (!S.active) invalid("tm_strip_search_finish: no strip search in progress");
+        tm_image* simg = S.prep->search_img ? S.prep->search_img.get() : S.img;
+        const WS* ws = S.prep->search_img ? S.prep->search_ws.get() : &get_ws(ctx, S.img, S.m, S.n);
+        const Tmpl& Tm = S.T;
+        const tmk::GridDesc& g = S.g;
+        const size_t E = size_t(g.er) * g.ec;
+        CK(cudaMemcpyAsync(ctx->thr.p, &T, 8, cudaMemcpyHostToDevice, ctx->s));
+        ctx->visits.ensure(E);
+        ctx->locs.ensure(E);
+        CK(cudaMemsetAsync(ctx->tally.p, 0, sizeof(tmk::Tally), ctx->s));
+        const uint8_t* seeded = S.policy == TM_POLICY_SEEDED ? ctx->seeded.p : nullptr;
+        CK(tmk::sec_compact(g, S.prep->map.p, ctx->rho_c.p, ctx->deg_c.p, ws->fl.p, Tm.ts.flat,
+                            ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, ctx->visits.p,
+                            ctx->s));
+        ctx->add(1);
+        tmk::Tally tally{};
+        CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        eval_survivors(ctx, simg, *ws, Tm, g, tally.survivors, nullptr);
+        tmk::CellH cells[3];
+        CK(cudaMemcpyAsync(cells, ctx->cells.p, sizeof cells, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        tmk::CellH best = cells[0];
+        if (S.policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
+        if (better_h(cells[2], best)) best = cells[2];
+        double fin = T;
+        if ((cells[2].flags & 1) && !(cells[2].flags & 2) && cells[2].rho > fin) fin = cells[2].rho;
+        std::memset(out, 0, sizeof *out);
+        out->best_rho = best.rho;
+        out->best_row = best.row;
+        out->best_col = best.col;
+        out->best_flags = best.flags;
+        out->centers = (int64_t)(g.ti_hi - g.ti_lo) * g.tc;
+        out->eliminated = (int64_t)tally.eliminated;
+        out->retained = (int64_t)tally.retained;
+        out->final_threshold = fin;
+        S.active = false;
     });
 }
 

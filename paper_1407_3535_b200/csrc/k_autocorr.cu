@@ -44,8 +44,9 @@ __device__ __forceinline__ int crow(const Grid& g, int ti) { return g.center_row
 __global__ void k_autocorr_u8(ACParams P) {
     extern __shared__ __align__(16) unsigned char smem[];
     const Grid& g = P.g;
-    const int ti0 = blockIdx.y * P.gtr, tj0 = blockIdx.x * P.gtc;
-    const int nti = min(P.gtr, g.tr - ti0), ntj = min(P.gtc, g.tc - tj0);
+    const int ti0 = g.ti_lo + blockIdx.y * P.gtr, tj0 = blockIdx.x * P.gtc;
+    const int nti = min(P.gtr, g.ti_hi - ti0), ntj = min(P.gtc, g.tc - tj0);
+    if (nti <= 0) return;
     const int hr = g.h >> 1, wr = g.w >> 1;
     const int crA = crow(g, ti0), crB = crow(g, ti0 + nti - 1);
     const int ccA = ccol(g, tj0), ccB = ccol(g, tj0 + ntj - 1);
@@ -381,13 +382,13 @@ constexpr int kAcvThreads = 128;
 template <int H, int D>
 __global__ void __launch_bounds__(kAcvThreads)
     k_acv(const uint8_t* __restrict__ img, int p, int q, int m, int W, int trr, int tr,
-          int seg, unsigned* __restrict__ V) {
+          int seg, unsigned* __restrict__ V, int ti_base) {
     constexpr int hr = H / 2;
     constexpr int P = D * H;  // prefetch distance in rows (a multiple of H)
     const int y = blockIdx.x * kAcvThreads + threadIdx.x;
     const int t = blockIdx.y;  // dj index
     const int dj = t - W / 2;
-    const int ti0 = blockIdx.z * seg, ti1 = min(ti0 + seg, trr);
+    const int ti0 = ti_base + blockIdx.z * seg, ti1 = min(ti0 + seg, trr);
     if (ti0 >= ti1) return;
     const int yb = y + dj;
     const bool col_ok = y < q && yb >= 0 && yb < q;
@@ -487,7 +488,7 @@ __global__ void __launch_bounds__(128)
               double thr, double* __restrict__ map, unsigned long long* n_r, int tw, int lpitch) {
     extern __shared__ __align__(16) unsigned lines[];  // W lines x lpitch
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-    const int ti = blockIdx.x, dii = blockIdx.y;
+    const int ti = g.ti_lo + blockIdx.x, dii = blockIdx.y;
     const int c0 = blockIdx.z * tw;  // multiple of w: every tile here starts at or after c0
     const int hr = g.h / 2, wr = g.w / 2;
     const int di = dii - hr;
@@ -545,16 +546,18 @@ __global__ void __launch_bounds__(128)
 }
 
 template <int H>
-cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int trr, int tr,
-                       unsigned* V, cudaStream_t s) {
+cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int ti_base, int trr,
+                       int tr, unsigned* V, cudaStream_t s) {
     constexpr int D = H == 1 ? 16 : (H == 3 ? 8 : (H == 5 ? 4 : (H == 7 ? 3 : 2)));
     // segments of centre rows: enough CTAs for ~4 waves, at least 2*m rows of walk each
     const int colblocks = (q + kAcvThreads - 1) / kAcvThreads;
     int nseg = std::max(1, (148 * 16) / std::max(1, colblocks * w));
-    int seg = std::max((2 * m) / H + 1, (trr + nseg - 1) / nseg);
-    nseg = (trr + seg - 1) / seg;
-    dim3 grid(colblocks, w, nseg);
-    if (trr > 0) k_acv<H, D><<<grid, kAcvThreads, 0, s>>>(img, p, q, m, w, trr, tr, seg, V);
+    const int rows = trr - ti_base;
+    int seg = std::max((2 * m) / H + 1, (rows + nseg - 1) / nseg);
+    nseg = (rows + seg - 1) / seg;
+    dim3 grid(colblocks, w, std::max(1, nseg));
+    if (rows > 0)
+        k_acv<H, D><<<grid, kAcvThreads, 0, s>>>(img, p, q, m, w, trr, tr, seg, V, ti_base);
     return cudaGetLastError();
 }
 
@@ -638,6 +641,7 @@ __global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int
     for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
          gi += (long long)gridDim.x * blockDim.x) {
         const int ti = int(gi / g.tc), tj = int(gi % g.tc);
+        if (ti < g.ti_lo || ti >= g.ti_hi) continue;
         const int cr = g.center_row(ti), cc = g.center_col(tj);
         const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
         const int c0 = tj * g.w, c1 = min(c0 + g.w, g.ec) - 1;
@@ -656,9 +660,9 @@ __global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int
 
 __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
                            unsigned long long* n_r) {
-    const size_t E = size_t(g.er) * g.ec;
+    const size_t k0 = size_t(g.row_lo()) * g.ec, k1 = size_t(g.row_hi()) * g.ec;
     unsigned long long local = 0;
-    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+    for (size_t k = k0 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < k1;
          k += size_t(gridDim.x) * blockDim.x) {
         int r, c;
         g.rc(k, r, c);
@@ -670,7 +674,9 @@ __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(n_r, local);
 }
 
-Grid to_grid(GridDesc d) { return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc); }
+Grid to_grid(GridDesc d) {
+    return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc, d.ti_lo, d.ti_hi);
+}
 
 }  // namespace
 
@@ -716,12 +722,13 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
         cudaFuncSetAttribute(k_autocorr_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr_set = true;
     }
-    const int base = ((gd.tc + gtc - 1) / gtc) * ((gd.tr + gtr - 1) / gtr);
+    const int strip_rows = std::max(1, gd.ti_hi - gd.ti_lo);
+    const int base = ((gd.tc + gtc - 1) / gtc) * ((strip_rows + gtr - 1) / gtr);
     const int noff = gd.h * gd.w - 1;
     int splits = std::max(1, std::min(noff, (148 * 6 + base - 1) / base));
     P.noff_per = std::max(1, (noff + splits - 1) / splits);
     splits = std::max(1, (noff + P.noff_per - 1) / P.noff_per);
-    dim3 grid((gd.tc + gtc - 1) / gtc, (gd.tr + gtr - 1) / gtr, std::max(splits, 1));
+    dim3 grid((gd.tc + gtc - 1) / gtc, (strip_rows + gtr - 1) / gtr, std::max(splits, 1));
     k_autocorr_u8<<<grid, 256, bytes, s>>>(P);
     return cudaGetLastError();
 }
@@ -745,20 +752,22 @@ cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, 
                                 DevStats st, double retain_threshold, double* map,
                                 unsigned long long* n_r, unsigned* V, cudaStream_t s) {
     const bool clipped = size_t(gd.tr) * gd.h > size_t(gd.er);
-    const int trr = clipped ? gd.tr - 1 : gd.tr;
+    // regular centre rows of this strip: [ti_lo, trr)
+    const int trr = std::min(gd.ti_hi, clipped ? gd.tr - 1 : gd.tr);
+    const int tb = gd.ti_lo;
     cudaError_t e = cudaSuccess;
     switch (gd.h) {
-        case 1: e = launch_acv<1>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
-        case 3: e = launch_acv<3>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
-        case 5: e = launch_acv<5>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
-        case 7: e = launch_acv<7>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
-        case 9: e = launch_acv<9>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
-        case 11: e = launch_acv<11>(img, p, q, m, gd.w, trr, gd.tr, V, s); break;
+        case 1: e = launch_acv<1>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
+        case 3: e = launch_acv<3>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
+        case 5: e = launch_acv<5>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
+        case 7: e = launch_acv<7>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
+        case 9: e = launch_acv<9>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
+        case 11: e = launch_acv<11>(img, p, q, m, gd.w, tb, trr, gd.tr, V, s); break;
         default: return cudaErrorInvalidValue;
     }
     if (e != cudaSuccess) return e;
     const Grid g = to_grid(gd);
-    if (clipped) {
+    if (clipped && gd.tr - 1 >= gd.ti_lo && gd.tr - 1 < gd.ti_hi) {
         dim3 grid((q + 127) / 128, gd.w, gd.h);
         k_acv_last<<<grid, 128, 0, s>>>(img, p, q, m, gd.h, gd.w, g.center_row(gd.tr - 1),
                                         gd.tr - 1, gd.tr, V);
@@ -774,8 +783,9 @@ cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, 
         cudaFuncSetAttribute(k_ac_hrow, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    dim3 grid(gd.tr, gd.h, (gd.ec + tw - 1) / tw);
-    k_ac_hrow<<<grid, 128, smem, s>>>(V, q, m, n, g, st, retain_threshold, map, n_r, tw, lpitch);
+    dim3 grid(std::max(1, gd.ti_hi - gd.ti_lo), gd.h, (gd.ec + tw - 1) / tw);
+    if (gd.ti_hi > gd.ti_lo)
+        k_ac_hrow<<<grid, 128, smem, s>>>(V, q, m, n, g, st, retain_threshold, map, n_r, tw, lpitch);
     return cudaGetLastError();
 }
 

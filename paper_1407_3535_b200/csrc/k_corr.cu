@@ -88,7 +88,9 @@ __global__ void __launch_bounds__(NW * 32)
     const int p_rows = job.st.er + job.m - 1;  // image rows
     const int q_cols = job.st.ec + job.n - 1;
 
-    for (int i0 = 0; i0 < job.m; i0 += kIC) {
+    // template-row slice of this CTA (K split across blockIdx.z)
+    const int i_lo = blockIdx.z * task.ms, i_hi = min(job.m, i_lo + task.ms);
+    for (int i0 = i_lo; i0 < i_hi; i0 += kIC) {
         __syncthreads();
         // stage image rows [r_first + i0, r_first + i0 + span), columns [cstart, +width):
         // one warp per row, 8 independent coalesced loads in flight per lane
@@ -113,10 +115,10 @@ __global__ void __launch_bounds__(NW * 32)
         }
         for (int idx = threadIdx.x; idx < kIC * job.npad; idx += NW * 32) {
             const int a = idx / job.npad, b = idx - a * job.npad;
-            stp[idx] = (i0 + a < job.m) ? job.tf[size_t(i0 + a) * job.npad + b] : 0.f;
+            stp[idx] = (i0 + a < i_hi) ? job.tf[size_t(i0 + a) * job.npad + b] : 0.f;
         }
         __syncthreads();
-        const int nii = min(kIC, job.m - i0);
+        const int nii = min(kIC, i_hi - i0);
         for (int ii = 0; ii < nii; ++ii) {
             const float* irow = simg + (yo + ii) * spitch + lane_col;
             const float* trow = stp + ii * job.npad;
@@ -144,7 +146,7 @@ __global__ void __launch_bounds__(NW * 32)
 #pragma unroll
                     for (int x = 0; x < kRX; ++x) acc[x] = fmaf(tv[j], win[x * SW + j], acc[x]);
             }
-            if ((i0 + ii + 1) % job.flush_rows == 0) {
+            if ((i0 + ii + 1 - i_lo) % job.flush_rows == 0) {
 #pragma unroll
                 for (int x = 0; x < kRX; ++x) {
                     dacc[x] += double(acc[x]);
@@ -156,10 +158,22 @@ __global__ void __launch_bounds__(NW * 32)
 #pragma unroll
     for (int x = 0; x < kRX; ++x) dacc[x] += double(acc[x]);
 
+    const int k0 = kb + wid * 32 + sx * kRX;
+    if (task.dot) {  // K split: exact integer partial dots accumulate in FP64
+#pragma unroll
+        for (int x = 0; x < kRX; ++x) {
+            const int k = k0 + x;
+            if (!row_ok || k >= task.nc) continue;
+            const int c = task.cbase + k * SW;
+            const size_t idx = task.mode == 1 ? size_t(task.yi_base + yi) * task.tc + task.col0 + k
+                                              : size_t(r) * job.st.ec + c;
+            atomicAdd(task.dot + idx, dacc[x]);
+        }
+        return;
+    }
     // ---- epilogue ---------------------------------------------------------------------
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
-    const int k0 = kb + wid * 32 + sx * kRX;
 #pragma unroll
     for (int x = 0; x < kRX; ++x) {
         const int k = k0 + x;
@@ -171,7 +185,7 @@ __global__ void __launch_bounds__(NW * 32)
         const double rho = zncc_epilogue(dacc[x], ts, job.st.mu[kk], job.st.omega[kk], wflat);
         const bool deg = ts.flat || wflat;
         if (task.mode == 1) {
-            const size_t gi = size_t(yi) * task.tc + task.col0 + k;
+            const size_t gi = size_t(task.yi_base + yi) * task.tc + task.col0 + k;
             task.out_rho[gi] = rho;
             task.out_deg[gi] = deg;
         } else if (task.out_rho) {
@@ -184,6 +198,34 @@ __global__ void __launch_bounds__(NW * 32)
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+// Epilogue of a K-split centre scan: rho/deg per group from the accumulated dots.
+__global__ void __launch_bounds__(256)
+    k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
+                 int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
+                 CellH* partials) {
+    __shared__ Cell scratch[8];
+    const TStats ts = to_ts(job.ts);
+    Cell best = no_cell();
+    const int nrows = g.ti_hi - g.ti_lo;
+    const long long total = (long long)nrows * nc;
+    for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
+         it += (long long)gridDim.x * blockDim.x) {
+        const int yi = int(it / nc), k = int(it % nc);
+        const int r = rows[yi], c = cbase + k * sw;
+        const size_t gi = size_t(g.ti_lo + yi) * g.tc + col0 + k;
+        const size_t kk = size_t(r) * job.st.ec + c;
+        const bool wflat = job.st.flat[kk];
+        const double rho = zncc_epilogue(dot[gi], ts, job.st.mu[kk], job.st.omega[kk], wflat);
+        const bool deg = ts.flat || wflat;
+        rho_c[gi] = rho;
+        deg_c[gi] = deg;
+        const Cell cand = make_cell(r, c, rho, deg);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+}
+
 // ---- sparse: one warp per location ----------------------------------------------------
 // The template is staged once per CTA in shared memory; lanes own template columns
 // j = lane, lane+32, ...; the row loop is unrolled for memory-level parallelism.
@@ -191,11 +233,8 @@ __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                 int lane_flush, int rho_by_loc) {
-    extern __shared__ __align__(16) float stmp[];  // m x npad template
     __shared__ Cell scratch[8];
     const int lane = threadIdx.x & 31;
-    for (int i = threadIdx.x; i < job.m * job.npad; i += blockDim.x) stmp[i] = job.tf[i];
-    __syncthreads();
     const long long nloc = min((long long)*count, (long long)max_count);
     const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
     const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
@@ -204,21 +243,33 @@ __global__ void __launch_bounds__(256)
     for (long long li = warp0; li < nloc; li += nwarps) {
         const int2 rc = locs[li];
         double dacc = 0.0;
-        float acc = 0.f;
         const float* ib = job.imgf + size_t(rc.x) * job.pitch + rc.y;
+        // a lane accumulates one template column over rows; two independent FP32 partials
+        // (even/odd rows) stay exact while each covers < lane_flush rows (2^24 bound)
         for (int j = lane; j < job.n; j += 32) {
-            int since = 0;
-#pragma unroll 8
-            for (int i = 0; i < job.m; ++i) {
-                acc = fmaf(stmp[i * job.npad + j], __ldg(ib + size_t(i) * job.pitch + j), acc);
-                if (++since == lane_flush) {
-                    dacc += double(acc);
-                    acc = 0.f;
-                    since = 0;
+            const float* tp = job.tf + j;
+            for (int i0 = 0; i0 < job.m; i0 += 2 * lane_flush) {
+                const int i1 = min(job.m, i0 + 2 * lane_flush);
+                float a0 = 0.f, a1 = 0.f;
+                int i = i0;
+                for (; i + 8 <= i1; i += 8) {
+                    float v[8], t[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        v[u] = __ldg(ib + size_t(i + u) * job.pitch + j);
+                        t[u] = __ldg(tp + size_t(i + u) * job.npad);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 8; u += 2) {
+                        a0 = fmaf(t[u], v[u], a0);
+                        a1 = fmaf(t[u + 1], v[u + 1], a1);
+                    }
                 }
+                for (; i < i1; ++i)
+                    a0 = fmaf(__ldg(tp + size_t(i) * job.npad), __ldg(ib + size_t(i) * job.pitch + j), a0);
+                dacc += double(a0) + double(a1);
             }
         }
-        dacc += double(acc);
         dacc = warp_sum(dacc);
         if (lane == 0) {
             const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
@@ -337,10 +388,10 @@ __global__ void __launch_bounds__(256)
                   int2* locs, unsigned long long max_locs, Tally* tally, uint8_t* visits) {
     const double T = *thr_ptr;
     const double tb = dmin(T, 1.0);
-    const size_t E = size_t(g.er) * g.ec;
+    const size_t K0 = size_t(g.row_lo()) * g.ec, E = size_t(g.row_hi()) * g.ec;
     const int lane = threadIdx.x & 31;
     unsigned long long n_elim = 0, n_keep = 0;
-    for (size_t base = blockIdx.x * size_t(blockDim.x); base < E;
+    for (size_t base = K0 + blockIdx.x * size_t(blockDim.x); base < E;
          base += size_t(gridDim.x) * blockDim.x) {
         const size_t k = base + threadIdx.x;
         bool survivor = false;
@@ -410,10 +461,10 @@ __global__ void k_seed_members(Grid g, const double* __restrict__ rho_c,
                                double margin, uint8_t* seeded, int2* locs,
                                unsigned long long* count, unsigned long long max_locs,
                                unsigned long long* n_groups, unsigned long long max_groups) {
-    const long long G = (long long)g.tr * g.tc;
+    const long long G = (long long)g.ti_hi * g.tc;
     const double T = *thr;
-    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
-         gi += (long long)gridDim.x * blockDim.x) {
+    for (long long gi = (long long)g.ti_lo * g.tc + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+         gi < G; gi += (long long)gridDim.x * blockDim.x) {
         seeded[gi] = 0;
         if (deg_c[gi] || !(rho_c[gi] >= T - margin)) continue;
         const unsigned long long slot = atomicAdd(n_groups, 1ull);
@@ -526,7 +577,9 @@ __global__ void k_seq_final(Grid g, const int2* __restrict__ locs, const unsigne
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
 }
 
-Grid to_grid(GridDesc d) { return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc); }
+Grid to_grid(GridDesc d) {
+    return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc, d.ti_lo, d.ti_hi);
+}
 
 template <int SW, int NW>
 cudaError_t launch_band(const CorrJob& job, const BandTask& task, CellH* partials, int* n_partials,
@@ -543,9 +596,9 @@ cudaError_t launch_band(const CorrJob& job, const BandTask& task, CellH* partial
         attr = true;
     }
     if (geo.smem > 200 * 1024) return cudaErrorInvalidValue;
-    dim3 grid((task.nc + NW * 32 - 1) / (NW * 32), bands);
+    dim3 grid((task.nc + NW * 32 - 1) / (NW * 32), bands, std::max(1, task.ksplit));
     k_corr_band<SW, NW><<<grid, NW * 32, geo.smem, s>>>(job, task, geo.spitch, geo.srows, partials);
-    *n_partials = int(grid.x * grid.y);
+    *n_partials = task.dot ? 0 : int(grid.x * grid.y);
     return cudaGetLastError();
 }
 
@@ -569,17 +622,10 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                       int n_partials, cudaStream_t s, int rho_by_loc) {
-    // one lane accumulates one template column at a time: flush before 2^24
-    int lane_flush = int(16777216LL / 65025LL);
-    const size_t smem = size_t(job.m) * job.npad * sizeof(float);
-    if (smem > 200 * 1024) return cudaErrorInvalidValue;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_corr_list, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
-    k_corr_list<<<n_partials, 256, smem, s>>>(job, locs, count, max_count, out_rho, out_deg,
-                                              partials, lane_flush, rho_by_loc);
+    // one FP32 partial covers lane_flush rows of one template column: < 2^24 exactly
+    const int lane_flush = int(16777216LL / 65025LL);
+    k_corr_list<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
+                                           partials, lane_flush, rho_by_loc);
     return cudaGetLastError();
 }
 
@@ -610,6 +656,14 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
         rho_c[size_t(i) * tc + col] = rho[i];
         deg_c[size_t(i) * tc + col] = deg[i];
     }
+}
+
+cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
+                            int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
+                            CellH* partials, int n_partials, cudaStream_t s) {
+    k_centre_epi<<<n_partials, 256, 0, s>>>(job, to_grid(g), rows, cbase, sw, nc, col0, dot, rho_c,
+                                            deg_c, partials);
+    return cudaGetLastError();
 }
 
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,

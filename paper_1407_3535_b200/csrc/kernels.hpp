@@ -18,6 +18,8 @@ struct DevStats {  // WindowStats (stats.hpp:35-47) resident in HBM
 
 struct GridDesc {  // GroupGrid (autocorr.hpp:24-52)
     int er, ec, h, w, tr, tc;
+    // group rows this device processes (row strip); [0, tr) = everything
+    int ti_lo, ti_hi;
 };
 
 struct TStatsH {  // TemplateStats (detail.hpp:24-28) + mn
@@ -130,12 +132,18 @@ struct BandTask {
     int nrows;
     int cbase, sw, nc;
     int mode;
+    int yi_base;   // mode 1: group row of rows[0] (row strips)
     int row_span;  // max over 8-row bands of rows[yb+7]-rows[yb] (staging height - kIC)
     int col0;  // column-index offset for mode 1 group indexing
     int tc;    // groups per grid row (mode 1)
     double* out_rho;
     uint8_t* out_deg;
     const uint8_t* mask;  // mode 2
+    // K split: ksplit CTAs per output tile, each over `ms` template rows; partial dots are
+    // atomically accumulated into `dot` (exact integers in FP64) and no epilogue runs.
+    int ksplit;
+    int ms;
+    double* dot;
 };
 cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
                       int* n_partials, cudaStream_t s);
@@ -154,6 +162,10 @@ cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint
 cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
                            cudaStream_t s);
 
+// Epilogue of a K-split centre scan (rho/deg from the accumulated dots + argmax partials).
+cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
+                            int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
+                            CellH* partials, int n_partials, cudaStream_t s);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);

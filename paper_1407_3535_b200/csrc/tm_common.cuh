@@ -150,11 +150,15 @@ struct FastDiv {
 // centre = (r0 + r1) / 2.  fh/fw/fec divide by h, w and ec on the fast path.
 struct Grid {
     int er, ec, h, w, tr, tc;
+    int ti_lo, ti_hi;  // group-row range of this device (row strip)
     FastDiv fh, fw, fec;
-    __host__ static Grid make(int er, int ec, int h, int w, int tr, int tc) {
-        return Grid{er, ec, h, w, tr, tc, FastDiv::make(unsigned(h)), FastDiv::make(unsigned(w)),
-                    FastDiv::make(unsigned(ec))};
+    __host__ static Grid make(int er, int ec, int h, int w, int tr, int tc, int ti_lo, int ti_hi) {
+        return Grid{er, ec, h, w, tr, tc, ti_lo, ti_hi, FastDiv::make(unsigned(h)),
+                    FastDiv::make(unsigned(w)), FastDiv::make(unsigned(ec))};
     }
+    // extent rows [row_lo, row_hi) owned by the strip
+    __host__ __device__ __forceinline__ int row_lo() const { return ti_lo * h; }
+    __host__ __device__ __forceinline__ int row_hi() const { return ti_hi * h < er ? ti_hi * h : er; }
     __host__ __device__ __forceinline__ int tile_r(int r) const {
 #ifdef __CUDA_ARCH__
         return min(int(fh.div(r)), tr - 1);

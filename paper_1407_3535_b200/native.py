@@ -87,6 +87,13 @@ class PrepInfo(C.Structure):
                 ("prep_ms", C.c_double)]
 
 
+class StripPart(C.Structure):  # tm_strip_part
+    _fields_ = [("best_rho", C.c_double), ("best_row", C.c_int32), ("best_col", C.c_int32),
+                ("best_flags", C.c_int32), ("_pad0", C.c_int32), ("centers", C.c_int64),
+                ("eliminated", C.c_int64), ("retained", C.c_int64),
+                ("final_threshold", C.c_double)]
+
+
 _P = C.c_void_p
 _D = C.POINTER(C.c_double)
 _U8 = C.POINTER(C.c_uint8)
@@ -139,6 +146,15 @@ SIGNATURES = {
                                          C.c_int, _I, _I, _D, _I]),
     "tm_match": (C.c_int, [_P, _D, C.c_int, C.c_int, _D, C.c_int, C.c_int,
                            C.POINTER(MatchParams), C.POINTER(MatchResult), _U8]),
+    "tm_strip_autocorr": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                    C.c_double, C.c_int, C.POINTER(C.c_int64)]),
+    "tm_strip_commit": (C.c_int, [_P, _P, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                  C.POINTER(MatchParams), C.POINTER(EgsIter), C.c_int,
+                                  C.POINTER(_P)]),
+    "tm_strip_search_begin": (C.c_int, [_P, _P, _P, _D, C.POINTER(MatchParams), C.c_int, C.c_int,
+                                        _D]),
+    "tm_strip_search_seed": (C.c_int, [_P, C.c_double, _D]),
+    "tm_strip_search_finish": (C.c_int, [_P, C.c_double, C.POINTER(StripPart)]),
 }
 
 
