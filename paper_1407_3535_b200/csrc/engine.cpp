@@ -16,6 +16,7 @@
 // thresholds, costs) follow the reference's evaluation order.
 #include <algorithm>
 #include <chrono>
+#include <atomic>
 #include <climits>
 #include <cstdio>
 #include <cmath>
@@ -172,6 +173,10 @@ struct tm_ctx {
     int device = 0;
     cudaStream_t s = nullptr;
     std::mutex mu;
+    // images and preparations keep their context alive: tm_ctx_destroy only marks it
+    // closing, and the last dependent object releases it
+    std::atomic<int> refs{0};
+    std::atomic<bool> closing{false};
     int64_t launches = 0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // scratch (grow-only)
@@ -288,6 +293,7 @@ struct tm_prep {
     double prep_ms = -1.0;
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     tm_image* source = nullptr;  // not owned
+    tm_ctx* ctx = nullptr;       // keeps the context alive (ref)
     ~tm_prep() {
         if (ev0) cudaEventDestroy(ev0);
         if (ev1) cudaEventDestroy(ev1);
@@ -1317,6 +1323,23 @@ int guard(tm_ctx* ctx, F&& f) {
 
 }  // namespace
 
+// Actually free a context (no dependents left).
+void ctx_release(tm_ctx* ctx) {
+    cudaSetDevice(ctx->device);
+    cudaStream_t st = ctx->s;
+    cudaStreamSynchronize(st);
+    cudaEventDestroy(ctx->ev0);
+    cudaEventDestroy(ctx->ev1);
+    for (cudaEvent_t ev : ctx->pool) cudaEventDestroy(ev);
+    delete ctx;  // stream-ordered frees of the scratch buffers
+    cudaStreamSynchronize(st);
+    cudaStreamDestroy(st);
+}
+
+void ctx_unref(tm_ctx* ctx) {
+    if (ctx && --ctx->refs == 0 && ctx->closing) ctx_release(ctx);
+}
+
 // ==== C ABI ===========================================================================
 extern "C" {
 
@@ -1371,16 +1394,8 @@ int tm_ctx_create(int device, tm_ctx** out) {
 
 void tm_ctx_destroy(tm_ctx* ctx) {
     if (!ctx) return;
-    cudaSetDevice(ctx->device);
-    cudaStream_t st = ctx->s;
-    cudaStreamSynchronize(st);
-    cudaEventDestroy(ctx->ev0);
-    cudaEventDestroy(ctx->ev1);
-    for (auto& kv : ctx->phase_ms) (void)kv;
-    for (cudaEvent_t e : ctx->pool) cudaEventDestroy(e);
-    delete ctx;  // stream-ordered frees of the scratch buffers
-    cudaStreamSynchronize(st);
-    cudaStreamDestroy(st);
+    ctx->closing = true;
+    if (ctx->refs.load() == 0) ctx_release(ctx);
 }
 
 int tm_ctx_synchronize(tm_ctx* ctx) {
@@ -1433,6 +1448,7 @@ int tm_image_create(tm_ctx* ctx, const double* pixels, int rows, int cols, tm_im
         img->q = cols;
         const size_t N = size_t(rows) * cols;
         img->f64.ensure(N);
+        ++ctx->refs;
         CK(cudaMemcpyAsync(img->f64.p, pixels, N * 8, cudaMemcpyHostToDevice, ctx->s));
         classify_device_image(ctx, img.get());
         *out = img.release();
@@ -1447,6 +1463,7 @@ int tm_image_create_u8(tm_ctx* ctx, const uint8_t* pixels, int rows, int cols, t
         img->p = rows;
         img->q = cols;
         img->integer = true;
+        ++ctx->refs;
         const size_t N = size_t(rows) * cols;
         img->u8.ensure(N);
         CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
@@ -1483,11 +1500,15 @@ int tm_image_is_integer(const tm_image* img) { return img && img->integer ? 1 : 
 
 void tm_image_destroy(tm_image* img) {
     if (!img) return;
-    if (img->ctx) {
-        std::lock_guard<std::mutex> lk(img->ctx->mu);
-        cudaSetDevice(img->ctx->device);
-        cudaStreamSynchronize(img->ctx->s);
-        delete img;
+    tm_ctx* ctx = img->ctx;
+    if (ctx) {
+        {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            cudaSetDevice(ctx->device);
+            cudaStreamSynchronize(ctx->s);
+            delete img;
+        }
+        ctx_unref(ctx);
     } else {
         delete img;
     }
@@ -1660,7 +1681,11 @@ int tm_unblur_violations(tm_ctx* ctx, tm_image* blurred, tm_image* original, con
 
 int tm_prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params* params,
                tm_prep** out) {
-    return guard(ctx, [&] { *out = prepare(ctx, img, m, n, *params); });
+    return guard(ctx, [&] {
+        *out = prepare(ctx, img, m, n, *params);
+        (*out)->ctx = ctx;
+        ++ctx->refs;
+    });
 }
 
 int tm_prep_get_info(const tm_prep* prep, tm_prep_info* info) {
@@ -1706,11 +1731,15 @@ int tm_prep_download(tm_ctx* ctx, const tm_prep* prep, double* map, double* imag
 
 void tm_prep_destroy(tm_prep* prep) {
     if (!prep) return;
-    tm_ctx* ctx = prep->source ? prep->source->ctx : nullptr;
+    tm_ctx* ctx = prep->ctx;
     if (ctx) {
-        std::lock_guard<std::mutex> lk(ctx->mu);
-        cudaStreamSynchronize(ctx->s);
-        delete prep;
+        {
+            std::lock_guard<std::mutex> lk(ctx->mu);
+            cudaSetDevice(ctx->device);
+            cudaStreamSynchronize(ctx->s);
+            delete prep;
+        }
+        ctx_unref(ctx);
     } else {
         delete prep;
     }
@@ -1835,6 +1864,8 @@ int tm_strip_commit(tm_ctx* ctx, tm_image* img, int m, int n, int slot, int h, i
         prep->egs_trace.assign(trace, trace + std::max(0, trace_len));
         if (trace_len > 0) prep->cost = trace[trace_len - 1];
         prep->prep_ms = 0.0;
+        prep->ctx = ctx;
+        ++ctx->refs;
         *out = prep.release();
     });
 }

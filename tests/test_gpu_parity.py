@@ -230,3 +230,22 @@ def test_below_threshold_flag(ctx, port):
         b = port.match(t, img, mode=mode, init_threshold=0.9999)
         np.testing.assert_array_equal(res_vec(a), res_vec(b))
         assert a.below_threshold
+
+
+@pytest.mark.gpu
+def test_context_closed_before_its_images(port):
+    """Closing a context first defers its release to the last image/preparation."""
+    from paper_1407_3535_b200 import api
+    rng = np.random.default_rng(5)
+    img = rng.integers(0, 256, (48, 52)).astype(np.uint8)
+    t = img[10:19, 12:21].copy()
+    c = api.Context(0)
+    im = c.image(img)
+    prep = c.prepare(im, 9, 9)
+    c.close()
+    r = c.__class__(0).match(t, img)  # an independent context still works
+    prep2 = prep
+    prep2.close()
+    im.close()
+    b = port.brute(t.astype(np.float64), img.astype(np.float64))
+    assert (r.best_row, r.best_col) == (b.best_row, b.best_col)
