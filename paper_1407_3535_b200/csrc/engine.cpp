@@ -210,6 +210,9 @@ struct tm_ctx {
     void add(int k) { launches += k; }
     // optional per-phase device timing (CUDA events on the context stream)
     bool profiling = false;
+    // R_co kernel choice: fused sliding-window (default) or the column-walk + line-scan pair
+    // (TMATCH_AUTOCORR=colwalk; kept for A/B measurements and as a cross-check in tests)
+    bool ac_fused = true;
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -328,6 +331,15 @@ int centre_col_h(const tmk::GridDesc& g, int tj) {
 }
 
 // ---- images ----------------------------------------------------------------------------
+// 8-bit pixels are stored with tmk::kU8PadRows zero rows below the image, so row walks
+// may read a few rows past the bottom without bounds checks (k_acf).
+void alloc_u8(tm_ctx* ctx, tm_image* img) {
+    const size_t N = size_t(img->p) * img->q;
+    const size_t pad = size_t(tmk::kU8PadRows) * img->q;
+    img->u8.ensure(N + pad);
+    CK(cudaMemsetAsync(img->u8.p + N, 0, pad, ctx->s));
+}
+
 void finish_integer_image(tm_ctx* ctx, tm_image* img) {
     img->pitch = ((img->q + 3) & ~3) + 128;  // zero pad: vector loads past the last column
     img->f32.ensure(size_t(img->p) * img->pitch);
@@ -356,7 +368,7 @@ void classify_device_image(tm_ctx* ctx, tm_image* img) {
     img->have_f64 = true;
     img->integer = hbad == 0;
     if (img->integer) {
-        img->u8.ensure(N);
+        alloc_u8(ctx, img);
         CK(tmk::f64_to_u8(img->f64.p, N, img->u8.p, ctx->s));
         ctx->add(1);
         finish_integer_image(ctx, img);
@@ -661,7 +673,10 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
     if (img->integer) {
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
-        if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
+        if (ctx->ac_fused && tmk::autocorr_fused_supported(m, n, g)) {
+            CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
+            ctx->add(1);
+        } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
             CK(tmk::autocorr_u8_colwalk(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
                                         reinterpret_cast<unsigned*>(ctx->acH.p), ctx->s));
@@ -1375,6 +1390,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
             throw TmError{TM_ENODEV, "tmatch kernels are built for sm_100a (Blackwell)"};
         auto ctx = std::make_unique<tm_ctx>();
         ctx->device = device;
+        if (const char* e = std::getenv("TMATCH_AUTOCORR")) ctx->ac_fused = std::strcmp(e, "colwalk") != 0;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
         cudaMemPool_t pool;
@@ -1465,7 +1481,7 @@ int tm_image_create_u8(tm_ctx* ctx, const uint8_t* pixels, int rows, int cols, t
         img->integer = true;
         ++ctx->refs;
         const size_t N = size_t(rows) * cols;
-        img->u8.ensure(N);
+        alloc_u8(ctx, img.get());
         CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
         finish_integer_image(ctx, img.get());
         CK(cudaStreamSynchronize(ctx->s));

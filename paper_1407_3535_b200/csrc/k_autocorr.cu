@@ -545,6 +545,259 @@ __global__ void __launch_bounds__(128)
     if (lane == 0 && local) atomicAdd(n_r, local);
 }
 
+Grid to_grid(GridDesc d);
+
+// ---- fused sliding-window R_co (preferred path) -----------------------------------------
+//
+// CTA = (column offset dj, column tile [c0, c0+tw), segment of centre rows).  Thread = one
+// image column y of the tile plus its n-1 halo (NY = blockDim.x columns).  Each thread keeps
+// the vertical window sums V_di(y) = sum_{a<m} I(cr+a, y) * I(cr+di+a, y+dj) for all h row
+// offsets di as SLIDING sums: every row step adds the leading row and subtracts the row m
+// above it (two register rings of B values, u32 arithmetic exact mod 2^32 and the true sums
+// are < 2^32), so any centre row - the clipped last one included - is just an event on the
+// walk.  At the event the CTA scans the h lines along y (block-wide inclusive scan into
+// shared memory) and evaluates its members directly: S = L[cc+n-1] - L[cc-1], then the FP64
+// epilogue of autocorr.cpp:84-88 and the retained count of egs.cpp:12-25.  Nothing but the
+// map goes to HBM.
+template <int H>
+__global__ void __launch_bounds__(512)
+    k_acf(const uint8_t* __restrict__ img, int p, int q, int m, int n, Grid g, DevStats st,
+          double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int tw,
+          int seg) {
+    constexpr int hr = H / 2;
+    extern __shared__ __align__(16) unsigned acf_smem[];
+    const int NY = blockDim.x;
+    unsigned* L = acf_smem;  // 2 x [H][NY] warp-inclusive prefixes along y
+    unsigned* wt = acf_smem + 2 * H * NY;  // 2 x [H][32] warp totals
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int dj = int(blockIdx.x) - g.w / 2;
+    const int c0 = blockIdx.y * tw;
+    const int ti0 = g.ti_lo + blockIdx.z * seg;
+    const int ti1 = min(ti0 + seg, g.ti_hi);
+    if (ti0 >= ti1 || c0 >= g.ec) return;  // uniform
+    // Columns outside the image and rows below it only feed window sums that no valid
+    // member reads (member windows lie inside the image), so the walk clamps columns and
+    // relies on the kU8PadRows zero rows under the image instead of bounds checks.
+    const int y = c0 + threadIdx.x;
+    const uint8_t* ca = img + min(y, q - 1);
+    const uint8_t* cb = img + min(max(y + dj, 0), q - 1);
+    unsigned V[H], rl[H], rt[H];
+    int cr = g.center_row(ti0);
+#pragma unroll
+    for (int d = 0; d < H; ++d) {
+        V[d] = 0u;
+        const int xr = max(cr - 1 - hr + d, 0);  // rows cr-hr .. cr+hr-1 in slots 1..H-1
+        rl[d] = d >= 1 ? unsigned(__ldg(cb + unsigned(xr) * unsigned(q))) : 0u;
+        rt[d] = rl[d];
+    }
+    // leading edge: A row x, B row x+hr; trailing edge: the same m rows above
+    const uint8_t* la = ca + unsigned(cr) * unsigned(q);
+    const uint8_t* lb = cb + unsigned(cr + hr) * unsigned(q);
+    const uint8_t* ta = la;
+    const uint8_t* tb = lb;
+    auto lead = [&]() {
+#pragma unroll
+        for (int d = 0; d < H - 1; ++d) rl[d] = rl[d + 1];
+        rl[H - 1] = unsigned(__ldg(lb));
+        const unsigned a = unsigned(__ldg(la));
+        la += q;
+        lb += q;
+#pragma unroll
+        for (int d = 0; d < H; ++d) V[d] += a * rl[d];  // di = d - hr
+    };
+    auto trail = [&]() {  // remove the row m above the leading edge
+#pragma unroll
+        for (int d = 0; d < H - 1; ++d) rt[d] = rt[d + 1];
+        rt[H - 1] = unsigned(__ldg(tb));
+        const unsigned a = unsigned(__ldg(ta));
+        ta += q;
+        tb += q;
+#pragma unroll
+        for (int d = 0; d < H; ++d) V[d] -= a * rt[d];
+    };
+    // warm-up: the first window rows [cr, cr+m)
+    {
+        int x = cr;
+        const int xe = cr + m;
+#pragma unroll 1
+        for (; x + H <= xe; x += H) {
+#pragma unroll
+            for (int j = 0; j < H; ++j) lead();
+        }
+#pragma unroll 1
+        for (; x < xe; ++x) lead();
+    }
+    const double mn = double(m) * double(n);
+    const int tj0 = c0 / g.w;
+    const int tj1 = min(g.tc, (c0 + tw) / g.w);
+    const int ng = tj1 - tj0;
+    // Fixed member slots: slot j of this thread is member i = tid + j*NY of every event,
+    // (row offset d = i / ng, group k = i % ng); the column side is constant per CTA.
+    constexpr int kSlots = 1;  // acf_geom keeps h * groups-per-tile <= NY
+    int s_d[kSlots], s_c[kSlots], s_cc[kSlots], s_u[kSlots];
+    bool s_ok[kSlots];
+#pragma unroll
+    for (int j = 0; j < kSlots; ++j) {
+        const int i = threadIdx.x + j * NY;
+        s_ok[j] = i < H * ng;
+        const int d = s_ok[j] ? i / ng : 0, k = s_ok[j] ? i - d * ng : 0;
+        const int tj = tj0 + k;
+        const int gc0 = tj * g.w, gc1 = min(gc0 + g.w, g.ec) - 1;
+        const int cc = (gc0 + gc1) >> 1;
+        const int c = cc + dj;
+        s_ok[j] = s_ok[j] && c >= gc0 && c <= gc1;
+        s_d[j] = d;
+        s_c[j] = c;
+        s_cc[j] = cc;
+        s_u[j] = cc - c0;
+    }
+    // statistics of the next event's members, loaded one walk ahead
+    uint8_t pf_fc[kSlots], pf_fm[kSlots];
+    double pf_mc[kSlots], pf_mm[kSlots], pf_oc[kSlots], pf_om[kSlots];
+    bool pf_row[kSlots];
+    auto prefetch = [&](int tin, int crn) {
+        const int r0 = tin * g.h, r1 = min(r0 + g.h, g.er) - 1;
+#pragma unroll
+        for (int j = 0; j < kSlots; ++j) {
+            const int mr = crn + s_d[j] - hr;
+            pf_row[j] = s_ok[j] && mr >= r0 && mr <= r1;
+            const size_t kc = pf_row[j] ? size_t(crn) * g.ec + s_cc[j] : 0;
+            const size_t km = pf_row[j] ? size_t(mr) * g.ec + s_c[j] : 0;
+            pf_fc[j] = st.flat[kc];
+            pf_fm[j] = st.flat[km];
+            pf_mc[j] = st.mu[kc];
+            pf_mm[j] = st.mu[km];
+            pf_oc[j] = st.omega[kc];
+            pf_om[j] = st.omega[km];
+        }
+    };
+    prefetch(ti0, cr);
+    unsigned long long local = 0;
+    int parity = 0;
+#pragma unroll 1
+    for (int ti = ti0;;) {
+        // ---- event: window [cr, cr+m) complete in V ----
+        // warp-local inclusive prefixes + warp totals, double-buffered by event parity so a
+        // single barrier per event suffices (the next writer of this buffer is two events
+        // away, behind the next event's barrier).
+        unsigned* Lb = L + (parity ? H * NY : 0);
+        unsigned* wb = wt + (parity ? H * 32 : 0);
+        parity ^= 1;
+        {
+            unsigned v[H];
+#pragma unroll
+            for (int d = 0; d < H; ++d) v[d] = V[d];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int d = 0; d < H; ++d) {
+                    const unsigned t = __shfl_up_sync(0xffffffffu, v[d], o);
+                    if (lane >= o) v[d] += t;
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < H; ++d) {
+                Lb[d * NY + threadIdx.x] = v[d];
+                if (lane == 31) wb[d * 32 + wid] = v[d];
+            }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int j = 0; j < kSlots; ++j) {
+            if (!pf_row[j]) continue;
+            const int d = s_d[j];
+            const size_t km = size_t(cr + d - hr) * g.ec + s_c[j];
+            if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
+                map[km] = 1.0;
+                continue;
+            }
+            // S = P[u+n-1] - P[u-1], P the block prefix = warp prefix + earlier warp totals
+            const int u = s_u[j];
+            const int i1 = u + n - 1, w1 = i1 >> 5;
+            const unsigned* Ld = Lb + d * NY;
+            unsigned S = Ld[i1];
+            int w0 = 0;
+            if (u > 0) {
+                S -= Ld[u - 1];
+                w0 = (u - 1) >> 5;
+            }
+            for (int ww = w0; ww < w1; ++ww) S += wb[d * 32 + ww];
+            double val = 0.0;
+            if (!pf_fc[j] && !pf_fm[j]) {
+                const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc[j]), pf_mm[j]));
+                val = dclamp(__ddiv_rn(num, __dmul_rn(pf_oc[j], pf_om[j])), -1.0, 1.0);
+            }
+            map[km] = val;
+            if (val < thr) ++local;
+        }
+        if (++ti >= ti1) break;
+        // ---- advance the window to the next centre row ----
+        const int crn = g.center_row(ti);
+        prefetch(ti, crn);
+        if (crn - cr == H) {
+#pragma unroll
+            for (int j = 0; j < H; ++j) {
+                lead();
+                trail();
+            }
+        } else {
+#pragma unroll 1
+            for (int x = cr; x < crn; ++x) {
+                lead();
+                trail();
+            }
+        }
+        cr = crn;
+    }
+    local = warp_sum(local);
+    if (lane == 0 && local) atomicAdd(n_r, local);
+}
+
+struct AcfGeom {
+    int ny, tw, seg, nseg, ntiles;
+    size_t smem;
+};
+
+AcfGeom acf_geom(int m, int n, GridDesc gd) {
+    AcfGeom a{};
+    int ny = std::max(128, 3 * n);
+    ny = std::max(ny, n - 1 + 2 * gd.w);
+    ny = (ny + 31) & ~31;
+    if (ny > 512) return AcfGeom{};
+    a.ny = ny;
+    a.tw = ((a.ny - n + 1) / gd.w) * gd.w;
+    if (a.tw < gd.w) return AcfGeom{};
+    a.tw = std::min(a.tw, (a.ny / gd.h) * gd.w);  // one member slot per thread
+    if (a.tw < gd.w) return AcfGeom{};
+    a.ntiles = (gd.ec + a.tw - 1) / a.tw;
+    const int rows = gd.ti_hi - gd.ti_lo;
+    const int seg_min = std::max(1, (m + gd.h - 1) / gd.h);
+    const int resident = std::max(1, 2048 / a.ny);
+    int nseg = std::max(1, (148 * resident * 2) / std::max(1, gd.w * a.ntiles));
+    nseg = std::min(nseg, std::max(1, (rows + seg_min - 1) / seg_min));
+    a.seg = std::max(1, (rows + nseg - 1) / nseg);
+    a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
+    a.smem = 2 * size_t(gd.h) * (a.ny + 32) * sizeof(unsigned);
+    return a;
+}
+
+template <int H>
+cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc gd, DevStats st,
+                       double thr, double* map, unsigned long long* n_r, cudaStream_t s) {
+    const AcfGeom a = acf_geom(m, n, gd);
+    if (a.ny == 0) return cudaErrorInvalidValue;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_acf<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
+        attr = true;
+    }
+    dim3 grid(gd.w, a.ntiles, a.nseg);
+    if (gd.ti_hi > gd.ti_lo)
+        k_acf<H><<<grid, a.ny, a.smem, s>>>(img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
+                                            a.seg);
+    return cudaGetLastError();
+}
+
 template <int H>
 cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int ti_base, int trr,
                        int tr, unsigned* V, cudaStream_t s) {
@@ -738,6 +991,28 @@ size_t autocorr_rowsum_bytes(int p, GridDesc g) {  // H and its transposed prefi
 }
 
 bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h, g.w); }
+
+
+bool autocorr_fused_supported(int m, int n, GridDesc g) {
+    // 32-bit row offsets; the walk may read h/2 <= kU8PadRows rows below the image
+    const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
+    return g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
+           (p + kU8PadRows) * q < (size_t(1) << 31) && acf_geom(m, n, g).ny > 0;
+}
+
+cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
+                              DevStats st, double retain_threshold, double* map,
+                              unsigned long long* n_r, cudaStream_t s) {
+    switch (gd.h) {
+        case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 3: return launch_acf<3>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 5: return launch_acf<5>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 7: return launch_acf<7>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 9: return launch_acf<9>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 11: return launch_acf<11>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        default: return cudaErrorInvalidValue;
+    }
+}
 
 size_t autocorr_colwalk_bytes(int q, GridDesc g) {
     return size_t(g.h) * g.w * g.tr * q * sizeof(unsigned);

@@ -9,6 +9,8 @@
 
 namespace tmk {
 
+constexpr int kU8PadRows = 16;  // zero rows stored below every 8-bit image
+
 struct DevStats {  // WindowStats (stats.hpp:35-47) resident in HBM
     double* mu = nullptr;
     double* omega = nullptr;
@@ -93,7 +95,12 @@ bool autocorr_two_pass_supported(int n, GridDesc g);
 cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
                                  DevStats st, double retain_threshold, double* map,
                                  unsigned long long* n_r, int* H, cudaStream_t s);
-// Column-walk variant (preferred): V scratch of autocorr_colwalk_bytes(q, g) bytes.
+// Fused sliding-window variant (preferred): no scratch, one launch.
+bool autocorr_fused_supported(int m, int n, GridDesc g);
+cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
+                              DevStats st, double retain_threshold, double* map,
+                              unsigned long long* n_r, cudaStream_t s);
+// Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.
 size_t autocorr_colwalk_bytes(int q, GridDesc g);
 bool autocorr_colwalk_supported(int m, int q, GridDesc g);
 cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, GridDesc g,

@@ -249,3 +249,31 @@ def test_context_closed_before_its_images(port):
     im.close()
     b = port.brute(t.astype(np.float64), img.astype(np.float64))
     assert (r.best_row, r.best_col) == (b.best_row, b.best_col)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(9, 7), (16, 16), (33, 20)])
+def test_fused_autocorr_equals_colwalk(port, m, n):
+    """The fused sliding-window R_co kernel and the column-walk pair agree bit for bit
+    (clipped last group row/column included) and match the oracle."""
+    import os
+    from paper_1407_3535_b200 import api
+    rng = np.random.default_rng(m * 100 + n)
+    base = np.cumsum(np.cumsum(rng.normal(size=(101, 87)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    maps = {}
+    for path in ("fused", "colwalk"):
+        os.environ["TMATCH_AUTOCORR"] = path
+        try:
+            c = api.Context(0)
+        finally:
+            os.environ.pop("TMATCH_AUTOCORR", None)
+        im = c.image(img)
+        for h in (1, 3, 5, 7, 9, 11):
+            maps[(path, h)] = c.local_autocorrelation(im, m, n, h, h)
+        im.close()
+        c.close()
+    for h in (1, 3, 5, 7, 9, 11):
+        want = port.local_autocorrelation(img.astype(np.float64), m, n, h, h)
+        assert np.array_equal(maps[("fused", h)], maps[("colwalk", h)]), h
+        assert np.array_equal(maps[("fused", h)], want), h
