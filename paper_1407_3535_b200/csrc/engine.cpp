@@ -194,8 +194,8 @@ struct tm_ctx {
     DBuf<double> td;
     DBuf<int> rows_list;
     DBuf<double> map_tmp, map_user;
-    DBuf<double> egs_maps[3];
-    Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt;
+    DBuf<double> egs_maps[4];
+    Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
     // row-strip search protocol state (tm_strip_search_*)
     struct StripState {
         bool active = false;
@@ -666,7 +666,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
 // Launch the R_co map + retained count for one group size; n_r lands in *nr (device).
 void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
-                     double thr, double* map, unsigned long long* nr) {
+                     double thr, double* map, unsigned long long* nr, const int* stop = nullptr) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
@@ -674,7 +674,8 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
         if (ctx->ac_fused && tmk::autocorr_fused_supported(m, n, g)) {
-            CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
+            CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, stop,
+                                      ctx->s));
             ctx->add(1);
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
@@ -762,16 +763,24 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     double prev_cost = std::numeric_limits<double>::infinity();
     int h = h0, w = w0;
     bool done = false;
-    // Candidates are launched in batches of up to three group sizes and decided after one
-    // readback; the accept/stop sequence is exactly egs.cpp:61-88 (a candidate after the
-    // first rejection is computed but ignored).
+    // Candidates are launched in batches of up to four group sizes and decided after one
+    // readback; the accept/stop sequence is exactly egs.cpp:61-88.  A one-thread kernel
+    // replays the same decision on the device after each candidate, so candidates the host
+    // is going to ignore (after the first rejection) exit at entry instead of running.
+    double* dprev = reinterpret_cast<double*>(ctx->counters.p + 20);
+    int* dstop = reinterpret_cast<int*>(ctx->counters.p + 21);
+    {
+        const double inf = std::numeric_limits<double>::infinity();
+        CK(cudaMemsetAsync(dstop, 0, sizeof(int), ctx->s));
+        ctx->pin_egs.upload(dprev, &inf, sizeof inf, ctx->s);
+    }
     while (!done) {
         struct Cand {
             int h, w;
-        } cand[3];
+        } cand[4];
         int nc = 0;
         int hh = h, ww = w;
-        for (; nc < 3;) {
+        for (; nc < 4;) {
             cand[nc++] = Cand{hh, ww};
             if ((hh >= er && ww >= ec) || (hh >= cap && ww >= cap)) break;
             hh = std::min(hh + 2, cap);
@@ -780,9 +789,15 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         for (int k = 0; k < nc; ++k) {
             const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
             ctx->egs_maps[k].ensure(E);
-            autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p, ctx->counters.p + 8 + k);
+            autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p, ctx->counters.p + 8 + k,
+                            dstop);
+            if (k + 1 < nc) {
+                CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
+                                   cand[k].w, xi, cap, ctx->s));
+                ctx->add(1);
+            }
         }
-        unsigned long long nr[3] = {0, 0, 0};
+        unsigned long long nr[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
         for (int k = 0; k < nc; ++k) {

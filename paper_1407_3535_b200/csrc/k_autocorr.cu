@@ -563,7 +563,8 @@ template <int H>
 __global__ void __launch_bounds__(512)
     k_acf(const uint8_t* __restrict__ img, int p, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int tw,
-          int seg) {
+          int seg, const int* __restrict__ stop) {
+    if (stop && *stop) return;  // EGS already decided (egs_decide): candidate not needed
     constexpr int hr = H / 2;
     extern __shared__ __align__(16) unsigned acf_smem[];
     const int NY = blockDim.x;
@@ -595,26 +596,33 @@ __global__ void __launch_bounds__(512)
     const uint8_t* lb = cb + unsigned(cr + hr) * unsigned(q);
     const uint8_t* ta = la;
     const uint8_t* tb = lb;
-    auto lead = [&]() {
+    auto lead_v = [&](unsigned a, unsigned b) {
 #pragma unroll
         for (int d = 0; d < H - 1; ++d) rl[d] = rl[d + 1];
-        rl[H - 1] = unsigned(__ldg(lb));
-        const unsigned a = unsigned(__ldg(la));
-        la += q;
-        lb += q;
+        rl[H - 1] = b;
 #pragma unroll
         for (int d = 0; d < H; ++d) V[d] += a * rl[d];  // di = d - hr
     };
-    auto trail = [&]() {  // remove the row m above the leading edge
+    auto trail_v = [&](unsigned a, unsigned b) {  // remove the row m above the leading edge
 #pragma unroll
         for (int d = 0; d < H - 1; ++d) rt[d] = rt[d + 1];
-        rt[H - 1] = unsigned(__ldg(tb));
-        const unsigned a = unsigned(__ldg(ta));
-        ta += q;
-        tb += q;
+        rt[H - 1] = b;
 #pragma unroll
         for (int d = 0; d < H; ++d) V[d] -= a * rt[d];
     };
+    auto lead = [&]() {
+        const unsigned b = unsigned(__ldg(lb)), a = unsigned(__ldg(la));
+        la += q;
+        lb += q;
+        lead_v(a, b);
+    };
+    auto trail = [&]() {
+        const unsigned b = unsigned(__ldg(tb)), a = unsigned(__ldg(ta));
+        ta += q;
+        tb += q;
+        trail_v(a, b);
+    };
+
     // warm-up: the first window rows [cr, cr+m)
     {
         int x = cr;
@@ -783,7 +791,8 @@ AcfGeom acf_geom(int m, int n, GridDesc gd) {
 
 template <int H>
 cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc gd, DevStats st,
-                       double thr, double* map, unsigned long long* n_r, cudaStream_t s) {
+                       double thr, double* map, unsigned long long* n_r, const int* stop,
+                       cudaStream_t s) {
     const AcfGeom a = acf_geom(m, n, gd);
     if (a.ny == 0) return cudaErrorInvalidValue;
     static bool attr = false;
@@ -794,7 +803,7 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
         k_acf<H><<<grid, a.ny, a.smem, s>>>(img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
-                                            a.seg);
+                                            a.seg, stop);
     return cudaGetLastError();
 }
 
@@ -993,6 +1002,33 @@ size_t autocorr_rowsum_bytes(int p, GridDesc g) {  // H and its transposed prefi
 bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h, g.w); }
 
 
+// One EGS acceptance step on the device (egs.cpp:61-88 with total_cost of egs.cpp:28-37,
+// the same FP64 operations as the host replay in engine.cpp): after candidate (h, w) with
+// retained count *n_r, set *stop when it is rejected or is the last one, so the kernels of
+// the remaining candidates of the batch exit at entry.  The host still decides from the
+// counts; this only skips work the host would ignore.
+__global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
+                             int ec, int h, int w, double xi, int cap) {
+    if (*stop) return;
+    const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
+    const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
+    const double prev = *prev_cost;
+    const bool first = !(fabs(prev) <= 1.7976931348623157e308);  // !isfinite
+    const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(xi, prev);
+    if (!accepted) {
+        *stop = 1;
+        return;
+    }
+    *prev_cost = total;
+    if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
+}
+
+cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
+                       int h, int w, double xi, int cap, cudaStream_t s) {
+    k_egs_decide<<<1, 1, 0, s>>>(n_r, prev_cost, stop, er, ec, h, w, xi, cap);
+    return cudaGetLastError();
+}
+
 bool autocorr_fused_supported(int m, int n, GridDesc g) {
     // 32-bit row offsets; the walk may read h/2 <= kU8PadRows rows below the image
     const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
@@ -1002,14 +1038,14 @@ bool autocorr_fused_supported(int m, int n, GridDesc g) {
 
 cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
                               DevStats st, double retain_threshold, double* map,
-                              unsigned long long* n_r, cudaStream_t s) {
+                              unsigned long long* n_r, const int* stop, cudaStream_t s) {
     switch (gd.h) {
-        case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
-        case 3: return launch_acf<3>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
-        case 5: return launch_acf<5>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
-        case 7: return launch_acf<7>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
-        case 9: return launch_acf<9>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
-        case 11: return launch_acf<11>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, s);
+        case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 3: return launch_acf<3>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 5: return launch_acf<5>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 7: return launch_acf<7>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 9: return launch_acf<9>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 11: return launch_acf<11>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
         default: return cudaErrorInvalidValue;
     }
 }

@@ -10,6 +10,8 @@
 // prefix[r] + row_acc) is rebuilt in the same operation order -- one thread scans one
 // row (through a shared-memory transpose for coalescing), one thread accumulates one
 // column -- and window sums use the reference's difference order (stats.cpp:50).
+#include <algorithm>
+
 #include "kernels.hpp"
 #include "tm_common.cuh"
 
@@ -288,9 +290,116 @@ cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, d
     return cudaGetLastError();
 }
 
+namespace {
+
+// Fused window statistics (preferred integer path).  CTA = (column tile [c0, c0+tw),
+// segment of extent rows); thread = one image column of the tile plus its n-1 halo.  Each
+// thread slides the vertical sums s(y) = sum_{a<m} I(r+a, y) and q(y) (squares) down the
+// rows (leading row in, row m above out; exact u32), and at every extent row the CTA
+// scans s and q along y (warp prefixes + double-buffered warp totals, one barrier per
+// row) so the window sums are S = P[c+n-1] - P[c-1].  The FP64 epilogue
+// (stats.cpp:84-91) runs on consecutive columns, so mu/omega/flat are written coalesced.
+__global__ void __launch_bounds__(512)
+    k_wstats_u8(const uint8_t* __restrict__ img, int p, int q, int m, int n, int tw, int seg,
+                const double* __restrict__ pn, DevStats st) {
+    __shared__ unsigned ls[2][2][512], wtot[2][2][16];
+    const int NY = blockDim.x;
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int er = p - m + 1, ec = q - n + 1;
+    const int c0 = blockIdx.x * tw;
+    const int r0 = blockIdx.y * seg, r1 = min(r0 + seg, er);
+    if (r0 >= er || c0 >= ec) return;
+    const int y = min(c0 + int(threadIdx.x), q - 1);  // clamped halo columns are never read
+    const uint8_t* lead = img + size_t(r0) * q + y;
+    const uint8_t* trail = lead;
+    unsigned vs = 0, vq = 0;
+#pragma unroll 4
+    for (int a = 0; a < m; ++a) {
+        const unsigned v = __ldg(lead);
+        lead += q;
+        vs += v;
+        vq += v * v;
+    }
+    const double inv_mn = 1.0 / (double(m) * double(n));
+    const long long mn = (long long)m * n;
+    const double prefix_noise = *pn;
+    const int c = c0 + int(threadIdx.x);
+    const bool out_ok = int(threadIdx.x) < tw && c < ec;
+    const int i1 = threadIdx.x + n - 1, w1 = i1 >> 5;
+    const int w0 = threadIdx.x > 0 ? (int(threadIdx.x) - 1) >> 5 : 0;
+    int par = 0;
+    // next row's leading/trailing pixels, loaded before this row's scan + epilogue so the
+    // load latency hides behind them
+    unsigned vi = 0, vo = 0;
+#pragma unroll 1
+    for (int r = r0;;) {
+        if (r + 1 < r1) {
+            vi = __ldg(lead);
+            vo = __ldg(trail);
+        }
+        unsigned a = vs, b = vq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned ta = __shfl_up_sync(0xffffffffu, a, o);
+            const unsigned tb = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                a += ta;
+                b += tb;
+            }
+        }
+        ls[par][0][threadIdx.x] = a;
+        ls[par][1][threadIdx.x] = b;
+        if (lane == 31) {
+            wtot[par][0][wid] = a;
+            wtot[par][1][wid] = b;
+        }
+        __syncthreads();
+        if (out_ok) {
+            unsigned S = ls[par][0][i1], Q = ls[par][1][i1];
+            if (threadIdx.x > 0) {
+                S -= ls[par][0][threadIdx.x - 1];
+                Q -= ls[par][1][threadIdx.x - 1];
+            }
+            for (int ww = w0; ww < w1; ++ww) {
+                S += wtot[par][0][ww];
+                Q += wtot[par][1][ww];
+            }
+            double mu, om;
+            uint8_t fl;
+            window_epilogue(double(S), double(Q), inv_mn, mn, prefix_noise, mu, om, fl);
+            const size_t k = size_t(r) * ec + c;
+            st.mu[k] = mu;
+            st.omega[k] = om;
+            st.flat[k] = fl;
+        }
+        par ^= 1;
+        if (++r >= r1) break;
+        lead += q;
+        trail += q;
+        vs += vi - vo;
+        vq += vi * vi - vo * vo;
+    }
+}
+
+}  // namespace
+
 cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s) {
     const int ec = q - n + 1, er = p - m + 1;
+    // fused path: u32 sums exact while m*n*255^2 < 2^32; column tile + halo <= 512 threads
+    if (double(m) * double(n) * 65025.0 < 4294967296.0 && n <= 384) {
+        int ny = std::max(128, ((2 * n + 31) / 32) * 32);
+        ny = std::min(ny, 512);
+        const int tw = ny - n + 1;
+        const int ntiles = (ec + tw - 1) / tw;
+        // segments: ~4 resident waves of CTAs, each walking at least 2m rows of output
+        int nseg = std::max(1, (148 * 16) / ntiles);
+        int seg = std::max(std::min(m, 64), (er + nseg - 1) / nseg);
+        nseg = (er + seg - 1) / seg;
+        dim3 grid(ntiles, nseg);
+        k_wstats_u8<<<grid, ny, 0, s>>>(img, p, q, m, n, tw, seg, prefix_noise, st);
+        return cudaGetLastError();
+    }
     const int tpr = (ec + kChunk - 1) / kChunk;
     dim3 g1((tpr + 127) / 128, p);
     k_hsum_u8<<<g1, 128, 0, s>>>(img, p, q, n, hs, hq);

@@ -277,3 +277,16 @@ def test_fused_autocorr_equals_colwalk(port, m, n):
         want = port.local_autocorrelation(img.astype(np.float64), m, n, h, h)
         assert np.array_equal(maps[("fused", h)], maps[("colwalk", h)]), h
         assert np.array_equal(maps[("fused", h)], want), h
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(1, 1), (5, 7), (33, 64), (64, 200), (130, 3)])
+def test_window_stats_fused_tiles(ctx, port, m, n):
+    """Fused window statistics over several column tiles and row segments, with flat
+    patches (variance exactly zero and near the noise floor), equal to the oracle."""
+    rng = np.random.default_rng(m * 1000 + n)
+    img = rng.integers(0, 256, (300, 700)).astype(np.uint8)
+    img[40:200, 100:400] = 77  # flat region
+    img[210:260, 500:690] = rng.integers(100, 102, (50, 190))  # tiny variance
+    gi = ctx.image(img)
+    _ws_equal(ctx.window_stats(gi, m, n), port.window_stats(img.astype(np.float64), m, n))
