@@ -29,7 +29,7 @@ NVCC_FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
 CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextra",
              "-I" + INCLUDE, "-I" + CSRC, "-I" + os.path.join(CUDA_HOME, "include")]
 
-CU_SOURCES = ["k_stats.cu", "k_autocorr.cu", "k_corr.cu", "k_opta.cu"]
+CU_SOURCES = ["k_stats.cu", "k_autocorr.cu", "k_corr.cu", "k_opta.cu", "k_tc.cu"]
 CUDA_LIB_SOURCES = ["engine.cpp"]
 API_SOURCES = ["tmatch_api.cpp"]
 HEADERS = ["kernels.hpp", "tm_common.cuh"]

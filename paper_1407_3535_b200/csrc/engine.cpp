@@ -213,6 +213,13 @@ struct tm_ctx {
     // R_co kernel choice: fused sliding-window (default) or the column-walk + line-scan pair
     // (TMATCH_AUTOCORR=colwalk; kept for A/B measurements and as a cross-check in tests)
     bool ac_fused = true;
+    // integer tensor-core correlation (tcgen05 kind::i8) for centre scans / dense work;
+    // TMATCH_TC=0 selects the CUDA-core FP32-exact kernels (A/B measurements, cross-checks)
+    bool tc = true;
+    DBuf<uint8_t> tc_b;
+    DBuf<tmk::TcBand> tc_bands;
+    DBuf<int4> tc_sched;
+    Pinned pin_bands, pin_sched;
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -277,6 +284,9 @@ struct tm_image {
     DBuf<double> pn;           // [0] q_total (FP64 path) / [1] prefix_noise
     DBuf<unsigned long long> qt;
     std::map<std::pair<int, int>, std::unique_ptr<WS>> ws_cache;
+    // 16-byte pitched zero-padded 8-bit copy for the tensor-core path (k_tc.cu)
+    DBuf<uint8_t> u8p;
+    int u8p_pitch = 0;
 };
 
 struct tm_prep {
@@ -516,6 +526,100 @@ int row_span(const std::vector<int>& rows) {
     return span;
 }
 
+
+// ---- integer tensor-core path (k_tc.cu) -------------------------------------------------
+constexpr size_t kTcSmemBudget = 224 * 1024;  // 227 KB opt-in minus static shared memory
+
+bool tc_path(tm_ctx* ctx, const tm_image* img, const Tmpl& T) {
+    return ctx->tc && fp32_path(img, T) && tmk::tc_supported(T.m, T.n) &&
+           tmk::tc_plan(T.m, T.n, 1, kTcSmemBudget).nch > 0;
+}
+
+const uint8_t* tc_image(tm_ctx* ctx, tm_image* img, int ec) {
+    const int pitch = tmk::tc_pitch(img->q, ec);
+    if (img->u8p_pitch != pitch) {
+        const int rows = img->p + 1;
+        img->u8p.ensure(size_t(rows) * pitch);
+        CK(tmk::tc_pitch_image(img->u8.p, img->p, img->q, img->u8p.p, pitch, rows, ctx->s));
+        ctx->add(1);
+        img->u8p_pitch = pitch;
+    }
+    return img->u8p.p;
+}
+
+// Bands of up to `rmax` output rows r0 + sr*k; a list of rows with irregular spacing
+// becomes single-row bands.
+std::vector<tmk::TcBand> tc_bands(const std::vector<int>& rows, const std::vector<int>& yi, int sr,
+                                  int rmax) {
+    std::vector<tmk::TcBand> out;
+    size_t i = 0;
+    while (i < rows.size()) {
+        size_t j = i + 1;
+        while (j < rows.size() && int(j - i) < rmax && rows[j] - rows[j - 1] == sr &&
+               yi[j] - yi[j - 1] == 1)
+            ++j;
+        const int cnt = int(j - i);
+        out.push_back(tmk::TcBand{rows[i], cnt > 1 ? sr : 1, cnt, yi[i]});
+        i = j;
+    }
+    return out;
+}
+
+// Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
+int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const std::vector<int>& rows,
+           const std::vector<int>& yi, int sr, tmk::TcTask task) {
+    const tmk::TcPlan plan = tmk::tc_plan(T.m, T.n, sr, kTcSmemBudget);
+    if (plan.nch == 0) invalid("tensor-core plan unavailable");
+    ctx->tc_b.ensure(plan.total_bytes);
+    CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s));
+    const int ntc = (ws.ec + tmk::tc_tile_cols() - 1) / tmk::tc_tile_cols();
+    // rows per band: as many as the tiles allow while keeping >= 2 tiles per SM
+    int rmax = 16;
+    while (rmax > 1 && size_t((rows.size() + rmax - 1) / rmax) * ntc < 148) rmax /= 2;
+    const std::vector<tmk::TcBand> bands = tc_bands(rows, yi, sr, rmax);
+    ctx->tc_bands.ensure(bands.size());
+    ctx->pin_bands.upload(ctx->tc_bands.p, bands.data(), bands.size() * sizeof(tmk::TcBand), ctx->s);
+    tmk::TcJob job{};
+    job.imgp = tc_image(ctx, img, ws.ec);
+    job.pitch = img->u8p_pitch;
+    job.bglob = ctx->tc_b.p;
+    job.plan = plan;
+    job.ts = T.ts;
+    job.st = ws.dev();
+    task.bands = ctx->tc_bands.p;
+    task.nbands = int(bands.size());
+    task.ntc = ntc;
+    const std::vector<int> sched = tmk::tc_schedule(plan, rmax, task.sched_off, task.sched_len);
+    ctx->tc_sched.ensure(sched.size() / 4 + 1);
+    ctx->pin_sched.upload(ctx->tc_sched.p, sched.data(), sched.size() * sizeof(int), ctx->s);
+    task.sched = ctx->tc_sched.p;
+    task.sched_total = int(sched.size() / 4);
+    int np = 0;  // caller sizes ctx->partials for >= 148 entries
+    static const bool dbg = std::getenv("TMATCH_TC_DEBUG") != nullptr;
+    DBuf<long long> dbuf;
+    if (dbg) {
+        dbuf.ensure(148 * 8);
+        CK(cudaMemsetAsync(dbuf.p, 0, 148 * 8 * 8, ctx->s));
+        task.dbg = dbuf.p;
+        task.dbg_flags = std::atoi(std::getenv("TMATCH_TC_DEBUG"));
+    }
+    CK(tmk::tc_corr(job, task, ctx->partials.p, &np, ctx->s));
+    ctx->add(2);
+    if (dbg) {
+        std::vector<long long> h(148 * 8);
+        CK(cudaMemcpyAsync(h.data(), dbuf.p, h.size() * 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        double a[8] = {};
+        for (int b = 0; b < np; ++b)
+            for (int j = 0; j < 8; ++j) a[j] += double(h[b * 8 + j]) / np;
+        std::fprintf(stderr,
+                     "[tc] ctas=%d bands=%d ntc=%d rows/cta=%.0f | producer total=%.0f wait_empty=%.0f "
+                     "wait_bempty=%.0f | mma total=%.0f wait_full=%.0f wait_dempty=%.0f wait_bfull=%.0f\n",
+                     np, task.nbands, task.ntc, a[3], a[0], a[1], a[2], a[4], a[5], a[6], a[7]);
+    }
+    return np;
+}
+
 void upload_rows(tm_ctx* ctx, const std::vector<int>& rows) {
     ctx->rows_list.ensure(rows.size());
     ctx->pin_rows.upload(ctx->rows_list.p, rows.data(), rows.size() * 4, ctx->s);
@@ -561,6 +665,46 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     const int wr = g.w / 2;
     Phase ph(ctx, "centre_scan");
+    if (tc_path(ctx, img, T) && g.h <= tmk::kTcMaxClasses) {
+        const int nstrip = g.ti_hi - g.ti_lo;
+        if (nstrip <= 0) {
+            reduce_to(ctx, 0, 0);
+            return;
+        }
+        std::vector<int> rows(nstrip), yi(nstrip);
+        for (int ti = g.ti_lo; ti < g.ti_hi; ++ti) {
+            rows[ti - g.ti_lo] = centre_row_h(g, ti);
+            yi[ti - g.ti_lo] = ti;
+        }
+        const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
+        const int nc_reg = clipped ? g.tc - 1 : g.tc;
+        int n1 = 0, n2 = 0;
+        // partials: <= 148 from the tensor-core kernel + the clipped column's list blocks
+        // (sized once: a later ensure() could reallocate under pending writes)
+        ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
+        {
+            // exact centre dots on the tensor cores -> dotbuf (the clipped last group
+            // column included, at tj = tc-1), then the FP64 epilogue
+            ctx->dotbuf.ensure(G);
+            tmk::TcTask task{};
+            task.mode = 1;
+            task.cbase = wr;
+            task.cstep = g.w;
+            task.nc = nc_reg;
+            task.tc = g.tc;
+            task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
+            task.out_rho = ctx->dotbuf.p;
+            tc_run(ctx, img, ws, T, rows, yi, g.h, task);
+            upload_rows(ctx, rows);
+            n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
+            CK(tmk::centre_epilogue(job, g, ctx->rows_list.p, wr, g.w, g.tc, 0, ctx->dotbuf.p,
+                                    ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
+                                    task.c_last));
+            ctx->add(1);
+        }
+        reduce_to(ctx, n1 + n2, 0);
+        return;
+    }
     if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
         const int nstrip = g.ti_hi - g.ti_lo;
         if (nstrip <= 0) {
@@ -574,7 +718,9 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         const int nc_reg = clipped ? g.tc - 1 : g.tc;
         const int np_main = nc_reg > 0 ? band_partials(nstrip, nc_reg, g.w) : 0;
         const int np_last = clipped ? band_partials(nstrip, 1, 1) : 0;
-        ctx->partials.ensure(size_t(np_main + np_last) + 1);
+        // sized once for every writer below (a later ensure() could reallocate under
+        // pending writes): the band or K-split epilogue partials + the clipped column
+        ctx->partials.ensure(size_t(std::max(np_main, kListBlocks) + np_last) + 1);
         int n1 = 0, n2 = 0;
         tmk::BandTask t{};
         t.rows = ctx->rows_list.p;
@@ -631,7 +777,6 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             ctx->seq_rho.ensure(size_t(nstrip));
             ctx->seq_deg.ensure(size_t(nstrip));
             n2 = std::min(kListBlocks, (nstrip + 7) / 8);
-            ctx->partials.ensure(size_t(n1 + n2) + 1);
             CK(tmk::corr_list(job, ctx->seed_locs.p, ctx->counters.p + 12, nstrip, ctx->seq_rho.p,
                               ctx->seq_deg.p, ctx->partials.p + n1, n2, ctx->s));
             const size_t off = size_t(g.ti_lo) * g.tc;
@@ -693,7 +838,7 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
         }
         return;
     }
-    CK(tmk::autocorr_init(map, g, ctx->s));
+    CK(tmk::autocorr_init(map, g, ctx->s, stop));
     ctx->add(1);
     const int hr = g.h / 2, wr = g.w / 2;
     for (int di = -hr; di <= hr; ++di)
@@ -704,13 +849,13 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             if (ph_ < m || pw < n) continue;
             ctx->rowacc.ensure(size_t(ph_) * pw);
             ctx->prefix.ensure(size_t(ph_ + 1) * (pw + 1));
-            tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0};
+            tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0, stop};
             CK(tmk::replica_prefix(src, ph_, pw, ctx->rowacc.p, ctx->prefix.p, ctx->s));
             CK(tmk::autocorr_offset_epilogue(ctx->prefix.p, ph_, pw, m, n, g, ws.dev(), di, dj,
-                                             map, ctx->s));
+                                             map, ctx->s, stop));
             ctx->add(3);
         }
-    CK(tmk::retained_count(map, g, thr, nr, ctx->s));
+    CK(tmk::retained_count(map, g, thr, nr, ctx->s, stop));
     ctx->add(1);
 }
 
@@ -992,7 +1137,24 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const unsigned long long* count = &ctx->tally.p->survivors;
     uint8_t* visits = ctx->visits.p;
     const bool dense = survivors * 16 > E && fp32_path(img, T);
-    if (dense) {
+    if (dense && tc_path(ctx, img, T)) {
+        const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
+        std::vector<int> rows(std::max(0, rhi - rlo));
+        for (int r = rlo; r < rhi; ++r) rows[r - rlo] = r;
+        tmk::TcTask task{};
+        task.mode = 2;
+        task.c_lim = g.ec;
+        task.c_last = -1;
+        task.mask = visits;
+        task.out_rho = rho_loc;
+        ctx->partials.ensure(148 + 1);
+        int np = 0;
+        if (!rows.empty()) {
+            Phase ph(ctx, "survivor_dense");
+            np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+        }
+        reduce_to(ctx, np, 2);
+    } else if (dense) {
         const tmk::CorrJob job = make_job(ctx, img, ws, T);
         const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
         std::vector<int> rows(std::max(0, rhi - rlo));
@@ -1217,7 +1379,18 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
     }
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     Phase ph(ctx, "brute_dense");
-    if (fp32_path(img, T)) {
+    if (tc_path(ctx, img, T)) {
+        std::vector<int> rows(er);
+        for (int r = 0; r < er; ++r) rows[r] = r;
+        tmk::TcTask task{};
+        task.mode = 0;
+        task.c_lim = ec;
+        task.c_last = -1;
+        task.out_rho = surface;
+        ctx->partials.ensure(148 + 1);
+        const int np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+        reduce_to(ctx, np, 2);
+    } else if (fp32_path(img, T)) {
         std::vector<int> rows(er);
         for (int r = 0; r < er; ++r) rows[r] = r;
         upload_rows(ctx, rows);
@@ -1406,6 +1579,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         auto ctx = std::make_unique<tm_ctx>();
         ctx->device = device;
         if (const char* e = std::getenv("TMATCH_AUTOCORR")) ctx->ac_fused = std::strcmp(e, "colwalk") != 0;
+        if (const char* e = std::getenv("TMATCH_TC")) ctx->tc = std::strcmp(e, "0") != 0;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
         cudaMemPool_t pool;
@@ -1467,6 +1641,7 @@ int tm_image_reset_cache(tm_image* img) {
     return guard(ctx, [&] {
         img->ws_cache.clear();
         img->have_qtotal = false;
+        img->u8p_pitch = 0;
     });
 }
 
@@ -1513,6 +1688,7 @@ int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
         ctx->add(1);
         img->have_f64 = false;
         img->have_qtotal = false;
+        img->u8p_pitch = 0;
         img->ws_cache.clear();
     });
 }

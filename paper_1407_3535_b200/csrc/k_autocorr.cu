@@ -880,7 +880,8 @@ bool ac_supported(int n, int h, int w) {
 
 // ---- replica path helpers ---------------------------------------------------------------
 
-__global__ void k_autocorr_init(double* map, Grid g) {
+__global__ void k_autocorr_init(double* map, Grid g, const int* stop) {
+    if (stop && *stop) return;
     const size_t E = size_t(g.er) * g.ec;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
          k += size_t(gridDim.x) * blockDim.x) {
@@ -895,7 +896,9 @@ __global__ void k_autocorr_init(double* map, Grid g) {
 // whose origin is (orr, occ) (autocorr.cpp:64-76); cross sum at the centre is the window
 // difference at (cr - orr, cc - occ) in stats.cpp:50 order.
 __global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int pw, int m, int n,
-                                  Grid g, DevStats st, int di, int dj, double* __restrict__ map) {
+                                  Grid g, DevStats st, int di, int dj, double* __restrict__ map,
+                                  const int* stop) {
+    if (stop && *stop) return;
     const long long G = (long long)g.tr * g.tc;
     const int orr = max(0, -di), occ = max(0, -dj);
     const size_t ppw = size_t(pw) + 1;
@@ -921,7 +924,8 @@ __global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int
 }
 
 __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
-                           unsigned long long* n_r) {
+                           unsigned long long* n_r, const int* stop) {
+    if (stop && *stop) return;
     const size_t k0 = size_t(g.row_lo()) * g.ec, k1 = size_t(g.row_hi()) * g.ec;
     unsigned long long local = 0;
     for (size_t k = k0 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < k1;
@@ -1133,27 +1137,28 @@ cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n,
     return cudaGetLastError();
 }
 
-cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s) {
+cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s, const int* stop) {
     const size_t E = size_t(g.er) * g.ec;
     const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 16));
-    k_autocorr_init<<<blocks, 256, 0, s>>>(map, to_grid(g));
+    k_autocorr_init<<<blocks, 256, 0, s>>>(map, to_grid(g), stop);
     return cudaGetLastError();
 }
 
 cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
                                      GridDesc g, DevStats st, int di, int dj, double* map,
-                                     cudaStream_t s) {
+                                     cudaStream_t s, const int* stop) {
     const long long G = (long long)g.tr * g.tc;
     const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 16));
-    k_autocorr_offset<<<blocks, 256, 0, s>>>(prefix, ph, pw, m, n, to_grid(g), st, di, dj, map);
+    k_autocorr_offset<<<blocks, 256, 0, s>>>(prefix, ph, pw, m, n, to_grid(g), st, di, dj, map,
+                                             stop);
     return cudaGetLastError();
 }
 
 cudaError_t retained_count(const double* map, GridDesc g, double threshold,
-                           unsigned long long* n_r, cudaStream_t s) {
+                           unsigned long long* n_r, cudaStream_t s, const int* stop) {
     const size_t E = size_t(g.er) * g.ec;
     const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 16));
-    k_retained<<<blocks, 256, 0, s>>>(map, to_grid(g), threshold, n_r);
+    k_retained<<<blocks, 256, 0, s>>>(map, to_grid(g), threshold, n_r, stop);
     return cudaGetLastError();
 }
 

@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(NW * 32)
 __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
-                 CellH* partials) {
+                 CellH* partials, int c_last) {
     __shared__ Cell scratch[8];
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
@@ -211,7 +211,8 @@ __global__ void __launch_bounds__(256)
     for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
          it += (long long)gridDim.x * blockDim.x) {
         const int yi = int(it / nc), k = int(it % nc);
-        const int r = rows[yi], c = cbase + k * sw;
+        const int r = rows[yi];
+        const int c = (c_last >= 0 && col0 + k == g.tc - 1) ? c_last : cbase + k * sw;
         const size_t gi = size_t(g.ti_lo + yi) * g.tc + col0 + k;
         const size_t kk = size_t(r) * job.st.ec + c;
         const bool wflat = job.st.flat[kk];
@@ -660,9 +661,9 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
 
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
-                            CellH* partials, int n_partials, cudaStream_t s) {
+                            CellH* partials, int n_partials, cudaStream_t s, int c_last) {
     k_centre_epi<<<n_partials, 256, 0, s>>>(job, to_grid(g), rows, cbase, sw, nc, col0, dot, rho_c,
-                                            deg_c, partials);
+                                            deg_c, partials, c_last);
     return cudaGetLastError();
 }
 

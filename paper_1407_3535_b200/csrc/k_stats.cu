@@ -164,6 +164,7 @@ __device__ __forceinline__ double src_value(const ProdSrc& s, int a, int b) {
 // reads/writes stay coalesced while each lane scans its own row sequentially
 // (row_acc += v, stats.cpp:34).
 __global__ void k_rowscan(ProdSrc src, int rows, int cols, double* __restrict__ rowacc) {
+    if (src.stop && *src.stop) return;
     __shared__ double tile[4][32][33];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int r0 = (blockIdx.x * 4 + wid) * 32;
@@ -192,7 +193,8 @@ __global__ void k_rowscan(ProdSrc src, int rows, int cols, double* __restrict__ 
 
 // prefix[(r+1)][c+1] = prefix[r][c+1] + rowacc[r][c]  (stats.cpp:35), one thread per column.
 __global__ void k_colacc(const double* __restrict__ rowacc, int rows, int cols,
-                         double* __restrict__ prefix) {
+                         double* __restrict__ prefix, const int* stop) {
+    if (stop && *stop) return;
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t pw = size_t(cols) + 1;
     if (c > cols) return;
@@ -303,7 +305,6 @@ __global__ void __launch_bounds__(512)
     k_wstats_u8(const uint8_t* __restrict__ img, int p, int q, int m, int n, int tw, int seg,
                 const double* __restrict__ pn, DevStats st) {
     __shared__ unsigned ls[2][2][512], wtot[2][2][16];
-    const int NY = blockDim.x;
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int er = p - m + 1, ec = q - n + 1;
     const int c0 = blockIdx.x * tw;
@@ -423,7 +424,7 @@ cudaError_t replica_prefix(ProdSrc src, int rows, int cols, double* rowacc, doub
                            cudaStream_t s) {
     const int warps = (rows + 31) / 32;
     k_rowscan<<<(warps + 3) / 4, 128, 0, s>>>(src, rows, cols, rowacc);
-    k_colacc<<<(cols + 1 + 127) / 128, 128, 0, s>>>(rowacc, rows, cols, prefix);
+    k_colacc<<<(cols + 1 + 127) / 128, 128, 0, s>>>(rowacc, rows, cols, prefix, src.stop);
     return cudaGetLastError();
 }
 

@@ -1,0 +1,611 @@
+// k_tc.cu -- integer tensor-core correlation (tcgen05.mma kind::i8, sm_100a).
+//
+// window_dot (detail.hpp:32-41) on 8-bit data is a sum of u8*u8 products; the 5th-gen
+// tensor cores compute it exactly (s32 accumulation, m*n*255^2 < 2^31), so the dot that
+// feeds the FP64 zncc_at epilogue (detail.hpp:45-51) is bit-identical to the CUDA-core
+// path and to the reference.
+//
+// Formulation.  For an output row r and a 2048-column tile c0, write the column as
+// c = c0 + 16a + phi (a < 128 = MMA M, phi < 16).  Then
+//     out[r, c] = sum_i sum_t I[r+i, c0 + 16a + t] * T[i, t - phi]     (t < Kx)
+// so for image row x = r+i the A operand A_x[a, t] = I[x, c0 + 16a + t] is a Toeplitz
+// view of ONE staged image row: a no-swizzle K-major shared-memory descriptor with core
+// matrix rows 16 B apart (LBO = 16 B between K halves, SBO = 128 B between 8-row groups)
+// reads row a at byte 16a -- no im2col is materialised.  B[(i, phi), t] = T[i, t - phi]
+// holds the template rows at the 16 column phases (built once per template).
+// A CTA owns a band of R output rows r_k = r0 + sr*k (sr = group height for the centre
+// scan, 1 for dense work) and accumulates D[a, (k, phi)] in TMEM; image row x feeds every
+// k with 0 <= x - r_k < m in ONE MMA chain whose N = 16 * (#k): the B rows it needs are
+// T rows x - r_k, descending by sr, which is one contiguous window when B is stored
+// grouped by (row mod sr) in descending row order.
+//
+// Roles (one CTA per SM, persistent over (band, column tile) tiles):
+//   warp 0      producer: cp.async.bulk of image rows (from a 16-byte pitched copy) into a
+//               ring of shared-memory slots, and of the B chunk; mbarrier expect_tx.
+//   warp 1      TMEM allocation; one elected thread issues the MMAs and commits.
+//   warps 2..5  epilogue: tcgen05.ld of the exact s32 dots, FP64 ZNCC, argmax / outputs;
+//               re-zero the TMEM buffer and hand it back (double buffered).
+#include <algorithm>
+#include <cstdio>
+#include <vector>
+
+#include "kernels.hpp"
+#include "tm_common.cuh"
+
+namespace tmk {
+
+namespace {
+
+constexpr int kTcThreads = 320;  // producer, MMA, 8 epilogue warps
+constexpr int kTcMaxStages = 64;
+constexpr int kTcBarBytes = 2048;  // barriers + TMEM slot at the start of shared memory
+constexpr int kTcCols = 2048;  // output columns per tile (M=128 rows x 16 phases)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// shared-memory matrix descriptor, no swizzle, SM100 version field = 1
+__device__ __forceinline__ uint64_t sdesc(uint32_t addr, uint32_t lbo, uint32_t sbo) {
+    return uint64_t((addr >> 4) & 0x3FFF) | (uint64_t((lbo >> 4) & 0x3FFF) << 16) |
+           (uint64_t((sbo >> 4) & 0x3FFF) << 32) | (uint64_t(1) << 46);
+}
+
+// instruction descriptor: kind::i8, u8 x u8 -> s32, K-major A and B, M = 128
+__device__ __forceinline__ uint32_t idesc_i8(int n) {
+    return (2u << 4) | (uint32_t(n >> 3) << 17) | (uint32_t(128 >> 4) << 24);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes));
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)));
+}
+
+// bounded wait: a protocol error traps (kernel error) instead of hanging the device.
+// Waiters off the MMA critical path back off with nanosleep so their polling does not
+// steal issue slots from the MMA warp on the same SM sub-partition.
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity, int sleep_ns = 0) {
+    uint32_t ok = 0;
+    for (long long it = 0;; ++it) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(ok)
+            : "r"(smem_u32(b)), "r"(parity)
+            : "memory");
+        if (ok) return;
+        if (sleep_ns) __nanosleep(sleep_ns);
+        if (it > (1ll << 26)) __trap();
+    }
+}
+
+__device__ __forceinline__ void mbar_wait_t(uint64_t* b, uint32_t parity, long long* acc,
+                                            int sleep_ns = 0) {
+    if (!acc) {
+        mbar_wait(b, parity, sleep_ns);
+        return;
+    }
+    const long long t0 = clock64();
+    mbar_wait(b, parity, sleep_ns);
+    *acc += clock64() - t0;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(b))
+        : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t addr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15])
+        : "r"(addr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void tmem_zero16(uint32_t addr) {
+    const uint32_t z = 0;
+    asm volatile(
+        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(
+            addr),
+        "r"(z)
+        : "memory");
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask task, CellH* partials) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    const TcPlan& P = job.plan;
+    const int kTcStages = P.stages;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
+    int4* ssched = reinterpret_cast<int4*>(sm + kTcBarBytes);  // staged row schedule
+    uint8_t* sB = sm + P.header;                // B chunk (P.b_smem bytes)
+    uint8_t* sA = sB + P.b_smem;                // ring of P.stages image-row slots
+    uint64_t* full = bars;                      // [kTcMaxStages]
+    uint64_t* empty = bars + kTcMaxStages;      // [kTcMaxStages]
+    uint64_t* bfull = bars + 2 * kTcMaxStages;
+    uint64_t* bempty = bfull + 1;
+    uint64_t* dfull = bfull + 2;                // [2]
+    uint64_t* dempty = bfull + 4;               // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bfull + 6);
+    __shared__ Cell scratch[8];
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntiles = task.nbands * task.ntc;
+
+    if (tid == 0) {
+        for (int s = 0; s < kTcStages; ++s) {
+            mbar_init(full + s, 1);
+            mbar_init(empty + s, 1);
+        }
+        mbar_init(bfull, 1);
+        mbar_init(bempty, 1);
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(dfull + b, 1);
+            mbar_init(dempty + b, 256);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    const bool sched_smem = task.sched_total * 16 <= P.header - kTcBarBytes;
+    if (sched_smem)
+        for (int i = tid; i < task.sched_total; i += blockDim.x) ssched[i] = __ldg(task.sched + i);
+    const int4* sched = sched_smem ? ssched : task.sched;
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ============================ producer ============================
+        if (lane == 0) {
+            long long w_empty = 0, w_bempty = 0;
+            const long long t_start = clock64();
+            long long* pe = task.dbg ? &w_empty : nullptr;
+            long long* pb = task.dbg ? &w_bempty : nullptr;
+            uint32_t it = 0;   // ring uses
+            uint32_t bl = 0;   // B loads
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const TcBand bd = task.bands[t / task.ntc];
+                const int c0 = (t % task.ntc) * kTcCols;
+                for (int ch = 0; ch < P.nch; ++ch) {
+                    if (P.nch > 1 || bl == 0) {
+                        if (bl > 0) mbar_wait_t(bempty, (bl - 1) & 1, pb, 128);
+                        const uint32_t bytes = uint32_t(P.b_bytes[ch]);
+                        mbar_expect_tx(bfull, bytes);
+                        const uint8_t* src = job.bglob + P.b_off[ch];
+                        for (uint32_t o = 0; o < bytes; o += 32768)
+                            bulk_g2s(sB + o, src + o, min(32768u, bytes - o), bfull);
+                        ++bl;
+                    }
+                    const int4* sc = sched + task.sched_off[ch];
+                    const int ns = task.sched_len[ch];
+                    int s = it % kTcStages;
+                    uint32_t par = ((it / kTcStages) & 1) ^ 1;
+                    for (int e = 0; e < ns; ++e) {
+                        const int4 row = sc[e];  // {dx, k_lo, k_hi, B entry}
+                        if (row.y >= bd.cnt) break;      // rows are in k_lo order
+                        mbar_wait_t(empty + s, par, pe, 64);
+                        if (task.dbg_flags & 1) {  // timing experiment: no copy
+                            mbar_arrive(full + s);
+                        } else {
+                            mbar_expect_tx(full + s, uint32_t(P.a_bytes));
+                            bulk_g2s(sA + size_t(s) * P.a_slot,
+                                     job.imgp + size_t(bd.r0 + row.x) * job.pitch + c0,
+                                     uint32_t(P.a_bytes), full + s);
+                        }
+                        ++it;
+                        if (++s == kTcStages) {
+                            s = 0;
+                            par ^= 1;
+                        }
+                    }
+                }
+            }
+            if (task.dbg) {
+                long long* d = task.dbg + blockIdx.x * 8;
+                d[0] = clock64() - t_start;
+                d[1] = w_empty;
+                d[2] = w_bempty;
+                d[3] = it;
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer ==========================
+        // The whole warp runs the (warp-uniform) loop so descriptors live in uniform
+        // registers; one elected lane issues.  Descriptors are built once and advanced by
+        // adds (16-byte units): A +2 per K-step (32 B), B +16 per K-step (two 128 B core
+        // matrices), N field of idesc at bit 17 in units of 8.
+        long long w_full = 0, w_dempty = 0, w_bfull = 0;
+        const long long t_start = clock64();
+        long long* pf = task.dbg && lane == 0 ? &w_full : nullptr;
+        long long* pd = task.dbg && lane == 0 ? &w_dempty : nullptr;
+        long long* pbf = task.dbg && lane == 0 ? &w_bfull : nullptr;
+        uint32_t it = 0, bl = 0, tl = 0;
+        const uint32_t b_sbo = 128u * uint32_t(P.kx / 16);
+        const uint32_t entry16 = uint32_t(P.kx);  // entry bytes / 16
+        const uint32_t slot16 = uint32_t(P.a_slot) >> 4;
+        const uint64_t a_desc0 = sdesc(smem_u32(sA), 16, 128);
+        const uint64_t b_desc0 = sdesc(smem_u32(sB), 128, b_sbo);
+        const uint32_t idesc0 = idesc_i8(0);
+        const int ksteps = P.kx / 32;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const TcBand bd = task.bands[t / task.ntc];
+            const uint32_t buf = tl & 1;
+            mbar_wait_t(dempty + buf, (tl >> 1) & 1, pd);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            const uint32_t dbase = tmem + buf * 256;
+            for (int ch = 0; ch < P.nch; ++ch) {
+                if (P.nch > 1 || bl == 0) {
+                    mbar_wait_t(bfull, bl & 1, pbf);
+                    ++bl;
+                }
+                const int4* sc = sched + task.sched_off[ch];
+                const int ns = task.sched_len[ch];
+                int s = it % kTcStages;
+                uint32_t par = (it / kTcStages) & 1;
+                // rows in groups of up to 4: independent barrier waits and schedule reads
+                // overlap, then all MMAs of the group, then one commit per slot
+                constexpr int kGroup = 4;
+                for (int e0 = 0; e0 < ns; e0 += kGroup) {
+                    int4 rows[kGroup];
+                    int nr = 0;
+#pragma unroll
+                    for (int j = 0; j < kGroup; ++j) {
+                        rows[j] = e0 + j < ns ? sc[e0 + j] : make_int4(0, 1 << 30, 0, 0);
+                        if (rows[j].y < bd.cnt) nr = j + 1;
+                    }
+                    if (nr == 0) break;
+                    int ss[kGroup];
+                    {
+                        int s2 = s;
+                        uint32_t p2 = par;
+#pragma unroll
+                        for (int j = 0; j < kGroup; ++j) {
+                            ss[j] = s2;
+                            if (j < nr) mbar_wait_t(full + s2, p2, pf);
+                            if (++s2 == kTcStages) {
+                                s2 = 0;
+                                p2 ^= 1;
+                            }
+                        }
+                    }
+                    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < kGroup; ++j) {
+                        if (j >= nr) break;
+                        const int k_hi = min(rows[j].z, bd.cnt - 1);
+                        uint64_t ad = a_desc0 + uint64_t(uint32_t(ss[j]) * slot16);
+                        uint64_t bdsc = b_desc0 + uint64_t(uint32_t(rows[j].w) * entry16);
+                        const uint32_t idesc = idesc0 | (uint32_t(k_hi - rows[j].y + 1) << 18);
+                        const uint32_t d = dbase + uint32_t(16 * rows[j].y);
+                        for (int ks = 0; ks < ksteps; ++ks) {
+                            asm volatile(
+                                "{\n .reg .pred e, acc;\n elect.sync _|e, 0xffffffff;\n"
+                                " setp.ne.b32 acc, 1, 0;\n"
+                                " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, acc;\n}\n" ::"r"(d),
+                                "l"(ad), "l"(bdsc), "r"(idesc));
+                            ad += 2;
+                            bdsc += 16;
+                        }
+                    }
+#pragma unroll
+                    for (int j = 0; j < kGroup; ++j) {
+                        if (j >= nr) break;
+                        asm volatile(
+                            "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                            " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                                smem_u32(empty + ss[j])));
+                    }
+                    it += nr;
+                    s = int(it % kTcStages);
+                    par = (it / kTcStages) & 1;
+                    if (nr < kGroup) break;
+                }
+                if (P.nch > 1)
+                    asm volatile(
+                        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                            smem_u32(bempty)));
+            }
+            asm volatile(
+                "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                    smem_u32(dfull + buf)));
+        }
+        if (task.dbg && lane == 0) {
+            long long* dd = task.dbg + blockIdx.x * 8;
+            dd[4] = clock64() - t_start;
+            dd[5] = w_full;
+            dd[6] = w_dempty;
+            dd[7] = w_bfull;
+        }
+        __syncwarp();
+    } else {
+        // ============================ epilogue ============================
+        // 8 warps: group eg = 0/1 handles output rows k of parity eg; the four warps of a
+        // group cover the four TMEM lane quarters (warp w may only touch lanes 32*(w%4)..).
+        const int ew = warp - 2;
+        const int eg = ew >> 2;
+        const int q4 = warp & 3;
+        const int a = q4 * 32 + lane;  // MMA row = TMEM lane
+        const uint32_t lane_addr = uint32_t(q4 * 32) << 16;
+        // zero this group's columns (k of parity eg) of both buffers, hand them over
+        for (int b = 0; b < 2; ++b)
+            for (int k = eg; k < 16; k += 2) tmem_zero16(tmem + lane_addr + b * 256 + 16 * k);
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+        asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+        mbar_arrive(dempty + 0);
+        mbar_arrive(dempty + 1);
+
+        const TStats ts = TStats{job.ts.mu, job.ts.omega, job.ts.mn, job.ts.flat};
+        const DevStats st = job.st;
+        Cell best = no_cell();
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const TcBand bd = task.bands[t / task.ntc];
+            const int c0 = (t % task.ntc) * kTcCols;
+            const uint32_t buf = tl & 1;
+            const int cb = c0 + 16 * a;  // this thread's 16 consecutive columns
+            // MODE 1: which of the 16 columns are group centres (constant over the tile)
+            uint32_t cmask = 0;
+            int tj0 = 0, ph_last = -1;
+            if (MODE == 1) {
+                const int d0 = cb - task.cbase;
+                int first = d0 <= 0 ? -d0 : (d0 % task.cstep == 0 ? 0 : task.cstep - d0 % task.cstep);
+                tj0 = (cb + first - task.cbase) / task.cstep;
+                for (int ph = first, tj = tj0; ph < 16 && tj < task.nc; ph += task.cstep, ++tj)
+                    cmask |= 1u << ph;
+                // the clipped last group column (irregular centre), stored at tj = tc - 1
+                if (task.c_last >= cb && task.c_last < cb + 16) ph_last = task.c_last - cb;
+            } else {
+                for (int ph = 0; ph < 16; ++ph)
+                    if (cb + ph < task.c_lim) cmask |= 1u << ph;
+            }
+            mbar_wait(dfull + buf, (tl >> 1) & 1, 256);
+            asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            for (int k = eg; k < bd.cnt && !(task.dbg_flags & 2); k += 2) {
+                uint32_t v[16];
+                const uint32_t addr = tmem + lane_addr + buf * 256 + uint32_t(16 * k);
+                tmem_ld16(addr, v);
+                tmem_zero16(addr);
+                const int r = bd.r0 + bd.sr * k;
+                if (MODE == 1) {
+                    // centres: the exact dot goes to a compact per-group array; the FP64
+                    // epilogue runs in k_centre_epi (coalesced statistics loads)
+                    double* row_out = task.out_rho + size_t(bd.yi0 + k) * task.tc;
+                    int tj = tj0;
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) {
+                        if (ph == ph_last) row_out[task.tc - 1] = double(int(v[ph]));
+                        if (!((cmask >> ph) & 1u)) continue;
+                        row_out[tj++] = double(int(v[ph]));
+                    }
+                    continue;
+                }
+                const size_t rb = size_t(r) * st.ec + cb;
+                // all loads first (independent, predicated), then the FP64 epilogues
+                uint8_t fl[16], mk[16];
+                double mu[16], om[16];
+#pragma unroll
+                for (int ph = 0; ph < 16; ++ph) {
+                    const bool on = (cmask >> ph) & 1u;
+                    const size_t kk = on ? rb + ph : 0;
+                    fl[ph] = on ? st.flat[kk] : uint8_t(1);
+                    mu[ph] = on ? st.mu[kk] : 0.0;
+                    om[ph] = on ? st.omega[kk] : 0.0;
+                    if (MODE == 2) mk[ph] = on ? task.mask[kk] : uint8_t(0);
+                }
+#pragma unroll
+                for (int ph = 0; ph < 16; ++ph) {
+                    if (!((cmask >> ph) & 1u)) continue;
+                    if (MODE == 2 && mk[ph] != 2) continue;
+                    const int c = cb + ph;
+                    const bool wflat = fl[ph];
+                    const double rho = zncc_epilogue(double(int(v[ph])), ts, mu[ph], om[ph], wflat);
+                    const bool deg = ts.flat || wflat;
+                    if (task.out_rho) task.out_rho[rb + ph] = rho;
+                    const Cell cand = make_cell(r, c, rho, deg);
+                    if (better(cand, best)) best = cand;
+                }
+            }
+            asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+            asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+            mbar_arrive(dempty + buf);
+        }
+        // block best over the 8 epilogue warps
+        best = warp_best(best);
+        if (lane == 0) scratch[ew] = best;
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+        if (ew == 0 && lane == 0) {
+            Cell b = scratch[0];
+            for (int w = 1; w < 8; ++w)
+                if (better(scratch[w], b)) b = scratch[w];
+            partials[blockIdx.x] = CellH{b.rho, b.row, b.col, b.flags};
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+// B chunk layout: entry e (16 rows = the 16 column phases of one template row i) x Kx
+// bytes, canonical no-swizzle K-major: byte (row rho, t) at
+// (rho/8)*SBO + (rho%8)*16 + (t/16)*128 + t%16, SBO = 128*Kx/16.
+__global__ void k_tc_build_b(const float* __restrict__ tf, int npad, int m, int n, TcPlan P,
+                             uint8_t* __restrict__ out) {
+    const int ch = blockIdx.y;
+    const int i0 = P.i0[ch], i1 = P.i1[ch];
+    const int entries = i1 - i0;
+    const size_t bytes = size_t(entries) * 16 * P.kx;
+    uint8_t* o = out + P.b_off[ch];
+    const int sbo = 128 * (P.kx / 16);
+    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < bytes;
+         idx += size_t(gridDim.x) * blockDim.x) {
+        const int e = int(idx / (size_t(16) * P.kx));
+        const int rem = int(idx - size_t(e) * 16 * P.kx);
+        const int ph = rem / P.kx, t = rem - ph * P.kx;
+        // entry e -> (class, position) -> template row i
+        int cls = 0;
+        while (cls + 1 < P.sr && P.cls_off[ch][cls + 1] <= e) ++cls;
+        const int i = P.cls_max[ch][cls] - P.sr * (e - P.cls_off[ch][cls]);
+        const int j = t - ph;
+        uint8_t val = 0;
+        if (i >= i0 && i < i1 && j >= 0 && j < n) val = uint8_t(tf[size_t(i) * npad + j]);
+        const int row = e * 16 + ph;
+        o[size_t(row / 8) * sbo + (row % 8) * 16 + (t / 16) * 128 + (t % 16)] = val;
+    }
+}
+
+__global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_t* __restrict__ out,
+                           int pitch, int rows) {
+    const int r = blockIdx.y;
+    if (r >= rows) return;
+    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x)
+        out[size_t(r) * pitch + c] = (r < p && c < q) ? img[size_t(r) * q + c] : 0;
+}
+
+}  // namespace
+
+bool tc_supported(int m, int n) {
+    // exact s32 dots; Kx <= 256 bytes per MMA chain; at least one template row per chunk
+    return double(m) * double(n) * 65025.0 < 2147483648.0 && n + 15 <= 256;
+}
+
+TcPlan tc_plan(int m, int n, int sr, size_t smem_budget) {
+    TcPlan P{};
+    P.kx = ((n + 15) + 31) / 32 * 32;
+    P.sr = std::max(1, sr);
+    P.a_bytes = ((2032 + P.kx) + 15) / 16 * 16;
+    P.a_slot = (P.a_bytes + 127) / 128 * 128;
+    // header: barriers + up to 16 KB of staged row schedule; at least 16 ring stages; B
+    // gets the rest (the ring grows back into what B leaves)
+    P.header = kTcBarBytes + 16 * 1024;
+    const size_t fixed = size_t(16) * P.a_slot + P.header;
+    const size_t entry = size_t(16) * P.kx;
+    const int per_chunk = int((smem_budget - fixed) / entry);
+    if (per_chunk < 1) return TcPlan{};
+    P.nch = (m + per_chunk - 1) / per_chunk;
+    if (P.nch > kTcMaxChunks || P.sr > kTcMaxClasses) return TcPlan{};
+    const int rows = (m + P.nch - 1) / P.nch;
+    size_t off = 0, bmax = 0;
+    for (int ch = 0; ch < P.nch; ++ch) {
+        P.i0[ch] = ch * rows;
+        P.i1[ch] = std::min(m, (ch + 1) * rows);
+        int e = 0;
+        for (int c = 0; c < P.sr; ++c) {
+            P.cls_off[ch][c] = e;
+            // largest i in [i0, i1) with i % sr == c
+            int hi = P.i1[ch] - 1;
+            while (hi >= P.i0[ch] && hi % P.sr != c) --hi;
+            P.cls_max[ch][c] = hi;
+            if (hi >= P.i0[ch]) e += (hi - P.i0[ch]) / P.sr + 1;
+        }
+        P.b_off[ch] = off;
+        P.b_bytes[ch] = size_t(e) * entry;
+        off += P.b_bytes[ch];
+        bmax = std::max(bmax, P.b_bytes[ch]);
+    }
+    P.total_bytes = off;
+    P.b_smem = (bmax + 1023) / 1024 * 1024;
+    const size_t left = smem_budget - P.header - P.b_smem;
+    P.stages = int(std::min<size_t>(kTcMaxStages, left / P.a_slot));
+    P.smem = P.header + P.b_smem + size_t(P.stages) * P.a_slot;
+    return P;
+}
+
+std::vector<int> tc_schedule(const TcPlan& P, int rmax, int* off, int* len) {
+    // per chunk, rows dx = x - r0 of a band of rmax rows at stride P.sr that feed at least
+    // one output row: {dx, k_lo, k_hi, B entry of T row dx - sr*k_lo}, in increasing dx
+    // (so k_lo is non-decreasing: a band with fewer rows stops at k_lo >= cnt).
+    std::vector<int> out;
+    for (int ch = 0; ch < P.nch; ++ch) {
+        off[ch] = int(out.size() / 4);
+        const int i0 = P.i0[ch], i1 = P.i1[ch];
+        for (int dx = i0; dx < P.sr * (rmax - 1) + i1; ++dx) {
+            const int lo_num = dx - i1 + 1;
+            const int k_lo = lo_num <= 0 ? 0 : (lo_num + P.sr - 1) / P.sr;
+            const int k_hi = std::min(rmax - 1, (dx - i0) / P.sr);
+            if (k_lo > k_hi) continue;
+            const int i_top = dx - P.sr * k_lo;
+            const int cls = i_top % P.sr;
+            const int pos = (P.cls_max[ch][cls] - i_top) / P.sr;
+            out.push_back(dx);
+            out.push_back(k_lo);
+            out.push_back(k_hi);
+            out.push_back(P.cls_off[ch][cls] + pos);
+        }
+        len[ch] = int(out.size() / 4) - off[ch];
+    }
+    return out;
+}
+
+int tc_pitch(int q, int ec) {
+    const int ntc = (ec + kTcCols - 1) / kTcCols;
+    return ((std::max(q, ntc * kTcCols + 256) + 15) / 16) * 16;
+}
+
+int tc_tile_cols() { return kTcCols; }
+
+cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int pitch, int rows,
+                           cudaStream_t s) {
+    dim3 grid((pitch + 255) / 256 > 8 ? 8 : (pitch + 255) / 256, rows);
+    k_tc_pitch<<<grid, 256, 0, s>>>(img, p, q, out, pitch, rows);
+    return cudaGetLastError();
+}
+
+cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
+                       cudaStream_t s) {
+    dim3 grid(64, plan.nch);
+    k_tc_build_b<<<grid, 256, 0, s>>>(tf, npad, m, n, plan, out);
+    return cudaGetLastError();
+}
+
+cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* nparts,
+                    cudaStream_t s) {
+    const int ntiles = task.nbands * task.ntc;
+    const int grid = std::max(1, std::min(148, ntiles));
+    *nparts = grid;
+    const size_t smem = job.plan.smem;
+    cudaError_t e = cudaSuccess;
+    switch (task.mode) {
+        case 0:
+            cudaFuncSetAttribute(k_tc_corr<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            k_tc_corr<0><<<grid, kTcThreads, smem, s>>>(job, task, partials);
+            break;
+        case 1:
+            cudaFuncSetAttribute(k_tc_corr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            k_tc_corr<1><<<grid, kTcThreads, smem, s>>>(job, task, partials);
+            break;
+        case 2:
+            cudaFuncSetAttribute(k_tc_corr<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+            k_tc_corr<2><<<grid, kTcThreads, smem, s>>>(job, task, partials);
+            break;
+        default:
+            return cudaErrorInvalidValue;
+    }
+    e = cudaGetLastError();
+    return e;
+}
+
+}  // namespace tmk

@@ -5,6 +5,7 @@
 
 #include <cstddef>
 #include <cstdint>
+#include <vector>
 #include <cuda_runtime.h>
 
 namespace tmk {
@@ -73,6 +74,7 @@ struct ProdSrc {
     const double* Y;
     int yq, yr, yc;
     int square;
+    const int* stop = nullptr;  // device flag: skip the work when set (EGS early exit)
 };
 // rowacc: rows*cols; prefix: (rows+1)*(cols+1) with zero first row/col.
 cudaError_t replica_prefix(ProdSrc src, int rows, int cols, double* rowacc, double* prefix,
@@ -111,10 +113,11 @@ cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, 
 // replica path, one offset: cross-sum prefix table of the product image for (di,dj).
 cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
                                      GridDesc g, DevStats st, int di, int dj, double* map,
-                                     cudaStream_t s);
-cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s);  // zeros + centres=1
+                                     cudaStream_t s, const int* stop = nullptr);
+cudaError_t autocorr_init(double* map, GridDesc g, cudaStream_t s,
+                          const int* stop = nullptr);  // zeros + centres=1
 cudaError_t retained_count(const double* map, GridDesc g, double threshold,
-                           unsigned long long* n_r, cudaStream_t s);
+                           unsigned long long* n_r, cudaStream_t s, const int* stop = nullptr);
 
 // ---- correlation -----------------------------------------------------------------------
 struct CorrJob {
@@ -174,7 +177,7 @@ cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials,
 // Epilogue of a K-split centre scan (rho/deg from the accumulated dots + argmax partials).
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
-                            CellH* partials, int n_partials, cudaStream_t s);
+                            CellH* partials, int n_partials, cudaStream_t s, int c_last = -1);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
@@ -227,5 +230,58 @@ cudaError_t mark_violations(const double* fid, const double* changed_in_window, 
 cudaError_t restore_covered(double* blurred, const double* original, const uint8_t* marks,
                             int er, int ec, int m, int n, int p, int q, int* scratch,
                             cudaStream_t s);
+
+
+// ---- integer tensor-core correlation (k_tc.cu) --------------------------------------
+constexpr int kTcMaxChunks = 8;
+constexpr int kTcMaxClasses = 12;
+struct TcPlan {  // B arrangement + shared-memory plan for one (template size, row stride)
+    int kx = 0, sr = 1, nch = 0;
+    int a_bytes = 0, a_slot = 0, stages = 0, header = 0;
+    int i0[kTcMaxChunks] = {}, i1[kTcMaxChunks] = {};
+    int cls_off[kTcMaxChunks][kTcMaxClasses] = {};
+    int cls_max[kTcMaxChunks][kTcMaxClasses] = {};
+    size_t b_off[kTcMaxChunks] = {}, b_bytes[kTcMaxChunks] = {};
+    size_t total_bytes = 0, b_smem = 0, smem = 0;
+};
+struct TcJob {
+    const uint8_t* imgp;  // pitched 8-bit image (tc_pitch), zero padded
+    int pitch;
+    const uint8_t* bglob;  // tc_build_b output
+    TcPlan plan;
+    TStatsH ts;
+    DevStats st;
+};
+struct TcBand {  // output rows r0 + sr*k, k < cnt (cnt <= 16); yi0 = group row of k = 0
+    int r0, sr, cnt, yi0;
+};
+struct TcTask {
+    const TcBand* bands;
+    int nbands, ntc;  // tiles = bands x 2048-column tiles
+    int mode;         // 0 dense (out_rho = surface), 1 centres, 2 dense masked (mask == 2)
+    int c_lim;        // modes 0/2: output columns < c_lim
+    int cbase, cstep, nc, tc;  // mode 1: centre columns cbase + cstep*tj, tj < nc; tc = row stride
+    int c_last;                // mode 1: clipped last group's centre column (tj = tc-1) or -1
+    double* out_rho;
+    uint8_t* out_deg;
+    const uint8_t* mask;
+    long long* dbg;     // optional per-CTA pipeline wait counters (8 per CTA)
+    int dbg_flags;      // timing experiments only: 1 = no image copies, 2 = no epilogue
+    const int4* sched;  // tc_schedule() rows, per chunk at sched_off[ch], sched_len[ch]
+    int sched_total;    // rows over all chunks
+    int sched_off[kTcMaxChunks], sched_len[kTcMaxChunks];
+};
+bool tc_supported(int m, int n);
+TcPlan tc_plan(int m, int n, int sr, size_t smem_budget);
+// rows of a band of rmax rows, see k_tc.cu (4 ints per row)
+std::vector<int> tc_schedule(const TcPlan& plan, int rmax, int* off, int* len);
+int tc_pitch(int q, int ec);
+int tc_tile_cols();
+cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int pitch, int rows,
+                           cudaStream_t s);
+cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
+                       cudaStream_t s);
+cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* nparts,
+                    cudaStream_t s);
 
 }  // namespace tmk

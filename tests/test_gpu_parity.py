@@ -290,3 +290,82 @@ def test_window_stats_fused_tiles(ctx, port, m, n):
     img[210:260, 500:690] = rng.integers(100, 102, (50, 190))  # tiny variance
     gi = ctx.image(img)
     _ws_equal(ctx.window_stats(gi, m, n), port.window_stats(img.astype(np.float64), m, n))
+
+
+def _ctx_with(env, value):
+    import os
+    from paper_1407_3535_b200 import api
+    old = os.environ.get(env)
+    os.environ[env] = value
+    try:
+        return api.Context(0)
+    finally:
+        if old is None:
+            os.environ.pop(env, None)
+        else:
+            os.environ[env] = old
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,h", [(16, 16, 3), (40, 64, 5), (33, 70, 7), (96, 96, 3),
+                                   (130, 120, 3), (20, 24, 11)])
+def test_tc_centre_scan_equals_cuda_core(m, n, h):
+    """The tcgen05 kind::i8 centre scan (2 column tiles, several bands, B chunking for the
+    130x120 template, clipped last group row/column) equals the CUDA-core FP32-exact scan
+    bit for bit: centre rho, degenerate flags and the best centre."""
+    rng = np.random.default_rng(m * 7 + n * 3 + h)
+    base = np.cumsum(np.cumsum(rng.normal(size=(m + 61, n + 2200)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    img[5:25, 100:300] = 40  # flat windows
+    t = np.clip(np.rint(img[11:11 + m, 1500:1500 + n] * 0.9 + 7 + rng.normal(0, 3, (m, n))),
+                0, 255)
+    tc, cc = _ctx_with("TMATCH_TC", "1"), _ctx_with("TMATCH_TC", "0")
+    a = tc.center_scan(t, img, h, h)
+    b = cc.center_scan(t, img, h, h)
+    np.testing.assert_array_equal(a["rho"], b["rho"])
+    np.testing.assert_array_equal(a["degenerate"], b["degenerate"])
+    assert a["best"] == b["best"]
+    tc.close()
+    cc.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n", [(16, 16), (40, 64), (96, 96), (130, 120)])
+def test_tc_brute_surface_equals_cuda_core(m, n):
+    """Tensor-core brute force (dense mode 0): the whole rho surface and the argmax equal
+    the CUDA-core FP32-exact kernel bit for bit (2 column tiles, B chunking)."""
+    rng = np.random.default_rng(m + 5 * n)
+    base = np.cumsum(np.cumsum(rng.normal(size=(m + 40, n + 2100)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    img[3:30, 50:400] = 9
+    t = np.clip(np.rint(img[17:17 + m, 1900:1900 + n] * 1.1 - 4 + rng.normal(0, 2, (m, n))),
+                0, 255)
+    tc, cc = _ctx_with("TMATCH_TC", "1"), _ctx_with("TMATCH_TC", "0")
+    a, sa = tc.brute_force_match(t, img, record_surface=True)
+    b, sb = cc.brute_force_match(t, img, record_surface=True)
+    np.testing.assert_array_equal(sa, sb)
+    assert (a.best_row, a.best_col, a.best_rho) == (b.best_row, b.best_col, b.best_rho)
+    tc.close()
+    cc.close()
+
+
+@pytest.mark.gpu
+def test_tc_dense_survivors_weak_template(port):
+    """A noise template (no elimination) takes the dense survivor path: tensor-core and
+    CUDA-core runs give identical results, equal to the brute-force argmax."""
+    rng = np.random.default_rng(77)
+    base = np.cumsum(np.cumsum(rng.normal(size=(300, 2200)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    t = rng.integers(0, 256, (24, 24)).astype(np.float64)
+    res = []
+    for flag in ("1", "0"):
+        c = _ctx_with("TMATCH_TC", flag)
+        prep = c.prepare(c.image(img), 24, 24)
+        for pol in ("seeded", "frozen", "sequential"):
+            r = c.run(prep, t, policy=pol, parallel=(pol == "frozen"), threads=2)
+            res.append((pol, r.best_row, r.best_col, r.best_rho, r.eliminated, r.retained))
+        prep.close()
+        c.close()
+    assert res[:3] == res[3:]
+    b = port.brute(t, img.astype(np.float64))
+    assert (res[0][1], res[0][2], res[0][3]) == (b.best_row, b.best_col, b.best_rho)

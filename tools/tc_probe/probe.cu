@@ -124,6 +124,248 @@ __global__ void k_probe(const uint8_t* gA, const uint8_t* gB, int N, int ksteps,
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(256));
 }
 
+
+// Throughput: `iters` x ksteps MMAs on resident operands; one commit at the end.
+__global__ void k_bench(int N, int ksteps, int mode, int iters, long long* cycles, int nacc) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bar;
+    __shared__ uint32_t tmem_base;
+    const int K = 32 * ksteps;
+    uint8_t* sA = sm;
+    uint8_t* sB = sm + 128 * 1024;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 100 * 1024; i += blockDim.x) sm[i] = uint8_t(i * 7);
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (tid == 0) {
+        mbar_init(&bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    if (tid == 0) {
+        const uint32_t idesc = make_idesc_i8(128, N);
+        int acc_i = 0;
+        const long long t0 = clock64();
+        for (int it = 0; it < iters; ++it)
+            for (int s = 0; s < ksteps; ++s) {
+                uint64_t ad;
+                if (mode == 0) ad = make_desc(smem_u32(sA) + 256 * s, 128, 128 * (K / 16));  // canonical
+                else if (mode == 1) ad = make_desc(smem_u32(sA) + 32 * s, 16, 128);          // Toeplitz
+                else ad = make_desc(smem_u32(sA) + 128 * (s / 4) + 0, 8192, 128);             // 8 phase copies
+                uint64_t bd = make_desc(smem_u32(sB) + 256 * s, 128, 128 * (K / 16));
+                mma_i8(tmem + uint32_t(acc_i * N), ad, bd, idesc, 1u);
+                if (++acc_i == nacc) acc_i = 0;
+            }
+        mma_commit(&bar);
+        mbar_wait(&bar, 0);
+        cycles[0] = clock64() - t0;
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+static void run_bench(int N, int ksteps, int mode, int nacc) {
+    long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(k_bench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int iters = 2000;
+    k_bench<<<1, 128, 200 * 1024>>>(N, ksteps, mode, iters, d, nacc);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    printf("bench N=%3d nacc=%d ksteps=%d mode=%s: %.1f cycles/MMA (%s)\n", N, nacc, ksteps,
+           mode == 0 ? "canonical" : (mode == 1 ? "toeplitz " : "phasecopy"),
+           double(c) / (iters * ksteps), cudaGetErrorString(e));
+    cudaFree(d);
+}
+
+
+// Row-loop mimic: per "row" [optional fence], 3 MMAs (Toeplitz A in ring slot, B window),
+// [optional commit to a ring of mbarriers].  Warp-uniform issue with elect.sync.
+__global__ void k_rowbench(int N, int rows, int fence, int commit, long long* cycles) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bars[64];
+    __shared__ uint32_t tmem_base;
+    uint8_t* sA = sm;
+    uint8_t* sB = sm + 160 * 1024;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 190 * 1024; i += blockDim.x) sm[i] = uint8_t(i * 7);
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (tid == 0) {
+        for (int i = 0; i < 64; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    if (warp == 0) {
+        const uint32_t idesc = make_idesc_i8(128, N);
+        const uint64_t a0 = make_desc(smem_u32(sA), 16, 128);
+        const uint64_t b0 = make_desc(smem_u32(sB), 128, 128 * 6);
+        const long long t0 = clock64();
+        for (int r = 0; r < rows; ++r) {
+            if (fence) asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+            uint64_t ad = a0 + uint64_t((r % 60) * 144);   // 2304-byte slots
+            uint64_t bd = b0 + uint64_t((r % 8) * 96);      // 1536-byte entries
+            for (int ks = 0; ks < 3; ++ks) {
+                asm volatile(
+                    "{\n .reg .pred e, acc;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 acc, 1, 0;\n"
+                    " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, acc;\n}\n" ::"r"(tmem + 16 * (r % 4)),
+                    "l"(ad), "l"(bd), "r"(idesc));
+                ad += 2;
+                bd += 16;
+            }
+            if (commit)
+                asm volatile(
+                    "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                    " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                        smem_u32(&bars[r % 64])));
+        }
+        asm volatile(
+            "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+            " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                smem_u32(&bars[63])));
+        if (tid == 0) cycles[0] = clock64() - t0;
+    }
+    __syncthreads();
+    // drain: wait until the last commit landed (phase parity depends on counts; just sleep)
+    if (tid == 0) { long long t = clock64(); while (clock64() - t < 2000000) {} }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+static void run_rowbench(int N, int fence, int commit) {
+    long long* d;
+    cudaMalloc(&d, 8);
+    cudaFuncSetAttribute(k_rowbench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int rows = 2000;
+    k_rowbench<<<1, 128, 200 * 1024>>>(N, rows, fence, commit, d);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c = 0;
+    cudaMemcpy(&c, d, 8, cudaMemcpyDeviceToHost);
+    printf("rowbench N=%3d fence=%d commit=%d: %.1f cycles/row issue (%s)\n", N, fence, commit,
+           double(c) / rows, cudaGetErrorString(e));
+    cudaFree(d);
+}
+
+
+// Replays the centre-scan band schedule (sr, m, R rows, Kx=96): per image row dx, one MMA
+// chain with N = 16*(k_hi-k_lo+1) into D columns 16*k_lo.., B window at entry(i_top).
+__global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long long* cycles, int variant) {
+    extern __shared__ __align__(1024) uint8_t sm[];
+    __shared__ uint64_t bars[64];
+    __shared__ uint32_t tmem_base;
+    uint8_t* sA = sm;
+    uint8_t* sB = sm + 100 * 1024;
+    const int tid = threadIdx.x, warp = tid >> 5;
+    for (int i = tid; i < 200 * 1024; i += blockDim.x) sm[i] = uint8_t(i * 7);
+    asm volatile("fence.proxy.async.shared::cta;");
+    if (tid == 0) {
+        for (int i = 0; i < 64; ++i) mbar_init(&bars[i], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(&tmem_base)), "r"(512));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const uint32_t tmem = tmem_base;
+    long long nmma = 0;
+    __shared__ int4 tab[256];
+    int ntab = 0;
+    if (tid == 0) {
+        for (int dx = 0; dx < sr * (R - 1) + m; ++dx) {
+            const int lo_num = dx - m + 1;
+            const int k_lo = lo_num <= 0 ? 0 : (lo_num + sr - 1) / sr;
+            const int k_hi = min(R - 1, dx / sr);
+            if (k_lo > k_hi) continue;
+            const int i_top = dx - sr * k_lo;
+            const int entry = (i_top % sr) * ((m + sr - 1) / sr) + (m - 1 - i_top) / sr;
+            tab[ntab++] = make_int4(dx, k_lo, k_hi, entry);
+        }
+        tab[255].x = ntab;
+    }
+    __syncthreads();
+    ntab = tab[255].x;
+    if (warp == 0) {
+        const uint64_t a0 = make_desc(smem_u32(sA), 16, 128);
+        const uint64_t b0 = make_desc(smem_u32(sB), 128, 768);
+        const long long t0 = clock64();
+        int slot = 0;
+        for (int b = 0; b < bands; ++b)
+            for (int e = 0; e < ntab; ++e) {
+                const int4 row = tab[e];
+                const int k_lo = row.y, k_hi = row.z, entry = row.w;
+                uint64_t ad = a0 + uint64_t(slot * 136);
+                uint64_t bd = b0 + uint64_t(entry * 96);
+                const int nfix = variant == 1 || variant == 3 ? R : (k_hi - k_lo + 1);
+                const int kfix = variant == 1 || variant == 2 ? 0 : k_lo;
+                const uint32_t idesc = make_idesc_i8(128, 16 * nfix);
+                const uint32_t d = tmem + (b & 1) * 256 + 16 * kfix;
+                for (int ks = 0; ks < 3; ++ks) {
+                    asm volatile(
+                        "{\n .reg .pred e, acc;\n elect.sync _|e, 0xffffffff;\n setp.ne.b32 acc, 1, 0;\n"
+                        " @e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, acc;\n}\n" ::"r"(d),
+                        "l"(ad), "l"(bd), "r"(idesc));
+                    ad += 2;
+                    bd += 16;
+                    ++nmma;
+                }
+                if (commit)
+                    asm volatile(
+                        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                            smem_u32(&bars[slot % 64])));
+                slot = (slot + 1) % 40;
+            }
+        if (tid == 0) {
+            cycles[blockIdx.x * 2] = clock64() - t0;
+            cycles[blockIdx.x * 2 + 1] = nmma;
+        }
+    }
+    __syncthreads();
+    if (tid == 0) { long long t = clock64(); while (clock64() - t < 3000000) {} }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    if (warp == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
+}
+
+static void run_sched(int sr, int m, int R, int grid, int commit, int variant) {
+    long long* d;
+    cudaMalloc(&d, 2 * 8 * 148);
+    cudaFuncSetAttribute(k_schedbench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    const int bands = 5;
+    k_schedbench<<<grid, 128, 200 * 1024>>>(sr, m, R, bands, commit, d, variant);
+    cudaError_t e = cudaDeviceSynchronize();
+    long long c[2] = {0, 0};
+    cudaMemcpy(c, d, 16, cudaMemcpyDeviceToHost);
+    const int rows = bands * (sr * (R - 1) + m);
+    printf("sched sr=%d m=%d R=%2d variant=%d commit=%d: %.1f cycles/row, %.1f cycles/MMA (%s)\n", sr, m,
+           R, variant, commit, double(c[0]) / rows, double(c[0]) / c[1], cudaGetErrorString(e));
+    cudaFree(d);
+}
+
 static int run_case(int N, int ksteps, int toeplitz) {
     const int K = 32 * ksteps;
     const int asz = toeplitz ? 2048 + K : 128 * K;
@@ -194,5 +436,9 @@ int main() {
     fails += run_case(256, 3, 1);
     fails += run_case(64, 2, 0);
     printf("fails=%d\n", fails);
+    // variant 0: as scheduled; 1: fixed N=16R, D offset 0; 2: varying N, D offset 0;
+    // 3: fixed N=16R, D offset 16*k_lo (N range clipped at 512 columns)
+    for (int R : {4, 16})
+        for (int variant : {0, 1, 2, 3}) run_sched(3, 64, R, 1, 1, variant);
     return fails ? 1 : 0;
 }
