@@ -49,6 +49,30 @@ void ck(cudaError_t e, const char* what) {
 
 constexpr double kEps = 2.220446049250313e-16;
 
+// Optional host timeline (TMATCH_HOST_TRACE=1): labelled timestamps printed per API call.
+struct HostTrace {
+    bool on = std::getenv("TMATCH_HOST_TRACE") != nullptr;
+    std::vector<std::pair<const char*, std::chrono::steady_clock::time_point>> pts;
+    void mark(const char* l) {
+        if (on) pts.emplace_back(l, std::chrono::steady_clock::now());
+    }
+    void flush(const char* call) {
+        if (!on || pts.empty()) return;
+        std::fprintf(stderr, "[host] %s:", call);
+        for (size_t i = 1; i < pts.size(); ++i)
+            std::fprintf(stderr, " %s=%.1f", pts[i].first,
+                         std::chrono::duration<double, std::micro>(pts[i].second - pts[i - 1].second)
+                             .count());
+        std::fprintf(stderr, "\n");
+        pts.clear();
+    }
+};
+HostTrace& htrace() {
+    static thread_local HostTrace t;
+    return t;
+}
+#define HT(label) htrace().mark(label)
+
 // Stream the current API call runs on (set by guard()); device buffers are allocated and
 // freed stream-ordered from the device's memory pool, so buffer churn never synchronises.
 thread_local cudaStream_t g_stream = nullptr;
@@ -161,6 +185,17 @@ struct Tmpl {
     int flush_rows = 0;
 };
 
+// Geometry-dependent tensor-core launch data (band table, row schedule, plan), built and
+// uploaded once per (template size, row set) and reused by every later search.
+struct TcGeo {
+    tmk::TcPlan plan{};
+    DBuf<tmk::TcBand> bands;
+    DBuf<int4> sched;
+    DBuf<int> rows;  // the row list itself (centre epilogue)
+    int nbands = 0, ntc = 0, sched_total = 0;
+    int sched_off[tmk::kTcMaxChunks] = {}, sched_len[tmk::kTcMaxChunks] = {};
+};
+
 // ==== context ========================================================================
 struct WS {
     DBuf<double> mu, om;
@@ -217,9 +252,7 @@ struct tm_ctx {
     // TMATCH_TC=0 selects the CUDA-core FP32-exact kernels (A/B measurements, cross-checks)
     bool tc = true;
     DBuf<uint8_t> tc_b;
-    DBuf<tmk::TcBand> tc_bands;
-    DBuf<int4> tc_sched;
-    Pinned pin_bands, pin_sched;
+    std::map<std::vector<long long>, std::unique_ptr<TcGeo>> tc_geo;
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -566,19 +599,48 @@ std::vector<tmk::TcBand> tc_bands(const std::vector<int>& rows, const std::vecto
 }
 
 // Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
+TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const std::vector<int>& rows,
+                   const std::vector<int>& yi, int sr) {
+    std::vector<long long> key = {T.m, T.n, sr, ws.ec, (long long)rows.size()};
+    unsigned long long h = 1469598103934665603ull;
+    for (size_t i = 0; i < rows.size(); ++i) h = (h ^ (unsigned long long)(rows[i] * 131 + yi[i])) * 1099511628211ull;
+    key.push_back((long long)h);
+    auto it = ctx->tc_geo.find(key);
+    if (it != ctx->tc_geo.end()) return *it->second;
+    if (ctx->tc_geo.size() > 64) ctx->tc_geo.clear();
+    auto geo = std::make_unique<TcGeo>();
+    geo->plan = tmk::tc_plan(T.m, T.n, sr, kTcSmemBudget);
+    if (geo->plan.nch == 0) invalid("tensor-core plan unavailable");
+    geo->ntc = (ws.ec + tmk::tc_tile_cols() - 1) / tmk::tc_tile_cols();
+    // rows per band: as many as the tiles allow while keeping >= 1 tile per SM
+    int rmax = 16;
+    while (rmax > 1 && size_t((rows.size() + rmax - 1) / rmax) * geo->ntc < 148) rmax /= 2;
+    const std::vector<tmk::TcBand> bands = tc_bands(rows, yi, sr, rmax);
+    geo->nbands = int(bands.size());
+    geo->bands.ensure(bands.size());
+    CK(cudaMemcpyAsync(geo->bands.p, bands.data(), bands.size() * sizeof(tmk::TcBand),
+                       cudaMemcpyHostToDevice, ctx->s));
+    const std::vector<int> sched = tmk::tc_schedule(geo->plan, rmax, geo->sched_off, geo->sched_len);
+    geo->sched_total = int(sched.size() / 4);
+    geo->sched.ensure(sched.size() / 4 + 1);
+    CK(cudaMemcpyAsync(geo->sched.p, sched.data(), sched.size() * sizeof(int),
+                       cudaMemcpyHostToDevice, ctx->s));
+    geo->rows.ensure(rows.size() + 1);
+    CK(cudaMemcpyAsync(geo->rows.p, rows.data(), rows.size() * sizeof(int), cudaMemcpyHostToDevice,
+                       ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));  // host vectors go out of scope (pageable copies)
+    TcGeo& ref = *geo;
+    ctx->tc_geo.emplace(std::move(key), std::move(geo));
+    return ref;
+}
+
+// Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
 int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const std::vector<int>& rows,
-           const std::vector<int>& yi, int sr, tmk::TcTask task) {
-    const tmk::TcPlan plan = tmk::tc_plan(T.m, T.n, sr, kTcSmemBudget);
-    if (plan.nch == 0) invalid("tensor-core plan unavailable");
+           const std::vector<int>& yi, int sr, tmk::TcTask task, const int** rows_dev = nullptr) {
+    TcGeo& geo = tc_geometry(ctx, ws, T, rows, yi, sr);
+    const tmk::TcPlan& plan = geo.plan;
     ctx->tc_b.ensure(plan.total_bytes);
     CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s));
-    const int ntc = (ws.ec + tmk::tc_tile_cols() - 1) / tmk::tc_tile_cols();
-    // rows per band: as many as the tiles allow while keeping >= 2 tiles per SM
-    int rmax = 16;
-    while (rmax > 1 && size_t((rows.size() + rmax - 1) / rmax) * ntc < 148) rmax /= 2;
-    const std::vector<tmk::TcBand> bands = tc_bands(rows, yi, sr, rmax);
-    ctx->tc_bands.ensure(bands.size());
-    ctx->pin_bands.upload(ctx->tc_bands.p, bands.data(), bands.size() * sizeof(tmk::TcBand), ctx->s);
     tmk::TcJob job{};
     job.imgp = tc_image(ctx, img, ws.ec);
     job.pitch = img->u8p_pitch;
@@ -586,14 +648,16 @@ int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const std::v
     job.plan = plan;
     job.ts = T.ts;
     job.st = ws.dev();
-    task.bands = ctx->tc_bands.p;
-    task.nbands = int(bands.size());
-    task.ntc = ntc;
-    const std::vector<int> sched = tmk::tc_schedule(plan, rmax, task.sched_off, task.sched_len);
-    ctx->tc_sched.ensure(sched.size() / 4 + 1);
-    ctx->pin_sched.upload(ctx->tc_sched.p, sched.data(), sched.size() * sizeof(int), ctx->s);
-    task.sched = ctx->tc_sched.p;
-    task.sched_total = int(sched.size() / 4);
+    task.bands = geo.bands.p;
+    task.nbands = geo.nbands;
+    task.ntc = geo.ntc;
+    task.sched = geo.sched.p;
+    task.sched_total = geo.sched_total;
+    for (int c = 0; c < tmk::kTcMaxChunks; ++c) {
+        task.sched_off[c] = geo.sched_off[c];
+        task.sched_len[c] = geo.sched_len[c];
+    }
+    if (rows_dev) *rows_dev = geo.rows.p;
     int np = 0;  // caller sizes ctx->partials for >= 148 entries
     static const bool dbg = std::getenv("TMATCH_TC_DEBUG") != nullptr;
     DBuf<long long> dbuf;
@@ -694,10 +758,10 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             task.tc = g.tc;
             task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
             task.out_rho = ctx->dotbuf.p;
-            tc_run(ctx, img, ws, T, rows, yi, g.h, task);
-            upload_rows(ctx, rows);
+            const int* rows_dev = nullptr;
+            tc_run(ctx, img, ws, T, rows, yi, g.h, task, &rows_dev);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
-            CK(tmk::centre_epilogue(job, g, ctx->rows_list.p, wr, g.w, g.tc, 0, ctx->dotbuf.p,
+            CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
                                     task.c_last));
             ctx->add(1);
@@ -1200,6 +1264,39 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 
 }
 
+// eval_survivors without the host round trip (tensor-core path): the survivor count stays
+// on the device; survivor_dispatch selects dense (masked tensor-core kernel) or list, the
+// other launch only writes empty partials.
+void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                        const tmk::GridDesc& g, double* rho_loc) {
+    cudaStream_t s = ctx->s;
+    const size_t E = size_t(g.er) * g.ec;
+    int* dense_flag = reinterpret_cast<int*>(ctx->counters.p + 22);
+    unsigned long long* list_count = ctx->counters.p + 23;
+    CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s));
+    ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
+    const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
+    int np = 0;
+    if (rhi > rlo) {
+        std::vector<int> rows(rhi - rlo);
+        for (int r = rlo; r < rhi; ++r) rows[r - rlo] = r;
+        tmk::TcTask task{};
+        task.mode = 2;
+        task.c_lim = g.ec;
+        task.c_last = -1;
+        task.mask = ctx->visits.p;
+        task.out_rho = rho_loc;
+        task.gate = dense_flag;
+        Phase ph(ctx, "survivor_eval");
+        np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+    }
+    const tmk::CorrJob job = make_job(ctx, img, ws, T);
+    CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
+                      nullptr, ctx->partials.p + np, kListBlocks, s, 1));
+    ctx->add(2);
+    reduce_to(ctx, np + kListBlocks, 2);
+}
+
 tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
                        const tm_match_params& P, uint8_t* visits_host) {
     const tmk::GridDesc& g = in.g;
@@ -1217,7 +1314,9 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     const bool seq = policy == TM_POLICY_SEQUENTIAL;
 
     // ---- scan 1 + threshold bootstrap (matcher.cpp:116-125) ---------------------------
+    HT("search_begin");
     centre_scan(ctx, img, ws, T, g);
+    HT("centre_scan");
     CK(tmk::threshold_init(ctx->cells.p + 0, P.has_init_threshold, P.init_threshold,
                            ctx->thr.p, s));
     ctx->add(1);
@@ -1238,6 +1337,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         CK(tmk::threshold_raise(ctx->cells.p + 1, ctx->thr.p, s));
         ctx->add(1);
         seeded = ctx->seeded.p;
+        HT("seeds");
     }
 
     // ---- scan 2: bound test + survivor compaction -------------------------------------
@@ -1253,16 +1353,24 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     }
     double T0 = 0.0;
     tmk::Tally tally{};
-    CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
-    CK(cudaStreamSynchronize(s));
     const unsigned long long* count = &ctx->tally.p->survivors;
     double* rho_loc = nullptr;
-    if (seq) {
-        ctx->seq_rho.ensure(E);
-        rho_loc = ctx->seq_rho.p;
+    HT("sec_compact");
+    const bool device_dispatch = !seq && tc_path(ctx, img, T);
+    if (device_dispatch) {
+        // frozen / seeded: nothing changes the threshold after scan 2's bound test, so the
+        // final readback gives T0; the survivor count never leaves the device
+        eval_survivors_dev(ctx, img, ws, T, g, nullptr);
+    } else {
+        CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        if (seq) {
+            ctx->seq_rho.ensure(E);
+            rho_loc = ctx->seq_rho.p;
+        }
+        eval_survivors(ctx, img, ws, T, g, tally.survivors, rho_loc);
     }
-    eval_survivors(ctx, img, ws, T, g, tally.survivors, rho_loc);
 
     double final_T = T0;
     if (seq) {
@@ -1305,13 +1413,16 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         reduce_to(ctx, kListBlocks, 2);
         final_T = Tcur;
     }
+    HT("survivors");
     tmk::CellH cells[3];
     CK(cudaMemcpyAsync(cells, ctx->cells.p, sizeof cells, cudaMemcpyDeviceToHost, s));
     CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
     double thr_after = 0.0;
     CK(cudaMemcpyAsync(&thr_after, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
     if (visits_host) CK(cudaMemcpyAsync(visits_host, visits, E, cudaMemcpyDeviceToHost, s));
+    HT("readback_enq");
     CK(cudaStreamSynchronize(s));
+    HT("sync");
 
     tmk::CellH best = cells[0];
     if (policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
@@ -1320,6 +1431,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     const long long eliminated = (long long)tally.eliminated;
     // sequential: alive candidates (dead ones were moved to `eliminated` by seq_final)
     const long long retained = seq ? (long long)tally.pad : (long long)tally.retained;
+    if (device_dispatch) final_T = thr_after;  // = T0 (see above)
     if (policy == TM_POLICY_SEEDED) {
         final_T = thr_after;
         if ((cells[2].flags & 1) && !(cells[2].flags & 2)) final_T = std::max(final_T, cells[2].rho);
@@ -1475,11 +1587,15 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
 tm_match_result run_one(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* t,
                         const tm_match_params& P, uint8_t* visits) {
     const int m = prep->m, n = prep->n;
+    HT("start");
     const Tmpl T = upload_template(ctx, t, m, n);
+    HT("template");
     tm_image* search_img = prep->search_img ? prep->search_img.get() : img;
     const WS* ws = prep->search_img ? prep->search_ws.get() : &get_ws(ctx, img, m, n);
     SearchIn in{search_img, ws, prep->g, prep->map.p};
     tm_match_result r = search(ctx, in, T, P, visits);
+    HT("search_end");
+    htrace().flush("run");
     if (prep->mode == TM_MODE_OPTA) {
         r.mode = TM_MODE_OPTA;
         const int d = prep->kappa * prep->radius;

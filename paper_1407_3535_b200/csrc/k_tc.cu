@@ -145,6 +145,10 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ntiles = task.nbands * task.ntc;
+    if (task.gate && *task.gate == 0) {  // not selected on the device (survivor_dispatch)
+        if (tid == 0) partials[blockIdx.x] = CellH{0.0, -1, -1, 2};
+        return;
+    }
 
     if (tid == 0) {
         for (int s = 0; s < kTcStages; ++s) {
@@ -487,6 +491,23 @@ __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_
 
 }  // namespace
 
+namespace {
+__global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
+                                    unsigned long long* list_count) {
+    const unsigned long long n = tally->survivors;
+    const bool dense = n * 16 > E;
+    *dense_flag = dense ? 1 : 0;
+    *list_count = dense ? 0ull : n;
+}
+
+}  // namespace
+
+cudaError_t survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
+                              unsigned long long* list_count, cudaStream_t s) {
+    k_survivor_dispatch<<<1, 1, 0, s>>>(tally, E, dense_flag, list_count);
+    return cudaGetLastError();
+}
+
 bool tc_supported(int m, int n) {
     // exact s32 dots; Kx <= 256 bytes per MMA chain; at least one template row per chunk
     return double(m) * double(n) * 65025.0 < 2147483648.0 && n + 15 <= 256;
@@ -588,21 +609,18 @@ cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* 
     *nparts = grid;
     const size_t smem = job.plan.smem;
     cudaError_t e = cudaSuccess;
+    static size_t attr_set[3] = {0, 0, 0};
+    if (task.mode < 0 || task.mode > 2) return cudaErrorInvalidValue;
+    if (attr_set[task.mode] < smem) {
+        const void* fn = task.mode == 0 ? (const void*)k_tc_corr<0>
+                        : task.mode == 1 ? (const void*)k_tc_corr<1> : (const void*)k_tc_corr<2>;
+        cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
+        attr_set[task.mode] = smem;
+    }
     switch (task.mode) {
-        case 0:
-            cudaFuncSetAttribute(k_tc_corr<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            k_tc_corr<0><<<grid, kTcThreads, smem, s>>>(job, task, partials);
-            break;
-        case 1:
-            cudaFuncSetAttribute(k_tc_corr<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            k_tc_corr<1><<<grid, kTcThreads, smem, s>>>(job, task, partials);
-            break;
-        case 2:
-            cudaFuncSetAttribute(k_tc_corr<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
-            k_tc_corr<2><<<grid, kTcThreads, smem, s>>>(job, task, partials);
-            break;
-        default:
-            return cudaErrorInvalidValue;
+        case 0: k_tc_corr<0><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
+        case 1: k_tc_corr<1><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
+        default: k_tc_corr<2><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
     }
     e = cudaGetLastError();
     return e;

@@ -267,10 +267,15 @@ struct TcTask {
     const uint8_t* mask;
     long long* dbg;     // optional per-CTA pipeline wait counters (8 per CTA)
     int dbg_flags;      // timing experiments only: 1 = no image copies, 2 = no epilogue
+    const int* gate;    // optional device flag: 0 -> the launch only writes empty partials
     const int4* sched;  // tc_schedule() rows, per chunk at sched_off[ch], sched_len[ch]
     int sched_total;    // rows over all chunks
     int sched_off[kTcMaxChunks], sched_len[kTcMaxChunks];
 };
+// Device-side choice between the dense (tensor-core) and list survivor evaluation:
+// dense_flag = survivors*16 > E, list_count = dense ? 0 : survivors.
+cudaError_t survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
+                              unsigned long long* list_count, cudaStream_t s);
 bool tc_supported(int m, int n);
 TcPlan tc_plan(int m, int n, int sr, size_t smem_budget);
 // rows of a band of rmax rows, see k_tc.cu (4 ints per row)
