@@ -8,8 +8,8 @@ image with half the tiles blurred, one 64x64 template; seeded synthetic data).
 
   value : extent locations per second of device time, image resident in HBM, L2 flushed
           between steps (the device-timed step excludes the flush).
-  e2e   : the same metric through the reference-facing call tm_match() (host FP64 image
-          in pinned memory -> device -> result back to the host), wall-clock per step.
+  e2e   : the same metric through the public 8-bit API (pinned host image ->
+          tm_image_upload_u8 -> tm_prepare -> tm_run_u8 -> result on the host), wall clock.
 
 --impl reference times the reference's own CPU implementation (oracle/_ref, compiled from
 /root/reference) on the same workload with all host threads.
@@ -60,7 +60,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -199,7 +199,7 @@ def run_b200(args):
     ctx.synchronize()
     if ws > 1:
         torch.distributed.barrier()
-    ctx.set_profiling(True)
+    # ---- timed region: profiling off (no per-call event timers or syncs) --------------
     launches0 = ctx.launches
     clocks = ClockSampler(local)
     clocks.start()
@@ -219,8 +219,6 @@ def run_b200(args):
     torch.cuda.synchronize()
     clk = clocks.stop()
     launches = (ctx.launches - launches0) / args.steps
-    phases = ctx.phase_times()
-    ctx.set_profiling(False)
     ms = statistics.mean(times)
     if ws > 1:
         t = torch.tensor([ms], device=f"cuda:{local}")
@@ -229,26 +227,52 @@ def run_b200(args):
         torch.distributed.barrier()
     value = ws * wl.extent / (ms / 1e3)
 
-    # ---- e2e through the reference-facing C ABI call (host FP64 buffers) -------------
-    img_host = torch.empty(wl.image.shape, dtype=torch.float64, pin_memory=True)
+    # ---- per-phase device times: a separate, untimed profiled pass ---------------------
+    ctx.set_profiling(True)
+    base = ctx.phase_times()
+    nprof = max(3, min(args.steps, 10))
+    for _ in range(nprof):
+        with torch.cuda.stream(stream):
+            flush.zero_()
+        torch.cuda.synchronize()
+        step()
+    after = ctx.phase_times()
+    ctx.set_profiling(False)
+    phases = {k: {"count": (v["count"] - base.get(k, {"count": 0})["count"]) / nprof,
+                  "ms": (v["ms"] - base.get(k, {"ms": 0.0})["ms"]) / nprof}
+              for k, v in after.items() if v["ms"] - base.get(k, {"ms": 0.0})["ms"] > 0}
+
+    # ---- e2e through the public 8-bit API: pinned host image -> tm_image_upload_u8 ->
+    # tm_prepare -> tm_run_u8 -> result on the host, wall clock per step ---------------
+    img_host = torch.empty(wl.image.shape, dtype=torch.uint8, pin_memory=True)
     img_host.numpy()[:] = wl.image
-    t_host = tmpl.astype(np.float64)
+    t_host = torch.empty(tmpl.shape, dtype=torch.uint8, pin_memory=True)
+    t_host.numpy()[:] = tmpl
+    img_e2e = ctx.image(np.zeros(wl.image.shape, np.uint8))
+
+    def e2e_step():
+        img_e2e.upload_u8(img_host.numpy())
+        prep = ctx.prepare(img_e2e, m, n, mode="egs")
+        r = ctx.run(prep, t_host.numpy(), policy=args.policy)
+        prep.close()
+        return r
+
     for _ in range(max(1, args.warmup)):
-        ctx.match(t_host, img_host.numpy(), mode="egs", policy=args.policy)
+        e2e_step()
     e2e_ms = []
     for _ in range(args.steps):
         with torch.cuda.stream(stream):
             flush.zero_()
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        r2 = ctx.match(t_host, img_host.numpy(), mode="egs", policy=args.policy)
+        r2 = e2e_step()
         e2e_ms.append((time.perf_counter() - t0) * 1e3)
     e2e = statistics.mean(e2e_ms)
     if ws > 1:
         t = torch.tensor([e2e], device=f"cuda:{local}")
         torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
         e2e = float(t.item())
-    assert (r2.best_row, r2.best_col) == (res.best_row, res.best_col)
+    assert (r2.best_row, r2.best_col, r2.best_rho) == (res.best_row, res.best_col, res.best_rho)
 
     if rank != 0:
         if ws > 1:
@@ -256,22 +280,37 @@ def run_b200(args):
         return 0
 
     # ---- roofline of the dominant kernel ---------------------------------------------
+    # The step's dominant kernel is the fused R_co kernel k_acf (EGS candidates).  Its
+    # algorithmic HBM traffic per evaluated candidate: the 8-bit image once (p*q bytes),
+    # the member statistics (mu, omega, flat: 17 B per extent location) and the R_co map
+    # write (8 B per location).  Candidates after the first rejection exit at entry.
     peaks = _peaks()
+    p_, q_ = wl.image.shape
+    E = wl.extent
+    n_cand = len(info.get("egs_trace", [])) + 1
+    ac = phases.get("autocorr_u8", {"count": 0, "ms": float("nan")})
+    ac_bytes = n_cand * (p_ * q_ + 25.0 * E)
+    hbm_peak = peaks.get("hbm_gbs", 6534.1)
+    ac_gbs = ac_bytes / (ac["ms"] / 1e3) / 1e9
+    roofline = {"bound": "hbm", "kernel": "k_acf<H> (fused sliding-window R_co, EGS)",
+                "achieved": ac_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ac_gbs / hbm_peak,
+                "traffic": None,
+                "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
+                "algorithmic": f"{n_cand} candidates x (p*q + 25 B x {E} locations)",
+                "kernel_ms": ac["ms"],
+                "share_of_step": ac["ms"] / max(sum(v["ms"] for v in phases.values()), 1e-9)}
+    # secondary: the tensor-core centre scan (tcgen05 kind::i8), useful ops only
     G = res.centers
     cs = phases.get("centre_scan", {"count": 1, "ms": float("nan")})
-    cs_ms = cs["ms"] / max(cs["count"], 1)
-    flops = 2.0 * m * n * G
-    sm_max = peaks.get("sm_max_mhz", 1965.0)
-    fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12
-    achieved = flops / (cs_ms / 1e3) / 1e12
-    share = cs["ms"] / max(sum(p["ms"] for p in phases.values()), 1e-9)
-    roofline = {"bound": "fp32", "kernel": "k_corr_band (centre scan, FP32-exact FFMA)",
-                "achieved": achieved, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": achieved / fp32_peak, "traffic": None,
-                "peak_source": f"nominal FP32 148 SM x 128 lanes x 2 x {sm_max:.0f} MHz "
-                               "(MEASURED_PEAKS.json has no FP32 entry)",
-                "algorithmic": f"2*m*n FLOP per centre x {G} centres per launch",
-                "kernel_ms": cs_ms, "share_of_step": share}
+    i8_peak = 2.0 * peaks.get("bf16_tflops", 1649.1)
+    cs_tops = 2.0 * m * n * G / (cs["ms"] / 1e3) / 1e12
+    roofline["secondary"] = [{
+        "bound": "tensor", "kernel": "k_tc_corr<1> + k_centre_epi (centre scan, tcgen05 kind::i8)",
+        "achieved": cs_tops, "peak": i8_peak, "unit": "TOP/s", "frac": cs_tops / i8_peak,
+        "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (i8 MMA: K=32 per instruction "
+                       "vs K=16 for bf16 at the same issue rate)",
+        "algorithmic": f"2*m*n useful ops per centre x {G} centres (phase time incl. B build "
+                       "and FP64 epilogue)", "kernel_ms": cs["ms"]}]
 
     cpu = None
     if not args.no_cpu_baseline:
@@ -285,7 +324,8 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "u8->fp32-exact (int dot), f64 epilogue",
+        "vs_baseline": None,
+        "dtype": "u8 (s32 tensor-core / exact-FP32 dots, u32 window sums), f64 epilogues",
         "data": "synthetic (seeded 1/f^beta generator, SURVEY 8d; BASELINE config 2)",
         "config": {"workload": f"{wl.name}: {wl.description}", "extent": wl.extent,
                    "templates": 1, "mode": "egs", "policy": args.policy,
@@ -295,11 +335,13 @@ def run_b200(args):
                    "elim_pct": res.elim_pct, "eliminated": res.eliminated,
                    "retained": res.retained, "centers": res.centers, "h_e": info["h"],
                    "prep_ms": info["prep_ms"]},
-        "phases_ms_per_step": {k: v["ms"] / args.steps for k, v in phases.items()},
+        "phases_ms_per_step": {k: v["ms"] for k, v in phases.items()},
         "gpu_launches": launches,
         "e2e": {"value": ws * wl.extent / (e2e / 1e3), "unit": UNIT,
-                "h2d_bytes_per_step": int(wl.image.size * 8 + tmpl.size * 8),
-                "d2h_bytes_per_step": 128, "ms_per_step": e2e},
+                "h2d_bytes_per_step": int(wl.image.size + tmpl.size),
+                "d2h_bytes_per_step": 112, "ms_per_step": e2e,
+                "path": "pinned u8 host image -> tm_image_upload_u8 -> tm_prepare -> "
+                        "tm_run_u8 -> tm_match_result on the host (wall clock)"},
         "roofline": roofline,
         "cpu_baseline": cpu,
         "clocks": clk,
@@ -313,7 +355,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
