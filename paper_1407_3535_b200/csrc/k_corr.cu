@@ -234,31 +234,35 @@ __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                 int lane_flush, int rho_by_loc) {
+    // One CTA per location (grid-stride): warp w owns template rows [w*m/8, (w+1)*m/8), so
+    // a location costs one or two batches of independent loads per warp instead of m/8
+    // dependent batches for a single warp.  Each lane's FP32 partials cover < lane_flush
+    // rows of one column (exact); warp and block sums of these exact integers in FP64 are
+    // order-independent.
     __shared__ Cell scratch[8];
-    const int lane = threadIdx.x & 31;
+    __shared__ double wsum[8];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long long nloc = min((long long)*count, (long long)max_count);
-    const long long warp0 = (blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5;
-    const long long nwarps = (gridDim.x * (long long)blockDim.x) >> 5;
     const TStats ts = to_ts(job.ts);
+    const int rows_per = (job.m + 7) / 8;
+    const int i_lo = min(job.m, wid * rows_per), i_hi = min(job.m, i_lo + rows_per);
     Cell best = no_cell();
-    for (long long li = warp0; li < nloc; li += nwarps) {
+    for (long long li = blockIdx.x; li < nloc; li += gridDim.x) {
         const int2 rc = locs[li];
         double dacc = 0.0;
         const float* ib = job.imgf + size_t(rc.x) * job.pitch + rc.y;
-        // a lane accumulates one template column over rows; two independent FP32 partials
-        // (even/odd rows) stay exact while each covers < lane_flush rows (2^24 bound)
         for (int j = lane; j < job.n; j += 32) {
             const float* tp = job.tf + j;
-            for (int i0 = 0; i0 < job.m; i0 += 2 * lane_flush) {
-                const int i1 = min(job.m, i0 + 2 * lane_flush);
+            for (int i0 = i_lo; i0 < i_hi; i0 += 2 * lane_flush) {
+                const int i1 = min(i_hi, i0 + 2 * lane_flush);
                 float a0 = 0.f, a1 = 0.f;
-                int i = i0;
-                for (; i + 8 <= i1; i += 8) {
+                for (int i = i0; i < i1; i += 8) {
                     float v[8], t[8];
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
-                        v[u] = __ldg(ib + size_t(i + u) * job.pitch + j);
-                        t[u] = __ldg(tp + size_t(i + u) * job.npad);
+                        const bool ok = i + u < i1;
+                        v[u] = ok ? __ldg(ib + size_t(i + u) * job.pitch + j) : 0.f;
+                        t[u] = ok ? __ldg(tp + size_t(i + u) * job.npad) : 0.f;
                     }
 #pragma unroll
                     for (int u = 0; u < 8; u += 2) {
@@ -266,21 +270,25 @@ __global__ void __launch_bounds__(256)
                         a1 = fmaf(t[u + 1], v[u + 1], a1);
                     }
                 }
-                for (; i < i1; ++i)
-                    a0 = fmaf(__ldg(tp + size_t(i) * job.npad), __ldg(ib + size_t(i) * job.pitch + j), a0);
                 dacc += double(a0) + double(a1);
             }
         }
         dacc = warp_sum(dacc);
-        if (lane == 0) {
+        if (lane == 0) wsum[wid] = dacc;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double d = 0.0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) d += wsum[w];
             const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
             const bool wflat = job.st.flat[kk];
-            const double rho = zncc_epilogue(dacc, ts, job.st.mu[kk], job.st.omega[kk], wflat);
+            const double rho = zncc_epilogue(d, ts, job.st.mu[kk], job.st.omega[kk], wflat);
             if (out_rho) out_rho[rho_by_loc ? kk : li] = rho;
             if (out_deg) out_deg[li] = ts.flat || wflat;
             const Cell cand = make_cell(rc.x, rc.y, rho, ts.flat || wflat);
             if (better(cand, best)) best = cand;
         }
+        __syncthreads();
     }
     best = block_best(best, scratch);
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
