@@ -292,9 +292,18 @@ def run_b200(args):
     ac_bytes = n_cand * (p_ * q_ + 25.0 * E)
     hbm_peak = peaks.get("hbm_gbs", 6534.1)
     ac_gbs = ac_bytes / (ac["ms"] / 1e3) / 1e9
+    traffic = None  # DRAM read+write per k_acf launch from the committed ncu --set full capture
+    try:
+        kt = json.load(open(os.path.join(ROOT, "profiles", "r01_kernel_traffic.json")))["kernels"]
+        acf = [v for k, v in kt.items() if "k_acf" in k and v["duration_us"] > 10.0]
+        if acf:
+            traffic = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for v in acf) / len(acf)
+    except Exception:
+        traffic = None
     roofline = {"bound": "hbm", "kernel": "k_acf<H> (fused sliding-window R_co, EGS)",
                 "achieved": ac_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ac_gbs / hbm_peak,
-                "traffic": None,
+                "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r01_kernel_traffic.json)",
+                "algorithmic_bytes_per_launch": ac_bytes / max(n_cand, 1),
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
                 "algorithmic": f"{n_cand} candidates x (p*q + 25 B x {E} locations)",
                 "kernel_ms": ac["ms"],
