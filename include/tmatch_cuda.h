@@ -202,6 +202,14 @@ int tm_run(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, int n
 int tm_run_u8(tm_ctx* ctx, tm_prep* prep, tm_image* img, const uint8_t* tmpls, int ntmpl,
               const tm_match_params* params, tm_match_result* out, uint8_t* visits);
 
+/* One full search on a device-resident image: prepare_egs / prepare_opta + run_egs /
+ * run_opta (matcher.hpp:80 match, without the image upload).  The template is uploaded
+ * while the preparation's kernels run, and no preparation handle is returned. */
+int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+              const tm_match_params* params, tm_match_result* out);
+int tm_search_u8(tm_ctx* ctx, tm_image* img, const uint8_t* tmpl, int m, int n,
+                 const tm_match_params* params, tm_match_result* out);
+
 /* transitive_search (matcher.hpp:37-38) with a caller-supplied map/grid. */
 int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
                          const double* map, int h, int w, const tm_match_params* params,

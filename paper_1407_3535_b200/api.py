@@ -335,6 +335,22 @@ class Context:
                                                C.byref(rho), C.byref(deg)))
         return r.value, c.value, rho.value, bool(deg.value)
 
+    def search(self, img, t, mode="egs", **kw):
+        """One full search on a device-resident image (tm_search / tm_search_u8): prepare +
+        run in one call, the template upload overlapped with the preparation."""
+        img = self.image(img)
+        t = np.asarray(t)
+        m, n = t.shape
+        p = make_params(mode=mode, **kw)
+        res = MatchResult()
+        if t.dtype == np.uint8:
+            t = np.ascontiguousarray(t)
+            N.check(N.lib().tm_search_u8(self.h, img.h, _u8ptr(t), m, n, C.byref(p), C.byref(res)))
+        else:
+            t = np.ascontiguousarray(t, dtype=np.float64)
+            N.check(N.lib().tm_search(self.h, img.h, _dptr(t), m, n, C.byref(p), C.byref(res)))
+        return res
+
     def match(self, t, image, mode="egs", record_visits=False, **kw):
         """match (matcher.hpp:80): host buffers in, host result out (end to end)."""
         t = np.ascontiguousarray(t, dtype=np.float64)

@@ -21,6 +21,7 @@
 #include <cstdio>
 #include <cmath>
 #include <cstring>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -955,7 +956,8 @@ struct EgsOut {
 
 // efficient_group_size (egs.cpp:39-91); best map ends in `best`.
 EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, int h0, int w0,
-                      double rho_tb, double xi, int max_group, DBuf<double>& best) {
+                      double rho_tb, double xi, int max_group, DBuf<double>& best,
+                      const std::function<void()>* before_sync = nullptr) {
     if (h0 < 1 || w0 < 1 || h0 % 2 == 0 || w0 % 2 == 0)
         invalid("efficient_group_size: initial group size must be odd");
     if (rho_tb <= 0.0 || rho_tb >= 1.0)
@@ -1008,6 +1010,10 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         }
         unsigned long long nr[4] = {0, 0, 0, 0};
         CK(cudaMemcpyAsync(nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost, ctx->s));
+        if (before_sync && *before_sync) {  // host work overlapped with the candidates
+            (*before_sync)();
+            before_sync = nullptr;
+        }
         CK(cudaStreamSynchronize(ctx->s));
         for (int k = 0; k < nc; ++k) {
             const tm_egs_iter cost = total_cost_h(er, ec, cand[k].h, cand[k].w, (long long)nr[k], 0.0);
@@ -1555,7 +1561,8 @@ std::vector<double> params_profile(const tm_match_params& P) {
     return std::vector<double>(P.kernel_profile, P.kernel_profile + P.kernel_len);
 }
 
-tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params& P) {
+tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params& P,
+                 const std::function<void()>* before_sync = nullptr) {
     auto prep = std::make_unique<tm_prep>();
     prep->params = P;
     prep->profile = params_profile(P);
@@ -1571,7 +1578,7 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     if (prep->mode == TM_MODE_EGS) {
         WS& ws = get_ws(ctx, img, m, n);
         EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
-                                  P.max_group, prep->map);
+                                  P.max_group, prep->map, before_sync);
         prep->h = e.h;
         prep->w = e.w;
         prep->cost = e.cost;
@@ -1584,12 +1591,21 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     return prep.release();
 }
 
+tm_match_result run_uploaded(tm_ctx* ctx, tm_prep* prep, tm_image* img, const Tmpl& T,
+                             const tm_match_params& P, uint8_t* visits);
+
 tm_match_result run_one(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* t,
                         const tm_match_params& P, uint8_t* visits) {
-    const int m = prep->m, n = prep->n;
     HT("start");
-    const Tmpl T = upload_template(ctx, t, m, n);
+    const Tmpl T = upload_template(ctx, t, prep->m, prep->n);
     HT("template");
+    return run_uploaded(ctx, prep, img, T, P, visits);
+}
+
+// run_egs / run_opta with the template already uploaded (ctx->tf / ctx->td).
+tm_match_result run_uploaded(tm_ctx* ctx, tm_prep* prep, tm_image* img, const Tmpl& T,
+                             const tm_match_params& P, uint8_t* visits) {
+    const int m = prep->m, n = prep->n;
     tm_image* search_img = prep->search_img ? prep->search_img.get() : img;
     const WS* ws = prep->search_img ? prep->search_ws.get() : &get_ws(ctx, img, m, n);
     SearchIn in{search_img, ws, prep->g, prep->map.p};
@@ -1826,9 +1842,10 @@ void tm_image_destroy(tm_image* img) {
     tm_ctx* ctx = img->ctx;
     if (ctx) {
         {
+            // stream-ordered frees (cudaFreeAsync on the context stream): no sync needed
             std::lock_guard<std::mutex> lk(ctx->mu);
             cudaSetDevice(ctx->device);
-            cudaStreamSynchronize(ctx->s);
+            g_stream = ctx->s;
             delete img;
         }
         ctx_unref(ctx);
@@ -2059,7 +2076,7 @@ void tm_prep_destroy(tm_prep* prep) {
         {
             std::lock_guard<std::mutex> lk(ctx->mu);
             cudaSetDevice(ctx->device);
-            cudaStreamSynchronize(ctx->s);
+            g_stream = ctx->s;
             delete prep;
         }
         ctx_unref(ctx);
@@ -2089,6 +2106,38 @@ int tm_run_u8(tm_ctx* ctx, tm_prep* prep, tm_image* img, const uint8_t* tmpls, i
     std::vector<double> t(mn * size_t(ntmpl));
     for (size_t i = 0; i < t.size(); ++i) t[i] = tmpls[i];
     return tm_run(ctx, prep, img, t.data(), ntmpl, params, out, visits);
+}
+
+int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+              const tm_match_params* params, tm_match_result* out) {
+    return guard(ctx, [&] {
+        if (!img || !tmpl || !params || !out) invalid("tm_search: null argument");
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        Tmpl T;
+        bool uploaded = false;
+        const std::function<void()> hook = [&] {
+            T = upload_template(ctx, tmpl, m, n);
+            uploaded = true;
+        };
+        std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params, &hook));
+        prep->ctx = nullptr;  // internal: not counted as a context reference
+        if (!uploaded) T = upload_template(ctx, tmpl, m, n);
+        *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);
+        CK(cudaEventRecord(ctx->ev1, ctx->s));
+        CK(cudaEventSynchronize(ctx->ev1));
+        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+    });
+}
+
+int tm_search_u8(tm_ctx* ctx, tm_image* img, const uint8_t* tmpl, int m, int n,
+                 const tm_match_params* params, tm_match_result* out) {
+    if (!tmpl || m < 1 || n < 1) {
+        g_err = "tm_search_u8: invalid template";
+        return TM_EINVAL;
+    }
+    std::vector<double> t(size_t(m) * n);
+    for (size_t i = 0; i < t.size(); ++i) t[i] = tmpl[i];
+    return tm_search(ctx, img, t.data(), m, n, params, out);
 }
 
 int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,

@@ -369,3 +369,25 @@ def test_tc_dense_survivors_weak_template(port):
     assert res[:3] == res[3:]
     b = port.brute(t, img.astype(np.float64))
     assert (res[0][1], res[0][2], res[0][3]) == (b.best_row, b.best_col, b.best_rho)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("policy", ["seeded", "frozen", "sequential", "reference"])
+@pytest.mark.parametrize("mode", ["egs", "opta"])
+def test_search_equals_prepare_run(ctx, policy, mode):
+    """tm_search / tm_search_u8 (prepare + run in one call, template uploaded while the
+    preparation runs) give exactly the prepare + run results."""
+    rng = np.random.default_rng(3)
+    base = np.cumsum(np.cumsum(rng.normal(size=(140, 170)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    t = np.clip(np.rint(img[50:70, 90:112] * 0.9 + 8 + rng.normal(0, 3, (20, 22))), 0, 255)
+    gi = ctx.image(img)
+    prep = ctx.prepare(gi, 20, 22, mode=mode)
+    want = ctx.run(prep, t, policy=policy, parallel=True, threads=4)
+    prep.close()
+    for tt in (t, t.astype(np.uint8)):
+        got = ctx.search(gi, tt, mode=mode, policy=policy, parallel=True, threads=4)
+        for k in ("best_row", "best_col", "best_rho", "refined_row", "refined_col",
+                  "refined_rho", "eliminated", "retained", "centers", "ops",
+                  "final_threshold"):
+            assert getattr(got, k) == getattr(want, k), k
