@@ -254,6 +254,15 @@ struct tm_ctx {
     bool tc = true;
     DBuf<uint8_t> tc_b;
     std::map<std::vector<long long>, std::unique_ptr<TcGeo>> tc_geo;
+    // pinned readback block: device->host copies into it are asynchronous, so the host can
+    // keep working (e.g. upload the next template) until it synchronises
+    struct HostRes {
+        unsigned long long nr[4];
+        tmk::CellH cells[3];
+        tmk::Tally tally;
+        double thr;
+    };
+    HostRes* hres = nullptr;
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -1008,13 +1017,15 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
                 ctx->add(1);
             }
         }
-        unsigned long long nr[4] = {0, 0, 0, 0};
-        CK(cudaMemcpyAsync(nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaMemcpyAsync(ctx->hres->nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost,
+                           ctx->s));
         if (before_sync && *before_sync) {  // host work overlapped with the candidates
             (*before_sync)();
             before_sync = nullptr;
         }
         CK(cudaStreamSynchronize(ctx->s));
+        unsigned long long nr[4] = {0, 0, 0, 0};
+        for (int k = 0; k < nc; ++k) nr[k] = ctx->hres->nr[k];
         for (int k = 0; k < nc; ++k) {
             const tm_egs_iter cost = total_cost_h(er, ec, cand[k].h, cand[k].w, (long long)nr[k], 0.0);
             const bool accepted =
@@ -1420,15 +1431,17 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         final_T = Tcur;
     }
     HT("survivors");
-    tmk::CellH cells[3];
-    CK(cudaMemcpyAsync(cells, ctx->cells.p, sizeof cells, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
-    double thr_after = 0.0;
-    CK(cudaMemcpyAsync(&thr_after, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+    tm_ctx::HostRes* hr = ctx->hres;
+    CK(cudaMemcpyAsync(hr->cells, ctx->cells.p, sizeof hr->cells, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hr->tally, ctx->tally.p, sizeof hr->tally, cudaMemcpyDeviceToHost, s));
+    CK(cudaMemcpyAsync(&hr->thr, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
     if (visits_host) CK(cudaMemcpyAsync(visits_host, visits, E, cudaMemcpyDeviceToHost, s));
     HT("readback_enq");
     CK(cudaStreamSynchronize(s));
     HT("sync");
+    tmk::CellH cells[3] = {hr->cells[0], hr->cells[1], hr->cells[2]};
+    tally = hr->tally;
+    const double thr_after = hr->thr;
 
     tmk::CellH best = cells[0];
     if (policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
@@ -1666,6 +1679,7 @@ void ctx_release(tm_ctx* ctx) {
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t ev : ctx->pool) cudaEventDestroy(ev);
+    if (ctx->hres) cudaFreeHost(ctx->hres);
     delete ctx;  // stream-ordered frees of the scratch buffers
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -1721,6 +1735,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         g_stream = ctx->s;
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
+        CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->hres), sizeof(tm_ctx::HostRes)));
         ctx->counters.ensure(32);
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
