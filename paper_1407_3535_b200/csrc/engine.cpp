@@ -393,11 +393,23 @@ void alloc_u8(tm_ctx* ctx, tm_image* img) {
     CK(cudaMemsetAsync(img->u8.p + N, 0, pad, ctx->s));
 }
 
+// Layout conversions of a new 8-bit raster: the FP32 copy (list kernels) and the
+// 16-byte-pitched copy for the tensor-core kernels (sized for any template width).
+void tc_pitch_copy(tm_ctx* ctx, tm_image* img) {
+    const int pitch = tmk::tc_pitch(img->q, img->q);
+    const int rows = img->p + 1;
+    img->u8p.ensure(size_t(rows) * pitch);
+    CK(tmk::tc_pitch_image(img->u8.p, img->p, img->q, img->u8p.p, pitch, rows, ctx->s));
+    ctx->add(1);
+    img->u8p_pitch = pitch;
+}
+
 void finish_integer_image(tm_ctx* ctx, tm_image* img) {
     img->pitch = ((img->q + 3) & ~3) + 128;  // zero pad: vector loads past the last column
     img->f32.ensure(size_t(img->p) * img->pitch);
     CK(tmk::u8_to_f32_pitched(img->u8.p, img->p, img->q, img->f32.p, img->pitch, ctx->s));
     ctx->add(1);
+    tc_pitch_copy(ctx, img);
 }
 
 void ensure_f64(tm_ctx* ctx, tm_image* img) {
@@ -579,14 +591,7 @@ bool tc_path(tm_ctx* ctx, const tm_image* img, const Tmpl& T) {
 }
 
 const uint8_t* tc_image(tm_ctx* ctx, tm_image* img, int ec) {
-    const int pitch = tmk::tc_pitch(img->q, ec);
-    if (img->u8p_pitch != pitch) {
-        const int rows = img->p + 1;
-        img->u8p.ensure(size_t(rows) * pitch);
-        CK(tmk::tc_pitch_image(img->u8.p, img->p, img->q, img->u8p.p, pitch, rows, ctx->s));
-        ctx->add(1);
-        img->u8p_pitch = pitch;
-    }
+    if (img->u8p_pitch < tmk::tc_pitch(img->q, ec)) tc_pitch_copy(ctx, img);
     return img->u8p.p;
 }
 
@@ -1788,7 +1793,6 @@ int tm_image_reset_cache(tm_image* img) {
     return guard(ctx, [&] {
         img->ws_cache.clear();
         img->have_qtotal = false;
-        img->u8p_pitch = 0;
     });
 }
 
@@ -1835,7 +1839,7 @@ int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
         ctx->add(1);
         img->have_f64 = false;
         img->have_qtotal = false;
-        img->u8p_pitch = 0;
+        tc_pitch_copy(ctx, img);
         img->ws_cache.clear();
     });
 }

@@ -50,16 +50,41 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ img, int p, int q, float
         out[size_t(r) * pitch + c] = c < q ? float(img[size_t(r) * q + c]) : 0.0f;
 }
 
-__global__ void k_sum_sq_u8(const uint8_t* __restrict__ img, size_t n,
-                            unsigned long long* out) {
+// Sum of squares of all pixels (q_total for 8-bit images, exact in u64): 16-byte loads,
+// block reduction, one atomic per block.
+__global__ void __launch_bounds__(256) k_sum_sq_u8(const uint8_t* __restrict__ img, size_t n,
+                                                   unsigned long long* out) {
+    __shared__ unsigned long long part[8];
     unsigned long long acc = 0;
-    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+    const size_t nv = n / 16;
+    const uint4* v4 = reinterpret_cast<const uint4*>(img);
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < nv;
          i += size_t(gridDim.x) * blockDim.x) {
-        const unsigned v = img[i];
-        acc += v * v;
+        const uint4 v = __ldg(v4 + i);
+        const unsigned w[4] = {v.x, v.y, v.z, v.w};
+        unsigned s = 0;  // 16 squares <= 16 * 65025 fit in 32 bits
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) {
+                const unsigned x = (w[k] >> (8 * b)) & 0xffu;
+                s += x * x;
+            }
+        acc += s;
     }
+    if (blockIdx.x == 0)  // tail bytes
+        for (size_t i = nv * 16 + threadIdx.x; i < n; i += blockDim.x) {
+            const unsigned x = img[i];
+            acc += x * x;
+        }
     acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+    if ((threadIdx.x & 31) == 0) part[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long t = 0;
+        for (int w = 0; w < int(blockDim.x >> 5); ++w) t += part[w];
+        atomicAdd(out, t);
+    }
 }
 
 // q_total for non-integer images.  The reference sums sequentially (stats.cpp:79); a
@@ -279,7 +304,8 @@ cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long
                             double* out, cudaStream_t s) {
     const size_t n = size_t(p) * q;
     cudaMemsetAsync(q_total, 0, sizeof(*q_total), s);
-    k_sum_sq_u8<<<grid_for(n, 256), 256, 0, s>>>(img, n, q_total);
+    const int blocks = int(std::min<size_t>(148 * 4, (n / 16 + 255) / 256 + 1));
+    k_sum_sq_u8<<<blocks, 256, 0, s>>>(img, n, q_total);
     k_prefix_noise_u64<<<1, 1, 0, s>>>(q_total, p, q, out);
     return cudaGetLastError();
 }
