@@ -890,7 +890,8 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
 // Launch the R_co map + retained count for one group size; n_r lands in *nr (device).
 void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
-                     double thr, double* map, unsigned long long* nr, const int* stop = nullptr) {
+                     double thr, double* map, unsigned long long* nr, int* stop = nullptr,
+                     const double* egs_prev = nullptr, double egs_xi = 0.0) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
@@ -898,8 +899,10 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
         if (ctx->ac_fused && tmk::autocorr_fused_supported(m, n, g)) {
+            // total_cost's central term (egs.cpp:28-37) for the in-kernel early rejection
+            const double central = double((g.er + g.h - 1) / g.h) * double((g.ec + g.w - 1) / g.w);
             CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, stop,
-                                      ctx->s));
+                                      ctx->s, egs_prev, central, egs_xi));
             ctx->add(1);
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
@@ -1015,7 +1018,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
             ctx->egs_maps[k].ensure(E);
             autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p, ctx->counters.p + 8 + k,
-                            dstop);
+                            dstop, dprev, xi);
             if (k + 1 < nc) {
                 CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
                                    cand[k].w, xi, cap, ctx->s));

@@ -563,7 +563,8 @@ template <int H>
 __global__ void __launch_bounds__(512)
     k_acf(const uint8_t* __restrict__ img, int p, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int tw,
-          int seg, const int* __restrict__ stop) {
+          int seg, int* __restrict__ stop, const double* __restrict__ egs_prev, double egs_central,
+          double egs_xi) {
     if (stop && *stop) return;  // EGS already decided (egs_decide): candidate not needed
     constexpr int hr = H / 2;
     extern __shared__ __align__(16) unsigned acf_smem[];
@@ -669,8 +670,8 @@ __global__ void __launch_bounds__(512)
         for (int j = 0; j < kSlots; ++j) {
             const int mr = crn + s_d[j] - hr;
             pf_row[j] = s_ok[j] && mr >= r0 && mr <= r1;
-            const size_t kc = pf_row[j] ? size_t(crn) * g.ec + s_cc[j] : 0;
-            const size_t km = pf_row[j] ? size_t(mr) * g.ec + s_c[j] : 0;
+            const unsigned kc = pf_row[j] ? unsigned(crn) * unsigned(g.ec) + unsigned(s_cc[j]) : 0u;
+            const unsigned km = pf_row[j] ? unsigned(mr) * unsigned(g.ec) + unsigned(s_c[j]) : 0u;
             pf_fc[j] = st.flat[kc];
             pf_fm[j] = st.flat[km];
             pf_mc[j] = st.mu[kc];
@@ -680,7 +681,17 @@ __global__ void __launch_bounds__(512)
         }
     };
     prefetch(ti0, cr);
-    unsigned long long local = 0;
+    // Retained count: per-event warp sums into a CTA counter.  Inside an EGS batch
+    // (egs_prev != 0) thread 0 flushes it to the global count every 4 events and replays
+    // the acceptance test of egs.cpp:61-88 (same FP64 operations as k_egs_decide): the test
+    // is monotone in n_r, so once the partial count already rejects the candidate the rest
+    // of its work cannot change the decision -- the CTA stops, and the stop flag makes the
+    // remaining CTAs and candidates exit.  Accepted candidates are always counted in full.
+    __shared__ unsigned cta_cnt;
+    if (threadIdx.x == 0) cta_cnt = 0u;
+    const double prev = (egs_prev && stop) ? *egs_prev : 0.0;
+    const bool can_reject = egs_prev && stop && fabs(prev) <= 1.7976931348623157e308;
+    int my_abort = 0, ev = 0;
     int parity = 0;
 #pragma unroll 1
     for (int ti = ti0;;) {
@@ -709,17 +720,28 @@ __global__ void __launch_bounds__(512)
                 if (lane == 31) wb[d * 32 + wid] = v[d];
             }
         }
-        __syncthreads();
+        if (__syncthreads_or(my_abort)) break;  // uniform: thread 0's flag from a past event
+        if (can_reject && threadIdx.x == 0 && (++ev & 3) == 0) {
+            const unsigned c = atomicExch(&cta_cnt, 0u);
+            const unsigned long long tot = atomicAdd(n_r, (unsigned long long)c) + c;
+            const double total = __dadd_rn(__dadd_rn(egs_central, double(tot)), 0.0);
+            if (!(__dsub_rn(prev, total) > __dmul_rn(egs_xi, prev))) {
+                my_abort = 1;
+                *reinterpret_cast<volatile int*>(stop) = 1;
+            }
+        }
+        unsigned evc = 0;
 #pragma unroll
         for (int j = 0; j < kSlots; ++j) {
             if (!pf_row[j]) continue;
             const int d = s_d[j];
-            const size_t km = size_t(cr + d - hr) * g.ec + s_c[j];
+            const unsigned km = unsigned(cr + d - hr) * unsigned(g.ec) + unsigned(s_c[j]);
             if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
                 map[km] = 1.0;
                 continue;
             }
             // S = P[u+n-1] - P[u-1], P the block prefix = warp prefix + earlier warp totals
+            // (at most kSpan warp totals between the two ends; wt is padded for the reads)
             const int u = s_u[j];
             const int i1 = u + n - 1, w1 = i1 >> 5;
             const unsigned* Ld = Lb + d * NY;
@@ -729,15 +751,20 @@ __global__ void __launch_bounds__(512)
                 S -= Ld[u - 1];
                 w0 = (u - 1) >> 5;
             }
-            for (int ww = w0; ww < w1; ++ww) S += wb[d * 32 + ww];
+            const unsigned* wd = wb + d * 32 + w0;
+            constexpr int kSpan = 8;
+#pragma unroll
+            for (int k = 0; k < kSpan; ++k) S += (w0 + k < w1) ? wd[k] : 0u;
             double val = 0.0;
             if (!pf_fc[j] && !pf_fm[j]) {
                 const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc[j]), pf_mm[j]));
                 val = dclamp(__ddiv_rn(num, __dmul_rn(pf_oc[j], pf_om[j])), -1.0, 1.0);
             }
             map[km] = val;
-            if (val < thr) ++local;
+            if (val < thr) ++evc;
         }
+        evc = __reduce_add_sync(0xffffffffu, evc);
+        if (lane == 0 && evc) atomicAdd(&cta_cnt, evc);
         if (++ti >= ti1) break;
         // ---- advance the window to the next centre row ----
         const int crn = g.center_row(ti);
@@ -757,8 +784,8 @@ __global__ void __launch_bounds__(512)
         }
         cr = crn;
     }
-    local = warp_sum(local);
-    if (lane == 0 && local) atomicAdd(n_r, local);
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
 }
 
 struct AcfGeom {
@@ -785,14 +812,14 @@ AcfGeom acf_geom(int m, int n, GridDesc gd) {
     nseg = std::min(nseg, std::max(1, (rows + seg_min - 1) / seg_min));
     a.seg = std::max(1, (rows + nseg - 1) / nseg);
     a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
-    a.smem = 2 * size_t(gd.h) * (a.ny + 32) * sizeof(unsigned);
+    a.smem = (2 * size_t(gd.h) * (a.ny + 32) + 16) * sizeof(unsigned);  // + padding (kSpan)
     return a;
 }
 
 template <int H>
 cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc gd, DevStats st,
-                       double thr, double* map, unsigned long long* n_r, const int* stop,
-                       cudaStream_t s) {
+                       double thr, double* map, unsigned long long* n_r, int* stop,
+                       const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
     const AcfGeom a = acf_geom(m, n, gd);
     if (a.ny == 0) return cudaErrorInvalidValue;
     static bool attr = false;
@@ -803,7 +830,7 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
         k_acf<H><<<grid, a.ny, a.smem, s>>>(img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
-                                            a.seg, stop);
+                                            a.seg, stop, egs_prev, egs_central, egs_xi);
     return cudaGetLastError();
 }
 
@@ -1037,19 +1064,27 @@ bool autocorr_fused_supported(int m, int n, GridDesc g) {
     // 32-bit row offsets; the walk may read h/2 <= kU8PadRows rows below the image
     const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
     return g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
-           (p + kU8PadRows) * q < (size_t(1) << 31) && acf_geom(m, n, g).ny > 0;
+           (p + kU8PadRows) * q < (size_t(1) << 31) &&
+           size_t(g.er) * g.ec < (size_t(1) << 32) && acf_geom(m, n, g).ny > 0;
 }
 
 cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
                               DevStats st, double retain_threshold, double* map,
-                              unsigned long long* n_r, const int* stop, cudaStream_t s) {
+                              unsigned long long* n_r, int* stop, cudaStream_t s,
+                              const double* egs_prev, double egs_central, double egs_xi) {
     switch (gd.h) {
-        case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
-        case 3: return launch_acf<3>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
-        case 5: return launch_acf<5>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
-        case 7: return launch_acf<7>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
-        case 9: return launch_acf<9>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
-        case 11: return launch_acf<11>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop, s);
+        case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
+        case 3: return launch_acf<3>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
+        case 5: return launch_acf<5>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
+        case 7: return launch_acf<7>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
+        case 9: return launch_acf<9>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
+        case 11: return launch_acf<11>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                     egs_prev, egs_central, egs_xi, s);
         default: return cudaErrorInvalidValue;
     }
 }
