@@ -682,7 +682,7 @@ __global__ void __launch_bounds__(512)
     };
     prefetch(ti0, cr);
     // Retained count: per-event warp sums into a CTA counter.  Inside an EGS batch
-    // (egs_prev != 0) thread 0 flushes it to the global count every 4 events and replays
+    // (egs_prev != 0) thread 0 flushes it to the global count every 2 events and replays
     // the acceptance test of egs.cpp:61-88 (same FP64 operations as k_egs_decide): the test
     // is monotone in n_r, so once the partial count already rejects the candidate the rest
     // of its work cannot change the decision -- the CTA stops, and the stop flag makes the
@@ -721,7 +721,7 @@ __global__ void __launch_bounds__(512)
             }
         }
         if (__syncthreads_or(my_abort)) break;  // uniform: thread 0's flag from a past event
-        if (can_reject && threadIdx.x == 0 && (++ev & 3) == 0) {
+        if (can_reject && threadIdx.x == 0 && (++ev & 1) == 0) {
             const unsigned c = atomicExch(&cta_cnt, 0u);
             const unsigned long long tot = atomicAdd(n_r, (unsigned long long)c) + c;
             const double total = __dadd_rn(__dadd_rn(egs_central, double(tot)), 0.0);
