@@ -256,13 +256,9 @@ struct tm_ctx {
     std::map<std::vector<long long>, std::unique_ptr<TcGeo>> tc_geo;
     // pinned readback block: device->host copies into it are asynchronous, so the host can
     // keep working (e.g. upload the next template) until it synchronises
-    struct HostRes {
-        unsigned long long nr[4];
-        tmk::CellH cells[3];
-        tmk::Tally tally;
-        double thr;
-    };
-    HostRes* hres = nullptr;
+    using HostRes = tmk::ResultBlock;
+    HostRes* hres = nullptr;   // pinned
+    DBuf<tmk::ResultBlock> res_dev;  // packed on the device by the final reduction
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -445,7 +441,10 @@ const double* image_prefix_noise(tm_ctx* ctx, tm_image* img) {
     if (!img->have_qtotal) {
         img->pn.ensure(2);
         if (img->integer) {
-            img->qt.ensure(1);
+            if (!img->qt.p) {  // running sum + block counter, kept zero between uses
+                img->qt.ensure(2);
+                CK(cudaMemsetAsync(img->qt.p, 0, 16, ctx->s));
+            }
             CK(tmk::prefix_noise_u8(img->u8.p, img->p, img->q, img->qt.p, img->pn.p + 1, ctx->s));
         } else {
             CK(tmk::prefix_noise_f64(img->f64.p, img->p, img->q, img->pn.p, img->pn.p + 1, ctx->s));
@@ -707,21 +706,16 @@ void upload_rows(tm_ctx* ctx, const std::vector<int>& rows) {
 constexpr int kListBlocks = 148 * 4;
 
 // Reduce `n` partial cells to ctx->cells[slot].
-void reduce_to(tm_ctx* ctx, int n, int slot) {
-    if (n <= 0) {
-        tmk::CellH none{0.0, -1, -1, 2};
-        CK(cudaMemcpyAsync(ctx->cells.p + slot, &none, sizeof none, cudaMemcpyHostToDevice, ctx->s));
-        CK(cudaStreamSynchronize(ctx->s));
-        return;
-    }
-    CK(tmk::reduce_cells(ctx->partials.p, n, ctx->cells.p + slot, ctx->s));
+void reduce_to(tm_ctx* ctx, int n, int slot, const tmk::ReduceOp* op = nullptr) {
+    // n = 0 writes the empty cell (the kernel's loop does not run)
+    CK(tmk::reduce_cells(ctx->partials.p, std::max(n, 0), ctx->cells.p + slot, ctx->s, op));
     ctx->add(1);
 }
 
 // Evaluate a device location list (count on device) -> cells[slot].
 void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const int2* locs,
                const unsigned long long* count, int max_count, double* out_rho,
-               uint8_t* out_deg, int slot) {
+               uint8_t* out_deg, int slot, const tmk::ReduceOp* op = nullptr) {
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     ctx->partials.ensure(kListBlocks);
     Phase ph(ctx, slot == 1 ? "seed_eval" : (slot == 2 ? "survivor_eval" : "list_eval"));
@@ -732,12 +726,12 @@ void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const in
         CK(tmk::corr_list_f64(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
                               kListBlocks, ctx->s));
     ctx->add(1);
-    reduce_to(ctx, kListBlocks, slot);
+    reduce_to(ctx, kListBlocks, slot, op);
 }
 
 // ---- scan 1: every group centre (matcher.cpp:23-37) -> rho_c, deg_c, cells[0] --------
 void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
-                 const tmk::GridDesc& g) {
+                 const tmk::GridDesc& g, const tmk::ReduceOp* op = nullptr) {
     const size_t G = size_t(g.tr) * g.tc;
     ctx->rho_c.ensure(G);
     ctx->deg_c.ensure(G);
@@ -747,7 +741,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     if (tc_path(ctx, img, T) && g.h <= tmk::kTcMaxClasses) {
         const int nstrip = g.ti_hi - g.ti_lo;
         if (nstrip <= 0) {
-            reduce_to(ctx, 0, 0);
+            reduce_to(ctx, 0, 0, op);
             return;
         }
         std::vector<int> rows(nstrip), yi(nstrip);
@@ -781,13 +775,13 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                                     task.c_last));
             ctx->add(1);
         }
-        reduce_to(ctx, n1 + n2, 0);
+        reduce_to(ctx, n1 + n2, 0, op);
         return;
     }
     if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
         const int nstrip = g.ti_hi - g.ti_lo;
         if (nstrip <= 0) {
-            reduce_to(ctx, 0, 0);
+            reduce_to(ctx, 0, 0, op);
             return;
         }
         std::vector<int> rows(nstrip);
@@ -863,7 +857,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                                    ctx->rho_c.p + off, ctx->deg_c.p + off, ctx->s));
             ctx->add(2);
         }
-        reduce_to(ctx, n1 + n2, 0);
+        reduce_to(ctx, n1 + n2, 0, op);
         return;
     }
     // general path: explicit centre list in grid order
@@ -875,7 +869,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             locs[size_t(ti - g.ti_lo) * g.tc + tj] =
                 make_int2(centre_row_h(g, ti), centre_col_h(g, tj));
     if (GS == 0) {
-        reduce_to(ctx, 0, 0);
+        reduce_to(ctx, 0, 0, op);
         return;
     }
     ctx->seed_locs.ensure(GS);
@@ -884,7 +878,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     CK(cudaMemcpyAsync(ctx->counters.p + 4, &cnt, 8, cudaMemcpyHostToDevice, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
     eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(GS), ctx->rho_c.p + off,
-              ctx->deg_c.p + off, 0);
+              ctx->deg_c.p + off, 0, op);
 }
 
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
@@ -893,7 +887,7 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
                      double thr, double* map, unsigned long long* nr, int* stop = nullptr,
                      const double* egs_prev = nullptr, double egs_xi = 0.0) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
-    CK(cudaMemsetAsync(nr, 0, 8, ctx->s));
+    if (!egs_prev) CK(cudaMemsetAsync(nr, 0, 8, ctx->s));  // EGS batches: egs_init zeroes it
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
     if (img->integer) {
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
@@ -997,11 +991,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     // is going to ignore (after the first rejection) exit at entry instead of running.
     double* dprev = reinterpret_cast<double*>(ctx->counters.p + 20);
     int* dstop = reinterpret_cast<int*>(ctx->counters.p + 21);
-    {
-        const double inf = std::numeric_limits<double>::infinity();
-        CK(cudaMemsetAsync(dstop, 0, sizeof(int), ctx->s));
-        ctx->pin_egs.upload(dprev, &inf, sizeof inf, ctx->s);
-    }
+    bool first_batch = true;
     while (!done) {
         struct Cand {
             int h, w;
@@ -1013,6 +1003,13 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             if ((hh >= er && ww >= ec) || (hh >= cap && ww >= cap)) break;
             hh = std::min(hh + 2, cap);
             ww = std::min(ww + 2, cap);
+        }
+        if (first_batch) {  // stop = 0, prev = +inf, nr[0..3] = 0
+            CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s));
+            ctx->add(1);
+            first_batch = false;
+        } else {
+            CK(cudaMemsetAsync(ctx->counters.p + 8, 0, 32, ctx->s));
         }
         for (int k = 0; k < nc; ++k) {
             const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
@@ -1319,7 +1316,14 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
                       nullptr, ctx->partials.p + np, kListBlocks, s, 1));
     ctx->add(2);
-    reduce_to(ctx, np + kListBlocks, 2);
+    ctx->res_dev.ensure(1);
+    tmk::ReduceOp op_pack{};  // the final reduction packs the host-readable result
+    op_pack.kind = 3;
+    op_pack.cells = ctx->cells.p;
+    op_pack.tally = ctx->tally.p;
+    op_pack.thr = ctx->thr.p;
+    op_pack.packed = ctx->res_dev.p;
+    reduce_to(ctx, np + kListBlocks, 2, &op_pack);
 }
 
 tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
@@ -1340,11 +1344,18 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
 
     // ---- scan 1 + threshold bootstrap (matcher.cpp:116-125) ---------------------------
     HT("search_begin");
-    centre_scan(ctx, img, ws, T, g);
+    // the centre reduction also bootstraps the threshold (matcher.cpp:121-125) and zeroes
+    // the seeding counters and the scan-2 tally
+    tmk::ReduceOp op_init{};
+    op_init.kind = 1;
+    op_init.has_init = P.has_init_threshold;
+    op_init.init = P.init_threshold;
+    op_init.thr = ctx->thr.p;
+    op_init.zero64 = ctx->counters.p + 4;
+    op_init.nzero64 = 2;
+    op_init.zero_tally = ctx->tally.p;
+    centre_scan(ctx, img, ws, T, g, &op_init);
     HT("centre_scan");
-    CK(tmk::threshold_init(ctx->cells.p + 0, P.has_init_threshold, P.init_threshold,
-                           ctx->thr.p, s));
-    ctx->add(1);
 
     const uint8_t* seeded = nullptr;
     if (policy == TM_POLICY_SEEDED) {
@@ -1352,15 +1363,15 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
         ctx->seed_locs.ensure(max_locs);
         ctx->seeded.ensure(G);
-        CK(cudaMemsetAsync(ctx->counters.p + 4, 0, 16, s));
         CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, P.seed_margin,
                              ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
                              ctx->counters.p + 5, max_groups, s));
         ctx->add(1);
+        tmk::ReduceOp op_raise{};  // the seed reduction raises the threshold
+        op_raise.kind = 2;
+        op_raise.thr = ctx->thr.p;
         eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs), nullptr,
-                  nullptr, 1);
-        CK(tmk::threshold_raise(ctx->cells.p + 1, ctx->thr.p, s));
-        ctx->add(1);
+                  nullptr, 1, &op_raise);
         seeded = ctx->seeded.p;
         HT("seeds");
     }
@@ -1369,7 +1380,6 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     ctx->visits.ensure(E);
     uint8_t* visits = ctx->visits.p;
     ctx->locs.ensure(E);
-    CK(cudaMemsetAsync(ctx->tally.p, 0, sizeof(tmk::Tally), s));
     {
         Phase ph(ctx, "sec_compact");
         CK(tmk::sec_compact(g, in.map, ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
@@ -1440,9 +1450,13 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     }
     HT("survivors");
     tm_ctx::HostRes* hr = ctx->hres;
-    CK(cudaMemcpyAsync(hr->cells, ctx->cells.p, sizeof hr->cells, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hr->tally, ctx->tally.p, sizeof hr->tally, cudaMemcpyDeviceToHost, s));
-    CK(cudaMemcpyAsync(&hr->thr, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+    if (device_dispatch) {  // packed by the final reduction: one copy
+        CK(cudaMemcpyAsync(hr, ctx->res_dev.p, sizeof *hr, cudaMemcpyDeviceToHost, s));
+    } else {
+        CK(cudaMemcpyAsync(hr->cells, ctx->cells.p, sizeof hr->cells, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hr->tally, ctx->tally.p, sizeof hr->tally, cudaMemcpyDeviceToHost, s));
+        CK(cudaMemcpyAsync(&hr->thr, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
+    }
     if (visits_host) CK(cudaMemcpyAsync(visits_host, visits, E, cudaMemcpyDeviceToHost, s));
     HT("readback_enq");
     CK(cudaStreamSynchronize(s));

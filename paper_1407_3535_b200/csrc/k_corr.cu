@@ -377,7 +377,7 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---- reductions -----------------------------------------------------------------------
-__global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH* out) {
+__global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH* out, ReduceOp op) {
     __shared__ Cell scratch[32];
     Cell best = no_cell();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -386,7 +386,31 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
         if (better(c, best)) best = c;
     }
     best = block_best(best, scratch);
-    if (threadIdx.x == 0) out[0] = CellH{best.rho, best.row, best.col, best.flags};
+    if (threadIdx.x == 0) {
+        const CellH b{best.rho, best.row, best.col, best.flags};
+        out[0] = b;
+        if (op.kind == 1) {  // k_threshold_init + the zeroing the search needs next
+            double t = -INFINITY;
+            if ((b.flags & 1) && !(b.flags & 2)) t = b.rho;
+            if (op.has_init) t = dmax(t, dclamp(op.init, -1.0, 1.0));
+            *op.thr = t;
+            for (int i = 0; i < op.nzero64; ++i) op.zero64[i] = 0ull;
+            if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull};
+        } else if (op.kind == 2) {  // k_threshold_raise
+            if ((b.flags & 1) && !(b.flags & 2) && b.rho > *op.thr) *op.thr = b.rho;
+        } else if (op.kind == 3) {  // result block for one device->host copy
+            for (int i = 0; i < 3; ++i) op.packed->cells[i] = op.cells[i];
+            op.packed->cells[2] = b;  // this reduction's own slot (cells[2])
+            op.packed->tally = *op.tally;
+            op.packed->thr = *op.thr;
+        }
+    }
+}
+
+__global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4) {
+    *stop = 0;
+    *prev = INFINITY;
+    for (int i = 0; i < 4; ++i) nr4[i] = 0ull;
 }
 
 // ---- scan 2: SEC test + survivor compaction (matcher.cpp:48-78, bounds.cpp:41-46) -------
@@ -681,8 +705,14 @@ cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc,
     return cudaGetLastError();
 }
 
-cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s) {
-    k_reduce_cells<<<1, 1024, 0, s>>>(partials, n, out);
+cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
+                         const ReduceOp* op) {
+    k_reduce_cells<<<1, 1024, 0, s>>>(partials, n, out, op ? *op : ReduceOp{});
+    return cudaGetLastError();
+}
+
+cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s) {
+    k_egs_init<<<1, 1, 0, s>>>(stop, prev, nr4);
     return cudaGetLastError();
 }
 

@@ -53,7 +53,11 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ img, int p, int q, float
 // Sum of squares of all pixels (q_total for 8-bit images, exact in u64): 16-byte loads,
 // block reduction, one atomic per block.
 __global__ void __launch_bounds__(256) k_sum_sq_u8(const uint8_t* __restrict__ img, size_t n,
-                                                   unsigned long long* out) {
+                                                   unsigned long long* acc_ctr, int rows,
+                                                   int cols, double* noise_out) {
+    // acc_ctr[0]: running sum, acc_ctr[1]: finished-block counter; both zero on entry and
+    // reset by the last block, which also writes prefix_noise (stats.cpp:79-81).
+    unsigned long long* out = acc_ctr;
     __shared__ unsigned long long part[8];
     unsigned long long acc = 0;
     const size_t nv = n / 16;
@@ -84,6 +88,14 @@ __global__ void __launch_bounds__(256) k_sum_sq_u8(const uint8_t* __restrict__ i
         unsigned long long t = 0;
         for (int w = 0; w < int(blockDim.x >> 5); ++w) t += part[w];
         atomicAdd(out, t);
+        __threadfence();
+        const unsigned long long ticket = atomicAdd(acc_ctr + 1, 1ull);
+        if (ticket == gridDim.x - 1) {  // last block: every partial is in
+            const unsigned long long q_total = atomicAdd(out, 0ull);
+            *noise_out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), double(q_total));
+            acc_ctr[0] = 0ull;
+            acc_ctr[1] = 0ull;
+        }
     }
 }
 
@@ -303,10 +315,8 @@ cudaError_t u8_to_f32_pitched(const uint8_t* img, int p, int q, float* out, int 
 cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long* q_total,
                             double* out, cudaStream_t s) {
     const size_t n = size_t(p) * q;
-    cudaMemsetAsync(q_total, 0, sizeof(*q_total), s);
     const int blocks = int(std::min<size_t>(148 * 4, (n / 16 + 255) / 256 + 1));
-    k_sum_sq_u8<<<blocks, 256, 0, s>>>(img, n, q_total);
-    k_prefix_noise_u64<<<1, 1, 0, s>>>(q_total, p, q, out);
+    k_sum_sq_u8<<<blocks, 256, 0, s>>>(img, n, q_total, p, q, out);  // q_total: 2 u64, zeroed
     return cudaGetLastError();
 }
 cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,

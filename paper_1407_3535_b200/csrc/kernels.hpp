@@ -43,6 +43,28 @@ struct Tally {  // accumulated on device by the search kernels
     unsigned long long pad;
 };
 
+// Host-readable result block (one device->host copy per search / EGS batch).
+struct ResultBlock {
+    unsigned long long nr[4];  // EGS retained counts of a candidate batch
+    CellH cells[3];            // best centre, best seeded member, best survivor
+    Tally tally;
+    double thr;                // threshold after the search
+};
+
+// Work fused into an argmax reduction (saves launches on the search's critical path).
+struct ReduceOp {
+    int kind = 0;  // 0 none, 1 threshold init (matcher.cpp:121-125), 2 raise, 3 pack
+    int has_init = 0;
+    double init = 0.0;
+    double* thr = nullptr;
+    unsigned long long* zero64 = nullptr;  // kind 1: zeroed counters
+    int nzero64 = 0;
+    Tally* zero_tally = nullptr;  // kind 1: zeroed tally
+    const CellH* cells = nullptr;  // kind 3: cells[0..2] to pack
+    const Tally* tally = nullptr;
+    ResultBlock* packed = nullptr;
+};
+
 // ---- image preparation ---------------------------------------------------------------
 cudaError_t check_u8_domain(const double* img, size_t n, int* bad, cudaStream_t s);
 cudaError_t f64_to_u8(const double* img, size_t n, uint8_t* out, cudaStream_t s);
@@ -184,7 +206,10 @@ cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
 // Reduce partial cells -> out[0] (better_candidate order).
-cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s);
+cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
+                         const ReduceOp* op = nullptr);
+// EGS batch start: stop = 0, prev cost = +inf, nr[0..3] = 0 (one launch).
+cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s);
 
 // ---- scan 2 (matcher.cpp:48-78) ---------------------------------------------------------
 // threshold read from *thr (device).  Survivors appended to locs (int2) with counters in
