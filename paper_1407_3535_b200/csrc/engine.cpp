@@ -613,15 +613,30 @@ std::vector<tmk::TcBand> tc_bands(const std::vector<int>& rows, const std::vecto
 }
 
 // Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
-TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const std::vector<int>& rows,
-                   const std::vector<int>& yi, int sr) {
-    std::vector<long long> key = {T.m, T.n, sr, ws.ec, (long long)rows.size()};
-    unsigned long long h = 1469598103934665603ull;
-    for (size_t i = 0; i < rows.size(); ++i) h = (h ^ (unsigned long long)(rows[i] * 131 + yi[i])) * 1099511628211ull;
-    key.push_back((long long)h);
+// Output rows of a tensor-core launch, described without materialising them (the host
+// only builds the vectors when the geometry is not cached yet).
+struct RowSet {
+    int kind = 0;  // 0: extent rows [lo, hi); 1: centre rows of group rows [lo, hi) of g
+    int lo = 0, hi = 0;
+    tmk::GridDesc g{};
+    void materialise(std::vector<int>& rows, std::vector<int>& yi) const {
+        rows.clear();
+        yi.clear();
+        for (int i = lo; i < hi; ++i) {
+            rows.push_back(kind == 0 ? i : centre_row_h(g, i));
+            yi.push_back(i);
+        }
+    }
+};
+
+TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, int sr) {
+    const std::vector<long long> key = {T.m, T.n, sr, ws.ec, rs.kind, rs.lo, rs.hi,
+                                        rs.kind ? rs.g.er : 0, rs.kind ? rs.g.h : 0};
     auto it = ctx->tc_geo.find(key);
     if (it != ctx->tc_geo.end()) return *it->second;
     if (ctx->tc_geo.size() > 64) ctx->tc_geo.clear();
+    std::vector<int> rows, yi;
+    rs.materialise(rows, yi);
     auto geo = std::make_unique<TcGeo>();
     geo->plan = tmk::tc_plan(T.m, T.n, sr, kTcSmemBudget);
     if (geo->plan.nch == 0) invalid("tensor-core plan unavailable");
@@ -644,14 +659,14 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const std::vector<i
                        ctx->s));
     CK(cudaStreamSynchronize(ctx->s));  // host vectors go out of scope (pageable copies)
     TcGeo& ref = *geo;
-    ctx->tc_geo.emplace(std::move(key), std::move(geo));
+    ctx->tc_geo.emplace(key, std::move(geo));
     return ref;
 }
 
 // Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
-int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const std::vector<int>& rows,
-           const std::vector<int>& yi, int sr, tmk::TcTask task, const int** rows_dev = nullptr) {
-    TcGeo& geo = tc_geometry(ctx, ws, T, rows, yi, sr);
+int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet& rs, int sr,
+           tmk::TcTask task, const int** rows_dev = nullptr) {
+    TcGeo& geo = tc_geometry(ctx, ws, T, rs, sr);
     const tmk::TcPlan& plan = geo.plan;
     ctx->tc_b.ensure(plan.total_bytes);
     CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s));
@@ -744,11 +759,11 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             reduce_to(ctx, 0, 0, op);
             return;
         }
-        std::vector<int> rows(nstrip), yi(nstrip);
-        for (int ti = g.ti_lo; ti < g.ti_hi; ++ti) {
-            rows[ti - g.ti_lo] = centre_row_h(g, ti);
-            yi[ti - g.ti_lo] = ti;
-        }
+        RowSet rs;
+        rs.kind = 1;
+        rs.lo = g.ti_lo;
+        rs.hi = g.ti_hi;
+        rs.g = g;
         const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
         const int nc_reg = clipped ? g.tc - 1 : g.tc;
         int n1 = 0, n2 = 0;
@@ -768,7 +783,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
             task.out_rho = ctx->dotbuf.p;
             const int* rows_dev = nullptr;
-            tc_run(ctx, img, ws, T, rows, yi, g.h, task, &rows_dev);
+            tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
@@ -1225,8 +1240,9 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const bool dense = survivors * 16 > E && fp32_path(img, T);
     if (dense && tc_path(ctx, img, T)) {
         const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
-        std::vector<int> rows(std::max(0, rhi - rlo));
-        for (int r = rlo; r < rhi; ++r) rows[r - rlo] = r;
+        RowSet rs;
+        rs.lo = rlo;
+        rs.hi = std::max(rlo, rhi);
         tmk::TcTask task{};
         task.mode = 2;
         task.c_lim = g.ec;
@@ -1235,9 +1251,9 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         task.out_rho = rho_loc;
         ctx->partials.ensure(148 + 1);
         int np = 0;
-        if (!rows.empty()) {
+        if (rs.hi > rs.lo) {
             Phase ph(ctx, "survivor_dense");
-            np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+            np = tc_run(ctx, img, ws, T, rs, 1, task);
         }
         reduce_to(ctx, np, 2);
     } else if (dense) {
@@ -1300,8 +1316,9 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
     int np = 0;
     if (rhi > rlo) {
-        std::vector<int> rows(rhi - rlo);
-        for (int r = rlo; r < rhi; ++r) rows[r - rlo] = r;
+        RowSet rs;
+        rs.lo = rlo;
+        rs.hi = rhi;
         tmk::TcTask task{};
         task.mode = 2;
         task.c_lim = g.ec;
@@ -1310,7 +1327,7 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         task.out_rho = rho_loc;
         task.gate = dense_flag;
         Phase ph(ctx, "survivor_eval");
-        np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+        np = tc_run(ctx, img, ws, T, rs, 1, task);
     }
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
@@ -1533,15 +1550,16 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     Phase ph(ctx, "brute_dense");
     if (tc_path(ctx, img, T)) {
-        std::vector<int> rows(er);
-        for (int r = 0; r < er; ++r) rows[r] = r;
+        RowSet rs;
+        rs.lo = 0;
+        rs.hi = er;
         tmk::TcTask task{};
         task.mode = 0;
         task.c_lim = ec;
         task.c_last = -1;
         task.out_rho = surface;
         ctx->partials.ensure(148 + 1);
-        const int np = tc_run(ctx, img, ws, T, rows, rows, 1, task);
+        const int np = tc_run(ctx, img, ws, T, rs, 1, task);
         reduce_to(ctx, np, 2);
     } else if (fp32_path(img, T)) {
         std::vector<int> rows(er);
