@@ -793,7 +793,7 @@ struct AcfGeom {
     size_t smem;
 };
 
-AcfGeom acf_geom(int m, int n, GridDesc gd) {
+AcfGeom acf_geom(int m, int n, GridDesc gd, int resident = 0) {
     AcfGeom a{};
     int ny = std::max(128, 3 * n);
     ny = std::max(ny, n - 1 + 2 * gd.w);
@@ -807,8 +807,15 @@ AcfGeom acf_geom(int m, int n, GridDesc gd) {
     a.ntiles = (gd.ec + a.tw - 1) / a.tw;
     const int rows = gd.ti_hi - gd.ti_lo;
     const int seg_min = std::max(1, (m + gd.h - 1) / gd.h);
-    const int resident = std::max(1, 2048 / a.ny);
-    int nseg = std::max(1, (148 * resident * 2) / std::max(1, gd.w * a.ntiles));
+    if (resident <= 0) resident = std::max(1, 2048 / a.ny);
+    // As few waves of resident CTAs as keep segments short: each segment pays its m-row
+    // warm-up once, and with one wave the EGS early rejection reaches every CTA at the same
+    // fraction of its work; long segments (large images) get up to 4 waves for balance.
+    const int slots = 148 * resident;
+    const int per_wave = std::max(1, slots / std::max(1, gd.w * a.ntiles));
+    const int seg_1 = (rows + per_wave - 1) / per_wave;
+    const int waves = std::min(4, std::max(1, (seg_1 + 4 * seg_min - 1) / (4 * seg_min)));
+    int nseg = std::max(1, waves * per_wave);
     nseg = std::min(nseg, std::max(1, (rows + seg_min - 1) / seg_min));
     a.seg = std::max(1, (rows + nseg - 1) / nseg);
     a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
@@ -820,13 +827,17 @@ template <int H>
 cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc gd, DevStats st,
                        double thr, double* map, unsigned long long* n_r, int* stop,
                        const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
-    const AcfGeom a = acf_geom(m, n, gd);
-    if (a.ny == 0) return cudaErrorInvalidValue;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_acf<H>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
         attr = true;
     }
+    const AcfGeom a0 = acf_geom(m, n, gd);
+    if (a0.ny == 0) return cudaErrorInvalidValue;
+    int occ = 0;  // resident CTAs per SM for this block size / shared memory
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acf<H>, a0.ny, a0.smem) != cudaSuccess)
+        occ = 0;
+    const AcfGeom a = acf_geom(m, n, gd, occ);
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
         k_acf<H><<<grid, a.ny, a.smem, s>>>(img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
