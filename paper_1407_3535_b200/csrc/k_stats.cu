@@ -425,7 +425,7 @@ cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, cons
     const int ec = q - n + 1, er = p - m + 1;
     // fused path: u32 sums exact while m*n*255^2 < 2^32; column tile + halo <= 512 threads
     if (double(m) * double(n) * 65025.0 < 4294967296.0 && n <= 384) {
-        int ny = std::max(128, ((2 * n + 31) / 32) * 32);
+        int ny = std::max(256, ((4 * n + 31) / 32) * 32);  // halo n-1 of ny columns
         ny = std::min(ny, 512);
         const int tw = ny - n + 1;
         const int ntiles = (ec + tw - 1) / tw;
