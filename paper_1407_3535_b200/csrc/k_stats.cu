@@ -431,7 +431,7 @@ cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, cons
         const int ntiles = (ec + tw - 1) / tw;
         // segments: ~4 resident waves of CTAs, each walking at least 2m rows of output
         int nseg = std::max(1, (148 * 16) / ntiles);
-        int seg = std::max(std::min(m, 64), (er + nseg - 1) / nseg);
+        int seg = std::max(std::min(m, 32), (er + nseg - 1) / nseg);
         nseg = (er + seg - 1) / seg;
         dim3 grid(ntiles, nseg);
         k_wstats_u8<<<grid, ny, 0, s>>>(img, p, q, m, n, tw, seg, prefix_noise, st);
