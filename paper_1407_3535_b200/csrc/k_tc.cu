@@ -129,7 +129,10 @@ template <int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask task, CellH* partials) {
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcPlan& P = job.plan;
-    const int kTcStages = P.stages;
+    // a ring stage holds kRows consecutive scheduled image rows (kRows slots of a_slot bytes):
+    // one expect_tx, one full-wait and one commit per stage instead of per row
+    constexpr int kRows = 4;
+    const int kTcStages = P.stages / kRows;
     uint64_t* bars = reinterpret_cast<uint64_t*>(sm);
     int4* ssched = reinterpret_cast<int4*>(sm + kTcBarBytes);  // staged row schedule
     uint8_t* sB = sm + P.header;                // B chunk (P.b_smem bytes)
@@ -202,25 +205,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     }
                     const int4* sc = sched + task.sched_off[ch];
                     const int ns = task.sched_len[ch];
-                    int s = it % kTcStages;
-                    uint32_t par = ((it / kTcStages) & 1) ^ 1;
-                    for (int e = 0; e < ns; ++e) {
-                        const int4 row = sc[e];  // {dx, k_lo, k_hi, B entry}
-                        if (row.y >= bd.cnt) break;      // rows are in k_lo order
+                    for (int e0 = 0; e0 < ns; e0 += kRows) {
+                        int dx[kRows];
+                        int nr = 0;  // rows are in k_lo order: the valid ones are a prefix
+#pragma unroll
+                        for (int j = 0; j < kRows; ++j) {
+                            const int4 row = e0 + j < ns ? sc[e0 + j] : make_int4(0, 1 << 30, 0, 0);
+                            dx[j] = row.x;
+                            if (row.y < bd.cnt && nr == j) nr = j + 1;
+                        }
+                        if (nr == 0) break;
+                        const int s = int(it % kTcStages);
+                        const uint32_t par = ((it / kTcStages) & 1) ^ 1;
                         mbar_wait_t(empty + s, par, pe, 64);
                         if (task.dbg_flags & 1) {  // timing experiment: no copy
                             mbar_arrive(full + s);
                         } else {
-                            mbar_expect_tx(full + s, uint32_t(P.a_bytes));
-                            bulk_g2s(sA + size_t(s) * P.a_slot,
-                                     job.imgp + size_t(bd.r0 + row.x) * job.pitch + c0,
-                                     uint32_t(P.a_bytes), full + s);
+                            mbar_expect_tx(full + s, uint32_t(nr * P.a_bytes));
+                            for (int j = 0; j < nr; ++j)
+                                bulk_g2s(sA + (size_t(s) * kRows + j) * P.a_slot,
+                                         job.imgp + size_t(bd.r0 + dx[j]) * job.pitch + c0,
+                                         uint32_t(P.a_bytes), full + s);
                         }
                         ++it;
-                        if (++s == kTcStages) {
-                            s = 0;
-                            par ^= 1;
-                        }
+                        if (nr < kRows) break;
                     }
                 }
             }
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
         // registers; one elected lane issues.  Descriptors are built once and advanced by
         // adds (16-byte units): A +2 per K-step (32 B), B +16 per K-step (two 128 B core
         // matrices), N field of idesc at bit 17 in units of 8.
-        long long w_full = 0, w_dempty = 0, w_bfull = 0;
+        long long w_full = 0, w_dempty = 0, w_bfull = 0, w_issue = 0;
         const long long t_start = clock64();
         long long* pf = task.dbg && lane == 0 ? &w_full : nullptr;
         long long* pd = task.dbg && lane == 0 ? &w_dempty : nullptr;
@@ -264,40 +272,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                 }
                 const int4* sc = sched + task.sched_off[ch];
                 const int ns = task.sched_len[ch];
-                int s = it % kTcStages;
-                uint32_t par = (it / kTcStages) & 1;
-                // rows in groups of up to 4: independent barrier waits and schedule reads
-                // overlap, then all MMAs of the group, then one commit per slot
-                constexpr int kGroup = 4;
-                for (int e0 = 0; e0 < ns; e0 += kGroup) {
-                    int4 rows[kGroup];
+                // one ring stage = up to kRows scheduled rows: one wait, their MMAs, one commit
+                for (int e0 = 0; e0 < ns; e0 += kRows) {
+                    int4 rows[kRows];
                     int nr = 0;
 #pragma unroll
-                    for (int j = 0; j < kGroup; ++j) {
+                    for (int j = 0; j < kRows; ++j) {
                         rows[j] = e0 + j < ns ? sc[e0 + j] : make_int4(0, 1 << 30, 0, 0);
-                        if (rows[j].y < bd.cnt) nr = j + 1;
+                        if (rows[j].y < bd.cnt && nr == j) nr = j + 1;
                     }
                     if (nr == 0) break;
-                    int ss[kGroup];
-                    {
-                        int s2 = s;
-                        uint32_t p2 = par;
-#pragma unroll
-                        for (int j = 0; j < kGroup; ++j) {
-                            ss[j] = s2;
-                            if (j < nr) mbar_wait_t(full + s2, p2, pf);
-                            if (++s2 == kTcStages) {
-                                s2 = 0;
-                                p2 ^= 1;
-                            }
-                        }
-                    }
+                    const int s = int(it % kTcStages);
+                    const uint32_t par = (it / kTcStages) & 1;
+                    if (!(task.dbg_flags & 8)) mbar_wait_t(full + s, par, pf);
                     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+                    const long long t_iss = pf ? clock64() : 0;
 #pragma unroll
-                    for (int j = 0; j < kGroup; ++j) {
+                    for (int j = 0; j < kRows; ++j) {
                         if (j >= nr) break;
                         const int k_hi = min(rows[j].z, bd.cnt - 1);
-                        uint64_t ad = a_desc0 + uint64_t(uint32_t(ss[j]) * slot16);
+                        uint64_t ad = a_desc0 + uint64_t(uint32_t(s * kRows + j) * slot16);
                         uint64_t bdsc = b_desc0 + uint64_t(uint32_t(rows[j].w) * entry16);
                         const uint32_t idesc = idesc0 | (uint32_t(k_hi - rows[j].y + 1) << 18);
                         const uint32_t d = dbase + uint32_t(16 * rows[j].y);
@@ -311,18 +305,13 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                             bdsc += 16;
                         }
                     }
-#pragma unroll
-                    for (int j = 0; j < kGroup; ++j) {
-                        if (j >= nr) break;
-                        asm volatile(
-                            "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
-                            " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
-                                smem_u32(empty + ss[j])));
-                    }
-                    it += nr;
-                    s = int(it % kTcStages);
-                    par = (it / kTcStages) & 1;
-                    if (nr < kGroup) break;
+                    if (pf) w_issue += clock64() - t_iss;
+                    asm volatile(
+                        "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
+                        " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
+                            smem_u32(empty + s)));
+                    ++it;
+                    if (nr < kRows) break;
                 }
                 if (P.nch > 1)
                     asm volatile(
@@ -341,6 +330,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
             dd[5] = w_full;
             dd[6] = w_dempty;
             dd[7] = w_bfull;
+            dd[3] = w_issue;  // (overrides the producer's row count slot)
         }
         __syncwarp();
     } else {

@@ -268,12 +268,16 @@ static void run_rowbench(int N, int fence, int commit) {
 
 // Replays the centre-scan band schedule (sr, m, R rows, Kx=96): per image row dx, one MMA
 // chain with N = 16*(k_hi-k_lo+1) into D columns 16*k_lo.., B window at entry(i_top).
-__global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long long* cycles, int variant) {
+__global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long long* cycles, int variant, int variant_spin_sleep) {
     extern __shared__ __align__(1024) uint8_t sm[];
     __shared__ uint64_t bars[64];
     __shared__ uint32_t tmem_base;
-    uint8_t* sA = sm;
-    uint8_t* sB = sm + 100 * 1024;
+    // variant >= 10: the production kernel's layout (B at 18 KB, 50-slot A ring after B)
+    uint8_t* sA = variant >= 10 ? sm + 18 * 1024 + 96 * 1024 : sm;
+    uint8_t* sB = variant >= 10 ? sm + 18 * 1024 : sm + 100 * 1024;
+    const int nslot = variant >= 10 ? 40 : 40;
+    const int slot_b = variant >= 10 ? 2176 : 2176;
+    variant = variant % 10;
     const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < 200 * 1024; i += blockDim.x) sm[i] = uint8_t(i * 7);
     asm volatile("fence.proxy.async.shared::cta;");
@@ -291,6 +295,7 @@ __global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long l
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = tmem_base;
     long long nmma = 0;
+    __shared__ int stop_spin;
     __shared__ int4 tab[256];
     int ntab = 0;
     if (tid == 0) {
@@ -304,9 +309,20 @@ __global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long l
             tab[ntab++] = make_int4(dx, k_lo, k_hi, entry);
         }
         tab[255].x = ntab;
+        stop_spin = 0;
     }
     __syncthreads();
     ntab = tab[255].x;
+    if (warp > 0) {  // waiters like the production kernel's producer/epilogue warps
+        uint32_t ok = 0;
+        while (!*(volatile int*)&stop_spin) {
+            asm volatile(
+                "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+                " selp.u32 %0, 1, 0, p;\n}\n"
+                : "=r"(ok) : "r"(smem_u32(&bars[62])), "r"(0u) : "memory");
+            if (variant_spin_sleep > 0) __nanosleep(variant_spin_sleep);
+        }
+    }
     if (warp == 0) {
         const uint64_t a0 = make_desc(smem_u32(sA), 16, 128);
         const uint64_t b0 = make_desc(smem_u32(sB), 128, 768);
@@ -316,7 +332,7 @@ __global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long l
             for (int e = 0; e < ntab; ++e) {
                 const int4 row = tab[e];
                 const int k_lo = row.y, k_hi = row.z, entry = row.w;
-                uint64_t ad = a0 + uint64_t(slot * 136);
+                uint64_t ad = a0 + uint64_t(slot * (slot_b / 16));
                 uint64_t bd = b0 + uint64_t(entry * 96);
                 const int nfix = variant == 1 || variant == 3 ? R : (k_hi - k_lo + 1);
                 const int kfix = variant == 1 || variant == 2 ? 0 : k_lo;
@@ -336,11 +352,12 @@ __global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long l
                         "{\n .reg .pred e;\n elect.sync _|e, 0xffffffff;\n"
                         " @e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}\n" ::"r"(
                             smem_u32(&bars[slot % 64])));
-                slot = (slot + 1) % 40;
+                slot = (slot + 1) % nslot;
             }
         if (tid == 0) {
             cycles[blockIdx.x * 2] = clock64() - t0;
             cycles[blockIdx.x * 2 + 1] = nmma;
+            *(volatile int*)&stop_spin = 1;
         }
     }
     __syncthreads();
@@ -351,18 +368,19 @@ __global__ void k_schedbench(int sr, int m, int R, int bands, int commit, long l
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512));
 }
 
-static void run_sched(int sr, int m, int R, int grid, int commit, int variant) {
+static void run_sched(int sr, int m, int R, int grid, int commit, int variant, int threads = 128,
+                      int sleep_ns = 0) {
     long long* d;
     cudaMalloc(&d, 2 * 8 * 148);
     cudaFuncSetAttribute(k_schedbench, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     const int bands = 5;
-    k_schedbench<<<grid, 128, 200 * 1024>>>(sr, m, R, bands, commit, d, variant);
+    k_schedbench<<<grid, threads, 200 * 1024>>>(sr, m, R, bands, commit, d, variant, sleep_ns);
     cudaError_t e = cudaDeviceSynchronize();
     long long c[2] = {0, 0};
     cudaMemcpy(c, d, 16, cudaMemcpyDeviceToHost);
     const int rows = bands * (sr * (R - 1) + m);
-    printf("sched sr=%d m=%d R=%2d variant=%d commit=%d: %.1f cycles/row, %.1f cycles/MMA (%s)\n", sr, m,
-           R, variant, commit, double(c[0]) / rows, double(c[0]) / c[1], cudaGetErrorString(e));
+    printf("sched sr=%d m=%d R=%2d threads=%d sleep=%d: %.1f cycles/row, %.1f cycles/MMA (%s)\n", sr, m,
+           R, threads, sleep_ns, double(c[0]) / rows, double(c[0]) / c[1], cudaGetErrorString(e));
     cudaFree(d);
 }
 
@@ -438,7 +456,11 @@ int main() {
     printf("fails=%d\n", fails);
     // variant 0: as scheduled; 1: fixed N=16R, D offset 0; 2: varying N, D offset 0;
     // 3: fixed N=16R, D offset 16*k_lo (N range clipped at 512 columns)
-    for (int R : {4, 16})
-        for (int variant : {0, 1, 2, 3}) run_sched(3, 64, R, 1, 1, variant);
+    for (int R : {4, 16}) {
+        run_sched(3, 64, R, 148, 1, 10, 32, 0);
+        run_sched(3, 64, R, 148, 1, 10, 320, 0);
+        run_sched(3, 64, R, 148, 1, 10, 320, 64);
+        run_sched(3, 64, R, 148, 1, 10, 320, 256);
+    }
     return fails ? 1 : 0;
 }
