@@ -231,6 +231,7 @@ struct tm_ctx {
     DBuf<int> rows_list;
     DBuf<double> map_tmp, map_user;
     DBuf<double> egs_maps[4];
+    DBuf<double> sa_c;  // per-group half_gap factor sqrt(1 - rho_c^2) (scan 2)
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
     // row-strip search protocol state (tm_strip_search_*)
     struct StripState {
@@ -1399,9 +1400,10 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     ctx->locs.ensure(E);
     {
         Phase ph(ctx, "sec_compact");
-        CK(tmk::sec_compact(g, in.map, ctx->rho_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
-                            ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
-        ctx->add(1);
+        ctx->sa_c.ensure(G);
+        CK(tmk::sec_rows(g, in.map, ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
+                         ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
+        ctx->add(2);
     }
     double T0 = 0.0;
     tmk::Tally tally{};

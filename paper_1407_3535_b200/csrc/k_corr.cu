@@ -474,6 +474,88 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Scan 2 over explicit extent rows: row-level quantities (group row, centre row) once per
+// row, the centre's half_gap factor sa precomputed per group (k_sqrt_gap, same
+// operations as half_gap), so a member costs one FastDiv, its own square root and the
+// bound test.  Same decisions, counts, visit codes and survivor list as k_sec_compact.
+__global__ void __launch_bounds__(256)
+    k_sec_rows(Grid g, const double* __restrict__ map, const double* __restrict__ rho_c,
+               const double* __restrict__ sa_c, const uint8_t* __restrict__ deg_c,
+               const uint8_t* __restrict__ flat, int tflat, const double* __restrict__ thr_ptr,
+               const uint8_t* __restrict__ seeded, int2* locs, unsigned long long max_locs,
+               Tally* tally, uint8_t* visits) {
+    const double T = *thr_ptr;
+    const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+    const bool thr_ok = T >= -1.0;
+    const int lane = threadIdx.x & 31;
+    unsigned long long n_elim = 0, n_keep = 0;
+    const int r_lo = g.row_lo(), r_hi = g.row_hi();
+    const int cols = ((g.ec + 31) / 32) * 32;  // whole warps per row (ballots)
+    for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const int ti = g.tile_r(r);
+        const bool centre_row = g.center_row(ti) == r;
+        const size_t rowk = size_t(r) * g.ec;
+        const size_t gbase = size_t(ti) * g.tc;
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            bool survivor = false;
+            if (c < g.ec) {
+                const size_t k = rowk + c;
+                const int tj = g.tile_c(c);
+                if (centre_row && g.center_col(tj) == c) {
+                    if (visits) visits[k] = 0;
+                } else {
+                    const size_t gi = gbase + tj;
+                    if (seeded && seeded[gi]) {
+                        ++n_keep;
+                        if (visits) visits[k] = 2;
+                    } else {
+                        bool elim = thr_ok && !deg_c[gi] && !(tflat || flat[k]);
+                        if (elim) {
+                            const double a = dclamp(rho_c[gi], -1.0, 1.0);
+                            const double b = dclamp(map[k], -1.0, 1.0);
+                            const double sb = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b))));
+                            elim = tb >= __dadd_rn(__dmul_rn(a, b), __dmul_rn(sa_c[gi], sb));
+                        }
+                        if (elim) {
+                            ++n_elim;
+                            if (visits) visits[k] = 1;
+                        } else {
+                            ++n_keep;
+                            survivor = true;
+                            if (visits) visits[k] = 2;
+                        }
+                    }
+                }
+            }
+            const unsigned ballot = __ballot_sync(0xffffffffu, survivor);
+            if (ballot) {
+                unsigned long long basepos = 0;
+                if (lane == 0) basepos = atomicAdd(&tally->survivors, (unsigned long long)__popc(ballot));
+                basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                if (survivor) {
+                    const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
+                    if (pos < max_locs) locs[pos] = make_int2(r, c);
+                }
+            }
+        }
+    }
+    n_elim = warp_sum(n_elim);
+    n_keep = warp_sum(n_keep);
+    if (lane == 0) {
+        if (n_elim) atomicAdd(&tally->eliminated, n_elim);
+        if (n_keep) atomicAdd(&tally->retained, n_keep);
+    }
+}
+
+// y = sqrt(max(0, 1 - clamp(x)^2)): one factor of half_gap (bounds.cpp:21-23).
+__global__ void k_sqrt_gap(const double* __restrict__ x, double* __restrict__ y, size_t n) {
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const double a = dclamp(x[i], -1.0, 1.0);
+        y[i] = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(a, a))));
+    }
+}
+
 __global__ void k_threshold_init(const CellH* best, int has_init, double init, double* thr) {
     double t = -INFINITY;
     const CellH b = *best;
@@ -724,6 +806,19 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c, cons
     const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 8));
     k_sec_compact<<<blocks, 256, 0, s>>>(to_grid(g), map, rho_c, deg_c, flat, tflat, thr, seeded,
                                          locs, max_locs, tally, visits);
+    return cudaGetLastError();
+}
+
+cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
+                     const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
+                     const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
+                     uint8_t* visits, cudaStream_t s) {
+    const size_t G = size_t(g.tr) * g.tc;
+    k_sqrt_gap<<<int(std::min<size_t>((G + 255) / 256, 148 * 8)), 256, 0, s>>>(rho_c, sa_c, G);
+    const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
+    const int blocks = std::max(1, std::min(rows, 148 * 8));
+    k_sec_rows<<<blocks, 256, 0, s>>>(to_grid(g), map, rho_c, sa_c, deg_c, flat, tflat, thr, seeded,
+                                      locs, max_locs, tally, visits);
     return cudaGetLastError();
 }
 

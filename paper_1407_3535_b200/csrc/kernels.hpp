@@ -219,6 +219,11 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c,
                         const uint8_t* seeded, int2* locs, unsigned long long max_locs,
                         Tally* tally, uint8_t* visits, cudaStream_t s);
 // Threshold bootstrap: thr = max(best non-degenerate centre rho, init) (matcher.cpp:121-125)
+// Row-structured scan 2 (same results as sec_compact); sa_c: G doubles of scratch.
+cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
+                     const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
+                     const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
+                     uint8_t* visits, cudaStream_t s);
 cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, double* thr,
                            cudaStream_t s);
 // Seeded policy: members of every group whose centre rho >= thr - margin -> list.
