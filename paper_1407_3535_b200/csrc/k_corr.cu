@@ -501,20 +501,28 @@ __global__ void __launch_bounds__(256)
             if (c < g.ec) {
                 const size_t k = rowk + c;
                 const int tj = g.tile_c(c);
+                const size_t gi = gbase + tj;
+                // every load of the element issued up front (one memory latency, not a
+                // chain of dependent ones through the short-circuit tests)
+                const double mv = __ldg(map + k);
+                const uint8_t fv = __ldg(flat + k);
+                const uint8_t sd = seeded ? __ldg(seeded + gi) : uint8_t(0);
+                const uint8_t dg = __ldg(deg_c + gi);
+                const double ra = __ldg(rho_c + gi);
+                const double sa = __ldg(sa_c + gi);
                 if (centre_row && g.center_col(tj) == c) {
                     if (visits) visits[k] = 0;
                 } else {
-                    const size_t gi = gbase + tj;
-                    if (seeded && seeded[gi]) {
+                    if (sd) {
                         ++n_keep;
                         if (visits) visits[k] = 2;
                     } else {
-                        bool elim = thr_ok && !deg_c[gi] && !(tflat || flat[k]);
+                        bool elim = thr_ok && !dg && !(tflat || fv);
                         if (elim) {
-                            const double a = dclamp(rho_c[gi], -1.0, 1.0);
-                            const double b = dclamp(map[k], -1.0, 1.0);
+                            const double a = dclamp(ra, -1.0, 1.0);
+                            const double b = dclamp(mv, -1.0, 1.0);
                             const double sb = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b))));
-                            elim = tb >= __dadd_rn(__dmul_rn(a, b), __dmul_rn(sa_c[gi], sb));
+                            elim = tb >= __dadd_rn(__dmul_rn(a, b), __dmul_rn(sa, sb));
                         }
                         if (elim) {
                             ++n_elim;
