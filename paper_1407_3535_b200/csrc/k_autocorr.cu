@@ -565,6 +565,7 @@ __global__ void __launch_bounds__(512)
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int tw,
           int seg, int* __restrict__ stop, const double* __restrict__ egs_prev, double egs_central,
           double egs_xi) {
+    pdl_wait();
     if (stop && *stop) return;  // EGS already decided (egs_decide): candidate not needed
     constexpr int hr = H / 2;
     extern __shared__ __align__(16) unsigned acf_smem[];
@@ -840,7 +841,7 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
     const AcfGeom a = acf_geom(m, n, gd, occ);
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
-        k_acf<H><<<grid, a.ny, a.smem, s>>>(img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
+        launch_pdl(k_acf<H>, dim3(grid), dim3(a.ny), a.smem, s, img, p, q, m, n, to_grid(gd), st, thr, map, n_r, a.tw,
                                             a.seg, stop, egs_prev, egs_central, egs_xi);
     return cudaGetLastError();
 }
@@ -1051,6 +1052,7 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 // counts; this only skips work the host would ignore.
 __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
                              int ec, int h, int w, double xi, int cap) {
+    pdl_wait();
     if (*stop) return;
     const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
     const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
@@ -1067,7 +1069,7 @@ __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, i
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, cudaStream_t s) {
-    k_egs_decide<<<1, 1, 0, s>>>(n_r, prev_cost, stop, er, ec, h, w, xi, cap);
+    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap);
     return cudaGetLastError();
 }
 

@@ -203,6 +203,7 @@ __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
                  CellH* partials, int c_last) {
+    pdl_wait();
     __shared__ Cell scratch[8];
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
@@ -234,6 +235,7 @@ __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                 int lane_flush, int rho_by_loc) {
+    pdl_wait();
     // One CTA per location (grid-stride): warp w owns template rows [w*m/8, (w+1)*m/8), so
     // a location costs one or two batches of independent loads per warp instead of m/8
     // dependent batches for a single warp.  Each lane's FP32 partials cover < lane_flush
@@ -378,6 +380,7 @@ __global__ void __launch_bounds__(256)
 
 // ---- reductions -----------------------------------------------------------------------
 __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH* out, ReduceOp op) {
+    pdl_wait();
     __shared__ Cell scratch[32];
     Cell best = no_cell();
     for (int i = threadIdx.x; i < n; i += blockDim.x) {
@@ -408,6 +411,7 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
 }
 
 __global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4) {
+    pdl_wait();
     *stop = 0;
     *prev = INFINITY;
     for (int i = 0; i < 4; ++i) nr4[i] = 0ull;
@@ -484,6 +488,7 @@ __global__ void __launch_bounds__(256)
                const uint8_t* __restrict__ flat, int tflat, const double* __restrict__ thr_ptr,
                const uint8_t* __restrict__ seeded, int2* locs, unsigned long long max_locs,
                Tally* tally, uint8_t* visits) {
+    pdl_wait();
     const double T = *thr_ptr;
     const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
     const bool thr_ok = T >= -1.0;
@@ -557,6 +562,7 @@ __global__ void __launch_bounds__(256)
 
 // y = sqrt(max(0, 1 - clamp(x)^2)): one factor of half_gap (bounds.cpp:21-23).
 __global__ void k_sqrt_gap(const double* __restrict__ x, double* __restrict__ y, size_t n) {
+    pdl_wait();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x) {
         const double a = dclamp(x[i], -1.0, 1.0);
@@ -584,6 +590,7 @@ __global__ void k_seed_members(Grid g, const double* __restrict__ rho_c,
                                double margin, uint8_t* seeded, int2* locs,
                                unsigned long long* count, unsigned long long max_locs,
                                unsigned long long* n_groups, unsigned long long max_groups) {
+    pdl_wait();
     const long long G = (long long)g.ti_hi * g.tc;
     const double T = *thr;
     for (long long gi = (long long)g.ti_lo * g.tc + blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -747,7 +754,7 @@ cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long 
                       int n_partials, cudaStream_t s, int rho_by_loc) {
     // one FP32 partial covers lane_flush rows of one template column: < 2^24 exactly
     const int lane_flush = int(16777216LL / 65025LL);
-    k_corr_list<<<n_partials, 256, 0, s>>>(job, locs, count, max_count, out_rho, out_deg,
+    launch_pdl(k_corr_list, dim3(n_partials), dim3(256), 0, s, job, locs, count, max_count, out_rho, out_deg,
                                            partials, lane_flush, rho_by_loc);
     return cudaGetLastError();
 }
@@ -784,7 +791,7 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last) {
-    k_centre_epi<<<n_partials, 256, 0, s>>>(job, to_grid(g), rows, cbase, sw, nc, col0, dot, rho_c,
+    launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw, nc, col0, dot, rho_c,
                                             deg_c, partials, c_last);
     return cudaGetLastError();
 }
@@ -797,12 +804,12 @@ cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc,
 
 cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
                          const ReduceOp* op) {
-    k_reduce_cells<<<1, 1024, 0, s>>>(partials, n, out, op ? *op : ReduceOp{});
+    launch_pdl(k_reduce_cells, dim3(1), dim3(1024), 0, s, partials, n, out, op ? *op : ReduceOp{});
     return cudaGetLastError();
 }
 
 cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s) {
-    k_egs_init<<<1, 1, 0, s>>>(stop, prev, nr4);
+    launch_pdl(k_egs_init, dim3(1), dim3(1), 0, s, stop, prev, nr4);
     return cudaGetLastError();
 }
 
@@ -822,10 +829,10 @@ cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double*
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
                      uint8_t* visits, cudaStream_t s) {
     const size_t G = size_t(g.tr) * g.tc;
-    k_sqrt_gap<<<int(std::min<size_t>((G + 255) / 256, 148 * 8)), 256, 0, s>>>(rho_c, sa_c, G);
+    launch_pdl(k_sqrt_gap, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256), 0, s, rho_c, sa_c, G);
     const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
     const int blocks = std::max(1, std::min(rows, 148 * 8));
-    k_sec_rows<<<blocks, 256, 0, s>>>(to_grid(g), map, rho_c, sa_c, deg_c, flat, tflat, thr, seeded,
+    launch_pdl(k_sec_rows, dim3(blocks), dim3(256), 0, s, to_grid(g), map, rho_c, sa_c, deg_c, flat, tflat, thr, seeded,
                                       locs, max_locs, tally, visits);
     return cudaGetLastError();
 }
@@ -847,7 +854,7 @@ cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, 
                          unsigned long long max_groups, cudaStream_t s) {
     const long long G = (long long)g.tr * g.tc;
     const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 8));
-    k_seed_members<<<blocks, 256, 0, s>>>(to_grid(g), rho_c, deg_c, thr, margin, seeded, locs, count,
+    launch_pdl(k_seed_members, dim3(blocks), dim3(256), 0, s, to_grid(g), rho_c, deg_c, thr, margin, seeded, locs, count,
                                           max_locs, n_groups, max_groups);
     return cudaGetLastError();
 }

@@ -55,6 +55,7 @@ __global__ void k_u8_to_f32(const uint8_t* __restrict__ img, int p, int q, float
 __global__ void __launch_bounds__(256) k_sum_sq_u8(const uint8_t* __restrict__ img, size_t n,
                                                    unsigned long long* acc_ctr, int rows,
                                                    int cols, double* noise_out) {
+    pdl_wait();
     // acc_ctr[0]: running sum, acc_ctr[1]: finished-block counter; both zero on entry and
     // reset by the last block, which also writes prefix_noise (stats.cpp:79-81).
     unsigned long long* out = acc_ctr;
@@ -316,7 +317,7 @@ cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long
                             double* out, cudaStream_t s) {
     const size_t n = size_t(p) * q;
     const int blocks = int(std::min<size_t>(148 * 4, (n / 16 + 255) / 256 + 1));
-    k_sum_sq_u8<<<blocks, 256, 0, s>>>(img, n, q_total, p, q, out);  // q_total: 2 u64, zeroed
+    launch_pdl(k_sum_sq_u8, dim3(blocks), dim3(256), 0, s, img, n, q_total, p, q, out);  // q_total: 2 u64, zeroed
     return cudaGetLastError();
 }
 cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,
@@ -340,6 +341,7 @@ namespace {
 __global__ void __launch_bounds__(512)
     k_wstats_u8(const uint8_t* __restrict__ img, int p, int q, int m, int n, int tw, int seg,
                 const double* __restrict__ pn, DevStats st) {
+    pdl_wait();
     __shared__ unsigned ls[2][2][512], wtot[2][2][16];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const int er = p - m + 1, ec = q - n + 1;
@@ -434,7 +436,7 @@ cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, cons
         int seg = std::max(std::min(m, 32), (er + nseg - 1) / nseg);
         nseg = (er + seg - 1) / seg;
         dim3 grid(ntiles, nseg);
-        k_wstats_u8<<<grid, ny, 0, s>>>(img, p, q, m, n, tw, seg, prefix_noise, st);
+        launch_pdl(k_wstats_u8, dim3(grid), dim3(ny), 0, s, img, p, q, m, n, tw, seg, prefix_noise, st);
         return cudaGetLastError();
     }
     const int tpr = (ec + kChunk - 1) / kChunk;

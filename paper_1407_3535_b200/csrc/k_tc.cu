@@ -127,6 +127,7 @@ __device__ __forceinline__ void tmem_zero16(uint32_t addr) {
 
 template <int MODE>
 __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask task, CellH* partials) {
+    pdl_wait();
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcPlan& P = job.plan;
     // a ring stage holds kRows consecutive scheduled image rows (kRows slots of a_slot bytes):
@@ -448,6 +449,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
 // (rho/8)*SBO + (rho%8)*16 + (t/16)*128 + t%16, SBO = 128*Kx/16.
 __global__ void k_tc_build_b(const float* __restrict__ tf, int npad, int m, int n, TcPlan P,
                              uint8_t* __restrict__ out) {
+    pdl_wait();
     const int ch = blockIdx.y;
     const int i0 = P.i0[ch], i1 = P.i1[ch];
     const int entries = i1 - i0;
@@ -484,6 +486,7 @@ __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_
 namespace {
 __global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
                                     unsigned long long* list_count) {
+    pdl_wait();
     const unsigned long long n = tally->survivors;
     const bool dense = n * 16 > E;
     *dense_flag = dense ? 1 : 0;
@@ -494,7 +497,7 @@ __global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, in
 
 cudaError_t survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
                               unsigned long long* list_count, cudaStream_t s) {
-    k_survivor_dispatch<<<1, 1, 0, s>>>(tally, E, dense_flag, list_count);
+    launch_pdl(k_survivor_dispatch, dim3(1), dim3(1), 0, s, tally, E, dense_flag, list_count);
     return cudaGetLastError();
 }
 
@@ -588,7 +591,7 @@ cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int p
 cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
                        cudaStream_t s) {
     dim3 grid(64, plan.nch);
-    k_tc_build_b<<<grid, 256, 0, s>>>(tf, npad, m, n, plan, out);
+    launch_pdl(k_tc_build_b, dim3(grid), dim3(256), 0, s, tf, npad, m, n, plan, out);
     return cudaGetLastError();
 }
 
@@ -608,9 +611,9 @@ cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* 
         attr_set[task.mode] = smem;
     }
     switch (task.mode) {
-        case 0: k_tc_corr<0><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
-        case 1: k_tc_corr<1><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
-        default: k_tc_corr<2><<<grid, kTcThreads, smem, s>>>(job, task, partials); break;
+        case 0: launch_pdl(k_tc_corr<0>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
+        case 1: launch_pdl(k_tc_corr<1>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
+        default: launch_pdl(k_tc_corr<2>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
     }
     e = cudaGetLastError();
     return e;

@@ -5,11 +5,34 @@
 // the cited reference line.  Integer work (window sums, dot products on u8 data) is
 // exact in any order and is free to be re-associated.
 #pragma once
+#include <utility>
 
 #include <cstdint>
 #include <cuda_runtime.h>
 
 namespace tmk {
+
+// Programmatic dependent launch: kernels on the search path start with pdl_wait() (a
+// no-op unless launched with launch_pdl), so the next kernel's launch overlaps the tail
+// of the previous one; nothing produced by earlier work is touched before the wait.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                              cudaStream_t s, Args&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 
 constexpr double kEps = 2.220446049250313e-16;
 
