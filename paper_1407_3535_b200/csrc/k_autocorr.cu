@@ -796,7 +796,7 @@ struct AcfGeom {
 
 AcfGeom acf_geom(int m, int n, GridDesc gd, int resident = 0) {
     AcfGeom a{};
-    int ny = std::max(128, 3 * n);
+    int ny = std::max(128, 4 * n);
     ny = std::max(ny, n - 1 + 2 * gd.w);
     ny = (ny + 31) & ~31;
     if (ny > 512) return AcfGeom{};
