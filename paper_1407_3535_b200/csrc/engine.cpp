@@ -642,9 +642,11 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, i
     geo->plan = tmk::tc_plan(T.m, T.n, sr, kTcSmemBudget);
     if (geo->plan.nch == 0) invalid("tensor-core plan unavailable");
     geo->ntc = (ws.ec + tmk::tc_tile_cols() - 1) / tmk::tc_tile_cols();
-    // rows per band: as many as the tiles allow while keeping >= 1 tile per SM
-    int rmax = 16;
-    while (rmax > 1 && size_t((rows.size() + rmax - 1) / rmax) * geo->ntc < 148) rmax /= 2;
+    // rows per band: the fewest waves of 148 persistent CTAs with <= 16 rows per band, then
+    // bands as equal as possible so every CTA gets the same number of tiles
+    const size_t work = rows.size() * size_t(geo->ntc);
+    const size_t waves = std::max<size_t>(1, (work + 148 * 16 - 1) / (148 * 16));
+    int rmax = int(std::min<size_t>(16, std::max<size_t>(1, (work + 148 * waves - 1) / (148 * waves))));
     const std::vector<tmk::TcBand> bands = tc_bands(rows, yi, sr, rmax);
     geo->nbands = int(bands.size());
     geo->bands.ensure(bands.size());
