@@ -258,8 +258,11 @@ struct tm_ctx {
     // pinned readback block: device->host copies into it are asynchronous, so the host can
     // keep working (e.g. upload the next template) until it synchronises
     using HostRes = tmk::ResultBlock;
-    HostRes* hres = nullptr;   // pinned
-    DBuf<tmk::ResultBlock> res_dev;  // packed on the device by the final reduction
+    HostRes* hres = nullptr;      // pinned, mapped: kernels write results straight into it
+    HostRes* hres_dev = nullptr;  // its device address
+    // side stream for template uploads overlapped with the preparation's kernels
+    cudaStream_t s2 = nullptr;
+    cudaEvent_t ev_t = nullptr;
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -512,7 +515,7 @@ WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
 // ---- templates ---------------------------------------------------------------------------
 
 // template_stats (stats.cpp:98-111) in reference order, then upload.
-Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n) {
+Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = false) {
     Tmpl T;
     T.m = m;
     T.n = n;
@@ -535,10 +538,19 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n) {
     std::vector<float> tf(size_t(m) * T.npad, 0.f);
     for (int i = 0; i < m; ++i)
         for (int j = 0; j < n; ++j) tf[size_t(i) * T.npad + j] = float(t[size_t(i) * n + j]);
+    // side stream only when the device buffers already exist (a fresh stream-ordered
+    // allocation on ctx->s must not be touched from another stream)
+    side = side && ctx->tf.p && ctx->tf.cap >= tf.size() && ctx->td.p &&
+           ctx->td.cap >= size_t(m) * n;
     ctx->tf.ensure(tf.size());
     ctx->td.ensure(size_t(m) * n);
-    ctx->pin_tf.upload(ctx->tf.p, tf.data(), tf.size() * 4, ctx->s);
-    ctx->pin_td.upload(ctx->td.p, t, size_t(m) * n * 8, ctx->s);
+    cudaStream_t us = side ? ctx->s2 : ctx->s;
+    ctx->pin_tf.upload(ctx->tf.p, tf.data(), tf.size() * 4, us);
+    ctx->pin_td.upload(ctx->td.p, t, size_t(m) * n * 8, us);
+    if (side) {  // the main stream waits for the copies before any later work
+        CK(cudaEventRecord(ctx->ev_t, ctx->s2));
+        CK(cudaStreamWaitEvent(ctx->s, ctx->ev_t, 0));
+    }
     return T;
 }
 
@@ -1040,12 +1052,13 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
                 ctx->add(1);
             }
         }
-        CK(cudaMemcpyAsync(ctx->hres->nr, ctx->counters.p + 8, 8 * nc, cudaMemcpyDeviceToHost,
-                           ctx->s));
         if (before_sync && *before_sync) {  // host work overlapped with the candidates
             (*before_sync)();
             before_sync = nullptr;
         }
+        // counts straight into the mapped pinned block (no memcpy node on the stream)
+        CK(tmk::copy_u64(ctx->counters.p + 8, ctx->hres_dev->nr, nc, ctx->s));
+        ctx->add(1);
         CK(cudaStreamSynchronize(ctx->s));
         unsigned long long nr[4] = {0, 0, 0, 0};
         for (int k = 0; k < nc; ++k) nr[k] = ctx->hres->nr[k];
@@ -1336,13 +1349,12 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
                       nullptr, ctx->partials.p + np, kListBlocks, s, 1));
     ctx->add(2);
-    ctx->res_dev.ensure(1);
-    tmk::ReduceOp op_pack{};  // the final reduction packs the host-readable result
+    tmk::ReduceOp op_pack{};  // the final reduction packs the result into pinned host memory
     op_pack.kind = 3;
     op_pack.cells = ctx->cells.p;
     op_pack.tally = ctx->tally.p;
     op_pack.thr = ctx->thr.p;
-    op_pack.packed = ctx->res_dev.p;
+    op_pack.packed = ctx->hres_dev;
     reduce_to(ctx, np + kListBlocks, 2, &op_pack);
 }
 
@@ -1471,8 +1483,8 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     }
     HT("survivors");
     tm_ctx::HostRes* hr = ctx->hres;
-    if (device_dispatch) {  // packed by the final reduction: one copy
-        CK(cudaMemcpyAsync(hr, ctx->res_dev.p, sizeof *hr, cudaMemcpyDeviceToHost, s));
+    if (device_dispatch) {
+        // already packed into the mapped pinned block by the final reduction
     } else {
         CK(cudaMemcpyAsync(hr->cells, ctx->cells.p, sizeof hr->cells, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&hr->tally, ctx->tally.p, sizeof hr->tally, cudaMemcpyDeviceToHost, s));
@@ -1723,6 +1735,11 @@ void ctx_release(tm_ctx* ctx) {
     cudaEventDestroy(ctx->ev0);
     cudaEventDestroy(ctx->ev1);
     for (cudaEvent_t ev : ctx->pool) cudaEventDestroy(ev);
+    if (ctx->s2) {
+        cudaStreamSynchronize(ctx->s2);
+        cudaStreamDestroy(ctx->s2);
+    }
+    if (ctx->ev_t) cudaEventDestroy(ctx->ev_t);
     if (ctx->hres) cudaFreeHost(ctx->hres);
     delete ctx;  // stream-ordered frees of the scratch buffers
     cudaStreamSynchronize(st);
@@ -1779,7 +1796,11 @@ int tm_ctx_create(int device, tm_ctx** out) {
         g_stream = ctx->s;
         CK(cudaEventCreate(&ctx->ev0));
         CK(cudaEventCreate(&ctx->ev1));
-        CK(cudaMallocHost(reinterpret_cast<void**>(&ctx->hres), sizeof(tm_ctx::HostRes)));
+        CK(cudaHostAlloc(reinterpret_cast<void**>(&ctx->hres), sizeof(tm_ctx::HostRes),
+                         cudaHostAllocMapped));
+        CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->hres_dev), ctx->hres, 0));
+        CK(cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking));
+        CK(cudaEventCreateWithFlags(&ctx->ev_t, cudaEventDisableTiming));
         ctx->counters.ensure(32);
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
@@ -2174,7 +2195,7 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
         Tmpl T;
         bool uploaded = false;
         const std::function<void()> hook = [&] {
-            T = upload_template(ctx, tmpl, m, n);
+            T = upload_template(ctx, tmpl, m, n, /*side=*/true);
             uploaded = true;
         };
         std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params, &hook));

@@ -410,6 +410,11 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
     }
 }
 
+__global__ void k_copy_u64(const unsigned long long* src, unsigned long long* dst, int n) {
+    pdl_wait();
+    for (int i = 0; i < n; ++i) dst[i] = src[i];
+}
+
 __global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4) {
     pdl_wait();
     *stop = 0;
@@ -806,6 +811,10 @@ cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t 
                          const ReduceOp* op) {
     launch_pdl(k_reduce_cells, dim3(1), dim3(1024), 0, s, partials, n, out, op ? *op : ReduceOp{});
     return cudaGetLastError();
+}
+
+cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s) {
+    return launch_pdl(k_copy_u64, dim3(1), dim3(1), 0, s, src, dst, n);
 }
 
 cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s) {

@@ -208,6 +208,8 @@ cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc,
 // Reduce partial cells -> out[0] (better_candidate order).
 cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
                          const ReduceOp* op = nullptr);
+// dst[i] = src[i] for i < n (one thread; dst may be mapped pinned host memory).
+cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s);
 // EGS batch start: stop = 0, prev cost = +inf, nr[0..3] = 0 (one launch).
 cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s);
 
