@@ -946,21 +946,48 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
     }
     CK(tmk::autocorr_init(map, g, ctx->s, stop));
     ctx->add(1);
+    // the (di, dj) offsets in batches: their prefix problems are independent, one launch
+    // each for the row scans and the column accumulations of a batch
     const int hr = g.h / 2, wr = g.w / 2;
+    struct Off {
+        int di, dj;
+    };
+    std::vector<Off> offs;
     for (int di = -hr; di <= hr; ++di)
         for (int dj = -wr; dj <= wr; ++dj) {
             if (di == 0 && dj == 0) continue;
-            const int orr = std::max(0, -di), occ = std::max(0, -dj);
-            const int ph_ = p - std::abs(di), pw = q - std::abs(dj);
-            if (ph_ < m || pw < n) continue;
-            ctx->rowacc.ensure(size_t(ph_) * pw);
-            ctx->prefix.ensure(size_t(ph_ + 1) * (pw + 1));
-            tmk::ProdSrc src{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0, stop};
-            CK(tmk::replica_prefix(src, ph_, pw, ctx->rowacc.p, ctx->prefix.p, ctx->s));
-            CK(tmk::autocorr_offset_epilogue(ctx->prefix.p, ph_, pw, m, n, g, ws.dev(), di, dj,
-                                             map, ctx->s, stop));
-            ctx->add(3);
+            if (p - std::abs(di) < m || q - std::abs(dj) < n) continue;
+            offs.push_back(Off{di, dj});
         }
+    const size_t slot = size_t(p) * q, pslot = size_t(p + 1) * (q + 1);
+    // batch size bounded so the scratch stays modest (<= ~4.5 GB for 4096^2 images)
+    const int kb = int(std::max<size_t>(1, std::min<size_t>(tmk::kProdBatch,
+                                                             (size_t(4) << 30) / (16 * pslot))));
+    for (size_t o0 = 0; o0 < offs.size(); o0 += kb) {
+        const int nb = int(std::min<size_t>(kb, offs.size() - o0));
+        tmk::ProdBatch bt{};
+        bt.n = nb;
+        bt.slot = slot;
+        bt.pslot = pslot;
+        for (int k = 0; k < nb; ++k) {
+            const int di = offs[o0 + k].di, dj = offs[o0 + k].dj;
+            const int orr = std::max(0, -di), occ = std::max(0, -dj);
+            bt.src[k] = tmk::ProdSrc{img->f64.p, q, orr, occ, img->f64.p, q, orr + di, occ + dj, 0,
+                                     stop};
+            bt.rows[k] = p - std::abs(di);
+            bt.cols[k] = q - std::abs(dj);
+        }
+        ctx->rowacc.ensure(slot * nb);
+        ctx->prefix.ensure(pslot * nb);
+        CK(tmk::replica_prefix_batch(bt, ctx->rowacc.p, ctx->prefix.p, ctx->s));
+        ctx->add(2);
+        for (int k = 0; k < nb; ++k) {
+            CK(tmk::autocorr_offset_epilogue(ctx->prefix.p + size_t(k) * pslot, bt.rows[k],
+                                             bt.cols[k], m, n, g, ws.dev(), offs[o0 + k].di,
+                                             offs[o0 + k].dj, map, ctx->s, stop));
+            ctx->add(1);
+        }
+    }
     CK(tmk::retained_count(map, g, thr, nr, ctx->s, stop));
     ctx->add(1);
 }

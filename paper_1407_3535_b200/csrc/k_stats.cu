@@ -248,6 +248,64 @@ __global__ void k_colacc(const double* __restrict__ rowacc, int rows, int cols,
     }
 }
 
+// Batched replica prefixes: grid.y = offset k of a ProdBatch, each with its own source
+// (X, Y row/column offsets), extent and scratch slot; per offset the operations are
+// exactly k_rowscan / k_colacc's (same sequential order per row / column), so only the
+// amount of independent work per launch grows (one offset alone leaves ~128 warps).
+__global__ void k_rowscan_b(ProdBatch b, double* __restrict__ rowacc) {
+    const int k = blockIdx.y;
+    const ProdSrc src = b.src[k];
+    if (src.stop && *src.stop) return;
+    const int rows = b.rows[k], cols = b.cols[k];
+    double* out = rowacc + size_t(k) * b.slot;
+    __shared__ double tile[4][32][33];
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    const int r0 = (blockIdx.x * 4 + wid) * 32;
+    if (r0 >= rows) return;
+    double acc = 0.0;
+    for (int c0 = 0; c0 < cols; c0 += 32) {
+        const int c = c0 + lane;
+        for (int kk = 0; kk < 32; ++kk) {
+            const int r = r0 + kk;
+            tile[wid][kk][lane] = (r < rows && c < cols) ? src_value(src, r, c) : 0.0;
+        }
+        __syncwarp();
+        const int cn = min(32, cols - c0);
+        for (int jj = 0; jj < cn; ++jj) {
+            acc = __dadd_rn(acc, tile[wid][lane][jj]);
+            tile[wid][lane][jj] = acc;
+        }
+        __syncwarp();
+        for (int kk = 0; kk < 32; ++kk) {
+            const int r = r0 + kk;
+            if (r < rows && c < cols) out[size_t(r) * cols + c] = tile[wid][kk][lane];
+        }
+        __syncwarp();
+    }
+}
+
+__global__ void k_colacc_b(ProdBatch b, const double* __restrict__ rowacc,
+                           double* __restrict__ prefix) {
+    const int k = blockIdx.y;
+    if (b.src[k].stop && *b.src[k].stop) return;
+    const int rows = b.rows[k], cols = b.cols[k];
+    const double* in = rowacc + size_t(k) * b.slot;
+    double* pre = prefix + size_t(k) * b.pslot;
+    const int c = blockIdx.x * blockDim.x + threadIdx.x;
+    const size_t pw = size_t(cols) + 1;
+    if (c > cols) return;
+    pre[c] = 0.0;  // zero top row
+    if (c == cols) {
+        for (int r = 0; r < rows; ++r) pre[size_t(r + 1) * pw] = 0.0;  // zero first col
+        return;
+    }
+    double acc = 0.0;
+    for (int r = 0; r < rows; ++r) {
+        acc = __dadd_rn(acc, in[size_t(r) * cols + c]);
+        pre[size_t(r + 1) * pw + c + 1] = acc;
+    }
+}
+
 __global__ void k_window_diff(const double* __restrict__ prefix, int rows, int cols, int m, int n,
                               double* __restrict__ out) {
     const int er = rows - m + 1, ec = cols - n + 1;
@@ -455,6 +513,19 @@ cudaError_t window_sums_u8(const uint8_t* img, int p, int q, int m, int n, int* 
     k_hsum_u8<<<g1, 128, 0, s>>>(img, p, q, n, hs, nullptr);
     dim3 g2((ec + 127) / 128, (er + kChunk - 1) / kChunk);
     k_vsum_only<<<g2, 128, 0, s>>>(hs, p, ec, m, out);
+    return cudaGetLastError();
+}
+
+cudaError_t replica_prefix_batch(const ProdBatch& b, double* rowacc, double* prefix,
+                                 cudaStream_t s) {
+    int maxr = 0, maxc = 0;
+    for (int k = 0; k < b.n; ++k) {
+        maxr = std::max(maxr, b.rows[k]);
+        maxc = std::max(maxc, b.cols[k]);
+    }
+    const int warps = (maxr + 31) / 32;
+    k_rowscan_b<<<dim3((warps + 3) / 4, b.n), 128, 0, s>>>(b, rowacc);
+    k_colacc_b<<<dim3((maxc + 1 + 127) / 128, b.n), 128, 0, s>>>(b, rowacc, prefix);
     return cudaGetLastError();
 }
 

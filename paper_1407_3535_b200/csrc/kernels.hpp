@@ -98,6 +98,16 @@ struct ProdSrc {
     int square;
     const int* stop = nullptr;  // device flag: skip the work when set (EGS early exit)
 };
+// Up to kProdBatch independent prefix problems per launch (R_co replica offsets).
+constexpr int kProdBatch = 16;
+struct ProdBatch {
+    ProdSrc src[kProdBatch];
+    int rows[kProdBatch], cols[kProdBatch];
+    int n;
+    size_t slot, pslot;  // per-problem stride of rowacc / prefix (elements)
+};
+cudaError_t replica_prefix_batch(const ProdBatch& b, double* rowacc, double* prefix,
+                                 cudaStream_t s);
 // rowacc: rows*cols; prefix: (rows+1)*(cols+1) with zero first row/col.
 cudaError_t replica_prefix(ProdSrc src, int rows, int cols, double* rowacc, double* prefix,
                            cudaStream_t s);
