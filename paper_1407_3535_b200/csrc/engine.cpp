@@ -492,10 +492,21 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
     } else {
         ctx->S.ensure(E);
         ctx->Q.ensure(E);
-        replica_sums(ctx, tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 0}, p, q, m, n,
-                     ctx->S.p);
-        replica_sums(ctx, tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 1}, p, q, m, n,
-                     ctx->Q.p);
+        // S (pixels) and Q (squares): two independent prefix problems in one batch
+        tmk::ProdBatch bt{};
+        bt.n = 2;
+        bt.slot = size_t(p) * q;
+        bt.pslot = size_t(p + 1) * (q + 1);
+        bt.src[0] = tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 0};
+        bt.src[1] = tmk::ProdSrc{img->f64.p, q, 0, 0, nullptr, 0, 0, 0, 1};
+        bt.rows[0] = bt.rows[1] = p;
+        bt.cols[0] = bt.cols[1] = q;
+        ctx->rowacc.ensure(2 * bt.slot);
+        ctx->prefix.ensure(2 * bt.pslot);
+        CK(tmk::replica_prefix_batch(bt, ctx->rowacc.p, ctx->prefix.p, ctx->s));
+        CK(tmk::replica_window_diff(ctx->prefix.p, p, q, m, n, ctx->S.p, ctx->s));
+        CK(tmk::replica_window_diff(ctx->prefix.p + bt.pslot, p, q, m, n, ctx->Q.p, ctx->s));
+        ctx->add(4);
         CK(tmk::stats_from_sums(ctx->S.p, ctx->Q.p, E, m, n, prefix_noise, ws.dev(), ctx->s));
         ctx->add(1);
     }
