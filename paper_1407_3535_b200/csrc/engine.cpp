@@ -1453,8 +1453,12 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     {
         Phase ph(ctx, "sec_compact");
         ctx->sa_c.ensure(G);
+        // frozen / seeded on the exact 8-bit path: a survivor list longer than E/16 is never
+        // read (the dense path takes over, driven by the visit mask), so only that many
+        // locations are written; the sequential replay and the FP64 path read every one
+        const unsigned long long max_locs = (!seq && fp32_path(img, T)) ? E / 16 + 1 : E;
         CK(tmk::sec_rows(g, in.map, ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
-                         ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, visits, s));
+                         ctx->thr.p, seeded, ctx->locs.p, max_locs, ctx->tally.p, visits, s));
         ctx->add(2);
     }
     double T0 = 0.0;

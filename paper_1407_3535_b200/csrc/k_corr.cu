@@ -499,6 +499,8 @@ __global__ void __launch_bounds__(256)
     const bool thr_ok = T >= -1.0;
     const int lane = threadIdx.x & 31;
     unsigned long long n_elim = 0, n_keep = 0;
+    bool list_full = false;            // this warp saw the survivor list reach max_locs
+    unsigned long long surv_local = 0;  // survivors counted after that (one atomic at the end)
     const int r_lo = g.row_lo(), r_hi = g.row_hi();
     const int cols = ((g.ec + 31) / 32) * 32;  // whole warps per row (ballots)
     for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
@@ -547,12 +549,18 @@ __global__ void __launch_bounds__(256)
             }
             const unsigned ballot = __ballot_sync(0xffffffffu, survivor);
             if (ballot) {
-                unsigned long long basepos = 0;
-                if (lane == 0) basepos = atomicAdd(&tally->survivors, (unsigned long long)__popc(ballot));
-                basepos = __shfl_sync(0xffffffffu, basepos, 0);
-                if (survivor) {
-                    const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
-                    if (pos < max_locs) locs[pos] = make_int2(r, c);
+                if (list_full) {  // nothing more can be listed: count only (no atomics)
+                    surv_local += __popc(ballot);
+                } else {
+                    unsigned long long basepos = 0;
+                    if (lane == 0)
+                        basepos = atomicAdd(&tally->survivors, (unsigned long long)__popc(ballot));
+                    basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                    list_full = basepos + __popc(ballot) >= max_locs;  // warp-uniform
+                    if (survivor) {
+                        const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
+                        if (pos < max_locs) locs[pos] = make_int2(r, c);
+                    }
                 }
             }
         }
@@ -562,6 +570,7 @@ __global__ void __launch_bounds__(256)
     if (lane == 0) {
         if (n_elim) atomicAdd(&tally->eliminated, n_elim);
         if (n_keep) atomicAdd(&tally->retained, n_keep);
+        if (surv_local) atomicAdd(&tally->survivors, surv_local);
     }
 }
 
