@@ -45,18 +45,41 @@ def _peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    """SM clocks + throttle reasons sampled during the timed region.
+
+    In-process NVML polling every 2 ms (the timed region of a default run is only tens of
+    ms); nvidia-smi ``-lms 20`` when NVML is unavailable.  ``start()`` returns once the
+    first sample is in, so the samples cover the timed steps.
+    """
 
     FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
               "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
               "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index=0):
         self.index = index
         self.proc = None
+        self.nvml = None
         self.lines = []
+        self.sm, self.smax, self.reasons = [], None, set()
+        self.running = False
 
     def start(self):
+        try:
+            import pynvml as N
+            N.nvmlInit()
+            dev = N.nvmlDeviceGetHandleByIndex(self.index)
+            self.smax = float(N.nvmlDeviceGetMaxClockInfo(dev, N.NVML_CLOCK_SM))
+            self.nvml = (N, dev)
+            self.running = True
+            self.t = threading.Thread(target=self._poll, daemon=True)
+            self.t.start()
+            while not self.sm and self.t.is_alive():
+                time.sleep(0.001)
+            return
+        except Exception:
+            self.nvml = None
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
@@ -64,14 +87,38 @@ class ClockSampler:
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5:
+                time.sleep(0.005)
         except Exception:
             self.proc = None
+
+    def _poll(self):
+        N, dev = self.nvml
+        bits = [N.nvmlClocksEventReasonHwSlowdown, N.nvmlClocksEventReasonHwThermalSlowdown,
+                N.nvmlClocksEventReasonSwThermalSlowdown, N.nvmlClocksEventReasonSwPowerCap]
+        while self.running:
+            try:
+                self.sm.append(float(N.nvmlDeviceGetClockInfo(dev, N.NVML_CLOCK_SM)))
+                r = N.nvmlDeviceGetCurrentClocksEventReasons(dev)
+                for nm, b in zip(self.NAMES, bits):
+                    if r & b:
+                        self.reasons.add(nm)
+            except Exception:
+                return
+            time.sleep(0.002)
 
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
 
     def stop(self):
+        if self.nvml:
+            self.running = False
+            self.t.join(timeout=1)
+            sm = list(self.sm)
+            return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.smax,
+                    "reasons": sorted(self.reasons), "samples": len(sm), "source": "nvml"}
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -80,7 +127,6 @@ class ClockSampler:
         except Exception:
             self.proc.kill()
         sm, smax, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for ln in self.lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 6:
@@ -90,11 +136,11 @@ class ClockSampler:
                 smax = float(parts[1])
             except ValueError:
                 continue
-            for nm, v in zip(names, parts[2:6]):
+            for nm, v in zip(self.NAMES, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(nm)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm), "source": "nvidia-smi"}
 
 
 def dist_env():
