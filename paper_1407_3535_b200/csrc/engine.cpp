@@ -330,6 +330,7 @@ struct tm_image {
     // 16-byte pitched zero-padded 8-bit copy for the tensor-core path (k_tc.cu)
     DBuf<uint8_t> u8p;
     int u8p_pitch = 0;
+    int u8p_rows = 0;
 };
 
 struct tm_prep {
@@ -397,11 +398,12 @@ void alloc_u8(tm_ctx* ctx, tm_image* img) {
 // 16-byte-pitched copy for the tensor-core kernels (sized for any template width).
 void tc_pitch_copy(tm_ctx* ctx, tm_image* img) {
     const int pitch = tmk::tc_pitch(img->q, img->q);
-    const int rows = img->p + 1;
+    const int rows = img->p + tmk::kU8PadRows;  // zero rows below: look-ahead reads
     img->u8p.ensure(size_t(rows) * pitch);
     CK(tmk::tc_pitch_image(img->u8.p, img->p, img->q, img->u8p.p, pitch, rows, ctx->s));
     ctx->add(1);
     img->u8p_pitch = pitch;
+    img->u8p_rows = rows;
 }
 
 void finish_integer_image(tm_ctx* ctx, tm_image* img) {
@@ -936,8 +938,11 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
         if (ctx->ac_fused && tmk::autocorr_fused_supported(m, n, g)) {
             // total_cost's central term (egs.cpp:28-37) for the in-kernel early rejection
             const double central = double((g.er + g.h - 1) / g.h) * double((g.ec + g.w - 1) / g.w);
+            // (the group-column kernel stages rows from the 16-byte-pitched copy)
+            const bool pitched = img->u8p.p && img->u8p_rows >= p + tmk::kU8PadRows;
             CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, stop,
-                                      ctx->s, egs_prev, central, egs_xi));
+                                      ctx->s, egs_prev, central, egs_xi,
+                                      pitched ? img->u8p.p : nullptr, img->u8p_pitch));
             ctx->add(1);
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));

@@ -15,6 +15,8 @@
 // work is O((hw-1) * p * q) integer MACs per candidate size instead of the reference's
 // (hw-1) full-image FP64 prefix passes.
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.hpp"
 #include "tm_common.cuh"
@@ -846,6 +848,425 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
     return cudaGetLastError();
 }
 
+// ---- fused R_co, one thread per group column (square groups, h <= 5) ----------------------
+//
+// The walk of k_acf, but thread t owns the W = h image columns [cc_k, cc_k + W) of group
+// column k = k0 + t (cc_k = k*W + W/2, the centre column of a full group).  The W x h
+// vertical sliding sums stay in registers, the block scan runs over group blocks
+// B(t) = sum_j V[di][j] (W times fewer scan steps than per column), and at each event the
+// thread evaluates the h members of its own group (one centre statistic for h members).
+// A window [cc_k, cc_k + n) is the Q = n / W whole blocks t .. t+Q-1 plus the first
+// R = n % W columns of block t+Q ("head").  The clipped last group column (ec % W != 0) has
+// its centre delta columns left of cc_k: its window is the last delta columns of block t-1
+// ("tail"), Qc whole blocks from t and the first Rc columns of block t+Qc; the tile
+// geometry keeps that group off thread 0.  Same sums, same FP64 epilogue, same map and
+// count as k_acf (u32 sums are exact mod 2^32 and the true sums are < 2^32).
+//
+// Image rows reach the walk through a shared-memory ring (RR = m + 2h + h/2 rows of the
+// tile's SW-byte column span, A and B sides share it): the rows of the next transition
+// are copied with 16-byte cp.async one event ahead, so the walk reads bytes at shared-
+// memory latency instead of waiting on L2 for the trailing rows m rows back.  `img` is the
+// 16-byte-pitched zero-padded copy (pitch P, >= p + kU8PadRows rows).
+constexpr int kAcgWb = 8;  // warp-total stride (NT <= 256)
+// staged bytes per ring row: NT*W tile columns + 2*(h/2) for the B offsets + 16-byte alignment
+__host__ __device__ constexpr int acg_span(int nt, int h) { return (15 + nt * h + 2 * (h / 2) + 15) & ~15; }
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void opaque(unsigned& x) { asm("" : "+r"(x)); }
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+template <int H, int NT>
+__global__ void __launch_bounds__(NT)
+    k_acg(const uint8_t* __restrict__ img, int P, int q, int m, int n, Grid g, DevStats st,
+          double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
+          int seg, int RR, int* __restrict__ stop, const double* __restrict__ egs_prev,
+          double egs_central, double egs_xi) {
+    pdl_wait();
+    if (stop && *stop) return;
+    constexpr int W = H, hr = H / 2;
+    constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
+    constexpr int NCH = SW / 16;
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int dj = int(blockIdx.x) - hr;
+    const int k0 = blockIdx.y * G;
+    const int ti0 = g.ti_lo + blockIdx.z * seg;
+    const int ti1 = min(ti0 + seg, g.ti_hi);
+    if (ti0 >= ti1 || k0 >= g.tc) return;  // uniform
+    const int k = k0 + t;
+    const int Q = n / W, R = n - Q * W;
+    const int wl = g.ec - (g.tc - 1) * W;  // width of the last group column
+    const bool clip_tile = wl < W && g.tc - 1 < k0 + G;  // uniform
+    const int delta = hr - ((wl - 1) >> 1);
+    const int Qc = (n - delta) / W, Rc = (n - delta) - Qc * W;
+    extern __shared__ __align__(16) unsigned acg_smem[];
+    constexpr int PS = H * (4 * NT + kAcgWb);  // per parity: Lb | Hh | Tt | Hc [H][NT], wb [H][8]
+    uint8_t* ring = reinterpret_cast<uint8_t*>(acg_smem + 2 * PS);
+    const int s0 = (k0 * W) & ~15;  // first staged column (16-byte aligned)
+    auto stage = [&](int r_lo, int nrows) {  // rows [r_lo, r_lo + nrows) -> ring slots
+        const int slot0 = r_lo % RR;
+        for (int i = t; i < nrows * NCH; i += NT) {
+            const int rr = i / NCH, c = i - rr * NCH;
+            int slot = slot0 + rr;
+            if (slot >= RR) slot -= RR;
+            cp_async16(ring + slot * SW + c * 16, img + size_t(r_lo + rr) * P + s0 + c * 16);
+        }
+        cp_async_commit();
+    };
+
+    const int y0 = k * W + hr;  // every thread's columns lie inside the staged span
+    const int oa = y0 - s0, ob = y0 + dj - s0;
+    unsigned V[H][W], rl[H][W], rt[H][W];
+    int cr = g.center_row(ti0);
+    stage(cr, m + H + hr);
+#pragma unroll
+    for (int d = 0; d < H; ++d) {
+        const int xr = max(cr - 1 - hr + d, 0);
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            V[d][j] = 0u;
+            rl[d][j] = d >= 1 ? unsigned(__ldg(img + size_t(xr) * P + y0 + dj + j)) : 0u;
+            rt[d][j] = rl[d][j];
+        }
+    }
+    // ring byte offsets of the leading / trailing A and B rows (wrap at RR * SW)
+    const int ring_bytes = RR * SW;
+    int la = (cr % RR) * SW, lb = ((cr + hr) % RR) * SW;
+    int ta = la, tb = lb;
+    auto bump = [&](int& o, int by) {
+        o += by;
+        if (o >= ring_bytes) o -= ring_bytes;
+    };
+    auto lead_at = [&](const uint8_t* pa, const uint8_t* pb) {
+        unsigned a[W], b[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            b[j] = pb[j];
+            a[j] = pa[j];
+            opaque(a[j]);  // plain IMADs: keeps nvcc from packing bytes into IDP (PRMT-heavy)
+            opaque(b[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+#pragma unroll
+            for (int d = 0; d < H - 1; ++d) rl[d][j] = rl[d + 1][j];
+            rl[H - 1][j] = b[j];
+#pragma unroll
+            for (int d = 0; d < H; ++d) V[d][j] += a[j] * rl[d][j];
+        }
+    };
+    auto trail_at = [&](const uint8_t* pa, const uint8_t* pb) {
+        unsigned a[W], b[W];
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            b[j] = pb[j];
+            a[j] = pa[j];
+            opaque(a[j]);  // plain IMADs: keeps nvcc from packing bytes into IDP (PRMT-heavy)
+            opaque(b[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+#pragma unroll
+            for (int d = 0; d < H - 1; ++d) rt[d][j] = rt[d + 1][j];
+            rt[H - 1][j] = b[j];
+#pragma unroll
+            for (int d = 0; d < H; ++d) V[d][j] -= a[j] * rt[d][j];
+        }
+    };
+    auto lead = [&]() {
+        lead_at(ring + la + oa, ring + lb + ob);
+        bump(la, SW);
+        bump(lb, SW);
+    };
+    auto trail = [&]() {
+        trail_at(ring + ta + oa, ring + tb + ob);
+        bump(ta, SW);
+        bump(tb, SW);
+    };
+    // H row steps; straight-line (immediate ring offsets) unless a stream wraps inside them
+    const int lim = ring_bytes - (H - 1) * SW;
+    auto advance_lead = [&]() {
+        if (la < lim && lb < lim) {
+            const uint8_t* pa = ring + la + oa;
+            const uint8_t* pb = ring + lb + ob;
+#pragma unroll
+            for (int s = 0; s < H; ++s) lead_at(pa + s * SW, pb + s * SW);
+            bump(la, H * SW);
+            bump(lb, H * SW);
+        } else {
+#pragma unroll
+            for (int s = 0; s < H; ++s) lead();
+        }
+    };
+    auto advance_both = [&]() {
+        if (la < lim && lb < lim && ta < lim && tb < lim) {
+            const uint8_t* pa = ring + la + oa;
+            const uint8_t* pb = ring + lb + ob;
+            const uint8_t* qa = ring + ta + oa;
+            const uint8_t* qb = ring + tb + ob;
+#pragma unroll
+            for (int s = 0; s < H; ++s) {
+                lead_at(pa + s * SW, pb + s * SW);
+                trail_at(qa + s * SW, qb + s * SW);
+            }
+            bump(la, H * SW);
+            bump(lb, H * SW);
+            bump(ta, H * SW);
+            bump(tb, H * SW);
+        } else {
+#pragma unroll
+            for (int s = 0; s < H; ++s) {
+                lead();
+                trail();
+            }
+        }
+    };
+    cp_async_wait_all();
+    __syncthreads();
+    {
+        int x = cr;
+        const int xe = cr + m;
+#pragma unroll 1
+        for (; x + H <= xe; x += H) advance_lead();
+#pragma unroll 1
+        for (; x < xe; ++x) lead();
+    }
+    const double mn = double(m) * double(n);
+    // this thread's group: members (di, dj) of group column k, all h row offsets
+    const bool owner = t < G && k < g.tc;
+    const int gc0 = k * W, gc1 = min(gc0 + W, g.ec) - 1;
+    const int cc = (gc0 + gc1) >> 1;
+    const int c = cc + dj;
+    const bool col_ok = owner && c >= gc0 && c <= gc1;
+    const bool clipped = owner && gc1 - gc0 + 1 < W;
+    const int hi = clipped ? t + Qc : t + Q;  // whole blocks [t, hi)
+    const bool has_head = clipped ? Rc > 0 : R > 0;
+    const int i1 = hi - 1;
+    const int w0 = t > 0 ? (t - 1) >> 5 : 0, w1 = i1 >= 0 ? i1 >> 5 : 0;
+    uint8_t pf_fc, pf_fm[H];
+    double pf_mc, pf_oc, pf_mm[H], pf_om[H];
+    bool pf_row[H];
+    auto prefetch = [&](int tin, int crn) {
+        const int r0 = tin * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        const unsigned kc = col_ok ? unsigned(crn) * unsigned(g.ec) + unsigned(cc) : 0u;
+        pf_fc = st.flat[kc];
+        pf_mc = st.mu[kc];
+        pf_oc = st.omega[kc];
+#pragma unroll
+        for (int d = 0; d < H; ++d) {
+            const int mr = crn + d - hr;
+            pf_row[d] = col_ok && mr >= r0 && mr <= r1;
+            const unsigned km = pf_row[d] ? unsigned(mr) * unsigned(g.ec) + unsigned(c) : 0u;
+            pf_fm[d] = st.flat[km];
+            pf_mm[d] = st.mu[km];
+            pf_om[d] = st.omega[km];
+        }
+    };
+    prefetch(ti0, cr);
+    __shared__ unsigned cta_cnt;
+    if (t == 0) cta_cnt = 0u;
+    const double prev = (egs_prev && stop) ? *egs_prev : 0.0;
+    const bool can_reject = egs_prev && stop && fabs(prev) <= 1.7976931348623157e308;
+    int my_abort = 0, ev = 0, parity = 0;
+#pragma unroll 1
+    for (int ti = ti0;;) {
+        unsigned* Lb = acg_smem + (parity ? PS : 0);
+        unsigned* Hh = Lb + H * NT;
+        unsigned* Tt = Hh + H * NT;
+        unsigned* Hc = Tt + H * NT;
+        unsigned* wb = Hc + H * NT;
+        parity ^= 1;
+        {
+            unsigned v[H];
+#pragma unroll
+            for (int d = 0; d < H; ++d) {
+                unsigned bs = 0u, hh = 0u, tt = 0u, hc = 0u;
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    bs += V[d][j];
+                    if (j < R) hh += V[d][j];
+                    if (j >= W - delta) tt += V[d][j];
+                    if (j < Rc) hc += V[d][j];
+                }
+                v[d] = bs;
+                Hh[d * NT + t] = hh;
+                if (clip_tile) {
+                    Tt[d * NT + t] = tt;
+                    Hc[d * NT + t] = hc;
+                }
+            }
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+                for (int d = 0; d < H; ++d) {
+                    const unsigned u = __shfl_up_sync(0xffffffffu, v[d], o);
+                    if (lane >= o) v[d] += u;
+                }
+            }
+#pragma unroll
+            for (int d = 0; d < H; ++d) {
+                Lb[d * NT + t] = v[d];
+                if (lane == 31) wb[d * kAcgWb + wid] = v[d];
+            }
+        }
+        cp_async_wait_all();                    // this thread's rows of the next transition
+        if (__syncthreads_or(my_abort)) break;  // uniform
+        if (ti + 2 < ti1) stage(g.center_row(ti + 1) + m + hr, H);  // the one after it
+        if (can_reject && t == 0 && (++ev & 1) == 0) {
+            const unsigned cn = atomicExch(&cta_cnt, 0u);
+            const unsigned long long tot = atomicAdd(n_r, (unsigned long long)cn) + cn;
+            const double total = __dadd_rn(__dadd_rn(egs_central, double(tot)), 0.0);
+            if (!(__dsub_rn(prev, total) > __dmul_rn(egs_xi, prev))) {
+                my_abort = 1;
+                *reinterpret_cast<volatile int*>(stop) = 1;
+            }
+        }
+        unsigned evc = 0;
+        if (col_ok) {
+#pragma unroll
+            for (int d = 0; d < H; ++d) {
+                if (!pf_row[d]) continue;
+                const unsigned km = unsigned(cr + d - hr) * unsigned(g.ec) + unsigned(c);
+                if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
+                    map[km] = 1.0;
+                    continue;
+                }
+                const unsigned* Ld = Lb + d * NT;
+                unsigned S = 0u;
+                if (hi > t) {
+                    S = Ld[i1];
+                    if (t > 0) S -= Ld[t - 1];
+#pragma unroll 1
+                    for (int x = w0; x < w1; ++x) S += wb[d * kAcgWb + x];
+                }
+                if (has_head) S += (clipped ? Hc : Hh)[d * NT + hi];
+                if (clipped) S += Tt[d * NT + t - 1];
+                double val = 0.0;
+                if (!pf_fc && !pf_fm[d]) {
+                    const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc), pf_mm[d]));
+                    val = dclamp(__ddiv_rn(num, __dmul_rn(pf_oc, pf_om[d])), -1.0, 1.0);
+                }
+                map[km] = val;
+                if (val < thr) ++evc;
+            }
+        }
+        evc = __reduce_add_sync(0xffffffffu, evc);
+        if (lane == 0 && evc) atomicAdd(&cta_cnt, evc);
+        if (++ti >= ti1) break;
+        const int crn = g.center_row(ti);
+        prefetch(ti, crn);
+        if (crn - cr == H) {
+            advance_both();
+        } else {
+#pragma unroll 1
+            for (int x = cr; x < crn; ++x) {
+                lead();
+                trail();
+            }
+        }
+        cr = crn;
+    }
+    __syncthreads();
+    if (t == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
+}
+
+struct AcgGeom {
+    int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, SW = 0, RR = 0;
+    size_t smem = 0;
+};
+
+constexpr size_t kAcgSmemMax = 200 * 1024;
+
+AcgGeom acg_geom(int m, int n, GridDesc gd, int nt, int resident = 0) {
+    AcgGeom a{};
+    const int W = gd.w, hr = gd.h / 2;
+    if (gd.h != gd.w || (W != 3 && W != 5) || nt > 256 || nt % 32) return a;
+    const int Q = n / W, R = n % W;
+    int G = nt - (Q + (R > 0)) + 1;
+    if (G < 2) return a;
+    const bool clipped = gd.ec % W != 0;
+    if (clipped) {
+        if (gd.tc < 2) return a;
+        while (G > 1 && (gd.tc - 1) % G == 0) --G;  // keep the clipped group off thread 0
+        if ((gd.tc - 1) % G == 0) return a;
+    }
+    a.SW = acg_span(nt, gd.h);
+    a.RR = m + 2 * gd.h + hr;
+    a.smem = 2 * size_t(gd.h) * (4 * size_t(nt) + kAcgWb) * sizeof(unsigned) +
+             size_t(a.RR) * a.SW;
+    if (a.smem > kAcgSmemMax) return AcgGeom{};
+    a.nt = nt;
+    a.G = G;
+    a.ntiles = (gd.tc + G - 1) / G;
+    const int rows = gd.ti_hi - gd.ti_lo;
+    const int seg_min = std::max(1, (m + gd.h - 1) / gd.h);
+    if (resident <= 0) resident = std::max(1, 1024 / nt);
+    const int slots = 148 * resident;
+    const int per_wave = std::max(1, slots / std::max(1, gd.w * a.ntiles));
+    const int seg_1 = (rows + per_wave - 1) / per_wave;
+    const int waves = std::min(4, std::max(1, (seg_1 + 4 * seg_min - 1) / (4 * seg_min)));
+    int nseg = std::max(1, waves * per_wave);
+    nseg = std::min(nseg, std::max(1, (rows + seg_min - 1) / seg_min));
+    a.seg = std::max(1, (rows + nseg - 1) / nseg);
+    a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
+    return a;
+}
+
+int acg_threads() {
+    static int nt = [] {
+        const char* e = std::getenv("TMATCH_ACG_THREADS");
+        const int v = e ? std::atoi(e) : 256;
+        return v == 128 ? 128 : 256;
+    }();
+    return nt;
+}
+
+bool acg_enabled() {
+    static bool on = [] {
+        const char* e = std::getenv("TMATCH_ACF");
+        return !(e && std::strcmp(e, "column") == 0);
+    }();
+    return on;
+}
+
+template <int H, int NT>
+cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
+                          DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
+                          const double* egs_prev, double egs_central, double egs_xi,
+                          cudaStream_t s) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_acg<H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(kAcgSmemMax));
+        attr = true;
+    }
+    const AcgGeom a0 = acg_geom(m, n, gd, NT);
+    if (a0.nt == 0) return cudaErrorInvalidValue;
+    int occ = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acg<H, NT>, NT, a0.smem) != cudaSuccess)
+        occ = 0;
+    const AcgGeom a = acg_geom(m, n, gd, NT, occ);
+    dim3 grid(gd.w, a.ntiles, a.nseg);
+    if (gd.ti_hi > gd.ti_lo)
+        launch_pdl(k_acg<H, NT>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n, to_grid(gd), st,
+                   thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi);
+    return cudaGetLastError();
+}
+
+template <int H>
+cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
+                       DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
+                       const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
+    if (acg_threads() == 128)
+        return launch_acg_nt<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
+                                     egs_central, egs_xi, s);
+    return launch_acg_nt<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
+                                 egs_central, egs_xi, s);
+}
+
 template <int H>
 cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int ti_base, int trr,
                        int tr, unsigned* V, cudaStream_t s) {
@@ -1078,13 +1499,23 @@ bool autocorr_fused_supported(int m, int n, GridDesc g) {
     const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
     return g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
            (p + kU8PadRows) * q < (size_t(1) << 31) &&
-           size_t(g.er) * g.ec < (size_t(1) << 32) && acf_geom(m, n, g).ny > 0;
+           size_t(g.er) * g.ec < (size_t(1) << 32) &&
+           (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads()).nt > 0);
 }
 
 cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
                               DevStats st, double retain_threshold, double* map,
                               unsigned long long* n_r, int* stop, cudaStream_t s,
-                              const double* egs_prev, double egs_central, double egs_xi) {
+                              const double* egs_prev, double egs_central, double egs_xi,
+                              const uint8_t* imgp, int pitch) {
+    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads()).nt > 0) {
+        if (gd.h == 3)
+            return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                 egs_prev, egs_central, egs_xi, s);
+        if (gd.h == 5)
+            return launch_acg<5>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                                 egs_prev, egs_central, egs_xi, s);
+    }
     switch (gd.h) {
         case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                      egs_prev, egs_central, egs_xi, s);

@@ -135,7 +135,7 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               DevStats st, double retain_threshold, double* map,
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev = nullptr, double egs_central = 0.0,
-                              double egs_xi = 0.0);
+                              double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, cudaStream_t s);
 // Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.

@@ -280,6 +280,25 @@ def test_fused_autocorr_equals_colwalk(port, m, n):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("m,n,cols", [(64, 64, 2000), (20, 63, 1997), (17, 65, 1531),
+                                      (9, 7, 2100), (40, 10, 801)])
+def test_fused_autocorr_wide(ctx, port, m, n, cols):
+    """The group-column R_co kernel (h = 3, 5) over several column tiles: every remainder
+    n mod h (head columns), clipped and unclipped last group columns (tail columns), clipped
+    last group rows, flat patches — equal to the oracle bit for bit."""
+    rng = np.random.default_rng(m * 7 + n + cols)
+    base = np.cumsum(np.cumsum(rng.normal(size=(m + 40, cols)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    img[5:30, 100:180] = 91  # flat windows (degenerate statistics)
+    gi = ctx.image(img)
+    for h in (3, 5):
+        got = ctx.local_autocorrelation(gi, m, n, h, h)
+        want = port.local_autocorrelation(img.astype(np.float64), m, n, h, h)
+        assert np.array_equal(got, want), (h, np.argwhere(got != want)[:5])
+        assert ctx.autocorr_retained(gi, m, n, h, h) == port.retained_count(want, h, h), h
+
+
+@pytest.mark.gpu
 @pytest.mark.parametrize("m,n", [(1, 1), (5, 7), (33, 64), (64, 200), (130, 3)])
 def test_window_stats_fused_tiles(ctx, port, m, n):
     """Fused window statistics over several column tiles and row segments, with flat
