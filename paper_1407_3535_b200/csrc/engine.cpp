@@ -263,6 +263,16 @@ struct tm_ctx {
     // side stream for template uploads overlapped with the preparation's kernels
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev_t = nullptr;
+    cudaEvent_t ev_egs = nullptr;  // end of an EGS batch's count copy
+    // speculative centre scan (tm_search): predicted group size passed to the EGS decide
+    // kernels, and what was enqueued for it
+    int spec_want = 0;
+    struct Spec {
+        bool armed = false;
+        tmk::GridDesc g{};
+        const int* rows_dev = nullptr;
+    } spec;
+    std::map<std::vector<long long>, int> last_he;  // (p, q, m, n, h0) -> last accepted h
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -695,9 +705,11 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, i
 int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet& rs, int sr,
            tmk::TcTask task, const int** rows_dev = nullptr) {
     TcGeo& geo = tc_geometry(ctx, ws, T, rs, sr);
+    HT("tc_geo");
     const tmk::TcPlan& plan = geo.plan;
     ctx->tc_b.ensure(plan.total_bytes);
-    CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s));
+    CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s, task.gate));
+    HT("build_b");
     tmk::TcJob job{};
     job.imgp = tc_image(ctx, img, ws.ec);
     job.pitch = img->u8p_pitch;
@@ -725,6 +737,7 @@ int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet
         task.dbg_flags = std::atoi(std::getenv("TMATCH_TC_DEBUG"));
     }
     CK(tmk::tc_corr(job, task, ctx->partials.p, &np, ctx->s));
+    HT("tc_corr");
     ctx->add(2);
     if (dbg) {
         std::vector<long long> h(148 * 8);
@@ -811,11 +824,20 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
             task.out_rho = ctx->dotbuf.p;
             const int* rows_dev = nullptr;
-            tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+            // already enqueued behind the EGS batch (tm_search) and confirmed by the device
+            // decision for this grid: the dots are in flight, skip the launches
+            const auto& sp = ctx->spec;
+            if (sp.armed && sp.g.er == g.er && sp.g.ec == g.ec && sp.g.h == g.h && sp.g.w == g.w &&
+                sp.g.ti_lo == g.ti_lo && sp.g.ti_hi == g.ti_hi && ctx->hres->spec == 1)
+                rows_dev = sp.rows_dev;
+            else
+                tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+            ctx->spec.armed = false;
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
                                     task.c_last));
+            HT("centre_epi");
             ctx->add(1);
         }
         reduce_to(ctx, n1 + n2, 0, op);
@@ -924,11 +946,49 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
               ctx->deg_c.p + off, 0, op);
 }
 
+// Speculative centre scan for tm_search: the B build and the tensor-core centre dots for a
+// predicted group size, enqueued behind an EGS batch and gated on the device decision
+// (k_egs_decide: EGS finished with h_e == predicted).  On a wrong prediction both kernels
+// exit at entry and centre_scan launches the real ones.
+void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const tmk::GridDesc& g) {
+    ctx->spec.armed = false;
+    if (!(tc_path(ctx, img, T) && g.h <= tmk::kTcMaxClasses) || g.ti_hi <= g.ti_lo) return;
+    const size_t G = size_t(g.tr) * g.tc;
+    ctx->rho_c.ensure(G);
+    ctx->deg_c.ensure(G);
+    ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
+    ctx->dotbuf.ensure(G);
+    RowSet rs;
+    rs.kind = 1;
+    rs.lo = g.ti_lo;
+    rs.hi = g.ti_hi;
+    rs.g = g;
+    const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
+    tmk::TcTask task{};
+    task.mode = 1;
+    task.cbase = g.w / 2;
+    task.cstep = g.w;
+    task.nc = clipped ? g.tc - 1 : g.tc;
+    task.tc = g.tc;
+    task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
+    task.out_rho = ctx->dotbuf.p;
+    task.gate = reinterpret_cast<const int*>(ctx->counters.p + 24);
+    const int* rows_dev = nullptr;
+    tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+    ctx->spec.armed = true;
+    ctx->spec.g = g;
+    ctx->spec.rows_dev = rows_dev;
+}
+
 // ---- EGS: local auto-correlation + retained count ----------------------------------------
 // Launch the R_co map + retained count for one group size; n_r lands in *nr (device).
-void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
+// count_only: an EGS candidate whose map may never be used -- the fused 8-bit kernels then
+// produce the retained count alone (no map stores, no divisions away from the threshold);
+// returns whether `map` was written.
+bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
                      double thr, double* map, unsigned long long* nr, int* stop = nullptr,
-                     const double* egs_prev = nullptr, double egs_xi = 0.0) {
+                     const double* egs_prev = nullptr, double egs_xi = 0.0,
+                     bool count_only = false) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     if (!egs_prev) CK(cudaMemsetAsync(nr, 0, 8, ctx->s));  // EGS batches: egs_init zeroes it
     Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
@@ -940,10 +1000,12 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             const double central = double((g.er + g.h - 1) / g.h) * double((g.ec + g.w - 1) / g.w);
             // (the group-column kernel stages rows from the 16-byte-pitched copy)
             const bool pitched = img->u8p.p && img->u8p_rows >= p + tmk::kU8PadRows;
-            CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, stop,
-                                      ctx->s, egs_prev, central, egs_xi,
-                                      pitched ? img->u8p.p : nullptr, img->u8p_pitch));
+            CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr,
+                                      count_only ? nullptr : map, nr, stop, ctx->s, egs_prev,
+                                      central, egs_xi, pitched ? img->u8p.p : nullptr,
+                                      img->u8p_pitch));
             ctx->add(1);
+            return !count_only;
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
             CK(tmk::autocorr_u8_colwalk(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
@@ -958,7 +1020,7 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             CK(tmk::autocorr_u8(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr, ctx->s));
             ctx->add(1);
         }
-        return;
+        return true;
     }
     CK(tmk::autocorr_init(map, g, ctx->s, stop));
     ctx->add(1);
@@ -1006,12 +1068,13 @@ void autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
     }
     CK(tmk::retained_count(map, g, thr, nr, ctx->s, stop));
     ctx->add(1);
+    return true;
 }
 
 long long autocorr_map(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
-                       double thr, double* map) {
+                       double thr, double* map, bool count_only = false) {
     unsigned long long* nr = ctx->counters.p + 2;
-    autocorr_launch(ctx, img, ws, g, thr, map, nr);
+    autocorr_launch(ctx, img, ws, g, thr, map, nr, nullptr, nullptr, 0.0, count_only);
     unsigned long long v = 0;
     CK(cudaMemcpyAsync(&v, nr, 8, cudaMemcpyDeviceToHost, ctx->s));
     CK(cudaStreamSynchronize(ctx->s));
@@ -1064,7 +1127,14 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     // is going to ignore (after the first rejection) exit at entry instead of running.
     double* dprev = reinterpret_cast<double*>(ctx->counters.p + 20);
     int* dstop = reinterpret_cast<int*>(ctx->counters.p + 21);
+    unsigned long long* dgate_u64 = ctx->counters.p + 24;  // speculation gate (tm_search)
+    unsigned long long* dgate = dgate_u64;
+    int* dhacc = reinterpret_cast<int*>(ctx->counters.p + 25);
     bool first_batch = true;
+    // Only the accepted size's map is used: the first candidate (always accepted) writes its
+    // map, later candidates count only, and a size accepted without a map is recomputed once
+    // after the loop (its count re-derived and checked).
+    int map_h = -1, map_w = -1;
     while (!done) {
         struct Cand {
             int h, w;
@@ -1077,8 +1147,9 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             hh = std::min(hh + 2, cap);
             ww = std::min(ww + 2, cap);
         }
-        if (first_batch) {  // stop = 0, prev = +inf, nr[0..3] = 0
-            CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s));
+        bool map_written[4] = {false, false, false, false};
+        if (first_batch) {  // stop = 0, prev = +inf, nr[0..3] = 0, h_acc = 0, gate = 0
+            CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s, dhacc, dgate));
             ctx->add(1);
             first_batch = false;
         } else {
@@ -1087,24 +1158,31 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         for (int k = 0; k < nc; ++k) {
             const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
             ctx->egs_maps[k].ensure(E);
-            autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p, ctx->counters.p + 8 + k,
-                            dstop, dprev, xi);
-            if (k + 1 < nc) {
-                CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
-                                   cand[k].w, xi, cap, ctx->s));
-                ctx->add(1);
-            }
+            map_written[k] = autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p,
+                                             ctx->counters.p + 8 + k, dstop, dprev, xi,
+                                             /*count_only=*/!(cand[k].h == h0 && cand[k].w == w0));
+            // (after the last candidate too: the speculation gate needs the final decision)
+            CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
+                               cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s));
+            ctx->add(1);
         }
+        // counts (and the gate) straight into the mapped pinned block; the host waits for
+        // this point only, so work enqueued by the hook keeps the device busy meanwhile
+        CK(tmk::copy_u64(ctx->counters.p + 8, ctx->hres_dev->nr, nc, ctx->s, dgate_u64,
+                         &ctx->hres_dev->spec));
+        ctx->add(1);
+        CK(cudaEventRecord(ctx->ev_egs, ctx->s));
         if (before_sync && *before_sync) {  // host work overlapped with the candidates
             (*before_sync)();
             before_sync = nullptr;
         }
-        // counts straight into the mapped pinned block (no memcpy node on the stream)
-        CK(tmk::copy_u64(ctx->counters.p + 8, ctx->hres_dev->nr, nc, ctx->s));
-        ctx->add(1);
-        CK(cudaStreamSynchronize(ctx->s));
+        ctx->spec_want = 0;  // later batches: the speculation (if any) was for this one
+        HT("egs_enqueued");
+        CK(cudaEventSynchronize(ctx->ev_egs));
+        HT("egs_sync");
         unsigned long long nr[4] = {0, 0, 0, 0};
         for (int k = 0; k < nc; ++k) nr[k] = ctx->hres->nr[k];
+        for (int k = nc; k < 4; ++k) map_written[k] = false;
         for (int k = 0; k < nc; ++k) {
             const tm_egs_iter cost = total_cost_h(er, ec, cand[k].h, cand[k].w, (long long)nr[k], 0.0);
             const bool accepted =
@@ -1117,7 +1195,11 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             out.w = cand[k].w;
             out.cost = cost;
             out.trace.push_back(cost);
-            best.swap(ctx->egs_maps[k]);
+            if (map_written[k]) {
+                best.swap(ctx->egs_maps[k]);
+                map_h = cand[k].h;
+                map_w = cand[k].w;
+            }
             prev_cost = cost.total;
             if ((cand[k].h >= er && cand[k].w >= ec) || (cand[k].h >= cap && cand[k].w >= cap)) {
                 done = true;
@@ -1126,6 +1208,12 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             h = std::min(cand[k].h + 2, cap);
             w = std::min(cand[k].w + 2, cap);
         }
+    }
+    if (out.h != map_h || out.w != map_w) {
+        const long long n_r = autocorr_map(ctx, img, ws, make_grid(er, ec, out.h, out.w), thr,
+                                           best.p);
+        if (n_r != out.cost.retained)
+            throw TmError{TM_ECUDA, "efficient_group_size: map recount mismatch"};
     }
     return out;
 }
@@ -1704,6 +1792,7 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     }
     CK(cudaEventRecord(prep->ev1, ctx->s));
     prep->g = make_grid(img->p - m + 1, img->q - n + 1, prep->h, prep->w);
+    HT("prep_end");
     return prep.release();
 }
 
@@ -1787,6 +1876,7 @@ void ctx_release(tm_ctx* ctx) {
         cudaStreamDestroy(ctx->s2);
     }
     if (ctx->ev_t) cudaEventDestroy(ctx->ev_t);
+    if (ctx->ev_egs) cudaEventDestroy(ctx->ev_egs);
     if (ctx->hres) cudaFreeHost(ctx->hres);
     delete ctx;  // stream-ordered frees of the scratch buffers
     cudaStreamSynchronize(st);
@@ -1848,6 +1938,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&ctx->hres_dev), ctx->hres, 0));
         CK(cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_t, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_egs, cudaEventDisableTiming));
         ctx->counters.ensure(32);
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
@@ -2048,7 +2139,7 @@ int tm_autocorr_retained(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w,
         WS& ws = get_ws(ctx, img, m, n);
         ctx->map_user.ensure(size_t(g.er) * g.ec);
         *n_r = autocorr_map(ctx, img, ws, g, expected_elimination_threshold_h(rho_tb),
-                            ctx->map_user.p);
+                            ctx->map_user.p, /*count_only=*/true);
     });
 }
 
@@ -2238,14 +2329,39 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
               const tm_match_params* params, tm_match_result* out) {
     return guard(ctx, [&] {
         if (!img || !tmpl || !params || !out) invalid("tm_search: null argument");
+        HT("start");
         CK(cudaEventRecord(ctx->ev0, ctx->s));
         Tmpl T;
         bool uploaded = false;
+        // Predicted h_e: the last one seen for this image/template shape (else h0).  Its
+        // centre scan is enqueued behind the first EGS batch, gated on the device decision,
+        // so the device does not idle while the host reads the counts.
+        const bool egs = params->mode != TM_MODE_OPTA && params->h0 == params->w0;
+        const std::vector<long long> key = {img->p, img->q, m, n, params->h0};
+        int want = 0;
+        if (egs && img->integer && m <= img->p && n <= img->q) {
+            const auto it = ctx->last_he.find(key);
+            want = it != ctx->last_he.end() ? it->second : params->h0;
+        }
+        ctx->spec_want = want;
+        ctx->spec.armed = false;
         const std::function<void()> hook = [&] {
             T = upload_template(ctx, tmpl, m, n, /*side=*/true);
             uploaded = true;
+            if (want > 0)
+                spec_centre(ctx, img, get_ws(ctx, img, m, n),
+                            T, make_grid(img->p - m + 1, img->q - n + 1, want, want));
         };
-        std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params, &hook));
+        std::unique_ptr<tm_prep> prep;
+        try {
+            prep.reset(prepare(ctx, img, m, n, *params, &hook));
+        } catch (...) {
+            ctx->spec_want = 0;
+            ctx->spec.armed = false;
+            throw;
+        }
+        ctx->spec_want = 0;
+        if (egs) ctx->last_he[key] = prep->h;
         prep->ctx = nullptr;  // internal: not counted as a context reference
         if (!uploaded) T = upload_template(ctx, tmpl, m, n);
         *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);

@@ -740,7 +740,7 @@ __global__ void __launch_bounds__(512)
             const int d = s_d[j];
             const unsigned km = unsigned(cr + d - hr) * unsigned(g.ec) + unsigned(s_c[j]);
             if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
-                map[km] = 1.0;
+                if (map) map[km] = 1.0;
                 continue;
             }
             // S = P[u+n-1] - P[u-1], P the block prefix = warp prefix + earlier warp totals
@@ -758,11 +758,14 @@ __global__ void __launch_bounds__(512)
             constexpr int kSpan = 8;
 #pragma unroll
             for (int k = 0; k < kSpan; ++k) S += (w0 + k < w1) ? wd[k] : 0u;
-            double val = 0.0;
-            if (!pf_fc[j] && !pf_fm[j]) {
-                const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc[j]), pf_mm[j]));
-                val = dclamp(__ddiv_rn(num, __dmul_rn(pf_oc[j], pf_om[j])), -1.0, 1.0);
+            const bool flat = pf_fc[j] || pf_fm[j];
+            const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc[j]), pf_mm[j]));
+            const double den = __dmul_rn(pf_oc[j], pf_om[j]);
+            if (!map) {  // EGS candidate: retained count only
+                if (flat ? 0.0 < thr : retained_below(num, den, thr)) ++evc;
+                continue;
             }
+            const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
             map[km] = val;
             if (val < thr) ++evc;
         }
@@ -1131,7 +1134,7 @@ __global__ void __launch_bounds__(NT)
                 if (!pf_row[d]) continue;
                 const unsigned km = unsigned(cr + d - hr) * unsigned(g.ec) + unsigned(c);
                 if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
-                    map[km] = 1.0;
+                    if (map) map[km] = 1.0;
                     continue;
                 }
                 const unsigned* Ld = Lb + d * NT;
@@ -1144,11 +1147,15 @@ __global__ void __launch_bounds__(NT)
                 }
                 if (has_head) S += (clipped ? Hc : Hh)[d * NT + hi];
                 if (clipped) S += Tt[d * NT + t - 1];
-                double val = 0.0;
-                if (!pf_fc && !pf_fm[d]) {
-                    const double num = __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc), pf_mm[d]));
-                    val = dclamp(__ddiv_rn(num, __dmul_rn(pf_oc, pf_om[d])), -1.0, 1.0);
+                const bool flat = pf_fc || pf_fm[d];
+                const double num =
+                    __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc), pf_mm[d]));
+                const double den = __dmul_rn(pf_oc, pf_om[d]);
+                if (!map) {  // EGS candidate: retained count only (no map, no division)
+                    if (flat ? 0.0 < thr : retained_below(num, den, thr)) ++evc;
+                    continue;
                 }
+                const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
                 map[km] = val;
                 if (val < thr) ++evc;
             }
@@ -1215,13 +1222,16 @@ AcgGeom acg_geom(int m, int n, GridDesc gd, int nt, int resident = 0) {
     return a;
 }
 
-int acg_threads() {
-    static int nt = [] {
+// CTA size per group size: 256 threads for h = 3 (2 CTAs/SM, 9% halo threads at n = 64);
+// 128 for h = 5 (its 25 sliding sums + rings cap 256-thread CTAs at one per SM).
+// TMATCH_ACG_THREADS=128|256 forces one size for both (A/B measurements).
+int acg_threads(int h = 3) {
+    static int forced = [] {
         const char* e = std::getenv("TMATCH_ACG_THREADS");
-        const int v = e ? std::atoi(e) : 256;
-        return v == 128 ? 128 : 256;
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 128 || v == 256) ? v : 0;
     }();
-    return nt;
+    return forced ? forced : (h >= 5 ? 128 : 256);
 }
 
 bool acg_enabled() {
@@ -1260,7 +1270,7 @@ template <int H>
 cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                        DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                        const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
-    if (acg_threads() == 128)
+    if (acg_threads(H) == 128)
         return launch_acg_nt<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
                                      egs_central, egs_xi, s);
     return launch_acg_nt<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
@@ -1470,11 +1480,19 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 // the same FP64 operations as the host replay in engine.cpp): after candidate (h, w) with
 // retained count *n_r, set *stop when it is rejected or is the last one, so the kernels of
 // the remaining candidates of the batch exit at entry.  The host still decides from the
-// counts; this only skips work the host would ignore.
+// counts; this only skips work the host would ignore.  *h_acc tracks the last accepted
+// size and *gate = (EGS finished with h_e == want): the speculative centre scan enqueued
+// behind the batch for the predicted size `want` runs only then (0 = no speculation).  A
+// stop already set at entry came from an earlier decision or from the candidate's own
+// in-kernel rejection; either way the gate is final.
 __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
-                             int ec, int h, int w, double xi, int cap) {
+                             int ec, int h, int w, double xi, int cap, int* h_acc, int want,
+                             unsigned long long* gate) {
     pdl_wait();
-    if (*stop) return;
+    if (*stop) {
+        *gate = (want > 0 && *h_acc == want) ? 1ull : 0ull;
+        return;
+    }
     const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
     const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
     const double prev = *prev_cost;
@@ -1482,15 +1500,19 @@ __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, i
     const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(xi, prev);
     if (!accepted) {
         *stop = 1;
-        return;
+    } else {
+        *prev_cost = total;
+        *h_acc = h;
+        if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
     }
-    *prev_cost = total;
-    if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
+    *gate = (*stop && want > 0 && *h_acc == want) ? 1ull : 0ull;
 }
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
-                       int h, int w, double xi, int cap, cudaStream_t s) {
-    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap);
+                       int h, int w, double xi, int cap, int* h_acc, int want,
+                       unsigned long long* gate, cudaStream_t s) {
+    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap,
+               h_acc, want, gate);
     return cudaGetLastError();
 }
 
@@ -1500,7 +1522,7 @@ bool autocorr_fused_supported(int m, int n, GridDesc g) {
     return g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
            (p + kU8PadRows) * q < (size_t(1) << 31) &&
            size_t(g.er) * g.ec < (size_t(1) << 32) &&
-           (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads()).nt > 0);
+           (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads(g.h)).nt > 0);
 }
 
 cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
@@ -1508,7 +1530,7 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev, double egs_central, double egs_xi,
                               const uint8_t* imgp, int pitch) {
-    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads()).nt > 0) {
+    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd.h)).nt > 0) {
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                  egs_prev, egs_central, egs_xi, s);

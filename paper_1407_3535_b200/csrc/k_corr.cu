@@ -410,16 +410,21 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
     }
 }
 
-__global__ void k_copy_u64(const unsigned long long* src, unsigned long long* dst, int n) {
+__global__ void k_copy_u64(const unsigned long long* src, unsigned long long* dst, int n,
+                           const unsigned long long* src1, unsigned long long* dst1) {
     pdl_wait();
     for (int i = 0; i < n; ++i) dst[i] = src[i];
+    if (src1) *dst1 = *src1;
 }
 
-__global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4) {
+__global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4, int* h_acc,
+                           unsigned long long* gate) {
     pdl_wait();
     *stop = 0;
     *prev = INFINITY;
     for (int i = 0; i < 4; ++i) nr4[i] = 0ull;
+    if (h_acc) *h_acc = 0;
+    if (gate) *gate = 0ull;
 }
 
 // ---- scan 2: SEC test + survivor compaction (matcher.cpp:48-78, bounds.cpp:41-46) -------
@@ -822,12 +827,14 @@ cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t 
     return cudaGetLastError();
 }
 
-cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s) {
-    return launch_pdl(k_copy_u64, dim3(1), dim3(1), 0, s, src, dst, n);
+cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s,
+                     const unsigned long long* src1, unsigned long long* dst1) {
+    return launch_pdl(k_copy_u64, dim3(1), dim3(1), 0, s, src, dst, n, src1, dst1);
 }
 
-cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s) {
-    launch_pdl(k_egs_init, dim3(1), dim3(1), 0, s, stop, prev, nr4);
+cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s, int* h_acc,
+                     unsigned long long* gate) {
+    launch_pdl(k_egs_init, dim3(1), dim3(1), 0, s, stop, prev, nr4, h_acc, gate);
     return cudaGetLastError();
 }
 

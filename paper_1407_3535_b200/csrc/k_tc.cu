@@ -448,8 +448,9 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
 // bytes, canonical no-swizzle K-major: byte (row rho, t) at
 // (rho/8)*SBO + (rho%8)*16 + (t/16)*128 + t%16, SBO = 128*Kx/16.
 __global__ void k_tc_build_b(const float* __restrict__ tf, int npad, int m, int n, TcPlan P,
-                             uint8_t* __restrict__ out) {
+                             uint8_t* __restrict__ out, const int* __restrict__ gate) {
     pdl_wait();
+    if (gate && !*gate) return;  // the pass this B feeds is gated off (survivor_dispatch)
     const int ch = blockIdx.y;
     const int i0 = P.i0[ch], i1 = P.i1[ch];
     const int entries = i1 - i0;
@@ -589,9 +590,9 @@ cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int p
 }
 
 cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
-                       cudaStream_t s) {
+                       cudaStream_t s, const int* gate) {
     dim3 grid(64, plan.nch);
-    launch_pdl(k_tc_build_b, dim3(grid), dim3(256), 0, s, tf, npad, m, n, plan, out);
+    launch_pdl(k_tc_build_b, dim3(grid), dim3(256), 0, s, tf, npad, m, n, plan, out, gate);
     return cudaGetLastError();
 }
 

@@ -46,6 +46,7 @@ struct Tally {  // accumulated on device by the search kernels
 // Host-readable result block (one device->host copy per search / EGS batch).
 struct ResultBlock {
     unsigned long long nr[4];  // EGS retained counts of a candidate batch
+    unsigned long long spec;   // EGS speculation gate of the batch (k_egs_decide)
     CellH cells[3];            // best centre, best seeded member, best survivor
     Tally tally;
     double thr;                // threshold after the search
@@ -137,7 +138,8 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               const double* egs_prev = nullptr, double egs_central = 0.0,
                               double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
-                       int h, int w, double xi, int cap, cudaStream_t s);
+                       int h, int w, double xi, int cap, int* h_acc, int want,
+                       unsigned long long* gate, cudaStream_t s);
 // Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.
 size_t autocorr_colwalk_bytes(int q, GridDesc g);
 bool autocorr_colwalk_supported(int m, int q, GridDesc g);
@@ -219,9 +221,11 @@ cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc,
 cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
                          const ReduceOp* op = nullptr);
 // dst[i] = src[i] for i < n (one thread; dst may be mapped pinned host memory).
-cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s);
+cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s,
+                     const unsigned long long* src1 = nullptr, unsigned long long* dst1 = nullptr);
 // EGS batch start: stop = 0, prev cost = +inf, nr[0..3] = 0 (one launch).
-cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s);
+cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s,
+                     int* h_acc = nullptr, unsigned long long* gate = nullptr);
 
 // ---- scan 2 (matcher.cpp:48-78) ---------------------------------------------------------
 // threshold read from *thr (device).  Survivors appended to locs (int2) with counters in
@@ -329,7 +333,8 @@ int tc_tile_cols();
 cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int pitch, int rows,
                            cudaStream_t s);
 cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
-                       cudaStream_t s);
+                       cudaStream_t s,
+                       const int* gate = nullptr);
 cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* nparts,
                     cudaStream_t s);
 

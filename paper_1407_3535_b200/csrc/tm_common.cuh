@@ -43,6 +43,21 @@ __device__ __forceinline__ double dclamp(double v, double lo, double hi) {
     return (v < lo) ? lo : ((hi < v) ? hi : v);
 }
 
+// The retained test of egs.cpp:12-25 on a non-flat member, clamp(num / den, -1, 1) < thr with
+// the division rounded to nearest (autocorr.cpp:84-88), decided without the division unless
+// num / den lies within 1e-9 (relative) of thr: for 0 < thr <= 1 and den > 0 the clamp
+// cannot change the outcome, and num < thr*den*(1 - 1e-9) implies RN(num/den) < thr (the
+// margin is 10^7 ulps; the FP64 products below are off by at most 2 ulps).
+__device__ __forceinline__ bool retained_below(double num, double den, double thr) {
+    if (thr > 0.0 && thr <= 1.0 && den > 1e-290 && den < 1e290) {
+        const double lim = __dmul_rn(thr, den);
+        const double eps = __dmul_rn(lim, 2e-9);
+        if (num < __dsub_rn(lim, eps)) return true;
+        if (num > __dadd_rn(lim, eps)) return false;
+    }
+    return dclamp(__ddiv_rn(num, den), -1.0, 1.0) < thr;
+}
+
 // detail.hpp:18-22 variance_is_flat
 __device__ __forceinline__ bool variance_is_flat(double var_sum, double q_sum, long long mn) {
     const double abs_tol = __dmul_rn(1e-9, double(mn));

@@ -410,3 +410,29 @@ def test_search_equals_prepare_run(ctx, policy, mode):
                   "refined_rho", "eliminated", "retained", "centers", "ops",
                   "final_threshold"):
             assert getattr(got, k) == getattr(want, k), k
+
+
+def test_search_speculation_hit_and_miss(ctx):
+    """tm_search enqueues the centre scan for the predicted group size (the last h_e seen for
+    this shape) behind the EGS batch, gated on the device decision.  Alternating images of
+    one shape whose h_e differ exercises hits and misses; every result must equal the
+    prepare + run result, and the EGS sizes must differ (so misses really happen)."""
+    rng = np.random.default_rng(11)
+    rough = rng.integers(0, 256, (160, 190)).astype(np.uint8)  # white noise: small h_e
+    base = np.cumsum(np.cumsum(rng.normal(size=(160, 190)), 0), 1)  # smooth: larger h_e
+    smooth = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    keys = ("best_row", "best_col", "best_rho", "eliminated", "retained", "centers", "ops",
+            "final_threshold")
+    seen = set()
+    for img in (rough, smooth, smooth, rough, rough, smooth):
+        t = np.clip(np.rint(img[60:84, 70:96] * 1.05 - 4 + rng.normal(0, 3, (24, 26))), 0, 255)
+        gi = ctx.image(img)
+        prep = ctx.prepare(gi, 24, 26, mode="egs")
+        seen.add(prep.info["h"])
+        want = ctx.run(prep, t, policy="seeded")
+        prep.close()
+        got = ctx.search(gi, t.astype(np.uint8), mode="egs", policy="seeded")
+        for k in keys:
+            assert getattr(got, k) == getattr(want, k), k
+        gi.close()
+    assert len(seen) >= 2, seen
