@@ -250,6 +250,8 @@ struct tm_ctx {
     // R_co kernel choice: fused sliding-window (default) or the column-walk + line-scan pair
     // (TMATCH_AUTOCORR=colwalk; kept for A/B measurements and as a cross-check in tests)
     bool ac_fused = true;
+    // window statistics: four columns per thread (TMATCH_WSTATS=column: one per column)
+    bool ws4 = true;
     // integer tensor-core correlation (tcgen05 kind::i8) for centre scans / dense work;
     // TMATCH_TC=0 selects the CUDA-core FP32-exact kernels (A/B measurements, cross-checks)
     bool tc = true;
@@ -495,7 +497,13 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
     ws.n = n;
     const double* prefix_noise = image_prefix_noise(ctx, img);
     Phase ph(ctx, "window_stats");
-    if (img->integer) {
+    if (img->integer && ctx->ws4 && img->u8p.p && img->u8p_rows >= p + tmk::kU8PadRows &&
+        tmk::window_stats4_supported(p, q, m, n, img->u8p_pitch)) {
+        // four columns per thread from the 16-byte-pitched copy
+        CK(tmk::window_stats4_u8(img->u8p.p, img->u8p_pitch, p, q, m, n, prefix_noise, ws.dev(),
+                                 ctx->s));
+        ctx->add(1);
+    } else if (img->integer) {
         ctx->hs.ensure(size_t(p) * ec);
         ctx->hq.ensure(size_t(p) * ec);
         CK(tmk::window_stats_u8(img->u8.p, p, q, m, n, prefix_noise, ctx->hs.p, ctx->hq.p, ws.dev(),
@@ -1923,6 +1931,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         auto ctx = std::make_unique<tm_ctx>();
         ctx->device = device;
         if (const char* e = std::getenv("TMATCH_AUTOCORR")) ctx->ac_fused = std::strcmp(e, "colwalk") != 0;
+        if (const char* e = std::getenv("TMATCH_WSTATS")) ctx->ws4 = std::strcmp(e, "column") != 0;
         if (const char* e = std::getenv("TMATCH_TC")) ctx->tc = std::strcmp(e, "0") != 0;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));

@@ -11,6 +11,8 @@
 // row (through a shared-memory transpose for coalescing), one thread accumulates one
 // column -- and window sums use the reference's difference order (stats.cpp:50).
 #include <algorithm>
+#include <cstdlib>
+#include <cstring>
 
 #include "kernels.hpp"
 #include "tm_common.cuh"
@@ -478,7 +480,240 @@ __global__ void __launch_bounds__(512)
     }
 }
 
+// Fused window statistics, W (2 or 4) columns per thread (preferred when the 16-byte-pitched
+// copy exists).  Thread t of a CTA owns image columns [c0 + Wt, c0 + Wt + W): one aligned
+// load per row and edge, the vertical sums of its columns (pixel sums packed two per
+// register as 16-bit lanes -- exact while m*255 + 255 < 2^16 -- and squares in u32), and at
+// every extent row one block scan over W-column blocks.  Each thread publishes the
+// warp-local exclusive column prefixes PC(Wt + r), r < W (one vector store per quantity);
+// its W window sums are S(c) = PC(c + n) - PC(c) (+ the warp totals in between), and the
+// FP64 epilogue (stats.cpp:84-91) runs for W consecutive outputs.
+template <int NT, int W>
+__global__ void __launch_bounds__(NT)
+    k_wstats4(const uint8_t* __restrict__ img, int P, int p, int q, int m, int n, int G, int seg,
+              const double* __restrict__ pn, DevStats st) {
+    static_assert(W == 2 || W == 4, "two or four columns per thread");
+    pdl_wait();
+    constexpr int NW = NT / 32;
+    constexpr int TSH = W == 4 ? 7 : 6;  // log2(32 * W): tile column -> warp
+    __shared__ __align__(16) unsigned pcs[2][NT * W], pcq[2][NT * W];
+    __shared__ unsigned wts[2][NW + 1], wtq[2][NW + 1];
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int er = p - m + 1, ec = q - n + 1;
+    const int c0 = blockIdx.x * (W * G);
+    const int r0 = blockIdx.y * seg, r1 = min(r0 + seg, er);
+    if (r0 >= er || c0 >= ec) return;
+    // columns past the image read the zero padding / the next row: only sums no output reads
+    const uint8_t* col = img + (c0 + W * t);
+    const uint8_t* lead = col + size_t(r0) * P;
+    const uint8_t* trail = lead;
+    auto ld = [&](const uint8_t* ptr) -> unsigned {
+        if constexpr (W == 4) return __ldg(reinterpret_cast<const unsigned*>(ptr));
+        else return unsigned(__ldg(reinterpret_cast<const unsigned short*>(ptr)));
+    };
+    // packed pixel sums: W = 4 -> lanes (0,2) and (1,3); W = 2 -> lanes (0,1) in s02
+    unsigned s02 = 0, s13 = 0, qq[W];
+#pragma unroll
+    for (int j = 0; j < W; ++j) qq[j] = 0;
+    auto lanes = [&](unsigned x, unsigned& e, unsigned& o) {
+        if constexpr (W == 4) {
+            e = x & 0x00ff00ffu;
+            o = (x >> 8) & 0x00ff00ffu;
+        } else {
+            e = (x & 0xffu) | ((x & 0xff00u) << 8);
+            o = 0;
+        }
+    };
+#pragma unroll 4
+    for (int a = 0; a < m; ++a) {
+        const unsigned x = ld(lead);
+        lead += P;
+        unsigned e, o;
+        lanes(x, e, o);
+        s02 += e;
+        s13 += o;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const unsigned bj = (x >> (8 * j)) & 0xffu;
+            qq[j] += bj * bj;
+        }
+    }
+    const double inv_mn = 1.0 / (double(m) * double(n));
+    const long long mn = (long long)m * n;
+    const double prefix_noise = *pn;
+    const int cbase = c0 + W * t;
+    const bool any_out = t < G && cbase < ec;
+    const int idx = W * t + n;  // tile-local column of PC(c + n) for j = 0
+    const bool vec = (n % W) == 0;
+    int par = 0;
+    unsigned vi = 0, vo = 0;
+#pragma unroll 1
+    for (int r = r0;;) {
+        if (r + 1 < r1) {  // next row's edges, loaded before this row's scan + epilogue
+            vi = ld(lead);
+            vo = ld(trail);
+        }
+        unsigned sc[W];
+        if constexpr (W == 4) {
+            sc[0] = s02 & 0xffffu; sc[1] = s13 & 0xffffu; sc[2] = s02 >> 16; sc[3] = s13 >> 16;
+        } else {
+            sc[0] = s02 & 0xffffu; sc[1] = s02 >> 16;
+        }
+        unsigned bs = 0, bq = 0;
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            bs += sc[j];
+            bq += qq[j];
+        }
+        unsigned a = bs, b = bq;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned ta = __shfl_up_sync(0xffffffffu, a, o);
+            const unsigned tb = __shfl_up_sync(0xffffffffu, b, o);
+            if (lane >= o) {
+                a += ta;
+                b += tb;
+            }
+        }
+        // warp-local exclusive prefixes at the block's W columns
+        unsigned own_s[W], own_q[W];
+        own_s[0] = a - bs;
+        own_q[0] = b - bq;
+#pragma unroll
+        for (int j = 1; j < W; ++j) {
+            own_s[j] = own_s[j - 1] + sc[j - 1];
+            own_q[j] = own_q[j - 1] + qq[j - 1];
+        }
+        if constexpr (W == 4) {
+            *reinterpret_cast<uint4*>(&pcs[par][4 * t]) = make_uint4(own_s[0], own_s[1], own_s[2], own_s[3]);
+            *reinterpret_cast<uint4*>(&pcq[par][4 * t]) = make_uint4(own_q[0], own_q[1], own_q[2], own_q[3]);
+        } else {
+            *reinterpret_cast<uint2*>(&pcs[par][2 * t]) = make_uint2(own_s[0], own_s[1]);
+            *reinterpret_cast<uint2*>(&pcq[par][2 * t]) = make_uint2(own_q[0], own_q[1]);
+        }
+        if (lane == 31) {
+            wts[par][wid] = a;
+            wtq[par][wid] = b;
+        }
+        __syncthreads();
+        if (any_out) {
+            unsigned hs[W], hq[W];
+            if (vec) {
+                if constexpr (W == 4) {
+                    const uint4 xs = *reinterpret_cast<const uint4*>(&pcs[par][idx]);
+                    const uint4 xq = *reinterpret_cast<const uint4*>(&pcq[par][idx]);
+                    hs[0] = xs.x; hs[1] = xs.y; hs[2] = xs.z; hs[3] = xs.w;
+                    hq[0] = xq.x; hq[1] = xq.y; hq[2] = xq.z; hq[3] = xq.w;
+                } else {
+                    const uint2 xs = *reinterpret_cast<const uint2*>(&pcs[par][idx]);
+                    const uint2 xq = *reinterpret_cast<const uint2*>(&pcq[par][idx]);
+                    hs[0] = xs.x; hs[1] = xs.y;
+                    hq[0] = xq.x; hq[1] = xq.y;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < W; ++j) {
+                    hs[j] = pcs[par][idx + j];
+                    hq[j] = pcq[par][idx + j];
+                }
+            }
+            const size_t k = size_t(r) * ec + cbase;
+            const int nout = min(W, ec - cbase);
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                // + warp totals between this warp and the warp holding PC(c + n + j)
+                const int wj = (idx + j) >> TSH;
+                unsigned S = hs[j] - own_s[j], Qs = hq[j] - own_q[j];
+                for (int w = wid; w < wj; ++w) {
+                    S += wts[par][w];
+                    Qs += wtq[par][w];
+                }
+                double mu, om;
+                uint8_t fl;
+                window_epilogue(double(S), double(Qs), inv_mn, mn, prefix_noise, mu, om, fl);
+                if (j < nout) {
+                    st.mu[k + j] = mu;
+                    st.omega[k + j] = om;
+                    st.flat[k + j] = fl;
+                }
+            }
+        }
+        par ^= 1;
+        if (++r >= r1) break;
+        lead += P;
+        trail += P;
+        // slide: + leading row, - trailing row (packed lanes stay in [0, 2^16))
+        {
+            unsigned ei, oi, eo, oo;
+            lanes(vi, ei, oi);
+            lanes(vo, eo, oo);
+            s02 += ei;
+            s13 += oi;
+            s02 -= eo;
+            s13 -= oo;
+        }
+#pragma unroll
+        for (int j = 0; j < W; ++j) {
+            const unsigned ij = (vi >> (8 * j)) & 0xffu, oj = (vo >> (8 * j)) & 0xffu;
+            qq[j] += ij * ij - oj * oj;
+        }
+    }
+}
+
 }  // namespace
+
+bool window_stats4_supported(int p, int q, int m, int n, int pitch) {
+    const int ec = q - n + 1, er = p - m + 1;
+    return er >= 1 && ec >= 1 && pitch % 16 == 0 && m <= 255 &&
+           double(m) * double(n) * 65025.0 < 4294967296.0 && (n + 1) / 2 <= 64;
+}
+
+template <int NT, int W>
+cudaError_t launch_wstats4(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
+                           const double* prefix_noise, DevStats st, cudaStream_t s) {
+    const int ec = q - n + 1, er = p - m + 1;
+    const int G = NT - (n + W - 1) / W;  // output blocks per tile (PC(c + n) stays in the tile)
+    const int ntiles = (ec + W * G - 1) / (W * G);
+    // one wave of resident CTAs: a segment's m-row warm-up (~15 instructions a row) is small
+    // next to its output rows, so short segments beyond one wave only add tail
+    static int resident = 0;
+    if (!resident &&
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, k_wstats4<NT, W>, NT, 0) != cudaSuccess)
+        resident = 2;
+    resident = std::max(resident, 1);
+    int nseg = std::max(1, (148 * resident) / ntiles);
+    int seg = std::max(4, (er + nseg - 1) / nseg);
+    nseg = (er + seg - 1) / seg;
+    dim3 grid(ntiles, nseg);
+    launch_pdl(k_wstats4<NT, W>, grid, dim3(NT), 0, s, imgp, pitch, p, q, m, n, G, seg,
+               prefix_noise, st);
+    return cudaGetLastError();
+}
+
+// CTA shape: 256 threads x 2 columns (default; C2 36.5 us vs 46 us for one column per
+// thread and 61 us for four, whose four serial FP64 epilogues per row leave too few warps
+// to hide their latency).  TMATCH_WSTATS4=256x4|128x4|128x2 for A/B measurements.
+int wstats4_variant() {
+    static int v = [] {
+        const char* e = std::getenv("TMATCH_WSTATS4");
+        if (!e) return 2;
+        if (!std::strcmp(e, "256x4")) return 0;
+        if (!std::strcmp(e, "128x4")) return 1;
+        if (!std::strcmp(e, "128x2")) return 3;
+        return 2;
+    }();
+    return v;
+}
+
+cudaError_t window_stats4_u8(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
+                             const double* prefix_noise, DevStats st, cudaStream_t s) {
+    switch (wstats4_variant()) {
+        case 1: return launch_wstats4<128, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
+        case 2: return launch_wstats4<256, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
+        case 3: return launch_wstats4<128, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
+        default: return launch_wstats4<256, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
+    }
+}
 
 cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s) {

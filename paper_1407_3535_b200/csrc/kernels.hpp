@@ -81,6 +81,9 @@ cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, d
 
 // ---- window statistics, exact integer path (stats.cpp:55-94) ---------------------------
 // hs/hq scratch: p * ec int32 each.
+bool window_stats4_supported(int p, int q, int m, int n, int pitch);
+cudaError_t window_stats4_u8(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
+                             const double* prefix_noise, DevStats st, cudaStream_t s);
 cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n,
                             const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s);
