@@ -488,6 +488,22 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// The member bound test of scan 2, tb >= RN(RN(a*b) + RN(sa * RN(sqrt(x)))) with
+// x = RN(1 - RN(b*b)) in [0, 1] and sa in [0, 1] (bounds.cpp:21-23, 41-46), decided from an
+// FP32 square root (sqrt.approx.f32: relative error < 2^-21 after the conversions) unless
+// tb lies within 4e-6 of the approximate bound: the exact bound differs from it by at most
+// sa * |sqrt(x) - approx| + a few FP64 ulps < 1e-6, so outside that band the decision is
+// the exact one; inside it the exact FP64 expression decides.
+__device__ __forceinline__ bool sec_test_fast(double tb, double a, double b, double sa, double x) {
+    float sf;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(sf) : "f"(__double2float_rn(x)));
+    const double ab = __dmul_rn(a, b);
+    const double approx = __dadd_rn(ab, __dmul_rn(sa, double(sf)));
+    if (tb >= __dadd_rn(approx, 4e-6)) return true;
+    if (tb < __dsub_rn(approx, 4e-6)) return false;
+    return tb >= __dadd_rn(ab, __dmul_rn(sa, __dsqrt_rn(x)));
+}
+
 // Scan 2 over explicit extent rows: row-level quantities (group row, centre row) once per
 // row, the centre's half_gap factor sa precomputed per group (k_sqrt_gap, same
 // operations as half_gap), so a member costs one FastDiv, its own square root and the
@@ -538,8 +554,8 @@ __global__ void __launch_bounds__(256)
                         if (elim) {
                             const double a = dclamp(ra, -1.0, 1.0);
                             const double b = dclamp(mv, -1.0, 1.0);
-                            const double sb = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b))));
-                            elim = tb >= __dadd_rn(__dmul_rn(a, b), __dmul_rn(sa, sb));
+                            const double x = dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b)));
+                            elim = sec_test_fast(tb, a, b, sa, x);
                         }
                         if (elim) {
                             ++n_elim;
