@@ -327,46 +327,67 @@ def run_b200(args):
         return 0
 
     # ---- roofline of the dominant kernel ---------------------------------------------
-    # The step's dominant kernel is the fused R_co kernel k_acf (EGS candidates).  Its
-    # algorithmic HBM traffic per evaluated candidate: the 8-bit image once (p*q bytes),
-    # the member statistics (mu, omega, flat: 17 B per extent location) and the R_co map
-    # write (8 B per location).  Candidates after the first rejection exit at entry.
+    # R_co of the EGS candidates is the dominant phase.  Its full-work launch is the first
+    # candidate (h0, always accepted): the group-column kernel k_acg<3> reads the 8-bit
+    # image once (p*q bytes), the centre/member statistics (mu, omega, flat: 17 B per extent
+    # location) and writes the R_co map (8 B per location).  Later candidates run in
+    # count-only mode and stop at the EGS rejection point (data-dependent work): they are
+    # reported beside it with their measured time.
     peaks = _peaks()
     p_, q_ = wl.image.shape
     E = wl.extent
-    n_cand = len(info.get("egs_trace", [])) + 1
-    ac = phases.get("autocorr_u8", {"count": 0, "ms": float("nan")})
-    ac_bytes = n_cand * (p_ * q_ + 25.0 * E)
     hbm_peak = peaks.get("hbm_gbs", 6534.1)
-    ac_gbs = ac_bytes / (ac["ms"] / 1e3) / 1e9
-    traffic = None  # DRAM read+write per k_acf launch from the committed ncu --set full capture
+    ph_step = max(sum(v["ms"] for v in phases.values()), 1e-9)
+    ac = phases.get("autocorr_u8", {"count": 1, "ms": float("nan")})
+    ac_launch_ms = ac["ms"] / max(ac["count"], 1)
+    ac_bytes = p_ * q_ + 25.0 * E
+    ac_gbs = ac_bytes / (ac_launch_ms / 1e3) / 1e9
+    traffic = None  # DRAM read+write of that launch from the committed ncu --set full capture
+    traffic_src = os.path.join("profiles", "r01_kernel_traffic.json")
     try:
-        kt = json.load(open(os.path.join(ROOT, "profiles", "r01_kernel_traffic.json")))["kernels"]
-        acf = [v for k, v in kt.items() if "k_acf" in k and v["duration_us"] > 10.0]
-        if acf:
-            traffic = sum(v["dram_read_bytes"] + v["dram_write_bytes"] for v in acf) / len(acf)
+        kt = json.load(open(os.path.join(ROOT, traffic_src)))["kernels"]
+        hit = [v for k, v in kt.items() if "k_acg<3" in k]
+        if hit:
+            traffic = hit[0]["dram_read_bytes"] + hit[0]["dram_write_bytes"]
     except Exception:
         traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_acf<H> (fused sliding-window R_co, EGS)",
+    roofline = {"bound": "hbm", "kernel": "k_acg<3,256> (group-column fused R_co, first EGS "
+                "candidate: full map + retained count)",
                 "achieved": ac_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ac_gbs / hbm_peak,
-                "traffic": traffic, "traffic_unit": "bytes per launch (profiles/r01_kernel_traffic.json)",
-                "algorithmic_bytes_per_launch": ac_bytes / max(n_cand, 1),
+                "traffic": traffic, "traffic_unit": f"bytes per launch ({traffic_src})",
+                "algorithmic_bytes_per_launch": ac_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
-                "algorithmic": f"{n_cand} candidates x (p*q + 25 B x {E} locations)",
-                "kernel_ms": ac["ms"],
-                "share_of_step": ac["ms"] / max(sum(v["ms"] for v in phases.values()), 1e-9)}
-    # secondary: the tensor-core centre scan (tcgen05 kind::i8), useful ops only
+                "algorithmic": f"p*q + 25 B x {E} extent locations (image, 17 B statistics "
+                               "read, 8 B map write)",
+                "kernel_ms": ac_launch_ms, "share_of_step": ac["ms"] / ph_step}
+    sec = []
+    cnt = phases.get("autocorr_count")
+    if cnt:
+        sec.append({"bound": "issue", "kernel": "k_acg<5,128> count-only EGS candidate "
+                    "(stops when the partial retained count rejects the size)",
+                    "kernel_ms": cnt["ms"], "share_of_step": cnt["ms"] / ph_step})
+    wsp = phases.get("window_stats")
+    if wsp:
+        ws_bytes = p_ * q_ + 17.0 * E
+        ws_gbs = ws_bytes / (wsp["ms"] / 1e3) / 1e9
+        sec.append({"bound": "hbm", "kernel": "k_wstats4<256,2> (window statistics)",
+                    "achieved": ws_gbs, "peak": hbm_peak, "unit": "GB/s",
+                    "frac": ws_gbs / hbm_peak, "algorithmic": f"p*q + 17 B x {E} locations",
+                    "kernel_ms": wsp["ms"], "share_of_step": wsp["ms"] / ph_step})
+    # the tensor-core centre scan (tcgen05 kind::i8), useful ops only
     G = res.centers
     cs = phases.get("centre_scan", {"count": 1, "ms": float("nan")})
     i8_peak = 2.0 * peaks.get("bf16_tflops", 1649.1)
     cs_tops = 2.0 * m * n * G / (cs["ms"] / 1e3) / 1e12
-    roofline["secondary"] = [{
-        "bound": "tensor", "kernel": "k_tc_corr<1> + k_centre_epi (centre scan, tcgen05 kind::i8)",
+    sec.append({
+        "bound": "tensor", "kernel": "k_tc_build_b + k_tc_corr<1> + k_centre_epi (centre scan, "
+                                     "tcgen05 kind::i8)",
         "achieved": cs_tops, "peak": i8_peak, "unit": "TOP/s", "frac": cs_tops / i8_peak,
         "peak_source": "2 x MEASURED_PEAKS.json bf16_tflops (i8 MMA: K=32 per instruction "
                        "vs K=16 for bf16 at the same issue rate)",
         "algorithmic": f"2*m*n useful ops per centre x {G} centres (phase time incl. B build "
-                       "and FP64 epilogue)", "kernel_ms": cs["ms"]}]
+                       "and FP64 epilogue)", "kernel_ms": cs["ms"]})
+    roofline["secondary"] = sec
 
     cpu = None
     if not args.no_cpu_baseline:

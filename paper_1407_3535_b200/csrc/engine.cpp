@@ -274,7 +274,7 @@ struct tm_ctx {
         tmk::GridDesc g{};
         const int* rows_dev = nullptr;
     } spec;
-    std::map<std::vector<long long>, int> last_he;  // (p, q, m, n, h0) -> last accepted h
+    std::map<std::vector<long long>, int> last_he;  // (p, q, m, n, h0, w0) -> last accepted h
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -982,6 +982,7 @@ void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const 
     task.out_rho = ctx->dotbuf.p;
     task.gate = reinterpret_cast<const int*>(ctx->counters.p + 24);
     const int* rows_dev = nullptr;
+    Phase ph(ctx, "centre_scan");
     tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
     ctx->spec.armed = true;
     ctx->spec.g = g;
@@ -999,7 +1000,10 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
                      bool count_only = false) {
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     if (!egs_prev) CK(cudaMemsetAsync(nr, 0, 8, ctx->s));  // EGS batches: egs_init zeroes it
-    Phase ph(ctx, img->integer ? "autocorr_u8" : "autocorr_replica");
+    // (count-only candidates are timed apart: their work stops at the EGS rejection point)
+    const bool fused_count = count_only && img->integer && ctx->ac_fused &&
+                             tmk::autocorr_fused_supported(ws.m, ws.n, g);
+    Phase ph(ctx, !img->integer ? "autocorr_replica" : fused_count ? "autocorr_count" : "autocorr_u8");
     if (img->integer) {
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
@@ -1139,10 +1143,16 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     unsigned long long* dgate = dgate_u64;
     int* dhacc = reinterpret_cast<int*>(ctx->counters.p + 25);
     bool first_batch = true;
-    // Only the accepted size's map is used: the first candidate (always accepted) writes its
-    // map, later candidates count only, and a size accepted without a map is recomputed once
-    // after the loop (its count re-derived and checked).
+    // Only the accepted size's map is used: the predicted h_e (the last one seen for this
+    // image / template shape, else h0) writes its map, the other candidates count only, and
+    // a size accepted without a map is recomputed once after the loop (count re-checked).
     int map_h = -1, map_w = -1;
+    const std::vector<long long> he_key = {img->p, img->q, m, n, h0, w0};
+    int pred = h0;
+    if (h0 == w0) {
+        const auto it = ctx->last_he.find(he_key);
+        if (it != ctx->last_he.end()) pred = it->second;
+    }
     while (!done) {
         struct Cand {
             int h, w;
@@ -1168,7 +1178,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             ctx->egs_maps[k].ensure(E);
             map_written[k] = autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p,
                                              ctx->counters.p + 8 + k, dstop, dprev, xi,
-                                             /*count_only=*/!(cand[k].h == h0 && cand[k].w == w0));
+                                             /*count_only=*/!(cand[k].h == pred && cand[k].w == pred));
             // (after the last candidate too: the speculation gate needs the final decision)
             CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
                                cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s));
@@ -1222,6 +1232,10 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
                                            best.p);
         if (n_r != out.cost.retained)
             throw TmError{TM_ECUDA, "efficient_group_size: map recount mismatch"};
+    }
+    if (h0 == w0 && out.h == out.w) {
+        if (ctx->last_he.size() > 256) ctx->last_he.clear();
+        ctx->last_he[he_key] = out.h;
     }
     return out;
 }
@@ -2346,7 +2360,7 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
         // centre scan is enqueued behind the first EGS batch, gated on the device decision,
         // so the device does not idle while the host reads the counts.
         const bool egs = params->mode != TM_MODE_OPTA && params->h0 == params->w0;
-        const std::vector<long long> key = {img->p, img->q, m, n, params->h0};
+        const std::vector<long long> key = {img->p, img->q, m, n, params->h0, params->w0};
         int want = 0;
         if (egs && img->integer && m <= img->p && n <= img->q) {
             const auto it = ctx->last_he.find(key);
@@ -2369,8 +2383,7 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
             ctx->spec.armed = false;
             throw;
         }
-        ctx->spec_want = 0;
-        if (egs) ctx->last_he[key] = prep->h;
+        ctx->spec_want = 0;  // (run_egs_search recorded h_e for the next prediction)
         prep->ctx = nullptr;  // internal: not counted as a context reference
         if (!uploaded) T = upload_template(ctx, tmpl, m, n);
         *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);

@@ -1208,15 +1208,14 @@ AcgGeom acg_geom(int m, int n, GridDesc gd, int nt, int resident = 0) {
     a.nt = nt;
     a.G = G;
     a.ntiles = (gd.tc + G - 1) / G;
+    // Exactly one wave of resident CTAs, segments as short as that needs: every CTA has the
+    // same work (equal segments), so the critical path is one segment's m-row warm-up plus
+    // its events, and the EGS early rejection reaches all CTAs at the same fraction of work.
     const int rows = gd.ti_hi - gd.ti_lo;
-    const int seg_min = std::max(1, (m + gd.h - 1) / gd.h);
     if (resident <= 0) resident = std::max(1, 1024 / nt);
     const int slots = 148 * resident;
     const int per_wave = std::max(1, slots / std::max(1, gd.w * a.ntiles));
-    const int seg_1 = (rows + per_wave - 1) / per_wave;
-    const int waves = std::min(4, std::max(1, (seg_1 + 4 * seg_min - 1) / (4 * seg_min)));
-    int nseg = std::max(1, waves * per_wave);
-    nseg = std::min(nseg, std::max(1, (rows + seg_min - 1) / seg_min));
+    const int nseg = std::max(1, std::min(per_wave, rows));
     a.seg = std::max(1, (rows + nseg - 1) / nseg);
     a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
     return a;

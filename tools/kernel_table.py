@@ -41,6 +41,7 @@ def rows(rep):
                 break
         out.append({
             "kernel": d.get("Kernel Name", "?").split("(")[0].replace("void ", "").split("::")[-1],
+            "dram_read_bytes": rd, "dram_write_bytes": wr,
             "us": dur * 1e6 if dur else None,
             "dram_MB": (rd + wr) / 1e6,
             "dram_GBps": (rd + wr) / dur / 1e9 if dur else None,
@@ -54,6 +55,15 @@ def rows(rep):
 
 
 if __name__ == "__main__":
+    if sys.argv[1] == "--json":  # --json OUT REP: per-launch DRAM traffic for bench.py
+        out, rep = sys.argv[2], sys.argv[3]
+        ks = {f"{i}:{r['kernel']}": {"dram_read_bytes": r["dram_read_bytes"],
+                                    "dram_write_bytes": r["dram_write_bytes"],
+                                    "duration_us": r["us"]} for i, r in enumerate(rows(rep))}
+        json.dump({"source": f"ncu --set full --clock-control none, tools/prof_search.py C2 "
+                             f"({os.path.basename(rep)}); cold caches (ncu flushes between "
+                             "replays)", "kernels": ks}, open(out, "w"), indent=1)
+        sys.exit(0)
     for rep in sys.argv[1:]:
         print(f"## {os.path.basename(rep)}")
         print("| kernel | time (us) | DRAM MB | DRAM GB/s | of HBM peak | tensor pipe % | issue % | occupancy % |")
