@@ -776,6 +776,32 @@ void reduce_to(tm_ctx* ctx, int n, int slot, const tmk::ReduceOp* op = nullptr) 
     ctx->add(1);
 }
 
+// Scan 1's reduction op: the threshold bootstrap (matcher.cpp:121-125) plus the zeroing of
+// the seeding counters and the scan-2 tally.
+tmk::ReduceOp centre_op(tm_ctx* ctx, const tm_match_params& P) {
+    tmk::ReduceOp op{};
+    op.kind = 1;
+    op.has_init = P.has_init_threshold;
+    op.init = P.init_threshold;
+    op.thr = ctx->thr.p;
+    op.zero64 = ctx->counters.p + 4;
+    op.nzero64 = 2;
+    op.zero_tally = ctx->tally.p;
+    return op;
+}
+
+// The same reduction fused into the tail of the kernel that writes the phase's last
+// partials (partials[0, n) -> cells[slot], then op).
+tmk::TailReduce tail_to(tm_ctx* ctx, int n, int slot, const tmk::ReduceOp* op = nullptr) {
+    tmk::TailReduce t;
+    t.partials = ctx->partials.p;
+    t.n = n;
+    t.out = ctx->cells.p + slot;
+    t.ticket = reinterpret_cast<unsigned*>(ctx->counters.p + 26);
+    if (op) t.op = *op;
+    return t;
+}
+
 // Evaluate a device location list (count on device) -> cells[slot].
 void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const int2* locs,
                const unsigned long long* count, int max_count, double* out_rho,
@@ -783,12 +809,15 @@ void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const in
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
     ctx->partials.ensure(kListBlocks);
     Phase ph(ctx, slot == 1 ? "seed_eval" : (slot == 2 ? "survivor_eval" : "list_eval"));
-    if (fp32_path(img, T))
+    if (fp32_path(img, T)) {  // reduction fused into the list kernel's tail
+        const tmk::TailReduce tail = tail_to(ctx, kListBlocks, slot, op);
         CK(tmk::corr_list(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
+                          kListBlocks, ctx->s, 0, &tail));
+        ctx->add(1);
+        return;
+    }
+    CK(tmk::corr_list_f64(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
                           kListBlocks, ctx->s));
-    else
-        CK(tmk::corr_list_f64(job, locs, count, max_count, out_rho, out_deg, ctx->partials.p,
-                              kListBlocks, ctx->s));
     ctx->add(1);
     reduce_to(ctx, kListBlocks, slot, op);
 }
@@ -835,20 +864,20 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             // already enqueued behind the EGS batch (tm_search) and confirmed by the device
             // decision for this grid: the dots are in flight, skip the launches
             const auto& sp = ctx->spec;
-            if (sp.armed && sp.g.er == g.er && sp.g.ec == g.ec && sp.g.h == g.h && sp.g.w == g.w &&
-                sp.g.ti_lo == g.ti_lo && sp.g.ti_hi == g.ti_hi && ctx->hres->spec == 1)
-                rows_dev = sp.rows_dev;
-            else
-                tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+            const bool hit = sp.armed && sp.g.er == g.er && sp.g.ec == g.ec && sp.g.h == g.h &&
+                             sp.g.w == g.w && sp.g.ti_lo == g.ti_lo && sp.g.ti_hi == g.ti_hi &&
+                             ctx->hres->spec == 1;
             ctx->spec.armed = false;
+            if (hit) return;  // dots, epilogue and its reduction are already in flight
+            tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
+            const tmk::TailReduce tail = tail_to(ctx, n1 + n2, 0, op);  // n2 = 0 here
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
-                                    task.c_last));
+                                    task.c_last, &tail));
             HT("centre_epi");
             ctx->add(1);
         }
-        reduce_to(ctx, n1 + n2, 0, op);
         return;
     }
     if (fp32_path(img, T) && (g.w == 1 || g.w == 3 || g.w == 5 || g.w == 7)) {
@@ -958,7 +987,8 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // predicted group size, enqueued behind an EGS batch and gated on the device decision
 // (k_egs_decide: EGS finished with h_e == predicted).  On a wrong prediction both kernels
 // exit at entry and centre_scan launches the real ones.
-void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const tmk::GridDesc& g) {
+void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const tmk::GridDesc& g,
+                 const tm_match_params& P) {
     ctx->spec.armed = false;
     if (!(tc_path(ctx, img, T) && g.h <= tmk::kTcMaxClasses) || g.ti_hi <= g.ti_lo) return;
     const size_t G = size_t(g.tr) * g.tc;
@@ -984,6 +1014,14 @@ void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const 
     const int* rows_dev = nullptr;
     Phase ph(ctx, "centre_scan");
     tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+    // the epilogue + scan 1's reduction (the same op search() would use), same gate
+    const int n1 = std::min(kListBlocks, int((size_t(g.ti_hi - g.ti_lo) * g.tc + 255) / 256));
+    const tmk::ReduceOp op = centre_op(ctx, P);
+    const tmk::TailReduce tail = tail_to(ctx, n1, 0, &op);
+    CK(tmk::centre_epilogue(make_job(ctx, img, ws, T), g, rows_dev, g.w / 2, g.w, g.tc, 0,
+                            ctx->dotbuf.p, ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
+                            task.c_last, &tail, task.gate));
+    ctx->add(1);
     ctx->spec.armed = true;
     ctx->spec.g = g;
     ctx->spec.rows_dev = rows_dev;
@@ -1139,8 +1177,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
     // is going to ignore (after the first rejection) exit at entry instead of running.
     double* dprev = reinterpret_cast<double*>(ctx->counters.p + 20);
     int* dstop = reinterpret_cast<int*>(ctx->counters.p + 21);
-    unsigned long long* dgate_u64 = ctx->counters.p + 24;  // speculation gate (tm_search)
-    unsigned long long* dgate = dgate_u64;
+    unsigned long long* dgate = ctx->counters.p + 24;  // speculation gate (tm_search)
     int* dhacc = reinterpret_cast<int*>(ctx->counters.p + 25);
     bool first_batch = true;
     // Only the accepted size's map is used: the predicted h_e (the last one seen for this
@@ -1159,7 +1196,10 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         } cand[4];
         int nc = 0;
         int hh = h, ww = w;
-        for (; nc < 4;) {
+        // first batch: up to one size past the predicted h_e (a misprediction costs another
+        // batch); later batches: four
+        const int nmax = first_batch ? std::max(2, std::min(4, (pred - h) / 2 + 2)) : 4;
+        for (; nc < nmax;) {
             cand[nc++] = Cand{hh, ww};
             if ((hh >= er && ww >= ec) || (hh >= cap && ww >= cap)) break;
             hh = std::min(hh + 2, cap);
@@ -1179,16 +1219,16 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             map_written[k] = autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p,
                                              ctx->counters.p + 8 + k, dstop, dprev, xi,
                                              /*count_only=*/!(cand[k].h == pred && cand[k].w == pred));
-            // (after the last candidate too: the speculation gate needs the final decision)
+            // (after the last candidate too: the speculation gate needs the final decision,
+            // and that decide also writes the counts + gate into the mapped pinned block)
+            const bool last = k + 1 == nc;
             CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
-                               cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s));
+                               cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
+                               ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr));
             ctx->add(1);
         }
-        // counts (and the gate) straight into the mapped pinned block; the host waits for
-        // this point only, so work enqueued by the hook keeps the device busy meanwhile
-        CK(tmk::copy_u64(ctx->counters.p + 8, ctx->hres_dev->nr, nc, ctx->s, dgate_u64,
-                         &ctx->hres_dev->spec));
-        ctx->add(1);
+        // the host waits for this point only, so work enqueued by the hook keeps the device
+        // busy meanwhile
         CK(cudaEventRecord(ctx->ev_egs, ctx->s));
         if (before_sync && *before_sync) {  // host work overlapped with the candidates
             (*before_sync)();
@@ -1499,16 +1539,17 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         np = tc_run(ctx, img, ws, T, rs, 1, task);
     }
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
-    CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
-                      nullptr, ctx->partials.p + np, kListBlocks, s, 1));
-    ctx->add(2);
     tmk::ReduceOp op_pack{};  // the final reduction packs the result into pinned host memory
     op_pack.kind = 3;
     op_pack.cells = ctx->cells.p;
     op_pack.tally = ctx->tally.p;
     op_pack.thr = ctx->thr.p;
     op_pack.packed = ctx->hres_dev;
-    reduce_to(ctx, np + kListBlocks, 2, &op_pack);
+    // fused into the list kernel's tail: the tensor-core partials [0, np) are already in
+    const tmk::TailReduce tail = tail_to(ctx, np + kListBlocks, 2, &op_pack);
+    CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
+                      nullptr, ctx->partials.p + np, kListBlocks, s, 1, &tail));
+    ctx->add(2);
 }
 
 tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
@@ -1531,14 +1572,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     HT("search_begin");
     // the centre reduction also bootstraps the threshold (matcher.cpp:121-125) and zeroes
     // the seeding counters and the scan-2 tally
-    tmk::ReduceOp op_init{};
-    op_init.kind = 1;
-    op_init.has_init = P.has_init_threshold;
-    op_init.init = P.init_threshold;
-    op_init.thr = ctx->thr.p;
-    op_init.zero64 = ctx->counters.p + 4;
-    op_init.nzero64 = 2;
-    op_init.zero_tally = ctx->tally.p;
+    const tmk::ReduceOp op_init = centre_op(ctx, P);
     centre_scan(ctx, img, ws, T, g, &op_init);
     HT("centre_scan");
 
@@ -1963,6 +1997,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         CK(cudaEventCreateWithFlags(&ctx->ev_t, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_egs, cudaEventDisableTiming));
         ctx->counters.ensure(32);
+        CK(cudaMemsetAsync(ctx->counters.p, 0, 32 * sizeof(unsigned long long), ctx->s));
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
         ctx->tally.ensure(1);
@@ -2373,7 +2408,7 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
             uploaded = true;
             if (want > 0)
                 spec_centre(ctx, img, get_ws(ctx, img, m, n),
-                            T, make_grid(img->p - m + 1, img->q - n + 1, want, want));
+                            T, make_grid(img->p - m + 1, img->q - n + 1, want, want), *params);
         };
         std::unique_ptr<tm_prep> prep;
         try {

@@ -1486,32 +1486,39 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 // in-kernel rejection; either way the gate is final.
 __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
                              int ec, int h, int w, double xi, int cap, int* h_acc, int want,
-                             unsigned long long* gate) {
+                             unsigned long long* gate, const unsigned long long* nr_all, int nc,
+                             ResultBlock* out) {
     pdl_wait();
-    if (*stop) {
-        *gate = (want > 0 && *h_acc == want) ? 1ull : 0ull;
-        return;
+    if (!*stop) {
+        const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
+        const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
+        const double prev = *prev_cost;
+        const bool first = !(fabs(prev) <= 1.7976931348623157e308);  // !isfinite
+        const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(xi, prev);
+        if (!accepted) {
+            *stop = 1;
+        } else {
+            *prev_cost = total;
+            *h_acc = h;
+            if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
+        }
     }
-    const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
-    const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
-    const double prev = *prev_cost;
-    const bool first = !(fabs(prev) <= 1.7976931348623157e308);  // !isfinite
-    const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(xi, prev);
-    if (!accepted) {
-        *stop = 1;
-    } else {
-        *prev_cost = total;
-        *h_acc = h;
-        if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
+    // (a stop set at entry came from an earlier decision or from the candidate's own
+    // in-kernel rejection; either way h_acc is final)
+    const unsigned long long gv = (*stop && want > 0 && *h_acc == want) ? 1ull : 0ull;
+    *gate = gv;
+    if (out) {  // last candidate of the batch: counts + gate into the mapped result block
+        for (int i = 0; i < nc; ++i) out->nr[i] = nr_all[i];
+        out->spec = gv;
     }
-    *gate = (*stop && want > 0 && *h_acc == want) ? 1ull : 0ull;
 }
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
-                       unsigned long long* gate, cudaStream_t s) {
+                       unsigned long long* gate, cudaStream_t s, const unsigned long long* nr_all,
+                       int nc, ResultBlock* out) {
     launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap,
-               h_acc, want, gate);
+               h_acc, want, gate, nr_all, nc, out);
     return cudaGetLastError();
 }
 

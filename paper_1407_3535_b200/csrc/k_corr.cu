@@ -198,12 +198,15 @@ __global__ void __launch_bounds__(NW * 32)
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.y * gridDim.x + blockIdx.x);
 }
 
+__device__ void tail_reduce(const TailReduce& tr, Cell* scratch);
+
 // Epilogue of a K-split centre scan: rho/deg per group from the accumulated dots.
 __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
-                 CellH* partials, int c_last) {
+                 CellH* partials, int c_last, TailReduce tail, const int* __restrict__ gate) {
     pdl_wait();
+    if (gate && !*gate) return;  // speculative launch not confirmed (every block: no ticket)
     __shared__ Cell scratch[8];
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
@@ -226,6 +229,7 @@ __global__ void __launch_bounds__(256)
     }
     best = block_best(best, scratch);
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+    tail_reduce(tail, scratch);
 }
 
 // ---- sparse: one warp per location ----------------------------------------------------
@@ -234,7 +238,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     k_corr_list(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                 int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                int lane_flush, int rho_by_loc) {
+                int lane_flush, int rho_by_loc, TailReduce tail) {
     pdl_wait();
     // One CTA per location (grid-stride): warp w owns template rows [w*m/8, (w+1)*m/8), so
     // a location costs one or two batches of independent loads per warp instead of m/8
@@ -294,6 +298,7 @@ __global__ void __launch_bounds__(256)
     }
     best = block_best(best, scratch);
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+    tail_reduce(tail, scratch);
 }
 
 // ---- FP64 replica (non-integer images / templates) --------------------------------------
@@ -379,6 +384,27 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---- reductions -----------------------------------------------------------------------
+// The best cell of a phase -> *out, then the phase's follow-up (thread 0).
+__device__ void apply_reduce_op(const Cell& best, CellH* out, const ReduceOp& op) {
+    const CellH b{best.rho, best.row, best.col, best.flags};
+    out[0] = b;
+    if (op.kind == 1) {  // k_threshold_init + the zeroing the search needs next
+        double t = -INFINITY;
+        if ((b.flags & 1) && !(b.flags & 2)) t = b.rho;
+        if (op.has_init) t = dmax(t, dclamp(op.init, -1.0, 1.0));
+        *op.thr = t;
+        for (int i = 0; i < op.nzero64; ++i) op.zero64[i] = 0ull;
+        if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull};
+    } else if (op.kind == 2) {  // k_threshold_raise
+        if ((b.flags & 1) && !(b.flags & 2) && b.rho > *op.thr) *op.thr = b.rho;
+    } else if (op.kind == 3) {  // result block for one device->host copy
+        for (int i = 0; i < 3; ++i) op.packed->cells[i] = op.cells[i];
+        op.packed->cells[2] = b;  // this reduction's own slot (cells[2])
+        op.packed->tally = *op.tally;
+        op.packed->thr = *op.thr;
+    }
+}
+
 __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH* out, ReduceOp op) {
     pdl_wait();
     __shared__ Cell scratch[32];
@@ -389,24 +415,32 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
         if (better(c, best)) best = c;
     }
     best = block_best(best, scratch);
+    if (threadIdx.x == 0) apply_reduce_op(best, out, op);
+}
+
+// Fused tail reduction (TailReduce): called by every thread of every block after the
+// block's partial is stored.  The last block to take a ticket reads all partials through
+// L2 (other SMs wrote them) and finishes the phase like k_reduce_cells.
+__device__ void tail_reduce(const TailReduce& tr, Cell* scratch) {
+    if (!tr.ticket) return;  // uniform
+    __shared__ int is_last;
+    if (threadIdx.x == 0) {  // thread 0 stored this block's partial: publish it, take a ticket
+        __threadfence();
+        is_last = atomicAdd(tr.ticket, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (!is_last) return;
+    __threadfence();
+    Cell best = no_cell();
+    for (int i = threadIdx.x; i < tr.n; i += blockDim.x) {
+        const CellH* h = tr.partials + i;
+        const Cell c{__ldcg(&h->rho), __ldcg(&h->row), __ldcg(&h->col), __ldcg(&h->flags)};
+        if (better(c, best)) best = c;
+    }
+    best = block_best(best, scratch);
     if (threadIdx.x == 0) {
-        const CellH b{best.rho, best.row, best.col, best.flags};
-        out[0] = b;
-        if (op.kind == 1) {  // k_threshold_init + the zeroing the search needs next
-            double t = -INFINITY;
-            if ((b.flags & 1) && !(b.flags & 2)) t = b.rho;
-            if (op.has_init) t = dmax(t, dclamp(op.init, -1.0, 1.0));
-            *op.thr = t;
-            for (int i = 0; i < op.nzero64; ++i) op.zero64[i] = 0ull;
-            if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull};
-        } else if (op.kind == 2) {  // k_threshold_raise
-            if ((b.flags & 1) && !(b.flags & 2) && b.rho > *op.thr) *op.thr = b.rho;
-        } else if (op.kind == 3) {  // result block for one device->host copy
-            for (int i = 0; i < 3; ++i) op.packed->cells[i] = op.cells[i];
-            op.packed->cells[2] = b;  // this reduction's own slot (cells[2])
-            op.packed->tally = *op.tally;
-            op.packed->thr = *op.thr;
-        }
+        apply_reduce_op(best, tr.out, tr.op);
+        *tr.ticket = 0u;
     }
 }
 
@@ -786,11 +820,11 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
 
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                      int n_partials, cudaStream_t s, int rho_by_loc) {
+                      int n_partials, cudaStream_t s, int rho_by_loc, const TailReduce* tail) {
     // one FP32 partial covers lane_flush rows of one template column: < 2^24 exactly
     const int lane_flush = int(16777216LL / 65025LL);
-    launch_pdl(k_corr_list, dim3(n_partials), dim3(256), 0, s, job, locs, count, max_count, out_rho, out_deg,
-                                           partials, lane_flush, rho_by_loc);
+    launch_pdl(k_corr_list, dim3(n_partials), dim3(256), 0, s, job, locs, count, max_count,
+               out_rho, out_deg, partials, lane_flush, rho_by_loc, tail ? *tail : TailReduce{});
     return cudaGetLastError();
 }
 
@@ -825,9 +859,10 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
 
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
-                            CellH* partials, int n_partials, cudaStream_t s, int c_last) {
-    launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw, nc, col0, dot, rho_c,
-                                            deg_c, partials, c_last);
+                            CellH* partials, int n_partials, cudaStream_t s, int c_last,
+                            const TailReduce* tail, const int* gate) {
+    launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw,
+               nc, col0, dot, rho_c, deg_c, partials, c_last, tail ? *tail : TailReduce{}, gate);
     return cudaGetLastError();
 }
 

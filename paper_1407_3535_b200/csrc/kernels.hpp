@@ -66,6 +66,17 @@ struct ReduceOp {
     ResultBlock* packed = nullptr;
 };
 
+// A reduction fused into the tail of the kernel producing the last partials of a phase: the
+// block that finishes last reduces partials[0, n) (earlier kernels' included) into *out and
+// applies op -- k_reduce_cells without its own launch.  ticket: zero between launches.
+struct TailReduce {
+    const CellH* partials = nullptr;
+    int n = 0;
+    CellH* out = nullptr;
+    unsigned* ticket = nullptr;  // null: no fused reduction
+    ReduceOp op{};
+};
+
 // ---- image preparation ---------------------------------------------------------------
 cudaError_t check_u8_domain(const double* img, size_t n, int* bad, cudaStream_t s);
 cudaError_t f64_to_u8(const double* img, size_t n, uint8_t* out, cudaStream_t s);
@@ -142,7 +153,9 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
-                       unsigned long long* gate, cudaStream_t s);
+                       unsigned long long* gate, cudaStream_t s,
+                       const unsigned long long* nr_all = nullptr, int nc = 0,
+                       ResultBlock* out = nullptr);
 // Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.
 size_t autocorr_colwalk_bytes(int q, GridDesc g);
 bool autocorr_colwalk_supported(int m, int q, GridDesc g);
@@ -203,7 +216,8 @@ cudaError_t corr_band(const CorrJob& job, const BandTask& task, CellH* partials,
 // out_rho indexed by list position, or by location (r*ec+c) when rho_by_loc.
 cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long long* count,
                       int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
-                      int n_partials, cudaStream_t s, int rho_by_loc = 0);
+                      int n_partials, cudaStream_t s, int rho_by_loc = 0,
+                      const TailReduce* tail = nullptr);
 // FP64 replica (window_dot order, detail.hpp:32-41) over a location list or a dense range.
 cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
                           int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
@@ -216,7 +230,8 @@ cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials,
 // Epilogue of a K-split centre scan (rho/deg from the accumulated dots + argmax partials).
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
-                            CellH* partials, int n_partials, cudaStream_t s, int c_last = -1);
+                            CellH* partials, int n_partials, cudaStream_t s, int c_last = -1,
+                            const TailReduce* tail = nullptr, const int* gate = nullptr);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
