@@ -432,12 +432,41 @@ __device__ void tail_reduce(const TailReduce& tr, Cell* scratch) {
     if (!is_last) return;
     __threadfence();
     Cell best = no_cell();
-    for (int i = threadIdx.x; i < tr.n; i += blockDim.x) {
-        const CellH* h = tr.partials + i;
-        const Cell c{__ldcg(&h->rho), __ldcg(&h->row), __ldcg(&h->col), __ldcg(&h->flags)};
-        if (better(c, best)) best = c;
+    // all of a thread's partials loaded before any comparison (one L2 latency, not n/blockDim)
+    constexpr int kU = 4;
+    for (int i0 = threadIdx.x; i0 < tr.n; i0 += kU * blockDim.x) {
+        Cell c[kU];
+#pragma unroll
+        for (int u = 0; u < kU; ++u) {
+            const int i = i0 + u * blockDim.x;
+            c[u] = no_cell();
+            if (i < tr.n) {
+                const CellH* h = tr.partials + i;
+                c[u] = Cell{__ldcg(&h->rho), __ldcg(&h->row), __ldcg(&h->col), __ldcg(&h->flags)};
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < kU; ++u)
+            if (better(c[u], best)) best = c[u];
     }
     best = block_best(best, scratch);
+    const ReduceOp& op = tr.op;
+    if (op.kind == 3) {  // pack the result block with several threads (independent copies)
+        const int t = threadIdx.x;
+        if (t == 0) {
+            const CellH b{best.rho, best.row, best.col, best.flags};
+            tr.out[0] = b;
+            op.packed->cells[2] = b;
+            *tr.ticket = 0u;
+        } else if (t <= 2) {
+            op.packed->cells[t - 1] = op.cells[t - 1];
+        } else if (t == 3) {
+            op.packed->tally = *op.tally;
+        } else if (t == 4) {
+            op.packed->thr = *op.thr;
+        }
+        return;
+    }
     if (threadIdx.x == 0) {
         apply_reduce_op(best, tr.out, tr.op);
         *tr.ticket = 0u;
