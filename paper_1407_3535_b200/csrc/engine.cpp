@@ -332,6 +332,7 @@ struct tm_image {
     bool integer = false;
     DBuf<uint8_t> u8;
     DBuf<float> f32;
+    bool have_f32 = false;  // f32 is current (made on demand, ensure_f32)
     int pitch = 0;
     DBuf<double> f64;
     bool have_f64 = false;
@@ -418,12 +419,20 @@ void tc_pitch_copy(tm_ctx* ctx, tm_image* img) {
     img->u8p_rows = rows;
 }
 
+// The 16-byte-pitched copy is made at upload (tensor-core kernels, R_co, window statistics
+// and the list kernel read it); the FP32 copy only when a CUDA-core band kernel needs it.
 void finish_integer_image(tm_ctx* ctx, tm_image* img) {
     img->pitch = ((img->q + 3) & ~3) + 128;  // zero pad: vector loads past the last column
+    img->have_f32 = false;
+    tc_pitch_copy(ctx, img);
+}
+
+void ensure_f32(tm_ctx* ctx, tm_image* img) {
+    if (!img->integer || img->have_f32) return;
     img->f32.ensure(size_t(img->p) * img->pitch);
     CK(tmk::u8_to_f32_pitched(img->u8.p, img->p, img->q, img->f32.p, img->pitch, ctx->s));
     ctx->add(1);
-    tc_pitch_copy(ctx, img);
+    img->have_f32 = true;
 }
 
 void ensure_f64(tm_ctx* ctx, tm_image* img) {
@@ -595,6 +604,8 @@ tmk::CorrJob make_job(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
     if (!fp32) ensure_f64(ctx, img);
     j.imgf = img->f32.p;
     j.pitch = img->pitch;
+    j.imgb = img->u8p.p;
+    j.bpitch = img->u8p_pitch;
     j.imgd = img->f64.p;
     j.q = img->q;
     j.tf = ctx->tf.p;
@@ -605,6 +616,14 @@ tmk::CorrJob make_job(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
     j.flush_rows = std::max(1, T.flush_rows);
     j.ts = T.ts;
     j.st = ws.dev();
+    return j;
+}
+
+// A job for the CUDA-core band kernel (corr_band), which reads the FP32 copy (made on demand).
+tmk::CorrJob band_job(tm_ctx* ctx, tm_image* img, tmk::CorrJob j) {
+    ensure_f32(ctx, img);
+    j.imgf = img->f32.p;
+    j.pitch = img->pitch;
     return j;
 }
 
@@ -925,7 +944,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                 CK(cudaMemsetAsync(ctx->dotbuf.p, 0, G * sizeof(double), ctx->s));
                 t.dot = ctx->dotbuf.p;
                 int dummy = 0;
-                CK(tmk::corr_band(job, t, ctx->partials.p, &dummy, ctx->s));
+                CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &dummy, ctx->s));
                 n1 = std::min(kListBlocks, int((size_t(nstrip) * nc_reg + 255) / 256));
                 CK(tmk::centre_epilogue(job, g, ctx->rows_list.p, wr, g.w, nc_reg, 0, ctx->dotbuf.p,
                                         ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s));
@@ -936,7 +955,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             } else {
                 t.ksplit = 1;
                 t.ms = T.m;
-                CK(tmk::corr_band(job, t, ctx->partials.p, &n1, ctx->s));
+                CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &n1, ctx->s));
                 ctx->add(1);
             }
         }
@@ -1487,7 +1506,7 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         int np = 0;
         {
             Phase ph(ctx, "survivor_dense");
-            CK(tmk::corr_band(job, t, ctx->partials.p, &np, s));
+            CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &np, s));
             ctx->add(1);
         }
         reduce_to(ctx, np, 2);
@@ -1787,7 +1806,7 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
         t.out_rho = surface;
         ctx->partials.ensure(size_t(band_partials(er, ec, 1)));
         int np = 0;
-        CK(tmk::corr_band(job, t, ctx->partials.p, &np, ctx->s));
+        CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &np, ctx->s));
         ctx->add(1);
         reduce_to(ctx, np, 2);
     } else {
@@ -2091,8 +2110,7 @@ int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
         if (!img->integer) invalid("tm_image_upload_u8: image is not an 8-bit image");
         const size_t N = size_t(img->p) * img->q;
         CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
-        CK(tmk::u8_to_f32_pitched(img->u8.p, img->p, img->q, img->f32.p, img->pitch, ctx->s));
-        ctx->add(1);
+        img->have_f32 = false;
         img->have_f64 = false;
         img->have_qtotal = false;
         tc_pitch_copy(ctx, img);

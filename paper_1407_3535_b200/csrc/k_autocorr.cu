@@ -966,8 +966,10 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
         for (int j = 0; j < W; ++j) {
             b[j] = pb[j];
-            a[j] = pa[j];
-            opaque(a[j]);  // plain IMADs: keeps nvcc from packing bytes into IDP (PRMT-heavy)
+            // h = 5: negated once so the H updates are single IMADs (measured: h = 3 is
+            // faster with the plain subtraction, which nvcc schedules better there)
+            a[j] = H >= 5 ? 0u - unsigned(pa[j]) : unsigned(pa[j]);
+            opaque(a[j]);
             opaque(b[j]);
         }
 #pragma unroll
@@ -976,7 +978,10 @@ __global__ void __launch_bounds__(NT)
             for (int d = 0; d < H - 1; ++d) rt[d][j] = rt[d + 1][j];
             rt[H - 1][j] = b[j];
 #pragma unroll
-            for (int d = 0; d < H; ++d) V[d][j] -= a[j] * rt[d][j];
+            for (int d = 0; d < H; ++d) {
+                if (H >= 5) V[d][j] += a[j] * rt[d][j];  // exact mod 2^32
+                else V[d][j] -= a[j] * rt[d][j];
+            }
         }
     };
     auto lead = [&]() {

@@ -256,7 +256,7 @@ __global__ void __launch_bounds__(256)
     for (long long li = blockIdx.x; li < nloc; li += gridDim.x) {
         const int2 rc = locs[li];
         double dacc = 0.0;
-        const float* ib = job.imgf + size_t(rc.x) * job.pitch + rc.y;
+        const uint8_t* ib = job.imgb + size_t(rc.x) * job.bpitch + rc.y;  // pixels as bytes
         for (int j = lane; j < job.n; j += 32) {
             const float* tp = job.tf + j;
             for (int i0 = i_lo; i0 < i_hi; i0 += 2 * lane_flush) {
@@ -267,7 +267,7 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
                     for (int u = 0; u < 8; ++u) {
                         const bool ok = i + u < i1;
-                        v[u] = ok ? __ldg(ib + size_t(i + u) * job.pitch + j) : 0.f;
+                        v[u] = ok ? float(__ldg(ib + size_t(i + u) * job.bpitch + j)) : 0.f;
                         t[u] = ok ? __ldg(tp + size_t(i + u) * job.npad) : 0.f;
                     }
 #pragma unroll

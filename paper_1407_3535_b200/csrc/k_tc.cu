@@ -474,12 +474,30 @@ __global__ void k_tc_build_b(const float* __restrict__ tf, int npad, int m, int 
     }
 }
 
+// Pitched zero-padded copy, one 16-byte output chunk per thread (pitch % 16 == 0): 16-byte
+// loads when the source rows are 16-byte aligned (q % 16 == 0), byte loads otherwise.
 __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_t* __restrict__ out,
                            int pitch, int rows) {
-    const int r = blockIdx.y;
-    if (r >= rows) return;
-    for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < pitch; c += gridDim.x * blockDim.x)
-        out[size_t(r) * pitch + c] = (r < p && c < q) ? img[size_t(r) * q + c] : 0;
+    const int cpr = pitch >> 4;  // chunks per row
+    const size_t total = size_t(rows) * cpr;
+    const bool vec = (q & 15) == 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int r = int(i / cpr), c = int(i - size_t(r) * cpr) << 4;
+        uint4 v = make_uint4(0u, 0u, 0u, 0u);
+        if (r < p && c < q) {
+            const uint8_t* src = img + size_t(r) * q + c;
+            if (vec) {
+                v = __ldg(reinterpret_cast<const uint4*>(src));
+            } else {
+                unsigned w[4] = {0u, 0u, 0u, 0u};
+                const int nb = min(16, q - c);
+                for (int b = 0; b < nb; ++b) w[b >> 2] |= unsigned(__ldg(src + b)) << (8 * (b & 3));
+                v = make_uint4(w[0], w[1], w[2], w[3]);
+            }
+        }
+        *reinterpret_cast<uint4*>(out + size_t(r) * pitch + c) = v;
+    }
 }
 
 }  // namespace
@@ -584,8 +602,9 @@ int tc_tile_cols() { return kTcCols; }
 
 cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int pitch, int rows,
                            cudaStream_t s) {
-    dim3 grid((pitch + 255) / 256 > 8 ? 8 : (pitch + 255) / 256, rows);
-    k_tc_pitch<<<grid, 256, 0, s>>>(img, p, q, out, pitch, rows);
+    const size_t chunks = size_t(rows) * (pitch / 16);
+    const int blocks = int(std::min<size_t>((chunks + 255) / 256, 148 * 8));
+    k_tc_pitch<<<blocks, 256, 0, s>>>(img, p, q, out, pitch, rows);
     return cudaGetLastError();
 }
 

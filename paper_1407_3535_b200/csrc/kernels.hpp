@@ -173,9 +173,12 @@ cudaError_t retained_count(const double* map, GridDesc g, double threshold,
 
 // ---- correlation -----------------------------------------------------------------------
 struct CorrJob {
-    // image (integer path uses imgf, FP64 path uses imgd)
+    // image (integer path: imgb for the list kernel, imgf for the dense CUDA-core band
+    // kernel; FP64 path: imgd)
     const float* imgf;
     int pitch;  // floats per row of imgf
+    const uint8_t* imgb;  // the 16-byte-pitched 8-bit copy
+    int bpitch;
     const double* imgd;
     int q;  // columns of imgd
     // template
