@@ -209,6 +209,11 @@ int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
               const tm_match_params* params, tm_match_result* out);
 int tm_search_u8(tm_ctx* ctx, tm_image* img, const uint8_t* tmpl, int m, int n,
                  const tm_match_params* params, tm_match_result* out);
+/* match (matcher.hpp:80) from host memory in one call: upload the 8-bit pixels (rows x
+ * cols of `img`) into `img`, then tm_search_u8 (same results as tm_image_upload_u8 +
+ * tm_search_u8). */
+int tm_search_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels, const uint8_t* tmpl,
+                        int m, int n, const tm_match_params* params, tm_match_result* out);
 
 /* transitive_search (matcher.hpp:37-38) with a caller-supplied map/grid. */
 int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,

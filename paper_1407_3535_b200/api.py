@@ -351,6 +351,22 @@ class Context:
             N.check(N.lib().tm_search(self.h, img.h, _dptr(t), m, n, C.byref(p), C.byref(res)))
         return res
 
+    def search_upload(self, img, pixels, t, mode="egs", **kw):
+        """match from host memory into a device image in one call (tm_search_upload_u8):
+        upload the 8-bit pixels (img's shape), then the search."""
+        if not isinstance(img, Image) or not img.is_integer:
+            raise ValueError("search_upload: needs an 8-bit device image")
+        px = np.ascontiguousarray(pixels, dtype=np.uint8)
+        if px.shape != (img.rows, img.cols):
+            raise ValueError("search_upload: pixel array shape differs from the image")
+        t = np.ascontiguousarray(t, dtype=np.uint8)
+        m, n = t.shape
+        p = make_params(mode=mode, **kw)
+        res = MatchResult()
+        N.check(N.lib().tm_search_upload_u8(self.h, img.h, _u8ptr(px), _u8ptr(t), m, n,
+                                            C.byref(p), C.byref(res)))
+        return res
+
     def match(self, t, image, mode="egs", record_visits=False, **kw):
         """match (matcher.hpp:80): host buffers in, host result out (end to end)."""
         t = np.ascontiguousarray(t, dtype=np.float64)

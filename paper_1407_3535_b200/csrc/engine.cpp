@@ -2401,48 +2401,77 @@ int tm_run_u8(tm_ctx* ctx, tm_prep* prep, tm_image* img, const uint8_t* tmpls, i
     return tm_run(ctx, prep, img, t.data(), ntmpl, params, out, visits);
 }
 
+// prepare + run of one template on a resident image (tm_search's body; ev0 recorded).
+void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+                     const tm_match_params* params, tm_match_result* out) {
+    Tmpl T;
+    bool uploaded = false;
+    // Predicted h_e: the last one seen for this image/template shape (else h0).  Its
+    // centre scan is enqueued behind the first EGS batch, gated on the device decision,
+    // so the device does not idle while the host reads the counts.
+    const bool egs = params->mode != TM_MODE_OPTA && params->h0 == params->w0;
+    const std::vector<long long> key = {img->p, img->q, m, n, params->h0, params->w0};
+    int want = 0;
+    if (egs && img->integer && m <= img->p && n <= img->q) {
+        const auto it = ctx->last_he.find(key);
+        want = it != ctx->last_he.end() ? it->second : params->h0;
+    }
+    ctx->spec_want = want;
+    ctx->spec.armed = false;
+    const std::function<void()> hook = [&] {
+        T = upload_template(ctx, tmpl, m, n, /*side=*/true);
+        uploaded = true;
+        if (want > 0)
+            spec_centre(ctx, img, get_ws(ctx, img, m, n),
+                        T, make_grid(img->p - m + 1, img->q - n + 1, want, want), *params);
+    };
+    std::unique_ptr<tm_prep> prep;
+    try {
+        prep.reset(prepare(ctx, img, m, n, *params, &hook));
+    } catch (...) {
+        ctx->spec_want = 0;
+        ctx->spec.armed = false;
+        throw;
+    }
+    ctx->spec_want = 0;  // (run_egs_search recorded h_e for the next prediction)
+    prep->ctx = nullptr;  // internal: not counted as a context reference
+    if (!uploaded) T = upload_template(ctx, tmpl, m, n);
+    *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);
+    CK(cudaEventRecord(ctx->ev1, ctx->s));
+    CK(cudaEventSynchronize(ctx->ev1));
+    out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+}
+
 int tm_search(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
               const tm_match_params* params, tm_match_result* out) {
     return guard(ctx, [&] {
         if (!img || !tmpl || !params || !out) invalid("tm_search: null argument");
         HT("start");
         CK(cudaEventRecord(ctx->ev0, ctx->s));
-        Tmpl T;
-        bool uploaded = false;
-        // Predicted h_e: the last one seen for this image/template shape (else h0).  Its
-        // centre scan is enqueued behind the first EGS batch, gated on the device decision,
-        // so the device does not idle while the host reads the counts.
-        const bool egs = params->mode != TM_MODE_OPTA && params->h0 == params->w0;
-        const std::vector<long long> key = {img->p, img->q, m, n, params->h0, params->w0};
-        int want = 0;
-        if (egs && img->integer && m <= img->p && n <= img->q) {
-            const auto it = ctx->last_he.find(key);
-            want = it != ctx->last_he.end() ? it->second : params->h0;
-        }
-        ctx->spec_want = want;
-        ctx->spec.armed = false;
-        const std::function<void()> hook = [&] {
-            T = upload_template(ctx, tmpl, m, n, /*side=*/true);
-            uploaded = true;
-            if (want > 0)
-                spec_centre(ctx, img, get_ws(ctx, img, m, n),
-                            T, make_grid(img->p - m + 1, img->q - n + 1, want, want), *params);
-        };
-        std::unique_ptr<tm_prep> prep;
-        try {
-            prep.reset(prepare(ctx, img, m, n, *params, &hook));
-        } catch (...) {
-            ctx->spec_want = 0;
-            ctx->spec.armed = false;
-            throw;
-        }
-        ctx->spec_want = 0;  // (run_egs_search recorded h_e for the next prediction)
-        prep->ctx = nullptr;  // internal: not counted as a context reference
-        if (!uploaded) T = upload_template(ctx, tmpl, m, n);
-        *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);
-        CK(cudaEventRecord(ctx->ev1, ctx->s));
-        CK(cudaEventSynchronize(ctx->ev1));
-        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+        search_resident(ctx, img, tmpl, m, n, params, out);
+    });
+}
+
+int tm_search_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels, const uint8_t* tmpl,
+                        int m, int n, const tm_match_params* params, tm_match_result* out) {
+    return guard(ctx, [&] {
+        if (!img || !pixels || !tmpl || !params || !out)
+            invalid("tm_search_upload_u8: null argument");
+        if (!img->integer) invalid("tm_image_upload_u8: image is not an 8-bit image");
+        if (m < 1 || n < 1) invalid("tm_search_upload_u8: invalid template");
+        HT("start");
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        // (a row-chunked upload overlapping the window statistics with the copy was measured
+        // slower on C2: per-chunk statistics launches cost more than the copy they hide)
+        const size_t N = size_t(img->p) * img->q;
+        CK(cudaMemcpyAsync(img->u8.p, pixels, N, cudaMemcpyHostToDevice, ctx->s));
+        img->have_f32 = img->have_f64 = false;
+        img->have_qtotal = false;
+        tc_pitch_copy(ctx, img);
+        img->ws_cache.clear();
+        std::vector<double> t(size_t(m) * n);
+        for (size_t i = 0; i < t.size(); ++i) t[i] = tmpl[i];
+        search_resident(ctx, img, t.data(), m, n, params, out);
     });
 }
 

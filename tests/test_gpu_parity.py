@@ -436,3 +436,52 @@ def test_search_speculation_hit_and_miss(ctx):
             assert getattr(got, k) == getattr(want, k), k
         gi.close()
     assert len(seen) >= 2, seen
+
+
+@pytest.mark.parametrize("shape", [(300, 420, 40, 37), (700, 260, 64, 64), (130, 90, 20, 30)])
+def test_search_upload_streamed_equals_resident(ctx, port, shape):
+    """tm_search_upload_u8 (upload + search in one call) == tm_image_upload_u8 +
+    tm_search_u8, bit for bit, repeated on the same image; the image holds near-constant
+    windows, and the window statistics equal the oracle's."""
+    rows, cols, m, n = shape
+    rng = np.random.default_rng(rows + cols)
+    base = np.cumsum(np.cumsum(rng.normal(size=(rows, cols)), 0), 1)
+    img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
+    img[5:5 + 2 * m, 3:3 + 2 * n] = 200
+    img[5 + m, 3 + n] = 201  # variance 1 pixel away from flat: decided by the noise floor
+    t = np.clip(np.rint(img[rows // 3:rows // 3 + m, cols // 4:cols // 4 + n] * 1.05 + 3
+                        + rng.normal(0, 3, (m, n))), 0, 255).astype(np.uint8)
+    keys = ("best_row", "best_col", "best_rho", "eliminated", "retained", "centers", "ops",
+            "final_threshold")
+    a = ctx.image(np.zeros_like(img))
+    a.upload_u8(img)
+    want = ctx.search(a, t, policy="seeded")
+    b = ctx.image(np.zeros_like(img))
+    for _ in range(2):
+        got = ctx.search_upload(b, img, t, policy="seeded")
+        for k in keys:
+            assert getattr(got, k) == getattr(want, k), k
+    _ws_equal(ctx.window_stats(b, m, n), port.window_stats(img.astype(np.float64), m, n))
+
+
+@pytest.mark.parametrize("dense", [False, True])
+def test_search_upload_undecided_windows(ctx, port, dense):
+    """A 3400 x 3300 image whose noise floor ((rows + cols) * eps * sum of squares, about
+    0.36 here) sits just below the variance sum of windows with exactly one bumped pixel in
+    a constant region ((mn-1)/mn): window statistics equal the oracle's (flat decisions
+    included) and the one-call search equals upload + search."""
+    rng = np.random.default_rng(17 + dense)
+    rows, cols, m, n = 3400, 3300, 16, 16
+    img = rng.integers(0, 256, (rows, cols)).astype(np.uint8)
+    img[200:1400, 300:1500] = 90
+    step = 17 if dense else 97
+    img[200:1400:step, 300:1500:step] = 91
+    t = img[2000:2016, 2500:2516].copy()
+    b = ctx.image(np.zeros_like(img))
+    got = ctx.search_upload(b, img, t, policy="seeded")
+    _ws_equal(ctx.window_stats(b, m, n), port.window_stats(img.astype(np.float64), m, n))
+    a = ctx.image(np.zeros_like(img))
+    a.upload_u8(img)
+    want = ctx.search(a, t, policy="seeded")
+    for k in ("best_row", "best_col", "best_rho", "eliminated", "retained", "final_threshold"):
+        assert getattr(got, k) == getattr(want, k), k

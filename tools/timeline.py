@@ -11,23 +11,40 @@ from paper_1407_3535_b200 import api, workloads as W  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
+upload = len(sys.argv) > 3 and sys.argv[3] == "upload"  # the e2e step: tm_search_upload_u8
 wl = W.make(cfg)
 ctx = api.Context(0)
 img = ctx.image(wl.image)
 t = wl.templates[0].pixels
+pinned = torch.empty(wl.image.shape, dtype=torch.uint8, pin_memory=True)
+pinned.numpy()[:] = wl.image
+
+
+def step():
+    if upload:
+        ctx.search_upload(img, pinned.numpy(), t.astype("uint8"), policy="seeded")
+    else:
+        img.reset_cache()
+        ctx.search(img, t, policy="seeded")
+
+
 for _ in range(3):
-    img.reset_cache()
-    ctx.search(img, t, policy="seeded")
+    step()
 torch.cuda.synchronize()
 with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
     for _ in range(steps):
-        img.reset_cache()
-        ctx.search(img, t, policy="seeded")
+        step()
     torch.cuda.synchronize()
 evs = [e for e in prof.events() if e.device_type.name == "CUDA"]
 evs.sort(key=lambda e: e.time_range.start)
 # split into searches at the first window-statistics kernel
-starts = [i for i, e in enumerate(evs) if "k_sum_sq_u8" in e.name]
+def big_copy(e):  # an image chunk (the template copies are a few microseconds)
+    return "Memcpy HtoD" in e.name and (e.time_range.end - e.time_range.start) > 8.0
+
+
+starts = [i for i, e in enumerate(evs) if (upload and big_copy(e) and
+                                           (i == 0 or not big_copy(evs[i - 1])))
+          or (not upload and "k_sum_sq_u8" in e.name)]
 last = evs[starts[-1]:] if starts else evs
 t0 = last[0].time_range.start
 prev_end = t0
