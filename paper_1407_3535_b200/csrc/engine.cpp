@@ -232,6 +232,7 @@ struct tm_ctx {
     DBuf<double> map_tmp, map_user;
     DBuf<double> egs_maps[4];
     DBuf<double> sa_c;  // per-group half_gap factor sqrt(1 - rho_c^2) (scan 2)
+    bool sa_ready = false;  // sa_c filled by this search's centre epilogue
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
     // row-strip search protocol state (tm_strip_search_*)
     struct StripState {
@@ -266,9 +267,14 @@ struct tm_ctx {
     cudaStream_t s2 = nullptr;
     cudaEvent_t ev_t = nullptr;
     cudaEvent_t ev_egs = nullptr;  // end of an EGS batch's count copy
+    // speculative B build on the side stream: tc_b sized before the EGS batch (ev_b0), the
+    // build done (ev_b1); spec_b: this search's hook may build B on the side stream
+    cudaEvent_t ev_b0 = nullptr, ev_b1 = nullptr;
+    bool spec_b = false;
     // speculative centre scan (tm_search): predicted group size passed to the EGS decide
     // kernels, and what was enqueued for it
     int spec_want = 0;
+    unsigned long long egs_seq = 0;  // EGS batches launched (ResultBlock::seq)
     struct Spec {
         bool armed = false;
         tmk::GridDesc g{};
@@ -730,12 +736,21 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, i
 
 // Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
 int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet& rs, int sr,
-           tmk::TcTask task, const int** rows_dev = nullptr) {
+           tmk::TcTask task, const int** rows_dev = nullptr, bool side_build = false) {
     TcGeo& geo = tc_geometry(ctx, ws, T, rs, sr);
     HT("tc_geo");
     const tmk::TcPlan& plan = geo.plan;
-    ctx->tc_b.ensure(plan.total_bytes);
-    CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s, task.gate));
+    if (side_build && ctx->tc_b.cap >= plan.total_bytes) {
+        // speculative centre scan: B built on the side stream while the EGS batch runs
+        // (ungated: the gate is decided later; a miss rebuilds B on the main stream)
+        CK(cudaStreamWaitEvent(ctx->s2, ctx->ev_b0, 0));
+        CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s2));
+        CK(cudaEventRecord(ctx->ev_b1, ctx->s2));
+        CK(cudaStreamWaitEvent(ctx->s, ctx->ev_b1, 0));
+    } else {
+        ctx->tc_b.ensure(plan.total_bytes);
+        CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s, task.gate));
+    }
     HT("build_b");
     tmk::TcJob job{};
     job.imgp = tc_image(ctx, img, ws.ec);
@@ -845,6 +860,7 @@ void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const in
 void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                  const tmk::GridDesc& g, const tmk::ReduceOp* op = nullptr) {
     const size_t G = size_t(g.tr) * g.tc;
+    ctx->sa_ready = false;  // set below only by the epilogues that write sa_c
     ctx->rho_c.ensure(G);
     ctx->deg_c.ensure(G);
     const tmk::CorrJob job = make_job(ctx, img, ws, T);
@@ -887,13 +903,15 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                              sp.g.w == g.w && sp.g.ti_lo == g.ti_lo && sp.g.ti_hi == g.ti_hi &&
                              ctx->hres->spec == 1;
             ctx->spec.armed = false;
+            ctx->sa_c.ensure(G);
+            ctx->sa_ready = true;  // both epilogues below write scan 2's half-gap factors
             if (hit) return;  // dots, epilogue and its reduction are already in flight
             tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
             const tmk::TailReduce tail = tail_to(ctx, n1 + n2, 0, op);  // n2 = 0 here
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
-                                    task.c_last, &tail));
+                                    task.c_last, &tail, nullptr, ctx->sa_c.p));
             HT("centre_epi");
             ctx->add(1);
         }
@@ -1032,14 +1050,15 @@ void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const 
     task.gate = reinterpret_cast<const int*>(ctx->counters.p + 24);
     const int* rows_dev = nullptr;
     Phase ph(ctx, "centre_scan");
-    tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+    tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev, /*side_build=*/ctx->spec_b);
     // the epilogue + scan 1's reduction (the same op search() would use), same gate
     const int n1 = std::min(kListBlocks, int((size_t(g.ti_hi - g.ti_lo) * g.tc + 255) / 256));
     const tmk::ReduceOp op = centre_op(ctx, P);
     const tmk::TailReduce tail = tail_to(ctx, n1, 0, &op);
+    ctx->sa_c.ensure(G);
     CK(tmk::centre_epilogue(make_job(ctx, img, ws, T), g, rows_dev, g.w / 2, g.w, g.tc, 0,
                             ctx->dotbuf.p, ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
-                            task.c_last, &tail, task.gate));
+                            task.c_last, &tail, task.gate, ctx->sa_c.p));
     ctx->add(1);
     ctx->spec.armed = true;
     ctx->spec.g = g;
@@ -1225,6 +1244,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             ww = std::min(ww + 2, cap);
         }
         bool map_written[4] = {false, false, false, false};
+        const unsigned long long batch_seq = ++ctx->egs_seq;
         if (first_batch) {  // stop = 0, prev = +inf, nr[0..3] = 0, h_acc = 0, gate = 0
             CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s, dhacc, dgate));
             ctx->add(1);
@@ -1243,7 +1263,8 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             const bool last = k + 1 == nc;
             CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
                                cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
-                               ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr));
+                               ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr,
+                               batch_seq));
             ctx->add(1);
         }
         // the host waits for this point only, so work enqueued by the hook keeps the device
@@ -1255,7 +1276,20 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         }
         ctx->spec_want = 0;  // later batches: the speculation (if any) was for this one
         HT("egs_enqueued");
-        CK(cudaEventSynchronize(ctx->ev_egs));
+        // poll the sequence number the last decide writes into mapped pinned memory after
+        // the counts (lower wake-up latency than an event wait); the event still guards
+        // against a device error
+        {
+            const volatile unsigned long long* sq = &ctx->hres->seq;
+            for (unsigned spins = 0; *sq != batch_seq; ++spins) {
+                if ((spins & 255) == 255) {
+                    const cudaError_t q = cudaEventQuery(ctx->ev_egs);
+                    if (q == cudaSuccess) break;
+                    if (q != cudaErrorNotReady) CK(q);
+                }
+            }
+            CK(cudaEventSynchronize(ctx->ev_egs));  // normally complete already
+        }
         HT("egs_sync");
         unsigned long long nr[4] = {0, 0, 0, 0};
         for (int k = 0; k < nc; ++k) nr[k] = ctx->hres->nr[k];
@@ -1626,8 +1660,9 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         // locations are written; the sequential replay and the FP64 path read every one
         const unsigned long long max_locs = (!seq && fp32_path(img, T)) ? E / 16 + 1 : E;
         CK(tmk::sec_rows(g, in.map, ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
-                         ctx->thr.p, seeded, ctx->locs.p, max_locs, ctx->tally.p, visits, s));
-        ctx->add(2);
+                         ctx->thr.p, seeded, ctx->locs.p, max_locs, ctx->tally.p, visits, s,
+                         ctx->sa_ready));
+        ctx->add(ctx->sa_ready ? 1 : 2);
     }
     double T0 = 0.0;
     tmk::Tally tally{};
@@ -1841,7 +1876,7 @@ std::vector<double> params_profile(const tm_match_params& P) {
 }
 
 tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params& P,
-                 const std::function<void()>* before_sync = nullptr) {
+                 const std::function<void()>* before_sync = nullptr, bool timed = true) {
     auto prep = std::make_unique<tm_prep>();
     prep->params = P;
     prep->profile = params_profile(P);
@@ -1851,9 +1886,13 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     prep->source = img;
     prep->mode = P.mode == TM_MODE_OPTA ? TM_MODE_OPTA : TM_MODE_EGS;
     if (m > img->p || n > img->q) invalid("match: template larger than search image");
-    CK(cudaEventCreate(&prep->ev0));
-    CK(cudaEventCreate(&prep->ev1));
-    CK(cudaEventRecord(prep->ev0, ctx->s));
+    // (tm_search skips the timing events: an event record between two kernels breaks the
+    // programmatic-launch chain of the search that follows)
+    if (timed) {
+        CK(cudaEventCreate(&prep->ev0));
+        CK(cudaEventCreate(&prep->ev1));
+        CK(cudaEventRecord(prep->ev0, ctx->s));
+    }
     if (prep->mode == TM_MODE_EGS) {
         WS& ws = get_ws(ctx, img, m, n);
         EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
@@ -1865,7 +1904,7 @@ tm_prep* prepare(tm_ctx* ctx, tm_image* img, int m, int n, const tm_match_params
     } else {
         run_opta_prep(ctx, img, prep.get());
     }
-    CK(cudaEventRecord(prep->ev1, ctx->s));
+    if (timed) CK(cudaEventRecord(prep->ev1, ctx->s));
     prep->g = make_grid(img->p - m + 1, img->q - n + 1, prep->h, prep->w);
     HT("prep_end");
     return prep.release();
@@ -1952,6 +1991,8 @@ void ctx_release(tm_ctx* ctx) {
     }
     if (ctx->ev_t) cudaEventDestroy(ctx->ev_t);
     if (ctx->ev_egs) cudaEventDestroy(ctx->ev_egs);
+    if (ctx->ev_b0) cudaEventDestroy(ctx->ev_b0);
+    if (ctx->ev_b1) cudaEventDestroy(ctx->ev_b1);
     if (ctx->hres) cudaFreeHost(ctx->hres);
     delete ctx;  // stream-ordered frees of the scratch buffers
     cudaStreamSynchronize(st);
@@ -2015,6 +2056,8 @@ int tm_ctx_create(int device, tm_ctx** out) {
         CK(cudaStreamCreateWithFlags(&ctx->s2, cudaStreamNonBlocking));
         CK(cudaEventCreateWithFlags(&ctx->ev_t, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_egs, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_b0, cudaEventDisableTiming));
+        CK(cudaEventCreateWithFlags(&ctx->ev_b1, cudaEventDisableTiming));
         ctx->counters.ensure(32);
         CK(cudaMemsetAsync(ctx->counters.p, 0, 32 * sizeof(unsigned long long), ctx->s));
         ctx->cells.ensure(8);
@@ -2418,6 +2461,18 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
     }
     ctx->spec_want = want;
     ctx->spec.armed = false;
+    // B of the predicted centre scan is built on the side stream during the EGS batch: its
+    // buffer is sized now, before the batch is enqueued, so the side stream only waits for
+    // this point
+    ctx->spec_b = false;
+    if (want > 0 && ctx->tc && m <= img->p && n <= img->q) {
+        const tmk::TcPlan plan = tmk::tc_plan(m, n, want, kTcSmemBudget);
+        if (plan.nch > 0) {
+            ctx->tc_b.ensure(plan.total_bytes);
+            CK(cudaEventRecord(ctx->ev_b0, ctx->s));
+            ctx->spec_b = true;
+        }
+    }
     const std::function<void()> hook = [&] {
         T = upload_template(ctx, tmpl, m, n, /*side=*/true);
         uploaded = true;
@@ -2427,13 +2482,15 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
     };
     std::unique_ptr<tm_prep> prep;
     try {
-        prep.reset(prepare(ctx, img, m, n, *params, &hook));
+        prep.reset(prepare(ctx, img, m, n, *params, &hook, /*timed=*/false));
     } catch (...) {
         ctx->spec_want = 0;
+        ctx->spec_b = false;
         ctx->spec.armed = false;
         throw;
     }
     ctx->spec_want = 0;  // (run_egs_search recorded h_e for the next prediction)
+    ctx->spec_b = false;
     prep->ctx = nullptr;  // internal: not counted as a context reference
     if (!uploaded) T = upload_template(ctx, tmpl, m, n);
     *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);

@@ -1492,7 +1492,7 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
                              int ec, int h, int w, double xi, int cap, int* h_acc, int want,
                              unsigned long long* gate, const unsigned long long* nr_all, int nc,
-                             ResultBlock* out) {
+                             ResultBlock* out, unsigned long long seq) {
     pdl_wait();
     if (!*stop) {
         const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
@@ -1515,15 +1515,17 @@ __global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, i
     if (out) {  // last candidate of the batch: counts + gate into the mapped result block
         for (int i = 0; i < nc; ++i) out->nr[i] = nr_all[i];
         out->spec = gv;
+        __threadfence_system();  // counts visible to the host before the sequence number
+        *reinterpret_cast<volatile unsigned long long*>(&out->seq) = seq;
     }
 }
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s, const unsigned long long* nr_all,
-                       int nc, ResultBlock* out) {
+                       int nc, ResultBlock* out, unsigned long long seq) {
     launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap,
-               h_acc, want, gate, nr_all, nc, out);
+               h_acc, want, gate, nr_all, nc, out, seq);
     return cudaGetLastError();
 }
 

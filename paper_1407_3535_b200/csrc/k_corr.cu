@@ -204,7 +204,8 @@ __device__ void tail_reduce(const TailReduce& tr, Cell* scratch);
 __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
-                 CellH* partials, int c_last, TailReduce tail, const int* __restrict__ gate) {
+                 CellH* partials, int c_last, TailReduce tail, const int* __restrict__ gate,
+                 double* __restrict__ sa_out) {
     pdl_wait();
     if (gate && !*gate) return;  // speculative launch not confirmed (every block: no ticket)
     __shared__ Cell scratch[8];
@@ -224,6 +225,10 @@ __global__ void __launch_bounds__(256)
         const bool deg = ts.flat || wflat;
         rho_c[gi] = rho;
         deg_c[gi] = deg;
+        if (sa_out) {  // scan 2's centre half-gap factor (k_sqrt_gap, bounds.cpp:21-23)
+            const double a = dclamp(rho, -1.0, 1.0);
+            sa_out[gi] = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(a, a))));
+        }
         const Cell cand = make_cell(r, c, rho, deg);
         if (better(cand, best)) best = cand;
     }
@@ -889,9 +894,10 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last,
-                            const TailReduce* tail, const int* gate) {
+                            const TailReduce* tail, const int* gate, double* sa_out) {
     launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw,
-               nc, col0, dot, rho_c, deg_c, partials, c_last, tail ? *tail : TailReduce{}, gate);
+               nc, col0, dot, rho_c, deg_c, partials, c_last, tail ? *tail : TailReduce{}, gate,
+               sa_out);
     return cudaGetLastError();
 }
 
@@ -932,9 +938,10 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c, cons
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
                      const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
-                     uint8_t* visits, cudaStream_t s) {
+                     uint8_t* visits, cudaStream_t s, bool sa_ready) {
     const size_t G = size_t(g.tr) * g.tc;
-    launch_pdl(k_sqrt_gap, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256), 0, s, rho_c, sa_c, G);
+    if (!sa_ready)
+        launch_pdl(k_sqrt_gap, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256), 0, s, rho_c, sa_c, G);
     const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
     const int blocks = std::max(1, std::min(rows, 148 * 8));
     launch_pdl(k_sec_rows, dim3(blocks), dim3(256), 0, s, to_grid(g), map, rho_c, sa_c, deg_c, flat, tflat, thr, seeded,

@@ -47,6 +47,7 @@ struct Tally {  // accumulated on device by the search kernels
 struct ResultBlock {
     unsigned long long nr[4];  // EGS retained counts of a candidate batch
     unsigned long long spec;   // EGS speculation gate of the batch (k_egs_decide)
+    unsigned long long seq;    // written last by the batch's final decide (host polls it)
     CellH cells[3];            // best centre, best seeded member, best survivor
     Tally tally;
     double thr;                // threshold after the search
@@ -155,7 +156,7 @@ cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* st
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s,
                        const unsigned long long* nr_all = nullptr, int nc = 0,
-                       ResultBlock* out = nullptr);
+                       ResultBlock* out = nullptr, unsigned long long seq = 0);
 // Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.
 size_t autocorr_colwalk_bytes(int q, GridDesc g);
 bool autocorr_colwalk_supported(int m, int q, GridDesc g);
@@ -234,7 +235,8 @@ cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials,
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last = -1,
-                            const TailReduce* tail = nullptr, const int* gate = nullptr);
+                            const TailReduce* tail = nullptr, const int* gate = nullptr,
+                            double* sa_out = nullptr);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
@@ -260,7 +262,7 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c,
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
                      const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
-                     uint8_t* visits, cudaStream_t s);
+                     uint8_t* visits, cudaStream_t s, bool sa_ready = false);
 cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, double* thr,
                            cudaStream_t s);
 // Seeded policy: members of every group whose centre rho >= thr - margin -> list.
