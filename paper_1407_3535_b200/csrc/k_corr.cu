@@ -597,20 +597,36 @@ __global__ void __launch_bounds__(256)
         const bool centre_row = g.center_row(ti) == r;
         const size_t rowk = size_t(r) * g.ec;
         const size_t gbase = size_t(ti) * g.tc;
+        // software pipeline: every load of the next column is in flight while this one is
+        // tested (one memory latency per two columns, not a chain through the tests)
+        struct Elem {
+            double mv, ra, sa;
+            uint8_t fv, sd, dg;
+            int tj;
+        };
+        auto load = [&](int c, Elem& e) {
+            const bool in = c < g.ec;
+            const size_t k = rowk + (in ? c : 0);
+            e.tj = g.tile_c(in ? c : 0);
+            const size_t gi = gbase + e.tj;
+            e.mv = __ldg(map + k);
+            e.fv = __ldg(flat + k);
+            e.sd = seeded ? __ldg(seeded + gi) : uint8_t(0);
+            e.dg = __ldg(deg_c + gi);
+            e.ra = __ldg(rho_c + gi);
+            e.sa = __ldg(sa_c + gi);
+        };
+        Elem cur;
+        load(threadIdx.x, cur);
         for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            Elem nxt = cur;
+            if (c + int(blockDim.x) < cols) load(c + blockDim.x, nxt);
             bool survivor = false;
             if (c < g.ec) {
                 const size_t k = rowk + c;
-                const int tj = g.tile_c(c);
-                const size_t gi = gbase + tj;
-                // every load of the element issued up front (one memory latency, not a
-                // chain of dependent ones through the short-circuit tests)
-                const double mv = __ldg(map + k);
-                const uint8_t fv = __ldg(flat + k);
-                const uint8_t sd = seeded ? __ldg(seeded + gi) : uint8_t(0);
-                const uint8_t dg = __ldg(deg_c + gi);
-                const double ra = __ldg(rho_c + gi);
-                const double sa = __ldg(sa_c + gi);
+                const int tj = cur.tj;
+                const double mv = cur.mv, ra = cur.ra, sa = cur.sa;
+                const uint8_t fv = cur.fv, sd = cur.sd, dg = cur.dg;
                 if (centre_row && g.center_col(tj) == c) {
                     if (visits) visits[k] = 0;
                 } else {
@@ -652,6 +668,7 @@ __global__ void __launch_bounds__(256)
                     }
                 }
             }
+            cur = nxt;
         }
     }
     n_elim = warp_sum(n_elim);
