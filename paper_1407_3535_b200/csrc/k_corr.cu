@@ -212,10 +212,11 @@ __global__ void __launch_bounds__(256)
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
     const int nrows = g.ti_hi - g.ti_lo;
-    const long long total = (long long)nrows * nc;
-    for (long long it = blockIdx.x * (long long)blockDim.x + threadIdx.x; it < total;
-         it += (long long)gridDim.x * blockDim.x) {
-        const int yi = int(it / nc), k = int(it % nc);
+    const unsigned total = unsigned(nrows) * unsigned(nc);  // group count: < 2^32
+    for (unsigned it = blockIdx.x * blockDim.x + threadIdx.x; it < total;
+         it += gridDim.x * blockDim.x) {
+        const unsigned yq = it / unsigned(nc);  // 32-bit division (a 64-bit one per centre
+        const int yi = int(yq), k = int(it - yq * unsigned(nc));  // cost more than the epilogue)
         const int r = rows[yi];
         const int c = (c_last >= 0 && col0 + k == g.tc - 1) ? c_last : cbase + k * sw;
         const size_t gi = size_t(g.ti_lo + yi) * g.tc + col0 + k;

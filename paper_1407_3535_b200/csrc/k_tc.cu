@@ -454,28 +454,36 @@ __global__ void k_tc_build_b(const float* __restrict__ tf, int npad, int m, int 
     const int ch = blockIdx.y;
     const int i0 = P.i0[ch], i1 = P.i1[ch];
     const int entries = i1 - i0;
-    const size_t bytes = size_t(entries) * 16 * P.kx;
     uint8_t* o = out + P.b_off[ch];
     const int sbo = 128 * (P.kx / 16);
-    for (size_t idx = blockIdx.x * size_t(blockDim.x) + threadIdx.x; idx < bytes;
-         idx += size_t(gridDim.x) * blockDim.x) {
-        const int e = int(idx / (size_t(16) * P.kx));
-        const int rem = int(idx - size_t(e) * 16 * P.kx);
-        const int ph = rem / P.kx, t = rem - ph * P.kx;
+    const int nk16 = P.kx / 16;
+    // one thread per 16-byte run of one (entry, phase) row: the run is contiguous in the
+    // core-matrix layout ((t/16)*128 + t%16) and in the template row, one 16-byte store
+    const unsigned total = unsigned(entries) * 16u * unsigned(nk16);
+    for (unsigned idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += gridDim.x * blockDim.x) {
+        const unsigned eph = idx / unsigned(nk16);
+        const int t16 = int(idx - eph * unsigned(nk16));
+        const int e = int(eph >> 4), ph = int(eph & 15u);
         // entry e -> (class, position) -> template row i
         int cls = 0;
         while (cls + 1 < P.sr && P.cls_off[ch][cls + 1] <= e) ++cls;
         const int i = P.cls_max[ch][cls] - P.sr * (e - P.cls_off[ch][cls]);
-        const int j = t - ph;
-        uint8_t val = 0;
-        if (i >= i0 && i < i1 && j >= 0 && j < n) val = uint8_t(tf[size_t(i) * npad + j]);
+        const bool row_ok = i >= i0 && i < i1;
+        const float* trow = tf + size_t(row_ok ? i : 0) * npad;
+        unsigned w[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int bb = 0; bb < 16; ++bb) {
+            const int j = t16 * 16 + bb - ph;
+            const unsigned v = (row_ok && j >= 0 && j < n) ? unsigned(trow[j]) : 0u;
+            w[bb >> 2] |= v << (8 * (bb & 3));
+        }
         const int row = e * 16 + ph;
-        o[size_t(row / 8) * sbo + (row % 8) * 16 + (t / 16) * 128 + (t % 16)] = val;
+        *reinterpret_cast<uint4*>(o + size_t(row / 8) * sbo + (row % 8) * 16 + t16 * 128) =
+            make_uint4(w[0], w[1], w[2], w[3]);
     }
 }
 
-// Pitched zero-padded copy, one 16-byte output chunk per thread (pitch % 16 == 0): 16-byte
-// loads when the source rows are 16-byte aligned (q % 16 == 0), byte loads otherwise.
 __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_t* __restrict__ out,
                            int pitch, int rows) {
     const int cpr = pitch >> 4;  // chunks per row
