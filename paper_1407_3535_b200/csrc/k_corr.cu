@@ -345,30 +345,6 @@ __global__ void __launch_bounds__(256)
 }
 
 __global__ void __launch_bounds__(256)
-    k_centres_f64(CorrJob job, Grid g, double* rho_c, uint8_t* deg_c, CellH* partials) {
-    __shared__ Cell scratch[8];
-    const long long G = (long long)g.tr * g.tc;
-    const TStats ts = to_ts(job.ts);
-    Cell best = no_cell();
-    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
-         gi += (long long)gridDim.x * blockDim.x) {
-        const int ti = int(gi / g.tc), tj = int(gi % g.tc);
-        const int r = g.center_row(ti), c = g.center_col(tj);
-        const size_t kk = size_t(r) * job.st.ec + c;
-        const bool wflat = job.st.flat[kk];
-        const double rho = (ts.flat || wflat) ? 0.0
-                                              : zncc_epilogue(dot_f64(job, r, c), ts, job.st.mu[kk],
-                                                              job.st.omega[kk], wflat);
-        rho_c[gi] = rho;
-        deg_c[gi] = ts.flat || wflat;
-        const Cell cand = make_cell(r, c, rho, ts.flat || wflat);
-        if (better(cand, best)) best = cand;
-    }
-    best = block_best(best, scratch);
-    if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
-}
-
-__global__ void __launch_bounds__(256)
     k_dense_f64(CorrJob job, double* surface, CellH* partials) {
     __shared__ Cell scratch[8];
     const long long E = (long long)job.st.er * job.st.ec;
@@ -477,13 +453,6 @@ __device__ void tail_reduce(const TailReduce& tr, Cell* scratch) {
         apply_reduce_op(best, tr.out, tr.op);
         *tr.ticket = 0u;
     }
-}
-
-__global__ void k_copy_u64(const unsigned long long* src, unsigned long long* dst, int n,
-                           const unsigned long long* src1, unsigned long long* dst1) {
-    pdl_wait();
-    for (int i = 0; i < n; ++i) dst[i] = src[i];
-    if (src1) *dst1 = *src1;
 }
 
 __global__ void k_egs_init(int* stop, double* prev, unsigned long long* nr4, int* h_acc,
@@ -888,11 +857,6 @@ cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned l
     return cudaGetLastError();
 }
 
-cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint8_t* deg_c,
-                             CellH* partials, int n_partials, cudaStream_t s) {
-    k_centres_f64<<<n_partials, 256, 0, s>>>(job, to_grid(g), rho_c, deg_c, partials);
-    return cudaGetLastError();
-}
 
 cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
                            cudaStream_t s) {
@@ -929,11 +893,6 @@ cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t 
                          const ReduceOp* op) {
     launch_pdl(k_reduce_cells, dim3(1), dim3(1024), 0, s, partials, n, out, op ? *op : ReduceOp{});
     return cudaGetLastError();
-}
-
-cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s,
-                     const unsigned long long* src1, unsigned long long* dst1) {
-    return launch_pdl(k_copy_u64, dim3(1), dim3(1), 0, s, src, dst, n, src1, dst1);
 }
 
 cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s, int* h_acc,

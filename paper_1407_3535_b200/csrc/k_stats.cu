@@ -340,10 +340,6 @@ __global__ void k_stats_from_sums(const double* __restrict__ S, const double* __
 }
 
 // stats.cpp:80-81: prefix_noise = double(rows + cols) * eps * q_total
-__global__ void k_prefix_noise_u64(const unsigned long long* q_total, int rows, int cols,
-                                   double* out) {
-    *out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), double(*q_total));
-}
 __global__ void k_prefix_noise_f64(const double* q_total, int rows, int cols, double* out) {
     *out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), *q_total);
 }

@@ -226,8 +226,6 @@ cudaError_t corr_list(const CorrJob& job, const int2* locs, const unsigned long 
 cudaError_t corr_list_f64(const CorrJob& job, const int2* locs, const unsigned long long* count,
                           int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                           int n_partials, cudaStream_t s, int rho_by_loc = 0);
-cudaError_t corr_centres_f64(const CorrJob& job, GridDesc g, double* rho_c, uint8_t* deg_c,
-                             CellH* partials, int n_partials, cudaStream_t s);
 cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials, int n_partials,
                            cudaStream_t s);
 
@@ -244,8 +242,6 @@ cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc,
 cudaError_t reduce_cells(const CellH* partials, int n, CellH* out, cudaStream_t s,
                          const ReduceOp* op = nullptr);
 // dst[i] = src[i] for i < n (one thread; dst may be mapped pinned host memory).
-cudaError_t copy_u64(const unsigned long long* src, unsigned long long* dst, int n, cudaStream_t s,
-                     const unsigned long long* src1 = nullptr, unsigned long long* dst1 = nullptr);
 // EGS batch start: stop = 0, prev cost = +inf, nr[0..3] = 0 (one launch).
 cudaError_t egs_init(int* stop, double* prev, unsigned long long* nr4, cudaStream_t s,
                      int* h_acc = nullptr, unsigned long long* gate = nullptr);
