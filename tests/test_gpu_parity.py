@@ -485,3 +485,21 @@ def test_search_upload_undecided_windows(ctx, port, dense):
     want = ctx.search(a, t, policy="seeded")
     for k in ("best_row", "best_col", "best_rho", "eliminated", "retained", "final_threshold"):
         assert getattr(got, k) == getattr(want, k), k
+
+
+@pytest.mark.parametrize("m,n", [(1, 1), (2, 2), (3, 4), (4, 3), (5, 5), (2, 9), (7, 15), (1, 30)])
+def test_group_column_autocorr_small_windows(ctx, port, m, n):
+    """The group-column R_co kernel at window widths below, at and just above the group
+    width (n < h: head columns only, no whole blocks; n % h == 0: no head), one-row extents
+    and every clipped last group column, h = 3 and 5, equal to the oracle with counts."""
+    rng = np.random.default_rng(m * 31 + n)
+    for rows, cols in ((m + 2, 263), (m, 131), (m + 11, 517)):
+        img = rng.integers(0, 256, (rows, cols)).astype(np.uint8)
+        img[:, 40:70] = 128  # flat columns: degenerate members
+        gi = ctx.image(img)
+        for h in (3, 5):
+            want = port.local_autocorrelation(img.astype(np.float64), m, n, h, h)
+            got = ctx.local_autocorrelation(gi, m, n, h, h)
+            assert np.array_equal(got, want), (rows, cols, h, np.argwhere(got != want)[:3])
+            assert ctx.autocorr_retained(gi, m, n, h, h) == port.retained_count(want, h, h)
+        gi.close()
