@@ -214,6 +214,14 @@ int tm_search_u8(tm_ctx* ctx, tm_image* img, const uint8_t* tmpl, int m, int n,
  * tm_search_u8). */
 int tm_search_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels, const uint8_t* tmpl,
                         int m, int n, const tm_match_params* params, tm_match_result* out);
+/* A stream of matches (match, matcher.hpp:80, once per image; the reference CLI's bench
+ * loop over a corpus, cli.cpp:239-293): nimg 8-bit host images of rows x cols, one 8-bit
+ * template.  out[i] equals tm_search_upload_u8 on images[i].  Two device image slots owned
+ * by the context: image i+1 is copied on a copy stream while image i is searched, so with
+ * pinned host buffers the PCIe transfer hides behind the previous search. */
+int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int rows, int cols,
+                        const uint8_t* tmpl, int m, int n, const tm_match_params* params,
+                        tm_match_result* out);
 
 /* transitive_search (matcher.hpp:37-38) with a caller-supplied map/grid. */
 int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,

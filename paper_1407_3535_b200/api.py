@@ -367,6 +367,26 @@ class Context:
                                             C.byref(p), C.byref(res)))
         return res
 
+    def search_stream(self, images, t, mode="egs", **kw):
+        """match over a stream of 8-bit host images with one template
+        (tm_search_stream_u8): image i+1 crosses PCIe while image i is searched.  `images`
+        is a sequence of equally shaped uint8 arrays (pinned memory for an overlapped copy);
+        returns one MatchResult per image."""
+        imgs = [np.ascontiguousarray(a, dtype=np.uint8) for a in images]
+        if not imgs:
+            return []
+        shape = imgs[0].shape
+        if len(shape) != 2 or any(a.shape != shape for a in imgs):
+            raise ValueError("search_stream: images must be equally shaped 2-D arrays")
+        t = np.ascontiguousarray(t, dtype=np.uint8)
+        m, n = t.shape
+        p = make_params(mode=mode, **kw)
+        ptrs = (C.c_void_p * len(imgs))(*[a.ctypes.data for a in imgs])
+        res = (MatchResult * len(imgs))()
+        N.check(N.lib().tm_search_stream_u8(self.h, ptrs, len(imgs), shape[0], shape[1],
+                                            _u8ptr(t), m, n, C.byref(p), res))
+        return list(res)
+
     def match(self, t, image, mode="egs", record_visits=False, **kw):
         """match (matcher.hpp:80): host buffers in, host result out (end to end)."""
         t = np.ascontiguousarray(t, dtype=np.float64)

@@ -206,6 +206,7 @@ struct WS {
 };
 
 struct tm_ctx {
+    ~tm_ctx();
     int device = 0;
     cudaStream_t s = nullptr;
     std::mutex mu;
@@ -281,6 +282,11 @@ struct tm_ctx {
         const int* rows_dev = nullptr;
     } spec;
     std::map<std::vector<long long>, int> last_he;  // (p, q, m, n, h0, w0) -> last accepted h
+    // streamed searches (tm_search_stream_u8): two device image slots and a copy stream, so
+    // image i+1 crosses PCIe while image i is searched
+    cudaStream_t s_up = nullptr;
+    cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
+    std::unique_ptr<tm_image> sslot[2];
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -351,6 +357,11 @@ struct tm_image {
     int u8p_pitch = 0;
     int u8p_rows = 0;
 };
+
+tm_ctx::~tm_ctx() {
+    sslot[0].reset();  // stream-ordered frees on s, before the scratch buffers
+    sslot[1].reset();
+}
 
 struct tm_prep {
     tm_match_params params{};
@@ -1994,6 +2005,14 @@ void ctx_release(tm_ctx* ctx) {
     if (ctx->ev_b0) cudaEventDestroy(ctx->ev_b0);
     if (ctx->ev_b1) cudaEventDestroy(ctx->ev_b1);
     if (ctx->hres) cudaFreeHost(ctx->hres);
+    if (ctx->s_up) {
+        cudaStreamSynchronize(ctx->s_up);
+        cudaStreamDestroy(ctx->s_up);
+    }
+    for (int k = 0; k < 2; ++k) {
+        if (ctx->ev_up[k]) cudaEventDestroy(ctx->ev_up[k]);
+        if (ctx->ev_free[k]) cudaEventDestroy(ctx->ev_free[k]);
+    }
     delete ctx;  // stream-ordered frees of the scratch buffers
     cudaStreamSynchronize(st);
     cudaStreamDestroy(st);
@@ -2529,6 +2548,68 @@ int tm_search_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels, const
         std::vector<double> t(size_t(m) * n);
         for (size_t i = 0; i < t.size(); ++i) t[i] = tmpl[i];
         search_resident(ctx, img, t.data(), m, n, params, out);
+    });
+}
+
+int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int rows, int cols,
+                        const uint8_t* tmpl, int m, int n, const tm_match_params* params,
+                        tm_match_result* out) {
+    return guard(ctx, [&] {
+        if (!images || !tmpl || !params || !out) invalid("tm_search_stream_u8: null argument");
+        if (nimg < 0) invalid("tm_search_stream_u8: negative image count");
+        if (rows < 1 || cols < 1) invalid("image dimensions must be at least 1x1");
+        if (m < 1 || n < 1) invalid("tm_search_stream_u8: invalid template");
+        for (int i = 0; i < nimg; ++i)
+            if (!images[i]) invalid("tm_search_stream_u8: null image pointer");
+        if (nimg == 0) return;
+        if (!ctx->s_up) {
+            CK(cudaStreamCreateWithFlags(&ctx->s_up, cudaStreamNonBlocking));
+            for (int k = 0; k < 2; ++k) {
+                CK(cudaEventCreateWithFlags(&ctx->ev_up[k], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&ctx->ev_free[k], cudaEventDisableTiming));
+            }
+        }
+        for (int k = 0; k < 2; ++k) {
+            auto& sl = ctx->sslot[k];
+            if (!sl || sl->p != rows || sl->q != cols) {
+                sl.reset();  // stream-ordered free
+                sl = std::make_unique<tm_image>();
+                sl->ctx = ctx;  // internal: owned by the context, no reference
+                sl->p = rows;
+                sl->q = cols;
+                sl->integer = true;
+                sl->pitch = ((cols + 3) & ~3) + 128;
+                alloc_u8(ctx, sl.get());
+            }
+            // the slot's buffer is free (allocated / last read) at this point of stream s
+            CK(cudaEventRecord(ctx->ev_free[k], ctx->s));
+        }
+        std::vector<double> t(size_t(m) * n);
+        for (size_t i = 0; i < t.size(); ++i) t[i] = tmpl[i];
+        const size_t N = size_t(rows) * cols;
+        auto enqueue_upload = [&](int i) {
+            const int k = i & 1;
+            CK(cudaStreamWaitEvent(ctx->s_up, ctx->ev_free[k], 0));
+            CK(cudaMemcpyAsync(ctx->sslot[k]->u8.p, images[i], N, cudaMemcpyHostToDevice,
+                               ctx->s_up));
+            CK(cudaEventRecord(ctx->ev_up[k], ctx->s_up));
+        };
+        enqueue_upload(0);
+        for (int i = 0; i < nimg; ++i) {
+            tm_image* img = ctx->sslot[i & 1].get();
+            HT("start");
+            CK(cudaEventRecord(ctx->ev0, ctx->s));
+            CK(cudaStreamWaitEvent(ctx->s, ctx->ev_up[i & 1], 0));
+            // the next image crosses PCIe while this one is searched (the other slot's last
+            // reader, search i-1, has completed: search_resident returns after its readback)
+            if (i + 1 < nimg) enqueue_upload(i + 1);
+            img->have_f32 = img->have_f64 = false;
+            img->have_qtotal = false;
+            tc_pitch_copy(ctx, img);
+            img->ws_cache.clear();
+            search_resident(ctx, img, t.data(), m, n, params, &out[i]);
+            CK(cudaEventRecord(ctx->ev_free[i & 1], ctx->s));
+        }
     });
 }
 

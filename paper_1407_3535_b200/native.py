@@ -144,6 +144,9 @@ SIGNATURES = {
                                C.POINTER(MatchResult)]),
     "tm_search_upload_u8": (C.c_int, [_P, _P, _U8, _U8, C.c_int, C.c_int,
                                       C.POINTER(MatchParams), C.POINTER(MatchResult)]),
+    "tm_search_stream_u8": (C.c_int, [_P, C.POINTER(C.c_void_p), C.c_int, C.c_int, C.c_int,
+                                      _U8, C.c_int, C.c_int, C.POINTER(MatchParams),
+                                      C.POINTER(MatchResult)]),
     "tm_transitive_search": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, _D, C.c_int, C.c_int,
                                        C.POINTER(MatchParams), C.POINTER(MatchResult), _U8]),
     "tm_center_scan": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, C.c_int, C.c_int, _D, _U8, _I,

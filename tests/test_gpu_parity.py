@@ -464,6 +464,34 @@ def test_search_upload_streamed_equals_resident(ctx, port, shape):
     _ws_equal(ctx.window_stats(b, m, n), port.window_stats(img.astype(np.float64), m, n))
 
 
+def test_search_stream_equals_single_calls(ctx):
+    """tm_search_stream_u8 over a stream of different images (two device slots, the next
+    copy overlapped with the current search) == tm_search_upload_u8 per image, bit for bit;
+    then a stream with a different shape (slots re-created) and an empty stream."""
+    keys = ("best_row", "best_col", "best_rho", "eliminated", "retained", "centers", "ops",
+            "final_threshold")
+    rng = np.random.default_rng(11)
+    for rows, cols, m, n in [(300, 420, 40, 37), (257, 190, 21, 16)]:
+        imgs = []
+        for k in range(5):
+            base = np.cumsum(np.cumsum(rng.normal(size=(rows, cols)), 0), 1)
+            imgs.append(np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0,
+                                255).astype(np.uint8))
+        src = imgs[2]
+        t = np.clip(np.rint(src[rows // 3:rows // 3 + m, cols // 4:cols // 4 + n] * 1.05 + 3
+                            + rng.normal(0, 3, (m, n))), 0, 255).astype(np.uint8)
+        for policy in ("seeded", "frozen", "sequential"):
+            got = ctx.search_stream(imgs, t, policy=policy)
+            assert len(got) == len(imgs)
+            b = ctx.image(np.zeros((rows, cols), np.uint8))
+            for g, a in zip(got, imgs):
+                want = ctx.search_upload(b, a, t, policy=policy)
+                for k in keys:
+                    assert getattr(g, k) == getattr(want, k), (policy, k)
+            b.close()
+    assert ctx.search_stream([], t) == []
+
+
 @pytest.mark.parametrize("dense", [False, True])
 def test_search_upload_undecided_windows(ctx, port, dense):
     """A 3400 x 3300 image whose noise floor ((rows + cols) * eps * sum of squares, about
