@@ -872,7 +872,8 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
 // 16-byte-pitched zero-padded copy (pitch P, >= p + kU8PadRows rows).
 constexpr int kAcgWb = 8;  // warp-total stride (NT <= 256)
 // staged bytes per ring row: NT*W tile columns + 2*(h/2) for the B offsets + 16-byte alignment
-__host__ __device__ constexpr int acg_span(int nt, int h) { return (15 + nt * h + 2 * (h / 2) + 15) & ~15; }
+// (+8: the packed walk reads two aligned words from up to 3 bytes before a thread's columns)
+__host__ __device__ constexpr int acg_span(int nt, int h) { return (15 + nt * h + 2 * (h / 2) + 8 + 15) & ~15; }
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     const unsigned sa = unsigned(__cvta_generic_to_shared(sdst));
@@ -882,7 +883,16 @@ __device__ __forceinline__ void opaque(unsigned& x) { asm("" : "+r"(x)); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
-template <int H, int NT>
+// NP > 0: packed walk.  A thread's W columns are cut into NP parts (each <= 4 columns) at
+// the column counts its block sums are read at -- R = n % W for every thread, plus the
+// clipped group's tail (W - delta) and head (Rc) on the two threads that provide them --
+// and each part's vertical sum is one dp4a per row step (u8 x u8 -> u32, exact): the A row
+// part words are byte permutes of two aligned shared-memory words, the B row part words
+// (kept in the register ring for H steps) are masked to the part's bytes.  Leading and
+// trailing rows accumulate separately (dp4a only adds) and are subtracted at the events.
+// NP = 2 when the grid has no clipped group column, 3 otherwise; NP = 0 is the per-column
+// walk (one IMAD per column, offset and row step).
+template <int H, int NT, int NP>
 __global__ void __launch_bounds__(NT)
     k_acg(const uint8_t* __restrict__ img, int P, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
@@ -922,17 +932,81 @@ __global__ void __launch_bounds__(NT)
 
     const int y0 = k * W + hr;  // every thread's columns lie inside the staged span
     const int oa = y0 - s0, ob = y0 + dj - s0;
-    unsigned V[H][W], rl[H][W], rt[H][W];
+    // this thread's group column geometry (also used by the packed walk's cuts)
+    const int tcl = g.tc - 1 - k0;  // tile-local index of the clipped group column (if here)
+    constexpr int NPV = NP > 0 ? NP : 1;
+    constexpr int NA = NP > 0 ? NP : W;  // accumulators per row offset
+    unsigned V[H][NA], Vt[H][NP > 0 ? NP : 1], rl[H][NA], rt[H][NA];
+    // packed walk: parts [plo[i], plo[i+1]) of the W columns, selectors and masks
+    unsigned selA[NPV], selB[NPV], mskB[NPV];
+    unsigned pm_h = 0, pm_t = 0, pm_c = 0;  // parts inside the head R / tail / clipped head
+    if constexpr (NP > 0) {
+        int cut[4], nc = 0;
+        auto add_cut = [&](int c) {
+            if (c <= 0 || c >= W) return;
+            for (int i = 0; i < nc; ++i)
+                if (cut[i] == c) return;
+            cut[nc++] = c;
+        };
+        add_cut(R);
+        if (clip_tile && tcl >= 1 && t == tcl - 1) add_cut(W - delta);
+        if (clip_tile && tcl >= 0 && t == tcl + Qc) add_cut(Rc);
+        if (nc == 0 && W > 4) add_cut(4);  // every part fits one 32-bit word
+        for (int i = 1; i < nc; ++i)       // sort (nc <= 3)
+            for (int j = i; j > 0 && cut[j - 1] > cut[j]; --j) {
+                const int x = cut[j];
+                cut[j] = cut[j - 1];
+                cut[j - 1] = x;
+            }
+        const int sha = oa & 3, shb = ob & 3;
+#pragma unroll
+        for (int i = 0; i < NPV; ++i) {
+            const int lo = i == 0 ? 0 : (i - 1 < nc ? cut[i - 1] : W);
+            const int hi = i < nc ? cut[i] : W;
+            unsigned sa = 0, sb = 0, mb = 0;
+            for (int b = 0; b < 4; ++b) {
+                if (lo + b < hi) {
+                    sa |= unsigned(sha + lo + b) << (4 * b);
+                    sb |= unsigned(shb + lo + b) << (4 * b);
+                    mb |= 0xffu << (8 * b);
+                }
+            }
+            selA[i] = sa;
+            selB[i] = sb;
+            mskB[i] = mb;
+            if (hi > lo && hi <= R) pm_h |= 1u << i;
+            if (hi > lo && lo >= W - delta) pm_t |= 1u << i;
+            if (hi > lo && hi <= Rc) pm_c |= 1u << i;
+        }
+    }
+    const int oa4 = NP > 0 ? (oa & ~3) : oa, ob4 = NP > 0 ? (ob & ~3) : ob;
     int cr = g.center_row(ti0);
     stage(cr, m + H + hr);
 #pragma unroll
     for (int d = 0; d < H; ++d) {
         const int xr = max(cr - 1 - hr + d, 0);
+        if constexpr (NP > 0) {
+            // ring prefill from global memory (the staged ring starts at row cr)
+            unsigned w0 = 0, w1 = 0;
+            if (d >= 1) {
+                const uint8_t* src = img + size_t(xr) * P + s0 + ob4;
+                w0 = __ldg(reinterpret_cast<const unsigned*>(src));
+                w1 = __ldg(reinterpret_cast<const unsigned*>(src + 4));
+            }
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-            V[d][j] = 0u;
-            rl[d][j] = d >= 1 ? unsigned(__ldg(img + size_t(xr) * P + y0 + dj + j)) : 0u;
-            rt[d][j] = rl[d][j];
+            for (int i = 0; i < NP; ++i) {
+                V[d][i] = 0u;
+                Vt[d][i] = 0u;
+                rl[d][i] = __byte_perm(w0, w1, selB[i]) & mskB[i];
+                rt[d][i] = rl[d][i];
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+                V[d][j] = 0u;
+                rl[d][j] = d >= 1 ? unsigned(__ldg(img + size_t(xr) * P + y0 + dj + j)) : 0u;
+                rt[d][j] = rl[d][j];
+            }
         }
     }
     // ring byte offsets of the leading / trailing A and B rows (wrap at RR * SW)
@@ -944,53 +1018,85 @@ __global__ void __launch_bounds__(NT)
         if (o >= ring_bytes) o -= ring_bytes;
     };
     auto lead_at = [&](const uint8_t* pa, const uint8_t* pb) {
-        unsigned a[W], b[W];
+        if constexpr (NP > 0) {
+            const unsigned a0 = *reinterpret_cast<const unsigned*>(pa);
+            const unsigned a1 = *reinterpret_cast<const unsigned*>(pa + 4);
+            const unsigned b0 = *reinterpret_cast<const unsigned*>(pb);
+            const unsigned b1 = *reinterpret_cast<const unsigned*>(pb + 4);
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-            b[j] = pb[j];
-            a[j] = pa[j];
-            opaque(a[j]);  // plain IMADs: keeps nvcc from packing bytes into IDP (PRMT-heavy)
-            opaque(b[j]);
-        }
+            for (int i = 0; i < NP; ++i) {
+                const unsigned aw = __byte_perm(a0, a1, selA[i]);  // bytes past the part: x 0
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
+                for (int d = 0; d < H - 1; ++d) rl[d][i] = rl[d + 1][i];
+                rl[H - 1][i] = __byte_perm(b0, b1, selB[i]) & mskB[i];
 #pragma unroll
-            for (int d = 0; d < H - 1; ++d) rl[d][j] = rl[d + 1][j];
-            rl[H - 1][j] = b[j];
+                for (int d = 0; d < H; ++d) V[d][i] = __dp4a(aw, rl[d][i], V[d][i]);
+            }
+        } else {
+            unsigned a[W], b[W];
 #pragma unroll
-            for (int d = 0; d < H; ++d) V[d][j] += a[j] * rl[d][j];
+            for (int j = 0; j < W; ++j) {
+                b[j] = pb[j];
+                a[j] = pa[j];
+                opaque(a[j]);  // plain IMADs: keeps nvcc from packing bytes into IDP (PRMT-heavy)
+                opaque(b[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+#pragma unroll
+                for (int d = 0; d < H - 1; ++d) rl[d][j] = rl[d + 1][j];
+                rl[H - 1][j] = b[j];
+#pragma unroll
+                for (int d = 0; d < H; ++d) V[d][j] += a[j] * rl[d][j];
+            }
         }
     };
     auto trail_at = [&](const uint8_t* pa, const uint8_t* pb) {
-        unsigned a[W], b[W];
+        if constexpr (NP > 0) {
+            const unsigned a0 = *reinterpret_cast<const unsigned*>(pa);
+            const unsigned a1 = *reinterpret_cast<const unsigned*>(pa + 4);
+            const unsigned b0 = *reinterpret_cast<const unsigned*>(pb);
+            const unsigned b1 = *reinterpret_cast<const unsigned*>(pb + 4);
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
-            b[j] = pb[j];
-            // h = 5: negated once so the H updates are single IMADs (measured: h = 3 is
-            // faster with the plain subtraction, which nvcc schedules better there)
-            a[j] = H >= 5 ? 0u - unsigned(pa[j]) : unsigned(pa[j]);
-            opaque(a[j]);
-            opaque(b[j]);
-        }
+            for (int i = 0; i < NP; ++i) {
+                const unsigned aw = __byte_perm(a0, a1, selA[i]);
 #pragma unroll
-        for (int j = 0; j < W; ++j) {
+                for (int d = 0; d < H - 1; ++d) rt[d][i] = rt[d + 1][i];
+                rt[H - 1][i] = __byte_perm(b0, b1, selB[i]) & mskB[i];
 #pragma unroll
-            for (int d = 0; d < H - 1; ++d) rt[d][j] = rt[d + 1][j];
-            rt[H - 1][j] = b[j];
+                for (int d = 0; d < H; ++d) Vt[d][i] = __dp4a(aw, rt[d][i], Vt[d][i]);
+            }
+        } else {
+            unsigned a[W], b[W];
 #pragma unroll
-            for (int d = 0; d < H; ++d) {
-                if (H >= 5) V[d][j] += a[j] * rt[d][j];  // exact mod 2^32
-                else V[d][j] -= a[j] * rt[d][j];
+            for (int j = 0; j < W; ++j) {
+                b[j] = pb[j];
+                // h = 5: negated once so the H updates are single IMADs (measured: h = 3 is
+                // faster with the plain subtraction, which nvcc schedules better there)
+                a[j] = H >= 5 ? 0u - unsigned(pa[j]) : unsigned(pa[j]);
+                opaque(a[j]);
+                opaque(b[j]);
+            }
+#pragma unroll
+            for (int j = 0; j < W; ++j) {
+#pragma unroll
+                for (int d = 0; d < H - 1; ++d) rt[d][j] = rt[d + 1][j];
+                rt[H - 1][j] = b[j];
+#pragma unroll
+                for (int d = 0; d < H; ++d) {
+                    if (H >= 5) V[d][j] += a[j] * rt[d][j];  // exact mod 2^32
+                    else V[d][j] -= a[j] * rt[d][j];
+                }
             }
         }
     };
     auto lead = [&]() {
-        lead_at(ring + la + oa, ring + lb + ob);
+        lead_at(ring + la + oa4, ring + lb + ob4);
         bump(la, SW);
         bump(lb, SW);
     };
     auto trail = [&]() {
-        trail_at(ring + ta + oa, ring + tb + ob);
+        trail_at(ring + ta + oa4, ring + tb + ob4);
         bump(ta, SW);
         bump(tb, SW);
     };
@@ -998,8 +1104,8 @@ __global__ void __launch_bounds__(NT)
     const int lim = ring_bytes - (H - 1) * SW;
     auto advance_lead = [&]() {
         if (la < lim && lb < lim) {
-            const uint8_t* pa = ring + la + oa;
-            const uint8_t* pb = ring + lb + ob;
+            const uint8_t* pa = ring + la + oa4;
+            const uint8_t* pb = ring + lb + ob4;
 #pragma unroll
             for (int s = 0; s < H; ++s) lead_at(pa + s * SW, pb + s * SW);
             bump(la, H * SW);
@@ -1011,10 +1117,10 @@ __global__ void __launch_bounds__(NT)
     };
     auto advance_both = [&]() {
         if (la < lim && lb < lim && ta < lim && tb < lim) {
-            const uint8_t* pa = ring + la + oa;
-            const uint8_t* pb = ring + lb + ob;
-            const uint8_t* qa = ring + ta + oa;
-            const uint8_t* qb = ring + tb + ob;
+            const uint8_t* pa = ring + la + oa4;
+            const uint8_t* pb = ring + lb + ob4;
+            const uint8_t* qa = ring + ta + oa4;
+            const uint8_t* qb = ring + tb + ob4;
 #pragma unroll
             for (int s = 0; s < H; ++s) {
                 lead_at(pa + s * SW, pb + s * SW);
@@ -1092,12 +1198,23 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
             for (int d = 0; d < H; ++d) {
                 unsigned bs = 0u, hh = 0u, tt = 0u, hc = 0u;
+                if constexpr (NP > 0) {
 #pragma unroll
-                for (int j = 0; j < W; ++j) {
-                    bs += V[d][j];
-                    if (j < R) hh += V[d][j];
-                    if (j >= W - delta) tt += V[d][j];
-                    if (j < Rc) hc += V[d][j];
+                    for (int i = 0; i < NP; ++i) {
+                        const unsigned x = V[d][i] - Vt[d][i];  // exact mod 2^32
+                        bs += x;
+                        if ((pm_h >> i) & 1u) hh += x;
+                        if ((pm_t >> i) & 1u) tt += x;
+                        if ((pm_c >> i) & 1u) hc += x;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < W; ++j) {
+                        bs += V[d][j];
+                        if (j < R) hh += V[d][j];
+                        if (j >= W - delta) tt += V[d][j];
+                        if (j < Rc) hc += V[d][j];
+                    }
                 }
                 v[d] = bs;
                 Hh[d * NT + t] = hh;
@@ -1246,28 +1363,56 @@ bool acg_enabled() {
     return on;
 }
 
-template <int H, int NT>
+template <int H, int NT, int NP>
 cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
                           cudaStream_t s) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_acg<H, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_acg<H, NT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kAcgSmemMax));
         attr = true;
     }
     const AcgGeom a0 = acg_geom(m, n, gd, NT);
     if (a0.nt == 0) return cudaErrorInvalidValue;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acg<H, NT>, NT, a0.smem) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acg<H, NT, NP>, NT, a0.smem) !=
+        cudaSuccess)
         occ = 0;
     const AcgGeom a = acg_geom(m, n, gd, NT, occ);
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
-        launch_pdl(k_acg<H, NT>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n, to_grid(gd), st,
-                   thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi);
+        launch_pdl(k_acg<H, NT, NP>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n, to_grid(gd),
+                   st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi);
     return cudaGetLastError();
+}
+
+// Packed (dp4a) walk for h = 5 (NP = 2 without a clipped group column, else 3); the
+// per-column walk for h = 3, where a packed row step saves nothing (W = 3 columns: two
+// parts cost as many loads and permutes as three IMADs).  TMATCH_ACG_PACK=0|1 forces the
+// per-column / packed walk for both sizes (A/B measurements, parity tests).
+int acg_pack(int h) {
+    static int forced = [] {
+        const char* e = std::getenv("TMATCH_ACG_PACK");
+        return e ? (std::atoi(e) ? 1 : 0) : -1;
+    }();
+    return forced >= 0 ? forced : (h >= 5 ? 1 : 0);
+}
+
+template <int H, int NT>
+cudaError_t launch_acg_np(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
+                          DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
+                          const double* egs_prev, double egs_central, double egs_xi,
+                          cudaStream_t s) {
+    if (!acg_pack(H))
+        return launch_acg_nt<H, NT, 0>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                       egs_prev, egs_central, egs_xi, s);
+    if (gd.ec % gd.w == 0)
+        return launch_acg_nt<H, NT, 2>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                       egs_prev, egs_central, egs_xi, s);
+    return launch_acg_nt<H, NT, 3>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
+                                   egs_central, egs_xi, s);
 }
 
 template <int H>
@@ -1275,9 +1420,9 @@ cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, Grid
                        DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                        const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
     if (acg_threads(H) == 128)
-        return launch_acg_nt<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
+        return launch_acg_np<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
                                      egs_central, egs_xi, s);
-    return launch_acg_nt<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
+    return launch_acg_np<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
                                  egs_central, egs_xi, s);
 }
 

@@ -1,7 +1,8 @@
 """The A/B kernel variants behind the environment switches give
 the oracle's bits too.  The switches are read once per process, so every variant runs in
-a subprocess: window statistics, R_co maps and retained counts for h = 3, 5, 7 on two
-image shapes (multi-tile, clipped group columns), compared with the oracle."""
+a subprocess: window statistics, R_co maps and retained counts for h = 3, 5, 7 on four
+image shapes (multi-tile; clipped and unclipped group columns; n % h = 0 and != 0, i.e.
+every packed-walk part layout), compared with the oracle."""
 import os
 import subprocess
 import sys
@@ -21,7 +22,8 @@ from oracle.binding import Oracle
 port = Oracle("port")
 ctx = api.Context(0)
 rng = np.random.default_rng(5)
-for (rows, cols, m, n) in ((150, 1300, 40, 64), (120, 700, 33, 10)):
+for (rows, cols, m, n) in ((150, 1300, 40, 64), (120, 700, 33, 10), (140, 1063, 36, 64),
+                          (90, 619, 20, 20)):
     base = np.cumsum(np.cumsum(rng.normal(size=(rows, cols)), 0), 1)
     img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0, 255).astype(np.uint8)
     img[10:40, 50:120] = 60
@@ -44,6 +46,10 @@ print("ok")
     {"TMATCH_ACF": "column"},
     {"TMATCH_ACG_THREADS": "128"},
     {"TMATCH_ACG_THREADS": "256"},
+    {"TMATCH_ACG_PACK": "0"},
+    {"TMATCH_ACG_PACK": "1"},
+    {"TMATCH_ACG_PACK": "1", "TMATCH_ACG_THREADS": "256"},
+    {"TMATCH_ACG_PACK": "1", "TMATCH_ACG_THREADS": "128"},
     {"TMATCH_AUTOCORR": "colwalk"},
     {"TMATCH_WSTATS": "column"},
     {"TMATCH_WSTATS4": "256x4"},
