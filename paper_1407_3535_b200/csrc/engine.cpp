@@ -1084,7 +1084,9 @@ void spec_centre(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const 
 bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDesc& g,
                      double thr, double* map, unsigned long long* nr, int* stop = nullptr,
                      const double* egs_prev = nullptr, double egs_xi = 0.0,
-                     bool count_only = false) {
+                     bool count_only = false, const tmk::EgsDecide* dec = nullptr,
+                     bool* decided = nullptr) {
+    if (decided) *decided = false;
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     if (!egs_prev) CK(cudaMemsetAsync(nr, 0, 8, ctx->s));  // EGS batches: egs_init zeroes it
     // (count-only candidates are timed apart: their work stops at the EGS rejection point)
@@ -1102,7 +1104,7 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr,
                                       count_only ? nullptr : map, nr, stop, ctx->s, egs_prev,
                                       central, egs_xi, pitched ? img->u8p.p : nullptr,
-                                      img->u8p_pitch));
+                                      img->u8p_pitch, dec, decided));
             ctx->add(1);
             return !count_only;
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
@@ -1266,17 +1268,40 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         for (int k = 0; k < nc; ++k) {
             const tmk::GridDesc g = make_grid(er, ec, cand[k].h, cand[k].w);
             ctx->egs_maps[k].ensure(E);
+            // the decision after the candidate (after the last one too: the speculation gate
+            // needs the final decision, and that decide also writes the counts + gate into
+            // the mapped pinned block); fused into the R_co launch's tail where supported
+            const bool last = k + 1 == nc;
+            tmk::EgsDecide dec{};
+            dec.ticket = reinterpret_cast<unsigned*>(ctx->counters.p + 27);
+            dec.n_r = ctx->counters.p + 8 + k;
+            dec.prev = dprev;
+            dec.stop = dstop;
+            dec.er = er;
+            dec.ec = ec;
+            dec.h = cand[k].h;
+            dec.w = cand[k].w;
+            dec.xi = xi;
+            dec.cap = cap;
+            dec.h_acc = dhacc;
+            dec.want = ctx->spec_want;
+            dec.gate = dgate;
+            dec.nr_all = ctx->counters.p + 8;
+            dec.nc = nc;
+            dec.out = last ? ctx->hres_dev : nullptr;
+            dec.seq = batch_seq;
+            bool decided = false;
             map_written[k] = autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p,
                                              ctx->counters.p + 8 + k, dstop, dprev, xi,
-                                             /*count_only=*/!(cand[k].h == pred && cand[k].w == pred));
-            // (after the last candidate too: the speculation gate needs the final decision,
-            // and that decide also writes the counts + gate into the mapped pinned block)
-            const bool last = k + 1 == nc;
-            CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
-                               cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
-                               ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr,
-                               batch_seq));
-            ctx->add(1);
+                                             /*count_only=*/!(cand[k].h == pred && cand[k].w == pred),
+                                             &dec, &decided);
+            if (!decided) {
+                CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
+                                   cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
+                                   ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr,
+                                   batch_seq));
+                ctx->add(1);
+            }
         }
         // the host waits for this point only, so work enqueued by the hook keeps the device
         // busy meanwhile

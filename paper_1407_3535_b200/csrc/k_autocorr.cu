@@ -851,6 +851,52 @@ cudaError_t launch_acf(const uint8_t* img, int p, int q, int m, int n, GridDesc 
     return cudaGetLastError();
 }
 
+__device__ void egs_decide_run(const EgsDecide& d) {
+    if (!*d.stop) {
+        const double central =
+            __dmul_rn(double((d.er + d.h - 1) / d.h), double((d.ec + d.w - 1) / d.w));
+        const double total = __dadd_rn(__dadd_rn(central, double(*d.n_r)), 0.0);
+        const double prev = *d.prev;
+        const bool first = !(fabs(prev) <= 1.7976931348623157e308);  // !isfinite
+        const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(d.xi, prev);
+        if (!accepted) {
+            *d.stop = 1;
+        } else {
+            *d.prev = total;
+            *d.h_acc = d.h;
+            if ((d.h >= d.er && d.w >= d.ec) || (d.h >= d.cap && d.w >= d.cap)) *d.stop = 1;
+        }
+    }
+    // (a stop set at entry came from an earlier decision or from the candidate's own
+    // in-kernel rejection; either way h_acc is final)
+    const unsigned long long gv = (*d.stop && d.want > 0 && *d.h_acc == d.want) ? 1ull : 0ull;
+    *d.gate = gv;
+    if (d.out) {  // last candidate of the batch: counts + gate into the mapped result block
+        for (int i = 0; i < d.nc; ++i) d.out->nr[i] = d.nr_all[i];
+        d.out->spec = gv;
+        __threadfence_system();  // counts visible to the host before the sequence number
+        *reinterpret_cast<volatile unsigned long long*>(&d.out->seq) = d.seq;
+    }
+}
+
+// Tail of a fused R_co launch: every thread of every block calls it once, after the block's
+// count is published; the last block to take a ticket runs the decision.
+__device__ __forceinline__ void egs_tail(const EgsDecide& d) {
+    if (!d.ticket) return;  // uniform
+    __shared__ int is_last;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        is_last = atomicAdd(d.ticket, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+    }
+    __syncthreads();
+    if (is_last && threadIdx.x == 0) {
+        __threadfence();
+        *d.ticket = 0u;
+        egs_decide_run(d);
+    }
+}
+
 // ---- fused R_co, one thread per group column (square groups, h <= 5) ----------------------
 //
 // The walk of k_acf, but thread t owns the W = h image columns [cc_k, cc_k + W) of group
@@ -897,9 +943,8 @@ __global__ void __launch_bounds__(NT)
     k_acg(const uint8_t* __restrict__ img, int P, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
           int seg, int RR, int* __restrict__ stop, const double* __restrict__ egs_prev,
-          double egs_central, double egs_xi) {
+          double egs_central, double egs_xi, EgsDecide dec) {
     pdl_wait();
-    if (stop && *stop) return;
     constexpr int W = H, hr = H / 2;
     constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
     constexpr int NCH = SW / 16;
@@ -908,7 +953,18 @@ __global__ void __launch_bounds__(NT)
     const int k0 = blockIdx.y * G;
     const int ti0 = g.ti_lo + blockIdx.z * seg;
     const int ti1 = min(ti0 + seg, g.ti_hi);
-    if (ti0 >= ti1 || k0 >= g.tc) return;  // uniform
+    {
+        // skipped candidate (an earlier decision stopped EGS) or empty block: one read of
+        // the flag per block so the exit is uniform
+        __shared__ int skip;
+        if (t == 0) skip = (stop && *reinterpret_cast<volatile int*>(stop)) || ti0 >= ti1 ||
+                           k0 >= g.tc;
+        __syncthreads();
+        if (skip) {
+            egs_tail(dec);
+            return;
+        }
+    }
     const int k = k0 + t;
     const int Q = n / W, R = n - Q * W;
     const int wl = g.ec - (g.tc - 1) * W;  // width of the last group column
@@ -1300,6 +1356,7 @@ __global__ void __launch_bounds__(NT)
     }
     __syncthreads();
     if (t == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
+    egs_tail(dec);
 }
 
 struct AcgGeom {
@@ -1367,7 +1424,7 @@ template <int H, int NT, int NP>
 cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
-                          cudaStream_t s) {
+                          cudaStream_t s, const EgsDecide& dec) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_acg<H, NT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1384,7 +1441,8 @@ cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, G
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
         launch_pdl(k_acg<H, NT, NP>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n, to_grid(gd),
-                   st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi);
+                   st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi,
+                   dec);
     return cudaGetLastError();
 }
 
@@ -1404,26 +1462,27 @@ template <int H, int NT>
 cudaError_t launch_acg_np(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
-                          cudaStream_t s) {
+                          cudaStream_t s, const EgsDecide& dec) {
     if (!acg_pack(H))
         return launch_acg_nt<H, NT, 0>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                       egs_prev, egs_central, egs_xi, s);
+                                       egs_prev, egs_central, egs_xi, s, dec);
     if (gd.ec % gd.w == 0)
         return launch_acg_nt<H, NT, 2>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                       egs_prev, egs_central, egs_xi, s);
+                                       egs_prev, egs_central, egs_xi, s, dec);
     return launch_acg_nt<H, NT, 3>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                   egs_central, egs_xi, s);
+                                   egs_central, egs_xi, s, dec);
 }
 
 template <int H>
 cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                        DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
-                       const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s) {
+                       const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s,
+                       const EgsDecide& dec) {
     if (acg_threads(H) == 128)
         return launch_acg_np<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                     egs_central, egs_xi, s);
+                                     egs_central, egs_xi, s, dec);
     return launch_acg_np<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                 egs_central, egs_xi, s);
+                                 egs_central, egs_xi, s, dec);
 }
 
 template <int H>
@@ -1634,43 +1693,33 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 // behind the batch for the predicted size `want` runs only then (0 = no speculation).  A
 // stop already set at entry came from an earlier decision or from the candidate's own
 // in-kernel rejection; either way the gate is final.
-__global__ void k_egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er,
-                             int ec, int h, int w, double xi, int cap, int* h_acc, int want,
-                             unsigned long long* gate, const unsigned long long* nr_all, int nc,
-                             ResultBlock* out, unsigned long long seq) {
+__global__ void k_egs_decide(EgsDecide d) {
     pdl_wait();
-    if (!*stop) {
-        const double central = __dmul_rn(double((er + h - 1) / h), double((ec + w - 1) / w));
-        const double total = __dadd_rn(__dadd_rn(central, double(*n_r)), 0.0);
-        const double prev = *prev_cost;
-        const bool first = !(fabs(prev) <= 1.7976931348623157e308);  // !isfinite
-        const bool accepted = first || __dsub_rn(prev, total) > __dmul_rn(xi, prev);
-        if (!accepted) {
-            *stop = 1;
-        } else {
-            *prev_cost = total;
-            *h_acc = h;
-            if ((h >= er && w >= ec) || (h >= cap && w >= cap)) *stop = 1;
-        }
-    }
-    // (a stop set at entry came from an earlier decision or from the candidate's own
-    // in-kernel rejection; either way h_acc is final)
-    const unsigned long long gv = (*stop && want > 0 && *h_acc == want) ? 1ull : 0ull;
-    *gate = gv;
-    if (out) {  // last candidate of the batch: counts + gate into the mapped result block
-        for (int i = 0; i < nc; ++i) out->nr[i] = nr_all[i];
-        out->spec = gv;
-        __threadfence_system();  // counts visible to the host before the sequence number
-        *reinterpret_cast<volatile unsigned long long*>(&out->seq) = seq;
-    }
+    egs_decide_run(d);
 }
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s, const unsigned long long* nr_all,
                        int nc, ResultBlock* out, unsigned long long seq) {
-    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, n_r, prev_cost, stop, er, ec, h, w, xi, cap,
-               h_acc, want, gate, nr_all, nc, out, seq);
+    EgsDecide d{};
+    d.n_r = n_r;
+    d.prev = prev_cost;
+    d.stop = stop;
+    d.er = er;
+    d.ec = ec;
+    d.h = h;
+    d.w = w;
+    d.xi = xi;
+    d.cap = cap;
+    d.h_acc = h_acc;
+    d.want = want;
+    d.gate = gate;
+    d.nr_all = nr_all;
+    d.nc = nc;
+    d.out = out;
+    d.seq = seq;
+    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, d);
     return cudaGetLastError();
 }
 
@@ -1687,14 +1736,19 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               DevStats st, double retain_threshold, double* map,
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev, double egs_central, double egs_xi,
-                              const uint8_t* imgp, int pitch) {
-    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd.h)).nt > 0) {
+                              const uint8_t* imgp, int pitch, const EgsDecide* dec,
+                              bool* decided) {
+    if (decided) *decided = false;
+    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd.h)).nt > 0 &&
+        (gd.h == 3 || gd.h == 5)) {
+        // the EGS decision rides on the launch's tail (no k_egs_decide launch)
+        const EgsDecide d = dec ? *dec : EgsDecide{};
+        if (decided) *decided = d.ticket != nullptr;
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
-                                 egs_prev, egs_central, egs_xi, s);
-        if (gd.h == 5)
-            return launch_acg<5>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
-                                 egs_prev, egs_central, egs_xi, s);
+                                 egs_prev, egs_central, egs_xi, s, d);
+        return launch_acg<5>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
+                             egs_prev, egs_central, egs_xi, s, d);
     }
     switch (gd.h) {
         case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,

@@ -53,6 +53,26 @@ struct ResultBlock {
     double thr;                // threshold after the search
 };
 
+// efficient_group_size's accept/stop step (egs.cpp:61-88) after one candidate: the body of
+// k_egs_decide, optionally fused into the tail of the candidate's R_co launch (the CTA that
+// finishes last runs it; ticket zero between launches, null = not fused).
+struct EgsDecide {
+    unsigned* ticket = nullptr;
+    const unsigned long long* n_r = nullptr;
+    double* prev = nullptr;
+    int* stop = nullptr;
+    int er = 0, ec = 0, h = 0, w = 0;
+    double xi = 0.0;
+    int cap = 0;
+    int* h_acc = nullptr;
+    int want = 0;
+    unsigned long long* gate = nullptr;
+    const unsigned long long* nr_all = nullptr;
+    int nc = 0;
+    ResultBlock* out = nullptr;  // last candidate of a batch: counts + gate for the host
+    unsigned long long seq = 0;
+};
+
 // Work fused into an argmax reduction (saves launches on the search's critical path).
 struct ReduceOp {
     int kind = 0;  // 0 none, 1 threshold init (matcher.cpp:121-125), 2 raise, 3 pack
@@ -151,7 +171,8 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               DevStats st, double retain_threshold, double* map,
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev = nullptr, double egs_central = 0.0,
-                              double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0);
+                              double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0,
+                              const EgsDecide* dec = nullptr, bool* decided = nullptr);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s,
