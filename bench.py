@@ -347,43 +347,58 @@ def run_b200(args):
         return 0
 
     # ---- roofline of the dominant kernel ---------------------------------------------
-    # R_co of the EGS candidates is the dominant phase.  Its full-work launch is the first
-    # candidate (h0, always accepted): the group-column kernel k_acg<3> reads the 8-bit
-    # image once (p*q bytes), the centre/member statistics (mu, omega, flat: 17 B per extent
-    # location) and writes the R_co map (8 B per location).  Later candidates run in
-    # count-only mode and stop at the EGS rejection point (data-dependent work): they are
-    # reported beside it with their measured time.
+    # R_co of the EGS candidates is the dominant phase.  On the tm_search path the first
+    # candidate (h0 = the predicted h_e, always accepted) is the group-column kernel with
+    # scan 2 fused into its epilogue (k_acg<3,256,0,1>): it reads the 8-bit image once (p*q
+    # bytes), the centre/member statistics (mu, omega, flat: 17 B per extent location) and
+    # the scan-1 values of each group (rho_c, sa_c: 8 + 8 B, degenerate + seeded flags: 2 B)
+    # and writes one visit code per location (1 B); the E-sized R_co map is never written.
+    # (TMATCH_FUSE_SCAN2=0: the map-writing launch, p*q + 25 B per location.)  Later
+    # candidates run count-only and stop at the EGS rejection point (data-dependent work):
+    # they are reported beside it with their measured time.
     peaks = _peaks()
     p_, q_ = wl.image.shape
     E = wl.extent
     hbm_peak = peaks.get("hbm_gbs", 6534.1)
     ph_step = max(sum(v["ms"] for v in phases.values()), 1e-9)
-    ac = phases.get("autocorr_u8", {"count": 1, "ms": float("nan")})
+    fused = "autocorr_sec" in phases
+    ac = phases.get("autocorr_sec" if fused else "autocorr_u8", {"count": 1, "ms": float("nan")})
     ac_launch_ms = ac["ms"] / max(ac["count"], 1)
-    ac_bytes = p_ * q_ + 25.0 * E
+    G = res.centers
+    if fused:
+        ac_bytes = p_ * q_ + 18.0 * E + 18.0 * G
+        ac_alg = (f"p*q + 18 B x {E} extent locations (17 B statistics read, 1 B visit code "
+                  f"written) + 18 B x {G} groups (scan-1 rho, half-gap factor, flags)")
+        ac_name = ("k_acg<3,256,0,1> (group-column fused R_co of the first EGS candidate with "
+                   "scan 2 in its epilogue: retained count + bound test + survivor list)")
+        ac_key = "k_acg<3, 256, 0, 1>"
+    else:
+        ac_bytes = p_ * q_ + 25.0 * E
+        ac_alg = (f"p*q + 25 B x {E} extent locations (image, 17 B statistics read, 8 B map "
+                  "write)")
+        ac_name = "k_acg<3,256,0,0> (group-column fused R_co, first EGS candidate: full map)"
+        ac_key = "k_acg<3, 256, 0, 0>"
     ac_gbs = ac_bytes / (ac_launch_ms / 1e3) / 1e9
     traffic = None  # DRAM read+write of that launch from the committed ncu --set full capture
     traffic_src = os.path.join("profiles", "r01_kernel_traffic.json")
     try:
         kt = json.load(open(os.path.join(ROOT, traffic_src)))["kernels"]
-        hit = [v for k, v in kt.items() if "k_acg<3" in k]
+        hit = [v for k, v in kt.items() if ac_key in k]
         if hit:
             traffic = hit[0]["dram_read_bytes"] + hit[0]["dram_write_bytes"]
     except Exception:
         traffic = None
-    roofline = {"bound": "hbm", "kernel": "k_acg<3,256> (group-column fused R_co, first EGS "
-                "candidate: full map + retained count)",
+    roofline = {"bound": "hbm", "kernel": ac_name,
                 "achieved": ac_gbs, "peak": hbm_peak, "unit": "GB/s", "frac": ac_gbs / hbm_peak,
                 "traffic": traffic, "traffic_unit": f"bytes per launch ({traffic_src})",
                 "algorithmic_bytes_per_launch": ac_bytes,
                 "peak_source": "MEASURED_PEAKS.json hbm_gbs (copy bandwidth)",
-                "algorithmic": f"p*q + 25 B x {E} extent locations (image, 17 B statistics "
-                               "read, 8 B map write)",
+                "algorithmic": ac_alg,
                 "kernel_ms": ac_launch_ms, "share_of_step": ac["ms"] / ph_step}
     sec = []
     cnt = phases.get("autocorr_count")
     if cnt:
-        sec.append({"bound": "issue", "kernel": "k_acg<5,128> count-only EGS candidate "
+        sec.append({"bound": "issue", "kernel": "k_acg<5,128,2,0> count-only EGS candidate, packed dp4a walk "
                     "(stops when the partial retained count rejects the size)",
                     "kernel_ms": cnt["ms"], "share_of_step": cnt["ms"] / ph_step})
     wsp = phases.get("window_stats")

@@ -229,8 +229,12 @@ struct tm_ctx {
     DBuf<double> rho_c, surface, dotbuf;
     DBuf<float> tf;
     DBuf<double> td;
+    // the template ctx->tf / ctx->td hold (upload_template skips identical re-uploads);
+    // anything else writing tf / td resets tmpl_m
+    std::vector<double> tmpl_last;
+    int tmpl_m = 0, tmpl_n = 0;
     DBuf<int> rows_list;
-    DBuf<double> map_tmp, map_user;
+    DBuf<double> map_tmp, map_user, map_fused;
     DBuf<double> egs_maps[4];
     DBuf<double> sa_c;  // per-group half_gap factor sqrt(1 - rho_c^2) (scan 2)
     bool sa_ready = false;  // sa_c filled by this search's centre epilogue
@@ -287,6 +291,10 @@ struct tm_ctx {
     cudaStream_t s_up = nullptr;
     cudaEvent_t ev_up[2] = {nullptr, nullptr}, ev_free[2] = {nullptr, nullptr};
     std::unique_ptr<tm_image> sslot[2];
+    // enqueued by search() right before its final synchronisation (tm_search_stream_u8: the
+    // next image's layout copy and window statistics run while the host reads this result)
+    std::function<void()> before_final_sync;
+    bool ev1_set = false;  // search() recorded ev1 before running before_final_sync
     struct Mark {
         const char* name;
         cudaEvent_t a, b;
@@ -592,6 +600,13 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = fal
     T.ts.mn = double(m) * double(n);
     T.integer = integer;
     T.flush_rows = int(16777216LL / (65025LL * n));
+    // the device copy already holds this template (same bytes as the last upload): no copy
+    // (a stream of searches with one template uploads it once)
+    const size_t mnz = size_t(m) * n;
+    if (ctx->tmpl_m == m && ctx->tmpl_n == n && ctx->tmpl_last.size() == mnz && ctx->tf.p &&
+        ctx->td.p && std::memcmp(ctx->tmpl_last.data(), t, mnz * sizeof(double)) == 0)
+        return T;
+    ctx->tmpl_m = ctx->tmpl_n = 0;  // (re-set below once the copies are enqueued)
     std::vector<float> tf(size_t(m) * T.npad, 0.f);
     for (int i = 0; i < m; ++i)
         for (int j = 0; j < n; ++j) tf[size_t(i) * T.npad + j] = float(t[size_t(i) * n + j]);
@@ -608,6 +623,9 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = fal
         CK(cudaEventRecord(ctx->ev_t, ctx->s2));
         CK(cudaStreamWaitEvent(ctx->s, ctx->ev_t, 0));
     }
+    ctx->tmpl_last.assign(t, t + mnz);
+    ctx->tmpl_m = m;
+    ctx->tmpl_n = n;
     return T;
 }
 
@@ -868,8 +886,10 @@ void eval_list(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const in
 }
 
 // ---- scan 1: every group centre (matcher.cpp:23-37) -> rho_c, deg_c, cells[0] --------
+// side_b: B is built on the side stream (tc_b pre-sized and ev_b0 recorded by the caller)
 void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
-                 const tmk::GridDesc& g, const tmk::ReduceOp* op = nullptr) {
+                 const tmk::GridDesc& g, const tmk::ReduceOp* op = nullptr,
+                 bool side_b = false) {
     const size_t G = size_t(g.tr) * g.tc;
     ctx->sa_ready = false;  // set below only by the epilogues that write sa_c
     ctx->rho_c.ensure(G);
@@ -917,7 +937,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             ctx->sa_c.ensure(G);
             ctx->sa_ready = true;  // both epilogues below write scan 2's half-gap factors
             if (hit) return;  // dots, epilogue and its reduction are already in flight
-            tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev);
+            tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev, side_b);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
             const tmk::TailReduce tail = tail_to(ctx, n1 + n2, 0, op);  // n2 = 0 here
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
@@ -1085,14 +1105,17 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
                      double thr, double* map, unsigned long long* nr, int* stop = nullptr,
                      const double* egs_prev = nullptr, double egs_xi = 0.0,
                      bool count_only = false, const tmk::EgsDecide* dec = nullptr,
-                     bool* decided = nullptr) {
+                     bool* decided = nullptr, const tmk::SecFuse* fuse = nullptr) {
     if (decided) *decided = false;
     const int m = ws.m, n = ws.n, p = img->p, q = img->q;
     if (!egs_prev) CK(cudaMemsetAsync(nr, 0, 8, ctx->s));  // EGS batches: egs_init zeroes it
     // (count-only candidates are timed apart: their work stops at the EGS rejection point)
     const bool fused_count = count_only && img->integer && ctx->ac_fused &&
                              tmk::autocorr_fused_supported(ws.m, ws.n, g);
-    Phase ph(ctx, !img->integer ? "autocorr_replica" : fused_count ? "autocorr_count" : "autocorr_u8");
+    Phase ph(ctx, !img->integer ? "autocorr_replica"
+                  : fused_count ? "autocorr_count"
+                  : fuse        ? "autocorr_sec"
+                                : "autocorr_u8");
     if (img->integer) {
         const size_t vbytes = tmk::autocorr_colwalk_bytes(q, g);
         const size_t hbytes = tmk::autocorr_rowsum_bytes(p, g);
@@ -1104,9 +1127,9 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr,
                                       count_only ? nullptr : map, nr, stop, ctx->s, egs_prev,
                                       central, egs_xi, pitched ? img->u8p.p : nullptr,
-                                      img->u8p_pitch, dec, decided));
+                                      img->u8p_pitch, dec, decided, fuse));
             ctx->add(1);
-            return !count_only;
+            return !count_only && !fuse;
         } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
             CK(tmk::autocorr_u8_colwalk(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
@@ -1203,9 +1226,16 @@ struct EgsOut {
 };
 
 // efficient_group_size (egs.cpp:39-91); best map ends in `best`.
+// fuse (tm_search): the candidate of the predicted size runs scan 2 in its R_co launch
+// instead of writing its map (SecFuse); *fuse_hit tells whether EGS accepted that size, in
+// which case no map exists (and none is needed).  On a miss the accepted size's map is
+// computed as usual.
 EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, int h0, int w0,
                       double rho_tb, double xi, int max_group, DBuf<double>& best,
-                      const std::function<void()>* before_sync = nullptr) {
+                      const std::function<void()>* before_sync = nullptr,
+                      const tmk::SecFuse* fuse = nullptr, bool* fuse_hit = nullptr) {
+    if (fuse_hit) *fuse_hit = false;
+    bool fused_ran = false;  // the fused candidate was launched in the first batch
     if (h0 < 1 || w0 < 1 || h0 % 2 == 0 || w0 % 2 == 0)
         invalid("efficient_group_size: initial group size must be odd");
     if (rho_tb <= 0.0 || rho_tb >= 1.0)
@@ -1291,10 +1321,14 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             dec.out = last ? ctx->hres_dev : nullptr;
             dec.seq = batch_seq;
             bool decided = false;
-            map_written[k] = autocorr_launch(ctx, img, ws, g, thr, ctx->egs_maps[k].p,
+            const bool is_pred = cand[k].h == pred && cand[k].w == pred;
+            const bool fuse_here = fuse && is_pred && !fused_ran;
+            map_written[k] = autocorr_launch(ctx, img, ws, g, thr,
+                                             fuse_here ? nullptr : ctx->egs_maps[k].p,
                                              ctx->counters.p + 8 + k, dstop, dprev, xi,
-                                             /*count_only=*/!(cand[k].h == pred && cand[k].w == pred),
-                                             &dec, &decided);
+                                             /*count_only=*/!is_pred, &dec, &decided,
+                                             fuse_here ? fuse : nullptr);
+            if (fuse_here) fused_ran = true;
             if (!decided) {
                 CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
                                    cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
@@ -1342,6 +1376,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             out.w = cand[k].w;
             out.cost = cost;
             out.trace.push_back(cost);
+            if (fuse_hit) *fuse_hit = fused_ran && cand[k].h == pred && cand[k].w == pred;
             if (map_written[k]) {
                 best.swap(ctx->egs_maps[k]);
                 map_h = cand[k].h;
@@ -1356,7 +1391,9 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             w = std::min(cand[k].w + 2, cap);
         }
     }
-    if (out.h != map_h || out.w != map_w) {
+    if (fuse_hit && *fuse_hit && !(out.h == pred && out.w == pred)) *fuse_hit = false;
+    if ((out.h != map_h || out.w != map_w) && !(fuse_hit && *fuse_hit)) {
+        best.ensure(E);
         const long long n_r = autocorr_map(ctx, img, ws, make_grid(er, ec, out.h, out.w), thr,
                                            best.p);
         if (n_r != out.cost.retained)
@@ -1524,6 +1561,11 @@ struct SearchIn {
     const WS* ws;
     tmk::GridDesc g;
     const double* map;  // device
+    // scan 1, the seeding and scan 2 already ran (fused into the R_co launch, tm_search):
+    // only the survivors and the result remain
+    bool prescanned = false;
+    // ... and the survivor evaluation is already enqueued (gated on the EGS decision)
+    bool survivors_enqueued = false;
 };
 
 // Scan-2 survivors (listed in ctx->locs, marked 2 in ctx->visits) -> cells[2].  Dense
@@ -1604,12 +1646,13 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // on the device; survivor_dispatch selects dense (masked tensor-core kernel) or list, the
 // other launch only writes empty partials.
 void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
-                        const tmk::GridDesc& g, double* rho_loc) {
+                        const tmk::GridDesc& g, double* rho_loc,
+                        const unsigned long long* gate = nullptr) {
     cudaStream_t s = ctx->s;
     const size_t E = size_t(g.er) * g.ec;
     int* dense_flag = reinterpret_cast<int*>(ctx->counters.p + 22);
     unsigned long long* list_count = ctx->counters.p + 23;
-    CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s));
+    CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s, gate));
     ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
     const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
     int np = 0;
@@ -1661,11 +1704,12 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     HT("search_begin");
     // the centre reduction also bootstraps the threshold (matcher.cpp:121-125) and zeroes
     // the seeding counters and the scan-2 tally
+    const uint8_t* seeded = nullptr;
+    if (!in.prescanned) {
     const tmk::ReduceOp op_init = centre_op(ctx, P);
     centre_scan(ctx, img, ws, T, g, &op_init);
     HT("centre_scan");
 
-    const uint8_t* seeded = nullptr;
     if (policy == TM_POLICY_SEEDED) {
         const unsigned long long max_groups = 256;
         const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
@@ -1683,12 +1727,13 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         seeded = ctx->seeded.p;
         HT("seeds");
     }
+    }
 
     // ---- scan 2: bound test + survivor compaction -------------------------------------
     ctx->visits.ensure(E);
     uint8_t* visits = ctx->visits.p;
     ctx->locs.ensure(E);
-    {
+    if (!in.prescanned) {
         Phase ph(ctx, "sec_compact");
         ctx->sa_c.ensure(G);
         // frozen / seeded on the exact 8-bit path: a survivor list longer than E/16 is never
@@ -1709,7 +1754,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     if (device_dispatch) {
         // frozen / seeded: nothing changes the threshold after scan 2's bound test, so the
         // final readback gives T0; the survivor count never leaves the device
-        eval_survivors_dev(ctx, img, ws, T, g, nullptr);
+        if (!in.survivors_enqueued) eval_survivors_dev(ctx, img, ws, T, g, nullptr);
     } else {
         CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
@@ -1773,7 +1818,17 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     }
     if (visits_host) CK(cudaMemcpyAsync(visits_host, visits, E, cudaMemcpyDeviceToHost, s));
     HT("readback_enq");
-    CK(cudaStreamSynchronize(s));
+    if (ctx->before_final_sync) {  // wait for this search only, not for the hook's work
+        // (ev1 doubles as the end mark of tm_search's wall time)
+        CK(cudaEventRecord(ctx->ev1, s));
+        ctx->ev1_set = true;
+        const std::function<void()> f = std::move(ctx->before_final_sync);
+        ctx->before_final_sync = nullptr;
+        f();
+        CK(cudaEventSynchronize(ctx->ev1));
+    } else {
+        CK(cudaStreamSynchronize(s));
+    }
     HT("sync");
     tmk::CellH cells[3] = {hr->cells[0], hr->cells[1], hr->cells[2]};
     tally = hr->tally;
@@ -2488,21 +2543,211 @@ int tm_run_u8(tm_ctx* ctx, tm_prep* prep, tm_image* img, const uint8_t* tmpls, i
     return tm_run(ctx, prep, img, t.data(), ntmpl, params, out, visits);
 }
 
+// tm_search with scan 2 fused into the R_co launch of the predicted group size: scan 1
+// and the seeding run first on the predicted grid (they need only the window statistics and
+// the template), then the EGS batch, whose predicted candidate also runs the bound test on
+// every member as its R_co is computed (SecFuse) -- the E-sized map is neither written nor
+// read back, and the separate bound pass is gone.  If EGS accepts another size, the
+// standard path reruns on the accepted grid.  Applies to EGS on 8-bit images with the
+// frozen / seeded policies on the tensor-core path; returns false (nothing enqueued) when
+// it does not apply.  Results, counts and visit codes are those of prepare + run.
+// The first half of search_fused (scan 1 and the seeding on the predicted grid); the state
+// the second half needs.  A stream of searches runs the next image's first half behind the
+// current search, before the host waits for its result (tm_search_stream_u8).
+struct FusedPre {
+    bool ok = false;
+    const tm_image* img = nullptr;
+    int m = 0, n = 0, pred = 0, policy = 0;
+    std::vector<double> tmpl;  // the template it was started with
+    Tmpl T{};
+    tmk::GridDesc g{};
+    const uint8_t* seeded = nullptr;
+    void swap_from(FusedPre& o) {
+        std::swap(*this, o);
+        o.ok = false;
+    }
+};
+
+bool search_fused_begin(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+                        const tm_match_params& P, int pred, FusedPre& fp) {
+    fp.ok = false;
+    static const bool off = [] {
+        const char* e = std::getenv("TMATCH_FUSE_SCAN2");
+        return e && std::strcmp(e, "0") == 0;
+    }();
+    if (off || P.mode == TM_MODE_OPTA || !img->integer || !ctx->ac_fused || !ctx->tc) return false;
+    if (P.h0 != P.w0 || m > img->p || n > img->q) return false;
+    int policy = P.policy;
+    const int er = img->p - m + 1, ec = img->q - n + 1;
+    const tmk::GridDesc g = make_grid(er, ec, pred, pred);
+    const size_t G = size_t(g.tr) * g.tc;
+    if (policy == TM_POLICY_REFERENCE)
+        policy = (P.parallel && P.threads > 1 && G > 1) ? TM_POLICY_FROZEN : TM_POLICY_SEQUENTIAL;
+    if (policy != TM_POLICY_SEEDED && policy != TM_POLICY_FROZEN) return false;
+    if (!(img->u8p.p && img->u8p_rows >= img->p + tmk::kU8PadRows)) return false;
+    if (!tmk::autocorr_sec_fuse_supported(m, n, g) || g.h > tmk::kTcMaxClasses) return false;
+    // the template: exact 8-bit path (tensor cores) only
+    bool t_u8 = true;
+    for (size_t i = 0; i < size_t(m) * n && t_u8; ++i)
+        t_u8 = tmpl[i] >= 0.0 && tmpl[i] <= 255.0 && tmpl[i] == std::rint(tmpl[i]);
+    if (!t_u8) return false;
+    // the 8-bit tensor-core path for this template size (tc_path / fp32_path of the Tmpl)
+    if (!tmk::tc_supported(m, n) || tmk::tc_plan(m, n, 1, kTcSmemBudget).nch == 0 ||
+        16777216LL / (65025LL * n) < 1)
+        return false;
+    if (P.has_init_threshold && std::abs(P.init_threshold) > 1.0 + 1e-9)
+        invalid("transitive_search: init threshold out of [-1,1]");
+
+    HT("fused_begin");
+    // the window statistics first: the device starts while the host prepares the template;
+    // the template copies and the centre scan's B build go to the side stream, overlapping
+    // the statistics (tc_b sized on the main stream first: ev_b0)
+    WS& ws = get_ws(ctx, img, m, n);
+    HT("fused_ws");
+    const tmk::TcPlan bplan = tmk::tc_plan(m, n, pred, kTcSmemBudget);
+    const bool side_b = bplan.nch > 0;
+    if (side_b) {
+        ctx->tc_b.ensure(bplan.total_bytes);
+        CK(cudaEventRecord(ctx->ev_b0, ctx->s));
+    }
+    const Tmpl T = upload_template(ctx, tmpl, m, n, /*side=*/true);
+    if (T.ts.flat) invalid("transitive_search: constant template has no defined correlation");
+    HT("fused_template");
+    if (!tc_path(ctx, img, T) || !fp32_path(img, T))  // (implied by the checks above)
+        throw TmError{TM_ECUDA, "search_fused: template not on the 8-bit tensor-core path"};
+    // scan 1 on the predicted grid (+ threshold bootstrap, tally zeroing) and the seeding
+    const tmk::ReduceOp op_init = centre_op(ctx, P);
+    centre_scan(ctx, img, ws, T, g, &op_init, side_b);
+    HT("fused_centre");
+    if (!ctx->sa_ready) throw TmError{TM_ECUDA, "search_fused: centre factors missing"};
+    const uint8_t* seeded = nullptr;
+    if (policy == TM_POLICY_SEEDED) {
+        const unsigned long long max_groups = 256;
+        const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
+        ctx->seed_locs.ensure(max_locs);
+        ctx->seeded.ensure(G);
+        CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, P.seed_margin,
+                             ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
+                             ctx->counters.p + 5, max_groups, ctx->s));
+        ctx->add(1);
+        tmk::ReduceOp op_raise{};
+        op_raise.kind = 2;
+        op_raise.thr = ctx->thr.p;
+        eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs), nullptr,
+                  nullptr, 1, &op_raise);
+        seeded = ctx->seeded.p;
+    }
+    HT("fused_scan1");
+    fp.ok = true;
+    fp.img = img;
+    fp.m = m;
+    fp.n = n;
+    fp.pred = pred;
+    fp.policy = policy;
+    fp.tmpl.assign(tmpl, tmpl + size_t(m) * n);
+    fp.T = T;
+    fp.g = g;
+    fp.seeded = seeded;
+    return true;
+}
+
+// The second half: the EGS batch whose predicted candidate runs scan 2 (SecFuse), the
+// survivors behind it (gated on the device decision), the result.
+void search_fused_end(tm_ctx* ctx, tm_image* img, const tm_match_params& P, const FusedPre& fp,
+                      tm_match_result* out) {
+    const int m = fp.m, n = fp.n, pred = fp.pred;
+    const int er = img->p - m + 1, ec = img->q - n + 1;
+    const size_t E = size_t(er) * ec;
+    const tmk::GridDesc& g = fp.g;
+    const Tmpl& T = fp.T;
+    WS& ws = get_ws(ctx, img, m, n);
+    ctx->visits.ensure(E);
+    ctx->locs.ensure(E);
+    tmk::SecFuse sf{};
+    sf.thr = ctx->thr.p;
+    sf.rho_c = ctx->rho_c.p;
+    sf.sa_c = ctx->sa_c.p;
+    sf.deg_c = ctx->deg_c.p;
+    sf.seeded = fp.seeded;
+    sf.tflat = T.ts.flat;
+    sf.locs = ctx->locs.p;
+    sf.max_locs = E / 16 + 1;  // longer survivor lists go to the dense pass (visit mask)
+    sf.tally = ctx->tally.p;
+    sf.visits = ctx->visits.p;
+    bool hit = false;
+    // the survivor evaluation is enqueued behind the EGS batch, gated on the device decision
+    // (EGS finished with h_e == pred), so the device keeps working while the host reads the
+    // counts; on a miss its kernels do nothing and the standard path follows
+    const unsigned long long* gate = ctx->counters.p + 24;
+    const std::function<void()> hook = [&] {
+        eval_survivors_dev(ctx, img, ws, T, g, nullptr, gate);
+    };
+    ctx->spec_want = pred;  // the decide kernels set the gate for this size
+    const EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
+                                    P.max_group, ctx->map_fused, &hook, &sf, &hit);
+    ctx->spec_want = 0;
+    HT("fused_egs");
+    if (hit && ctx->hres->spec != 1)
+        throw TmError{TM_ECUDA, "search_fused: device gate disagrees with the EGS decision"};
+    if (hit) {
+        SearchIn in{img, &ws, g, nullptr};
+        in.prescanned = true;
+        in.survivors_enqueued = true;
+        *out = search(ctx, in, T, P, nullptr);
+    } else {  // EGS accepted another size: the standard scans on its grid
+        const tmk::GridDesc ga = make_grid(er, ec, e.h, e.w);
+        *out = search(ctx, SearchIn{img, &ws, ga, ctx->map_fused.p}, T, P, nullptr);
+    }
+    HT("fused_end");
+    htrace().flush("search_fused");
+}
+
+// tm_search with scan 2 fused into the R_co launch of the predicted group size: scan 1
+// and the seeding run first on the predicted grid (they need only the window statistics and
+// the template), then the EGS batch, whose predicted candidate also runs the bound test on
+// every member as its R_co is computed (SecFuse) -- the E-sized map is neither written nor
+// read back, and the separate bound pass is gone.  If EGS accepts another size, the
+// standard path reruns on the accepted grid.  Applies to EGS on 8-bit images with the
+// frozen / seeded policies on the tensor-core path; returns false (nothing enqueued but
+// cacheable window statistics) when it does not apply.  Results, counts and visit codes are
+// those of prepare + run.  `pre`: a first half already enqueued for this call (stream).
+bool search_fused(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+                  const tm_match_params& P, int pred, tm_match_result* out,
+                  const FusedPre* pre = nullptr) {
+    FusedPre local;
+    const FusedPre* fp = pre;
+    if (!fp || !fp->ok || fp->img != img || fp->m != m || fp->n != n || fp->pred != pred ||
+        std::memcmp(fp->tmpl.data(), tmpl, size_t(m) * n * sizeof(double)) != 0) {
+        // (a first half enqueued for other inputs is simply redone: its state is rewritten)
+        if (!search_fused_begin(ctx, img, tmpl, m, n, P, pred, local)) return false;
+        fp = &local;
+    }
+    search_fused_end(ctx, img, P, *fp, out);
+    return true;
+}
+
 // prepare + run of one template on a resident image (tm_search's body; ev0 recorded).
+// Predicted h_e of a search: the last one seen for this image/template shape (else h0);
+// 0 when no prediction applies.
+int predicted_he(tm_ctx* ctx, const tm_image* img, int m, int n, const tm_match_params& P) {
+    const bool egs = P.mode != TM_MODE_OPTA && P.h0 == P.w0;
+    if (!(egs && img->integer && m <= img->p && n <= img->q)) return 0;
+    const std::vector<long long> key = {img->p, img->q, m, n, P.h0, P.w0};
+    const auto it = ctx->last_he.find(key);
+    return it != ctx->last_he.end() ? it->second : P.h0;
+}
+
 void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
-                     const tm_match_params* params, tm_match_result* out) {
+                     const tm_match_params* params, tm_match_result* out,
+                     const FusedPre* pre = nullptr) {
+    ctx->ev1_set = false;
     Tmpl T;
     bool uploaded = false;
-    // Predicted h_e: the last one seen for this image/template shape (else h0).  Its
-    // centre scan is enqueued behind the first EGS batch, gated on the device decision,
-    // so the device does not idle while the host reads the counts.
-    const bool egs = params->mode != TM_MODE_OPTA && params->h0 == params->w0;
-    const std::vector<long long> key = {img->p, img->q, m, n, params->h0, params->w0};
-    int want = 0;
-    if (egs && img->integer && m <= img->p && n <= img->q) {
-        const auto it = ctx->last_he.find(key);
-        want = it != ctx->last_he.end() ? it->second : params->h0;
-    }
+    // Predicted h_e: the last one seen for this image/template shape (else h0).  Fused
+    // path: scan 1 on its grid first, scan 2 inside its R_co launch.  Otherwise its centre
+    // scan is enqueued behind the first EGS batch, gated on the device decision, so the
+    // device does not idle while the host reads the counts.
+    const int want = predicted_he(ctx, img, m, n, *params);
     ctx->spec_want = want;
     ctx->spec.armed = false;
     // B of the predicted centre scan is built on the side stream during the EGS batch: its
@@ -2524,6 +2769,16 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
             spec_centre(ctx, img, get_ws(ctx, img, m, n),
                         T, make_grid(img->p - m + 1, img->q - n + 1, want, want), *params);
     };
+    if (want > 0 && search_fused(ctx, img, tmpl, m, n, *params, want, out, pre)) {
+        ctx->spec_want = 0;
+        ctx->spec_b = false;
+        ctx->spec.armed = false;
+        if (!ctx->ev1_set) CK(cudaEventRecord(ctx->ev1, ctx->s));
+        ctx->ev1_set = false;
+        CK(cudaEventSynchronize(ctx->ev1));
+        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+        return;
+    }
     std::unique_ptr<tm_prep> prep;
     try {
         prep.reset(prepare(ctx, img, m, n, *params, &hook, /*timed=*/false));
@@ -2538,7 +2793,8 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
     prep->ctx = nullptr;  // internal: not counted as a context reference
     if (!uploaded) T = upload_template(ctx, tmpl, m, n);
     *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);
-    CK(cudaEventRecord(ctx->ev1, ctx->s));
+    if (!ctx->ev1_set) CK(cudaEventRecord(ctx->ev1, ctx->s));
+    ctx->ev1_set = false;
     CK(cudaEventSynchronize(ctx->ev1));
     out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
 }
@@ -2619,20 +2875,64 @@ int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int
                                ctx->s_up));
             CK(cudaEventRecord(ctx->ev_up[k], ctx->s_up));
         };
-        enqueue_upload(0);
-        for (int i = 0; i < nimg; ++i) {
+        // an image's prologue: its layout copy and window statistics (they need only the
+        // pixels); image i+1's is enqueued behind search i, before the host waits for that
+        // result, so the device does not idle while the host finishes search i
+        auto prologue = [&](int i) {
             tm_image* img = ctx->sslot[i & 1].get();
-            HT("start");
-            CK(cudaEventRecord(ctx->ev0, ctx->s));
             CK(cudaStreamWaitEvent(ctx->s, ctx->ev_up[i & 1], 0));
-            // the next image crosses PCIe while this one is searched (the other slot's last
-            // reader, search i-1, has completed: search_resident returns after its readback)
-            if (i + 1 < nimg) enqueue_upload(i + 1);
             img->have_f32 = img->have_f64 = false;
             img->have_qtotal = false;
             tc_pitch_copy(ctx, img);
             img->ws_cache.clear();
-            search_resident(ctx, img, t.data(), m, n, params, &out[i]);
+            get_ws(ctx, img, m, n);
+        };
+        const bool ws_ok = m <= rows && n <= cols;  // (else the search reports the error)
+        enqueue_upload(0);
+        bool pro_done = false;
+        FusedPre next_pre;  // the next image's first half, enqueued behind the current search
+        for (int i = 0; i < nimg; ++i) {
+            tm_image* img = ctx->sslot[i & 1].get();
+            HT("start");
+            CK(cudaEventRecord(ctx->ev0, ctx->s));
+            // the next image crosses PCIe while this one is searched (the other slot's last
+            // reader, search i-1, has completed: search_resident returns after its readback)
+            if (i + 1 < nimg) enqueue_upload(i + 1);
+            if (!pro_done) {
+                if (ws_ok) {
+                    prologue(i);
+                } else {
+                    CK(cudaStreamWaitEvent(ctx->s, ctx->ev_up[i & 1], 0));
+                    img->have_f32 = img->have_f64 = img->have_qtotal = false;
+                    tc_pitch_copy(ctx, img);
+                    img->ws_cache.clear();
+                }
+            }
+            pro_done = false;
+            FusedPre cur_pre;
+            cur_pre.swap_from(next_pre);
+            if (ws_ok && i + 1 < nimg)
+                ctx->before_final_sync = [&, i] {
+                    prologue(i + 1);
+                    pro_done = true;
+                    // ... and the next search's scan 1 + seeding when it takes the fused path
+                    tm_image* nimg_ = ctx->sslot[(i + 1) & 1].get();
+                    const int pred = predicted_he(ctx, nimg_, m, n, *params);
+                    if (pred > 0)
+                        search_fused_begin(ctx, nimg_, t.data(), m, n, *params, pred, next_pre);
+                };
+            try {
+                search_resident(ctx, img, t.data(), m, n, params, &out[i],
+                                cur_pre.ok ? &cur_pre : nullptr);
+            } catch (...) {
+                ctx->before_final_sync = nullptr;
+                throw;
+            }
+            if (ctx->before_final_sync) {  // (a search path without the hook: run it now)
+                ctx->before_final_sync = nullptr;
+                prologue(i + 1);
+                pro_done = true;
+            }
             CK(cudaEventRecord(ctx->ev_free[i & 1], ctx->s));
         }
     });

@@ -897,6 +897,12 @@ __device__ __forceinline__ void egs_tail(const EgsDecide& d) {
     }
 }
 
+__device__ __forceinline__ float sqrt_approx(float x) {
+    float r;
+    asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
+
 // ---- fused R_co, one thread per group column (square groups, h <= 5) ----------------------
 //
 // The walk of k_acf, but thread t owns the W = h image columns [cc_k, cc_k + W) of group
@@ -938,12 +944,13 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // trailing rows accumulate separately (dp4a only adds) and are subtracted at the events.
 // NP = 2 when the grid has no clipped group column, 3 otherwise; NP = 0 is the per-column
 // walk (one IMAD per column, offset and row step).
-template <int H, int NT, int NP>
+// FUSE: scan 2 in the epilogue (SecFuse; the map is not written).
+template <int H, int NT, int NP, bool FUSE>
 __global__ void __launch_bounds__(NT)
     k_acg(const uint8_t* __restrict__ img, int P, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
           int seg, int RR, int* __restrict__ stop, const double* __restrict__ egs_prev,
-          double egs_central, double egs_xi, EgsDecide dec) {
+          double egs_central, double egs_xi, EgsDecide dec, SecFuse sf) {
     pdl_wait();
     constexpr int W = H, hr = H / 2;
     constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
@@ -1219,8 +1226,18 @@ __global__ void __launch_bounds__(NT)
     uint8_t pf_fc, pf_fm[H];
     double pf_mc, pf_oc, pf_mm[H], pf_om[H];
     bool pf_row[H];
+    // FUSE: the group's scan-1 values (one group per thread and event)
+    double pf_ra = 0.0, pf_sa = 0.0;
+    uint8_t pf_dg = 0, pf_sd = 0;
     auto prefetch = [&](int tin, int crn) {
         const int r0 = tin * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        if constexpr (FUSE) {
+            const size_t gi = col_ok ? size_t(tin) * g.tc + k : 0;
+            pf_ra = sf.rho_c[gi];
+            pf_sa = sf.sa_c[gi];
+            pf_dg = sf.deg_c[gi];
+            pf_sd = sf.seeded ? sf.seeded[gi] : uint8_t(0);
+        }
         const unsigned kc = col_ok ? unsigned(crn) * unsigned(g.ec) + unsigned(cc) : 0u;
         pf_fc = st.flat[kc];
         pf_mc = st.mu[kc];
@@ -1241,6 +1258,19 @@ __global__ void __launch_bounds__(NT)
     const double prev = (egs_prev && stop) ? *egs_prev : 0.0;
     const bool can_reject = egs_prev && stop && fabs(prev) <= 1.7976931348623157e308;
     int my_abort = 0, ev = 0, parity = 0;
+    // FUSE: scan-2 state (k_sec_rows): threshold, tallies, survivor-list state of this warp
+    double sec_tb = 0.0;
+    float sec_tbf = 0.f;
+    bool thr_ok = false;
+    if constexpr (FUSE) {
+        const double T = *sf.thr;
+        sec_tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sec_tbf = float(sec_tb);
+        thr_ok = T >= -1.0;
+    }
+    unsigned n_elim = 0, n_keep = 0;
+    bool list_full = false;
+    unsigned long long surv_local = 0;
 #pragma unroll 1
     for (int ti = ti0;;) {
         unsigned* Lb = acg_smem + (parity ? PS : 0);
@@ -1306,6 +1336,17 @@ __global__ void __launch_bounds__(NT)
             }
         }
         unsigned evc = 0;
+        unsigned surv = 0;  // FUSE: members of this event that survive the bound test (bit d)
+        // FUSE: this event's group constants (centre rho clamped, its FP32 copies)
+        bool grp_test = false;
+        double g_a = 0.0;
+        float g_af = 0.f, g_saf = 0.f;
+        if constexpr (FUSE) {
+            grp_test = thr_ok && !pf_dg && !sf.tflat;
+            g_a = dclamp(pf_ra, -1.0, 1.0);
+            g_af = float(g_a);
+            g_saf = float(pf_sa);
+        }
         if (col_ok) {
 #pragma unroll
             for (int d = 0; d < H; ++d) {
@@ -1313,6 +1354,7 @@ __global__ void __launch_bounds__(NT)
                 const unsigned km = unsigned(cr + d - hr) * unsigned(g.ec) + unsigned(c);
                 if (d == hr && dj == 0) {  // centres carry exactly 1 (autocorr.cpp:92-93)
                     if (map) map[km] = 1.0;
+                    if constexpr (FUSE) sf.visits[km] = 0;  // a centre is not a member
                     continue;
                 }
                 const unsigned* Ld = Lb + d * NT;
@@ -1329,13 +1371,66 @@ __global__ void __launch_bounds__(NT)
                 const double num =
                     __dsub_rn(double(S), __dmul_rn(__dmul_rn(mn, pf_mc), pf_mm[d]));
                 const double den = __dmul_rn(pf_oc, pf_om[d]);
-                if (!map) {  // EGS candidate: retained count only (no map, no division)
+                if (!FUSE && !map) {  // EGS candidate: retained count only (no map, no division)
                     if (flat ? 0.0 < thr : retained_below(num, den, thr)) ++evc;
                     continue;
                 }
                 const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
-                map[km] = val;
+                if (map) map[km] = val;
                 if (val < thr) ++evc;
+                if constexpr (FUSE) {  // scan 2 (matcher.cpp:48-78), as k_sec_rows
+                    uint8_t vis = 2;
+                    if (pf_sd) {
+                        ++n_keep;  // a seeded group: its members were evaluated already
+                    } else {
+                        bool elim = grp_test && !pf_fm[d];
+                        if (elim) {
+                            // FP32 decision with a 4e-6 margin (errors < 1e-6: every input is
+                            // an exactly rounded value in [-1, 1], x = 1 - b^2 in FP64 before
+                            // its square root), the exact FP64 test of k_sec_rows inside it
+                            const float s = sqrt_approx(float(fma(-val, val, 1.0)));
+                            const float f = fmaf(g_af, float(val), g_saf * s);
+                            if (sec_tbf >= f + 4e-6f) {
+                                elim = true;
+                            } else if (sec_tbf < f - 4e-6f) {
+                                elim = false;
+                            } else {
+                                const double x = dmax(0.0, __dsub_rn(1.0, __dmul_rn(val, val)));
+                                elim = sec_tb >= __dadd_rn(__dmul_rn(g_a, val),
+                                                           __dmul_rn(pf_sa, __dsqrt_rn(x)));
+                            }
+                        }
+                        if (elim) {
+                            ++n_elim;
+                            vis = 1;
+                        } else {
+                            ++n_keep;
+                            surv |= 1u << d;
+                        }
+                    }
+                    sf.visits[km] = vis;
+                }
+            }
+        }
+        if constexpr (FUSE) {  // survivor compaction, one ballot per member row offset
+#pragma unroll
+            for (int d = 0; d < H; ++d) {
+                const bool sv = (surv >> d) & 1u;
+                const unsigned ballot = __ballot_sync(0xffffffffu, sv);
+                if (!ballot) continue;
+                if (list_full) {  // nothing more can be listed: count only
+                    surv_local += __popc(ballot);
+                    continue;
+                }
+                unsigned long long basepos = 0;
+                if (lane == 0)
+                    basepos = atomicAdd(&sf.tally->survivors, (unsigned long long)__popc(ballot));
+                basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                list_full = basepos + __popc(ballot) >= sf.max_locs;
+                if (sv) {
+                    const unsigned long long pos = basepos + __popc(ballot & ((1u << lane) - 1));
+                    if (pos < sf.max_locs) sf.locs[pos] = make_int2(cr + d - hr, c);
+                }
             }
         }
         evc = __reduce_add_sync(0xffffffffu, evc);
@@ -1356,6 +1451,15 @@ __global__ void __launch_bounds__(NT)
     }
     __syncthreads();
     if (t == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
+    if constexpr (FUSE) {
+        const unsigned long long ne = warp_sum((unsigned long long)n_elim);
+        const unsigned long long nk = warp_sum((unsigned long long)n_keep);
+        if (lane == 0) {  // (surv_local is warp-uniform)
+            if (ne) atomicAdd(&sf.tally->eliminated, ne);
+            if (nk) atomicAdd(&sf.tally->retained, nk);
+            if (surv_local) atomicAdd(&sf.tally->survivors, surv_local);
+        }
+    }
     egs_tail(dec);
 }
 
@@ -1420,30 +1524,42 @@ bool acg_enabled() {
     return on;
 }
 
-template <int H, int NT, int NP>
-cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
-                          DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
-                          const double* egs_prev, double egs_central, double egs_xi,
-                          cudaStream_t s, const EgsDecide& dec) {
+template <int H, int NT, int NP, bool FUSE>
+cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
+                         DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
+                         const double* egs_prev, double egs_central, double egs_xi,
+                         cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(k_acg<H, NT, NP>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        cudaFuncSetAttribute(k_acg<H, NT, NP, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              int(kAcgSmemMax));
         attr = true;
     }
     const AcgGeom a0 = acg_geom(m, n, gd, NT);
     if (a0.nt == 0) return cudaErrorInvalidValue;
     int occ = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acg<H, NT, NP>, NT, a0.smem) !=
-        cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, k_acg<H, NT, NP, FUSE>, NT,
+                                                      a0.smem) != cudaSuccess)
         occ = 0;
     const AcgGeom a = acg_geom(m, n, gd, NT, occ);
     dim3 grid(gd.w, a.ntiles, a.nseg);
     if (gd.ti_hi > gd.ti_lo)
-        launch_pdl(k_acg<H, NT, NP>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n, to_grid(gd),
-                   st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central, egs_xi,
-                   dec);
+        launch_pdl(k_acg<H, NT, NP, FUSE>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n,
+                   to_grid(gd), st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central,
+                   egs_xi, dec, sf);
     return cudaGetLastError();
+}
+
+template <int H, int NT, int NP>
+cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
+                          DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
+                          const double* egs_prev, double egs_central, double egs_xi,
+                          cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+    if (sf.thr)
+        return launch_acg_f<H, NT, NP, true>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                             egs_prev, egs_central, egs_xi, s, dec, sf);
+    return launch_acg_f<H, NT, NP, false>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                          egs_prev, egs_central, egs_xi, s, dec, sf);
 }
 
 // Packed (dp4a) walk for h = 5 (NP = 2 without a clipped group column, else 3); the
@@ -1462,27 +1578,27 @@ template <int H, int NT>
 cudaError_t launch_acg_np(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
-                          cudaStream_t s, const EgsDecide& dec) {
+                          cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
     if (!acg_pack(H))
         return launch_acg_nt<H, NT, 0>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                       egs_prev, egs_central, egs_xi, s, dec);
+                                       egs_prev, egs_central, egs_xi, s, dec, sf);
     if (gd.ec % gd.w == 0)
         return launch_acg_nt<H, NT, 2>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                       egs_prev, egs_central, egs_xi, s, dec);
+                                       egs_prev, egs_central, egs_xi, s, dec, sf);
     return launch_acg_nt<H, NT, 3>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                   egs_central, egs_xi, s, dec);
+                                   egs_central, egs_xi, s, dec, sf);
 }
 
 template <int H>
 cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                        DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                        const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s,
-                       const EgsDecide& dec) {
+                       const EgsDecide& dec, const SecFuse& sf) {
     if (acg_threads(H) == 128)
         return launch_acg_np<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                     egs_central, egs_xi, s, dec);
+                                     egs_central, egs_xi, s, dec, sf);
     return launch_acg_np<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
-                                 egs_central, egs_xi, s, dec);
+                                 egs_central, egs_xi, s, dec, sf);
 }
 
 template <int H>
@@ -1723,6 +1839,11 @@ cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* st
     return cudaGetLastError();
 }
 
+bool autocorr_sec_fuse_supported(int m, int n, GridDesc g) {
+    return autocorr_fused_supported(m, n, g) && acg_enabled() && (g.h == 3 || g.h == 5) &&
+           g.h == g.w && acg_geom(m, n, g, acg_threads(g.h)).nt > 0;
+}
+
 bool autocorr_fused_supported(int m, int n, GridDesc g) {
     // 32-bit row offsets; the walk may read h/2 <= kU8PadRows rows below the image
     const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
@@ -1737,19 +1858,21 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev, double egs_central, double egs_xi,
                               const uint8_t* imgp, int pitch, const EgsDecide* dec,
-                              bool* decided) {
+                              bool* decided, const SecFuse* fuse) {
     if (decided) *decided = false;
     if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd.h)).nt > 0 &&
         (gd.h == 3 || gd.h == 5)) {
         // the EGS decision rides on the launch's tail (no k_egs_decide launch)
         const EgsDecide d = dec ? *dec : EgsDecide{};
+        const SecFuse f = fuse ? *fuse : SecFuse{};
         if (decided) *decided = d.ticket != nullptr;
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
-                                 egs_prev, egs_central, egs_xi, s, d);
+                                 egs_prev, egs_central, egs_xi, s, d, f);
         return launch_acg<5>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
-                             egs_prev, egs_central, egs_xi, s, d);
+                             egs_prev, egs_central, egs_xi, s, d, f);
     }
+    if (fuse && fuse->thr) return cudaErrorInvalidValue;  // scan 2 fuses into k_acg only
     switch (gd.h) {
         case 1: return launch_acf<1>(img, p, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                      egs_prev, egs_central, egs_xi, s);

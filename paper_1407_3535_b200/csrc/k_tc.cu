@@ -512,8 +512,14 @@ __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_
 
 namespace {
 __global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
-                                    unsigned long long* list_count) {
+                                    unsigned long long* list_count,
+                                    const unsigned long long* gate) {
     pdl_wait();
+    if (gate && !*gate) {  // speculative launch not confirmed: the passes behind it do nothing
+        *dense_flag = 0;
+        *list_count = 0ull;
+        return;
+    }
     const unsigned long long n = tally->survivors;
     const bool dense = n * 16 > E;
     *dense_flag = dense ? 1 : 0;
@@ -523,8 +529,10 @@ __global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, in
 }  // namespace
 
 cudaError_t survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
-                              unsigned long long* list_count, cudaStream_t s) {
-    launch_pdl(k_survivor_dispatch, dim3(1), dim3(1), 0, s, tally, E, dense_flag, list_count);
+                              unsigned long long* list_count, cudaStream_t s,
+                              const unsigned long long* gate) {
+    launch_pdl(k_survivor_dispatch, dim3(1), dim3(1), 0, s, tally, E, dense_flag, list_count,
+               gate);
     return cudaGetLastError();
 }
 

@@ -73,6 +73,23 @@ struct EgsDecide {
     unsigned long long seq = 0;
 };
 
+// Scan 2 fused into the R_co launch of the predicted group size (tm_search): scan 1 and the
+// seeding ran before it, so each member's bound test (matcher.cpp:48-78 with sec_holds,
+// bounds.cpp:41-46) runs where its R_co is computed -- no E-sized map round trip and no
+// separate bound pass.  Same decisions, counts, visit codes and survivor list as k_sec_rows.
+struct SecFuse {
+    const double* thr = nullptr;  // threshold after scan 1 / seeding (null: not fused)
+    const double* rho_c = nullptr;
+    const double* sa_c = nullptr;  // per-group half_gap factor sqrt(1 - rho_c^2)
+    const uint8_t* deg_c = nullptr;
+    const uint8_t* seeded = nullptr;  // seeded policy: groups already searched (may be null)
+    int tflat = 0;
+    int2* locs = nullptr;
+    unsigned long long max_locs = 0;
+    Tally* tally = nullptr;
+    uint8_t* visits = nullptr;
+};
+
 // Work fused into an argmax reduction (saves launches on the search's critical path).
 struct ReduceOp {
     int kind = 0;  // 0 none, 1 threshold init (matcher.cpp:121-125), 2 raise, 3 pack
@@ -172,7 +189,10 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev = nullptr, double egs_central = 0.0,
                               double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0,
-                              const EgsDecide* dec = nullptr, bool* decided = nullptr);
+                              const EgsDecide* dec = nullptr, bool* decided = nullptr,
+                              const SecFuse* fuse = nullptr);
+// The group-column R_co kernel can run scan 2 in its epilogue (SecFuse) for this geometry.
+bool autocorr_sec_fuse_supported(int m, int n, GridDesc g);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s,
@@ -363,7 +383,8 @@ struct TcTask {
 // Device-side choice between the dense (tensor-core) and list survivor evaluation:
 // dense_flag = survivors*16 > E, list_count = dense ? 0 : survivors.
 cudaError_t survivor_dispatch(const Tally* tally, unsigned long long E, int* dense_flag,
-                              unsigned long long* list_count, cudaStream_t s);
+                              unsigned long long* list_count, cudaStream_t s,
+                              const unsigned long long* gate = nullptr);
 bool tc_supported(int m, int n);
 TcPlan tc_plan(int m, int n, int sr, size_t smem_budget);
 // rows of a band of rmax rows, see k_tc.cu (4 ints per row)

@@ -438,6 +438,47 @@ def test_search_speculation_hit_and_miss(ctx):
     assert len(seen) >= 2, seen
 
 
+@pytest.mark.parametrize("policy", ["seeded", "frozen"])
+@pytest.mark.parametrize("case", ["cut", "noise"])
+def test_search_fused_scan2_equals_prepare_run(ctx, policy, case):
+    """tm_search runs scan 2 inside the R_co launch of the predicted group size (no map):
+    on smooth (h_e = 5, packed walk), rough (h_e = 3) and wide multi-tile images, with a cut
+    template (few survivors, list path) and a pure-noise template (weak elimination, dense
+    tensor-core survivor pass driven by the visit codes), repeated (the second call
+    predicts from the first), every result equals prepare + run bit for bit."""
+    rng = np.random.default_rng(23)
+    keys = ("best_row", "best_col", "best_rho", "best_degenerate", "eliminated", "retained",
+            "centers", "ops", "final_threshold", "elim_pct")
+    seen = set()
+    for rows, cols, m, n, smooth in [(300, 420, 32, 32, True), (260, 333, 24, 40, False),
+                                     (200, 1500, 48, 64, True), (257, 260, 31, 17, True)]:
+        if smooth:
+            base = np.cumsum(np.cumsum(rng.normal(size=(rows, cols)), 0), 1)
+            img = np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0,
+                          255).astype(np.uint8)
+            img[20:60, 30:90] = 77  # flat windows
+        else:
+            img = rng.integers(0, 256, (rows, cols)).astype(np.uint8)
+        if case == "cut":
+            t = np.clip(np.rint(img[rows // 3:rows // 3 + m, cols // 2:cols // 2 + n] * 0.95 + 6
+                                + rng.normal(0, 4, (m, n))), 0, 255).astype(np.uint8)
+        else:
+            t = rng.integers(0, 256, (m, n)).astype(np.uint8)
+        gi = ctx.image(img)
+        prep = ctx.prepare(gi, m, n, mode="egs")
+        seen.add(prep.info["h"])
+        want = ctx.run(prep, t, policy=policy, parallel=(policy == "frozen"), threads=2)
+        prep.close()
+        for _ in range(2):
+            gi.reset_cache()
+            got = ctx.search(gi, t, mode="egs", policy=policy, parallel=(policy == "frozen"),
+                             threads=2)
+            for k in keys:
+                assert getattr(got, k) == getattr(want, k), (rows, cols, k)
+        gi.close()
+    assert {3, 5} <= seen, seen
+
+
 @pytest.mark.parametrize("shape", [(300, 420, 40, 37), (700, 260, 64, 64), (130, 90, 20, 30)])
 def test_search_upload_streamed_equals_resident(ctx, port, shape):
     """tm_search_upload_u8 (upload + search in one call) == tm_image_upload_u8 +

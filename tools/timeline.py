@@ -1,4 +1,4 @@
-"""GPU timeline of a few C2 searches via torch.profiler (CUPTI sees every kernel in the
+"""GPU timeline of a few C2 searches (or tm_search_stream_u8 calls: arg 3 = stream) via torch.profiler (CUPTI sees every kernel in the
 process): prints each kernel / memcpy with its start offset, duration and the idle gap
 before it, for the last search.   python tools/timeline.py [C2] [steps]"""
 import sys
@@ -12,6 +12,7 @@ from paper_1407_3535_b200 import api, workloads as W  # noqa: E402
 cfg = sys.argv[1] if len(sys.argv) > 1 else "C2"
 steps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
 upload = len(sys.argv) > 3 and sys.argv[3] == "upload"  # the e2e step: tm_search_upload_u8
+stream = len(sys.argv) > 3 and sys.argv[3] == "stream"  # tm_search_stream_u8 over `steps` images
 wl = W.make(cfg)
 ctx = api.Context(0)
 img = ctx.image(wl.image)
@@ -21,7 +22,9 @@ pinned.numpy()[:] = wl.image
 
 
 def step():
-    if upload:
+    if stream:
+        ctx.search_stream([pinned.numpy()] * 4, t.astype("uint8"), policy="seeded")
+    elif upload:
         ctx.search_upload(img, pinned.numpy(), t.astype("uint8"), policy="seeded")
     else:
         img.reset_cache()
@@ -45,6 +48,10 @@ def big_copy(e):  # an image chunk (the template copies are a few microseconds)
 starts = [i for i, e in enumerate(evs) if (upload and big_copy(e) and
                                            (i == 0 or not big_copy(evs[i - 1])))
           or (not upload and "k_sum_sq_u8" in e.name)]
+if stream:  # the search before the last (its next image's copy overlaps it)
+    starts = [i for i, e in enumerate(evs) if "k_tc_pitch" in e.name]
+    starts = starts[-2:-1] + [len(evs)] if len(starts) >= 2 else starts
+    evs, starts = evs[:starts[-1]], starts[:1]
 last = evs[starts[-1]:] if starts else evs
 t0 = last[0].time_range.start
 prev_end = t0
