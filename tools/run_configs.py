@@ -3,7 +3,8 @@
 For every template: the seeded, frozen (and, for small extents, sequential) searches must
 return the brute-force argmax (location and rho bits; brute force = the exact sm_100a
 dense kernel), and every eliminated member must satisfy rho <= final threshold on the
-brute-force surface (soundness, acceptance.cpp:105-116).  Timings are device-synchronous
+brute-force surface (soundness, acceptance.cpp:105-116); for EGS configs tm_search (the
+fused single-call path) must equal prepare + run.  Timings are device-synchronous
 wall clock around each API call.  Prints one JSON object per config.
 
     python tools/run_configs.py C1 C2 C3 C4 C5 [--no-sequential]
@@ -63,8 +64,23 @@ def run(name, seq=True):
             sound = bool(np.all(surf_s[vis == 1] <= r.final_threshold + 1e-9))
             ok = ok and same and sound
             rec[pol] = dict(ms=ms, refined=list(loc), elim_pct=r.elim_pct, retained=r.retained,
-                            ops=r.ops, argmax_equals_brute=same, sound=sound,
-                            final_threshold=r.final_threshold)
+                            eliminated=r.eliminated, ops=r.ops, argmax_equals_brute=same,
+                            sound=sound, final_threshold=r.final_threshold)
+        if wl.mode == "egs":
+            # tm_search (prepare + run in one call; scan 2 fused into the R_co launch of the
+            # predicted group size) must give exactly the prepare + run result
+            for pol in ("seeded", "frozen"):
+                t0 = time.perf_counter()
+                r = ctx.search(img, t, mode="egs", policy=pol, parallel=(pol == "frozen"),
+                               threads=2)
+                ms = (time.perf_counter() - t0) * 1e3
+                same = ([r.best_row, r.best_col, r.best_rho, r.eliminated, r.retained, r.ops,
+                         r.final_threshold] ==
+                        [rec[pol]["refined"][0], rec[pol]["refined"][1], rec[pol]["refined"][2],
+                         rec[pol]["eliminated"], rec[pol]["retained"], rec[pol]["ops"],
+                         rec[pol]["final_threshold"]])
+                rec[f"search_{pol}"] = dict(ms=ms, equals_prepare_run=same)
+                ok = ok and same
         rec["ok"] = ok
         out["results"].append(rec)
     out["all_ok"] = all(r["ok"] for r in out["results"])
