@@ -3174,9 +3174,15 @@ int tm_match(tm_ctx* ctx, const double* tmpl, int m, int n, const double* image,
         } else {
             const Tmpl T = upload_template(ctx, tmpl, m, n);
             if (T.ts.flat) invalid("match: constant template has no defined correlation");
-            std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params));
-            *out = run_one(ctx, prep.get(), img, tmpl, *params, visits);
-            prep.reset();
+            if (params->mode != TM_MODE_OPTA && !visits) {
+                // no preparation handle or visit map leaves the call: tm_search's path (scan 2
+                // fused into R_co for the frozen / seeded policies), same results
+                search_resident(ctx, img, tmpl, m, n, params, out);
+            } else {
+                std::unique_ptr<tm_prep> prep(prepare(ctx, img, m, n, *params));
+                *out = run_one(ctx, prep.get(), img, tmpl, *params, visits);
+                prep.reset();
+            }
         }
         out->wall_ms =
             std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();

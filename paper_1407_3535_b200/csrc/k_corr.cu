@@ -198,7 +198,9 @@ __global__ void __launch_bounds__(NW * 32)
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.y * gridDim.x + blockIdx.x);
 }
 
-__device__ void tail_reduce(const TailReduce& tr, Cell* scratch);
+// nblocks: blocks taking a ticket (default: the grid); n: partials to reduce (default tr.n)
+__device__ void tail_reduce(const TailReduce& tr, Cell* scratch, unsigned nblocks = 0,
+                            int n = -1);
 
 // Epilogue of a K-split centre scan: rho/deg per group from the accumulated dots.
 __global__ void __launch_bounds__(256)
@@ -255,6 +257,13 @@ __global__ void __launch_bounds__(256)
     __shared__ double wsum[8];
     const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
     const long long nloc = min((long long)*count, (long long)max_count);
+    // only the blocks with a location take part (short lists: no empty blocks queueing on the
+    // reduction ticket); without a fused reduction every block still writes its partial
+    const int active = int(max(1LL, min((long long)gridDim.x, nloc)));
+    if (int(blockIdx.x) >= active) {
+        if (!tail.ticket && threadIdx.x == 0) store_partial(no_cell(), partials, blockIdx.x);
+        return;
+    }
     const TStats ts = to_ts(job.ts);
     const int rows_per = (job.m + 7) / 8;
     const int i_lo = min(job.m, wid * rows_per), i_hi = min(job.m, i_lo + rows_per);
@@ -304,7 +313,7 @@ __global__ void __launch_bounds__(256)
     }
     best = block_best(best, scratch);
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
-    tail_reduce(tail, scratch);
+    tail_reduce(tail, scratch, unsigned(active), tail.n - int(gridDim.x) + active);
 }
 
 // ---- FP64 replica (non-integer images / templates) --------------------------------------
@@ -403,12 +412,14 @@ __global__ void k_reduce_cells(const CellH* __restrict__ partials, int n, CellH*
 // Fused tail reduction (TailReduce): called by every thread of every block after the
 // block's partial is stored.  The last block to take a ticket reads all partials through
 // L2 (other SMs wrote them) and finishes the phase like k_reduce_cells.
-__device__ void tail_reduce(const TailReduce& tr, Cell* scratch) {
+__device__ void tail_reduce(const TailReduce& tr, Cell* scratch, unsigned nblocks, int n) {
     if (!tr.ticket) return;  // uniform
+    if (nblocks == 0) nblocks = gridDim.x * gridDim.y * gridDim.z;
+    const int nred = n >= 0 ? n : tr.n;
     __shared__ int is_last;
     if (threadIdx.x == 0) {  // thread 0 stored this block's partial: publish it, take a ticket
         __threadfence();
-        is_last = atomicAdd(tr.ticket, 1u) == gridDim.x * gridDim.y * gridDim.z - 1;
+        is_last = atomicAdd(tr.ticket, 1u) == nblocks - 1;
     }
     __syncthreads();
     if (!is_last) return;
@@ -416,13 +427,13 @@ __device__ void tail_reduce(const TailReduce& tr, Cell* scratch) {
     Cell best = no_cell();
     // all of a thread's partials loaded before any comparison (one L2 latency, not n/blockDim)
     constexpr int kU = 4;
-    for (int i0 = threadIdx.x; i0 < tr.n; i0 += kU * blockDim.x) {
+    for (int i0 = threadIdx.x; i0 < nred; i0 += kU * blockDim.x) {
         Cell c[kU];
 #pragma unroll
         for (int u = 0; u < kU; ++u) {
             const int i = i0 + u * blockDim.x;
             c[u] = no_cell();
-            if (i < tr.n) {
+            if (i < nred) {
                 const CellH* h = tr.partials + i;
                 c[u] = Cell{__ldcg(&h->rho), __ldcg(&h->row), __ldcg(&h->col), __ldcg(&h->flags)};
             }
