@@ -171,6 +171,24 @@ bool better_h(const tmk::CellH& a, const tmk::CellH& b) {
     return a.col < b.col;
 }
 
+// Wait for an event by polling (no blocking-sync wake-up latency at the end of a search;
+// TMATCH_SPIN=0 uses cudaEventSynchronize).
+void spin_wait(cudaEvent_t ev) {
+    static const bool spin = [] {
+        const char* e = std::getenv("TMATCH_SPIN");
+        return !(e && std::strcmp(e, "0") == 0);
+    }();
+    if (!spin) {
+        CK(cudaEventSynchronize(ev));
+        return;
+    }
+    for (;;) {
+        const cudaError_t q = cudaEventQuery(ev);
+        if (q == cudaSuccess) return;
+        if (q != cudaErrorNotReady) CK(q);
+    }
+}
+
 double ms_between(cudaEvent_t a, cudaEvent_t b) {
     float ms = 0.f;
     cudaEventElapsedTime(&ms, a, b);
@@ -1825,9 +1843,11 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         const std::function<void()> f = std::move(ctx->before_final_sync);
         ctx->before_final_sync = nullptr;
         f();
-        CK(cudaEventSynchronize(ctx->ev1));
+        spin_wait(ctx->ev1);
     } else {
-        CK(cudaStreamSynchronize(s));
+        CK(cudaEventRecord(ctx->ev1, s));
+        ctx->ev1_set = true;
+        spin_wait(ctx->ev1);
     }
     HT("sync");
     tmk::CellH cells[3] = {hr->cells[0], hr->cells[1], hr->cells[2]};
@@ -2741,6 +2761,10 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
                      const tm_match_params* params, tm_match_result* out,
                      const FusedPre* pre = nullptr) {
     ctx->ev1_set = false;
+    // the window statistics first (every path needs them): the device starts while the
+    // host does the rest of the call's set-up
+    if (m >= 1 && n >= 1 && m <= img->p && n <= img->q) get_ws(ctx, img, m, n);
+    HT("ws_enqueued");
     Tmpl T;
     bool uploaded = false;
     // Predicted h_e: the last one seen for this image/template shape (else h0).  Fused
@@ -2775,7 +2799,7 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
         ctx->spec.armed = false;
         if (!ctx->ev1_set) CK(cudaEventRecord(ctx->ev1, ctx->s));
         ctx->ev1_set = false;
-        CK(cudaEventSynchronize(ctx->ev1));
+        spin_wait(ctx->ev1);
         out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
         return;
     }
@@ -2795,7 +2819,7 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
     *out = run_uploaded(ctx, prep.get(), img, T, *params, nullptr);
     if (!ctx->ev1_set) CK(cudaEventRecord(ctx->ev1, ctx->s));
     ctx->ev1_set = false;
-    CK(cudaEventSynchronize(ctx->ev1));
+    spin_wait(ctx->ev1);
     out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
 }
 
