@@ -26,6 +26,26 @@ def _u8ptr(a):
     return a.ctypes.data_as(C.POINTER(C.c_uint8))
 
 
+_PARAMS_CACHE: dict = {}
+
+
+def cached_params(**kw):
+    """make_params memoised on its (hashable) arguments: the per-call cost of building the
+    struct is most of a small search's Python overhead.  The returned struct is shared and
+    must not be modified."""
+    try:
+        key = tuple(sorted(kw.items()))
+        hash(key)
+    except TypeError:  # e.g. a numpy kernel profile
+        return make_params(**kw)
+    p = _PARAMS_CACHE.get(key)
+    if p is None:
+        if len(_PARAMS_CACHE) > 256:
+            _PARAMS_CACHE.clear()
+        p = _PARAMS_CACHE[key] = make_params(**kw)
+    return p
+
+
 def make_params(mode="egs", policy="reference", init_threshold=None, parallel=False, threads=2,
                 h0=3, w0=3, rho_th=0.8, rho_max=0.95, xi_fraction=0.005, opta_margin=0.005,
                 kernel=DEFAULT_PROFILE, record_visits=False, max_group=127, seed_margin=0.02):
@@ -341,7 +361,7 @@ class Context:
         img = self.image(img)
         t = np.asarray(t)
         m, n = t.shape
-        p = make_params(mode=mode, **kw)
+        p = cached_params(mode=mode, **kw)
         res = MatchResult()
         if t.dtype == np.uint8:
             t = np.ascontiguousarray(t)
@@ -361,7 +381,7 @@ class Context:
             raise ValueError("search_upload: pixel array shape differs from the image")
         t = np.ascontiguousarray(t, dtype=np.uint8)
         m, n = t.shape
-        p = make_params(mode=mode, **kw)
+        p = cached_params(mode=mode, **kw)
         res = MatchResult()
         N.check(N.lib().tm_search_upload_u8(self.h, img.h, _u8ptr(px), _u8ptr(t), m, n,
                                             C.byref(p), C.byref(res)))
@@ -380,7 +400,7 @@ class Context:
             raise ValueError("search_stream: images must be equally shaped 2-D arrays")
         t = np.ascontiguousarray(t, dtype=np.uint8)
         m, n = t.shape
-        p = make_params(mode=mode, **kw)
+        p = cached_params(mode=mode, **kw)
         ptrs = (C.c_void_p * len(imgs))(*[a.ctypes.data for a in imgs])
         res = (MatchResult * len(imgs))()
         N.check(N.lib().tm_search_stream_u8(self.h, ptrs, len(imgs), shape[0], shape[1],
