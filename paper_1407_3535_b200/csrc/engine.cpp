@@ -220,6 +220,7 @@ struct WS {
     DBuf<double> mu, om;
     DBuf<uint8_t> fl;
     int er = 0, ec = 0, m = 0, n = 0;
+    bool valid = false;  // false: the image changed; recomputed into the same buffers
     tmk::DevStats dev() const { return tmk::DevStats{mu.p, om.p, fl.p, er, ec, m, n}; }
 };
 
@@ -584,12 +585,25 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
     }
 }
 
+// The image's pixels changed: its cached window statistics are stale (kept allocated and
+// recomputed in place by the next get_ws).
+void invalidate_ws(tm_image* img) {
+    for (auto& kv : img->ws_cache) kv.second->valid = false;
+}
+
 WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
     auto key = std::make_pair(m, n);
     auto it = img->ws_cache.find(key);
-    if (it != img->ws_cache.end()) return *it->second;
+    if (it != img->ws_cache.end()) {
+        if (!it->second->valid) {  // stale (new pixels): recompute, no buffer churn
+            compute_ws(ctx, img, m, n, *it->second);
+            it->second->valid = true;
+        }
+        return *it->second;
+    }
     auto ws = std::make_unique<WS>();
     compute_ws(ctx, img, m, n, *ws);
+    ws->valid = true;
     WS& ref = *ws;
     img->ws_cache[key] = std::move(ws);
     return ref;
@@ -2228,7 +2242,7 @@ int tm_image_reset_cache(tm_image* img) {
     if (!img) return TM_EINVAL;
     tm_ctx* ctx = img->ctx;
     return guard(ctx, [&] {
-        img->ws_cache.clear();
+        invalidate_ws(img);
         img->have_qtotal = false;
     });
 }
@@ -2276,7 +2290,7 @@ int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
         img->have_f64 = false;
         img->have_qtotal = false;
         tc_pitch_copy(ctx, img);
-        img->ws_cache.clear();
+        invalidate_ws(img);
     });
 }
 
@@ -2849,7 +2863,7 @@ int tm_search_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels, const
         img->have_f32 = img->have_f64 = false;
         img->have_qtotal = false;
         tc_pitch_copy(ctx, img);
-        img->ws_cache.clear();
+        invalidate_ws(img);
         std::vector<double> t(size_t(m) * n);
         for (size_t i = 0; i < t.size(); ++i) t[i] = tmpl[i];
         search_resident(ctx, img, t.data(), m, n, params, out);
@@ -2908,7 +2922,7 @@ int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int
             img->have_f32 = img->have_f64 = false;
             img->have_qtotal = false;
             tc_pitch_copy(ctx, img);
-            img->ws_cache.clear();
+            invalidate_ws(img);
             get_ws(ctx, img, m, n);
         };
         const bool ws_ok = m <= rows && n <= cols;  // (else the search reports the error)
@@ -2929,7 +2943,7 @@ int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int
                     CK(cudaStreamWaitEvent(ctx->s, ctx->ev_up[i & 1], 0));
                     img->have_f32 = img->have_f64 = img->have_qtotal = false;
                     tc_pitch_copy(ctx, img);
-                    img->ws_cache.clear();
+                    invalidate_ws(img);
                 }
             }
             pro_done = false;
