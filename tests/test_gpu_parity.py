@@ -533,6 +533,42 @@ def test_search_stream_equals_single_calls(ctx):
     assert ctx.search_stream([], t) == []
 
 
+@pytest.mark.parametrize("policy", ["seeded", "frozen"])
+def test_search_stream_mixed_group_sizes(ctx, policy):
+    """A stream whose images alternate between white noise (small h_e) and smooth fields
+    (larger h_e): the next image's scan 1 + seeding, enqueued behind the current search on
+    the predicted grid, is mispredicted every other image and must fall back to the
+    standard path -- every result equals the single-call result."""
+    rng = np.random.default_rng(29)
+    rows, cols, m, n = 170, 230, 24, 26
+    rough = [rng.integers(0, 256, (rows, cols)).astype(np.uint8) for _ in range(3)]
+    smooth = []
+    for _ in range(3):
+        base = np.cumsum(np.cumsum(rng.normal(size=(rows, cols)), 0), 1)
+        smooth.append(np.clip(np.rint((base - base.min()) / np.ptp(base) * 255), 0,
+                              255).astype(np.uint8))
+    imgs = [rough[0], smooth[0], smooth[1], rough[1], smooth[2], rough[2]]
+    t = np.clip(np.rint(smooth[1][60:84, 70:96] * 1.05 - 4 + rng.normal(0, 3, (m, n))), 0,
+                255).astype(np.uint8)
+    keys = ("best_row", "best_col", "best_rho", "eliminated", "retained", "centers", "ops",
+            "final_threshold")
+    got = ctx.search_stream(imgs, t, policy=policy, parallel=(policy == "frozen"), threads=2)
+    b = ctx.image(np.zeros((rows, cols), np.uint8))
+    hs = set()
+    for g, a in zip(got, imgs):
+        want = ctx.search_upload(b, a, t, policy=policy, parallel=(policy == "frozen"),
+                                 threads=2)
+        for k in keys:
+            assert getattr(g, k) == getattr(want, k), (policy, k)
+        gi = ctx.image(a)
+        prep = ctx.prepare(gi, m, n, mode="egs")
+        hs.add(prep.info["h"])
+        prep.close()
+        gi.close()
+    b.close()
+    assert len(hs) >= 2, hs  # the group size really changes along the stream
+
+
 @pytest.mark.parametrize("dense", [False, True])
 def test_search_upload_undecided_windows(ctx, port, dense):
     """A 3400 x 3300 image whose noise floor ((rows + cols) * eps * sum of squares, about
