@@ -1265,9 +1265,11 @@ struct EgsOut {
 EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, int h0, int w0,
                       double rho_tb, double xi, int max_group, DBuf<double>& best,
                       const std::function<void()>* before_sync = nullptr,
-                      const tmk::SecFuse* fuse = nullptr, bool* fuse_hit = nullptr) {
+                      const tmk::SecFuse* fuse = nullptr, bool* fuse_hit = nullptr,
+                      bool egs_preinit = false) {
     if (fuse_hit) *fuse_hit = false;
     bool fused_ran = false;  // the fused candidate was launched in the first batch
+    unsigned long long first_seq = 0;
     if (h0 < 1 || w0 < 1 || h0 % 2 == 0 || w0 % 2 == 0)
         invalid("efficient_group_size: initial group size must be odd");
     if (rho_tb <= 0.0 || rho_tb >= 1.0)
@@ -1320,9 +1322,12 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
         }
         bool map_written[4] = {false, false, false, false};
         const unsigned long long batch_seq = ++ctx->egs_seq;
+        if (first_batch) first_seq = batch_seq;
         if (first_batch) {  // stop = 0, prev = +inf, nr[0..3] = 0, h_acc = 0, gate = 0
-            CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s, dhacc, dgate));
-            ctx->add(1);
+            if (!egs_preinit) {  // (else done by the centre scan's reduction)
+                CK(tmk::egs_init(dstop, dprev, ctx->counters.p + 8, ctx->s, dhacc, dgate));
+                ctx->add(1);
+            }
             first_batch = false;
         } else {
             CK(cudaMemsetAsync(ctx->counters.p + 8, 0, 32, ctx->s));
@@ -1352,6 +1357,12 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
             dec.nc = nc;
             dec.out = last ? ctx->hres_dev : nullptr;
             dec.seq = batch_seq;
+            if (fuse && last && batch_seq == first_seq) {  // the gated survivors' dispatch
+                dec.disp_tally = ctx->tally.p;
+                dec.disp_E = E;
+                dec.disp_dense = reinterpret_cast<int*>(ctx->counters.p + 22);
+                dec.disp_list = ctx->counters.p + 23;
+            }
             bool decided = false;
             const bool is_pred = cand[k].h == pred && cand[k].w == pred;
             const bool fuse_here = fuse && is_pred && !fused_ran;
@@ -1362,10 +1373,7 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
                                              fuse_here ? fuse : nullptr);
             if (fuse_here) fused_ran = true;
             if (!decided) {
-                CK(tmk::egs_decide(ctx->counters.p + 8 + k, dprev, dstop, er, ec, cand[k].h,
-                                   cand[k].w, xi, cap, dhacc, ctx->spec_want, dgate, ctx->s,
-                                   ctx->counters.p + 8, nc, last ? ctx->hres_dev : nullptr,
-                                   batch_seq));
+                CK(tmk::egs_decide_d(dec, ctx->s));
                 ctx->add(1);
             }
         }
@@ -1677,14 +1685,15 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // eval_survivors without the host round trip (tensor-core path): the survivor count stays
 // on the device; survivor_dispatch selects dense (masked tensor-core kernel) or list, the
 // other launch only writes empty partials.
+// dispatched: the dense/list choice is already made on the device (by the last EGS decision)
 void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                         const tmk::GridDesc& g, double* rho_loc,
-                        const unsigned long long* gate = nullptr) {
+                        const unsigned long long* gate = nullptr, bool dispatched = false) {
     cudaStream_t s = ctx->s;
     const size_t E = size_t(g.er) * g.ec;
     int* dense_flag = reinterpret_cast<int*>(ctx->counters.p + 22);
     unsigned long long* list_count = ctx->counters.p + 23;
-    CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s, gate));
+    if (!dispatched) CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s, gate));
     ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
     const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
     int np = 0;
@@ -2650,7 +2659,12 @@ bool search_fused_begin(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, i
     if (!tc_path(ctx, img, T) || !fp32_path(img, T))  // (implied by the checks above)
         throw TmError{TM_ECUDA, "search_fused: template not on the 8-bit tensor-core path"};
     // scan 1 on the predicted grid (+ threshold bootstrap, tally zeroing) and the seeding
-    const tmk::ReduceOp op_init = centre_op(ctx, P);
+    tmk::ReduceOp op_init = centre_op(ctx, P);
+    op_init.egs_stop = reinterpret_cast<int*>(ctx->counters.p + 21);  // (k_egs_init's work)
+    op_init.egs_prev = reinterpret_cast<double*>(ctx->counters.p + 20);
+    op_init.egs_nr4 = ctx->counters.p + 8;
+    op_init.egs_hacc = reinterpret_cast<int*>(ctx->counters.p + 25);
+    op_init.egs_gate = ctx->counters.p + 24;
     centre_scan(ctx, img, ws, T, g, &op_init, side_b);
     HT("fused_centre");
     if (!ctx->sa_ready) throw TmError{TM_ECUDA, "search_fused: centre factors missing"};
@@ -2714,11 +2728,13 @@ void search_fused_end(tm_ctx* ctx, tm_image* img, const tm_match_params& P, cons
     // counts; on a miss its kernels do nothing and the standard path follows
     const unsigned long long* gate = ctx->counters.p + 24;
     const std::function<void()> hook = [&] {
-        eval_survivors_dev(ctx, img, ws, T, g, nullptr, gate);
+        // (the dense/list choice is made by the batch's last EGS decision)
+        eval_survivors_dev(ctx, img, ws, T, g, nullptr, gate, /*dispatched=*/true);
     };
     ctx->spec_want = pred;  // the decide kernels set the gate for this size
     const EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,
-                                    P.max_group, ctx->map_fused, &hook, &sf, &hit);
+                                    P.max_group, ctx->map_fused, &hook, &sf, &hit,
+                                    /*egs_preinit=*/true);  // (search_fused_begin's centre reduction)
     ctx->spec_want = 0;
     HT("fused_egs");
     if (hit && ctx->hres->spec != 1)

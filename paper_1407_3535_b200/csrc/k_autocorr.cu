@@ -871,6 +871,12 @@ __device__ void egs_decide_run(const EgsDecide& d) {
     // in-kernel rejection; either way h_acc is final)
     const unsigned long long gv = (*d.stop && d.want > 0 && *d.h_acc == d.want) ? 1ull : 0ull;
     *d.gate = gv;
+    if (d.out && d.disp_dense) {  // k_survivor_dispatch for the gated survivors behind
+        const unsigned long long ns = gv ? d.disp_tally->survivors : 0ull;
+        const bool dense = ns * 16 > d.disp_E;
+        *d.disp_dense = dense ? 1 : 0;
+        *d.disp_list = dense ? 0ull : ns;
+    }
     if (d.out) {  // last candidate of the batch: counts + gate into the mapped result block
         for (int i = 0; i < d.nc; ++i) d.out->nr[i] = d.nr_all[i];
         d.out->spec = gv;
@@ -1812,6 +1818,11 @@ bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h
 __global__ void k_egs_decide(EgsDecide d) {
     pdl_wait();
     egs_decide_run(d);
+}
+
+cudaError_t egs_decide_d(const EgsDecide& d, cudaStream_t s) {
+    launch_pdl(k_egs_decide, dim3(1), dim3(1), 0, s, d);
+    return cudaGetLastError();
 }
 
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,

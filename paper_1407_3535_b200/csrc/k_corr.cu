@@ -386,6 +386,13 @@ __device__ void apply_reduce_op(const Cell& best, CellH* out, const ReduceOp& op
         *op.thr = t;
         for (int i = 0; i < op.nzero64; ++i) op.zero64[i] = 0ull;
         if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull};
+        if (op.egs_stop) {  // k_egs_init
+            *op.egs_stop = 0;
+            *op.egs_prev = INFINITY;
+            for (int i = 0; i < 4; ++i) op.egs_nr4[i] = 0ull;
+            *op.egs_hacc = 0;
+            *op.egs_gate = 0ull;
+        }
     } else if (op.kind == 2) {  // k_threshold_raise
         if ((b.flags & 1) && !(b.flags & 2) && b.rho > *op.thr) *op.thr = b.rho;
     } else if (op.kind == 3) {  // result block for one device->host copy

@@ -71,6 +71,12 @@ struct EgsDecide {
     int nc = 0;
     ResultBlock* out = nullptr;  // last candidate of a batch: counts + gate for the host
     unsigned long long seq = 0;
+    // with out: k_survivor_dispatch's choice for the survivors enqueued behind the batch
+    // (gated: nothing to evaluate unless the gate is set); null = not fused
+    const Tally* disp_tally = nullptr;
+    unsigned long long disp_E = 0;
+    int* disp_dense = nullptr;
+    unsigned long long* disp_list = nullptr;
 };
 
 // Scan 2 fused into the R_co launch of the predicted group size (tm_search): scan 1 and the
@@ -102,6 +108,12 @@ struct ReduceOp {
     const CellH* cells = nullptr;  // kind 3: cells[0..2] to pack
     const Tally* tally = nullptr;
     ResultBlock* packed = nullptr;
+    // kind 1 (fused tm_search path): the EGS batch state k_egs_init would set
+    int* egs_stop = nullptr;
+    double* egs_prev = nullptr;
+    unsigned long long* egs_nr4 = nullptr;
+    int* egs_hacc = nullptr;
+    unsigned long long* egs_gate = nullptr;
 };
 
 // A reduction fused into the tail of the kernel producing the last partials of a phase: the
@@ -193,6 +205,8 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               const SecFuse* fuse = nullptr);
 // The group-column R_co kernel can run scan 2 in its epilogue (SecFuse) for this geometry.
 bool autocorr_sec_fuse_supported(int m, int n, GridDesc g);
+// k_egs_decide with a full decision record (the dispatch fields included)
+cudaError_t egs_decide_d(const EgsDecide& d, cudaStream_t s);
 cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* stop, int er, int ec,
                        int h, int w, double xi, int cap, int* h_acc, int want,
                        unsigned long long* gate, cudaStream_t s,
