@@ -2649,10 +2649,11 @@ bool search_fused_begin(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, i
     HT("fused_ws");
     const tmk::TcPlan bplan = tmk::tc_plan(m, n, pred, kTcSmemBudget);
     const bool side_b = bplan.nch > 0;
-    if (side_b) {
-        ctx->tc_b.ensure(bplan.total_bytes);
+    if (side_b && !(ctx->spec_b && ctx->tc_b.cap >= bplan.total_bytes)) {
+        ctx->tc_b.ensure(bplan.total_bytes);  // (not sized before the statistics by b_early)
         CK(cudaEventRecord(ctx->ev_b0, ctx->s));
     }
+    ctx->spec_b = false;
     const Tmpl T = upload_template(ctx, tmpl, m, n, /*side=*/true);
     if (T.ts.flat) invalid("transitive_search: constant template has no defined correlation");
     HT("fused_template");
@@ -2777,6 +2778,20 @@ bool search_fused(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
 }
 
 // prepare + run of one template on a resident image (tm_search's body; ev0 recorded).
+// Size tc_b for the predicted centre scan and record ev_b0 (the side-stream B build waits
+// only for it), before the call's first kernel; sets spec_b.
+void b_early(tm_ctx* ctx, const tm_image* img, int m, int n, int want) {
+    ctx->spec_b = false;
+    if (want > 0 && ctx->tc && m >= 1 && n >= 1 && m <= img->p && n <= img->q) {
+        const tmk::TcPlan plan = tmk::tc_plan(m, n, want, kTcSmemBudget);
+        if (plan.nch > 0) {
+            ctx->tc_b.ensure(plan.total_bytes);
+            CK(cudaEventRecord(ctx->ev_b0, ctx->s));
+            ctx->spec_b = true;
+        }
+    }
+}
+
 // Predicted h_e of a search: the last one seen for this image/template shape (else h0);
 // 0 when no prediction applies.
 int predicted_he(tm_ctx* ctx, const tm_image* img, int m, int n, const tm_match_params& P) {
@@ -2791,10 +2806,6 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
                      const tm_match_params* params, tm_match_result* out,
                      const FusedPre* pre = nullptr) {
     ctx->ev1_set = false;
-    // the window statistics first (every path needs them): the device starts while the
-    // host does the rest of the call's set-up
-    if (m >= 1 && n >= 1 && m <= img->p && n <= img->q) get_ws(ctx, img, m, n);
-    HT("ws_enqueued");
     Tmpl T;
     bool uploaded = false;
     // Predicted h_e: the last one seen for this image/template shape (else h0).  Fused
@@ -2804,18 +2815,15 @@ void search_resident(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int 
     const int want = predicted_he(ctx, img, m, n, *params);
     ctx->spec_want = want;
     ctx->spec.armed = false;
-    // B of the predicted centre scan is built on the side stream during the EGS batch: its
-    // buffer is sized now, before the batch is enqueued, so the side stream only waits for
-    // this point
+    // B of the predicted centre scan is built on the side stream (during the statistics on
+    // the fused path, during the EGS batch otherwise): its buffer is sized now, before any
+    // kernel of this call is enqueued, so the side stream waits for nothing of this call
     ctx->spec_b = false;
-    if (want > 0 && ctx->tc && m <= img->p && n <= img->q) {
-        const tmk::TcPlan plan = tmk::tc_plan(m, n, want, kTcSmemBudget);
-        if (plan.nch > 0) {
-            ctx->tc_b.ensure(plan.total_bytes);
-            CK(cudaEventRecord(ctx->ev_b0, ctx->s));
-            ctx->spec_b = true;
-        }
-    }
+    if (!pre || !pre->ok) b_early(ctx, img, m, n, want);
+    // the window statistics next (every path needs them): the device starts while the host
+    // does the rest of the call's set-up
+    if (m >= 1 && n >= 1 && m <= img->p && n <= img->q) get_ws(ctx, img, m, n);
+    HT("ws_enqueued");
     const std::function<void()> hook = [&] {
         T = upload_template(ctx, tmpl, m, n, /*side=*/true);
         uploaded = true;
@@ -2967,13 +2975,15 @@ int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int
             cur_pre.swap_from(next_pre);
             if (ws_ok && i + 1 < nimg)
                 ctx->before_final_sync = [&, i] {
+                    tm_image* nimg_ = ctx->sslot[(i + 1) & 1].get();
+                    const int pred = predicted_he(ctx, nimg_, m, n, *params);
+                    b_early(ctx, nimg_, m, n, pred);  // (B build overlaps the statistics)
                     prologue(i + 1);
                     pro_done = true;
                     // ... and the next search's scan 1 + seeding when it takes the fused path
-                    tm_image* nimg_ = ctx->sslot[(i + 1) & 1].get();
-                    const int pred = predicted_he(ctx, nimg_, m, n, *params);
                     if (pred > 0)
                         search_fused_begin(ctx, nimg_, t.data(), m, n, *params, pred, next_pre);
+                    ctx->spec_b = false;
                 };
             try {
                 search_resident(ctx, img, t.data(), m, n, params, &out[i],
