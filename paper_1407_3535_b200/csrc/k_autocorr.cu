@@ -1418,7 +1418,9 @@ __global__ void __launch_bounds__(NT)
                 }
             }
         }
-        if constexpr (FUSE) {  // survivor compaction, one ballot per member row offset
+        // survivor compaction, one ballot per member row offset (skipped by the whole warp
+        // when none of its members survived: the common case)
+        if (FUSE && __any_sync(0xffffffffu, surv != 0u)) {
 #pragma unroll
             for (int d = 0; d < H; ++d) {
                 const bool sv = (surv >> d) & 1u;
