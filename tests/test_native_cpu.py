@@ -46,3 +46,17 @@ def test_built_for_sm100a_only():
         pytest.skip("cuobjdump unavailable")
     arches = {ln.split(".")[-2] for ln in out.stdout.splitlines() if ".cubin" in ln}
     assert arches == {"sm_100a"}, arches
+
+
+def test_cached_params_are_memoised_per_arguments():
+    """api.cached_params (the search calls' parameter structs): equal arguments share one
+    struct, different arguments never do, and the fields are the requested ones."""
+    from paper_1407_3535_b200 import api
+    a = api.cached_params(mode="egs", policy="seeded")
+    b = api.cached_params(mode="egs", policy="seeded")
+    c = api.cached_params(mode="egs", policy="frozen", parallel=True, threads=4)
+    assert a is b and a is not c
+    assert (a.policy, c.policy, c.parallel, c.threads) == (N.POLICY["seeded"],
+                                                           N.POLICY["frozen"], 1, 4)
+    d = api.make_params(mode="egs", policy="seeded")
+    assert (d.mode, d.policy, d.h0, d.rho_th) == (a.mode, a.policy, a.h0, a.rho_th)
