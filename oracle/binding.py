@@ -305,6 +305,76 @@ class Oracle:
                                                  C.byref(rm)))
         return res, pm.value, rm.value
 
+    def brute_threads(self, t, img, threads=None):
+        """brute_force_match with the reference's own thread pool (stats.cpp:186-195)."""
+        assert self.kind == "ref"
+        t, img = _d(t), _d(img)
+        res = TmoResult()
+        self._check(self.lib.ref_brute_threads(_ptr(t), t.shape[0], t.shape[1], _ptr(img),
+                                               img.shape[0], img.shape[1],
+                                               threads or os.cpu_count(), C.byref(res)))
+        return res
+
+    def prepare_run_batch(self, tmpls, img, mode="egs", parallel=True, threads=None):
+        """One prepare_egs/prepare_opta + run_* per template (cmd_bench's cache,
+        cli.cpp:213-237).  Returns (results, info{h,w,kappa,lambda}, prep_ms, run_ms[])."""
+        assert self.kind == "ref"
+        tm = np.ascontiguousarray(np.stack([_d(t) for t in tmpls]))
+        img = _d(img)
+        k, m, n = tm.shape
+        res = (TmoResult * k)()
+        info = np.zeros(4)
+        run_ms = np.zeros(k)
+        pm = C.c_double()
+        self._check(self.lib.ref_prepare_run_batch(
+            _ptr(tm), k, m, n, _ptr(img), img.shape[0], img.shape[1], MODES[mode],
+            int(parallel), threads or os.cpu_count(), res, _ptr(info), C.byref(pm),
+            _ptr(run_ms)))
+        return list(res), dict(h=int(info[0]), w=int(info[1]), kappa=int(info[2]),
+                               lam=float(info[3])), pm.value, run_ms
+
+    def content_hash(self, img):
+        assert self.kind == "ref"
+        img = _d(img)
+        self.lib.ref_content_hash.restype = C.c_uint64
+        return self.lib.ref_content_hash(_ptr(img), img.shape[0], img.shape[1])
+
+    def autocorr_cache_key(self, img, m, n, h, w):
+        assert self.kind == "ref"
+        img = _d(img)
+        self.lib.ref_autocorr_cache_key.restype = C.c_uint64
+        return self.lib.ref_autocorr_cache_key(_ptr(img), img.shape[0], img.shape[1], m, n,
+                                               h, w)
+
+    def save_autocorr(self, amap, h, w, key, path):
+        assert self.kind == "ref"
+        amap = _d(amap)
+        self._check(self.lib.ref_save_autocorr(_ptr(amap), amap.shape[0], amap.shape[1], h, w,
+                                               C.c_uint64(key), path.encode()))
+
+    def load_autocorr(self, path, key, rows, cols, h, w):
+        assert self.kind == "ref"
+        out = np.empty((rows, cols))
+        ok = self.lib.ref_load_autocorr(path.encode(), C.c_uint64(key), rows, cols, h, w,
+                                        _ptr(out))
+        return out if ok else None
+
+    def load_image(self, path):
+        assert self.kind == "ref"
+        r, c = C.c_int(), C.c_int()
+        self._check(self.lib.ref_load_image(path.encode(), C.byref(r), C.byref(c), None, 0))
+        out = np.empty((r.value, c.value))
+        self._check(self.lib.ref_load_image(path.encode(), C.byref(r), C.byref(c), _ptr(out),
+                                            out.size))
+        return out
+
+    def save_image(self, img, path):
+        assert self.kind == "ref"
+        img = _d(img)
+        self._check(self.lib.ref_save_image(_ptr(img), img.shape[0], img.shape[1],
+                                            path.encode()))
+
+
 
 def available(kind):
     return os.path.exists(PORT_SO if kind == "port" else REF_SO)

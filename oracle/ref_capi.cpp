@@ -4,6 +4,8 @@
 // bench.py can drive "the reference itself" and "the port" through one ctypes binding.
 // Output: oracle/_ref/libtmatch_ref.so (git-ignored; travels to the GPU box).
 #include <chrono>
+#include <cstdint>
+#include <optional>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -98,18 +100,6 @@ WindowStats to_ws(const double* mu, const double* om, const uint8_t* fl, int er,
     return ws;
 }
 }  // namespace
-
-namespace tmatch {
-// image.cpp needs libpng (absent); content_hash only feeds the map-cache key.
-std::uint64_t content_hash(const Image& img) {
-    std::uint64_t h = 1469598103934665603ull;
-    for (double v : img.data()) {
-        h ^= std::uint64_t(v);
-        h *= 1099511628211ull;
-    }
-    return h;
-}
-}  // namespace tmatch
 
 extern "C" {
 
@@ -434,6 +424,102 @@ int ref_prepare_run_egs(const double* t, int m, int n, const double* img, int p,
         *prep_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
         *run_ms = std::chrono::duration<double, std::milli>(t2 - t1).count();
     });
+}
+
+// ---- reference-only extras for the per-config goldens and the map-cache interop -------
+
+// brute_force_match (stats.cpp:156-213) with the reference's own row-partitioned threads.
+int ref_brute_threads(const double* t, int m, int n, const double* img, int p, int q,
+                      int threads, tmo_result* res) {
+    return guard([&] {
+        BruteOptions bo;
+        bo.threads = threads;
+        fill(brute_force_match(wrap(t, m, n), wrap(img, p, q), bo), res);
+    });
+}
+
+// One preparation (prepare_egs matcher.cpp:205 or prepare_opta :217) shared by a batch of
+// templates of one size, then run_egs/run_opta per template -- cmd_bench's cache
+// (cli.cpp:213-237).  info = {h_e, w_e, kappa, lambda}; run_ms per template.
+int ref_prepare_run_batch(const double* tmpls, int ntmpl, int m, int n, const double* img,
+                          int p, int q, int mode, int parallel, int threads, tmo_result* res,
+                          double* info, double* prep_ms, double* run_ms) {
+    return guard([&] {
+        MatchParams mp;
+        mp.parallel = parallel != 0;
+        mp.threads = threads;
+        const Image I = wrap(img, p, q);
+        const std::size_t mn = std::size_t(m) * n;
+        const auto t0 = std::chrono::steady_clock::now();
+        std::optional<PreparedEgs> pe;
+        std::optional<PreparedOptA> po;
+        if (mode == 2) {
+            po.emplace(prepare_opta(I, m, n, mp));
+            info[0] = po->opta.egs.h;
+            info[1] = po->opta.egs.w;
+            info[2] = po->opta.kappa;
+            info[3] = po->opta.lambda;
+        } else {
+            pe.emplace(prepare_egs(I, m, n, mp));
+            info[0] = pe->egs.h;
+            info[1] = pe->egs.w;
+            info[2] = 0;
+            info[3] = 0;
+        }
+        *prep_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                       .count();
+        for (int k = 0; k < ntmpl; ++k) {
+            const Image T = wrap(tmpls + k * mn, m, n);
+            const auto t1 = std::chrono::steady_clock::now();
+            const MatchResult r = mode == 2 ? run_opta(T, I, *po, mp) : run_egs(T, I, *pe, mp);
+            run_ms[k] = std::chrono::duration<double, std::milli>(
+                            std::chrono::steady_clock::now() - t1).count();
+            fill(r, res + k);
+        }
+    });
+}
+
+// image.cpp:215-228 and autocorr.cpp:102-153, compiled from the reference sources.
+uint64_t ref_content_hash(const double* img, int p, int q) { return content_hash(wrap(img, p, q)); }
+
+uint64_t ref_autocorr_cache_key(const double* img, int p, int q, int m, int n, int h, int w) {
+    return autocorr_cache_key(wrap(img, p, q), m, n, h, w);
+}
+
+int ref_save_autocorr(const double* map, int rows, int cols, int h, int w, uint64_t key,
+                      const char* path) {
+    return guard([&] {
+        AutoCorrMap a;
+        a.rows = rows;
+        a.cols = cols;
+        a.group_h = h;
+        a.group_w = w;
+        a.values.assign(map, map + std::size_t(rows) * cols);
+        save_autocorr(a, key, path);
+    });
+}
+
+// 1 = loaded into map (rows*cols doubles; header checked against rows/cols/h/w), 0 = miss.
+int ref_load_autocorr(const char* path, uint64_t key, int rows, int cols, int h, int w,
+                      double* map) {
+    const auto a = load_autocorr(path, key);
+    if (!a || a->rows != rows || a->cols != cols || a->group_h != h || a->group_w != w) return 0;
+    std::memcpy(map, a->values.data(), a->values.size() * 8);
+    return 1;
+}
+
+// PGM I/O (image.cpp:25-84, 187-213): load into out (rows*cols) or report the size.
+int ref_load_image(const char* path, int* rows, int* cols, double* out, int cap) {
+    return guard([&] {
+        const Image I = load_image(path);
+        *rows = I.rows();
+        *cols = I.cols();
+        if (out && cap >= int(I.size())) std::memcpy(out, I.data().data(), I.size() * 8);
+    });
+}
+
+int ref_save_image(const double* img, int p, int q, const char* path) {
+    return guard([&] { save_image(wrap(img, p, q), path); });
 }
 
 }  // extern "C"

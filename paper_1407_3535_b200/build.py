@@ -85,6 +85,13 @@ def build(verbose: bool = False) -> dict:
             _run(["g++"] + CXX_FLAGS + ["-o", check_bin, check_src, "-L" + LIB, "-ltmatch",
                                         "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
         out["api_check"] = check_bin
+        for tool in ("cache_interop",):
+            src = os.path.join(ROOT, "tests", "cpp", tool + ".cpp")
+            binp = os.path.join(LIB, tool)
+            if os.path.exists(src) and _newer(binp, [src, api_so] + api_hdrs):
+                _run(["g++"] + CXX_FLAGS + ["-o", binp, src, "-L" + LIB, "-ltmatch",
+                                            "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
+            out[tool] = binp
     return out
 
 

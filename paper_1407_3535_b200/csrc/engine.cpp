@@ -376,7 +376,8 @@ struct tm_image {
     DBuf<double> f64;
     bool have_f64 = false;
     bool have_qtotal = false;  // prefix_noise computed on the device
-    DBuf<double> pn;           // [0] q_total (FP64 path) / [1] prefix_noise
+    DBuf<double> pn;           // [1] prefix_noise; FP64 path: the noise block (k_stats.cu)
+    DBuf<double> pnpart;       // FP64 path: per-block partial sums of squares
     DBuf<unsigned long long> qt;
     std::map<std::pair<int, int>, std::unique_ptr<WS>> ws_cache;
     // 16-byte pitched zero-padded 8-bit copy for the tensor-core path (k_tc.cu)
@@ -510,7 +511,7 @@ void classify_device_image(tm_ctx* ctx, tm_image* img) {
 // prefix_noise (stats.cpp:78-81) on the device; returns a device pointer.
 const double* image_prefix_noise(tm_ctx* ctx, tm_image* img) {
     if (!img->have_qtotal) {
-        img->pn.ensure(2);
+        img->pn.ensure(8);
         if (img->integer) {
             if (!img->qt.p) {  // running sum + block counter, kept zero between uses
                 img->qt.ensure(2);
@@ -518,7 +519,8 @@ const double* image_prefix_noise(tm_ctx* ctx, tm_image* img) {
             }
             CK(tmk::prefix_noise_u8(img->u8.p, img->p, img->q, img->qt.p, img->pn.p + 1, ctx->s));
         } else {
-            CK(tmk::prefix_noise_f64(img->f64.p, img->p, img->q, img->pn.p, img->pn.p + 1, ctx->s));
+            img->pnpart.ensure(tmk::prefix_noise_f64_parts());
+            CK(tmk::prefix_noise_f64(img->f64.p, img->p, img->q, img->pnpart.p, img->pn.p, ctx->s));
         }
         ctx->add(2);
         img->have_qtotal = true;
@@ -580,8 +582,11 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
         CK(tmk::replica_window_diff(ctx->prefix.p, p, q, m, n, ctx->S.p, ctx->s));
         CK(tmk::replica_window_diff(ctx->prefix.p + bt.pslot, p, q, m, n, ctx->Q.p, ctx->s));
         ctx->add(4);
-        CK(tmk::stats_from_sums(ctx->S.p, ctx->Q.p, E, m, n, prefix_noise, ws.dev(), ctx->s));
-        ctx->add(1);
+        // the flat floor against the bracket of the reference's sequential q_total;
+        // undecided windows trigger the sequential replay and a redo (k_stats.cu)
+        CK(tmk::stats_from_sums(ctx->S.p, ctx->Q.p, E, m, n, img->f64.p, p, q, img->pn.p,
+                                ws.dev(), ctx->s));
+        ctx->add(4);
     }
 }
 
@@ -1162,12 +1167,12 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
                                       img->u8p_pitch, dec, decided, fuse));
             ctx->add(1);
             return !count_only && !fuse;
-        } else if (tmk::autocorr_colwalk_supported(m, q, g) && vbytes <= (size_t(16) << 30)) {
+        } else if (tmk::autocorr_colwalk_supported(m, n, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
             CK(tmk::autocorr_u8_colwalk(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
                                         reinterpret_cast<unsigned*>(ctx->acH.p), ctx->s));
             ctx->add(3);
-        } else if (tmk::autocorr_two_pass_supported(n, g) && hbytes <= (size_t(16) << 30)) {
+        } else if (tmk::autocorr_two_pass_supported(m, n, g) && hbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(hbytes / sizeof(int));
             CK(tmk::autocorr_u8_two_pass(img->u8.p, p, q, m, n, g, ws.dev(), thr, map, nr,
                                          ctx->acH.p, ctx->s));

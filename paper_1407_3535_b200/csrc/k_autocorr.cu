@@ -1805,7 +1805,16 @@ size_t autocorr_rowsum_bytes(int p, GridDesc g) {  // H and its transposed prefi
     return 2 * size_t(g.h) * g.w * g.tc * p * sizeof(unsigned);
 }
 
-bool autocorr_two_pass_supported(int n, GridDesc g) { return ac_supported(n, g.h, g.w); }
+// The 8-bit R_co kernels (k_acg, k_acf, the column walk and the two-pass kernel) keep the
+// centre-member cross sum S = sum of m*n products of two bytes in u32: exact only while
+// m*n*255^2 < 2^32 (m*n < 66051).  Larger templates take the generic k_autocorr_u8 (s64).
+static bool u32_cross_exact(int m, int n) {
+    return double(m) * double(n) * 65025.0 < 4294967296.0;
+}
+
+bool autocorr_two_pass_supported(int m, int n, GridDesc g) {
+    return u32_cross_exact(m, n) && ac_supported(n, g.h, g.w);
+}
 
 
 // One EGS acceptance step on the device (egs.cpp:61-88 with total_cost of egs.cpp:28-37,
@@ -1860,7 +1869,7 @@ bool autocorr_sec_fuse_supported(int m, int n, GridDesc g) {
 bool autocorr_fused_supported(int m, int n, GridDesc g) {
     // 32-bit row offsets; the walk may read h/2 <= kU8PadRows rows below the image
     const size_t p = size_t(g.er) + m - 1, q = size_t(g.ec) + n - 1;
-    return g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
+    return u32_cross_exact(m, n) && g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
            (p + kU8PadRows) * q < (size_t(1) << 31) &&
            size_t(g.er) * g.ec < (size_t(1) << 32) &&
            (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads(g.h)).nt > 0);
@@ -1907,9 +1916,9 @@ size_t autocorr_colwalk_bytes(int q, GridDesc g) {
     return size_t(g.h) * g.w * g.tr * q * sizeof(unsigned);
 }
 
-bool autocorr_colwalk_supported(int m, int q, GridDesc g) {
+bool autocorr_colwalk_supported(int m, int n, int q, GridDesc g) {
     (void)q;
-    return acv_supported(m, g.h) && g.w <= 11;
+    return u32_cross_exact(m, n) && acv_supported(m, g.h) && g.w <= 11;
 }
 
 cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,

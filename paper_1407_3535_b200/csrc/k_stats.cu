@@ -102,16 +102,92 @@ __global__ void __launch_bounds__(256) k_sum_sq_u8(const uint8_t* __restrict__ i
     }
 }
 
-// q_total for non-integer images.  The reference sums sequentially (stats.cpp:79); a
-// parallel tree sum differs in the last bits, which only matters for windows whose
-// variance sits exactly on the prefix-noise floor (documented in DESIGN.md).
-__global__ void k_sum_sq_f64(const double* __restrict__ img, size_t n, double* out) {
-    double acc = 0.0;
+// q_total for non-integer images (stats.cpp:78-81).  The reference adds the squares
+// sequentially, and a parallel sum differs from that in the last bits, which matters only
+// for windows whose variance sits on the prefix-noise floor.  So the flat decision is
+// made against a guaranteed bracket [pn_lo, pn_hi] of the reference's prefix_noise, and
+// only if some window falls inside the bracket is the sequential sum replayed on the
+// device (one warp, reference order) and that window-statistics pass redone with the
+// exact value.  Layout of the image's noise block `nb` (doubles):
+//   [0] q_par  [1] prefix_noise (exact once resolved)  [2] pn_lo  [3] pn_hi
+//   [4] ambiguous-window count (u64)  [5] resolved flag (u64)
+constexpr int kSqBlocks = 592, kSqThreads = 256;
+
+__global__ void __launch_bounds__(kSqThreads)
+    k_sum_sq_f64(const double* __restrict__ img, size_t n, double* __restrict__ part) {
+    double acc = 0.0;  // fixed per-thread order: deterministic, unlike atomics
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
          i += size_t(gridDim.x) * blockDim.x)
-        acc += img[i] * img[i];
+        acc = __dadd_rn(acc, __dmul_rn(img[i], img[i]));
     acc = warp_sum(acc);
-    if ((threadIdx.x & 31) == 0) atomicAdd(out, acc);
+    __shared__ double ws[kSqThreads / 32];
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = acc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double b = 0.0;
+        for (int w = 0; w < kSqThreads / 32; ++w) b = __dadd_rn(b, ws[w]);
+        part[blockIdx.x] = b;
+    }
+}
+
+// All addends are >= 0, so any summation order of k terms is within gamma_k = k*u/(1-k*u)
+// of the exact sum S* of the (identically rounded) squares: the sequential sum within
+// gamma_n, this tree within gamma_depth.  The bracket of q_seq is then monotonically
+// mapped through prefix_noise = RN(RN((rows + cols) * eps) * q_total).
+__global__ void k_prefix_noise_f64(const double* __restrict__ part, int nb, size_t n, int rows,
+                                   int cols, double* __restrict__ nbk) {
+    double q = 0.0;
+    for (int b = 0; b < nb; ++b) q = __dadd_rn(q, part[b]);
+    const double per_thread = double((n + size_t(nb) * kSqThreads - 1) / (size_t(nb) * kSqThreads));
+    const double u = 1.0000001 * 1.1102230246251565e-16;  // 2^-53 with slack
+    const double depth = per_thread + 5.0 + 3.0 + double(nb);
+    const double d_par = depth * u / (1.0 - depth * u);
+    const double d_seq = double(n) * u / (1.0 - double(n) * u);
+    const double delta = __ddiv_ru(__dadd_ru(d_par, d_seq), __dsub_rd(1.0, d_par));
+    const double q_lo = __dmul_rd(q, __dsub_rd(1.0, delta));
+    const double q_hi = __dmul_ru(q, __dadd_ru(1.0, delta));
+    const double c = __dmul_rn(double(rows + cols), kEps);
+    nbk[0] = q;
+    nbk[1] = __dmul_rn(c, q);
+    nbk[2] = __dmul_rn(c, q_lo);
+    nbk[3] = __dmul_rn(c, q_hi);
+    reinterpret_cast<unsigned long long*>(nbk)[4] = 0ull;
+    reinterpret_cast<unsigned long long*>(nbk)[5] = 0ull;
+}
+
+// The reference's sequential q_total (stats.cpp:79: q_total += v*v over the row-major
+// image), replayed only when a window was undecided: one warp streams coalesced chunks
+// of squares into shared memory and lane 0 adds them in order.
+__global__ void __launch_bounds__(32)
+    k_resolve_prefix_noise(const double* __restrict__ img, size_t n, int rows, int cols,
+                           double* __restrict__ nbk) {
+    auto* cnt = reinterpret_cast<unsigned long long*>(nbk);
+    if (cnt[4] == 0ull || cnt[5] != 0ull) return;
+    constexpr int kC = 32 * 16;
+    __shared__ double sq[kC];
+    double q = 0.0;
+    for (size_t base = 0; base < n; base += kC) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+            const size_t i = base + size_t(j) * 32 + threadIdx.x;
+            const double v = i < n ? img[i] : 0.0;
+            sq[j * 32 + threadIdx.x] = __dmul_rn(v, v);
+        }
+        __syncwarp();
+        if (threadIdx.x == 0) {
+            const int lim = int(n - base < size_t(kC) ? n - base : size_t(kC));
+            for (int k = 0; k < lim; ++k) q = __dadd_rn(q, sq[k]);
+        }
+        __syncwarp();
+    }
+    if (threadIdx.x == 0) {
+        const double pn = __dmul_rn(__dmul_rn(double(rows + cols), kEps), q);
+        nbk[0] = q;
+        nbk[1] = pn;
+        nbk[2] = pn;
+        nbk[3] = pn;
+        cnt[5] = 1ull;
+    }
 }
 
 constexpr int kChunk = 32;
@@ -322,26 +398,42 @@ __global__ void k_window_diff(const double* __restrict__ prefix, int rows, int c
     }
 }
 
+// stats.cpp:84-92 on replica window sums (non-integer images).  The prefix-noise floor is
+// tested against the bracket [pn_lo, pn_hi] (k_prefix_noise_f64): outside it the decision
+// equals the reference's; inside it the window is counted as undecided.  `fix` = the
+// redo pass after k_resolve_prefix_noise: runs only if windows were undecided, with the
+// exact floor, and clears the count.
 __global__ void k_stats_from_sums(const double* __restrict__ S, const double* __restrict__ Q,
-                                  size_t E, int m, int n, const double* __restrict__ pn,
-                                  DevStats st) {
-    const double prefix_noise = *pn;
+                                  size_t E, int m, int n, double* __restrict__ nbk,
+                                  DevStats st, int fix) {
+    auto* cnt = reinterpret_cast<unsigned long long*>(nbk);
+    if (fix && cnt[4] == 0ull) return;
+    const double pn = nbk[1], pn_lo = nbk[2], pn_hi = nbk[3];
     const double inv_mn = 1.0 / (double(m) * double(n));
     const long long mn = (long long)m * n;
+    unsigned undecided = 0;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
          k += size_t(gridDim.x) * blockDim.x) {
         double mu, om;
         uint8_t fl;
-        window_epilogue(S[k], Q[k], inv_mn, mn, prefix_noise, mu, om, fl);
+        window_epilogue(S[k], Q[k], inv_mn, mn, pn, mu, om, fl);
+        if (!fix) {
+            const double var_sum = __dsub_rn(Q[k], __dmul_rn(__dmul_rn(S[k], S[k]), inv_mn));
+            undecided += !variance_is_flat(var_sum, Q[k], mn) && var_sum > pn_lo &&
+                         var_sum <= pn_hi;
+        }
         st.mu[k] = mu;
         st.omega[k] = om;
         st.flat[k] = fl;
     }
+    if (!fix) {
+        undecided = warp_sum(undecided);
+        if ((threadIdx.x & 31) == 0 && undecided) atomicAdd(cnt + 4, (unsigned long long)undecided);
+    }
 }
 
-// stats.cpp:80-81: prefix_noise = double(rows + cols) * eps * q_total
-__global__ void k_prefix_noise_f64(const double* q_total, int rows, int cols, double* out) {
-    *out = __dmul_rn(__dmul_rn(double(rows + cols), kEps), *q_total);
+__global__ void k_clear_undecided(double* nbk) {
+    reinterpret_cast<unsigned long long*>(nbk)[4] = 0ull;
 }
 
 int grid_for(size_t n, int threads) {
@@ -376,14 +468,15 @@ cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long
     launch_pdl(k_sum_sq_u8, dim3(blocks), dim3(256), 0, s, img, n, q_total, p, q, out);  // q_total: 2 u64, zeroed
     return cudaGetLastError();
 }
-cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,
+cudaError_t prefix_noise_f64(const double* img, int p, int q, double* part, double* nbk,
                              cudaStream_t s) {
     const size_t n = size_t(p) * q;
-    cudaMemsetAsync(q_total, 0, sizeof(*q_total), s);
-    k_sum_sq_f64<<<grid_for(n, 256), 256, 0, s>>>(img, n, q_total);
-    k_prefix_noise_f64<<<1, 1, 0, s>>>(q_total, p, q, out);
+    k_sum_sq_f64<<<kSqBlocks, kSqThreads, 0, s>>>(img, n, part);
+    k_prefix_noise_f64<<<1, 1, 0, s>>>(part, kSqBlocks, n, p, q, nbk);
     return cudaGetLastError();
 }
+
+size_t prefix_noise_f64_parts() { return kSqBlocks; }
 
 namespace {
 
@@ -776,8 +869,12 @@ cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m,
 }
 
 cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
-                            const double* prefix_noise, DevStats st, cudaStream_t s) {
-    k_stats_from_sums<<<grid_for(E, 256), 256, 0, s>>>(S, Q, E, m, n, prefix_noise, st);
+                            const double* img, int p, int q, double* nbk, DevStats st,
+                            cudaStream_t s) {
+    k_stats_from_sums<<<grid_for(E, 256), 256, 0, s>>>(S, Q, E, m, n, nbk, st, 0);
+    k_resolve_prefix_noise<<<1, 32, 0, s>>>(img, size_t(p) * q, p, q, nbk);
+    k_stats_from_sums<<<grid_for(E, 256), 256, 0, s>>>(S, Q, E, m, n, nbk, st, 1);
+    k_clear_undecided<<<1, 1, 0, s>>>(nbk);
     return cudaGetLastError();
 }
 

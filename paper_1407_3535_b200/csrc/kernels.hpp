@@ -137,8 +137,11 @@ cudaError_t u8_to_f64(const uint8_t* img, size_t n, double* out, cudaStream_t s)
 // sum is exact; the FP64 sum is a parallel tree sum (parity notes).
 cudaError_t prefix_noise_u8(const uint8_t* img, int p, int q, unsigned long long* q_total,
                             double* out, cudaStream_t s);
-cudaError_t prefix_noise_f64(const double* img, int p, int q, double* q_total, double* out,
+// Non-integer images: deterministic parallel q_total (`part`: prefix_noise_f64_parts()
+// doubles) and the bracketed noise block `nbk` (8 doubles, layout in k_stats.cu).
+cudaError_t prefix_noise_f64(const double* img, int p, int q, double* part, double* nbk,
                              cudaStream_t s);
+size_t prefix_noise_f64_parts();
 
 // ---- window statistics, exact integer path (stats.cpp:55-94) ---------------------------
 // hs/hq scratch: p * ec int32 each.
@@ -181,7 +184,8 @@ cudaError_t replica_window_diff(const double* prefix, int rows, int cols, int m,
                                 double* out, cudaStream_t s);
 // stats epilogue from FP64 window sums S, Q (E entries).
 cudaError_t stats_from_sums(const double* S, const double* Q, size_t E, int m, int n,
-                            const double* prefix_noise, DevStats st, cudaStream_t s);
+                            const double* img, int p, int q, double* nbk, DevStats st,
+                            cudaStream_t s);
 
 // ---- local auto-correlation + retained count (autocorr.cpp:40-96, egs.cpp:12-25) -------
 cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc g, DevStats st,
@@ -190,7 +194,7 @@ cudaError_t autocorr_u8(const uint8_t* img, int p, int q, int m, int n, GridDesc
 // Two-pass variant (row walk + column slide) for w in {1,3,...,11}; H scratch of
 // autocorr_rowsum_bytes(p, g) bytes.
 size_t autocorr_rowsum_bytes(int p, GridDesc g);
-bool autocorr_two_pass_supported(int n, GridDesc g);
+bool autocorr_two_pass_supported(int m, int n, GridDesc g);
 cudaError_t autocorr_u8_two_pass(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
                                  DevStats st, double retain_threshold, double* map,
                                  unsigned long long* n_r, int* H, cudaStream_t s);
@@ -214,7 +218,7 @@ cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* st
                        ResultBlock* out = nullptr, unsigned long long seq = 0);
 // Column-walk variant: V scratch of autocorr_colwalk_bytes(q, g) bytes.
 size_t autocorr_colwalk_bytes(int q, GridDesc g);
-bool autocorr_colwalk_supported(int m, int q, GridDesc g);
+bool autocorr_colwalk_supported(int m, int n, int q, GridDesc g);
 cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, GridDesc g,
                                 DevStats st, double retain_threshold, double* map,
                                 unsigned long long* n_r, unsigned* V, cudaStream_t s);

@@ -150,18 +150,48 @@ EGSResult egs_from_info(const tm_prep_info& info, std::vector<double> map) {
 
 }  // namespace
 
-// Opaque device-resident preparation carried by PreparedEgs/PreparedOptA.
+// 64-bit fingerprint of an image's pixel words (8 independent multiply-xor lanes, several
+// GB/s per core).  Not the reference's content_hash (that one keys the TMACMAP1 cache and
+// is byte-serial FNV-1a); this only detects that a caller changed an Image in place
+// between prepare_* and run_*.
+std::uint64_t pixel_fingerprint(const Image& I) {
+    constexpr std::uint64_t kMul = 0x9E3779B97F4A7C15ull;
+    std::uint64_t lane[8] = {1, 2, 3, 4, 5, 6, 7, 8};
+    const double* d = I.data().data();
+    const std::size_t n = I.data().size();
+    std::size_t i = 0;
+    for (; i + 8 <= n; i += 8)
+        for (int k = 0; k < 8; ++k) {
+            std::uint64_t w;
+            std::memcpy(&w, d + i + k, 8);
+            lane[k] = (lane[k] ^ w) * kMul;
+        }
+    for (; i < n; ++i) {
+        std::uint64_t w;
+        std::memcpy(&w, d + i, 8);
+        lane[0] = (lane[0] ^ w) * kMul;
+    }
+    std::uint64_t h = std::uint64_t(I.rows()) * kMul ^ std::uint64_t(I.cols());
+    for (int k = 0; k < 8; ++k) h = (h ^ (lane[k] >> 29) ^ lane[k]) * kMul;
+    return h;
+}
+
+// Opaque device-resident preparation carried by PreparedEgs/PreparedOptA.  It serves a
+// run_* call only for the same buffer with the same dimensions and unchanged pixels (the
+// reference always correlates against the current contents of I).
 struct DeviceState {
     tm_image* img = nullptr;
     tm_prep* prep = nullptr;
     const double* source = nullptr;  // Image buffer it was prepared from
     int rows = 0, cols = 0;
+    std::uint64_t fingerprint = 0;
     ~DeviceState() {
         tm_prep_destroy(prep);
         tm_image_destroy(img);
     }
     bool serves(const Image& I) const {
-        return I.data().data() == source && I.rows() == rows && I.cols() == cols;
+        return I.data().data() == source && I.rows() == rows && I.cols() == cols &&
+               pixel_fingerprint(I) == fingerprint;
     }
 };
 
@@ -198,16 +228,19 @@ void save_image(const Image& img, const std::string& path) {
     if (!out) throw std::runtime_error("write failed: " + path);
 }
 
+// image.cpp:215-228: FNV-1a over the int64 dimensions {rows, cols}, then over the raw
+// bytes of the FP64 pixels -- the reference's key, so TMACMAP1 files written by either
+// library load in the other.
 std::uint64_t content_hash(const Image& img) {
-    std::uint64_t h = 1469598103934665603ull;
-    auto mix = [&](unsigned char b) {
-        h ^= b;
-        h *= 1099511628211ull;
+    constexpr std::uint64_t kBasis = 1469598103934665603ull, kPrime = 1099511628211ull;
+    std::uint64_t h = kBasis;
+    auto bytes = [&h](const void* src, std::size_t len) {
+        const auto* c = static_cast<const unsigned char*>(src);
+        for (std::size_t k = 0; k < len; ++k) h = (h ^ c[k]) * kPrime;
     };
-    for (double v : img.data()) mix(static_cast<unsigned char>(std::clamp(std::round(v), 0.0, 255.0)));
-    const std::int64_t dims[2] = {img.rows(), img.cols()};
-    const auto* b = reinterpret_cast<const unsigned char*>(dims);
-    for (std::size_t i = 0; i < sizeof dims; ++i) mix(b[i]);
+    const std::int64_t shape[2] = {img.rows(), img.cols()};
+    bytes(shape, sizeof shape);
+    bytes(img.data().data(), img.data().size() * sizeof(double));
     return h;
 }
 
@@ -517,11 +550,58 @@ CostEstimate total_cost(int extent_rows, int extent_cols, int h, int w, long lon
     return e;
 }
 
+namespace {
+// efficient_group_size with the amortised map-building term (egs.cpp:59-88 with
+// include_autocorr_cost): the term depends on the candidate size, so the device batch
+// decision (which knows only central + n_r) does not apply; candidates run one at a time,
+// each map and retained count on the device, the decision on the host in the reference's
+// FP64 order.
+EGSResult efficient_group_size_amortized(const Image& I, int m, int n, const EgsParams& params) {
+    if (params.h0 < 1 || params.w0 < 1 || params.h0 % 2 == 0 || params.w0 % 2 == 0)
+        throw std::invalid_argument("efficient_group_size: initial group size must be odd");
+    if (params.rho_tb <= 0.0 || params.rho_tb >= 1.0)
+        throw std::invalid_argument("efficient_group_size: rho_tb must be in (0,1)");
+    const int er = I.rows() - m + 1, ec = I.cols() - n + 1;
+    if (er < 1 || ec < 1) throw std::invalid_argument("efficient_group_size: template does not fit");
+    const double extent = double(er) * double(ec);
+    const double mn = double(m) * double(n);
+    int cap = params.max_group > 0 ? params.max_group : std::numeric_limits<int>::max();
+    if (cap % 2 == 0) ++cap;
+    DevImage d(I);
+    EGSResult best;
+    double prev = std::numeric_limits<double>::infinity();
+    std::vector<double> map(std::size_t(er) * ec);
+    for (int h = params.h0, w = params.w0;;) {
+        check(tm_local_autocorrelation(ctx(), d.h, m, n, h, w, map.data()));
+        std::int64_t n_r = 0;
+        check(tm_autocorr_retained(ctx(), d.h, m, n, h, w, params.rho_tb, &n_r));
+        g_tables.fetch_add(std::uint64_t(h) * w - 1, std::memory_order_relaxed);
+        const double amortized =
+            (double(h) * w - 1.0) * extent / (mn * std::max(1, params.n_templates));
+        const CostEstimate cost = total_cost(er, ec, h, w, n_r, amortized);
+        if (std::isfinite(prev) && !(prev - cost.total > params.xi_fraction * prev)) break;
+        best.h = h;
+        best.w = w;
+        best.grid = GroupGrid(er, ec, h, w);
+        best.map.rows = er;
+        best.map.cols = ec;
+        best.map.group_h = h;
+        best.map.group_w = w;
+        best.map.values = map;
+        best.cost = cost;
+        best.trace.push_back(EgsIteration{h, w, cost});
+        prev = cost.total;
+        if ((h >= er && w >= ec) || (h >= cap && w >= cap)) break;
+        h = std::min(h + 2, cap);
+        w = std::min(w + 2, cap);
+    }
+    return best;
+}
+}  // namespace
+
 EGSResult efficient_group_size(const Image& I, int m, int n, const EgsParams& params,
                                const WindowStats&) {
-    if (params.include_autocorr_cost)
-        throw std::invalid_argument(
-            "efficient_group_size: include_autocorr_cost is not supported by the device path");
+    if (params.include_autocorr_cost) return efficient_group_size_amortized(I, m, n, params);
     DevImage d(I);
     int h = 0, w = 0, tl = 0;
     tm_egs_iter trace[TM_MAX_TRACE];
@@ -715,6 +795,7 @@ std::shared_ptr<DeviceState> device_prepare(const Image& I, int m, int n, const 
     st->source = I.data().data();
     st->rows = I.rows();
     st->cols = I.cols();
+    st->fingerprint = pixel_fingerprint(I);
     return st;
 }
 

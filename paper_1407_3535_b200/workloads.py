@@ -4,10 +4,14 @@ The reference ships no generator for these configs (its synth.cpp:19-40 makes sm
 white noise) and the paper's SI/AI datasets are not available, so these seeded inputs
 stand in for them.  The generator is:
 
-1. Gaussian white field (numpy PCG64, explicit seed).
+1. Gaussian white field (numpy PCG64, explicit seed), FP64.
 2. FFT; multiply by |f|^(-beta/2) with DC = 0; optional Gaussian blur applied as the
    transfer function exp(-2 pi^2 sigma^2 |f|^2) in the same spectrum (periodic border).
 3. Inverse FFT, real part; min-max rescale to [0, 255], round, clamp -> uint8.
+
+The bytes are host-independent: FP64 pocketfft (compile-time vectorised, thread-count
+invariant) and elementwise math restricted to correctly rounded operations (det_exp /
+det_log below).  Each config's SHA-256 is pinned in tests/golden/configs.json.
 
 Templates are cut at seeded locations and perturbed photometrically:
 round(clip(gain * t + offset + N(0, sigma^2), 0, 255)).  Everything is integer-valued
@@ -22,7 +26,7 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-try:  # multithreaded pocketfft; falls back to numpy
+try:  # multithreaded pocketfft (each 1-D transform is independent: thread-count invariant)
     import scipy.fft as _fft
 
     def _rfft2(x):
@@ -36,6 +40,44 @@ except Exception:  # pragma: no cover
 
     def _irfft2(x, s):
         return np.fft.irfft2(x, s=s)
+
+
+# ---- bit-deterministic elementwise transcendental functions ---------------------------
+# numpy dispatches exp/log/power to CPU-specific SIMD kernels (AVX512_SKX SVML vs AVX2 vs
+# scalar libm) whose last-ulp results differ, and a single ulp can move a pixel across a
+# rounding boundary of the u8 quantisation: measured here, C1-C3 hashed differently with
+# NPY_DISABLE_CPU_FEATURES=AVX512*.  These use only +, -, *, /, frexp, ldexp and rint,
+# which IEEE 754 rounds exactly on every CPU, so the inputs are the same bytes on any host.
+_LN2 = 0.6931471805599453
+
+
+def det_log(x: np.ndarray) -> np.ndarray:
+    """Natural log of x > 0 (float64): frexp range reduction + atanh series."""
+    m, e = np.frexp(np.asarray(x, dtype=np.float64))
+    low = m < 0.7071067811865476
+    m = np.where(low, m * 2.0, m)
+    e = e - low.astype(e.dtype)
+    s = (m - 1.0) / (m + 1.0)          # |s| <= 0.1716
+    s2 = s * s
+    acc = np.full_like(s, 1.0 / 25.0)
+    for k in range(23, 0, -2):          # 2 * (s + s^3/3 + ... + s^25/25)
+        acc = acc * s2 + 1.0 / k
+    return 2.0 * s * acc + e.astype(np.float64) * _LN2
+
+
+def det_exp(y: np.ndarray) -> np.ndarray:
+    """exp(y) (float64): k = rint(y / ln2), Taylor series of the remainder, ldexp."""
+    y = np.asarray(y, dtype=np.float64)
+    k = np.rint(y / _LN2)
+    r = y - k * _LN2                    # |r| <= 0.35
+    acc = np.full_like(r, 1.0)
+    for j in range(18, 0, -1):          # Horner form of sum r^j / j!
+        acc = acc * (r / j) + 1.0
+    return np.ldexp(acc, k.astype(np.int32))
+
+
+def det_pow(x: np.ndarray, a: float) -> np.ndarray:
+    return det_exp(a * det_log(x))
 
 
 @dataclass
@@ -71,23 +113,25 @@ class Workload:
 
 
 def _spectral_field(rng, rows, cols, beta, blur_sigmas=(0.0,)):
-    """Return one float field per blur sigma, all sharing the same white noise."""
-    white = rng.standard_normal((rows, cols)).astype(np.float32)
+    """Return one float field per blur sigma, all sharing the same white noise.
+
+    FP64 throughout; the spectral weights use det_pow/det_exp (bit-deterministic)."""
+    white = rng.standard_normal((rows, cols))
     spec = _rfft2(white)
-    fy = np.fft.fftfreq(rows).astype(np.float32)[:, None]
-    fx = np.fft.rfftfreq(cols).astype(np.float32)[None, :]
+    fy = np.fft.fftfreq(rows)[:, None]          # k / rows: exact divisions
+    fx = np.fft.rfftfreq(cols)[None, :]
     f2 = fy * fy + fx * fx
     f2[0, 0] = 1.0
-    amp = f2 ** np.float32(-beta / 4.0)  # |f|^(-beta/2)
+    amp = det_pow(f2, -beta / 4.0)              # |f|^(-beta/2)
     amp[0, 0] = 0.0
     spec *= amp
     out = []
     for s in blur_sigmas:
         if s > 0:
-            g = np.exp(np.float32(-2.0 * np.pi ** 2 * s * s) * f2).astype(np.float32)
-            out.append(_irfft2(spec * g, (rows, cols)).astype(np.float32))
+            g = det_exp((-2.0 * np.pi ** 2 * s * s) * f2)
+            out.append(_irfft2(spec * g, (rows, cols)))
         else:
-            out.append(_irfft2(spec, (rows, cols)).astype(np.float32))
+            out.append(_irfft2(spec, (rows, cols)))
     return out
 
 
