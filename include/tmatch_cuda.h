@@ -268,6 +268,8 @@ int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out);
 
 /* Instrumentation: number of kernels this context launched (bench gpu_launches). */
 int64_t tm_ctx_launch_count(const tm_ctx* ctx);
+/* tm_search h_e predictions (the fused scan-2 path ran on the accepted size / did not). */
+int tm_ctx_search_stats(const tm_ctx* ctx, int64_t* fused_hits, int64_t* fused_misses);
 /* The context's CUDA stream (cudaStream_t) for callers that time or order work on it. */
 void* tm_ctx_stream(tm_ctx* ctx);
 /* Per-phase device timing with CUDA events on the context stream (off by default). */

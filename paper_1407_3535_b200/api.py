@@ -192,6 +192,12 @@ class Context:
     def stream_ptr(self) -> int:
         return int(N.lib().tm_ctx_stream(self.h) or 0)
 
+    def search_stats(self) -> dict:
+        """tm_search h_e prediction outcomes: fused scan-2 path hit / missed."""
+        h, m = C.c_int64(), C.c_int64()
+        N.check(N.lib().tm_ctx_search_stats(self.h, C.byref(h), C.byref(m)))
+        return {"fused_hits": h.value, "fused_misses": m.value}
+
     def set_profiling(self, enable=True):
         N.check(N.lib().tm_ctx_set_profiling(self.h, int(bool(enable))))
 

@@ -171,6 +171,19 @@ bool better_h(const tmk::CellH& a, const tmk::CellH& b) {
     return a.col < b.col;
 }
 
+// The cell of the first retained flat member (Tally::flat_key), invalid if none: rho 0,
+// degenerate (zncc_at detail.hpp:47; matcher.cpp:69 marks member_flat as degenerate).
+tmk::CellH flat_cell(const tmk::Tally& t) {
+    tmk::CellH c{};
+    if (t.flat_n) {
+        c.rho = 0.0;
+        c.row = tmk::flat_key_row(t.flat_key);
+        c.col = tmk::flat_key_col(t.flat_key);
+        c.flags = 3;
+    }
+    return c;
+}
+
 // Wait for an event by polling (no blocking-sync wake-up latency at the end of a search;
 // TMATCH_SPIN=0 uses cudaEventSynchronize).
 void spin_wait(cudaEvent_t ev) {
@@ -234,6 +247,7 @@ struct tm_ctx {
     std::atomic<int> refs{0};
     std::atomic<bool> closing{false};
     int64_t launches = 0;
+    int64_t fused_hits = 0, fused_misses = 0;  // tm_search h_e prediction outcomes
     cudaEvent_t ev0 = nullptr, ev1 = nullptr;
     // scratch (grow-only)
     DBuf<int> hs, hq, markP, acH;
@@ -1885,10 +1899,13 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     tmk::CellH best = cells[0];
     if (policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
     if (better_h(cells[2], best)) best = cells[2];
+    if (better_h(flat_cell(tally), best)) best = flat_cell(tally);
 
     const long long eliminated = (long long)tally.eliminated;
-    // sequential: alive candidates (dead ones were moved to `eliminated` by seq_final)
-    const long long retained = seq ? (long long)tally.pad : (long long)tally.retained;
+    // sequential: alive candidates (dead ones were moved to `eliminated` by seq_final) and
+    // the retained flat members, which are never listed
+    const long long retained =
+        seq ? (long long)(tally.pad + tally.flat_n) : (long long)tally.retained;
     if (device_dispatch) final_T = thr_after;  // = T0 (see above)
     if (policy == TM_POLICY_SEEDED) {
         final_T = thr_after;
@@ -2225,6 +2242,13 @@ int tm_ctx_synchronize(tm_ctx* ctx) {
 }
 
 int64_t tm_ctx_launch_count(const tm_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int tm_ctx_search_stats(const tm_ctx* ctx, int64_t* fused_hits, int64_t* fused_misses) {
+    if (!ctx || !fused_hits || !fused_misses) return TM_EINVAL;
+    *fused_hits = ctx->fused_hits;
+    *fused_misses = ctx->fused_misses;
+    return TM_OK;
+}
 
 void* tm_ctx_stream(tm_ctx* ctx) { return ctx ? reinterpret_cast<void*>(ctx->s) : nullptr; }
 
@@ -2743,6 +2767,7 @@ void search_fused_end(tm_ctx* ctx, tm_image* img, const tm_match_params& P, cons
                                     /*egs_preinit=*/true);  // (search_fused_begin's centre reduction)
     ctx->spec_want = 0;
     HT("fused_egs");
+    ++(hit ? ctx->fused_hits : ctx->fused_misses);
     if (hit && ctx->hres->spec != 1)
         throw TmError{TM_ECUDA, "search_fused: device gate disagrees with the EGS decision"};
     if (hit) {
@@ -3212,6 +3237,7 @@ int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out) {
         tmk::CellH best = cells[0];
         if (S.policy == TM_POLICY_SEEDED && better_h(cells[1], best)) best = cells[1];
         if (better_h(cells[2], best)) best = cells[2];
+        if (better_h(flat_cell(tally), best)) best = flat_cell(tally);
         double fin = T;
         if ((cells[2].flags & 1) && !(cells[2].flags & 2) && cells[2].rho > fin) fin = cells[2].rho;
         std::memset(out, 0, sizeof *out);

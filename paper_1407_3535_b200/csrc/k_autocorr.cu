@@ -1274,7 +1274,8 @@ __global__ void __launch_bounds__(NT)
         sec_tbf = float(sec_tb);
         thr_ok = T >= -1.0;
     }
-    unsigned n_elim = 0, n_keep = 0;
+    unsigned n_elim = 0, n_keep = 0, n_flat = 0;
+    unsigned long long fkey = 0;  // retained flat members: first position (Tally::flat_key)
     bool list_full = false;
     unsigned long long surv_local = 0;
 #pragma unroll 1
@@ -1409,6 +1410,10 @@ __global__ void __launch_bounds__(NT)
                         if (elim) {
                             ++n_elim;
                             vis = 1;
+                        } else if (pf_fm[d] || sf.tflat) {  // rho 0 without a dot
+                            ++n_keep;
+                            ++n_flat;
+                            fkey = max(fkey, flat_member_key(cr + d - hr, c));
                         } else {
                             ++n_keep;
                             surv |= 1u << d;
@@ -1462,10 +1467,16 @@ __global__ void __launch_bounds__(NT)
     if constexpr (FUSE) {
         const unsigned long long ne = warp_sum((unsigned long long)n_elim);
         const unsigned long long nk = warp_sum((unsigned long long)n_keep);
+        const unsigned long long nf = warp_sum((unsigned long long)n_flat);
+        fkey = warp_max_u64(fkey);
         if (lane == 0) {  // (surv_local is warp-uniform)
             if (ne) atomicAdd(&sf.tally->eliminated, ne);
             if (nk) atomicAdd(&sf.tally->retained, nk);
             if (surv_local) atomicAdd(&sf.tally->survivors, surv_local);
+            if (nf) {
+                atomicAdd(&sf.tally->flat_n, nf);
+                atomicMax(&sf.tally->flat_key, fkey);
+            }
         }
     }
     egs_tail(dec);

@@ -385,7 +385,7 @@ __device__ void apply_reduce_op(const Cell& best, CellH* out, const ReduceOp& op
         if (op.has_init) t = dmax(t, dclamp(op.init, -1.0, 1.0));
         *op.thr = t;
         for (int i = 0; i < op.nzero64; ++i) op.zero64[i] = 0ull;
-        if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull};
+        if (op.zero_tally) *op.zero_tally = Tally{0ull, 0ull, 0ull, 0ull, 0ull, 0ull};
         if (op.egs_stop) {  // k_egs_init
             *op.egs_stop = 0;
             *op.egs_prev = INFINITY;
@@ -575,7 +575,7 @@ __global__ void __launch_bounds__(256)
     const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
     const bool thr_ok = T >= -1.0;
     const int lane = threadIdx.x & 31;
-    unsigned long long n_elim = 0, n_keep = 0;
+    unsigned long long n_elim = 0, n_keep = 0, n_flat = 0, fkey = 0;
     bool list_full = false;            // this warp saw the survivor list reach max_locs
     unsigned long long surv_local = 0;  // survivors counted after that (one atomic at the end)
     const int r_lo = g.row_lo(), r_hi = g.row_hi();
@@ -632,6 +632,11 @@ __global__ void __launch_bounds__(256)
                         if (elim) {
                             ++n_elim;
                             if (visits) visits[k] = 1;
+                        } else if (tflat || fv) {  // retained, rho 0 without a dot
+                            ++n_keep;
+                            ++n_flat;
+                            fkey = max(fkey, flat_member_key(r, c));
+                            if (visits) visits[k] = 2;
                         } else {
                             ++n_keep;
                             survivor = true;
@@ -661,10 +666,16 @@ __global__ void __launch_bounds__(256)
     }
     n_elim = warp_sum(n_elim);
     n_keep = warp_sum(n_keep);
+    n_flat = warp_sum(n_flat);
+    fkey = warp_max_u64(fkey);
     if (lane == 0) {
         if (n_elim) atomicAdd(&tally->eliminated, n_elim);
         if (n_keep) atomicAdd(&tally->retained, n_keep);
         if (surv_local) atomicAdd(&tally->survivors, surv_local);
+        if (n_flat) {
+            atomicAdd(&tally->flat_n, n_flat);
+            atomicMax(&tally->flat_key, fkey);
+        }
     }
 }
 

@@ -40,8 +40,27 @@ struct Tally {  // accumulated on device by the search kernels
     unsigned long long eliminated;
     unsigned long long retained;
     unsigned long long survivors;  // entries appended to the survivor list
-    unsigned long long pad;
+    unsigned long long pad;        // sequential replay: candidates alive at their key
+    // Retained FLAT members (matcher.cpp:57-76: never eliminated; zncc_at is 0 without a
+    // dot, detail.hpp:47) are not listed for evaluation: their cell is (rho 0, degenerate),
+    // so only the first one in (row, col) order can matter.  flat_key = max of
+    // flat_member_key over them (0: none), flat_n = how many.
+    unsigned long long flat_key;
+    unsigned long long flat_n;
 };
+
+// Order-reversing key of a position: max over keys = min (row, col) (better_candidate's
+// tie order among equal-rho degenerate cells, stats.cpp:147-154).
+inline __host__ __device__ unsigned long long flat_member_key(int r, int c) {
+    return ((unsigned long long)(0x7FFFFFFFu - unsigned(r)) << 32) |
+           (unsigned long long)(0xFFFFFFFFu - unsigned(c));
+}
+inline __host__ __device__ int flat_key_row(unsigned long long k) {
+    return int(0x7FFFFFFFu - unsigned(k >> 32));
+}
+inline __host__ __device__ int flat_key_col(unsigned long long k) {
+    return int(0xFFFFFFFFu - unsigned(k & 0xFFFFFFFFull));
+}
 
 // Host-readable result block (one device->host copy per search / EGS batch).
 struct ResultBlock {

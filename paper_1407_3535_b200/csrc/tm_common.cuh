@@ -166,6 +166,15 @@ __device__ __forceinline__ T warp_sum(T v) {
     return v;
 }
 
+__device__ __forceinline__ unsigned long long warp_max_u64(unsigned long long v) {
+#pragma unroll
+    for (int s = 16; s > 0; s >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, s);
+        v = o > v ? o : v;
+    }
+    return v;
+}
+
 // Exact unsigned division by a runtime constant without the XU pipe: floor(x / d) =
 // umulhi64(x, ceil(2^64 / d)) for every 32-bit x (the error term x*eps/2^64 < 1/d).
 struct FastDiv {
