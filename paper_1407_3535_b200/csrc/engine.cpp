@@ -1636,7 +1636,7 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     const size_t E = size_t(g.er) * g.ec;
     const unsigned long long* count = &ctx->tally.p->survivors;
     uint8_t* visits = ctx->visits.p;
-    const bool dense = survivors * 16 > E && fp32_path(img, T);
+    const bool dense = survivors * tmk::kDenseDiv > E && fp32_path(img, T);
     if (dense && tc_path(ctx, img, T)) {
         const int rlo = g.ti_lo * g.h, rhi = std::min(g.ti_hi * g.h, g.er);
         RowSet rs;
@@ -1739,6 +1739,7 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     op_pack.packed = ctx->hres_dev;
     // fused into the list kernel's tail: the tensor-core partials [0, np) are already in
     const tmk::TailReduce tail = tail_to(ctx, np + kListBlocks, 2, &op_pack);
+    Phase ph(ctx, "survivor_list");
     CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
                       nullptr, ctx->partials.p + np, kListBlocks, s, 1, &tail));
     ctx->add(2);

@@ -873,7 +873,7 @@ __device__ void egs_decide_run(const EgsDecide& d) {
     *d.gate = gv;
     if (d.out && d.disp_dense) {  // k_survivor_dispatch for the gated survivors behind
         const unsigned long long ns = gv ? d.disp_tally->survivors : 0ull;
-        const bool dense = ns * 16 > d.disp_E;
+        const bool dense = ns * kDenseDiv > d.disp_E;
         *d.disp_dense = dense ? 1 : 0;
         *d.disp_list = dense ? 0ull : ns;
     }

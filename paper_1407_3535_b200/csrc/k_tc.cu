@@ -521,7 +521,7 @@ __global__ void k_survivor_dispatch(const Tally* tally, unsigned long long E, in
         return;
     }
     const unsigned long long n = tally->survivors;
-    const bool dense = n * 16 > E;
+    const bool dense = n * kDenseDiv > E;
     *dense_flag = dense ? 1 : 0;
     *list_count = dense ? 0ull : n;
 }

@@ -12,6 +12,11 @@ namespace tmk {
 
 constexpr int kU8PadRows = 16;  // zero rows stored below every 8-bit image
 
+// Survivor evaluation: the masked dense tensor-core pass over the strip costs about as much
+// as listing E / 1500 survivors on CUDA cores (C5, 96x96: dense 3.8 ms for the whole extent
+// vs 22.5 ns per listed survivor), so lists longer than E / kDenseDiv go dense.
+constexpr unsigned long long kDenseDiv = 1024;
+
 struct DevStats {  // WindowStats (stats.hpp:35-47) resident in HBM
     double* mu = nullptr;
     double* omega = nullptr;
