@@ -174,11 +174,23 @@ class ClockSampler:
 
 
 
+# Functional check of the multi-rank path on a one-GPU box (never for numbers): every rank
+# on cuda:0, collectives over gloo.  The strip kernels never wait on each other.
+DIST_BACKEND = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+
+
 def dist_env():
     ws = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if DIST_BACKEND != "nccl":
+        local = 0
     return ws, rank, local
+
+
+def coll_device(local):
+    import torch
+    return torch.device(f"cuda:{local}") if DIST_BACKEND == "nccl" else torch.device("cpu")
 
 
 def golden(name):
@@ -396,12 +408,15 @@ def run_b200(args):
     ws, rank, local = dist_env()
     if ws > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        if DIST_BACKEND == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        else:
+            dist.init_process_group(DIST_BACKEND)
     torch.cuda.set_device(local)
     from paper_1407_3535_b200 import api, workloads as W
 
     t_gen = time.perf_counter()
-    wl = W.make(args.config)
+    wl = broadcast_workload(args.config, rank, local) if ws > 1 else W.make(args.config)
     gen_s = time.perf_counter() - t_gen
     g = golden(args.config)
     if g and wl.sha256() != g["sha256"]:
@@ -604,22 +619,77 @@ def run_b200(args):
     return 0
 
 
+def broadcast_workload(name, rank, local):
+    """Rank 0 generates the workload, every rank receives it over NCCL (generating C5 on
+    every rank at once would take minutes of host time)."""
+    import torch
+    import torch.distributed as dist
+    from paper_1407_3535_b200 import workloads as W
+    wl = W.make(name) if rank == 0 else None
+    meta = [None]
+    if rank == 0:
+        meta = [dict(name=wl.name, mode=wl.mode, description=wl.description,
+                     shape=wl.image.shape,
+                     templates=[(t.row, t.col, t.gain, t.offset, t.noise_sigma,
+                                 t.pixels.shape) for t in wl.templates])]
+    dist.broadcast_object_list(meta, src=0)
+    meta = meta[0]
+    dev = coll_device(local)
+    img = torch.empty(meta["shape"], dtype=torch.uint8, device=dev)
+    k = len(meta["templates"])
+    m, n = meta["templates"][0][5]
+    tm = torch.empty((k, m, n), dtype=torch.uint8, device=dev)
+    if rank == 0:
+        img.copy_(torch.from_numpy(wl.image))
+        tm.copy_(torch.from_numpy(np.stack([t.pixels for t in wl.templates])))
+    dist.broadcast(img, src=0)
+    dist.broadcast(tm, src=0)
+    if rank != 0:
+        ts = [W.Template(tm[i].cpu().numpy(), *meta["templates"][i][:5]) for i in range(k)]
+        wl = W.Workload(meta["name"], img.cpu().numpy(), ts, meta["mode"], (1,),
+                        meta["description"])
+    return wl
+
+
 def run_strips(args, wl, ws, rank, local):
-    """N > 1: the search sharded as row strips (distributed.py) over NCCL."""
+    """N > 1: the search sharded as row strips of the group grid (distributed.py) over NCCL:
+    each rank holds and computes only its strip (+ halo) of the image, statistics and R_co;
+    the noise floor, EGS counts, thresholds and best cells are exchanged by collectives."""
     import torch
     import torch.distributed as dist
     from paper_1407_3535_b200 import api, distributed as D
     ctx = api.Context(local)
-    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=torch.device(f"cuda:{local}"))
-    comm = D.TorchComm(device=torch.device(f"cuda:{local}"))
+    dev = torch.device(f"cuda:{local}")
+    stream = torch.cuda.ExternalStream(ctx.stream_ptr, device=dev)
+    comm = D.Comm(device=coll_device(local))
     m, n = wl.templates[0].pixels.shape
-    backend = D.DeviceBackend(ctx, wl.image)
-    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    strip = wl.mode == "egs"
+    backend = D.DeviceBackend.strip(ctx, wl.image, m, n, rank, ws) if strip else \
+        D.DeviceBackend(ctx, wl.image)
+    flush = torch.empty(512 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
 
     def step():
         backend.reset()
         return [D.match_strips(backend, comm, t.pixels, wl.image.shape, mode=wl.mode,
                                policy=args.policy) for t in wl.templates]
+
+    def timed(steps, fn):
+        times, res = [], None
+        for _ in range(steps):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            torch.cuda.synchronize()
+            dist.barrier()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            res = fn()
+            e1.record(stream)
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        t = torch.tensor([statistics.mean(times)], device=coll_device(local))
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)  # device time, max over ranks
+        return float(t.item()), res
 
     for _ in range(args.warmup):
         step()
@@ -628,26 +698,27 @@ def run_strips(args, wl, ws, rank, local):
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = ctx.launches
-    times, res = [], None
-    for _ in range(args.steps):
-        with torch.cuda.stream(stream):
-            flush.zero_()
-        torch.cuda.synchronize()
-        dist.barrier()
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        res = step()
-        e1.record(stream)
-        e1.synchronize()
-        times.append(e0.elapsed_time(e1))
-    torch.cuda.synchronize()
-    clk = clocks.stop()
+    ms, res = timed(args.steps, step)
     launches = (ctx.launches - launches0) / args.steps
-    t = torch.tensor([statistics.mean(times)], device=f"cuda:{local}")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    parity = check_against_golden(args.config, [D.as_result(r) for r in res], args.policy)
+    clk = clocks.stop()
+    parity = check_against_golden(args.config, res, args.policy)
+
+    # e2e: every step uploads the rank's rows of a distinct pinned host image (H2D inside
+    # the timed region), recomputes the noise floor (allreduce) and searches
+    host = []
+    for a in variants(wl, 3):
+        hb = torch.empty(a.shape, dtype=torch.uint8, pin_memory=True)
+        hb.numpy()[:] = a
+        host.append(hb.numpy())
+    ctr = [0]
+
+    def e2e_step():
+        backend.upload(host[ctr[0] % len(host)])
+        ctr[0] += 1
+        return step()
+    e2e_step()
+    e2e_ms, _ = timed(args.steps, e2e_step)
+    rows = backend.rows if strip else (0, wl.image.shape[0])
     dist.barrier()
     if rank == 0:
         units = wl.extent * len(wl.templates)
@@ -658,10 +729,23 @@ def run_strips(args, wl, ws, rank, local):
                 "data": "synthetic (seeded bit-deterministic 1/f^beta generator, SURVEY 8d)",
                 "config": {"workload": f"{wl.name}: {wl.description}", "extent": wl.extent,
                            "templates": len(wl.templates), "mode": wl.mode,
-                           "policy": args.policy, "parallelism": f"row strips x{ws} (NCCL)"},
-                "result": [D.as_dict(r) for r in res[:4]],
+                           "policy": args.policy,
+                           "parallelism": f"row strips x{ws} (NCCL collectives: noise-floor "
+                                          "sum, EGS counts, thresholds, best cells)",
+                           "rank0_image_rows": list(rows),
+                           "l2": "flushed between steps (512 MB write, untimed)"},
+                "result": [r.as_dict() for r in res[:4]],
+                "elimination_pct": statistics.mean(r.elim_pct for r in res),
                 "parity": {"full_size_vs_reference": parity},
-                "gpu_launches": launches, "clocks": clk}
+                "gpu_launches": launches,
+                "e2e": {"value": units / (e2e_ms / 1e3), "unit": UNIT,
+                        "h2d_bytes_per_step": int((rows[1] - rows[0]) * wl.image.shape[1]),
+                        "d2h_bytes_per_step": 64 * len(wl.templates),
+                        "ms_per_step": e2e_ms,
+                        "path": "per rank: tm_image_upload_strip_u8 of its rows of a distinct "
+                                "pinned host image + the strip search; device time, max over "
+                                "ranks (h2d bytes: rank 0's rows)"},
+                "clocks": clk}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
     return 0

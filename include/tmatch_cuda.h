@@ -261,6 +261,17 @@ int tm_strip_autocorr(tm_ctx* ctx, tm_image* img, int m, int n, int h, int w, in
 int tm_strip_commit(tm_ctx* ctx, tm_image* img, int m, int n, int slot, int h, int w,
                     const tm_match_params* params, const tm_egs_iter* trace, int trace_len,
                     tm_prep** out);
+/* Row-strip images (one rank of a strip-sharded search): a rows x cols 8-bit image of
+ * which only rows [row0, row0 + nrows) -- the rank's strip plus its template_height-1 halo
+ * -- are uploaded (pixels: nrows x cols); window statistics are computed for the extent
+ * rows whose windows lie in them.  The image-global flat-noise floor (stats.cpp:78-81) is
+ * set from the allreduced sum of squares: each rank sums a disjoint row range
+ * (tm_image_sum_sq_rows), the caller allreduces, tm_image_set_noise_floor applies it. */
+int tm_image_create_strip_u8(tm_ctx* ctx, int rows, int cols, int row0, int nrows,
+                             const uint8_t* pixels, tm_image** out);
+int tm_image_upload_strip_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels);
+int tm_image_sum_sq_rows(tm_ctx* ctx, tm_image* img, int row0, int nrows, uint64_t* q_sum);
+int tm_image_set_noise_floor(tm_ctx* ctx, tm_image* img, uint64_t q_total);
 int tm_strip_search_begin(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpl,
                           const tm_match_params* params, int rank, int world, double* T0);
 int tm_strip_search_seed(tm_ctx* ctx, double T, double* T1);

@@ -122,6 +122,17 @@ class Oracle:
                                               _ptr(fl, C.c_uint8)))
         return mu, om, fl
 
+    def window_stats_floor(self, img, m, n, floor):
+        """Port only: window_stats with the flat-noise floor of a larger image."""
+        img = _d(img)
+        p, q = img.shape
+        er, ec = p - m + 1, q - n + 1
+        mu, om = np.empty((er, ec)), np.empty((er, ec))
+        fl = np.empty((er, ec), dtype=np.uint8)
+        self._check(self.lib.tmo_window_stats_floor(_ptr(img), p, q, m, n, C.c_double(floor),
+                                                    _ptr(mu), _ptr(om), _ptr(fl, C.c_uint8)))
+        return mu, om, fl
+
     def template_stats(self, t):
         t = _d(t)
         mu, om, fl = C.c_double(), C.c_double(), C.c_int()

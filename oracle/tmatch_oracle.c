@@ -94,6 +94,13 @@ static int variance_is_flat(double var_sum, double q_sum, long long mn) {
 /* ---- stats.cpp:55-94 ------------------------------------------------------------- */
 int tmo_window_stats(const double* img, int p, int q, int m, int n, double* mu, double* omega,
                      uint8_t* flat) {
+    return tmo_window_stats_floor(img, p, q, m, n, NAN, mu, omega, flat);
+}
+
+/* window_stats with the flat-noise floor given (NaN: the image's own, stats.cpp:78-81) --
+ * a row strip of a larger image takes the floor of the whole image (row-strip tests). */
+int tmo_window_stats_floor(const double* img, int p, int q, int m, int n, double floor_in,
+                           double* mu, double* omega, uint8_t* flat) {
     const int er = p - m + 1, ec = q - n + 1;
     if (m < 1 || n < 1 || er < 1 || ec < 1) return fail("running_sum: window does not fit the source");
     const size_t E = (size_t)er * ec, P = (size_t)p * q;
@@ -108,7 +115,7 @@ int tmo_window_stats(const double* img, int p, int q, int m, int n, double* mu, 
     const long long mn = (long long)m * n;
     double q_total = 0.0;
     for (size_t i = 0; i < P; ++i) q_total += squared[i];
-    const double prefix_noise = (double)(p + q) * kEps * q_total;
+    const double prefix_noise = isnan(floor_in) ? (double)(p + q) * kEps * q_total : floor_in;
     for (size_t i = 0; i < E; ++i) {
         const double sum = s[i];
         const double sqs = sq[i];

@@ -72,6 +72,10 @@ int tmo_running_sum(const double* src, int p, int q, int m, int n, double* out);
 /* stats.cpp:55-94 */
 int tmo_window_stats(const double* img, int p, int q, int m, int n, double* mu, double* omega,
                      uint8_t* flat);
+/* Port only: window_stats with an externally given flat-noise floor (NaN = the image's own
+ * stats.cpp:78-81 value), for row strips of a larger image. */
+int tmo_window_stats_floor(const double* img, int p, int q, int m, int n, double floor_in,
+                           double* mu, double* omega, uint8_t* flat);
 /* stats.cpp:98-111 */
 void tmo_template_stats(const double* t, int m, int n, double* mu, double* omega, int* flat);
 /* detail.hpp:45-51 (window_dot detail.hpp:32-41) */

@@ -91,6 +91,36 @@ class Image:
                                             C.byref(h)))
         self.h = h
 
+    @classmethod
+    def strip(cls, ctx: "Context", pixels, shape, row0: int):
+        """A rows x cols 8-bit image holding only rows [row0, row0 + len(pixels)) -- one
+        rank's strip + halo of a row-strip search (tm_image_create_strip_u8)."""
+        a = np.ascontiguousarray(pixels, dtype=np.uint8)
+        self = cls.__new__(cls)
+        self.ctx = ctx
+        self.rows, self.cols = int(shape[0]), int(shape[1])
+        if a.ndim != 2 or a.shape[1] != self.cols:
+            raise InvalidArgument("strip pixels must be nrows x cols")
+        h = C.c_void_p()
+        N.check(N.lib().tm_image_create_strip_u8(ctx.h, self.rows, self.cols, int(row0),
+                                                 a.shape[0], _u8ptr(a), C.byref(h)))
+        self.h = h
+        self.row0, self.nrows = int(row0), a.shape[0]
+        return self
+
+    def upload_strip(self, pixels):
+        a = np.ascontiguousarray(pixels, dtype=np.uint8)
+        N.check(N.lib().tm_image_upload_strip_u8(self.ctx.h, self.h, _u8ptr(a)))
+
+    def sum_sq_rows(self, row0: int, nrows: int) -> int:
+        v = C.c_uint64()
+        N.check(N.lib().tm_image_sum_sq_rows(self.ctx.h, self.h, int(row0), int(nrows),
+                                             C.byref(v)))
+        return v.value
+
+    def set_noise_floor(self, q_total: int):
+        N.check(N.lib().tm_image_set_noise_floor(self.ctx.h, self.h, C.c_uint64(int(q_total))))
+
     @property
     def is_integer(self) -> bool:
         return bool(N.lib().tm_image_is_integer(self.h))

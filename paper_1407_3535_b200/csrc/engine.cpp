@@ -398,6 +398,11 @@ struct tm_image {
     DBuf<uint8_t> u8p;
     int u8p_pitch = 0;
     int u8p_rows = 0;
+    // Row-strip image (tm_image_create_strip_u8): only image rows [row_lo, row_hi) hold
+    // pixels (the rank's strip + halo); window statistics cover the extent rows whose
+    // windows lie inside them; prefix_noise comes from the allreduced global q_total.
+    int row_lo = 0, row_hi = 1 << 30;
+    bool noise_external = false;
 };
 
 tm_ctx::~tm_ctx() {
@@ -524,6 +529,7 @@ void classify_device_image(tm_ctx* ctx, tm_image* img) {
 
 // prefix_noise (stats.cpp:78-81) on the device; returns a device pointer.
 const double* image_prefix_noise(tm_ctx* ctx, tm_image* img) {
+    if (img->noise_external) return img->pn.p + 1;
     if (!img->have_qtotal) {
         img->pn.ensure(8);
         if (img->integer) {
@@ -570,7 +576,7 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
         tmk::window_stats4_supported(p, q, m, n, img->u8p_pitch)) {
         // four columns per thread from the 16-byte-pitched copy
         CK(tmk::window_stats4_u8(img->u8p.p, img->u8p_pitch, p, q, m, n, prefix_noise, ws.dev(),
-                                 ctx->s));
+                                 ctx->s, img->row_lo, img->row_hi - m + 1));
         ctx->add(1);
     } else if (img->integer) {
         ctx->hs.ensure(size_t(p) * ec);
@@ -2329,6 +2335,74 @@ int tm_image_upload_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
         img->have_f64 = false;
         img->have_qtotal = false;
         tc_pitch_copy(ctx, img);
+        invalidate_ws(img);
+    });
+}
+
+int tm_image_create_strip_u8(tm_ctx* ctx, int rows, int cols, int row0, int nrows,
+                             const uint8_t* pixels, tm_image** out) {
+    return guard(ctx, [&] {
+        if (rows < 1 || cols < 1) invalid("image dimensions must be at least 1x1");
+        if (row0 < 0 || nrows < 1 || row0 + nrows > rows)
+            invalid("tm_image_create_strip_u8: rows outside the image");
+        auto img = std::make_unique<tm_image>();
+        img->ctx = ctx;
+        img->p = rows;
+        img->q = cols;
+        img->integer = true;
+        img->row_lo = row0;
+        img->row_hi = row0 + nrows;
+        ++ctx->refs;
+        alloc_u8(ctx, img.get());
+        CK(cudaMemsetAsync(img->u8.p, 0, size_t(rows) * cols, ctx->s));
+        CK(cudaMemcpyAsync(img->u8.p + size_t(row0) * cols, pixels, size_t(nrows) * cols,
+                           cudaMemcpyHostToDevice, ctx->s));
+        finish_integer_image(ctx, img.get());
+        CK(cudaStreamSynchronize(ctx->s));
+        *out = img.release();
+    });
+}
+
+int tm_image_upload_strip_u8(tm_ctx* ctx, tm_image* img, const uint8_t* pixels) {
+    return guard(ctx, [&] {
+        if (!img || !img->integer) invalid("tm_image_upload_strip_u8: not an 8-bit image");
+        const int nrows = std::min(img->row_hi, img->p) - img->row_lo;
+        CK(cudaMemcpyAsync(img->u8.p + size_t(img->row_lo) * img->q, pixels,
+                           size_t(nrows) * img->q, cudaMemcpyHostToDevice, ctx->s));
+        img->have_f32 = false;
+        img->have_f64 = false;
+        if (!img->noise_external) img->have_qtotal = false;
+        tc_pitch_copy(ctx, img);
+        invalidate_ws(img);
+    });
+}
+
+int tm_image_sum_sq_rows(tm_ctx* ctx, tm_image* img, int row0, int nrows, uint64_t* q_sum) {
+    return guard(ctx, [&] {
+        if (!img || !img->integer || !q_sum) invalid("tm_image_sum_sq_rows: needs an 8-bit image");
+        if (row0 < img->row_lo || row0 + nrows > std::min(img->row_hi, img->p) || nrows < 0)
+            invalid("tm_image_sum_sq_rows: rows outside the pixels held");
+        unsigned long long* d = ctx->counters.p + 30;
+        CK(tmk::sum_sq_rows_u8(img->u8.p, img->q, row0, nrows, d, ctx->s));
+        ctx->add(1);
+        unsigned long long v = 0;
+        CK(cudaMemcpyAsync(&v, d, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        *q_sum = v;
+    });
+}
+
+int tm_image_set_noise_floor(tm_ctx* ctx, tm_image* img, uint64_t q_total) {
+    return guard(ctx, [&] {
+        if (!img || !img->integer) invalid("tm_image_set_noise_floor: needs an 8-bit image");
+        // stats.cpp:80-81 with the GLOBAL rows + cols and sum of squares (exact for 8-bit
+        // data: q_total < 2^53)
+        const double pn = double(img->p + img->q) * 2.220446049250313e-16 * double(q_total);
+        img->pn.ensure(8);
+        CK(cudaMemcpyAsync(img->pn.p + 1, &pn, 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        img->noise_external = true;
+        img->have_qtotal = true;
         invalidate_ws(img);
     });
 }

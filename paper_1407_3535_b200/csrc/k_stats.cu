@@ -580,7 +580,7 @@ __global__ void __launch_bounds__(512)
 template <int NT, int W>
 __global__ void __launch_bounds__(NT)
     k_wstats4(const uint8_t* __restrict__ img, int P, int p, int q, int m, int n, int G, int seg,
-              const double* __restrict__ pn, DevStats st) {
+              int rlo, int rhi, const double* __restrict__ pn, DevStats st) {
     static_assert(W == 2 || W == 4, "two or four columns per thread");
     pdl_wait();
     constexpr int NW = NT / 32;
@@ -590,8 +590,8 @@ __global__ void __launch_bounds__(NT)
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int er = p - m + 1, ec = q - n + 1;
     const int c0 = blockIdx.x * (W * G);
-    const int r0 = blockIdx.y * seg, r1 = min(r0 + seg, er);
-    if (r0 >= er || c0 >= ec) return;
+    const int r0 = rlo + blockIdx.y * seg, r1 = min(r0 + seg, min(rhi, er));
+    if (r0 >= r1 || c0 >= ec) return;
     // columns past the image read the zero padding / the next row: only sums no output reads
     const uint8_t* col = img + (c0 + W * t);
     const uint8_t* lead = col + size_t(r0) * P;
@@ -759,8 +759,13 @@ bool window_stats4_supported(int p, int q, int m, int n, int pitch) {
 
 template <int NT, int W>
 cudaError_t launch_wstats4(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
-                           const double* prefix_noise, DevStats st, cudaStream_t s) {
-    const int ec = q - n + 1, er = p - m + 1;
+                           const double* prefix_noise, DevStats st, cudaStream_t s, int rlo,
+                           int rhi) {
+    const int ec = q - n + 1;
+    rlo = std::max(0, rlo);
+    rhi = std::min(rhi, p - m + 1);
+    const int er = std::max(0, rhi - rlo);  // extent rows of this launch (a strip or all)
+    if (er == 0) return cudaSuccess;
     const int G = NT - (n + W - 1) / W;  // output blocks per tile (PC(c + n) stays in the tile)
     const int ntiles = (ec + W * G - 1) / (W * G);
     // one wave of resident CTAs: a segment's m-row warm-up (~15 instructions a row) is small
@@ -774,8 +779,8 @@ cudaError_t launch_wstats4(const uint8_t* imgp, int pitch, int p, int q, int m, 
     int seg = std::max(4, (er + nseg - 1) / nseg);
     nseg = (er + seg - 1) / seg;
     dim3 grid(ntiles, nseg);
-    launch_pdl(k_wstats4<NT, W>, grid, dim3(NT), 0, s, imgp, pitch, p, q, m, n, G, seg,
-               prefix_noise, st);
+    launch_pdl(k_wstats4<NT, W>, grid, dim3(NT), 0, s, imgp, pitch, p, q, m, n, G, seg, rlo,
+               rhi, prefix_noise, st);
     return cudaGetLastError();
 }
 
@@ -795,13 +800,36 @@ int wstats4_variant() {
 }
 
 cudaError_t window_stats4_u8(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
-                             const double* prefix_noise, DevStats st, cudaStream_t s) {
+                             const double* prefix_noise, DevStats st, cudaStream_t s, int rlo,
+                             int rhi) {
     switch (wstats4_variant()) {
-        case 1: return launch_wstats4<128, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
-        case 2: return launch_wstats4<256, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
-        case 3: return launch_wstats4<128, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
-        default: return launch_wstats4<256, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s);
+        case 1: return launch_wstats4<128, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s, rlo, rhi);
+        case 2: return launch_wstats4<256, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s, rlo, rhi);
+        case 3: return launch_wstats4<128, 2>(imgp, pitch, p, q, m, n, prefix_noise, st, s, rlo, rhi);
+        default: return launch_wstats4<256, 4>(imgp, pitch, p, q, m, n, prefix_noise, st, s, rlo, rhi);
     }
+}
+
+// Sum of squares of rows [r0, r0 + nrows) of an 8-bit image (the rank's share of the
+// image-global q_total, stats.cpp:78-79, before the allreduce of a row-strip search).
+__global__ void k_sum_sq_rows(const uint8_t* __restrict__ img, size_t n,
+                              unsigned long long* __restrict__ out) {
+    unsigned long long acc = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const unsigned x = img[i];
+        acc += x * x;
+    }
+    acc = warp_sum(acc);
+    if ((threadIdx.x & 31) == 0 && acc) atomicAdd(out, acc);
+}
+
+cudaError_t sum_sq_rows_u8(const uint8_t* img, int q, int r0, int nrows, unsigned long long* out,
+                           cudaStream_t s) {
+    cudaMemsetAsync(out, 0, sizeof *out, s);
+    const size_t n = size_t(nrows) * q;
+    if (n) k_sum_sq_rows<<<grid_for(n, 256), 256, 0, s>>>(img + size_t(r0) * q, n, out);
+    return cudaGetLastError();
 }
 
 cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n, const double* prefix_noise,

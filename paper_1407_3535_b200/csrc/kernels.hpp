@@ -170,8 +170,12 @@ size_t prefix_noise_f64_parts();
 // ---- window statistics, exact integer path (stats.cpp:55-94) ---------------------------
 // hs/hq scratch: p * ec int32 each.
 bool window_stats4_supported(int p, int q, int m, int n, int pitch);
+// extent rows [rlo, rhi) only (a row strip; default everything)
 cudaError_t window_stats4_u8(const uint8_t* imgp, int pitch, int p, int q, int m, int n,
-                             const double* prefix_noise, DevStats st, cudaStream_t s);
+                             const double* prefix_noise, DevStats st, cudaStream_t s,
+                             int rlo = 0, int rhi = 1 << 30);
+cudaError_t sum_sq_rows_u8(const uint8_t* img, int q, int r0, int nrows, unsigned long long* out,
+                           cudaStream_t s);
 cudaError_t window_stats_u8(const uint8_t* img, int p, int q, int m, int n,
                             const double* prefix_noise,
                             int* hs, int* hq, DevStats st, cudaStream_t s);

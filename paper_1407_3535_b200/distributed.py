@@ -41,6 +41,40 @@ def strip_rows(tr: int, rank: int, world: int) -> tuple:
     return (tr * rank) // world, (tr * (rank + 1)) // world
 
 
+def noise_rows(p: int, rank: int, world: int) -> tuple:
+    """Image rows whose squares rank `rank` sums for the image-global q_total (stats.cpp:79):
+    a disjoint partition, allreduced by SUM."""
+    return (p * rank) // world, (p * (rank + 1)) // world
+
+
+HOLD_GROUP = 15  # group sizes a strip image covers up front (EGS rarely passes h = 7)
+
+
+def strip_image_rows(p: int, q: int, m: int, n: int, rank: int, world: int, h0: int = 3,
+                     max_group: int = HOLD_GROUP, pad: int = 16) -> tuple:
+    """Image rows [lo, hi) a rank must hold for a strip-local EGS search: for every group
+    size up to `max_group` (h0, h0+2, ...), the extent rows of the rank's group rows plus
+    the template_height-1 halo below them (windows reach m-1 rows down), plus the rank's
+    noise rows; `pad` rows of slack below (row walks read a few rows ahead).  A larger
+    candidate makes the backend extend its rows (DeviceBackend.autocorr)."""
+    er = p - m + 1
+    cap = max_group if max_group > 0 else 2 ** 31 - 1
+    if cap % 2 == 0:
+        cap += 1
+    lo, hi = noise_rows(p, rank, world)
+    h = h0
+    while True:
+        tr = (er + h - 1) // h
+        a, b = strip_rows(tr, rank, world)
+        if b > a:
+            lo = min(lo, a * h)
+            hi = max(hi, min(b * h, er) + m - 1)
+        if h >= er or h >= cap:
+            break
+        h = min(h + 2, cap)
+    return max(0, lo), min(p, hi + pad)
+
+
 # ---- cell order (stats.cpp:147-154) --------------------------------------------------------
 def better(a: dict, b: dict) -> bool:
     """better_candidate: valid, non-degenerate > degenerate, larger rho, smaller (row, col)."""
@@ -193,6 +227,12 @@ def match_strips(backend, comm, t, image_shape, mode="egs", policy="frozen", ini
     m, n = t.shape
     p, q = image_shape
     er, ec = p - m + 1, q - n + 1
+    if mode == "egs" and getattr(backend, "strip_local", False) and not backend.noise_set:
+        # strip-local window statistics need the image-global flat-noise floor
+        # (stats.cpp:78-81): each rank sums the squares of a disjoint row range
+        r0, r1 = noise_rows(p, comm.rank, comm.world)
+        (q_total,) = comm.allreduce_sum_i64([backend.sum_sq(r0, r1)])
+        backend.set_noise(q_total)
     if mode == "egs":
         h, w, trace, slot = egs_strips(backend, comm, p, q, m, n, h0, w0, rho_th, xi_fraction)
         prep = backend.commit(m, n, slot, h, w, trace)
@@ -217,7 +257,14 @@ def match_strips(backend, comm, t, image_shape, mode="egs", policy="frozen", ini
 
 # ---- the GPU backend (C ABI) -----------------------------------------------------------------
 class DeviceBackend:
-    """tm_strip_* primitives on one GPU (one context and one resident image per rank)."""
+    """tm_strip_* primitives on one GPU (one context and one resident image per rank).
+
+    `DeviceBackend(ctx, image)` holds the whole image (OptA: the blur / repair passes need
+    every row); `DeviceBackend.strip(...)` holds only the rank's rows (EGS): window
+    statistics and R_co are computed for its strip only, with the global noise floor."""
+
+    strip_local = False
+    noise_set = False
 
     def __init__(self, ctx, image):
         from .api import Image
@@ -225,7 +272,60 @@ class DeviceBackend:
         self.img = image if isinstance(image, Image) else ctx.image(image)
         self._preps = []
 
+    @classmethod
+    def strip(cls, ctx, image, m, n, rank, world, h0=3, hold=HOLD_GROUP):
+        """Upload only rows strip_image_rows(...) of `image` (a full host array, kept by
+        reference for a later extension)."""
+        from .api import Image
+        p, q = image.shape
+        lo, hi = strip_image_rows(p, q, m, n, rank, world, h0, hold)
+        self = cls(ctx, Image.strip(ctx, image[lo:hi], image.shape, lo))
+        self.strip_local = True
+        self.rows = (lo, hi)
+        self.host, self.mn, self.h0, self.hold = image, (m, n), h0, hold
+        return self
+
+    def _extend(self, h):
+        """EGS reached a group size beyond the held rows: re-upload a wider strip (the
+        noise floor is image-global, so it carries over)."""
+        from .api import Image
+        m, n = self.mn
+        p, q = self.host.shape
+        lo, hi = strip_image_rows(p, q, m, n, self.rank, self.world, self.h0, h)
+        q_total = self.q_total
+        self.close()
+        self.img.close()
+        self.img = Image.strip(self.ctx, self.host[lo:hi], self.host.shape, lo)
+        self.rows, self.hold = (lo, hi), h
+        self.img.set_noise_floor(q_total)
+
+    def sum_sq(self, r0, r1):
+        return self.img.sum_sq_rows(r0, r1 - r0)
+
+    def set_noise(self, q_total):
+        self.img.set_noise_floor(q_total)
+        self.q_total = q_total
+        self.noise_set = True
+
+    def upload(self, image):
+        """New pixels for the same strip (e2e); the noise floor must be set again."""
+        lo, hi = self.rows if self.strip_local else (0, image.shape[0])
+        if self.strip_local:
+            self.img.upload_strip(image[lo:hi])
+        else:
+            self.img.upload_u8(image)
+        self.noise_set = False
+        self.reset()
+
+    def reset(self):
+        """Drop per-search state (cached window statistics, preparations)."""
+        self.img.reset_cache()
+        self.close()
+
     def autocorr(self, m, n, h, w, rank, world, rho_tb, slot):
+        if self.strip_local and max(h, w) > self.hold:
+            self.rank, self.world = rank, world
+            self._extend(max(h, w))
         v = C.c_int64()
         N.check(N.lib().tm_strip_autocorr(self.ctx.h, self.img.h, m, n, h, w, rank, world,
                                           C.c_double(rho_tb), slot, C.byref(v)))

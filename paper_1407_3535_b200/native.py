@@ -105,6 +105,11 @@ SIGNATURES = {
     "tm_ctx_create": (C.c_int, [C.c_int, C.POINTER(_P)]),
     "tm_ctx_destroy": (None, [_P]),
     "tm_ctx_synchronize": (C.c_int, [_P]),
+    "tm_image_create_strip_u8": (C.c_int, [_P, C.c_int, C.c_int, C.c_int, C.c_int, _U8,
+                                           C.POINTER(_P)]),
+    "tm_image_upload_strip_u8": (C.c_int, [_P, _P, _U8]),
+    "tm_image_sum_sq_rows": (C.c_int, [_P, _P, C.c_int, C.c_int, C.POINTER(C.c_uint64)]),
+    "tm_image_set_noise_floor": (C.c_int, [_P, _P, C.c_uint64]),
     "tm_ctx_launch_count": (C.c_int64, [_P]),
     "tm_ctx_search_stats": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tm_ctx_stream": (C.c_void_p, [_P]),

@@ -148,6 +148,132 @@ class NumpyBackend:
         return self.port.refine(t, self.img, row, col, d)
 
 
+class NumpyStripBackend(NumpyBackend):
+    """Strip-LOCAL restatement (test-only): holds only rows strip_image_rows(...) of the
+    image; window statistics of its strip use the allreduced global noise floor; R_co and
+    the search see only the rank's group rows (the sub-image starting at its first group
+    row, so the local group grid is the global one shifted)."""
+
+    strip_local = True
+    noise_set = False
+
+    def __init__(self, port, img, m, n, rank, world):
+        from paper_1407_3535_b200.distributed import strip_image_rows
+        self.full = np.asarray(img, np.float64)  # (only read again by _extend)
+        self.p, self.q = self.full.shape
+        self.m, self.n, self.rank, self.world = m, n, rank, world
+        self.hold = 15
+        self.r0, self.r1 = strip_image_rows(self.p, self.q, m, n, rank, world)
+        self.rows = self.full[self.r0:self.r1].copy()  # everything this rank sees
+        super().__init__(port, self.rows)
+        self.stat_rows = []  # extent rows whose statistics were computed (strip-locality)
+
+    def _extend(self, h):
+        from paper_1407_3535_b200.distributed import strip_image_rows
+        self.r0, self.r1 = strip_image_rows(self.p, self.q, self.m, self.n, self.rank,
+                                            self.world, 3, h)
+        self.rows = self.full[self.r0:self.r1].copy()
+        self.hold = h
+
+    def sum_sq(self, a, b):
+        assert self.r0 <= a and b <= self.r1
+        return int(np.sum(self.rows[a - self.r0:b - self.r0].astype(np.int64) ** 2))
+
+    def set_noise(self, q_total):
+        self.floor = float(self.p + self.q) * 2.220446049250313e-16 * float(q_total)
+        self.noise_set = True
+
+    def _sub(self, a, b, m):
+        """Image rows [a, b + m - 1) (extent rows [a, b)) from the held rows."""
+        assert self.r0 <= a and b + m - 1 <= self.r1, (a, b, self.r0, self.r1)
+        self.stat_rows.append((a, b))
+        return self.rows[a - self.r0:b + m - 1 - self.r0]
+
+    def _extent(self, m, h, rank, world):
+        from paper_1407_3535_b200.distributed import strip_rows
+        er = self.p - m + 1
+        tr = (er + h - 1) // h
+        lo, hi = strip_rows(tr, rank, world)
+        return lo * h, min(hi * h, er)
+
+    def autocorr(self, m, n, h, w, rank, world, rho_tb, slot):
+        if max(h, w) > self.hold:
+            self._extend(max(h, w))
+        a, b = self._extent(m, h, rank, world)
+        if b <= a:
+            self.slots[slot] = (None, a, b)
+            return 0
+        sub = self._sub(a, b, m)
+        ws = self.port.window_stats_floor(sub, m, n, self.floor)
+        amap = self.port.local_autocorrelation(sub, m, n, h, w, ws=ws)
+        self.slots[slot] = (amap, a, b)
+        return int(self.port.retained_count(amap, h, w, rho_tb))
+
+    def commit(self, m, n, slot, h, w, trace):
+        amap, a, b = self.slots[slot]
+        return dict(map=amap, a=a, b=b, h=h, w=w)
+
+    def search_begin(self, prep, t, rank, world, policy, init, margin):
+        self.t = np.asarray(t, np.float64)
+        m, n = self.t.shape
+        self.map, self.h, self.w = prep["map"], prep["h"], prep["w"]
+        a, b = prep["a"], prep["b"]
+        self.policy, self.margin, self.init = policy, margin, init
+        self.cells, self.centre, self.seeded = [], {}, set()
+        T0 = -math.inf
+        if b <= a:
+            return T0 if init is None else max(T0, min(max(init, -1.0), 1.0))
+        sub = self._sub(a, b, m)
+        _, _, self.flat = self.port.window_stats_floor(sub, m, n, self.floor)
+        _, local = self.port.brute(self.t, sub, surface=True)
+        # windows flat under the sub-image's own floor are flat under the (larger) global
+        # floor too, so the global-floor surface is the local one with those set to 0
+        self.surface = np.where(self.flat == 1, 0.0, local)
+        self.tflat = self.port.template_stats(self.t)[2]
+        er, ec = self.surface.shape
+        tr, tc = self._grid(er, ec, self.h, self.w)
+        for ti in range(tr):
+            r0, r1 = ti * self.h, min(ti * self.h + self.h, er) - 1
+            for tj in range(tc):
+                c0, c1 = tj * self.w, min(tj * self.w + self.w, ec) - 1
+                cr, cc = (r0 + r1) // 2, (c0 + c1) // 2
+                rho = self.surface[cr, cc]
+                deg = bool(self.tflat or self.flat[cr, cc])
+                self.centre[(ti, tj)] = (rho, deg, r0, r1, c0, c1, cr, cc)
+                self.cells.append(dict(rho=rho, row=a + cr, col=cc, valid=True, degenerate=deg))
+                if not deg:
+                    T0 = max(T0, rho)
+        self.row_off = a
+        if init is not None:
+            T0 = max(T0, min(max(init, -1.0), 1.0))
+        return T0
+
+    def search_seed(self, T):
+        T1 = NumpyBackend.search_seed(self, T)
+        for c in self.cells[len(self.centre):]:
+            c["row"] += self.row_off  # seeded members: local -> global rows
+        self._n_fixed = len(self.cells)
+        return T1
+
+    def search_finish(self, T):
+        n0 = getattr(self, "_n_fixed", len(self.centre))
+        part = NumpyBackend.search_finish(self, T) if self.centre else dict(
+            best_rho=0.0, best_row=-1, best_col=-1, best_flags=0, centers=0, eliminated=0,
+            retained=0, final_threshold=T)
+        if self.centre:  # survivors appended by search_finish are in local rows
+            for c in self.cells[n0:]:
+                c["row"] += self.row_off
+            from paper_1407_3535_b200.distributed import better
+            best = dict(valid=False, degenerate=True, rho=0.0, row=-1, col=-1)
+            for c in self.cells:
+                if better(c, best):
+                    best = c
+            part.update(best_rho=best["rho"], best_row=best["row"], best_col=best["col"],
+                        best_flags=(1 if best["valid"] else 0) | (2 if best["degenerate"] else 0))
+        self._n_fixed = None
+        return part
+
+
 def _free_port():
     s = socket.socket()
     s.bind(("127.0.0.1", 0))
@@ -171,15 +297,24 @@ def _worker(rank, world, port, out_path, backend_kind, mode, policy):
                             world_size=world)
     from paper_1407_3535_b200 import distributed as D
     img, t = _case()
+    m, n = t.shape
+    strip = mode == "egs"  # OptA keeps the whole image on every rank
     if backend_kind == "numpy":
         from oracle.binding import Oracle
-        backend = NumpyBackend(Oracle("port"), img)
+        backend = NumpyStripBackend(Oracle("port"), img, m, n, rank, world) if strip else \
+            NumpyBackend(Oracle("port"), img)
     else:
         from paper_1407_3535_b200 import api
         ctx = api.Context(0)
-        backend = D.DeviceBackend(ctx, img)
+        backend = D.DeviceBackend.strip(ctx, img.astype(np.uint8), m, n, rank, world) \
+            if strip else D.DeviceBackend(ctx, img)
     comm = D.Comm()
     res = D.match_strips(backend, comm, t, img.shape, mode=mode, policy=policy)
+    if strip and world > 1:  # strip-local: this rank held and computed only its rows
+        lo, hi = backend.rows if backend_kind == "cuda" else (backend.r0, backend.r1)
+        assert hi - lo < img.shape[0], (lo, hi)
+        if backend_kind == "numpy":
+            assert all(backend.r0 <= a and b + m - 1 <= backend.r1 for a, b in backend.stat_rows)
     if rank == 0:
         np.save(out_path, np.array([res.best_row, res.best_col, res.best_rho, res.refined_row,
                                     res.refined_col, res.refined_rho, res.eliminated,
