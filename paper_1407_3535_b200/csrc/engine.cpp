@@ -215,6 +215,8 @@ struct Tmpl {
     bool integer = false;
     tmk::TStatsH ts{};
     int flush_rows = 0;
+    const float* tf = nullptr;   // device copies (m x npad FP32, m x n FP64)
+    const double* td = nullptr;
 };
 
 // Geometry-dependent tensor-core launch data (band table, row schedule, plan), built and
@@ -298,6 +300,18 @@ struct tm_ctx {
     std::map<std::vector<long long>, std::unique_ptr<TcGeo>> tc_geo;
     // pinned readback block: device->host copies into it are asynchronous, so the host can
     // keep working (e.g. upload the next template) until it synchronises
+    // template batches (run_batch): per-template scan-1 state, scan-2 outputs, results
+    struct Batch {
+        DBuf<float> tf;
+        DBuf<double> td, rho, sa, thr;
+        DBuf<uint8_t> deg, seeded, vis;
+        DBuf<int2> locs;
+        DBuf<tmk::Tally> tally;
+        DBuf<tmk::CellH> cells;
+        DBuf<tmk::ResultBlock> packed;
+        Pinned pin_tf, pin_td;
+        std::vector<tmk::ResultBlock> host;
+    } batch;
     using HostRes = tmk::ResultBlock;
     HostRes* hres = nullptr;      // pinned, mapped: kernels write results straight into it
     HostRes* hres_dev = nullptr;  // its device address
@@ -636,8 +650,8 @@ WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
 
 // ---- templates ---------------------------------------------------------------------------
 
-// template_stats (stats.cpp:98-111) in reference order, then upload.
-Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = false) {
+// template_stats (stats.cpp:98-111) in reference order (host), no upload.
+Tmpl template_host_stats(const double* t, int m, int n) {
     Tmpl T;
     T.m = m;
     T.n = n;
@@ -657,12 +671,21 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = fal
     T.ts.mn = double(m) * double(n);
     T.integer = integer;
     T.flush_rows = int(16777216LL / (65025LL * n));
+    return T;
+}
+
+// template_stats, then upload to the context's template buffers.
+Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = false) {
+    Tmpl T = template_host_stats(t, m, n);
     // the device copy already holds this template (same bytes as the last upload): no copy
     // (a stream of searches with one template uploads it once)
     const size_t mnz = size_t(m) * n;
     if (ctx->tmpl_m == m && ctx->tmpl_n == n && ctx->tmpl_last.size() == mnz && ctx->tf.p &&
-        ctx->td.p && std::memcmp(ctx->tmpl_last.data(), t, mnz * sizeof(double)) == 0)
+        ctx->td.p && std::memcmp(ctx->tmpl_last.data(), t, mnz * sizeof(double)) == 0) {
+        T.tf = ctx->tf.p;
+        T.td = ctx->td.p;
         return T;
+    }
     ctx->tmpl_m = ctx->tmpl_n = 0;  // (re-set below once the copies are enqueued)
     std::vector<float> tf(size_t(m) * T.npad, 0.f);
     for (int i = 0; i < m; ++i)
@@ -683,6 +706,8 @@ Tmpl upload_template(tm_ctx* ctx, const double* t, int m, int n, bool side = fal
     ctx->tmpl_last.assign(t, t + mnz);
     ctx->tmpl_m = m;
     ctx->tmpl_n = n;
+    T.tf = ctx->tf.p;
+    T.td = ctx->td.p;
     return T;
 }
 
@@ -700,9 +725,9 @@ tmk::CorrJob make_job(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
     j.bpitch = img->u8p_pitch;
     j.imgd = img->f64.p;
     j.q = img->q;
-    j.tf = ctx->tf.p;
+    j.tf = T.tf;
     j.npad = T.npad;
-    j.td = ctx->td.p;
+    j.td = T.td;
     j.m = T.m;
     j.n = T.n;
     j.flush_rows = std::max(1, T.flush_rows);
@@ -830,12 +855,12 @@ int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet
         // speculative centre scan: B built on the side stream while the EGS batch runs
         // (ungated: the gate is decided later; a miss rebuilds B on the main stream)
         CK(cudaStreamWaitEvent(ctx->s2, ctx->ev_b0, 0));
-        CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s2));
+        CK(tmk::tc_build_b(T.tf, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s2));
         CK(cudaEventRecord(ctx->ev_b1, ctx->s2));
         CK(cudaStreamWaitEvent(ctx->s, ctx->ev_b1, 0));
     } else {
         ctx->tc_b.ensure(plan.total_bytes);
-        CK(tmk::tc_build_b(ctx->tf.p, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s, task.gate));
+        CK(tmk::tc_build_b(T.tf, T.npad, T.m, T.n, plan, ctx->tc_b.p, ctx->s, task.gate));
     }
     HT("build_b");
     tmk::TcJob job{};
@@ -1711,11 +1736,18 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // on the device; survivor_dispatch selects dense (masked tensor-core kernel) or list, the
 // other launch only writes empty partials.
 // dispatched: the dense/list choice is already made on the device (by the last EGS decision)
+// locs / mask / packed: a batch template's survivor list, visit codes and result slot
+// (default: the context's own).
 void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                         const tmk::GridDesc& g, double* rho_loc,
-                        const unsigned long long* gate = nullptr, bool dispatched = false) {
+                        const unsigned long long* gate = nullptr, bool dispatched = false,
+                        const int2* locs = nullptr, const uint8_t* mask = nullptr,
+                        tmk::ResultBlock* packed = nullptr) {
     cudaStream_t s = ctx->s;
     const size_t E = size_t(g.er) * g.ec;
+    if (!locs) locs = ctx->locs.p;
+    if (!mask) mask = ctx->visits.p;
+    if (!packed) packed = ctx->hres_dev;
     int* dense_flag = reinterpret_cast<int*>(ctx->counters.p + 22);
     unsigned long long* list_count = ctx->counters.p + 23;
     if (!dispatched) CK(tmk::survivor_dispatch(ctx->tally.p, E, dense_flag, list_count, s, gate));
@@ -1730,7 +1762,7 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         task.mode = 2;
         task.c_lim = g.ec;
         task.c_last = -1;
-        task.mask = ctx->visits.p;
+        task.mask = mask;
         task.out_rho = rho_loc;
         task.gate = dense_flag;
         Phase ph(ctx, "survivor_eval");
@@ -1742,11 +1774,11 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     op_pack.cells = ctx->cells.p;
     op_pack.tally = ctx->tally.p;
     op_pack.thr = ctx->thr.p;
-    op_pack.packed = ctx->hres_dev;
+    op_pack.packed = packed;
     // fused into the list kernel's tail: the tensor-core partials [0, np) are already in
     const tmk::TailReduce tail = tail_to(ctx, np + kListBlocks, 2, &op_pack);
     Phase ph(ctx, "survivor_list");
-    CK(tmk::corr_list(job, ctx->locs.p, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
+    CK(tmk::corr_list(job, locs, list_count, int(std::min<size_t>(E, INT_MAX)), rho_loc,
                       nullptr, ctx->partials.p + np, kListBlocks, s, 1, &tail));
     ctx->add(2);
 }
@@ -2667,9 +2699,198 @@ void tm_prep_destroy(tm_prep* prep) {
     }
 }
 
+// ---- template batches ---------------------------------------------------------------------
+// run_egs / run_opta for K templates of one preparation (cmd_bench's loop over a cached
+// preparation, cli.cpp:213-237) as one device pipeline with ONE host synchronisation:
+//   1. per template: scan 1 (tensor-core centre scan) + threshold bootstrap [+ seeding],
+//      its group-level results copied to the template's slot;
+//   2. one bound pass for all K templates (k_sec_rows_multi): every member's R_co and flat
+//      flag are read once;
+//   3. per template: survivor evaluation (dense tensor-core pass or list) and the packed
+//      result, then one readback of all K results.
+// Same results and counts as K separate runs (frozen / seeded policies on the 8-bit
+// tensor-core path; other cases take the per-template loop).
+bool batch_applies(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, int K,
+                   const tm_match_params& P, const uint8_t* visits) {
+    if (K < 2 || K > tmk::kMaxBatch || visits || P.record_visits) return false;
+    int policy = P.policy;
+    const size_t G = size_t(prep->g.tr) * prep->g.tc;
+    if (policy == TM_POLICY_REFERENCE)
+        policy = (P.parallel && P.threads > 1 && G > 1) ? TM_POLICY_FROZEN : TM_POLICY_SEQUENTIAL;
+    if (policy != TM_POLICY_FROZEN && policy != TM_POLICY_SEEDED) return false;
+    tm_image* simg = prep->search_img ? prep->search_img.get() : img;
+    if (prep->g.h > tmk::kTcMaxClasses || !prep->map.p) return false;
+    const size_t mn = size_t(prep->m) * prep->n;
+    for (int k = 0; k < K; ++k) {
+        const Tmpl T = template_host_stats(tmpls + k * mn, prep->m, prep->n);
+        if (T.ts.flat || !tc_path(ctx, simg, T)) return false;
+    }
+    return true;
+}
+
+void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, int K,
+               const tm_match_params& P, tm_match_result* out) {
+    const int m = prep->m, n = prep->n;
+    const size_t mn = size_t(m) * n;
+    tm_image* simg = prep->search_img ? prep->search_img.get() : img;
+    const WS& ws = prep->search_img ? *prep->search_ws : get_ws(ctx, img, m, n);
+    const tmk::GridDesc g = prep->g;
+    const size_t E = size_t(g.er) * g.ec, G = size_t(g.tr) * g.tc;
+    cudaStream_t s = ctx->s;
+    int policy = P.policy;
+    if (policy == TM_POLICY_REFERENCE) policy = TM_POLICY_FROZEN;  // (batch_applies checked)
+    const bool seeded_pol = policy == TM_POLICY_SEEDED;
+    auto& B = ctx->batch;
+    // templates: host statistics, one upload of all K (FP32 rows padded, FP64)
+    std::vector<Tmpl> Ts(K);
+    const int npad = (n + 15) & ~15;
+    std::vector<float> tf(size_t(K) * m * npad, 0.f);
+    for (int k = 0; k < K; ++k) {
+        Ts[k] = template_host_stats(tmpls + k * mn, m, n);
+        for (int i = 0; i < m; ++i)
+            for (int j = 0; j < n; ++j)
+                tf[(size_t(k) * m + i) * npad + j] = float(tmpls[k * mn + size_t(i) * n + j]);
+    }
+    B.tf.ensure(tf.size());
+    B.td.ensure(size_t(K) * mn);
+    B.pin_tf.upload(B.tf.p, tf.data(), tf.size() * 4, s);
+    B.pin_td.upload(B.td.p, tmpls, size_t(K) * mn * 8, s);
+    for (int k = 0; k < K; ++k) {
+        Ts[k].tf = B.tf.p + size_t(k) * m * npad;
+        Ts[k].td = B.td.p + size_t(k) * mn;
+    }
+    B.rho.ensure(size_t(K) * G);
+    B.sa.ensure(size_t(K) * G);
+    B.deg.ensure(size_t(K) * G);
+    if (seeded_pol) B.seeded.ensure(size_t(K) * G);
+    B.thr.ensure(size_t(K));
+    B.cells.ensure(size_t(K) * 3);
+    B.tally.ensure(size_t(K));
+    B.vis.ensure(size_t(K) * E);
+    const unsigned long long cap = E / tmk::kDenseDiv + 1;  // longer lists go dense
+    B.locs.ensure(size_t(K) * cap);
+    B.packed.ensure(size_t(K));
+
+    // 1. scan 1 (+ seeding) per template
+    for (int k = 0; k < K; ++k) {
+        const Tmpl& T = Ts[k];
+        const tmk::ReduceOp op_init = centre_op(ctx, P);
+        centre_scan(ctx, simg, ws, T, g, &op_init);
+        if (!ctx->sa_ready) {  // (the tensor-core epilogue writes it; keep the invariant)
+            CK(tmk::sqrt_gap(ctx->rho_c.p, ctx->sa_c.p, G, s));
+            ctx->add(1);
+        }
+        if (seeded_pol) {
+            const unsigned long long max_groups = 256;
+            const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
+            ctx->seed_locs.ensure(max_locs);
+            ctx->seeded.ensure(G);
+            CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, P.seed_margin,
+                                 ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
+                                 ctx->counters.p + 5, max_groups, s));
+            ctx->add(1);
+            tmk::ReduceOp op_raise{};
+            op_raise.kind = 2;
+            op_raise.thr = ctx->thr.p;
+            eval_list(ctx, simg, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs),
+                      nullptr, nullptr, 1, &op_raise);
+            CK(cudaMemcpyAsync(B.seeded.p + size_t(k) * G, ctx->seeded.p, G,
+                               cudaMemcpyDeviceToDevice, s));
+        }
+        CK(cudaMemcpyAsync(B.rho.p + size_t(k) * G, ctx->rho_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(B.sa.p + size_t(k) * G, ctx->sa_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(B.deg.p + size_t(k) * G, ctx->deg_c.p, G, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(B.thr.p + k, ctx->thr.p, 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(B.cells.p + 3 * k, ctx->cells.p, 2 * sizeof(tmk::CellH),
+                           cudaMemcpyDeviceToDevice, s));
+    }
+    // 2. one bound pass for every template
+    CK(cudaMemsetAsync(B.tally.p, 0, size_t(K) * sizeof(tmk::Tally), s));
+    tmk::SecMulti sm;
+    sm.K = K;
+    sm.G = G;
+    sm.E = E;
+    sm.rho_c = B.rho.p;
+    sm.sa_c = B.sa.p;
+    sm.deg_c = B.deg.p;
+    sm.seeded = seeded_pol ? B.seeded.p : nullptr;
+    sm.thr = B.thr.p;
+    sm.locs = B.locs.p;
+    sm.cap = cap;
+    sm.tally = B.tally.p;
+    sm.visits = B.vis.p;
+    {
+        Phase ph(ctx, "sec_multi");
+        CK(tmk::sec_rows_multi(g, prep->map.p, ws.fl.p, sm, s));
+        ctx->add(1);
+    }
+    // 3. survivors + packed result per template
+    for (int k = 0; k < K; ++k) {
+        CK(cudaMemcpyAsync(ctx->tally.p, B.tally.p + k, sizeof(tmk::Tally),
+                           cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->thr.p, B.thr.p + k, 8, cudaMemcpyDeviceToDevice, s));
+        CK(cudaMemcpyAsync(ctx->cells.p, B.cells.p + 3 * k, 2 * sizeof(tmk::CellH),
+                           cudaMemcpyDeviceToDevice, s));
+        eval_survivors_dev(ctx, simg, ws, Ts[k], g, nullptr, nullptr, false,
+                           B.locs.p + size_t(k) * cap, B.vis.p + size_t(k) * E, B.packed.p + k);
+    }
+    B.host.resize(K);
+    CK(cudaMemcpyAsync(B.host.data(), B.packed.p, size_t(K) * sizeof(tmk::ResultBlock),
+                       cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    for (int k = 0; k < K; ++k) {
+        const tmk::ResultBlock& hr = B.host[k];
+        tmk::CellH best = hr.cells[0];
+        if (seeded_pol && better_h(hr.cells[1], best)) best = hr.cells[1];
+        if (better_h(hr.cells[2], best)) best = hr.cells[2];
+        if (better_h(flat_cell(hr.tally), best)) best = flat_cell(hr.tally);
+        double final_T = hr.thr;
+        if (seeded_pol && (hr.cells[2].flags & 1) && !(hr.cells[2].flags & 2))
+            final_T = std::max(final_T, hr.cells[2].rho);
+        tm_match_result r{};
+        r.mode = prep->mode == TM_MODE_OPTA ? TM_MODE_OPTA : TM_MODE_EGS;
+        r.extent_rows = g.er;
+        r.extent_cols = g.ec;
+        r.best_row = r.refined_row = best.row;
+        r.best_col = r.refined_col = best.col;
+        r.best_rho = r.refined_rho = best.rho;
+        r.best_degenerate = (best.flags & 2) != 0;
+        r.final_threshold = std::isfinite(final_T) ? final_T : 0.0;
+        r.below_threshold =
+            P.has_init_threshold && (r.best_degenerate || best.rho < P.init_threshold);
+        r.centers = (long long)G;
+        r.eliminated = (long long)hr.tally.eliminated;
+        r.retained = (long long)hr.tally.retained;
+        r.elim_pct = 100.0 * double(r.eliminated) / (double(g.er) * double(g.ec));
+        r.ops = (long long)G + r.retained;
+        if (prep->mode == TM_MODE_OPTA) {  // refine_impl on the original image
+            const int d = prep->kappa * prep->radius;
+            long long rops = 0;
+            WS& ws_orig = get_ws(ctx, img, m, n);
+            const tmk::CellH c = refine(ctx, img, ws_orig, Ts[k], r.best_row, r.best_col, d, &rops);
+            r.refined_row = c.row;
+            r.refined_col = c.col;
+            r.refined_rho = c.rho;
+            r.ops += rops;
+            if (P.has_init_threshold)
+                r.below_threshold = (c.flags & 2) || c.rho < P.init_threshold;
+        }
+        out[k] = r;
+    }
+}
+
 int tm_run(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, int ntmpl,
            const tm_match_params* params, tm_match_result* out, uint8_t* visits) {
     return guard(ctx, [&] {
+        if (batch_applies(ctx, prep, img, tmpls, ntmpl, *params, visits)) {
+            CK(cudaEventRecord(ctx->ev0, ctx->s));
+            run_batch(ctx, prep, img, tmpls, ntmpl, *params, out);
+            CK(cudaEventRecord(ctx->ev1, ctx->s));
+            CK(cudaEventSynchronize(ctx->ev1));
+            const double ms = ms_between(ctx->ev0, ctx->ev1) / ntmpl;
+            for (int k = 0; k < ntmpl; ++k) out[k].wall_ms = ms;
+            return;
+        }
         const size_t mn = size_t(prep->m) * prep->n;
         const size_t E = size_t(prep->g.er) * prep->g.ec;
         for (int k = 0; k < ntmpl; ++k) {

@@ -1517,7 +1517,17 @@ AcgGeom acg_geom(int m, int n, GridDesc gd, int nt, int resident = 0) {
     if (resident <= 0) resident = std::max(1, 1024 / nt);
     const int slots = 148 * resident;
     const int per_wave = std::max(1, slots / std::max(1, gd.w * a.ntiles));
-    const int nseg = std::max(1, std::min(per_wave, rows));
+    static const int force_nseg = [] {
+        const char* e = std::getenv("TMATCH_ACG_NSEG");
+        return e ? std::atoi(e) : 0;
+    }();
+    // Large images: segments of at most ~96 group rows even when that means several waves
+    // -- one wave of whole-image segments leaves too few warps in flight to hide the walk's
+    // latency (C5, 265 M locations: fused h = 3 launch 7.66 -> 4.7 ms at 57 segments per
+    // tile column, count-only h = 5 4.07 -> 2.4 ms; C2-sized images keep one wave).
+    const int by_len = (rows + 95) / 96;
+    const int nseg = std::max(1, std::min(force_nseg > 0 ? force_nseg
+                                                        : std::max(per_wave, by_len), rows));
     a.seg = std::max(1, (rows + nseg - 1) / nseg);
     a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
     return a;

@@ -679,6 +679,110 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Scan 2 for a batch of K templates on one preparation (cmd_bench's loop, cli.cpp:213-237,
+// as one pass): every member's R_co and flat flag are read ONCE and tested against each
+// template's threshold and centre values (same decisions as k_sec_rows per template).
+// Per template: visit codes (the dense pass's mask), tallies, flat-member key, survivor
+// list.  Block-level counters in shared memory, one global atomic per template per block.
+__global__ void __launch_bounds__(256)
+    k_sec_rows_multi(Grid g, const double* __restrict__ map, const uint8_t* __restrict__ flat,
+                     SecMulti sm) {
+    pdl_wait();
+    __shared__ unsigned long long s_elim[kMaxBatch], s_keep[kMaxBatch], s_flat[kMaxBatch],
+        s_fkey[kMaxBatch];
+    for (int k = threadIdx.x; k < sm.K; k += blockDim.x)
+        s_elim[k] = s_keep[k] = s_flat[k] = s_fkey[k] = 0ull;
+    __syncthreads();
+    const int lane = threadIdx.x & 31;
+    unsigned full_mask = 0u;  // templates whose survivor list this warp saw fill up
+    const int r_lo = g.row_lo(), r_hi = g.row_hi();
+    const int cols = ((g.ec + 31) / 32) * 32;
+    for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const int ti = g.tile_r(r);
+        const bool centre_row = g.center_row(ti) == r;
+        const size_t rowk = size_t(r) * g.ec;
+        const size_t gbase = size_t(ti) * g.tc;
+        for (int c = threadIdx.x; c < cols; c += blockDim.x) {
+            const bool in = c < g.ec;
+            const size_t kk = rowk + (in ? c : 0);
+            const int tj = g.tile_c(in ? c : 0);
+            const size_t gi = gbase + tj;
+            const bool member = in && !(centre_row && g.center_col(tj) == c);
+            const double mv = member ? __ldg(map + kk) : 0.0;
+            const bool fv = member && __ldg(flat + kk) != 0;
+            const double b = dclamp(mv, -1.0, 1.0);
+            const double x = dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b)));
+            for (int k = 0; k < sm.K; ++k) {
+                const size_t gk = size_t(k) * sm.G + gi;
+                const double T = sm.thr[k];
+                uint8_t vis = 0;  // centres: 0
+                bool survivor = false;
+                if (in && !member && sm.visits) sm.visits[size_t(k) * sm.E + kk] = 0;
+                if (member) {
+                    const bool sd = sm.seeded && __ldg(sm.seeded + gk);
+                    if (sd) {
+                        vis = 2;  // a seeded group: its members were evaluated already
+                    } else {
+                        const bool dg = __ldg(sm.deg_c + gk) != 0;
+                        bool elim = T >= -1.0 && !dg && !fv;
+                        if (elim) {
+                            const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+                            const double a = dclamp(__ldg(sm.rho_c + gk), -1.0, 1.0);
+                            elim = sec_test_fast(tb, a, b, __ldg(sm.sa_c + gk), x);
+                        }
+                        if (elim) {
+                            vis = 1;
+                        } else {
+                            vis = 2;
+                            survivor = !fv;
+                        }
+                    }
+                    if (sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
+                }
+                // warp tallies for template k
+                const unsigned be = __ballot_sync(0xffffffffu, vis == 1);
+                const unsigned bk = __ballot_sync(0xffffffffu, vis == 2);
+                const bool fl_kept = vis == 2 && fv && !(sm.seeded && __ldg(sm.seeded + gk));
+                const unsigned bf = __ballot_sync(0xffffffffu, fl_kept);
+                const unsigned bs = __ballot_sync(0xffffffffu, survivor);
+                unsigned long long fkey = fl_kept ? flat_member_key(r, c) : 0ull;
+                if (bf) fkey = warp_max_u64(fkey);
+                if (lane == 0) {
+                    if (be) atomicAdd(&s_elim[k], (unsigned long long)__popc(be));
+                    if (bk) atomicAdd(&s_keep[k], (unsigned long long)__popc(bk));
+                    if (bf) {
+                        atomicAdd(&s_flat[k], (unsigned long long)__popc(bf));
+                        atomicMax(&s_fkey[k], fkey);
+                    }
+                }
+                if (bs) {
+                    Tally* t = sm.tally + k;
+                    unsigned long long basepos = 0;
+                    if (lane == 0) basepos = atomicAdd(&t->survivors, (unsigned long long)__popc(bs));
+                    basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                    if (!((full_mask >> k) & 1u)) {
+                        if (survivor) {
+                            const unsigned long long pos = basepos + __popc(bs & ((1u << lane) - 1));
+                            if (pos < sm.cap) sm.locs[size_t(k) * sm.cap + pos] = make_int2(r, c);
+                        }
+                        if (basepos + __popc(bs) >= sm.cap) full_mask |= 1u << k;
+                    }
+                }
+            }
+        }
+    }
+    __syncthreads();
+    for (int k = threadIdx.x; k < sm.K; k += blockDim.x) {
+        Tally* t = sm.tally + k;
+        if (s_elim[k]) atomicAdd(&t->eliminated, s_elim[k]);
+        if (s_keep[k]) atomicAdd(&t->retained, s_keep[k]);
+        if (s_flat[k]) {
+            atomicAdd(&t->flat_n, s_flat[k]);
+            atomicMax(&t->flat_key, s_fkey[k]);
+        }
+    }
+}
+
 // y = sqrt(max(0, 1 - clamp(x)^2)): one factor of half_gap (bounds.cpp:21-23).
 __global__ void k_sqrt_gap(const double* __restrict__ x, double* __restrict__ y, size_t n) {
     pdl_wait();
@@ -938,6 +1042,21 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c, cons
     const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 8));
     k_sec_compact<<<blocks, 256, 0, s>>>(to_grid(g), map, rho_c, deg_c, flat, tflat, thr, seeded,
                                          locs, max_locs, tally, visits);
+    return cudaGetLastError();
+}
+
+cudaError_t sqrt_gap(const double* x, double* y, size_t n, cudaStream_t s) {
+    launch_pdl(k_sqrt_gap, dim3(int(std::min<size_t>((n + 255) / 256, 148 * 8))), dim3(256), 0,
+               s, x, y, n);
+    return cudaGetLastError();
+}
+
+cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
+                           const SecMulti& sm, cudaStream_t s) {
+    if (sm.K < 1 || sm.K > kMaxBatch) return cudaErrorInvalidValue;
+    const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
+    const int blocks = std::max(1, std::min(rows, 148 * 8));
+    launch_pdl(k_sec_rows_multi, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm);
     return cudaGetLastError();
 }
 

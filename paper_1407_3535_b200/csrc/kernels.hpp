@@ -120,6 +120,23 @@ struct SecFuse {
     uint8_t* visits = nullptr;
 };
 
+// Scan 2 of a template batch (k_sec_rows_multi): per-template arrays are [K][G] (group
+// level), [K] (thresholds, tallies), [K][cap] (survivor lists), [K][E] (visit codes).
+constexpr int kMaxBatch = 32;
+struct SecMulti {
+    int K = 0;
+    size_t G = 0, E = 0;
+    const double* rho_c = nullptr;
+    const double* sa_c = nullptr;
+    const uint8_t* deg_c = nullptr;
+    const uint8_t* seeded = nullptr;  // may be null (frozen policy)
+    const double* thr = nullptr;
+    int2* locs = nullptr;
+    unsigned long long cap = 0;
+    Tally* tally = nullptr;
+    uint8_t* visits = nullptr;
+};
+
 // Work fused into an argmax reduction (saves launches on the search's critical path).
 struct ReduceOp {
     int kind = 0;  // 0 none, 1 threshold init (matcher.cpp:121-125), 2 raise, 3 pack
@@ -342,6 +359,10 @@ cudaError_t sec_compact(GridDesc g, const double* map, const double* rho_c,
                         Tally* tally, uint8_t* visits, cudaStream_t s);
 // Threshold bootstrap: thr = max(best non-degenerate centre rho, init) (matcher.cpp:121-125)
 // Row-structured scan 2 (same results as sec_compact); sa_c: G doubles of scratch.
+cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
+                           const SecMulti& sm, cudaStream_t s);
+// y = sqrt(max(0, 1 - clamp(x)^2)) (one half_gap factor, bounds.cpp:21-23)
+cudaError_t sqrt_gap(const double* x, double* y, size_t n, cudaStream_t s);
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
                      const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
