@@ -301,7 +301,9 @@ struct tm_ctx {
     // pinned readback block: device->host copies into it are asynchronous, so the host can
     // keep working (e.g. upload the next template) until it synchronises
     // template batches (run_batch): per-template scan-1 state, scan-2 outputs, results
+    DBuf<uint8_t> tflags;  // survivor tile flags of the current search (tmk::TileFlags)
     struct Batch {
+        DBuf<uint8_t> tflags;
         DBuf<float> tf;
         DBuf<double> td, rho, sa, thr;
         DBuf<uint8_t> deg, seeded, vis;
@@ -646,6 +648,15 @@ WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
     WS& ref = *ws;
     img->ws_cache[key] = std::move(ws);
     return ref;
+}
+
+// Survivor tile flags for an extent (zeroed on the stream): scan 2 marks the blocks holding
+// survivors, the masked dense pass skips the rest.
+tmk::TileFlags zero_tile_flags(tm_ctx* ctx, DBuf<uint8_t>& buf, int er, int ec, int count = 1) {
+    const size_t bytes = tmk::tile_flag_bytes(er, ec);
+    buf.ensure(bytes * count);
+    CK(cudaMemsetAsync(buf.p, 0, bytes * count, ctx->s));
+    return tmk::TileFlags{buf.p, (ec + 2047) >> 11};
 }
 
 // ---- templates ---------------------------------------------------------------------------
@@ -1742,7 +1753,8 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                         const tmk::GridDesc& g, double* rho_loc,
                         const unsigned long long* gate = nullptr, bool dispatched = false,
                         const int2* locs = nullptr, const uint8_t* mask = nullptr,
-                        tmk::ResultBlock* packed = nullptr) {
+                        tmk::ResultBlock* packed = nullptr,
+                        const tmk::TileFlags* tflags = nullptr) {
     cudaStream_t s = ctx->s;
     const size_t E = size_t(g.er) * g.ec;
     if (!locs) locs = ctx->locs.p;
@@ -1763,6 +1775,7 @@ void eval_survivors_dev(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         task.c_lim = g.ec;
         task.c_last = -1;
         task.mask = mask;
+        task.tf = tflags ? *tflags : tmk::TileFlags{};
         task.out_rho = rho_loc;
         task.gate = dense_flag;
         Phase ph(ctx, "survivor_eval");
@@ -1839,9 +1852,10 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
         // read (the dense path takes over, driven by the visit mask), so only that many
         // locations are written; the sequential replay and the FP64 path read every one
         const unsigned long long max_locs = (!seq && fp32_path(img, T)) ? E / 16 + 1 : E;
+        const tmk::TileFlags tf = zero_tile_flags(ctx, ctx->tflags, g.er, g.ec);
         CK(tmk::sec_rows(g, in.map, ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p, ws.fl.p, T.ts.flat,
                          ctx->thr.p, seeded, ctx->locs.p, max_locs, ctx->tally.p, visits, s,
-                         ctx->sa_ready));
+                         ctx->sa_ready, tf));
         ctx->add(ctx->sa_ready ? 1 : 2);
     }
     double T0 = 0.0;
@@ -1853,7 +1867,10 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     if (device_dispatch) {
         // frozen / seeded: nothing changes the threshold after scan 2's bound test, so the
         // final readback gives T0; the survivor count never leaves the device
-        if (!in.survivors_enqueued) eval_survivors_dev(ctx, img, ws, T, g, nullptr);
+        const tmk::TileFlags tf{ctx->tflags.p, (g.ec + 2047) >> 11};
+        if (!in.survivors_enqueued)
+            eval_survivors_dev(ctx, img, ws, T, g, nullptr, nullptr, false, nullptr, nullptr,
+                               nullptr, &tf);
     } else {
         CK(cudaMemcpyAsync(&T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, s));
         CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, s));
@@ -2819,6 +2836,8 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
     sm.cap = cap;
     sm.tally = B.tally.p;
     sm.visits = B.vis.p;
+    sm.tf = zero_tile_flags(ctx, B.tflags, g.er, g.ec, K);
+    sm.tf_stride = tmk::tile_flag_bytes(g.er, g.ec);
     {
         Phase ph(ctx, "sec_multi");
         CK(tmk::sec_rows_multi(g, prep->map.p, ws.fl.p, sm, s));
@@ -2831,8 +2850,10 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
         CK(cudaMemcpyAsync(ctx->thr.p, B.thr.p + k, 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(ctx->cells.p, B.cells.p + 3 * k, 2 * sizeof(tmk::CellH),
                            cudaMemcpyDeviceToDevice, s));
+        const tmk::TileFlags tfk{sm.tf.p + size_t(k) * sm.tf_stride, sm.tf.cols};
         eval_survivors_dev(ctx, simg, ws, Ts[k], g, nullptr, nullptr, false,
-                           B.locs.p + size_t(k) * cap, B.vis.p + size_t(k) * E, B.packed.p + k);
+                           B.locs.p + size_t(k) * cap, B.vis.p + size_t(k) * E, B.packed.p + k,
+                           &tfk);
     }
     B.host.resize(K);
     CK(cudaMemcpyAsync(B.host.data(), B.packed.p, size_t(K) * sizeof(tmk::ResultBlock),
@@ -3048,6 +3069,7 @@ void search_fused_end(tm_ctx* ctx, tm_image* img, const tm_match_params& P, cons
     sf.max_locs = E / 16 + 1;  // longer survivor lists go to the dense pass (visit mask)
     sf.tally = ctx->tally.p;
     sf.visits = ctx->visits.p;
+    sf.tf = zero_tile_flags(ctx, ctx->tflags, g.er, g.ec);
     bool hit = false;
     // the survivor evaluation is enqueued behind the EGS batch, gated on the device decision
     // (EGS finished with h_e == pred), so the device keeps working while the host reads the
@@ -3055,7 +3077,8 @@ void search_fused_end(tm_ctx* ctx, tm_image* img, const tm_match_params& P, cons
     const unsigned long long* gate = ctx->counters.p + 24;
     const std::function<void()> hook = [&] {
         // (the dense/list choice is made by the batch's last EGS decision)
-        eval_survivors_dev(ctx, img, ws, T, g, nullptr, gate, /*dispatched=*/true);
+        eval_survivors_dev(ctx, img, ws, T, g, nullptr, gate, /*dispatched=*/true, nullptr,
+                           nullptr, nullptr, &sf.tf);
     };
     ctx->spec_want = pred;  // the decide kernels set the gate for this size
     const EgsOut e = run_egs_search(ctx, img, ws, m, n, P.h0, P.w0, P.rho_th, P.xi_fraction,

@@ -1417,6 +1417,7 @@ __global__ void __launch_bounds__(NT)
                         } else {
                             ++n_keep;
                             surv |= 1u << d;
+                            mark_tile(sf.tf, cr + d - hr, c);
                         }
                     }
                     sf.visits[km] = vis;

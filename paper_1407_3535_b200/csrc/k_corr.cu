@@ -569,7 +569,7 @@ __global__ void __launch_bounds__(256)
                const double* __restrict__ sa_c, const uint8_t* __restrict__ deg_c,
                const uint8_t* __restrict__ flat, int tflat, const double* __restrict__ thr_ptr,
                const uint8_t* __restrict__ seeded, int2* locs, unsigned long long max_locs,
-               Tally* tally, uint8_t* visits) {
+               Tally* tally, uint8_t* visits, TileFlags tf) {
     pdl_wait();
     const double T = *thr_ptr;
     const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
@@ -641,6 +641,7 @@ __global__ void __launch_bounds__(256)
                             ++n_keep;
                             survivor = true;
                             if (visits) visits[k] = 2;
+                            mark_tile(tf, r, c);
                         }
                     }
                 }
@@ -735,6 +736,9 @@ __global__ void __launch_bounds__(256)
                         } else {
                             vis = 2;
                             survivor = !fv;
+                            if (survivor && sm.tf.p)
+                                mark_tile(TileFlags{sm.tf.p + size_t(k) * sm.tf_stride, sm.tf.cols},
+                                          r, c);
                         }
                     }
                     if (sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
@@ -1063,14 +1067,14 @@ cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
                      const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
-                     uint8_t* visits, cudaStream_t s, bool sa_ready) {
+                     uint8_t* visits, cudaStream_t s, bool sa_ready, TileFlags tf) {
     const size_t G = size_t(g.tr) * g.tc;
     if (!sa_ready)
         launch_pdl(k_sqrt_gap, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256), 0, s, rho_c, sa_c, G);
     const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
     const int blocks = std::max(1, std::min(rows, 148 * 8));
     launch_pdl(k_sec_rows, dim3(blocks), dim3(256), 0, s, to_grid(g), map, rho_c, sa_c, deg_c, flat, tflat, thr, seeded,
-                                      locs, max_locs, tally, visits);
+                                      locs, max_locs, tally, visits, tf);
     return cudaGetLastError();
 }
 

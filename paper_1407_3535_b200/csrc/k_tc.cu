@@ -149,6 +149,17 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int ntiles = task.nbands * task.ntc;
+    // mode 2 with tile flags: tasks whose 16-row x 2048-column blocks hold no survivor are
+    // skipped by all three roles alike (same read-only flags)
+    auto tile_on = [&](int t) -> bool {
+        if (MODE != 2 || !task.tf.p) return true;
+        const TcBand bd = task.bands[t / task.ntc];
+        const int cblk = t % task.ntc;  // kTcCols == 2048: one flag column per tile
+        const int b0 = bd.r0 >> 4, b1 = (bd.r0 + bd.sr * (bd.cnt - 1)) >> 4;
+        for (int b = b0; b <= b1; ++b)
+            if (task.tf.p[size_t(b) * task.tf.cols + cblk]) return true;
+        return false;
+    };
     if (task.gate && *task.gate == 0) {  // not selected on the device (survivor_dispatch)
         if (tid == 0) partials[blockIdx.x] = CellH{0.0, -1, -1, 2};
         return;
@@ -192,6 +203,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
             uint32_t it = 0;   // ring uses
             uint32_t bl = 0;   // B loads
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                if (!tile_on(t)) continue;
                 const TcBand bd = task.bands[t / task.ntc];
                 const int c0 = (t % task.ntc) * kTcCols;
                 for (int ch = 0; ch < P.nch; ++ch) {
@@ -260,10 +272,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
         const uint64_t b_desc0 = sdesc(smem_u32(sB), 128, b_sbo);
         const uint32_t idesc0 = idesc_i8(0);
         const int ksteps = P.kx / 32;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            if (!tile_on(t)) continue;
             const TcBand bd = task.bands[t / task.ntc];
             const uint32_t buf = tl & 1;
-            mbar_wait_t(dempty + buf, (tl >> 1) & 1, pd);
+            ++tl;
+            mbar_wait_t(dempty + buf, ((tl - 1) >> 1) & 1, pd);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             const uint32_t dbase = tmem + buf * 256;
             for (int ch = 0; ch < P.nch; ++ch) {
@@ -355,10 +369,12 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
         const DevStats st = job.st;
         Cell best = no_cell();
         uint32_t tl = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            if (!tile_on(t)) continue;
             const TcBand bd = task.bands[t / task.ntc];
             const int c0 = (t % task.ntc) * kTcCols;
             const uint32_t buf = tl & 1;
+            ++tl;
             const int cb = c0 + 16 * a;  // this thread's 16 consecutive columns
             // MODE 1: which of the 16 columns are group centres (constant over the tile)
             uint32_t cmask = 0;
@@ -375,7 +391,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                 for (int ph = 0; ph < 16; ++ph)
                     if (cb + ph < task.c_lim) cmask |= 1u << ph;
             }
-            mbar_wait(dfull + buf, (tl >> 1) & 1, 256);
+            mbar_wait(dfull + buf, ((tl - 1) >> 1) & 1, 256);
             asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
             for (int k = eg; k < bd.cnt && !(task.dbg_flags & 2); k += 2) {
                 uint32_t v[16];

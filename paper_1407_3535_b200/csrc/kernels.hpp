@@ -54,6 +54,22 @@ struct Tally {  // accumulated on device by the search kernels
     unsigned long long flat_n;
 };
 
+// Survivor tile flags: one byte per (16 extent rows) x (2048 columns) block, set by the
+// scan-2 passes for every listed survivor; the masked dense pass (k_tc_corr<2>) skips the
+// (band, column tile) tasks whose blocks hold none.  p == nullptr: every task runs.
+struct TileFlags {
+    uint8_t* p = nullptr;
+    int cols = 0;  // ceil(ec / 2048)
+};
+inline __host__ __device__ size_t tile_flag_bytes(int er, int ec) {
+    return size_t((er + 15) >> 4) * size_t((ec + 2047) >> 11);
+}
+#ifdef __CUDACC__
+__device__ __forceinline__ void mark_tile(const TileFlags& f, int r, int c) {
+    if (f.p) f.p[size_t(r >> 4) * f.cols + (c >> 11)] = 1;
+}
+#endif
+
 // Order-reversing key of a position: max over keys = min (row, col) (better_candidate's
 // tie order among equal-rho degenerate cells, stats.cpp:147-154).
 inline __host__ __device__ unsigned long long flat_member_key(int r, int c) {
@@ -118,6 +134,7 @@ struct SecFuse {
     unsigned long long max_locs = 0;
     Tally* tally = nullptr;
     uint8_t* visits = nullptr;
+    TileFlags tf{};
 };
 
 // Scan 2 of a template batch (k_sec_rows_multi): per-template arrays are [K][G] (group
@@ -135,6 +152,8 @@ struct SecMulti {
     unsigned long long cap = 0;
     Tally* tally = nullptr;
     uint8_t* visits = nullptr;
+    TileFlags tf{};       // template k's flags at tf.p + k * tf_stride
+    size_t tf_stride = 0;
 };
 
 // Work fused into an argmax reduction (saves launches on the search's critical path).
@@ -366,7 +385,7 @@ cudaError_t sqrt_gap(const double* x, double* y, size_t n, cudaStream_t s);
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
                      const uint8_t* deg_c, const uint8_t* flat, int tflat, const double* thr,
                      const uint8_t* seeded, int2* locs, unsigned long long max_locs, Tally* tally,
-                     uint8_t* visits, cudaStream_t s, bool sa_ready = false);
+                     uint8_t* visits, cudaStream_t s, bool sa_ready = false, TileFlags tf = TileFlags{});
 cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, double* thr,
                            cudaStream_t s);
 // Seeded policy: members of every group whose centre rho >= thr - margin -> list.
@@ -440,6 +459,7 @@ struct TcTask {
     double* out_rho;
     uint8_t* out_deg;
     const uint8_t* mask;
+    TileFlags tf;       // mode 2: skip (band, column tile) tasks without survivors
     long long* dbg;     // optional per-CTA pipeline wait counters (8 per CTA)
     int dbg_flags;      // timing experiments only: 1 = no image copies, 2 = no epilogue
     const int* gate;    // optional device flag: 0 -> the launch only writes empty partials
