@@ -306,7 +306,8 @@ struct tm_ctx {
         DBuf<uint8_t> tflags;
         DBuf<float> tf;
         DBuf<double> td, rho, sa, thr;
-        DBuf<uint8_t> deg, seeded, vis;
+        DBuf<uint8_t> vis;
+        DBuf<float4> rec;
         DBuf<int2> locs;
         DBuf<tmk::Tally> tally;
         DBuf<tmk::CellH> cells;
@@ -2778,8 +2779,7 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
     }
     B.rho.ensure(size_t(K) * G);
     B.sa.ensure(size_t(K) * G);
-    B.deg.ensure(size_t(K) * G);
-    if (seeded_pol) B.seeded.ensure(size_t(K) * G);
+    B.rec.ensure(size_t(K) * G);
     B.thr.ensure(size_t(K));
     B.cells.ensure(size_t(K) * 3);
     B.tally.ensure(size_t(K));
@@ -2811,12 +2811,12 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
             op_raise.thr = ctx->thr.p;
             eval_list(ctx, simg, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs),
                       nullptr, nullptr, 1, &op_raise);
-            CK(cudaMemcpyAsync(B.seeded.p + size_t(k) * G, ctx->seeded.p, G,
-                               cudaMemcpyDeviceToDevice, s));
         }
         CK(cudaMemcpyAsync(B.rho.p + size_t(k) * G, ctx->rho_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(B.sa.p + size_t(k) * G, ctx->sa_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
-        CK(cudaMemcpyAsync(B.deg.p + size_t(k) * G, ctx->deg_c.p, G, cudaMemcpyDeviceToDevice, s));
+        CK(tmk::batch_records(ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p,
+                              seeded_pol ? ctx->seeded.p : nullptr, G, B.rec.p + size_t(k) * G, s));
+        ctx->add(1);
         CK(cudaMemcpyAsync(B.thr.p + k, ctx->thr.p, 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(B.cells.p + 3 * k, ctx->cells.p, 2 * sizeof(tmk::CellH),
                            cudaMemcpyDeviceToDevice, s));
@@ -2827,10 +2827,9 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
     sm.K = K;
     sm.G = G;
     sm.E = E;
+    sm.rec = B.rec.p;
     sm.rho_c = B.rho.p;
     sm.sa_c = B.sa.p;
-    sm.deg_c = B.deg.p;
-    sm.seeded = seeded_pol ? B.seeded.p : nullptr;
     sm.thr = B.thr.p;
     sm.locs = B.locs.p;
     sm.cap = cap;

@@ -681,21 +681,37 @@ __global__ void __launch_bounds__(256)
 }
 
 // Scan 2 for a batch of K templates on one preparation (cmd_bench's loop, cli.cpp:213-237,
-// as one pass): every member's R_co and flat flag are read ONCE and tested against each
-// template's threshold and centre values (same decisions as k_sec_rows per template).
-// Per template: visit codes (the dense pass's mask), tallies, flat-member key, survivor
-// list.  Block-level counters in shared memory, one global atomic per template per block.
+// as one pass): every member's R_co, flat flag and half-gap factor are read and formed ONCE
+// for all templates, with the same decisions as k_sec_rows per template.  Thread = member;
+// the K templates are an unrolled loop (KP = K rounded up to a power of two) with the
+// counters in registers; group-level scan-1 values are per-template planes [K][G] (the
+// lanes of a warp read a few consecutive groups of one plane); visit codes go to plane k
+// (the dense pass's mask); survivor lists are warp-aggregated (one atomic per warp and
+// template that has survivors).
+template <int KP>
 __global__ void __launch_bounds__(256)
     k_sec_rows_multi(Grid g, const double* __restrict__ map, const uint8_t* __restrict__ flat,
                      SecMulti sm) {
     pdl_wait();
-    __shared__ unsigned long long s_elim[kMaxBatch], s_keep[kMaxBatch], s_flat[kMaxBatch],
-        s_fkey[kMaxBatch];
-    for (int k = threadIdx.x; k < sm.K; k += blockDim.x)
-        s_elim[k] = s_keep[k] = s_flat[k] = s_fkey[k] = 0ull;
+    // rarely-updated per-template counters (flat members, survivors past a full list) are
+    // block-level in shared memory; every member is either eliminated or kept, so a thread
+    // counts its members once and its eliminations per template in registers
+    __shared__ unsigned long long s_flat[KP], s_fkey[KP], s_surv[KP];
+    for (int k = threadIdx.x; k < KP; k += blockDim.x) s_flat[k] = s_fkey[k] = s_surv[k] = 0ull;
     __syncthreads();
     const int lane = threadIdx.x & 31;
-    unsigned full_mask = 0u;  // templates whose survivor list this warp saw fill up
+    unsigned n_elim[KP];
+    float tbf[KP];  // clamped thresholds (FP32 decision; the FP64 one inside the margin)
+    unsigned thr_ok = 0u;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+        n_elim[k] = 0u;
+        const double T = k < sm.K ? sm.thr[k] : -2.0;
+        tbf[k] = float(dclamp(dmin(T, 1.0), -1.0, 1.0));
+        if (T >= -1.0) thr_ok |= 1u << k;
+    }
+    unsigned members = 0;
+    unsigned full = 0u;  // templates whose list this warp saw fill up
     const int r_lo = g.row_lo(), r_hi = g.row_hi();
     const int cols = ((g.ec + 31) / 32) * 32;
     for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
@@ -709,81 +725,115 @@ __global__ void __launch_bounds__(256)
             const int tj = g.tile_c(in ? c : 0);
             const size_t gi = gbase + tj;
             const bool member = in && !(centre_row && g.center_col(tj) == c);
-            const double mv = member ? __ldg(map + kk) : 0.0;
+            members += member;
+            const double b = member ? dclamp(__ldg(map + kk), -1.0, 1.0) : 0.0;
             const bool fv = member && __ldg(flat + kk) != 0;
-            const double b = dclamp(mv, -1.0, 1.0);
             const double x = dmax(0.0, __dsub_rn(1.0, __dmul_rn(b, b)));
-            for (int k = 0; k < sm.K; ++k) {
+            float sq;
+            asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(__double2float_rn(x)));
+            const float bf = float(b);
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                if (k >= sm.K) break;
                 const size_t gk = size_t(k) * sm.G + gi;
-                const double T = sm.thr[k];
-                uint8_t vis = 0;  // centres: 0
-                bool survivor = false;
-                if (in && !member && sm.visits) sm.visits[size_t(k) * sm.E + kk] = 0;
+                const float4 rec = __ldg(sm.rec + gk);  // {a, sa, flags, -}: one load
+                const unsigned fl = __float_as_uint(rec.z);
+                uint8_t vis = 0;  // centres
+                bool survivor = false, flat_kept = false;
                 if (member) {
-                    const bool sd = sm.seeded && __ldg(sm.seeded + gk);
-                    if (sd) {
-                        vis = 2;  // a seeded group: its members were evaluated already
-                    } else {
-                        const bool dg = __ldg(sm.deg_c + gk) != 0;
-                        bool elim = T >= -1.0 && !dg && !fv;
+                    vis = 2;
+                    if (!(fl & 2u)) {  // (a seeded group: its members were evaluated already)
+                        bool elim = ((thr_ok >> k) & 1u) && !fv && !(fl & 1u);
                         if (elim) {
-                            const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
-                            const double a = dclamp(__ldg(sm.rho_c + gk), -1.0, 1.0);
-                            elim = sec_test_fast(tb, a, b, __ldg(sm.sa_c + gk), x);
+                            // FP32 bound with a 4e-6 margin (every input an exactly rounded
+                            // value in [-1, 1], x in FP64 before its square root: error <
+                            // 1e-6); the exact FP64 test of k_sec_rows inside it
+                            const float f = fmaf(rec.x, bf, rec.y * sq);
+                            if (tbf[k] >= f + 4e-6f) {
+                                elim = true;
+                            } else if (tbf[k] < f - 4e-6f) {
+                                elim = false;
+                            } else {
+                                const double T = sm.thr[k];
+                                const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+                                const double a = dclamp(sm.rho_c[gk], -1.0, 1.0);
+                                elim = tb >= __dadd_rn(__dmul_rn(a, b),
+                                                       __dmul_rn(sm.sa_c[gk], __dsqrt_rn(x)));
+                            }
                         }
                         if (elim) {
                             vis = 1;
+                            ++n_elim[k];
+                        } else if (fv) {
+                            flat_kept = true;  // rho 0 without a dot: first position kept
                         } else {
-                            vis = 2;
-                            survivor = !fv;
-                            if (survivor && sm.tf.p)
-                                mark_tile(TileFlags{sm.tf.p + size_t(k) * sm.tf_stride, sm.tf.cols},
-                                          r, c);
+                            survivor = true;
+                            if (sm.tf.p)
+                                mark_tile(TileFlags{sm.tf.p + size_t(k) * sm.tf_stride,
+                                                    sm.tf.cols}, r, c);
                         }
                     }
-                    if (sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
                 }
-                // warp tallies for template k
-                const unsigned be = __ballot_sync(0xffffffffu, vis == 1);
-                const unsigned bk = __ballot_sync(0xffffffffu, vis == 2);
-                const bool fl_kept = vis == 2 && fv && !(sm.seeded && __ldg(sm.seeded + gk));
-                const unsigned bf = __ballot_sync(0xffffffffu, fl_kept);
-                const unsigned bs = __ballot_sync(0xffffffffu, survivor);
-                unsigned long long fkey = fl_kept ? flat_member_key(r, c) : 0ull;
-                if (bf) fkey = warp_max_u64(fkey);
-                if (lane == 0) {
-                    if (be) atomicAdd(&s_elim[k], (unsigned long long)__popc(be));
-                    if (bk) atomicAdd(&s_keep[k], (unsigned long long)__popc(bk));
-                    if (bf) {
-                        atomicAdd(&s_flat[k], (unsigned long long)__popc(bf));
-                        atomicMax(&s_fkey[k], fkey);
+                if (in && sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
+                const unsigned bf2 = __ballot_sync(0xffffffffu, flat_kept);
+                if (bf2) {
+                    const unsigned long long fk = warp_max_u64(flat_kept ? flat_member_key(r, c) : 0ull);
+                    if (lane == 0) {
+                        atomicAdd(&s_flat[k], (unsigned long long)__popc(bf2));
+                        atomicMax(&s_fkey[k], fk);
                     }
                 }
-                if (bs) {
-                    Tally* t = sm.tally + k;
-                    unsigned long long basepos = 0;
-                    if (lane == 0) basepos = atomicAdd(&t->survivors, (unsigned long long)__popc(bs));
-                    basepos = __shfl_sync(0xffffffffu, basepos, 0);
-                    if (!((full_mask >> k) & 1u)) {
+                const unsigned ball = __ballot_sync(0xffffffffu, survivor);
+                if (ball) {
+                    if ((full >> k) & 1u) {
+                        if (lane == 0) atomicAdd(&s_surv[k], (unsigned long long)__popc(ball));
+                    } else {
+                        unsigned long long base = 0;
+                        if (lane == 0)
+                            base = atomicAdd(&sm.tally[k].survivors, (unsigned long long)__popc(ball));
+                        base = __shfl_sync(0xffffffffu, base, 0);
                         if (survivor) {
-                            const unsigned long long pos = basepos + __popc(bs & ((1u << lane) - 1));
+                            const unsigned long long pos = base + __popc(ball & ((1u << lane) - 1));
                             if (pos < sm.cap) sm.locs[size_t(k) * sm.cap + pos] = make_int2(r, c);
                         }
-                        if (basepos + __popc(bs) >= sm.cap) full_mask |= 1u << k;
+                        if (base + __popc(ball) >= sm.cap) full |= 1u << k;
                     }
                 }
             }
         }
     }
+    const unsigned long long nm = warp_sum((unsigned long long)members);
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+        if (k >= sm.K) break;
+        const unsigned long long ne = warp_sum((unsigned long long)n_elim[k]);
+        if (lane == 0) {
+            if (ne) atomicAdd(&sm.tally[k].eliminated, ne);
+            if (nm - ne) atomicAdd(&sm.tally[k].retained, nm - ne);
+        }
+    }
     __syncthreads();
     for (int k = threadIdx.x; k < sm.K; k += blockDim.x) {
         Tally* t = sm.tally + k;
-        if (s_elim[k]) atomicAdd(&t->eliminated, s_elim[k]);
-        if (s_keep[k]) atomicAdd(&t->retained, s_keep[k]);
+        if (s_surv[k]) atomicAdd(&t->survivors, s_surv[k]);
         if (s_flat[k]) {
             atomicAdd(&t->flat_n, s_flat[k]);
             atomicMax(&t->flat_key, s_fkey[k]);
         }
+    }
+}
+
+// One template's batch record per group: {float(clamp(rho_c)), float(sa_c), deg | seeded<<1}
+__global__ void k_batch_records(const double* __restrict__ rho_c, const double* __restrict__ sa_c,
+                                const uint8_t* __restrict__ deg_c,
+                                const uint8_t* __restrict__ seeded, size_t G,
+                                float4* __restrict__ rec) {
+    pdl_wait();
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < G;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const unsigned fl = (deg_c[i] ? 1u : 0u) | (seeded && seeded[i] ? 2u : 0u);
+        rec[i] = make_float4(float(dclamp(rho_c[i], -1.0, 1.0)), float(sa_c[i]),
+                             __uint_as_float(fl), 0.f);
     }
 }
 
@@ -1055,12 +1105,31 @@ cudaError_t sqrt_gap(const double* x, double* y, size_t n, cudaStream_t s) {
     return cudaGetLastError();
 }
 
+int batch_kp(int K) {
+    int kp = 1;
+    while (kp < K) kp <<= 1;
+    return kp;
+}
+
 cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
                            const SecMulti& sm, cudaStream_t s) {
     if (sm.K < 1 || sm.K > kMaxBatch) return cudaErrorInvalidValue;
     const int rows = std::max(1, std::min(g.ti_hi * g.h, g.er) - g.ti_lo * g.h);
     const int blocks = std::max(1, std::min(rows, 148 * 8));
-    launch_pdl(k_sec_rows_multi, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm);
+    switch (batch_kp(sm.K)) {
+        case 1: case 2: launch_pdl(k_sec_rows_multi<2>, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm); break;
+        case 4: launch_pdl(k_sec_rows_multi<4>, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm); break;
+        case 8: launch_pdl(k_sec_rows_multi<8>, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm); break;
+        case 16: launch_pdl(k_sec_rows_multi<16>, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm); break;
+        default: launch_pdl(k_sec_rows_multi<32>, dim3(blocks), dim3(256), 0, s, to_grid(g), map, flat, sm); break;
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t batch_records(const double* rho_c, const double* sa_c, const uint8_t* deg_c,
+                          const uint8_t* seeded, size_t G, float4* rec, cudaStream_t s) {
+    launch_pdl(k_batch_records, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256),
+               0, s, rho_c, sa_c, deg_c, seeded, G, rec);
     return cudaGetLastError();
 }
 

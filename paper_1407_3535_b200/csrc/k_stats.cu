@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(kSqThreads)
 // gamma_n, this tree within gamma_depth.  The bracket of q_seq is then monotonically
 // mapped through prefix_noise = RN(RN((rows + cols) * eps) * q_total).
 __global__ void k_prefix_noise_f64(const double* __restrict__ part, int nb, size_t n, int rows,
-                                   int cols, double* __restrict__ nbk) {
+                                   int cols, double* __restrict__ nbk, int widen) {
     double q = 0.0;
     for (int b = 0; b < nb; ++b) q = __dadd_rn(q, part[b]);
     const double per_thread = double((n + size_t(nb) * kSqThreads - 1) / (size_t(nb) * kSqThreads));
@@ -149,8 +149,8 @@ __global__ void k_prefix_noise_f64(const double* __restrict__ part, int nb, size
     const double c = __dmul_rn(double(rows + cols), kEps);
     nbk[0] = q;
     nbk[1] = __dmul_rn(c, q);
-    nbk[2] = __dmul_rn(c, q_lo);
-    nbk[3] = __dmul_rn(c, q_hi);
+    nbk[2] = widen ? -INFINITY : __dmul_rn(c, q_lo);  // widen: test hook, every window
+    nbk[3] = widen ? INFINITY : __dmul_rn(c, q_hi);   // undecided -> the sequential replay
     reinterpret_cast<unsigned long long*>(nbk)[4] = 0ull;
     reinterpret_cast<unsigned long long*>(nbk)[5] = 0ull;
 }
@@ -472,7 +472,10 @@ cudaError_t prefix_noise_f64(const double* img, int p, int q, double* part, doub
                              cudaStream_t s) {
     const size_t n = size_t(p) * q;
     k_sum_sq_f64<<<kSqBlocks, kSqThreads, 0, s>>>(img, n, part);
-    k_prefix_noise_f64<<<1, 1, 0, s>>>(part, kSqBlocks, n, p, q, nbk);
+    // TMATCH_PN_REPLAY=1 (tests): force the sequential q_total replay for every image
+    const char* e = std::getenv("TMATCH_PN_REPLAY");
+    const int widen = e && std::atoi(e) ? 1 : 0;
+    k_prefix_noise_f64<<<1, 1, 0, s>>>(part, kSqBlocks, n, p, q, nbk, widen);
     return cudaGetLastError();
 }
 

@@ -608,3 +608,30 @@ def test_group_column_autocorr_small_windows(ctx, port, m, n):
             assert np.array_equal(got, want), (rows, cols, h, np.argwhere(got != want)[:3])
             assert ctx.autocorr_retained(gi, m, n, h, h) == port.retained_count(want, h, h)
         gi.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("replay", ["0", "1"])
+def test_nonintegral_noise_floor_replay(ctx, port, replay, monkeypatch):
+    """Non-integer images (OptA's blurred image): the image-global q_total (stats.cpp:79) is
+    the reference's SEQUENTIAL sum only where it matters -- windows whose variance falls in
+    the error bracket of the parallel sum trigger the sequential replay on the device and a
+    redo pass.  replay=1 widens the bracket so every window takes that path.  Either way the
+    flat map, mu and omega equal the oracle's bit for bit, on an image whose blurred
+    constant regions put window variances at the noise floor."""
+    monkeypatch.setenv("TMATCH_PN_REPLAY", replay)
+    rng = np.random.default_rng(91)
+    img = rng.integers(0, 256, size=(120, 140)).astype(np.float64)
+    img[10:70, 20:90] = 137.0   # constant patches: blurred, their windows sit at the floor
+    img[80:115, 60:130] = 3.0
+    img = port.blur(port.blur(img))  # non-integer, the reference blur twice
+    for m, n in ((9, 11), (17, 17)):
+        gi = ctx.image(img)
+        assert not gi.is_integer
+        mu, om, fl = ctx.window_stats(gi, m, n)
+        pm, po, pf = port.window_stats(img, m, n)
+        assert fl.sum() > 0  # flat windows present
+        np.testing.assert_array_equal(fl, pf)
+        np.testing.assert_array_equal(mu, pm)
+        np.testing.assert_array_equal(om, po)
+        gi.close()
