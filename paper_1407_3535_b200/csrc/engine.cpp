@@ -307,7 +307,7 @@ struct tm_ctx {
         DBuf<float> tf;
         DBuf<double> td, rho, sa, thr;
         DBuf<uint8_t> vis;
-        DBuf<float4> rec;
+        DBuf<float2> rec;
         DBuf<int2> locs;
         DBuf<tmk::Tally> tally;
         DBuf<tmk::CellH> cells;

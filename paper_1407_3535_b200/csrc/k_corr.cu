@@ -732,23 +732,26 @@ __global__ void __launch_bounds__(256)
             float sq;
             asm("sqrt.approx.f32 %0, %1;" : "=f"(sq) : "f"(__double2float_rn(x)));
             const float bf = float(b);
+            // every template's group record first (independent loads, one latency)
+            float2 rec[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k)
+                rec[k] = k < sm.K ? __ldg(sm.rec + size_t(k) * sm.G + gi) : make_float2(0.f, -1.f);
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
                 if (k >= sm.K) break;
                 const size_t gk = size_t(k) * sm.G + gi;
-                const float4 rec = __ldg(sm.rec + gk);  // {a, sa, flags, -}: one load
-                const unsigned fl = __float_as_uint(rec.z);
                 uint8_t vis = 0;  // centres
                 bool survivor = false, flat_kept = false;
                 if (member) {
                     vis = 2;
-                    if (!(fl & 2u)) {  // (a seeded group: its members were evaluated already)
-                        bool elim = ((thr_ok >> k) & 1u) && !fv && !(fl & 1u);
+                    if (rec[k].y != -2.f) {  // (a seeded group: its members were evaluated already)
+                        bool elim = ((thr_ok >> k) & 1u) && !fv && rec[k].y >= 0.f;
                         if (elim) {
                             // FP32 bound with a 4e-6 margin (every input an exactly rounded
                             // value in [-1, 1], x in FP64 before its square root: error <
                             // 1e-6); the exact FP64 test of k_sec_rows inside it
-                            const float f = fmaf(rec.x, bf, rec.y * sq);
+                            const float f = fmaf(rec[k].x, bf, rec[k].y * sq);
                             if (tbf[k] >= f + 4e-6f) {
                                 elim = true;
                             } else if (tbf[k] < f - 4e-6f) {
@@ -823,17 +826,17 @@ __global__ void __launch_bounds__(256)
     }
 }
 
-// One template's batch record per group: {float(clamp(rho_c)), float(sa_c), deg | seeded<<1}
+// One template's batch record per group: {float(clamp(rho_c)), float(sa_c)}, the flags in
+// the (otherwise non-negative) second field: -1 degenerate centre, -2 seeded group.
 __global__ void k_batch_records(const double* __restrict__ rho_c, const double* __restrict__ sa_c,
                                 const uint8_t* __restrict__ deg_c,
                                 const uint8_t* __restrict__ seeded, size_t G,
-                                float4* __restrict__ rec) {
+                                float2* __restrict__ rec) {
     pdl_wait();
     for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < G;
          i += size_t(gridDim.x) * blockDim.x) {
-        const unsigned fl = (deg_c[i] ? 1u : 0u) | (seeded && seeded[i] ? 2u : 0u);
-        rec[i] = make_float4(float(dclamp(rho_c[i], -1.0, 1.0)), float(sa_c[i]),
-                             __uint_as_float(fl), 0.f);
+        const float sa = seeded && seeded[i] ? -2.f : (deg_c[i] ? -1.f : float(sa_c[i]));
+        rec[i] = make_float2(float(dclamp(rho_c[i], -1.0, 1.0)), sa);
     }
 }
 
@@ -1127,7 +1130,7 @@ cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
 }
 
 cudaError_t batch_records(const double* rho_c, const double* sa_c, const uint8_t* deg_c,
-                          const uint8_t* seeded, size_t G, float4* rec, cudaStream_t s) {
+                          const uint8_t* seeded, size_t G, float2* rec, cudaStream_t s) {
     launch_pdl(k_batch_records, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))), dim3(256),
                0, s, rho_c, sa_c, deg_c, seeded, G, rec);
     return cudaGetLastError();

@@ -143,7 +143,7 @@ constexpr int kMaxBatch = 32;
 struct SecMulti {
     int K = 0;
     size_t G = 0, E = 0;
-    const float4* rec = nullptr;      // [K][G] batch_records (the fast test's inputs)
+    const float2* rec = nullptr;      // [K][G] batch_records (the fast test's inputs)
     const double* rho_c = nullptr;    // [K][G] FP64 (the exact test inside the margin)
     const double* sa_c = nullptr;
     const double* thr = nullptr;
@@ -381,9 +381,9 @@ cudaError_t sec_rows_multi(GridDesc g, const double* map, const uint8_t* flat,
                            const SecMulti& sm, cudaStream_t s);
 // K rounded up to a power of two (>= 2): the kernel variant of a batch
 int batch_kp(int K);
-// rec[g] = {float(clamp(rho_c)), float(sa_c), deg | seeded << 1} for one template
+// rec[g] = {float(clamp(rho_c)), float(sa_c) | -1 degenerate | -2 seeded} for one template
 cudaError_t batch_records(const double* rho_c, const double* sa_c, const uint8_t* deg_c,
-                          const uint8_t* seeded, size_t G, float4* rec, cudaStream_t s);
+                          const uint8_t* seeded, size_t G, float2* rec, cudaStream_t s);
 // y = sqrt(max(0, 1 - clamp(x)^2)) (one half_gap factor, bounds.cpp:21-23)
 cudaError_t sqrt_gap(const double* x, double* y, size_t n, cudaStream_t s);
 cudaError_t sec_rows(GridDesc g, const double* map, const double* rho_c, double* sa_c,
