@@ -31,8 +31,13 @@ CXX_FLAGS = ["-O2", "-std=c++17", "-fPIC", "-ffp-contract=off", "-Wall", "-Wextr
 
 CU_SOURCES = ["k_stats.cu", "k_autocorr.cu", "k_corr.cu", "k_opta.cu", "k_tc.cu"]
 CUDA_LIB_SOURCES = ["engine.cpp"]
-API_SOURCES = ["tmatch_api.cpp"]
-HEADERS = ["kernels.hpp", "tm_common.cuh"]
+API_SOURCES = ["tmatch_api.cpp", "tmatch_cli.cpp"]
+# nlohmann::json for the reference's JSON views / CLI layer (include/tmatch/serialize.hpp):
+# the header-only copy this image ships with cudnn_frontend
+NLOHMANN = os.environ.get(
+    "TMATCH_NLOHMANN_DIR",
+    "/opt/prime-rl/.venv/lib/python3.12/site-packages/include/cudnn_frontend/thirdparty/nlohmann")
+HEADERS = ["kernels.hpp", "tm_common.cuh", "api_internal.hpp"]
 
 
 def _newer(target, deps):
@@ -70,13 +75,16 @@ def build(verbose: bool = False) -> dict:
                                                                     "-ldl", "-lpthread"], verbose)
     out = {"cuda": cuda_so}
     api_srcs = [os.path.join(CSRC, s) for s in API_SOURCES if os.path.exists(os.path.join(CSRC, s))]
+    if not os.path.exists(os.path.join(NLOHMANN, "json.hpp")):  # no JSON views without it
+        api_srcs = [s for s in api_srcs if not s.endswith("tmatch_cli.cpp")]
+    json_inc = ["-I" + NLOHMANN] if os.path.isdir(NLOHMANN) else []
     if api_srcs:
         api_so = os.path.join(LIB, "libtmatch.so")
         api_hdrs = [os.path.join(INCLUDE, "tmatch", f) for f in
                     os.listdir(os.path.join(INCLUDE, "tmatch"))] if os.path.isdir(
             os.path.join(INCLUDE, "tmatch")) else []
-        if _newer(api_so, api_srcs + api_hdrs + [cuda_so]):
-            _run(["g++"] + CXX_FLAGS + ["-shared", "-o", api_so] + api_srcs +
+        if _newer(api_so, api_srcs + api_hdrs + [cuda_so, os.path.join(CSRC, "api_internal.hpp")]):
+            _run(["g++"] + CXX_FLAGS + json_inc + ["-shared", "-o", api_so] + api_srcs +
                  ["-L" + LIB, "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
         out["api"] = api_so
         check_src = os.path.join(ROOT, "tests", "cpp", "api_check.cpp")
@@ -85,6 +93,14 @@ def build(verbose: bool = False) -> dict:
             _run(["g++"] + CXX_FLAGS + ["-o", check_bin, check_src, "-L" + LIB, "-ltmatch",
                                         "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"], verbose)
         out["api_check"] = check_bin
+        if json_inc:
+            src = os.path.join(ROOT, "tests", "cpp", "cli_driver.cpp")
+            binp = os.path.join(LIB, "cli_driver")
+            if os.path.exists(src) and _newer(binp, [src, api_so] + api_hdrs):
+                _run(["g++"] + CXX_FLAGS + json_inc + ["-o", binp, src, "-L" + LIB, "-ltmatch",
+                                                       "-ltmatch_cuda", "-Wl,-rpath,$ORIGIN"],
+                     verbose)
+            out["cli_driver"] = binp
         for tool in ("cache_interop",):
             src = os.path.join(ROOT, "tests", "cpp", tool + ".cpp")
             binp = os.path.join(LIB, tool)

@@ -905,3 +905,10 @@ MatchResult match(const Image& t, const Image& I, const MatchParams& params) {
 }
 
 }  // namespace tmatch
+
+namespace tmatch::internal {
+tm_ctx* context() { return ctx(); }
+void check_rc(int rc) { check(rc); }
+tm_match_params to_c_params(const MatchParams& p) { return to_c(p); }
+MatchResult from_c_result(const tm_match_result& r) { return from_c(r); }
+}  // namespace tmatch::internal
