@@ -52,7 +52,7 @@ METRIC = "ZNCC-equivalent search locations/sec"
 UNIT = "locations/s"
 GOLDEN_DIR = os.path.join(ROOT, "tests", "golden", "configs")
 # CPU-baseline sample: extent rows of a strip around the first template's cut location
-SAMPLE_ROWS = {"C1": None, "C2": None, "C3": 160, "C4": 384, "C5": 512}
+SAMPLE_ROWS = {"C1": None, "C2": None, "C3": 160, "C4": 384, "C5": 512, "C6": 256}
 
 
 def _json(path):
@@ -757,7 +757,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--config", default="C5", choices=["C1", "C2", "C3", "C4", "C5", "C6"])
     ap.add_argument("--policy", default="seeded", choices=["seeded", "frozen"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--reference-budget-s", type=float, default=150.0)

@@ -224,7 +224,19 @@ def config5(seed=505, size=16384) -> Workload:
                     "16384x16384 1/f^2 + rectangles + texture, 96x96 template")
 
 
-CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5}
+def config6(seed=707, n_templates=8) -> Workload:
+    """Not a BASELINE config: OptA at scale with kappa > 0 (the reference accepts two blur
+    iterations here), so the search runs on the non-integer blurred image -- 2048^2 1/f^2 +
+    blur sigma 1.0 (C1's content at 16x the area), 8 templates 32^2 with C1's perturbation."""
+    img = spectral_image(seed, 2048, 2048, beta=2.0, blur_sigma=1.0)
+    rng = np.random.default_rng(seed + 1)
+    ts = [cut_template(rng, img, 32, 32, 0.9, 10.0, 5.0) for _ in range(n_templates)]
+    return Workload("C6", img, ts, "opta", (1,),
+                    "2048x2048 1/f^2+blur1, 8x32^2 templates, OptA (kappa = 2)")
+
+
+CONFIGS = {"C1": config1, "C2": config2, "C3": config3, "C4": config4, "C5": config5,
+           "C6": config6}
 
 
 def make(name: str, **kw) -> Workload:

@@ -37,7 +37,7 @@ from oracle.binding import Oracle  # noqa: E402
 from paper_1407_3535_b200 import workloads as W  # noqa: E402
 
 OUT = os.path.join(HERE, "configs")
-SEQUENTIAL = {"C1", "C2"}  # the running-threshold policy is cheap enough only here
+SEQUENTIAL = {"C1", "C2", "C6"}  # the running-threshold policy is cheap enough only here
 
 
 def res_dict(r):
@@ -93,7 +93,7 @@ def run(name, ref, threads):
 
 
 def main():
-    names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5"]
+    names = sys.argv[1:] or ["C1", "C2", "C3", "C4", "C5", "C6"]
     ref = Oracle("ref")
     threads = max(2, os.cpu_count() or 2)
     for nm in names:
