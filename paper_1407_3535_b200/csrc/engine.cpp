@@ -1277,12 +1277,16 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
         ctx->prefix.ensure(pslot * nb);
         CK(tmk::replica_prefix_batch(bt, ctx->rowacc.p, ctx->prefix.p, ctx->s));
         ctx->add(2);
+        tmk::OffBatch ob;  // the batch's R_co epilogues in one launch
+        ob.n = nb;
         for (int k = 0; k < nb; ++k) {
-            CK(tmk::autocorr_offset_epilogue(ctx->prefix.p + size_t(k) * pslot, bt.rows[k],
-                                             bt.cols[k], m, n, g, ws.dev(), offs[o0 + k].di,
-                                             offs[o0 + k].dj, map, ctx->s, stop));
-            ctx->add(1);
+            ob.di[k] = offs[o0 + k].di;
+            ob.dj[k] = offs[o0 + k].dj;
+            ob.pw[k] = bt.cols[k];
         }
+        CK(tmk::autocorr_offset_epilogue_b(ctx->prefix.p, pslot, ob, m, n, g, ws.dev(), map,
+                                           ctx->s, stop));
+        ctx->add(1);
     }
     CK(tmk::retained_count(map, g, thr, nr, ctx->s, stop));
     ctx->add(1);

@@ -1747,6 +1747,39 @@ __global__ void k_autocorr_offset(const double* __restrict__ prefix, int ph, int
     }
 }
 
+// k_autocorr_offset for a batch of offsets (grid.y = offset k of the batch; its prefix
+// table at prefix + k * pslot): one launch instead of one per offset.
+__global__ void k_autocorr_offset_b(const double* __restrict__ prefix, size_t pslot, OffBatch ob,
+                                    int m, int n, Grid g, DevStats st, double* __restrict__ map,
+                                    const int* stop) {
+    if (stop && *stop) return;
+    const int kb = blockIdx.y;
+    const int di = ob.di[kb], dj = ob.dj[kb], pw = ob.pw[kb];
+    const double* pre = prefix + size_t(kb) * pslot;
+    const long long G = (long long)g.tr * g.tc;
+    const int orr = max(0, -di), occ = max(0, -dj);
+    const size_t ppw = size_t(pw) + 1;
+    const double mn = double(m) * double(n);
+    for (long long gi = blockIdx.x * (long long)blockDim.x + threadIdx.x; gi < G;
+         gi += (long long)gridDim.x * blockDim.x) {
+        const int ti = int(gi / g.tc), tj = int(gi % g.tc);
+        if (ti < g.ti_lo || ti >= g.ti_hi) continue;
+        const int cr = g.center_row(ti), cc = g.center_col(tj);
+        const int r0 = ti * g.h, r1 = min(r0 + g.h, g.er) - 1;
+        const int c0 = tj * g.w, c1 = min(c0 + g.w, g.ec) - 1;
+        const int mr = cr + di, mc = cc + dj;
+        if (mr < r0 || mr > r1 || mc < c0 || mc > c1) continue;
+        const size_t kc = size_t(cr) * g.ec + cc, km = size_t(mr) * g.ec + mc;
+        if (st.flat[kc] || st.flat[km]) continue;
+        const int r = cr - orr, c = cc - occ;
+        const double* top = pre + size_t(r) * ppw;
+        const double* bot = pre + size_t(r + m) * ppw;
+        const double cross = __dadd_rn(__dsub_rn(__dsub_rn(bot[c + n], top[c + n]), bot[c]), top[c]);
+        const double num = __dsub_rn(cross, __dmul_rn(__dmul_rn(mn, st.mu[kc]), st.mu[km]));
+        map[km] = dclamp(__ddiv_rn(num, __dmul_rn(st.omega[kc], st.omega[km])), -1.0, 1.0);
+    }
+}
+
 __global__ void k_retained(const double* __restrict__ map, Grid g, double thr,
                            unsigned long long* n_r, const int* stop) {
     if (stop && *stop) return;
@@ -2031,6 +2064,17 @@ cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m
     const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 16));
     k_autocorr_offset<<<blocks, 256, 0, s>>>(prefix, ph, pw, m, n, to_grid(g), st, di, dj, map,
                                              stop);
+    return cudaGetLastError();
+}
+
+cudaError_t autocorr_offset_epilogue_b(const double* prefix, size_t pslot, const OffBatch& ob,
+                                       int m, int n, GridDesc g, DevStats st, double* map,
+                                       cudaStream_t s, const int* stop) {
+    const long long G = (long long)g.tr * g.tc;
+    const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 4));
+    if (ob.n > 0)
+        k_autocorr_offset_b<<<dim3(blocks, ob.n), 256, 0, s>>>(prefix, pslot, ob, m, n, to_grid(g),
+                                                              st, map, stop);
     return cudaGetLastError();
 }
 

@@ -84,19 +84,29 @@ __global__ void k_marks(const double* __restrict__ fid, const double* __restrict
 }
 
 // Integer prefix of the marks (CoverageQuery, blur.cpp:137-150): rows then columns.
+// Integer prefix of the marks: exact in any order, so a warp scans a row 32 columns at a
+// time (coalesced, shuffle scan) and the column pass prefetches 16 rows ahead.
 __global__ void k_mark_rows(const uint8_t* __restrict__ marks, int er, int ec, int* __restrict__ P) {
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
     const size_t pw = size_t(ec) + 1;
     if (r > er) return;
     if (r == 0) {
-        for (int c = 0; c <= ec; ++c) P[c] = 0;
+        for (int c = lane; c <= ec; c += 32) P[c] = 0;
         return;
     }
-    int acc = 0;
-    P[size_t(r) * pw] = 0;
-    for (int c = 0; c < ec; ++c) {
-        acc += marks[size_t(r - 1) * ec + c];
-        P[size_t(r) * pw + c + 1] = acc;
+    if (lane == 0) P[size_t(r) * pw] = 0;
+    int carry = 0;
+    for (int c0 = 0; c0 < ec; c0 += 32) {
+        const int c = c0 + lane;
+        int v = c < ec ? marks[size_t(r - 1) * ec + c] : 0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int u = __shfl_up_sync(0xffffffffu, v, o);
+            if (lane >= o) v += u;
+        }
+        if (c < ec) P[size_t(r) * pw + c + 1] = carry + v;
+        carry += __shfl_sync(0xffffffffu, v, 31);
     }
 }
 
@@ -104,10 +114,18 @@ __global__ void k_mark_cols(int er, int ec, int* __restrict__ P) {
     const int c = blockIdx.x * blockDim.x + threadIdx.x;
     const size_t pw = size_t(ec) + 1;
     if (c > ec) return;
+    constexpr int kC = 16;
     int acc = 0;
-    for (int r = 1; r <= er; ++r) {
-        acc += P[size_t(r) * pw + c];
-        P[size_t(r) * pw + c] = acc;
+    for (int r0 = 1; r0 <= er; r0 += kC) {
+        int v[kC];
+#pragma unroll
+        for (int j = 0; j < kC; ++j) v[j] = r0 + j <= er ? P[size_t(r0 + j) * pw + c] : 0;
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+            if (r0 + j > er) break;
+            acc += v[j];
+            P[size_t(r0 + j) * pw + c] = acc;
+        }
     }
 }
 
@@ -165,7 +183,7 @@ cudaError_t mark_violations(const double* fid, const double* changed_in_window, 
 cudaError_t restore_covered(double* blurred, const double* original, const uint8_t* marks,
                             int er, int ec, int m, int n, int p, int q, int* scratch,
                             cudaStream_t s) {
-    k_mark_rows<<<(er + 1 + 127) / 128, 128, 0, s>>>(marks, er, ec, scratch);
+    k_mark_rows<<<(er + 1 + 7) / 8, 256, 0, s>>>(marks, er, ec, scratch);  // warp per row
     k_mark_cols<<<(ec + 1 + 127) / 128, 128, 0, s>>>(er, ec, scratch);
     k_restore<<<blocks_for(size_t(p) * q), 256, 0, s>>>(blurred, original, scratch, er, ec, m, n,
                                                         p, q);

@@ -276,6 +276,32 @@ __device__ __forceinline__ double src_value(const ProdSrc& s, int a, int b) {
     return x;
 }
 
+// The 32 source values of a warp's 32-row x 32-column tile column `c` (rows r0..r0+31):
+// every load issued before any use (branch-free: the source kind is uniform), so the tile
+// costs one memory latency instead of 32 serialised ones.
+__device__ __forceinline__ void src_column32(const ProdSrc& s, int r0, int c, int rows, int cols,
+                                             double (&v)[32]) {
+    const bool cin = c < cols;
+    const double* xp = s.X + size_t(r0 + s.xr) * s.xq + (c + s.xc);
+#pragma unroll
+    for (int k = 0; k < 32; ++k) v[k] = (cin && r0 + k < rows) ? __ldg(xp + size_t(k) * s.xq) : 0.0;
+    if (s.square) {
+#pragma unroll
+        for (int k = 0; k < 32; ++k) v[k] = __dmul_rn(v[k], v[k]);
+    } else if (s.Y) {
+        const double* yp = s.Y + size_t(r0 + s.yr) * s.yq + (c + s.yc);
+#pragma unroll
+        for (int h = 0; h < 32; h += 16) {  // (two halves: register budget)
+            double y[16];
+#pragma unroll
+            for (int k = 0; k < 16; ++k)
+                y[k] = (cin && r0 + h + k < rows) ? __ldg(yp + size_t(h + k) * s.yq) : 0.0;
+#pragma unroll
+            for (int k = 0; k < 16; ++k) v[h + k] = __dmul_rn(v[h + k], y[k]);
+        }
+    }
+}
+
 // One warp = 32 rows.  Tiles of 32 columns are staged through shared memory so global
 // reads/writes stay coalesced while each lane scans its own row sequentially
 // (row_acc += v, stats.cpp:34).
@@ -288,10 +314,10 @@ __global__ void k_rowscan(ProdSrc src, int rows, int cols, double* __restrict__ 
     double acc = 0.0;
     for (int c0 = 0; c0 < cols; c0 += 32) {
         const int c = c0 + lane;
-        for (int k = 0; k < 32; ++k) {
-            const int r = r0 + k;
-            tile[wid][k][lane] = (r < rows && c < cols) ? src_value(src, r, c) : 0.0;
-        }
+        double v[32];
+        src_column32(src, r0, c, rows, cols, v);
+#pragma unroll
+        for (int k = 0; k < 32; ++k) tile[wid][k][lane] = v[k];
         __syncwarp();
         const int cn = min(32, cols - c0);
         for (int j = 0; j < cn; ++j) {
@@ -319,10 +345,25 @@ __global__ void k_colacc(const double* __restrict__ rowacc, int rows, int cols,
         for (int r = 0; r < rows; ++r) prefix[size_t(r + 1) * pw] = 0.0;  // zero first col
         return;
     }
+    // rows in chunks of 16: the next chunk's loads are in flight while this chunk is
+    // accumulated (the additions stay sequential, stats.cpp:35)
+    constexpr int kC = 16;
+    double cur[kC], nxt[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) cur[j] = j < rows ? rowacc[size_t(j) * cols + c] : 0.0;
     double acc = 0.0;
-    for (int r = 0; r < rows; ++r) {
-        acc = __dadd_rn(acc, rowacc[size_t(r) * cols + c]);
-        prefix[size_t(r + 1) * pw + c + 1] = acc;
+    for (int r0 = 0; r0 < rows; r0 += kC) {
+#pragma unroll
+        for (int j = 0; j < kC; ++j)
+            nxt[j] = r0 + kC + j < rows ? rowacc[size_t(r0 + kC + j) * cols + c] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+            if (r0 + j >= rows) break;
+            acc = __dadd_rn(acc, cur[j]);
+            prefix[size_t(r0 + j + 1) * pw + c + 1] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j < kC; ++j) cur[j] = nxt[j];
     }
 }
 
@@ -343,10 +384,10 @@ __global__ void k_rowscan_b(ProdBatch b, double* __restrict__ rowacc) {
     double acc = 0.0;
     for (int c0 = 0; c0 < cols; c0 += 32) {
         const int c = c0 + lane;
-        for (int kk = 0; kk < 32; ++kk) {
-            const int r = r0 + kk;
-            tile[wid][kk][lane] = (r < rows && c < cols) ? src_value(src, r, c) : 0.0;
-        }
+        double v[32];
+        src_column32(src, r0, c, rows, cols, v);
+#pragma unroll
+        for (int kk = 0; kk < 32; ++kk) tile[wid][kk][lane] = v[kk];
         __syncwarp();
         const int cn = min(32, cols - c0);
         for (int jj = 0; jj < cn; ++jj) {
@@ -377,10 +418,23 @@ __global__ void k_colacc_b(ProdBatch b, const double* __restrict__ rowacc,
         for (int r = 0; r < rows; ++r) pre[size_t(r + 1) * pw] = 0.0;  // zero first col
         return;
     }
+    constexpr int kC = 16;  // as k_colacc: next chunk's loads in flight
+    double cur[kC], nxt[kC];
+#pragma unroll
+    for (int j = 0; j < kC; ++j) cur[j] = j < rows ? in[size_t(j) * cols + c] : 0.0;
     double acc = 0.0;
-    for (int r = 0; r < rows; ++r) {
-        acc = __dadd_rn(acc, in[size_t(r) * cols + c]);
-        pre[size_t(r + 1) * pw + c + 1] = acc;
+    for (int r0 = 0; r0 < rows; r0 += kC) {
+#pragma unroll
+        for (int j = 0; j < kC; ++j)
+            nxt[j] = r0 + kC + j < rows ? in[size_t(r0 + kC + j) * cols + c] : 0.0;
+#pragma unroll
+        for (int j = 0; j < kC; ++j) {
+            if (r0 + j >= rows) break;
+            acc = __dadd_rn(acc, cur[j]);
+            pre[size_t(r0 + j + 1) * pw + c + 1] = acc;
+        }
+#pragma unroll
+        for (int j = 0; j < kC; ++j) cur[j] = nxt[j];
     }
 }
 

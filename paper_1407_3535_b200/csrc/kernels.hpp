@@ -286,6 +286,14 @@ cudaError_t autocorr_u8_colwalk(const uint8_t* img, int p, int q, int m, int n, 
                                 DevStats st, double retain_threshold, double* map,
                                 unsigned long long* n_r, unsigned* V, cudaStream_t s);
 // replica path, one offset: cross-sum prefix table of the product image for (di,dj).
+// the R_co epilogue of a batch of offsets (one launch; prefix tables pslot apart)
+struct OffBatch {
+    int n = 0;
+    int di[kProdBatch], dj[kProdBatch], pw[kProdBatch];
+};
+cudaError_t autocorr_offset_epilogue_b(const double* prefix, size_t pslot, const OffBatch& ob,
+                                       int m, int n, GridDesc g, DevStats st, double* map,
+                                       cudaStream_t s, const int* stop);
 cudaError_t autocorr_offset_epilogue(const double* prefix, int ph, int pw, int m, int n,
                                      GridDesc g, DevStats st, int di, int dj, double* map,
                                      cudaStream_t s, const int* stop = nullptr);
