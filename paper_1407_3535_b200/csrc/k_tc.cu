@@ -413,22 +413,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     continue;
                 }
                 const size_t rb = size_t(r) * st.ec + cb;
+                // MODE 2: the visit codes first -- only the (rare) survivors' statistics are
+                // loaded; a thread whose 16 columns hold none skips the row
+                uint32_t on2 = cmask;
+                if (MODE == 2) {
+                    on2 = 0u;
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph)
+                        if (((cmask >> ph) & 1u) && task.mask[rb + ph] == 2) on2 |= 1u << ph;
+                    if (!on2) continue;
+                }
                 // all loads first (independent, predicated), then the FP64 epilogues
-                uint8_t fl[16], mk[16];
+                uint8_t fl[16];
                 double mu[16], om[16];
 #pragma unroll
                 for (int ph = 0; ph < 16; ++ph) {
-                    const bool on = (cmask >> ph) & 1u;
+                    const bool on = (on2 >> ph) & 1u;
                     const size_t kk = on ? rb + ph : 0;
                     fl[ph] = on ? st.flat[kk] : uint8_t(1);
                     mu[ph] = on ? st.mu[kk] : 0.0;
                     om[ph] = on ? st.omega[kk] : 0.0;
-                    if (MODE == 2) mk[ph] = on ? task.mask[kk] : uint8_t(0);
                 }
 #pragma unroll
                 for (int ph = 0; ph < 16; ++ph) {
-                    if (!((cmask >> ph) & 1u)) continue;
-                    if (MODE == 2 && mk[ph] != 2) continue;
+                    if (!((on2 >> ph) & 1u)) continue;
                     const int c = cb + ph;
                     const bool wflat = fl[ph];
                     const double rho = zncc_epilogue(double(int(v[ph])), ts, mu[ph], om[ph], wflat);
