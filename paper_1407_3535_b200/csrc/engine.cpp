@@ -1678,7 +1678,8 @@ struct SearchIn {
 // survivor sets run the band kernel masked by the visit map; sparse ones one warp per
 // location.  rho_loc (optional, extent-sized) receives rho by location.
 void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
-                    const tmk::GridDesc& g, unsigned long long survivors, double* rho_loc) {
+                    const tmk::GridDesc& g, unsigned long long survivors, double* rho_loc,
+                    const tmk::TileFlags* tflags = nullptr) {
     cudaStream_t s = ctx->s;
     const size_t E = size_t(g.er) * g.ec;
     const unsigned long long* count = &ctx->tally.p->survivors;
@@ -1694,6 +1695,7 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         task.c_lim = g.ec;
         task.c_last = -1;
         task.mask = visits;
+        task.tf = tflags ? *tflags : tmk::TileFlags{};
         task.out_rho = rho_loc;
         ctx->partials.ensure(148 + 1);
         int np = 0;
@@ -3545,14 +3547,20 @@ int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out) {
         ctx->locs.ensure(E);
         CK(cudaMemsetAsync(ctx->tally.p, 0, sizeof(tmk::Tally), ctx->s));
         const uint8_t* seeded = S.policy == TM_POLICY_SEEDED ? ctx->seeded.p : nullptr;
-        CK(tmk::sec_compact(g, S.prep->map.p, ctx->rho_c.p, ctx->deg_c.p, ws->fl.p, Tm.ts.flat,
-                            ctx->thr.p, seeded, ctx->locs.p, E, ctx->tally.p, ctx->visits.p,
-                            ctx->s));
-        ctx->add(1);
+        // scan 2 over the strip's rows (k_sec_rows: flat members kept but not listed,
+        // survivor tile flags for the masked dense pass)
+        const size_t G = size_t(g.tr) * g.tc;
+        ctx->sa_c.ensure(G);
+        const tmk::TileFlags tf = zero_tile_flags(ctx, ctx->tflags, g.er, g.ec);
+        const unsigned long long max_locs = fp32_path(simg, Tm) ? E / tmk::kDenseDiv + 1 : E;
+        CK(tmk::sec_rows(g, S.prep->map.p, ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p, ws->fl.p,
+                         Tm.ts.flat, ctx->thr.p, seeded, ctx->locs.p, max_locs, ctx->tally.p,
+                         ctx->visits.p, ctx->s, ctx->sa_ready, tf));
+        ctx->add(ctx->sa_ready ? 1 : 2);
         tmk::Tally tally{};
         CK(cudaMemcpyAsync(&tally, ctx->tally.p, sizeof tally, cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
-        eval_survivors(ctx, simg, *ws, Tm, g, tally.survivors, nullptr);
+        eval_survivors(ctx, simg, *ws, Tm, g, tally.survivors, nullptr, &tf);
         tmk::CellH cells[3];
         CK(cudaMemcpyAsync(cells, ctx->cells.p, sizeof cells, cudaMemcpyDeviceToHost, ctx->s));
         CK(cudaStreamSynchronize(ctx->s));
