@@ -227,6 +227,15 @@ int tm_search_stream_u8(tm_ctx* ctx, const uint8_t* const* images, int nimg, int
 int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
                          const double* map, int h, int w, const tm_match_params* params,
                          tm_match_result* out, uint8_t* visits);
+/* The same with caller-supplied window statistics (E = extent doubles / bytes): run_egs /
+ * run_opta on a preparation whose statistics (PreparedEgs::ws, PreparedOptA::ws_blur) were
+ * computed from earlier pixels -- the reference correlates the current pixels of I with
+ * the prepared statistics and map (matcher.cpp:235-276). */
+int tm_transitive_search_ws(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
+                            const double* map, int h, int w, const double* mu,
+                            const double* omega, const uint8_t* flat,
+                            const tm_match_params* params, tm_match_result* out,
+                            uint8_t* visits);
 /* center_scan (matcher.hpp:24): rho/degenerate per group in grid order; best cell. */
 int tm_center_scan(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img, int h, int w,
                    double* rho, uint8_t* degenerate, int* best_row, int* best_col,

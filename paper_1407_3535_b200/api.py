@@ -353,7 +353,9 @@ class Context:
     run_egs = run
     run_opta = run
 
-    def transitive_search(self, t, img, amap, h, w, record_visits=False, **kw):
+    def transitive_search(self, t, img, amap, h, w, record_visits=False, ws=None, **kw):
+        """transitive_search (matcher.hpp:37-38); `ws` = (mu, omega, flat) of a preparation
+        (possibly of earlier pixels) in place of the image's own statistics."""
         img = self.image(img)
         t = np.ascontiguousarray(t, dtype=np.float64)
         amap = np.ascontiguousarray(amap, dtype=np.float64)
@@ -361,9 +363,18 @@ class Context:
         p = make_params(record_visits=record_visits, **kw)
         res = MatchResult()
         vis = np.zeros(amap.shape, np.uint8) if record_visits else None
-        N.check(N.lib().tm_transitive_search(self.h, _dptr(t), m, n, img.h, _dptr(amap), h, w,
-                                             C.byref(p), C.byref(res),
-                                             _u8ptr(vis) if record_visits else None))
+        if ws is None:
+            N.check(N.lib().tm_transitive_search(self.h, _dptr(t), m, n, img.h, _dptr(amap), h,
+                                                 w, C.byref(p), C.byref(res),
+                                                 _u8ptr(vis) if record_visits else None))
+        else:
+            mu, om, fl = (np.ascontiguousarray(ws[0], np.float64),
+                          np.ascontiguousarray(ws[1], np.float64),
+                          np.ascontiguousarray(ws[2], np.uint8))
+            N.check(N.lib().tm_transitive_search_ws(self.h, _dptr(t), m, n, img.h, _dptr(amap),
+                                                    h, w, _dptr(mu), _dptr(om), _u8ptr(fl),
+                                                    C.byref(p), C.byref(res),
+                                                    _u8ptr(vis) if record_visits else None))
         return (res, vis) if record_visits else res
 
     def center_scan(self, t, img, h, w):

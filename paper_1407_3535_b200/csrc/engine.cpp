@@ -3386,6 +3386,39 @@ int tm_transitive_search(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image
     });
 }
 
+int tm_transitive_search_ws(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img,
+                            const double* map, int h, int w, const double* mu,
+                            const double* omega, const uint8_t* flat,
+                            const tm_match_params* params, tm_match_result* out,
+                            uint8_t* visits) {
+    return guard(ctx, [&] {
+        if (!mu || !omega || !flat) invalid("tm_transitive_search_ws: null window statistics");
+        if (m > img->p || n > img->q) invalid("group grid: template does not fit the image");
+        const tmk::GridDesc g = make_grid(img->p - m + 1, img->q - n + 1, h, w);
+        // the caller's statistics in place of the image's own for this search (a preparation
+        // of earlier pixels: run_egs with prep.ws, matcher.cpp:235-246), then dropped
+        WS& ws = get_ws(ctx, img, m, n);
+        const size_t E = size_t(g.er) * g.ec;
+        CK(cudaMemcpyAsync(ws.mu.p, mu, E * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaMemcpyAsync(ws.om.p, omega, E * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaMemcpyAsync(ws.fl.p, flat, E, cudaMemcpyHostToDevice, ctx->s));
+        ctx->map_user.ensure(E);
+        CK(cudaMemcpyAsync(ctx->map_user.p, map, E * 8, cudaMemcpyHostToDevice, ctx->s));
+        CK(cudaEventRecord(ctx->ev0, ctx->s));
+        const Tmpl T = upload_template(ctx, tmpl, m, n);
+        try {
+            *out = search(ctx, SearchIn{img, &ws, g, ctx->map_user.p}, T, *params, visits);
+        } catch (...) {
+            invalidate_ws(img);
+            throw;
+        }
+        invalidate_ws(img);  // the next user of the image recomputes its own statistics
+        CK(cudaEventRecord(ctx->ev1, ctx->s));
+        CK(cudaEventSynchronize(ctx->ev1));
+        out->wall_ms = ms_between(ctx->ev0, ctx->ev1);
+    });
+}
+
 int tm_center_scan(tm_ctx* ctx, const double* tmpl, int m, int n, tm_image* img, int h, int w,
                    double* rho, uint8_t* degenerate, int* best_row, int* best_col,
                    double* best_rho, int* best_degenerate) {

@@ -851,16 +851,50 @@ PreparedOptA prepare_opta(const Image& I, int m, int n, const MatchParams& param
     return prep;
 }
 
+namespace {
+// transitive_search_impl (matcher.cpp:95-177) on the CURRENT pixels of I with a
+// preparation's map and window statistics, as the reference's run_egs / run_opta do
+// (matcher.cpp:235-276) -- the path for preparations without (valid) device state.
+MatchResult search_with_prepared(const Image& t, const Image& I, const AutoCorrMap& map,
+                                 const GroupGrid& grid, const WindowStats& ws,
+                                 const MatchParams& params) {
+    if (map.rows != grid.extent_rows() || map.cols != grid.extent_cols() ||
+        map.group_h != grid.group_h() || map.group_w != grid.group_w())
+        throw std::invalid_argument("transitive_search: grid/map mismatch");
+    const std::size_t E = std::size_t(map.rows) * map.cols;
+    if (ws.mean.size() != E || ws.norm.size() != E || ws.flat_map.size() != E) {
+        SearchOptions o;  // no statistics recorded: the image's own
+        o.init_threshold = params.init_threshold;
+        o.parallel = params.parallel;
+        o.threads = params.threads;
+        o.record_visits = params.record_visits;
+        return transitive_search(t, I, map, grid, o);
+    }
+    MatchParams mp;
+    mp.init_threshold = params.init_threshold;
+    mp.parallel = params.parallel;
+    mp.threads = params.threads;
+    mp.record_visits = params.record_visits;
+    const tm_match_params c = to_c(mp);
+    DevImage d(I);
+    tm_match_result r;
+    std::vector<uint8_t> visits(params.record_visits ? E : 0);
+    check(tm_transitive_search_ws(ctx(), t.data().data(), t.rows(), t.cols(), d.h,
+                                  map.values.data(), grid.group_h(), grid.group_w(),
+                                  ws.mean.data(), ws.norm.data(), ws.flat_map.data(), &c, &r,
+                                  params.record_visits ? visits.data() : nullptr));
+    MatchResult out = from_c(r);
+    out.visits = std::move(visits);
+    return out;
+}
+}  // namespace
+
 MatchResult run_egs(const Image& t, const Image& I, const PreparedEgs& prep,
                     const MatchParams& params) {
     if (prep.device && prep.device->serves(I)) return run_prepared(t, I, prep.device.get(), params);
-    // a preparation without device state (built by hand or for another buffer)
-    SearchOptions o;
-    o.init_threshold = params.init_threshold;
-    o.parallel = params.parallel;
-    o.threads = params.threads;
-    o.record_visits = params.record_visits;
-    MatchResult r = transitive_search(t, I, prep.egs.map, prep.egs.grid, o);
+    // a preparation without valid device state (built by hand, for another buffer, or the
+    // caller changed the pixels since)
+    MatchResult r = search_with_prepared(t, I, prep.egs.map, prep.egs.grid, prep.ws, params);
     r.mode = MatchMode::egs;
     return r;
 }
@@ -869,12 +903,8 @@ MatchResult run_opta(const Image& t, const Image& I_original, const PreparedOptA
                      const MatchParams& params) {
     if (prep.device && prep.device->serves(I_original))
         return run_prepared(t, I_original, prep.device.get(), params);
-    SearchOptions o;
-    o.init_threshold = params.init_threshold;
-    o.parallel = params.parallel;
-    o.threads = params.threads;
-    o.record_visits = params.record_visits;
-    MatchResult r = transitive_search(t, prep.opta.image, prep.opta.egs.map, prep.opta.egs.grid, o);
+    MatchResult r = search_with_prepared(t, prep.opta.image, prep.opta.egs.map,
+                                         prep.opta.egs.grid, prep.ws_blur, params);
     r.mode = MatchMode::opta;
     const int d = prep.opta.kappa * params.kernel.radius;
     const BestCell b = refine_localization(t, I_original, r.best_row, r.best_col, d);

@@ -155,6 +155,9 @@ SIGNATURES = {
                                       C.POINTER(MatchResult)]),
     "tm_transitive_search": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, _D, C.c_int, C.c_int,
                                        C.POINTER(MatchParams), C.POINTER(MatchResult), _U8]),
+    "tm_transitive_search_ws": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, _D, C.c_int, C.c_int,
+                                          _D, _D, _U8, C.POINTER(MatchParams),
+                                          C.POINTER(MatchResult), _U8]),
     "tm_center_scan": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, C.c_int, C.c_int, _D, _U8, _I,
                                  _I, _D, _I]),
     "tm_refine_localization": (C.c_int, [_P, _D, C.c_int, C.c_int, _P, C.c_int, C.c_int,

@@ -88,6 +88,43 @@ int main() {
     check(po.opta.kappa >= 0 && po.opta.trace.size() == std::size_t(po.opta.kappa) + 1,
           "OptA trace carries kappa+1 accepted iterations");
 
+    {
+        // a caller edits the Image in place between prepare_egs and run_egs: the device copy
+        // of the preparation must not serve the stale pixels (the reference always
+        // correlates against the current contents of I)
+        Image J = I;
+        const PreparedEgs pj = prepare_egs(J, 21, 17, q);
+        const MatchResult stale = run_egs(t, J, pj, q);  // served by the device preparation
+        for (int r = 0; r < 21; ++r)
+            for (int c = 0; c < 17; ++c) J(100 + r, 150 + c) = t(r, c);  // plant an exact copy
+        const MatchResult after = run_egs(t, J, pj, q);
+        std::printf("  (stale %d,%d %.6f; after edit %d,%d %.6f)\n", stale.best_row,
+                    stale.best_col, stale.best_rho, after.best_row, after.best_col,
+                    after.best_rho);
+        // (the prepared statistics are the old pixels', so windows over the planted copy
+        // score up to the clamp at 1: the reference semantics, checked bit for bit against
+        // the oracle in tests/test_gpu_parity.py::test_transitive_search_with_prepared_statistics)
+        check(stale.best_row == 60 && stale.best_col == 90 && after.best_rho == 1.0 &&
+                  after.best_row >= 100 - 20 && after.best_row <= 100 + 20 &&
+                  after.best_col >= 150 - 16 && after.best_col <= 150 + 16,
+              "run_egs after an in-place edit sees the current pixels");
+    }
+
+    {
+        // amortised EGS cost (egs.cpp:65-67): include_autocorr_cost is honoured
+        EgsParams ep;
+        ep.include_autocorr_cost = true;
+        ep.n_templates = 4;
+        const EGSResult ea = efficient_group_size(I, 21, 17, ep);
+        const double extent = double(I.rows() - 20) * double(I.cols() - 16);
+        bool am_ok = !ea.trace.empty();
+        for (const auto& it : ea.trace)
+            am_ok = am_ok && it.cost.amortized ==
+                                 (double(it.h) * it.w - 1.0) * extent / (21.0 * 17.0 * 4);
+        check(am_ok && ea.map.values.size() == std::size_t(extent),
+              "efficient_group_size with include_autocorr_cost (amortised term)");
+    }
+
     try {
         Image flat(5, 5, 3.0);
         match(flat, I, MatchParams{});

@@ -635,3 +635,40 @@ def test_nonintegral_noise_floor_replay(ctx, port, replay, monkeypatch):
         np.testing.assert_array_equal(mu, pm)
         np.testing.assert_array_equal(om, po)
         gi.close()
+
+
+@pytest.mark.gpu
+def test_large_template_bright_image_u32_guard(ctx, port):
+    """Templates with m*n*255^2 >= 2^32 (here 258x260 = 67,080 pixels) on a near-saturated
+    image: the 8-bit R_co kernels' u32 cross sums would wrap, so these shapes must take the
+    64-bit path -- R_co, EGS and the search equal the oracle."""
+    rng = np.random.default_rng(5)
+    img = rng.integers(235, 256, size=(280, 290)).astype(np.float64)
+    t = np.clip(np.rint(img[10:268, 20:280] * 0.98 + rng.normal(0, 1, (258, 260))), 0, 255)
+    m, n = t.shape
+    for h in (1, 3):
+        np.testing.assert_array_equal(ctx.local_autocorrelation(img, m, n, h, h),
+                                      port.local_autocorrelation(img, m, n, h, h))
+    got = ctx.match(t, img, mode="egs")
+    want = port.match(t, img, mode="egs")
+    assert_same_result(got, want, keys=RESULT_KEYS[:-1])
+
+
+@pytest.mark.gpu
+def test_transitive_search_with_prepared_statistics(ctx, port):
+    """run_egs on a preparation of EARLIER pixels (the reference correlates the current
+    pixels with the prepared map and window statistics, matcher.cpp:235-246):
+    tm_transitive_search_ws equals the oracle's transitive_search with the same explicit
+    statistics, bit for bit."""
+    img, t = _cases()[0]
+    m, n = t.shape
+    ws_old = port.window_stats(img, m, n)
+    e = port.efficient_group_size(img, m, n, ws=ws_old)
+    edited = img.copy()
+    edited[5:5 + m, 7:7 + n] = t  # the pixels change after the preparation
+    for par in (False, True):
+        want = port.transitive_search(t, edited, e["map"], e["h"], e["w"], ws=ws_old,
+                                      parallel=par, threads=2)
+        got = ctx.transitive_search(t, edited, e["map"], e["h"], e["w"], ws=ws_old,
+                                    parallel=par, threads=2)
+        assert_same_result(got, want, keys=RESULT_KEYS[:-1])
