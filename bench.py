@@ -705,16 +705,21 @@ def run_strips(args, wl, ws, rank, local):
 
     # e2e: every step uploads the rank's rows of a distinct pinned host image (H2D inside
     # the timed region), recomputes the noise floor (allreduce) and searches
-    host = []
+    lo, hi = backend.rows if strip else (0, wl.image.shape[0])
+    host = []  # pinned copies of just this rank's rows of each distinct image
     for a in variants(wl, 3):
-        hb = torch.empty(a.shape, dtype=torch.uint8, pin_memory=True)
-        hb.numpy()[:] = a
+        hb = torch.empty((hi - lo, a.shape[1]), dtype=torch.uint8, pin_memory=True)
+        hb.numpy()[:] = a[lo:hi]
         host.append(hb.numpy())
     ctr = [0]
 
     def e2e_step():
-        backend.upload(host[ctr[0] % len(host)])
+        rows = host[ctr[0] % len(host)]
         ctr[0] += 1
+        if strip:
+            backend.upload_rows(rows)
+        else:
+            backend.upload(rows)
         return step()
     e2e_step()
     e2e_ms, _ = timed(args.steps, e2e_step)

@@ -307,6 +307,13 @@ class DeviceBackend:
         self.q_total = q_total
         self.noise_set = True
 
+    def upload_rows(self, rows):
+        """New pixels for the same strip, given as this rank's rows only (the rows
+        strip_image_rows chose; e.g. a pinned host buffer of just those rows)."""
+        self.img.upload_strip(rows)
+        self.noise_set = False
+        self.reset()
+
     def upload(self, image):
         """New pixels for the same strip (e2e); the noise floor must be set again."""
         lo, hi = self.rows if self.strip_local else (0, image.shape[0])
