@@ -1382,29 +1382,70 @@ __global__ void __launch_bounds__(NT)
                     if (flat ? 0.0 < thr : retained_below(num, den, thr)) ++evc;
                     continue;
                 }
-                const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
-                if (map) map[km] = val;
-                if (val < thr) ++evc;
-                if constexpr (FUSE) {  // scan 2 (matcher.cpp:48-78), as k_sec_rows
+                if constexpr (!FUSE) {
+                    const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
+                    if (map) map[km] = val;
+                    if (val < thr) ++evc;
+                }
+                if constexpr (FUSE) {  // retained count + scan 2 (matcher.cpp:48-78)
+                    // R_co = clamp(RN(num / den)) is needed exactly only near a decision:
+                    // the FP32 quotient qf (num, den rounded to FP32, one FP32 division:
+                    // relative error < 2e-7) decides the retained test (R_co < thr) and the
+                    // bound test outside margins that cover that error; the FP64 quotient
+                    // is formed only inside them (or near |R_co| = 1, where the bound's
+                    // slope in R_co is unbounded).
+                    float qf = 0.f;
+                    bool fast = !flat;
+                    if (fast) {
+                        qf = __fdiv_rn(float(num), float(den));
+                        fast = fabsf(qf) < 0.99f;
+                    }
+                    double val = 0.0;
+                    bool have_val = flat;  // flat: R_co = 0 exactly
+                    auto exact = [&]() {
+                        if (!have_val) {
+                            val = dclamp(__ddiv_rn(num, den), -1.0, 1.0);
+                            have_val = true;
+                        }
+                        return val;
+                    };
+                    bool ret;
+                    if (flat) {
+                        ret = 0.0 < thr;
+                    } else if (fast && qf < float(thr) - 1e-6f) {
+                        ret = true;
+                    } else if (fast && qf > float(thr) + 1e-6f) {
+                        ret = false;
+                    } else {
+                        ret = exact() < thr;
+                    }
+                    if (ret) ++evc;
                     uint8_t vis = 2;
                     if (pf_sd) {
                         ++n_keep;  // a seeded group: its members were evaluated already
                     } else {
                         bool elim = grp_test && !pf_fm[d];
                         if (elim) {
-                            // FP32 decision with a 4e-6 margin (errors < 1e-6: every input is
-                            // an exactly rounded value in [-1, 1], x = 1 - b^2 in FP64 before
-                            // its square root), the exact FP64 test of k_sec_rows inside it
-                            const float s = sqrt_approx(float(fma(-val, val, 1.0)));
-                            const float f = fmaf(g_af, float(val), g_saf * s);
-                            if (sec_tbf >= f + 4e-6f) {
+                            // FP32 decision with a margin covering the FP32 bound's error
+                            // (inputs exactly rounded values in [-1, 1], x = 1 - b^2 formed
+                            // before its square root: < 1e-6 with the exact b; with the FP32
+                            // quotient for b, |dbound/db| <= 1 + 0.99 / sqrt(1 - 0.99^2) < 8
+                            // adds < 2e-6), the exact FP64 test of k_sec_rows inside it
+                            const float b = have_val ? float(val) : qf;
+                            const float x = have_val ? float(fma(-val, val, 1.0))
+                                                     : fmaf(-qf, qf, 1.0f);
+                            const float s = sqrt_approx(fmaxf(x, 0.f));
+                            const float f = fmaf(g_af, b, g_saf * s);
+                            const float margin = have_val ? 4e-6f : 1e-5f;
+                            if (sec_tbf >= f + margin) {
                                 elim = true;
-                            } else if (sec_tbf < f - 4e-6f) {
+                            } else if (sec_tbf < f - margin) {
                                 elim = false;
                             } else {
-                                const double x = dmax(0.0, __dsub_rn(1.0, __dmul_rn(val, val)));
-                                elim = sec_tb >= __dadd_rn(__dmul_rn(g_a, val),
-                                                           __dmul_rn(pf_sa, __dsqrt_rn(x)));
+                                const double v = exact();
+                                const double xx = dmax(0.0, __dsub_rn(1.0, __dmul_rn(v, v)));
+                                elim = sec_tb >= __dadd_rn(__dmul_rn(g_a, v),
+                                                           __dmul_rn(pf_sa, __dsqrt_rn(xx)));
                             }
                         }
                         if (elim) {
