@@ -956,14 +956,14 @@ __global__ void __launch_bounds__(NT)
     k_acg(const uint8_t* __restrict__ img, int P, int q, int m, int n, Grid g, DevStats st,
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
           int seg, int RR, int* __restrict__ stop, const double* __restrict__ egs_prev,
-          double egs_central, double egs_xi, EgsDecide dec, SecFuse sf) {
+          double egs_central, double egs_xi, EgsDecide dec, SecFuse sf, int tile_base) {
     pdl_wait();
     constexpr int W = H, hr = H / 2;
     constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
     constexpr int NCH = SW / 16;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int dj = int(blockIdx.x) - hr;
-    const int k0 = blockIdx.y * G;
+    const int k0 = (int(blockIdx.y) + tile_base) * G;
     const int ti0 = g.ti_lo + blockIdx.z * seg;
     const int ti1 = min(ti0 + seg, g.ti_hi);
     {
@@ -1595,11 +1595,13 @@ bool acg_enabled() {
     return on;
 }
 
+// tiles [tile_lo, tile_hi) of the launch geometry (tile_hi < 0: to the end)
 template <int H, int NT, int NP, bool FUSE>
 cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                          DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                          const double* egs_prev, double egs_central, double egs_xi,
-                         cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+                         cudaStream_t s, const EgsDecide& dec, const SecFuse& sf,
+                         int tile_lo = 0, int tile_hi = -1) {
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_acg<H, NT, NP, FUSE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1613,24 +1615,30 @@ cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, Gr
                                                       a0.smem) != cudaSuccess)
         occ = 0;
     const AcgGeom a = acg_geom(m, n, gd, NT, occ);
-    dim3 grid(gd.w, a.ntiles, a.nseg);
-    if (gd.ti_hi > gd.ti_lo)
+    const int t1 = tile_hi < 0 ? a.ntiles : std::min(tile_hi, a.ntiles);
+    dim3 grid(gd.w, std::max(0, t1 - tile_lo), a.nseg);
+    if (gd.ti_hi > gd.ti_lo && grid.y > 0)
         launch_pdl(k_acg<H, NT, NP, FUSE>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n,
                    to_grid(gd), st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central,
-                   egs_xi, dec, sf);
+                   egs_xi, dec, sf, tile_lo);
     return cudaGetLastError();
 }
+
+int acg_ntiles(int m, int n, GridDesc gd, int nt) { return acg_geom(m, n, gd, nt).ntiles; }
 
 template <int H, int NT, int NP>
 cudaError_t launch_acg_nt(const uint8_t* imgp, int pitch, int q, int m, int n, GridDesc gd,
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
-                          cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+                          cudaStream_t s, const EgsDecide& dec, const SecFuse& sf,
+                          int tile_lo = 0, int tile_hi = -1) {
     if (sf.thr)
         return launch_acg_f<H, NT, NP, true>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                             egs_prev, egs_central, egs_xi, s, dec, sf);
+                                             egs_prev, egs_central, egs_xi, s, dec, sf, tile_lo,
+                                             tile_hi);
     return launch_acg_f<H, NT, NP, false>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
-                                          egs_prev, egs_central, egs_xi, s, dec, sf);
+                                          egs_prev, egs_central, egs_xi, s, dec, sf, tile_lo,
+                                          tile_hi);
 }
 
 // Packed (dp4a) walk for h = 5 (NP = 2 without a clipped group column, else 3); the
@@ -1642,6 +1650,10 @@ int acg_pack(int h) {
         const char* e = std::getenv("TMATCH_ACG_PACK");
         return e ? (std::atoi(e) ? 1 : 0) : -1;
     }();
+    // h = 0: the single-part h = 3 walk (n a multiple of 3), off unless forced on
+    // (measured on C5: 4.82 ms vs 4.58 ms for the per-column IMAD walk -- the walk is not
+    // what bounds this kernel)
+    if (h == 0) return forced >= 0 ? forced : 0;
     return forced >= 0 ? forced : (h >= 5 ? 1 : 0);
 }
 
@@ -1650,6 +1662,22 @@ cudaError_t launch_acg_np(const uint8_t* imgp, int pitch, int q, int m, int n, G
                           DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                           const double* egs_prev, double egs_central, double egs_xi,
                           cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+    if (H == 3 && n % 3 == 0 && acg_pack(0)) {
+        // n a multiple of the 3-column groups: every unclipped group column is ONE packed part
+        // (one dp4a per row offset and row step instead of three IMADs); the tile holding
+        // the clipped last group column (if any) runs its own launch with the cut parts
+        // (NP = 3), and carries the EGS decision (stream order: it runs after the first)
+        if (gd.ec % gd.w == 0)
+            return launch_acg_nt<H, NT, 1>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                           egs_prev, egs_central, egs_xi, s, dec, sf);
+        const int nt = acg_ntiles(m, n, gd, NT);
+        cudaError_t e = launch_acg_nt<H, NT, 1>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                               egs_prev, egs_central, egs_xi, s, EgsDecide{}, sf,
+                                               0, nt - 1);
+        if (e != cudaSuccess) return e;
+        return launch_acg_nt<H, NT, 3>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
+                                       egs_prev, egs_central, egs_xi, s, dec, sf, nt - 1, nt);
+    }
     if (!acg_pack(H))
         return launch_acg_nt<H, NT, 0>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop,
                                        egs_prev, egs_central, egs_xi, s, dec, sf);
