@@ -285,6 +285,18 @@ int tm_strip_search_begin(tm_ctx* ctx, tm_prep* prep, tm_image* img, const doubl
                           const tm_match_params* params, int rank, int world, double* T0);
 int tm_strip_search_seed(tm_ctx* ctx, double T, double* T1);
 int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out);
+/* Fused row-strip protocol (8-bit data, EGS, frozen / seeded policies): the single-GPU
+ * fused search split at its global decisions -- begin (strip statistics + scan 1 on the
+ * predicted grid -> T0), [seed -> T1], egs (the candidate batch on the strip, scan 2 fused
+ * into the predicted size's R_co at the global T -> local retained counts per candidate),
+ * finish (after the allreduced counts confirm the predicted size: survivors -> part).
+ * *supported == 0 from begin: use the tm_strip_search_* protocol instead. */
+int tm_strip_fused_begin(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+                         const tm_match_params* params, int rank, int world, int pred,
+                         int* supported, double* T0);
+int tm_strip_fused_seed(tm_ctx* ctx, double T, double* T1);
+int tm_strip_fused_egs(tm_ctx* ctx, double T, int* nc, int* hs, int64_t* n_r);
+int tm_strip_fused_finish(tm_ctx* ctx, tm_strip_part* out);
 
 /* Instrumentation: number of kernels this context launched (bench gpu_launches). */
 int64_t tm_ctx_launch_count(const tm_ctx* ctx);

@@ -284,6 +284,12 @@ struct tm_ctx {
         int policy = TM_POLICY_FROZEN;
         int m = 0, n = 0;
         Tmpl T{};
+        // fused protocol (tm_strip_fused_*): predicted group size, its strip grid, the
+        // extent, the survivor tile flags and the EGS candidates of the batch
+        bool fused = false;
+        int pred = 0, er = 0, ec = 0, rank = 0, world = 1;
+        tmk::TileFlags tf{};
+        int nc = 0, cand_h[4] = {0, 0, 0, 0};
     } strip;
     void add(int k) { launches += k; }
     // optional per-phase device timing (CUDA events on the context stream)
@@ -3611,6 +3617,191 @@ int tm_strip_search_finish(tm_ctx* ctx, double T, tm_strip_part* out) {
         out->centers = (int64_t)(g.ti_hi - g.ti_lo) * g.tc;
         out->eliminated = (int64_t)tally.eliminated;
         out->retained = (int64_t)tally.retained;
+        out->final_threshold = fin;
+        S.active = false;
+    });
+}
+
+// ---- fused row-strip protocol (scan 2 inside the strip's R_co launch) ---------------------
+// The single-GPU fused search (search_fused_begin / _end) split at its global decisions:
+//   begin   window statistics of the strip, scan 1 on the PREDICTED grid's strip -> T0
+//   [seed   the seeded policy's groups -> T1]                     (allreduce MAX between)
+//   egs     the EGS candidate batch on the strip: the predicted size with scan 2 fused
+//           (thresholded at the global T), the others count-only -> local retained counts
+//   finish  (after the allreduced counts confirm the predicted size) survivors -> part
+// 4 host round trips instead of ~7, no R_co map round trip.  *supported = 0: not applicable
+// (non-8-bit data, OptA, other policies): the caller uses the tm_strip_search_* protocol.
+int tm_strip_fused_begin(tm_ctx* ctx, tm_image* img, const double* tmpl, int m, int n,
+                         const tm_match_params* params, int rank, int world, int pred,
+                         int* supported, double* T0) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        S = tm_ctx::StripState{};
+        *supported = 0;
+        const tm_match_params& P = *params;
+        if (P.mode == TM_MODE_OPTA || !img->integer || !ctx->ac_fused || !ctx->tc) return;
+        if (P.h0 != P.w0 || m > img->p || n > img->q || pred < 1 || pred % 2 == 0) return;
+        int policy = P.policy;
+        if (policy == TM_POLICY_REFERENCE)
+            policy = (P.parallel && P.threads > 1) ? TM_POLICY_FROZEN : TM_POLICY_SEQUENTIAL;
+        if (policy != TM_POLICY_SEEDED && policy != TM_POLICY_FROZEN) return;
+        if (!(img->u8p.p && img->u8p_rows >= img->p + tmk::kU8PadRows)) return;
+        const int er = img->p - m + 1, ec = img->q - n + 1;
+        const tmk::GridDesc g = strip_of(make_grid(er, ec, pred, pred), rank, world);
+        if (!tmk::autocorr_sec_fuse_supported(m, n, g) || g.h > tmk::kTcMaxClasses) return;
+        const Tmpl probe = template_host_stats(tmpl, m, n);
+        if (probe.ts.flat) invalid("transitive_search: constant template has no defined correlation");
+        if (!tc_path(ctx, img, probe)) return;
+        if (P.has_init_threshold && std::abs(P.init_threshold) > 1.0 + 1e-9)
+            invalid("transitive_search: init threshold out of [-1,1]");
+        WS& ws = get_ws(ctx, img, m, n);  // the strip's rows (strip image) or all
+        S.T = upload_template(ctx, tmpl, m, n);
+        S.img = img;
+        S.P = P;
+        S.P.kernel_profile = nullptr;
+        S.policy = policy;
+        S.m = m;
+        S.n = n;
+        S.g = g;
+        S.pred = pred;
+        S.er = er;
+        S.ec = ec;
+        S.rank = rank;
+        S.world = world;
+        S.fused = true;
+        const size_t G = size_t(g.tr) * g.tc;
+        ctx->rho_c.ensure(G);
+        ctx->deg_c.ensure(G);
+        const tmk::ReduceOp op_init = centre_op(ctx, P);  // threshold init, tally zeroing
+        centre_scan(ctx, img, ws, S.T, g, &op_init);
+        if (!ctx->sa_ready) {
+            ctx->sa_c.ensure(G);
+            CK(tmk::sqrt_gap(ctx->rho_c.p, ctx->sa_c.p, G, ctx->s));
+            ctx->add(1);
+            ctx->sa_ready = true;
+        }
+        CK(cudaMemcpyAsync(T0, ctx->thr.p, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        S.active = true;
+        *supported = 1;
+    });
+}
+
+int tm_strip_fused_seed(tm_ctx* ctx, double T, double* T1) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        if (!S.active || !S.fused) invalid("tm_strip_fused_seed: no fused strip search in progress");
+        const tmk::GridDesc& g = S.g;
+        const size_t G = size_t(g.tr) * g.tc;
+        WS& ws = get_ws(ctx, S.img, S.m, S.n);
+        CK(cudaMemcpyAsync(ctx->thr.p, &T, 8, cudaMemcpyHostToDevice, ctx->s));
+        const unsigned long long max_groups = 256;
+        const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
+        ctx->seed_locs.ensure(max_locs);
+        ctx->seeded.ensure(G);
+        CK(cudaMemsetAsync(ctx->counters.p + 4, 0, 16, ctx->s));
+        CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, S.P.seed_margin,
+                             ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
+                             ctx->counters.p + 5, max_groups, ctx->s));
+        ctx->add(1);
+        tmk::ReduceOp op_raise{};
+        op_raise.kind = 2;
+        op_raise.thr = ctx->thr.p;
+        eval_list(ctx, S.img, ws, S.T, ctx->seed_locs.p, ctx->counters.p + 4, int(max_locs),
+                  nullptr, nullptr, 1, &op_raise);
+        CK(cudaMemcpyAsync(T1, ctx->thr.p, 8, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+    });
+}
+
+int tm_strip_fused_egs(tm_ctx* ctx, double T, int* nc, int* hs, int64_t* n_r) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        if (!S.active || !S.fused) invalid("tm_strip_fused_egs: no fused strip search in progress");
+        tm_image* img = S.img;
+        WS& ws = get_ws(ctx, img, S.m, S.n);
+        const tm_match_params& P = S.P;
+        const size_t E = size_t(S.er) * S.ec;
+        CK(cudaMemcpyAsync(ctx->thr.p, &T, 8, cudaMemcpyHostToDevice, ctx->s));
+        // the first EGS batch of the single-GPU path: h0 .. one size past the prediction
+        int cap = P.max_group > 0 ? P.max_group : INT_MAX;
+        if (cap % 2 == 0) ++cap;
+        const int nmax = std::max(2, std::min(4, (S.pred - P.h0) / 2 + 2));
+        S.nc = 0;
+        for (int h = P.h0; S.nc < nmax;) {
+            S.cand_h[S.nc++] = h;
+            if ((h >= S.er && h >= S.ec) || h >= cap) break;
+            h = std::min(h + 2, cap);
+        }
+        const double thr = expected_elimination_threshold_h(P.rho_th);
+        tmk::SecFuse sf{};
+        sf.thr = ctx->thr.p;
+        sf.rho_c = ctx->rho_c.p;
+        sf.sa_c = ctx->sa_c.p;
+        sf.deg_c = ctx->deg_c.p;
+        sf.seeded = S.policy == TM_POLICY_SEEDED ? ctx->seeded.p : nullptr;
+        sf.tflat = S.T.ts.flat;
+        ctx->locs.ensure(E / tmk::kDenseDiv + 1);
+        ctx->visits.ensure(E);
+        sf.locs = ctx->locs.p;
+        sf.max_locs = E / tmk::kDenseDiv + 1;
+        sf.tally = ctx->tally.p;  // (zeroed by the centre reduction)
+        sf.visits = ctx->visits.p;
+        sf.tf = zero_tile_flags(ctx, ctx->tflags, S.er, S.ec);
+        S.tf = sf.tf;
+        bool fused_ran = false;
+        for (int k = 0; k < S.nc; ++k) {
+            const int h = S.cand_h[k];
+            const tmk::GridDesc g = strip_of(make_grid(S.er, S.ec, h, h), S.rank, S.world);
+            const bool is_pred = h == S.pred && !fused_ran;
+            ctx->egs_maps[k].ensure(1);
+            // no in-kernel EGS rejection: a strip's partial count says nothing about the
+            // global one (the decision is the host's, on the allreduced counts)
+            autocorr_launch(ctx, img, ws, g, thr, nullptr, ctx->counters.p + 8 + k, nullptr,
+                            nullptr, 0.0, /*count_only=*/!is_pred, nullptr, nullptr,
+                            is_pred ? &sf : nullptr);
+            if (is_pred) fused_ran = true;
+        }
+        if (!fused_ran) invalid("tm_strip_fused_egs: the predicted size is not in the batch");
+        unsigned long long v[4] = {0, 0, 0, 0};
+        CK(cudaMemcpyAsync(v, ctx->counters.p + 8, 8 * S.nc, cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        *nc = S.nc;
+        for (int k = 0; k < S.nc; ++k) {
+            hs[k] = S.cand_h[k];
+            n_r[k] = (int64_t)v[k];
+        }
+    });
+}
+
+int tm_strip_fused_finish(tm_ctx* ctx, tm_strip_part* out) {
+    return guard(ctx, [&] {
+        auto& S = ctx->strip;
+        if (!S.active || !S.fused) invalid("tm_strip_fused_finish: no fused strip search in progress");
+        tm_image* img = S.img;
+        WS& ws = get_ws(ctx, img, S.m, S.n);
+        const tmk::GridDesc& g = S.g;
+        // survivors (dense or list on the device; the reduction packs the mapped block)
+        eval_survivors_dev(ctx, img, ws, S.T, g, nullptr, nullptr, false, nullptr, nullptr,
+                           nullptr, &S.tf);
+        CK(cudaEventRecord(ctx->ev1, ctx->s));
+        spin_wait(ctx->ev1);
+        const tm_ctx::HostRes* hr = ctx->hres;
+        tmk::CellH best = hr->cells[0];
+        if (S.policy == TM_POLICY_SEEDED && better_h(hr->cells[1], best)) best = hr->cells[1];
+        if (better_h(hr->cells[2], best)) best = hr->cells[2];
+        if (better_h(flat_cell(hr->tally), best)) best = flat_cell(hr->tally);
+        double fin = hr->thr;
+        if ((hr->cells[2].flags & 1) && !(hr->cells[2].flags & 2) && hr->cells[2].rho > fin)
+            fin = hr->cells[2].rho;
+        std::memset(out, 0, sizeof *out);
+        out->best_rho = best.rho;
+        out->best_row = best.row;
+        out->best_col = best.col;
+        out->best_flags = best.flags;
+        out->centers = (int64_t)(g.ti_hi - g.ti_lo) * g.tc;
+        out->eliminated = (int64_t)hr->tally.eliminated;
+        out->retained = (int64_t)hr->tally.retained;
         out->final_threshold = fin;
         S.active = false;
     });

@@ -198,6 +198,11 @@ def search_strips(backend, comm, prep, t, er, ec, policy="frozen", init_threshol
     if policy == "seeded":
         T = comm.allreduce_max_f64(backend.search_seed(T))
     part = backend.search_finish(T)
+    return _merge_parts(comm, part, T, policy, init_threshold, er, ec)
+
+
+def _merge_parts(comm, part, T, policy, init_threshold, er, ec):
+    """allgather of the strips' parts, merged in better_candidate order (matcher.cpp:150-153)."""
     vec = [part["best_rho"], part["best_row"], part["best_col"], part["best_flags"],
            part["centers"], part["eliminated"], part["retained"], part["final_threshold"]]
     parts = comm.allgather_f64(vec)
@@ -221,6 +226,45 @@ def search_strips(backend, comm, prep, t, er, ec, policy="frozen", init_threshol
                        er, ec)
 
 
+def _egs_accepts(er, ec, cands, counts, xi, cap=127):
+    """egs.cpp:61-88 on the allreduced counts of one candidate batch: (accepted h, complete)
+    -- complete = False when every candidate was accepted and larger sizes could follow."""
+    if cap % 2 == 0:
+        cap += 1
+    prev, acc = math.inf, None
+    for h, n_r in zip(cands, counts):
+        cost = total_cost(er, ec, h, h, n_r)["total"]
+        if math.isfinite(prev) and not (prev - cost > xi * prev):
+            return acc, True
+        acc, prev = h, cost
+        if (h >= er and h >= ec) or h >= cap:
+            return acc, True
+    return acc, False
+
+
+def search_strips_fused(backend, comm, t, er, ec, policy, init_threshold, h0, xi, seed_margin):
+    """The fused strip protocol (tm_strip_fused_*): 4 host round trips, scan 2 inside the
+    predicted size's R_co.  Returns None when it does not apply or the prediction missed
+    (the caller runs the classic protocol)."""
+    pred = getattr(backend, "predicted", None) or h0
+    ok, T0 = backend.fused_begin(t, comm.rank, comm.world, policy, init_threshold, pred,
+                                 seed_margin)
+    (ok_all,) = comm.allreduce_sum_i64([int(ok)])
+    if ok_all != comm.world:
+        return None
+    T = comm.allreduce_max_f64(T0)
+    if policy == "seeded":
+        T = comm.allreduce_max_f64(backend.fused_seed(T))
+    cands, local = backend.fused_egs(T)
+    counts = comm.allreduce_sum_i64(local)
+    acc, complete = _egs_accepts(er, ec, cands, counts, xi)
+    backend.predicted = acc if acc else pred
+    if not complete or acc != pred:
+        return None  # misprediction: the classic protocol on the accepted grid
+    part = backend.fused_finish()
+    return _merge_parts(comm, part, T, policy, init_threshold, er, ec)
+
+
 def match_strips(backend, comm, t, image_shape, mode="egs", policy="frozen", init_threshold=None,
                  h0=3, w0=3, rho_th=0.8, xi_fraction=0.005, seed_margin=0.02):
     """match() (matcher.cpp:278-307) with the grid rows split over the process group."""
@@ -233,6 +277,12 @@ def match_strips(backend, comm, t, image_shape, mode="egs", policy="frozen", ini
         r0, r1 = noise_rows(p, comm.rank, comm.world)
         (q_total,) = comm.allreduce_sum_i64([backend.sum_sq(r0, r1)])
         backend.set_noise(q_total)
+    if (mode == "egs" and h0 == w0 and policy in ("frozen", "seeded") and rho_th == 0.8 and
+            hasattr(backend, "fused_begin")):
+        res = search_strips_fused(backend, comm, t, er, ec, policy, init_threshold, h0,
+                                  xi_fraction, seed_margin)
+        if res is not None:
+            return res
     if mode == "egs":
         h, w, trace, slot = egs_strips(backend, comm, p, q, m, n, h0, w0, rho_th, xi_fraction)
         prep = backend.commit(m, n, slot, h, w, trace)
@@ -369,6 +419,38 @@ class DeviceBackend:
             self.ctx.h, prep, self.img.h, self._t.ctypes.data_as(C.POINTER(C.c_double)),
             C.byref(p), rank, world, C.byref(T0)))
         return T0.value
+
+    def fused_begin(self, t, rank, world, policy, init_threshold, pred, seed_margin):
+        from .api import make_params
+        if self.strip_local and pred + 2 > self.hold:  # the batch's largest candidate
+            self.rank, self.world = rank, world
+            self._extend(pred + 2)
+        self._t = np.ascontiguousarray(t, dtype=np.float64)
+        p = make_params(policy=policy, init_threshold=init_threshold, seed_margin=seed_margin,
+                        parallel=True, threads=2)
+        ok, T0 = C.c_int(), C.c_double()
+        N.check(N.lib().tm_strip_fused_begin(
+            self.ctx.h, self.img.h, self._t.ctypes.data_as(C.POINTER(C.c_double)),
+            self._t.shape[0], self._t.shape[1], C.byref(p), rank, world, pred, C.byref(ok),
+            C.byref(T0)))
+        return bool(ok.value), T0.value
+
+    def fused_seed(self, T):
+        T1 = C.c_double()
+        N.check(N.lib().tm_strip_fused_seed(self.ctx.h, C.c_double(T), C.byref(T1)))
+        return T1.value
+
+    def fused_egs(self, T):
+        nc = C.c_int()
+        hs = (C.c_int * 4)()
+        nr = (C.c_int64 * 4)()
+        N.check(N.lib().tm_strip_fused_egs(self.ctx.h, C.c_double(T), C.byref(nc), hs, nr))
+        return [hs[k] for k in range(nc.value)], [nr[k] for k in range(nc.value)]
+
+    def fused_finish(self):
+        part = StripPart()
+        N.check(N.lib().tm_strip_fused_finish(self.ctx.h, C.byref(part)))
+        return {k: getattr(part, k) for k, _ in StripPart._fields_ if not k.startswith("_")}
 
     def search_seed(self, T):
         T1 = C.c_double()

@@ -172,6 +172,13 @@ SIGNATURES = {
     "tm_strip_search_begin": (C.c_int, [_P, _P, _P, _D, C.POINTER(MatchParams), C.c_int, C.c_int,
                                         _D]),
     "tm_strip_search_seed": (C.c_int, [_P, C.c_double, _D]),
+    "tm_strip_fused_begin": (C.c_int, [_P, _P, _D, C.c_int, C.c_int, C.POINTER(MatchParams),
+                                       C.c_int, C.c_int, C.c_int, C.POINTER(C.c_int),
+                                       C.POINTER(C.c_double)]),
+    "tm_strip_fused_seed": (C.c_int, [_P, C.c_double, C.POINTER(C.c_double)]),
+    "tm_strip_fused_egs": (C.c_int, [_P, C.c_double, C.POINTER(C.c_int), C.POINTER(C.c_int),
+                                     C.POINTER(C.c_int64)]),
+    "tm_strip_fused_finish": (C.c_int, [_P, C.POINTER(StripPart)]),
     "tm_strip_search_finish": (C.c_int, [_P, C.c_double, C.POINTER(StripPart)]),
 }
 
