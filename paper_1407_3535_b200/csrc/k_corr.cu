@@ -688,6 +688,16 @@ __global__ void __launch_bounds__(256)
 // lanes of a warp read a few consecutive groups of one plane); visit codes go to plane k
 // (the dense pass's mask); survivor lists are warp-aggregated (one atomic per warp and
 // template that has survivors).
+// The exact FP64 bound test of k_sec_rows (inside the fast test's margin; rare): out of
+// line so the unrolled template loop stays small.
+__device__ __noinline__ bool sec_exact_multi(const SecMulti& sm, int k, size_t gk, double b,
+                                             double x) {
+    const double T = sm.thr[k];
+    const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+    const double a = dclamp(sm.rho_c[gk], -1.0, 1.0);
+    return tb >= __dadd_rn(__dmul_rn(a, b), __dmul_rn(sm.sa_c[gk], __dsqrt_rn(x)));
+}
+
 template <int KP>
 __global__ void __launch_bounds__(256)
     k_sec_rows_multi(Grid g, const double* __restrict__ map, const uint8_t* __restrict__ flat,
@@ -736,71 +746,61 @@ __global__ void __launch_bounds__(256)
             float2 rec[KP];
 #pragma unroll
             for (int k = 0; k < KP; ++k)
-                rec[k] = k < sm.K ? __ldg(sm.rec + size_t(k) * sm.G + gi) : make_float2(0.f, -1.f);
+                rec[k] = k < sm.K ? __ldg(sm.rec + size_t(k) * sm.G + gi) : make_float2(0.f, -2.f);
+            unsigned smask = 0u, fmask = 0u;  // survivors / kept flat members, bit k
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
                 if (k >= sm.K) break;
-                const size_t gk = size_t(k) * sm.G + gi;
-                uint8_t vis = 0;  // centres
-                bool survivor = false, flat_kept = false;
-                if (member) {
-                    vis = 2;
-                    if (rec[k].y != -2.f) {  // (a seeded group: its members were evaluated already)
-                        bool elim = ((thr_ok >> k) & 1u) && !fv && rec[k].y >= 0.f;
-                        if (elim) {
-                            // FP32 bound with a 4e-6 margin (every input an exactly rounded
-                            // value in [-1, 1], x in FP64 before its square root: error <
-                            // 1e-6); the exact FP64 test of k_sec_rows inside it
-                            const float f = fmaf(rec[k].x, bf, rec[k].y * sq);
-                            if (tbf[k] >= f + 4e-6f) {
-                                elim = true;
-                            } else if (tbf[k] < f - 4e-6f) {
-                                elim = false;
-                            } else {
-                                const double T = sm.thr[k];
-                                const double tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
-                                const double a = dclamp(sm.rho_c[gk], -1.0, 1.0);
-                                elim = tb >= __dadd_rn(__dmul_rn(a, b),
-                                                       __dmul_rn(sm.sa_c[gk], __dsqrt_rn(x)));
-                            }
-                        }
-                        if (elim) {
-                            vis = 1;
-                            ++n_elim[k];
-                        } else if (fv) {
-                            flat_kept = true;  // rho 0 without a dot: first position kept
-                        } else {
-                            survivor = true;
-                            if (sm.tf.p)
-                                mark_tile(TileFlags{sm.tf.p + size_t(k) * sm.tf_stride,
-                                                    sm.tf.cols}, r, c);
-                        }
+                // member: seeded group -> kept (evaluated already); else eliminated iff the
+                // bound holds (FP32 with a 4e-6 margin, FP64 inside it); kept flat members
+                // are not listed (rho 0 without a dot)
+                uint8_t vis = member ? 2 : 0;
+                if (member && rec[k].y != -2.f && !fv && rec[k].y >= 0.f && ((thr_ok >> k) & 1u)) {
+                    const float f = fmaf(rec[k].x, bf, rec[k].y * sq);
+                    const bool el = tbf[k] >= f + 4e-6f ||
+                                    (tbf[k] >= f - 4e-6f &&
+                                     sec_exact_multi(sm, k, size_t(k) * sm.G + gi, b, x));
+                    if (el) {
+                        vis = 1;
+                        ++n_elim[k];
                     }
+                }
+                if (vis == 2 && rec[k].y != -2.f) {
+                    if (fv) fmask |= 1u << k;
+                    else smask |= 1u << k;
                 }
                 if (in && sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
-                const unsigned bf2 = __ballot_sync(0xffffffffu, flat_kept);
-                if (bf2) {
-                    const unsigned long long fk = warp_max_u64(flat_kept ? flat_member_key(r, c) : 0ull);
-                    if (lane == 0) {
-                        atomicAdd(&s_flat[k], (unsigned long long)__popc(bf2));
-                        atomicMax(&s_fkey[k], fk);
+            }
+            if (__any_sync(0xffffffffu, (smask | fmask) != 0u)) {  // warp-uniform, rare
+#pragma unroll 1
+                for (int k = 0; k < sm.K; ++k) {
+                    const bool fk = (fmask >> k) & 1u, sk = (smask >> k) & 1u;
+                    const unsigned bfl = __ballot_sync(0xffffffffu, fk);
+                    if (bfl) {
+                        const unsigned long long key =
+                            warp_max_u64(fk ? flat_member_key(r, c) : 0ull);
+                        if (lane == 0) {
+                            atomicAdd(&s_flat[k], (unsigned long long)__popc(bfl));
+                            atomicMax(&s_fkey[k], key);
+                        }
                     }
-                }
-                const unsigned ball = __ballot_sync(0xffffffffu, survivor);
-                if (ball) {
+                    const unsigned ball = __ballot_sync(0xffffffffu, sk);
+                    if (!ball) continue;
+                    if (sk && sm.tf.p)
+                        mark_tile(TileFlags{sm.tf.p + size_t(k) * sm.tf_stride, sm.tf.cols}, r, c);
                     if ((full >> k) & 1u) {
                         if (lane == 0) atomicAdd(&s_surv[k], (unsigned long long)__popc(ball));
-                    } else {
-                        unsigned long long base = 0;
-                        if (lane == 0)
-                            base = atomicAdd(&sm.tally[k].survivors, (unsigned long long)__popc(ball));
-                        base = __shfl_sync(0xffffffffu, base, 0);
-                        if (survivor) {
-                            const unsigned long long pos = base + __popc(ball & ((1u << lane) - 1));
-                            if (pos < sm.cap) sm.locs[size_t(k) * sm.cap + pos] = make_int2(r, c);
-                        }
-                        if (base + __popc(ball) >= sm.cap) full |= 1u << k;
+                        continue;
                     }
+                    unsigned long long base = 0;
+                    if (lane == 0)
+                        base = atomicAdd(&sm.tally[k].survivors, (unsigned long long)__popc(ball));
+                    base = __shfl_sync(0xffffffffu, base, 0);
+                    if (sk) {
+                        const unsigned long long pos = base + __popc(ball & ((1u << lane) - 1));
+                        if (pos < sm.cap) sm.locs[size_t(k) * sm.cap + pos] = make_int2(r, c);
+                    }
+                    if (base + __popc(ball) >= sm.cap) full |= 1u << k;
                 }
             }
         }
