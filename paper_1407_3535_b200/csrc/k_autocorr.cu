@@ -1578,13 +1578,17 @@ AcgGeom acg_geom(int m, int n, GridDesc gd, int nt, int resident = 0) {
 // CTA size per group size: 256 threads for h = 3 (2 CTAs/SM, 9% halo threads at n = 64);
 // 128 for h = 5 (its 25 sliding sums + rings cap 256-thread CTAs at one per SM).
 // TMATCH_ACG_THREADS=128|256 forces one size for both (A/B measurements).
-int acg_threads(int h = 3) {
+int acg_threads(const GridDesc& gd) {
     static int forced = [] {
         const char* e = std::getenv("TMATCH_ACG_THREADS");
         const int v = e ? std::atoi(e) : 0;
         return (v == 128 || v == 256) ? v : 0;
     }();
-    return forced ? forced : (h >= 5 ? 128 : 256);
+    if (forced) return forced;
+    // h = 3: 256-thread CTAs on C2-sized extents, 128 on large ones (C5: 4.60 -> 4.47 ms;
+    // C2: 73 -> 79 us with 128)
+    const bool large = double(gd.er) * double(gd.ec) > 3.2e7;
+    return gd.h >= 5 || large ? 128 : 256;
 }
 
 bool acg_enabled() {
@@ -1693,7 +1697,7 @@ cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, Grid
                        DevStats st, double thr, double* map, unsigned long long* n_r, int* stop,
                        const double* egs_prev, double egs_central, double egs_xi, cudaStream_t s,
                        const EgsDecide& dec, const SecFuse& sf) {
-    if (acg_threads(H) == 128)
+    if (acg_threads(gd) == 128)
         return launch_acg_np<H, 128>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
                                      egs_central, egs_xi, s, dec, sf);
     return launch_acg_np<H, 256>(imgp, pitch, q, m, n, gd, st, thr, map, n_r, stop, egs_prev,
@@ -1987,7 +1991,7 @@ cudaError_t egs_decide(const unsigned long long* n_r, double* prev_cost, int* st
 
 bool autocorr_sec_fuse_supported(int m, int n, GridDesc g) {
     return autocorr_fused_supported(m, n, g) && acg_enabled() && (g.h == 3 || g.h == 5) &&
-           g.h == g.w && acg_geom(m, n, g, acg_threads(g.h)).nt > 0;
+           g.h == g.w && acg_geom(m, n, g, acg_threads(g)).nt > 0;
 }
 
 bool autocorr_fused_supported(int m, int n, GridDesc g) {
@@ -1996,7 +2000,7 @@ bool autocorr_fused_supported(int m, int n, GridDesc g) {
     return u32_cross_exact(m, n) && g.h % 2 == 1 && g.h / 2 <= kU8PadRows && g.h <= 11 &&
            (p + kU8PadRows) * q < (size_t(1) << 31) &&
            size_t(g.er) * g.ec < (size_t(1) << 32) &&
-           (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads(g.h)).nt > 0);
+           (acf_geom(m, n, g).ny > 0 || acg_geom(m, n, g, acg_threads(g)).nt > 0);
 }
 
 cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, GridDesc gd,
@@ -2006,7 +2010,7 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               const uint8_t* imgp, int pitch, const EgsDecide* dec,
                               bool* decided, const SecFuse* fuse) {
     if (decided) *decided = false;
-    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd.h)).nt > 0 &&
+    if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd)).nt > 0 &&
         (gd.h == 3 || gd.h == 5)) {
         // the EGS decision rides on the launch's tail (no k_egs_decide launch)
         const EgsDecide d = dec ? *dec : EgsDecide{};
