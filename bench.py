@@ -318,7 +318,7 @@ def run_reference(args):
 
 
 # ---- roofline -----------------------------------------------------------------------------
-def roofline(phases, wl, res, pk):
+def roofline(phases, wl, res, pk, fp64_search=False):
     """Per-phase achieved vs peak; the dominant phase (largest device time) is the headline
     roofline.  Algorithmic amounts per launch group:
       window_stats   p*q + 17 B per extent location (u8 read; mu, omega, flat written)
@@ -347,6 +347,9 @@ def roofline(phases, wl, res, pk):
         "centre_scan": ("tensor", 2.0 * m * n * G,
                         "k_tc_build_b + k_tc_corr<1> + k_centre_epi (tcgen05 kind::i8)"),
     }
+    if fp64_search:  # OptA with kappa > 0: the search image is non-integer (FP64 replica
+        defs.pop("centre_scan")  # kernels, no tensor-core / i8 roofline)
+        defs.pop("window_stats")
     rows = []
     for name, v in phases.items():
         per_launch = v["ms"] / max(v["count"], 1)
@@ -565,7 +568,8 @@ def run_b200(args):
             sample_parity = {"checked": True, "templates": len(gres),
                              "fields": sorted(res_fields(gres[0]))}
     pk = peaks()
-    head, rows = roofline(phases, wl, res[0], pk)
+    head, rows = roofline(phases, wl, res[0], pk,
+                          fp64_search=wl.mode == "opta" and info["kappa"] > 0)
     traffic = None
     tr = _json(os.path.join(ROOT, "profiles", "r02_kernel_traffic.json")) or {}
     if head and head.get("phase") in tr.get("phases", {}):

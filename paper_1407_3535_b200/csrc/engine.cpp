@@ -273,6 +273,7 @@ struct tm_ctx {
     DBuf<double> egs_maps[4];
     DBuf<double> sa_c;  // per-group half_gap factor sqrt(1 - rho_c^2) (scan 2)
     bool sa_ready = false;  // sa_c filled by this search's centre epilogue
+    float2* batch_rec = nullptr;  // run_batch: the centre epilogue also writes the records
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
     // row-strip search protocol state (tm_strip_search_*)
     struct StripState {
@@ -1042,7 +1043,7 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             const tmk::TailReduce tail = tail_to(ctx, n1 + n2, 0, op);  // n2 = 0 here
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
-                                    task.c_last, &tail, nullptr, ctx->sa_c.p));
+                                    task.c_last, &tail, nullptr, ctx->sa_c.p, ctx->batch_rec));
             HT("centre_epi");
             ctx->add(1);
         }
@@ -2800,11 +2801,16 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
     B.locs.ensure(size_t(K) * cap);
     B.packed.ensure(size_t(K));
 
-    // 1. scan 1 (+ seeding) per template
+    // 1. scan 1 (+ seeding) per template; the tensor-core centre epilogue writes the
+    //    template's batch records directly, the seeding marks its seeded groups in them
     for (int k = 0; k < K; ++k) {
         const Tmpl& T = Ts[k];
         const tmk::ReduceOp op_init = centre_op(ctx, P);
+        float2* recs = B.rec.p + size_t(k) * G;
+        ctx->batch_rec = recs;
         centre_scan(ctx, simg, ws, T, g, &op_init);
+        ctx->batch_rec = nullptr;
+        const bool recs_written = ctx->sa_ready;  // (the tensor-core epilogue ran)
         if (!ctx->sa_ready) {  // (the tensor-core epilogue writes it; keep the invariant)
             CK(tmk::sqrt_gap(ctx->rho_c.p, ctx->sa_c.p, G, s));
             ctx->add(1);
@@ -2816,7 +2822,8 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
             ctx->seeded.ensure(G);
             CK(tmk::seed_members(g, ctx->rho_c.p, ctx->deg_c.p, ctx->thr.p, P.seed_margin,
                                  ctx->seeded.p, ctx->seed_locs.p, ctx->counters.p + 4, max_locs,
-                                 ctx->counters.p + 5, max_groups, s));
+                                 ctx->counters.p + 5, max_groups, s,
+                                 recs_written ? recs : nullptr));
             ctx->add(1);
             tmk::ReduceOp op_raise{};
             op_raise.kind = 2;
@@ -2826,9 +2833,11 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
         }
         CK(cudaMemcpyAsync(B.rho.p + size_t(k) * G, ctx->rho_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(B.sa.p + size_t(k) * G, ctx->sa_c.p, G * 8, cudaMemcpyDeviceToDevice, s));
-        CK(tmk::batch_records(ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p,
-                              seeded_pol ? ctx->seeded.p : nullptr, G, B.rec.p + size_t(k) * G, s));
-        ctx->add(1);
+        if (!recs_written) {
+            CK(tmk::batch_records(ctx->rho_c.p, ctx->sa_c.p, ctx->deg_c.p,
+                                  seeded_pol ? ctx->seeded.p : nullptr, G, recs, s));
+            ctx->add(1);
+        }
         CK(cudaMemcpyAsync(B.thr.p + k, ctx->thr.p, 8, cudaMemcpyDeviceToDevice, s));
         CK(cudaMemcpyAsync(B.cells.p + 3 * k, ctx->cells.p, 2 * sizeof(tmk::CellH),
                            cudaMemcpyDeviceToDevice, s));

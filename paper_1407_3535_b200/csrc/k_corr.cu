@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
                  CellH* partials, int c_last, TailReduce tail, const int* __restrict__ gate,
-                 double* __restrict__ sa_out) {
+                 double* __restrict__ sa_out, float2* __restrict__ rec_out) {
     pdl_wait();
     if (gate && !*gate) return;  // speculative launch not confirmed (every block: no ticket)
     __shared__ Cell scratch[8];
@@ -228,9 +228,12 @@ __global__ void __launch_bounds__(256)
         const bool deg = ts.flat || wflat;
         rho_c[gi] = rho;
         deg_c[gi] = deg;
-        if (sa_out) {  // scan 2's centre half-gap factor (k_sqrt_gap, bounds.cpp:21-23)
+        if (sa_out || rec_out) {  // scan 2's centre half-gap factor (k_sqrt_gap, bounds.cpp:21-23)
             const double a = dclamp(rho, -1.0, 1.0);
-            sa_out[gi] = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(a, a))));
+            const double sa = __dsqrt_rn(dmax(0.0, __dsub_rn(1.0, __dmul_rn(a, a))));
+            if (sa_out) sa_out[gi] = sa;
+            // a template batch's record (k_sec_rows_multi): -1 marks a degenerate centre
+            if (rec_out) rec_out[gi] = make_float2(float(a), deg ? -1.f : float(sa));
         }
         const Cell cand = make_cell(r, c, rho, deg);
         if (better(cand, best)) best = cand;
@@ -869,7 +872,8 @@ __global__ void k_seed_members(Grid g, const double* __restrict__ rho_c,
                                const uint8_t* __restrict__ deg_c, const double* thr,
                                double margin, uint8_t* seeded, int2* locs,
                                unsigned long long* count, unsigned long long max_locs,
-                               unsigned long long* n_groups, unsigned long long max_groups) {
+                               unsigned long long* n_groups, unsigned long long max_groups,
+                               float2* rec) {
     pdl_wait();
     const long long G = (long long)g.ti_hi * g.tc;
     const double T = *thr;
@@ -887,6 +891,7 @@ __global__ void k_seed_members(Grid g, const double* __restrict__ rho_c,
         const unsigned long long pos = atomicAdd(count, nm);
         if (pos + nm > max_locs) continue;
         seeded[gi] = 1;
+        if (rec) rec[gi].y = -2.f;  // a template batch's record: a seeded group
         unsigned long long o = pos;
         for (int r = r0; r <= r1; ++r)
             for (int c = c0; c <= c1; ++c)
@@ -1066,10 +1071,11 @@ __global__ void k_scatter_column(const double* rho, const uint8_t* deg, int n, i
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last,
-                            const TailReduce* tail, const int* gate, double* sa_out) {
+                            const TailReduce* tail, const int* gate, double* sa_out,
+                            float2* rec_out) {
     launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw,
                nc, col0, dot, rho_c, deg_c, partials, c_last, tail ? *tail : TailReduce{}, gate,
-               sa_out);
+               sa_out, rec_out);
     return cudaGetLastError();
 }
 
@@ -1164,11 +1170,11 @@ cudaError_t threshold_raise(const CellH* best, double* thr, cudaStream_t s) {
 cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, const double* thr,
                          double margin, uint8_t* seeded, int2* locs, unsigned long long* count,
                          unsigned long long max_locs, unsigned long long* n_groups,
-                         unsigned long long max_groups, cudaStream_t s) {
+                         unsigned long long max_groups, cudaStream_t s, float2* rec) {
     const long long G = (long long)g.tr * g.tc;
     const int blocks = int(std::min<long long>((G + 255) / 256, 148 * 8));
     launch_pdl(k_seed_members, dim3(blocks), dim3(256), 0, s, to_grid(g), rho_c, deg_c, thr, margin, seeded, locs, count,
-                                          max_locs, n_groups, max_groups);
+                                          max_locs, n_groups, max_groups, rec);
     return cudaGetLastError();
 }
 

@@ -364,7 +364,8 @@ cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last = -1,
                             const TailReduce* tail = nullptr, const int* gate = nullptr,
-                            double* sa_out = nullptr);
+                            double* sa_out = nullptr,
+                            float2* rec_out = nullptr);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
@@ -404,7 +405,8 @@ cudaError_t threshold_init(const CellH* centre_best, int has_init, double init, 
 cudaError_t seed_members(GridDesc g, const double* rho_c, const uint8_t* deg_c, const double* thr,
                          double margin, uint8_t* seeded, int2* locs, unsigned long long* count,
                          unsigned long long max_locs, unsigned long long* n_groups,
-                         unsigned long long max_groups, cudaStream_t s);
+                         unsigned long long max_groups, cudaStream_t s,
+                         float2* rec = nullptr);
 cudaError_t threshold_raise(const CellH* best, double* thr, cudaStream_t s);
 // Sequential policy replay: candidates = scan-2 survivors at T0 with their rho.
 // rho: extent-sized, indexed by location.
