@@ -903,6 +903,11 @@ __device__ __forceinline__ void egs_tail(const EgsDecide& d) {
     }
 }
 
+__device__ __forceinline__ float rcp_approx(float x) {
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return r;
+}
 __device__ __forceinline__ float sqrt_approx(float x) {
     float r;
     asm("sqrt.approx.f32 %0, %1;" : "=f"(r) : "f"(x));
@@ -928,7 +933,7 @@ __device__ __forceinline__ float sqrt_approx(float x) {
 // are copied with 16-byte cp.async one event ahead, so the walk reads bytes at shared-
 // memory latency instead of waiting on L2 for the trailing rows m rows back.  `img` is the
 // 16-byte-pitched zero-padded copy (pitch P, >= p + kU8PadRows rows).
-constexpr int kAcgWb = 8;  // warp-total stride (NT <= 256)
+constexpr int kAcgWb = 8;  // warp-total stride (NT <= 256, read as uint4: NT % 128 == 0)
 // staged bytes per ring row: NT*W tile columns + 2*(h/2) for the B offsets + 16-byte alignment
 // (+8: the packed walk reads two aligned words from up to 3 bytes before a thread's columns)
 __host__ __device__ constexpr int acg_span(int nt, int h) { return (15 + nt * h + 2 * (h / 2) + 8 + 15) & ~15; }
@@ -957,6 +962,7 @@ __global__ void __launch_bounds__(NT)
           double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
           int seg, int RR, int* __restrict__ stop, const double* __restrict__ egs_prev,
           double egs_central, double egs_xi, EgsDecide dec, SecFuse sf, int tile_base) {
+    static_assert(NT % 128 == 0 && NT <= 32 * kAcgWb, "warp totals are read as uint4");
     pdl_wait();
     constexpr int W = H, hr = H / 2;
     constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
@@ -1369,8 +1375,17 @@ __global__ void __launch_bounds__(NT)
                 if (hi > t) {
                     S = Ld[i1];
                     if (t > 0) S -= Ld[t - 1];
-#pragma unroll 1
-                    for (int x = w0; x < w1; ++x) S += wb[d * kAcgWb + x];
+                    // + the warp totals of warps [w0, w1): vector reads, predicated adds
+                    const uint4* wq = reinterpret_cast<const uint4*>(wb + d * kAcgWb);
+#pragma unroll
+                    for (int v = 0; v < NT / 128; ++v) {
+                        const uint4 x = wq[v];
+                        const unsigned span = unsigned(w1 - w0);
+                        S += unsigned(4 * v + 0 - w0) < span ? x.x : 0u;
+                        S += unsigned(4 * v + 1 - w0) < span ? x.y : 0u;
+                        S += unsigned(4 * v + 2 - w0) < span ? x.z : 0u;
+                        S += unsigned(4 * v + 3 - w0) < span ? x.w : 0u;
+                    }
                 }
                 if (has_head) S += (clipped ? Hc : Hh)[d * NT + hi];
                 if (clipped) S += Tt[d * NT + t - 1];
@@ -1389,15 +1404,15 @@ __global__ void __launch_bounds__(NT)
                 }
                 if constexpr (FUSE) {  // retained count + scan 2 (matcher.cpp:48-78)
                     // R_co = clamp(RN(num / den)) is needed exactly only near a decision:
-                    // the FP32 quotient qf (num, den rounded to FP32, one FP32 division:
-                    // relative error < 2e-7) decides the retained test (R_co < thr) and the
+                    // the FP32 quotient qf (num, den rounded to FP32, times the approximate
+                    // reciprocal: relative error < 5 * 2^-24 < 3e-7) decides the retained test (R_co < thr) and the
                     // bound test outside margins that cover that error; the FP64 quotient
                     // is formed only inside them (or near |R_co| = 1, where the bound's
                     // slope in R_co is unbounded).
                     float qf = 0.f;
                     bool fast = !flat;
                     if (fast) {
-                        qf = __fdiv_rn(float(num), float(den));
+                        qf = __fmul_rn(float(num), rcp_approx(float(den)));  // rel. error < 3e-7
                         fast = fabsf(qf) < 0.99f;
                     }
                     double val = 0.0;
@@ -1430,7 +1445,7 @@ __global__ void __launch_bounds__(NT)
                             // (inputs exactly rounded values in [-1, 1], x = 1 - b^2 formed
                             // before its square root: < 1e-6 with the exact b; with the FP32
                             // quotient for b, |dbound/db| <= 1 + 0.99 / sqrt(1 - 0.99^2) < 8
-                            // adds < 2e-6), the exact FP64 test of k_sec_rows inside it
+                            // adds < 8 * 3e-7 < 2.5e-6), the exact FP64 test of k_sec_rows inside it
                             const float b = have_val ? float(val) : qf;
                             const float x = have_val ? float(fma(-val, val, 1.0))
                                                      : fmaf(-qf, qf, 1.0f);

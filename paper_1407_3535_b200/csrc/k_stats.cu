@@ -768,11 +768,16 @@ __global__ void __launch_bounds__(NT)
 #pragma unroll
             for (int j = 0; j < W; ++j) {
                 // + warp totals between this warp and the warp holding PC(c + n + j)
+                // (n + W <= 128 + W: at most two warps in between -- predicated, no loop;
+                // wts has NW + 1 slots so both reads stay inside)
                 const int wj = (idx + j) >> TSH;
                 unsigned S = hs[j] - own_s[j], Qs = hq[j] - own_q[j];
-                for (int w = wid; w < wj; ++w) {
-                    S += wts[par][w];
-                    Qs += wtq[par][w];
+#pragma unroll
+                for (int u = 0; u < 2; ++u) {
+                    const int w = min(wid + u, NW);
+                    const unsigned xs = wts[par][w], xq = wtq[par][w];
+                    S += wid + u < wj ? xs : 0u;
+                    Qs += wid + u < wj ? xq : 0u;
                 }
                 double mu, om;
                 uint8_t fl;
