@@ -1719,6 +1719,700 @@ cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, Grid
                                  egs_central, egs_xi, s, dec, sf);
 }
 
+// ---- R_co of 3x3 groups in two passes: exact cross sums (k_rco3_s), then the per-member
+// epilogue as a streaming pass (k_rco_epi) ---------------------------------------------------
+//
+// Pass 1, k_rco3_s: thread = one regular group column k (centre column cc = 3k+1) and ALL
+// nine offsets (di, dj) of its group, so an image row is loaded once for the nine cross sums
+// (the k_acg design runs one CTA per dj).  A row step of the vertical walk needs the bytes
+// I(x, 3k .. 3k+4) of one new row: they are packed as three words (the three dj shifts of
+// the group's three columns, fourth byte zero) and every offset's column-block sum is ONE
+// dp4a per row step (u8 x u8 -> u32, exact; leading and trailing rows in separate
+// accumulators since dp4a only adds); with n % 3 = R != 0 a second dp4a per offset sums the
+// first R columns ("head").  A's word of row x is B's dj = 0 word of row x, so the two-row
+// register ring of B words serves both sides.  Rows come straight from L2/HBM into
+// registers one event ahead (no shared-memory ring, no m-row staging).  At each event
+// (centre row) one warp scan per offset, warp totals in shared memory, and each thread forms
+// its window sums S = whole blocks [t, t+Q) + head of block t+Q -- exactly the autocorr.cpp
+// :77-83 cross sums -- and stores the eight members' S (u32, exact: m*n*255^2 < 2^32) in the
+// E-sized raster `Sout`.  The clipped last group column (ec % 3 != 0) is not walked here
+// (k_rco3_clip sums its few members directly).
+//
+// Pass 2, k_rco_epi<MODE>: thread = one extent location, rows grid-strided: the FP64
+// epilogue of autocorr.cpp:84-88 from S and the window statistics (the same operations as
+// k_acg), then the retained count (egs.cpp:12-25), and by MODE: 0 count only, 1 the R_co map,
+// 2 scan 2 fused (SecFuse: bound test, visit codes, tallies, survivor list -- the k_acg FUSE
+// epilogue).  Every load is coalesced along the row; the EGS decision rides on its tail.
+
+template <int NT, bool HEAD>
+__global__ void __launch_bounds__(NT, 512 / NT)
+    k_rco3_s(const uint8_t* __restrict__ img, int P, int m, int n, Grid g,
+             unsigned* __restrict__ Sout, int G, int seg, int tc_reg, const int* __restrict__ stop) {
+    constexpr int NW = NT / 32;
+    __shared__ unsigned Lb[2][9][NT];               // inclusive warp prefixes of the block sums
+    __shared__ unsigned Hb[2][HEAD ? 9 : 1][NT];    // head sums (first R columns of a block)
+    __shared__ unsigned Wb[2][9][NW + 2];           // warp totals (+ 2 pad slots)
+    pdl_wait();
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int k0 = int(blockIdx.x) * G;
+    const int ti0 = g.ti_lo + int(blockIdx.y) * seg;
+    const int ti1 = min(ti0 + seg, g.ti_hi);
+    if ((stop && *reinterpret_cast<const volatile int*>(stop)) || ti0 >= ti1 || k0 >= tc_reg)
+        return;  // uniform, before any barrier
+    const int k = k0 + t;
+    const int Q = n / 3, R = n - 3 * Q;
+    const unsigned hmask = R == 1 ? 0xffu : 0xffffu;  // A bytes of the head columns
+    const int sh = (3 * k) & 3;
+    const uint8_t* colp = img + ((3 * k) & ~3);
+    // B words of one row: bytes I(x, 3k+j+1+dj), j < 3, for dj = -1, 0, +1 (byte 3 zero)
+    auto ldrow = [&](int x, unsigned& w0, unsigned& w1) {
+        const uint8_t* p = colp + size_t(max(x, 0)) * P;
+        w0 = __ldg(reinterpret_cast<const unsigned*>(p));
+        w1 = __ldg(reinterpret_cast<const unsigned*>(p + 4));
+    };
+    auto words = [&](unsigned w0, unsigned w1, unsigned (&o)[3]) {
+        const unsigned lo = __funnelshift_r(w0, w1, 8 * sh);
+        const unsigned b4 = (w1 >> (8 * sh)) & 0xffu;
+        o[0] = lo & 0x00ffffffu;
+        o[1] = lo >> 8;
+        o[2] = __byte_perm(lo, b4, 0x5432);
+    };
+    unsigned VL[9], VT[9], HL[HEAD ? 9 : 1], HT[HEAD ? 9 : 1];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        VL[c] = VT[c] = 0u;
+        if constexpr (HEAD) HL[c] = HT[c] = 0u;
+    }
+    unsigned LW[2][3], TW[2][3];  // B words of rows x-1, x at the lead / trail position
+    // one row step: A row x (= ring[1]'s dj = 0 word), B rows x-1, x, x+1 (ring[0], ring[1], nw)
+    auto step = [&](unsigned (&ring)[2][3], unsigned w0, unsigned w1, unsigned* Vb,
+                    unsigned* Hh) {
+        unsigned nw[3];
+        words(w0, w1, nw);
+        const unsigned a = ring[1][1];
+        const unsigned ah = a & hmask;
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            Vb[0 + dj] = __dp4a(a, ring[0][dj], Vb[0 + dj]);
+            Vb[3 + dj] = __dp4a(a, ring[1][dj], Vb[3 + dj]);
+            Vb[6 + dj] = __dp4a(a, nw[dj], Vb[6 + dj]);
+            if constexpr (HEAD) {
+                Hh[0 + dj] = __dp4a(ah, ring[0][dj], Hh[0 + dj]);
+                Hh[3 + dj] = __dp4a(ah, ring[1][dj], Hh[3 + dj]);
+                Hh[6 + dj] = __dp4a(ah, nw[dj], Hh[6 + dj]);
+            }
+        }
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            ring[0][dj] = ring[1][dj];
+            ring[1][dj] = nw[dj];
+        }
+    };
+    int cr = g.center_row(ti0);
+    {
+        unsigned w0, w1;
+        ldrow(cr - 1, w0, w1);
+        words(w0, w1, LW[0]);
+        ldrow(cr, w0, w1);
+        words(w0, w1, LW[1]);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            TW[0][j] = LW[0][j];
+            TW[1][j] = LW[1][j];
+        }
+        // warm-up: the m lead rows [cr, cr + m), loads three rows ahead
+        unsigned pw[3][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ldrow(cr + 1 + i, pw[i][0], pw[i][1]);
+        int x = cr;
+#pragma unroll 1
+        for (; x + 3 <= cr + m; x += 3) {
+            unsigned cw[3][2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                cw[i][0] = pw[i][0];
+                cw[i][1] = pw[i][1];
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) ldrow(x + 4 + i, pw[i][0], pw[i][1]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) step(LW, cw[i][0], cw[i][1], VL, HL);
+        }
+#pragma unroll 1
+        for (; x < cr + m; ++x) {
+            unsigned w0b, w1b;
+            ldrow(x + 1, w0b, w1b);
+            step(LW, w0b, w1b, VL, HL);
+        }
+    }
+    const bool owner = t < G && k < tc_reg;
+    const int hi = t + Q;  // whole blocks [t, hi), head from block hi
+    const int whi = (hi - 1) >> 5;
+    const int cc = 3 * k + 1;
+    int par = 0;
+#pragma unroll 1
+    for (int ti = ti0;;) {
+        // loads of the next transition's rows (lead rows x+1 for x in [cr+m, crn+m), trail
+        // rows x+1 for x in [cr, crn)), one event ahead of their use
+        const bool more = ti + 1 < ti1;
+        const int crn = more ? g.center_row(ti + 1) : cr;
+        const bool regular = crn - cr == 3;
+        unsigned pl[3][2], pt[3][2];
+        if (more && regular) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                ldrow(cr + m + 1 + i, pl[i][0], pl[i][1]);
+                ldrow(cr + 1 + i, pt[i][0], pt[i][1]);
+            }
+        }
+        unsigned x[9], B[9];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) x[c] = B[c] = VL[c] - VT[c];  // exact mod 2^32
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, x[c], o);
+                if (lane >= o) x[c] += u;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            Lb[par][c][t] = x[c];
+            if constexpr (HEAD) Hb[par][c][t] = HL[c] - HT[c];
+            if (lane == 31) Wb[par][c][wid] = x[c];
+        }
+        __syncthreads();
+        if (owner) {
+            const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                if (c == 4) continue;  // the centre
+                const int di = c / 3 - 1, dj = c % 3 - 1;
+                const int r = cr + di;
+                if (r < r0 || r > r1) continue;
+                unsigned S = Lb[par][c][hi - 1] - (x[c] - B[c]);
+                const unsigned wa = Wb[par][c][wid], wb2 = Wb[par][c][wid + 1];
+                S += wid < whi ? wa : 0u;
+                S += wid + 1 < whi ? wb2 : 0u;
+                if constexpr (HEAD) S += Hb[par][c][hi];
+                Sout[unsigned(r) * unsigned(g.ec) + unsigned(cc + dj)] = S;
+            }
+        }
+        par ^= 1;
+        if (!more) break;
+        if (regular) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                step(LW, pl[i][0], pl[i][1], VL, HL);
+                step(TW, pt[i][0], pt[i][1], VT, HT);
+            }
+        } else {  // the clipped last group row: row by row
+#pragma unroll 1
+            for (int xx = cr; xx < crn; ++xx) {
+                unsigned w0, w1;
+                ldrow(xx + m + 1, w0, w1);
+                step(LW, w0, w1, VL, HL);
+                ldrow(xx + 1, w0, w1);
+                step(TW, w0, w1, VT, HT);
+            }
+        }
+        cr = crn;
+        ++ti;
+    }
+}
+
+// The clipped last group column (ec % 3 != 0: width wl = 1 or 2, centre column cc = 3*(tc-1),
+// members dj in [0, wl), di in {-1, 0, 1}): two small passes instead of a walk.
+// k_rco3_clip_rows: one warp per image row x, the row products
+//   Rp[c][x] = sum_{b<n} I(x, cc+b) * I(x+di, cc+dj+b)   (c = (di+1)*2 + dj, lanes over b);
+// k_rco3_clip_sum: one thread per (group row, member), S = sum_{a<m} Rp[c][cr+a] (exact u32).
+__global__ void __launch_bounds__(256)
+    k_rco3_clip_rows(const uint8_t* __restrict__ img, int P, int n, int cc, int x0, int nx,
+                     unsigned* __restrict__ Rp) {
+    pdl_wait();
+    const int lane = threadIdx.x & 31;
+    for (int xi = blockIdx.x * 8 + (threadIdx.x >> 5); xi < nx; xi += gridDim.x * 8) {
+        const int x = x0 + xi;
+        unsigned acc[6];
+#pragma unroll
+        for (int c = 0; c < 6; ++c) acc[c] = 0u;
+        const uint8_t* ra = img + size_t(x) * P + cc;
+        for (int b = lane; b < n; b += 32) {
+            const unsigned a = ra[b];
+#pragma unroll
+            for (int di = -1; di <= 1; ++di) {
+                const uint8_t* rb = img + size_t(max(x + di, 0)) * P + cc + b;
+                acc[(di + 1) * 2 + 0] += a * unsigned(rb[0]);
+                acc[(di + 1) * 2 + 1] += a * unsigned(rb[1]);
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 6; ++c) {
+            const unsigned v = warp_sum(acc[c]);
+            if (lane == 0) Rp[size_t(c) * nx + xi] = v;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256)
+    k_rco3_clip_sum(const unsigned* __restrict__ Rp, int m, Grid g, int cc, int wl, int x0, int nx,
+                    unsigned* __restrict__ Sout) {
+    pdl_wait();
+    const int items = (g.ti_hi - g.ti_lo) * 6;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
+        const int ti = g.ti_lo + it / 6, c = it % 6;
+        const int di = c / 2 - 1, dj = c % 2;
+        const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1, cr = (r0 + r1) >> 1;
+        const int r = cr + di;
+        if ((di == 0 && dj == 0) || dj >= wl || r < r0 || r > r1) continue;
+        const unsigned* rp = Rp + size_t(c) * nx + (cr - x0);
+        unsigned s = 0u;
+        for (int a = 0; a < m; ++a) s += rp[a];
+        Sout[unsigned(r) * unsigned(g.ec) + unsigned(cc + dj)] = s;
+    }
+}
+
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_rco_epi(Grid g, const unsigned* __restrict__ Sin, DevStats st, double mn, double thr,
+              double* __restrict__ map, unsigned long long* __restrict__ n_r, int* stop,
+              EgsDecide dec, SecFuse sf) {
+    pdl_wait();
+    {
+        __shared__ int skip;
+        if (threadIdx.x == 0) skip = stop && *reinterpret_cast<volatile int*>(stop);
+        __syncthreads();
+        if (skip) {
+            egs_tail(dec);
+            return;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+    double sec_tb = 0.0;
+    float sec_tbf = 0.f;
+    bool thr_ok = false;
+    if constexpr (MODE == 2) {
+        const double T = *sf.thr;
+        sec_tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sec_tbf = float(sec_tb);
+        thr_ok = T >= -1.0;
+    }
+    unsigned evc = 0, n_elim = 0, n_keep = 0, n_flat = 0;
+    unsigned long long fkey = 0, surv_local = 0;
+    bool list_full = false;
+    // CTA = one extent row at a time (grid-strided); thread = 4-location chunks of the linear
+    // extent index aligned to the strip's base (vector loads of S and the statistics), the
+    // row's partial edge chunks masked; the <= 2 groups a chunk touches are gathered once
+    const unsigned kb = unsigned(g.row_lo()) * unsigned(g.ec);
+    const unsigned ke = unsigned(g.row_hi()) * unsigned(g.ec);
+    const int r_lo = g.row_lo(), r_hi = g.row_hi();
+    for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const int ti = g.tile_r(r);
+        const int cr = g.center_row(ti);
+        const unsigned krow = unsigned(r) * unsigned(g.ec);          // first location of the row
+        const unsigned kcrow = unsigned(cr) * unsigned(g.ec);
+        const unsigned gbase = unsigned(ti) * unsigned(g.tc);
+        const unsigned ch0 = (krow - kb) >> 2, ch1 = (krow + g.ec - kb + 3) >> 2;
+        // whole warps per row (ballots)
+        const unsigned nthr = ((ch1 - ch0 + 31) / 32) * 32;
+        for (unsigned i = threadIdx.x; i < nthr; i += blockDim.x) {
+            const unsigned ch = ch0 + i;
+            const bool active = ch < ch1;
+            const unsigned k0 = kb + 4 * (active ? ch : ch0);
+            const int c0 = int(k0) - int(krow);  // column of element 0 (may be < 0 at the row start)
+            unsigned sv[4];
+            double mm[4], om[4];
+            uint8_t fm[4];
+            if (k0 + 4 <= ke) {
+                const uint4 s4 = *reinterpret_cast<const uint4*>(Sin + k0);
+                const double2 m01 = *reinterpret_cast<const double2*>(st.mu + k0);
+                const double2 m23 = *reinterpret_cast<const double2*>(st.mu + k0 + 2);
+                const double2 o01 = *reinterpret_cast<const double2*>(st.omega + k0);
+                const double2 o23 = *reinterpret_cast<const double2*>(st.omega + k0 + 2);
+                const unsigned f4 = *reinterpret_cast<const unsigned*>(st.flat + k0);
+                sv[0] = s4.x; sv[1] = s4.y; sv[2] = s4.z; sv[3] = s4.w;
+                mm[0] = m01.x; mm[1] = m01.y; mm[2] = m23.x; mm[3] = m23.y;
+                om[0] = o01.x; om[1] = o01.y; om[2] = o23.x; om[3] = o23.y;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) fm[j] = uint8_t(f4 >> (8 * j));
+            } else {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const unsigned kj = k0 + j < ke ? k0 + j : krow;
+                    sv[j] = Sin[kj];
+                    mm[j] = st.mu[kj];
+                    om[j] = st.omega[kj];
+                    fm[j] = st.flat[kj];
+                }
+            }
+            // the (at most two) groups of the chunk: tj0 = first in-row column / 3
+            const int cfirst = max(c0, 0);
+            const int tj0 = int(__umulhi(unsigned(cfirst), 0xAAAAAAABu) >> 1);
+            const int tj1 = min(tj0 + 1, g.tc - 1);
+            double mcg[2], ocg[2], rag[2] = {0.0, 0.0}, sag[2] = {0.0, 0.0};
+            uint8_t fcg[2], dgg[2] = {0, 0}, sdg[2] = {0, 0};
+            int ccg[2];
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+                const int tj = u ? tj1 : tj0;
+                ccg[u] = g.center_col(tj);
+                const unsigned kc = kcrow + unsigned(ccg[u]);
+                mcg[u] = __ldg(st.mu + kc);
+                ocg[u] = __ldg(st.omega + kc);
+                fcg[u] = __ldg(st.flat + kc);
+                if constexpr (MODE == 2) {
+                    const unsigned gi = gbase + unsigned(tj);
+                    rag[u] = __ldg(sf.rho_c + gi);
+                    sag[u] = __ldg(sf.sa_c + gi);
+                    dgg[u] = __ldg(sf.deg_c + gi);
+                    sdg[u] = sf.seeded ? __ldg(sf.seeded + gi) : uint8_t(0);
+                }
+            }
+            const int cnext = 3 * tj1;  // first column of the second group
+            uint8_t vis4[4] = {0, 0, 0, 0};
+            unsigned surv = 0, mine = 0;  // bit j: element j survives / belongs to this row
+            // phase 1 (branch-free over the four elements): membership, R_co's FP64 numerator
+            // and denominator, the FP32 quotient
+            unsigned memb = 0, flatm = 0, ucol = 0;
+            double num[4], den[4];
+            float qf[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                const int c = c0 + j;
+                const bool in = active && c >= 0 && c < g.ec;
+                const bool u = tj1 != tj0 && c >= cnext;  // (selects: no local-memory arrays)
+                const double mcu = u ? mcg[1] : mcg[0], ocu = u ? ocg[1] : ocg[0];
+                const bool fl = (u ? fcg[1] : fcg[0]) || fm[j];
+                const bool centre = r == cr && c == (u ? ccg[1] : ccg[0]);
+                mine |= unsigned(in) << j;
+                memb |= unsigned(in && !centre) << j;
+                flatm |= unsigned(fl) << j;
+                ucol |= unsigned(u) << j;
+                num[j] = __dsub_rn(double(sv[j]), __dmul_rn(__dmul_rn(mn, mcu), mm[j]));
+                den[j] = __dmul_rn(ocu, om[j]);
+                qf[j] = __fmul_rn(float(num[j]), rcp_approx(float(den[j])));
+            }
+            if constexpr (MODE != 2) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!((mine >> j) & 1u)) continue;
+                    const unsigned k = k0 + j;
+                    const bool flat = (flatm >> j) & 1u;
+                    if (!((memb >> j) & 1u)) {
+                        if constexpr (MODE == 1) map[k] = 1.0;  // autocorr.cpp:92-93
+                        continue;
+                    }
+                    if constexpr (MODE == 0) {
+                        if (flat ? 0.0 < thr : retained_below(num[j], den[j], thr)) ++evc;
+                    } else {
+                        const double val =
+                            flat ? 0.0 : dclamp(__ddiv_rn(num[j], den[j]), -1.0, 1.0);
+                        map[k] = val;
+                        if (val < thr) ++evc;
+                    }
+                }
+            } else {
+                // phase 2: the retained test and the scan-2 bound test of every member from
+                // the FP32 quotient with margins covering its error (see the k_acg FUSE
+                // epilogue); members whose tests fall inside a margin (or |qf| >= 0.99) take
+                // the exact FP64 path of phase 3
+                const float thr_lo = float(thr) - 1e-6f, thr_hi = float(thr) + 1e-6f;
+                unsigned slow = 0;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (!((memb >> j) & 1u)) continue;
+                    const bool flat = (flatm >> j) & 1u, u = (ucol >> j) & 1u;
+                    const bool fast = !flat && fabsf(qf[j]) < 0.99f;
+                    if (flat) {
+                        if (0.0 < thr) ++evc;
+                    } else if (fast && qf[j] < thr_lo) {
+                        ++evc;
+                    } else if (!(fast && qf[j] > thr_hi)) {
+                        slow |= 1u << j;
+                        continue;
+                    }
+                    uint8_t vis = 2;
+                    if (u ? sdg[1] : sdg[0]) {
+                        ++n_keep;
+                    } else {
+                        bool elim = thr_ok && !sf.tflat && !fm[j] && !(u ? dgg[1] : dgg[0]);
+                        if (elim) {
+                            // flat: R_co = 0 exactly (margin 4e-6), else qf (margin 1e-5)
+                            const float b = flat ? 0.f : qf[j];
+                            const float sq = sqrt_approx(fmaxf(fmaf(-b, b, 1.0f), 0.f));
+                            const float f = fmaf(float(dclamp(u ? rag[1] : rag[0], -1.0, 1.0)), b,
+                                                 float(u ? sag[1] : sag[0]) * sq);
+                            const float margin = flat ? 4e-6f : 1e-5f;
+                            if (sec_tbf >= f + margin) {
+                                elim = true;
+                            } else if (sec_tbf < f - margin) {
+                                elim = false;
+                            } else {
+                                slow |= 1u << j;
+                                continue;
+                            }
+                        }
+                        if (elim) {
+                            ++n_elim;
+                            vis = 1;
+                        } else if (fm[j] || sf.tflat) {
+                            ++n_keep;
+                            ++n_flat;
+                            fkey = max(fkey, flat_member_key(r, c0 + j));
+                        } else {
+                            ++n_keep;
+                            surv |= 1u << j;
+                            mark_tile(sf.tf, r, c0 + j);
+                        }
+                    }
+                    vis4[j] = vis;
+                }
+                // phase 3 (rare): the exact R_co = clamp(RN(num / den)) decides both tests
+                // (k_sec_rows' FP64 bound test inside the FP32 margin)
+                if (slow) {
+#pragma unroll 1
+                    for (int j = 0; j < 4; ++j) {
+                        if (!((slow >> j) & 1u)) continue;
+                        const bool flat = (flatm >> j) & 1u, u = (ucol >> j) & 1u;
+                        const double nj = j == 0 ? num[0] : j == 1 ? num[1] : j == 2 ? num[2] : num[3];
+                        const double dj2 = j == 0 ? den[0] : j == 1 ? den[1] : j == 2 ? den[2] : den[3];
+                        const bool fmj = j == 0 ? fm[0] : j == 1 ? fm[1] : j == 2 ? fm[2] : fm[3];
+                        const double val = flat ? 0.0 : dclamp(__ddiv_rn(nj, dj2), -1.0, 1.0);
+                        if (val < thr) ++evc;
+                        uint8_t vis = 2;
+                        if (u ? sdg[1] : sdg[0]) {
+                            ++n_keep;
+                        } else {
+                            bool elim = thr_ok && !sf.tflat && !fmj && !(u ? dgg[1] : dgg[0]);
+                            if (elim) {
+                                const double g_a = dclamp(u ? rag[1] : rag[0], -1.0, 1.0);
+                                const double g_sa = u ? sag[1] : sag[0];
+                                const float b = float(val);
+                                const float xf = float(fma(-val, val, 1.0));
+                                const float sq = sqrt_approx(fmaxf(xf, 0.f));
+                                const float f = fmaf(float(g_a), b, float(g_sa) * sq);
+                                if (sec_tbf >= f + 4e-6f) {
+                                    elim = true;
+                                } else if (sec_tbf < f - 4e-6f) {
+                                    elim = false;
+                                } else {
+                                    const double xx = dmax(0.0, __dsub_rn(1.0, __dmul_rn(val, val)));
+                                    elim = sec_tb >= __dadd_rn(__dmul_rn(g_a, val),
+                                                               __dmul_rn(g_sa, __dsqrt_rn(xx)));
+                                }
+                            }
+                            if (elim) {
+                                ++n_elim;
+                                vis = 1;
+                            } else if (fmj || sf.tflat) {
+                                ++n_keep;
+                                ++n_flat;
+                                fkey = max(fkey, flat_member_key(r, c0 + j));
+                            } else {
+                                ++n_keep;
+                                surv |= 1u << j;
+                                mark_tile(sf.tf, r, c0 + j);
+                            }
+                        }
+                        if (j == 0) vis4[0] = vis;
+                        else if (j == 1) vis4[1] = vis;
+                        else if (j == 2) vis4[2] = vis;
+                        else vis4[3] = vis;
+                    }
+                }
+            }
+            if constexpr (MODE == 2) {
+                if (mine == 0xfu) {
+                    *reinterpret_cast<unsigned*>(sf.visits + k0) =
+                        unsigned(vis4[0]) | (unsigned(vis4[1]) << 8) |
+                        (unsigned(vis4[2]) << 16) | (unsigned(vis4[3]) << 24);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        if ((mine >> j) & 1u) sf.visits[k0 + j] = vis4[j];
+                }
+                if (__any_sync(0xffffffffu, surv != 0u)) {
+                    const unsigned cnt = __popc(surv);
+                    unsigned incl = cnt;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+                        if (lane >= o) incl += v;
+                    }
+                    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+                    if (list_full) {
+                        surv_local += tot;
+                    } else {
+                        unsigned long long basepos = 0;
+                        if (lane == 0)
+                            basepos = atomicAdd(&sf.tally->survivors, (unsigned long long)tot);
+                        basepos = __shfl_sync(0xffffffffu, basepos, 0);
+                        list_full = basepos + tot >= sf.max_locs;
+                        unsigned long long pos = basepos + (incl - cnt);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            if ((surv >> j) & 1u) {
+                                if (pos < sf.max_locs) sf.locs[pos] = make_int2(r, c0 + j);
+                                ++pos;
+                            }
+                        }
+                    }
+                }
+            }
+        }
+    }
+    __shared__ unsigned cta_cnt;
+    if (threadIdx.x == 0) cta_cnt = 0u;
+    __syncthreads();
+    evc = __reduce_add_sync(0xffffffffu, evc);
+    if (lane == 0 && evc) atomicAdd(&cta_cnt, evc);
+    if constexpr (MODE == 2) {
+        const unsigned long long ne = warp_sum((unsigned long long)n_elim);
+        const unsigned long long nk = warp_sum((unsigned long long)n_keep);
+        const unsigned long long nf = warp_sum((unsigned long long)n_flat);
+        fkey = warp_max_u64(fkey);
+        if (lane == 0) {
+            if (ne) atomicAdd(&sf.tally->eliminated, ne);
+            if (nk) atomicAdd(&sf.tally->retained, nk);
+            if (surv_local) atomicAdd(&sf.tally->survivors, surv_local);
+            if (nf) {
+                atomicAdd(&sf.tally->flat_n, nf);
+                atomicMax(&sf.tally->flat_key, fkey);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
+    egs_tail(dec);
+}
+
+struct Rco3Geom {
+    int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, tc_reg = 0;
+};
+
+// TMATCH_RCO3=0 keeps the single-pass k_acg for h = 3; TMATCH_RCO3_NT=128|256 and
+// TMATCH_RCO3_SEG (group rows per segment) for A/B runs.
+bool rco3_enabled() {
+    static bool on = [] {
+        const char* e = std::getenv("TMATCH_RCO3");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
+Rco3Geom rco3_geom(int m, int n, GridDesc gd) {
+    Rco3Geom a{};
+    if (gd.h != 3 || gd.w != 3) return a;
+    static const int force_nt = [] {
+        const char* e = std::getenv("TMATCH_RCO3_NT");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 128 || v == 256) ? v : 0;
+    }();
+    static const int force_seg = [] {
+        const char* e = std::getenv("TMATCH_RCO3_SEG");
+        return e ? std::max(0, std::atoi(e)) : 0;
+    }();
+    const int Q = n / 3, R = n % 3;
+    if (Q < 1 || Q > 65) return a;  // the window's warp totals span at most two warps
+    if (gd.ec < 4) return a;        // k_rco_epi: a 4-location chunk wraps at most one row
+    const int nt = force_nt ? force_nt : 256;
+    const int G = nt - Q - (R > 0) + 1;
+    if (G < 32) return a;
+    a.nt = nt;
+    a.G = G;
+    a.tc_reg = gd.ec % 3 == 0 ? gd.tc : gd.tc - 1;
+    a.ntiles = (a.tc_reg + G - 1) / G;
+    const int rows = gd.ti_hi - gd.ti_lo;
+    // segments long enough that the m-row warm-up is a small share of the walk, short enough
+    // for a few waves of resident CTAs (2 per SM)
+    const int per_wave = std::max(1, (148 * 2) / std::max(1, a.ntiles));
+    int seg = force_seg > 0 ? force_seg : std::max((rows + per_wave - 1) / per_wave, 1);
+    if (!force_seg) seg = std::min(seg, std::max(m, 96));
+    a.seg = std::max(1, std::min(seg, std::max(rows, 1)));
+    a.nseg = std::max(1, (rows + a.seg - 1) / a.seg);
+    return a;
+}
+
+template <int NT, bool HEAD>
+void launch_rco3_s(const uint8_t* imgp, int pitch, int m, int n, const Grid& g, unsigned* S,
+                   const Rco3Geom& a, const int* stop, cudaStream_t s) {
+    launch_pdl(k_rco3_s<NT, HEAD>, dim3(a.ntiles, a.nseg), dim3(NT), 0, s, imgp, pitch, m, n, g,
+               S, a.G, a.seg, a.tc_reg, stop);
+}
+
+// k_rco_epi's vector loads/stores: the strip's first location must start 16-byte aligned
+// statistics (4-byte aligned flags / visit codes); the allocations are, strips offset them
+bool rco3_aligned(GridDesc gd, const DevStats& st, const SecFuse& sf) {
+    const size_t kb = size_t(gd.ti_lo) * gd.h * gd.ec;
+    auto al = [](const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
+    return al(st.mu + kb, 16) && al(st.omega + kb, 16) && al(st.flat + kb, 4) &&
+           (!sf.thr || al(sf.visits + kb, 4));
+}
+
+cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc gd, DevStats st,
+                        double thr, double* map, unsigned long long* n_r, int* stop,
+                        cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+    const Rco3Geom a = rco3_geom(m, n, gd);
+    if (a.nt == 0) return cudaErrorInvalidValue;
+    const Grid g = to_grid(gd);
+    const int row_lo = g.row_lo(), row_hi = g.row_hi();
+    if (row_hi <= row_lo) return cudaSuccess;
+    const size_t cells = size_t(row_hi - row_lo) * gd.ec;
+    unsigned* Sbuf = nullptr;
+    cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&Sbuf),
+                                    ((cells + 3) & ~size_t(3)) * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    unsigned* S = Sbuf - size_t(row_lo) * gd.ec;  // indexed by global extent position
+    const bool head = n % 3 != 0;
+    if (a.ntiles > 0) {
+        if (a.nt == 128) {
+            if (head) launch_rco3_s<128, true>(imgp, pitch, m, n, g, S, a, stop, s);
+            else launch_rco3_s<128, false>(imgp, pitch, m, n, g, S, a, stop, s);
+        } else {
+            if (head) launch_rco3_s<256, true>(imgp, pitch, m, n, g, S, a, stop, s);
+            else launch_rco3_s<256, false>(imgp, pitch, m, n, g, S, a, stop, s);
+        }
+    }
+    unsigned* Rp = nullptr;
+    if (a.tc_reg < gd.tc) {  // the clipped last group column
+        const int cc = 3 * (gd.tc - 1), wl = gd.ec - cc;
+        const int x0 = g.center_row(gd.ti_lo), x1 = g.center_row(gd.ti_hi - 1) + m;
+        const int nx = x1 - x0;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&Rp), size_t(6) * nx * sizeof(unsigned), s);
+        if (e != cudaSuccess) return e;
+        launch_pdl(k_rco3_clip_rows, dim3(std::min((nx + 7) / 8, 148 * 8)), dim3(256), 0, s, imgp,
+                   pitch, n, cc, x0, nx, Rp);
+        const int items = (gd.ti_hi - gd.ti_lo) * 6;
+        launch_pdl(k_rco3_clip_sum, dim3(std::min((items + 255) / 256, 148 * 4)), dim3(256), 0, s,
+                   Rp, m, g, cc, wl, x0, nx, S);
+    }
+    const double mn = double(m) * double(n);
+    const int blocks = std::min(row_hi - row_lo, 148 * 8);
+    static const int minb = [] {  // TMATCH_EPI_MINB: resident CTAs the epilogue is built for
+        const char* e = std::getenv("TMATCH_EPI_MINB");
+        const int v = e ? std::atoi(e) : 0;
+        return (v >= 2 && v <= 4) ? v : 3;
+    }();
+    auto epi = [&](auto kern) {
+        launch_pdl(kern, dim3(blocks), dim3(256), 0, s, g, S, st, mn, thr, map, n_r, stop, dec, sf);
+    };
+    const int mode = sf.thr ? 2 : (map ? 1 : 0);
+    if (mode == 2) {
+        if (minb == 3) epi(k_rco_epi<2, 3>);
+        else if (minb == 4) epi(k_rco_epi<2, 4>);
+        else epi(k_rco_epi<2, 2>);
+    } else if (mode == 1) {
+        epi(k_rco_epi<1, 3>);
+    } else {
+        epi(k_rco_epi<0, 3>);
+    }
+    e = cudaGetLastError();
+    cudaFreeAsync(Sbuf, s);
+    if (Rp) cudaFreeAsync(Rp, s);
+    return e;
+}
+
 template <int H>
 cudaError_t launch_acv(const uint8_t* img, int p, int q, int m, int w, int ti_base, int trr,
                        int tr, unsigned* V, cudaStream_t s) {
@@ -2031,6 +2725,9 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
         const EgsDecide d = dec ? *dec : EgsDecide{};
         const SecFuse f = fuse ? *fuse : SecFuse{};
         if (decided) *decided = d.ticket != nullptr;
+        if (gd.h == 3 && rco3_enabled() && rco3_geom(m, n, gd).nt > 0 && rco3_aligned(gd, st, f))
+            return launch_rco3(imgp, pitch, m, n, gd, st, retain_threshold, map, n_r, stop, s, d,
+                               f);
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                  egs_prev, egs_central, egs_xi, s, d, f);
