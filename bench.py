@@ -322,7 +322,9 @@ def roofline(phases, wl, res, pk, fp64_search=False):
     """Per-phase achieved vs peak; the dominant phase (largest device time) is the headline
     roofline.  Algorithmic amounts per launch group:
       window_stats   p*q + 17 B per extent location (u8 read; mu, omega, flat written)
-      autocorr_sec   p*q + 18 B per location + 18 B per group (fused R_co + scan 2)
+      autocorr_sec   p*q + 18 B per location + 18 B per group (fused R_co + scan 2; h = 3:
+                     k_rco3_s cross sums + k_rco_epi epilogue, whose u32 S round trip of
+                     8 B per location is implementation traffic, not algorithmic)
       autocorr_u8    p*q + 25 B per location (R_co map written)
       autocorr_count p*q + 17 B per location (count-only EGS candidate, stops early)
       sec_compact    10 B per location (map 8 + flat 1 + visit 1)
@@ -338,8 +340,9 @@ def roofline(phases, wl, res, pk, fp64_search=False):
     defs = {
         "window_stats": ("hbm", p * q + 17.0 * E, "k_wstats4 (window statistics)"),
         "autocorr_sec": ("hbm", p * q + 18.0 * E + 18.0 * G,
-                         "k_acg<h,...,FUSE=1> (R_co of the accepted EGS size with scan 2 fused: "
-                         "retained count + bound test + survivor list)"),
+                         "k_rco3_s + k_rco_epi<2> (h = 3; k_acg<h,...,FUSE=1> for h = 5): R_co "
+                         "of the accepted EGS size with scan 2 fused (retained count + bound "
+                         "test + survivor list)"),
         "autocorr_u8": ("hbm", p * q + 25.0 * E, "k_acg / k_acf (R_co map of one EGS size)"),
         "autocorr_count": ("hbm", p * q + 17.0 * E,
                            "k_acg count-only EGS candidate (stops at the EGS rejection point)"),
