@@ -272,6 +272,7 @@ struct tm_ctx {
     DBuf<double> map_tmp, map_user, map_fused;
     DBuf<double> egs_maps[4];
     DBuf<double> sa_c;  // per-group half_gap factor sqrt(1 - rho_c^2) (scan 2)
+    DBuf<unsigned> egs_rows;  // per-extent-row retained counts of a batch's first candidate
     bool sa_ready = false;  // sa_c filled by this search's centre epilogue
     float2* batch_rec = nullptr;  // run_batch: the centre epilogue also writes the records
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
@@ -298,6 +299,12 @@ struct tm_ctx {
     // R_co kernel choice: fused sliding-window (default) or the column-walk + line-scan pair
     // (TMATCH_AUTOCORR=colwalk; kept for A/B measurements and as a cross-check in tests)
     bool ac_fused = true;
+    // EGS count-only candidates ordered by the first candidate's row density (TMATCH_EGS_ORDER=0
+    // keeps the launch order)
+    bool egs_order = [] {
+        const char* e = std::getenv("TMATCH_EGS_ORDER");
+        return !(e && std::atoi(e) == 0);
+    }();
     // window statistics: four columns per thread (TMATCH_WSTATS=column: one per column)
     bool ws4 = true;
     // integer tensor-core correlation (tcgen05 kind::i8) for centre scans / dense work;
@@ -1225,11 +1232,12 @@ bool autocorr_launch(tm_ctx* ctx, tm_image* img, const WS& ws, const tmk::GridDe
             const double central = double((g.er + g.h - 1) / g.h) * double((g.ec + g.w - 1) / g.w);
             // (the group-column kernel stages rows from the 16-byte-pitched copy)
             const bool pitched = img->u8p.p && img->u8p_rows >= p + tmk::kU8PadRows;
+            int nl = 1;
             CK(tmk::autocorr_u8_fused(img->u8.p, p, q, m, n, g, ws.dev(), thr,
                                       count_only ? nullptr : map, nr, stop, ctx->s, egs_prev,
                                       central, egs_xi, pitched ? img->u8p.p : nullptr,
-                                      img->u8p_pitch, dec, decided, fuse));
-            ctx->add(1);
+                                      img->u8p_pitch, dec, decided, fuse, &nl));
+            ctx->add(nl);
             return !count_only && !fuse;
         } else if (tmk::autocorr_colwalk_supported(m, n, q, g) && vbytes <= (size_t(16) << 30)) {
             ctx->acH.ensure(vbytes / sizeof(int));
@@ -1435,6 +1443,17 @@ EgsOut run_egs_search(tm_ctx* ctx, tm_image* img, const WS& ws, int m, int n, in
                 dec.disp_E = E;
                 dec.disp_dense = reinterpret_cast<int*>(ctx->counters.p + 22);
                 dec.disp_list = ctx->counters.p + 23;
+            }
+            // the first candidate counts retained members per extent row; later count-only
+            // candidates (in-kernel rejection) walk their segments densest first
+            if (ctx->egs_order && nc > 1) {
+                if (k == 0) {
+                    ctx->egs_rows.ensure(size_t(er));
+                    CK(cudaMemsetAsync(ctx->egs_rows.p, 0, size_t(er) * sizeof(unsigned), ctx->s));
+                    dec.rows_out = ctx->egs_rows.p;
+                } else {
+                    dec.rows_in = ctx->egs_rows.p;
+                }
             }
             bool decided = false;
             const bool is_pred = cand[k].h == pred && cand[k].w == pred;

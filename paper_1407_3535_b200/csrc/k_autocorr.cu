@@ -970,7 +970,8 @@ __global__ void __launch_bounds__(NT)
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
     const int dj = int(blockIdx.x) - hr;
     const int k0 = (int(blockIdx.y) + tile_base) * G;
-    const int ti0 = g.ti_lo + blockIdx.z * seg;
+    const int zseg = dec.zorder ? dec.zorder[blockIdx.z] : int(blockIdx.z);
+    const int ti0 = g.ti_lo + zseg * seg;
     const int ti1 = min(ti0 + seg, g.ti_hi);
     {
         // skipped candidate (an earlier decision stopped EGS) or empty block: one read of
@@ -1539,6 +1540,31 @@ __global__ void __launch_bounds__(NT)
     egs_tail(dec);
 }
 
+// Segment order for a count-only candidate (EgsDecide::zorder): segment z covers group rows
+// [ti_lo + z*seg, ...) = extent rows [that * h, ...); its density is the earlier candidate's
+// retained count over those rows.  One CTA ranks the segments (descending, ties by index).
+__global__ void __launch_bounds__(1024)
+    k_seg_order(const unsigned* __restrict__ rows, int er, int h, int ti_lo, int seg, int nseg,
+                int* __restrict__ order) {
+    pdl_wait();
+    extern __shared__ unsigned long long segc[];
+    for (int z = threadIdx.x; z < nseg; z += blockDim.x) segc[z] = 0ull;
+    __syncthreads();
+    const int r_lo = ti_lo * h, r_hi = min((ti_lo + nseg * seg) * h, er);
+    for (int r = r_lo + int(threadIdx.x); r < r_hi; r += blockDim.x)
+        if (rows[r]) atomicAdd(&segc[(r / h - ti_lo) / seg], (unsigned long long)rows[r]);
+    __syncthreads();
+    for (int z = threadIdx.x; z < nseg; z += blockDim.x) {
+        const unsigned long long c = segc[z];
+        int rank = 0;
+        for (int y = 0; y < nseg; ++y) {
+            const unsigned long long d = segc[y];
+            rank += (d > c || (d == c && y < z)) ? 1 : 0;
+        }
+        order[rank] = z;
+    }
+}
+
 struct AcgGeom {
     int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, SW = 0, RR = 0;
     size_t smem = 0;
@@ -1636,10 +1662,23 @@ cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, Gr
     const AcgGeom a = acg_geom(m, n, gd, NT, occ);
     const int t1 = tile_hi < 0 ? a.ntiles : std::min(tile_hi, a.ntiles);
     dim3 grid(gd.w, std::max(0, t1 - tile_lo), a.nseg);
+    EgsDecide d = dec;
+    int* order = nullptr;
+    // (only when the launch runs in several waves: one wave has no order to exploit)
+    const long long waves = (long long)grid.x * grid.y * grid.z / std::max(1, 148 * occ);
+    if (!FUSE && !map && stop && egs_prev && dec.rows_in && a.nseg > 1 && a.nseg <= 4096 &&
+        waves >= 3 && gd.ti_hi > gd.ti_lo && grid.y > 0 &&
+        cudaMallocAsync(reinterpret_cast<void**>(&order), size_t(a.nseg) * sizeof(int), s) ==
+            cudaSuccess) {
+        launch_pdl(k_seg_order, dim3(1), dim3(1024), size_t(a.nseg) * 8, s, dec.rows_in, gd.er,
+                   gd.h, gd.ti_lo, a.seg, a.nseg, order);
+        d.zorder = order;
+    }
     if (gd.ti_hi > gd.ti_lo && grid.y > 0)
         launch_pdl(k_acg<H, NT, NP, FUSE>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n,
                    to_grid(gd), st, thr, map, n_r, a.G, a.seg, a.RR, stop, egs_prev, egs_central,
-                   egs_xi, dec, sf, tile_lo);
+                   egs_xi, d, sf, tile_lo);
+    if (order) cudaFreeAsync(order, s);
     return cudaGetLastError();
 }
 
@@ -2008,6 +2047,7 @@ __global__ void __launch_bounds__(256, MINB)
     const unsigned ke = unsigned(g.row_hi()) * unsigned(g.ec);
     const int r_lo = g.row_lo(), r_hi = g.row_hi();
     for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const unsigned evc_row = evc;  // (EgsDecide::rows_out: this row's retained count)
         const int ti = g.tile_r(r);
         const int cr = g.center_row(ti);
         const unsigned krow = unsigned(r) * unsigned(g.ec);          // first location of the row
@@ -2260,6 +2300,10 @@ __global__ void __launch_bounds__(256, MINB)
                     }
                 }
             }
+        }
+        if (dec.rows_out) {  // CTA-uniform
+            const unsigned d = __reduce_add_sync(0xffffffffu, evc - evc_row);
+            if (lane == 0 && d) atomicAdd(dec.rows_out + r, d);
         }
     }
     __shared__ unsigned cta_cnt;
@@ -2717,17 +2761,20 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               unsigned long long* n_r, int* stop, cudaStream_t s,
                               const double* egs_prev, double egs_central, double egs_xi,
                               const uint8_t* imgp, int pitch, const EgsDecide* dec,
-                              bool* decided, const SecFuse* fuse) {
+                              bool* decided, const SecFuse* fuse, int* launches) {
     if (decided) *decided = false;
+    if (launches) *launches = 1;
     if (imgp && pitch % 16 == 0 && acg_enabled() && acg_geom(m, n, gd, acg_threads(gd)).nt > 0 &&
         (gd.h == 3 || gd.h == 5)) {
         // the EGS decision rides on the launch's tail (no k_egs_decide launch)
         const EgsDecide d = dec ? *dec : EgsDecide{};
         const SecFuse f = fuse ? *fuse : SecFuse{};
         if (decided) *decided = d.ticket != nullptr;
-        if (gd.h == 3 && rco3_enabled() && rco3_geom(m, n, gd).nt > 0 && rco3_aligned(gd, st, f))
+        if (gd.h == 3 && rco3_enabled() && rco3_geom(m, n, gd).nt > 0 && rco3_aligned(gd, st, f)) {
+            if (launches) *launches = rco3_geom(m, n, gd).tc_reg < gd.tc ? 4 : 2;
             return launch_rco3(imgp, pitch, m, n, gd, st, retain_threshold, map, n_r, stop, s, d,
                                f);
+        }
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                  egs_prev, egs_central, egs_xi, s, d, f);

@@ -117,6 +117,14 @@ struct EgsDecide {
     unsigned long long disp_E = 0;
     int* disp_dense = nullptr;
     unsigned long long* disp_list = nullptr;
+    // Segment order of a count-only candidate: the batch's first candidate (two-pass h = 3
+    // R_co) counts its retained members per extent row into rows_out; a later count-only
+    // candidate with in-kernel rejection reads them as rows_in and walks its row segments in
+    // decreasing order of that density (zorder, set by the launcher), so its partial count
+    // reaches the rejection bound after fewer segments.  Null: launch order.
+    unsigned* rows_out = nullptr;
+    const unsigned* rows_in = nullptr;
+    const int* zorder = nullptr;
 };
 
 // Scan 2 fused into the R_co launch of the predicted group size (tm_search): scan 1 and the
@@ -269,7 +277,7 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
                               const double* egs_prev = nullptr, double egs_central = 0.0,
                               double egs_xi = 0.0, const uint8_t* imgp = nullptr, int pitch = 0,
                               const EgsDecide* dec = nullptr, bool* decided = nullptr,
-                              const SecFuse* fuse = nullptr);
+                              const SecFuse* fuse = nullptr, int* launches = nullptr);
 // The group-column R_co kernel can run scan 2 in its epilogue (SecFuse) for this geometry.
 bool autocorr_sec_fuse_supported(int m, int n, GridDesc g);
 // k_egs_decide with a full decision record (the dispatch fields included)
