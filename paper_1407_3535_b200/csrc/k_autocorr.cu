@@ -943,6 +943,11 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gsrc) : "memory");
 }
 __device__ __forceinline__ void opaque(unsigned& x) { asm("" : "+r"(x)); }
+__device__ __forceinline__ void cp_async4(void* sdst, const void* gsrc) {
+    const unsigned sa = unsigned(__cvta_generic_to_shared(sdst));
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 
@@ -1783,6 +1788,170 @@ cudaError_t launch_acg(const uint8_t* imgp, int pitch, int q, int m, int n, Grid
 // 2 scan 2 fused (SecFuse: bound test, visit codes, tallies, survivor list -- the k_acg FUSE
 // epilogue).  Every load is coalesced along the row; the EGS decision rides on its tail.
 
+
+// One member's R_co epilogue (autocorr.cpp:84-88: num = S - (mn*mu_c)*mu_m, den = om_c*om_m,
+// R_co = clamp(RN(num/den)), 0 for flat windows) and, by MODE, 0: the retained count
+// (egs.cpp:12-25), 1: + the map store, 2: + scan 2 (the k_acg FUSE epilogue: FP32 quotient
+// outside the margins, FP64 inside; visit code, tallies).  Returns whether the member survives
+// (MODE 2: it goes to the survivor list).
+struct RcoTally {
+    unsigned evc = 0, n_elim = 0, n_keep = 0, n_flat = 0;
+    unsigned long long fkey = 0;
+};
+struct SecCtx {
+    double tb = 0.0;
+    float tbf = 0.f;
+    bool thr_ok = false;
+};
+template <int MODE>
+__device__ __forceinline__ bool rco_member(RcoTally& T, int r, int c, unsigned k, unsigned S,
+                                           double mm, double om, bool fm, double mnmc, double oc,
+                                           bool fc, double ra, double sa, bool dg, bool sd,
+                                           double thr, const SecCtx& sc, double* map,
+                                           const SecFuse& sf) {
+    const bool flat = fc || fm;
+    const double num = __dsub_rn(double(S), __dmul_rn(mnmc, mm));
+    const double den = __dmul_rn(oc, om);
+    if constexpr (MODE == 0) {
+        if (flat ? 0.0 < thr : retained_below(num, den, thr)) ++T.evc;
+        return false;
+    } else if constexpr (MODE == 1) {
+        const double val = flat ? 0.0 : dclamp(__ddiv_rn(num, den), -1.0, 1.0);
+        map[k] = val;
+        if (val < thr) ++T.evc;
+        return false;
+    } else {
+        float qf = 0.f;
+        bool fast = !flat;
+        if (fast) {
+            qf = __fmul_rn(float(num), rcp_approx(float(den)));
+            fast = fabsf(qf) < 0.99f;
+        }
+        double val = 0.0;
+        bool have_val = flat;
+        auto exact = [&]() {
+            if (!have_val) {
+                val = dclamp(__ddiv_rn(num, den), -1.0, 1.0);
+                have_val = true;
+            }
+            return val;
+        };
+        bool ret;
+        if (flat) {
+            ret = 0.0 < thr;
+        } else if (fast && qf < float(thr) - 1e-6f) {
+            ret = true;
+        } else if (fast && qf > float(thr) + 1e-6f) {
+            ret = false;
+        } else {
+            ret = exact() < thr;
+        }
+        if (ret) ++T.evc;
+        uint8_t vis = 2;
+        bool survivor = false;
+        if (sd) {
+            ++T.n_keep;
+        } else {
+            bool elim = sc.thr_ok && !dg && !sf.tflat && !fm;
+            if (elim) {
+                const double g_a = dclamp(ra, -1.0, 1.0);
+                const float b = have_val ? float(val) : qf;
+                const float xf = have_val ? float(fma(-val, val, 1.0)) : fmaf(-qf, qf, 1.0f);
+                const float sq = sqrt_approx(fmaxf(xf, 0.f));
+                const float f = fmaf(float(g_a), b, float(sa) * sq);
+                const float margin = have_val ? 4e-6f : 1e-5f;
+                if (sc.tbf >= f + margin) {
+                    elim = true;
+                } else if (sc.tbf < f - margin) {
+                    elim = false;
+                } else {
+                    const double v = exact();
+                    const double xx = dmax(0.0, __dsub_rn(1.0, __dmul_rn(v, v)));
+                    elim = sc.tb >= __dadd_rn(__dmul_rn(g_a, v), __dmul_rn(sa, __dsqrt_rn(xx)));
+                }
+            }
+            if (elim) {
+                ++T.n_elim;
+                vis = 1;
+            } else if (fm || sf.tflat) {
+                ++T.n_keep;
+                ++T.n_flat;
+                T.fkey = max(T.fkey, flat_member_key(r, c));
+            } else {
+                ++T.n_keep;
+                survivor = true;
+                mark_tile(sf.tf, r, c);
+            }
+        }
+        sf.visits[k] = vis;
+        return survivor;
+    }
+}
+
+// Warp-aggregated append of this thread's survivors (bit i of `bits`: member (rows[i], cols[i]))
+template <int NB>
+__device__ __forceinline__ void rco_list(unsigned bits, const int* rr, const int* cc, const SecFuse& sf,
+                                         bool& list_full, unsigned long long& surv_local) {
+    const int lane = threadIdx.x & 31;
+    if (!__any_sync(0xffffffffu, bits != 0u)) return;
+    const unsigned cnt = __popc(bits);
+    unsigned incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const unsigned v = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += v;
+    }
+    const unsigned tot = __shfl_sync(0xffffffffu, incl, 31);
+    if (list_full) {
+        surv_local += tot;
+        return;
+    }
+    unsigned long long basepos = 0;
+    if (lane == 0) basepos = atomicAdd(&sf.tally->survivors, (unsigned long long)tot);
+    basepos = __shfl_sync(0xffffffffu, basepos, 0);
+    list_full = basepos + tot >= sf.max_locs;
+    unsigned long long pos = basepos + (incl - cnt);
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+        if ((bits >> i) & 1u) {
+            if (pos < sf.max_locs) sf.locs[pos] = make_int2(rr[i], cc[i]);
+            ++pos;
+        }
+    }
+}
+
+// Final tallies of an R_co epilogue: warp sums, one atomic per warp (MODE 2 tallies) and per
+// CTA (retained count), then the EGS decision on the launch's tail.
+template <int MODE>
+__device__ __forceinline__ void rco_finish(const RcoTally& T, unsigned long long surv_local,
+                                           unsigned long long* n_r, const SecFuse& sf,
+                                           const EgsDecide& dec) {
+    const int lane = threadIdx.x & 31;
+    __shared__ unsigned cta_cnt;
+    if (threadIdx.x == 0) cta_cnt = 0u;
+    __syncthreads();
+    const unsigned evc = __reduce_add_sync(0xffffffffu, T.evc);
+    if (lane == 0 && evc) atomicAdd(&cta_cnt, evc);
+    if constexpr (MODE == 2) {
+        const unsigned long long ne = warp_sum((unsigned long long)T.n_elim);
+        const unsigned long long nk = warp_sum((unsigned long long)T.n_keep);
+        const unsigned long long nf = warp_sum((unsigned long long)T.n_flat);
+        const unsigned long long fk = warp_max_u64(T.fkey);
+        if (lane == 0) {
+            if (ne) atomicAdd(&sf.tally->eliminated, ne);
+            if (nk) atomicAdd(&sf.tally->retained, nk);
+            if (surv_local) atomicAdd(&sf.tally->survivors, surv_local);
+            if (nf) {
+                atomicAdd(&sf.tally->flat_n, nf);
+                atomicMax(&sf.tally->flat_key, fk);
+            }
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0 && cta_cnt) atomicAdd(n_r, (unsigned long long)cta_cnt);
+    egs_tail(dec);
+}
+
 template <int NT, bool HEAD>
 __global__ void __launch_bounds__(NT, 512 / NT)
     k_rco3_s(const uint8_t* __restrict__ img, int P, int m, int n, Grid g,
@@ -1996,7 +2165,7 @@ __global__ void __launch_bounds__(256)
 
 __global__ void __launch_bounds__(256)
     k_rco3_clip_sum(const unsigned* __restrict__ Rp, int m, Grid g, int cc, int wl, int x0, int nx,
-                    unsigned* __restrict__ Sout) {
+                    unsigned* __restrict__ Sout, unsigned* __restrict__ Scomp) {
     pdl_wait();
     const int items = (g.ti_hi - g.ti_lo) * 6;
     for (int it = blockIdx.x * blockDim.x + threadIdx.x; it < items; it += gridDim.x * blockDim.x) {
@@ -2008,11 +2177,12 @@ __global__ void __launch_bounds__(256)
         const unsigned* rp = Rp + size_t(c) * nx + (cr - x0);
         unsigned s = 0u;
         for (int a = 0; a < m; ++a) s += rp[a];
-        Sout[unsigned(r) * unsigned(g.ec) + unsigned(cc + dj)] = s;
+        if (Scomp) Scomp[size_t(ti - g.ti_lo) * 6 + c] = s;  // [group row][slot] (fused path)
+        else Sout[unsigned(r) * unsigned(g.ec) + unsigned(cc + dj)] = s;
     }
 }
 
-template <int MODE, int MINB>
+template <int MODE, int MINB, int V>
 __global__ void __launch_bounds__(256, MINB)
     k_rco_epi(Grid g, const unsigned* __restrict__ Sin, DevStats st, double mn, double thr,
               double* __restrict__ map, unsigned long long* __restrict__ n_r, int* stop,
@@ -2053,32 +2223,45 @@ __global__ void __launch_bounds__(256, MINB)
         const unsigned krow = unsigned(r) * unsigned(g.ec);          // first location of the row
         const unsigned kcrow = unsigned(cr) * unsigned(g.ec);
         const unsigned gbase = unsigned(ti) * unsigned(g.tc);
-        const unsigned ch0 = (krow - kb) >> 2, ch1 = (krow + g.ec - kb + 3) >> 2;
+        constexpr int LV = V == 4 ? 2 : 1;
+        const unsigned ch0 = (krow - kb) >> LV, ch1 = (krow + g.ec - kb + V - 1) >> LV;
         // whole warps per row (ballots)
         const unsigned nthr = ((ch1 - ch0 + 31) / 32) * 32;
         for (unsigned i = threadIdx.x; i < nthr; i += blockDim.x) {
             const unsigned ch = ch0 + i;
             const bool active = ch < ch1;
-            const unsigned k0 = kb + 4 * (active ? ch : ch0);
+            const unsigned k0 = kb + V * (active ? ch : ch0);
             const int c0 = int(k0) - int(krow);  // column of element 0 (may be < 0 at the row start)
-            unsigned sv[4];
-            double mm[4], om[4];
-            uint8_t fm[4];
-            if (k0 + 4 <= ke) {
-                const uint4 s4 = *reinterpret_cast<const uint4*>(Sin + k0);
-                const double2 m01 = *reinterpret_cast<const double2*>(st.mu + k0);
-                const double2 m23 = *reinterpret_cast<const double2*>(st.mu + k0 + 2);
-                const double2 o01 = *reinterpret_cast<const double2*>(st.omega + k0);
-                const double2 o23 = *reinterpret_cast<const double2*>(st.omega + k0 + 2);
-                const unsigned f4 = *reinterpret_cast<const unsigned*>(st.flat + k0);
-                sv[0] = s4.x; sv[1] = s4.y; sv[2] = s4.z; sv[3] = s4.w;
-                mm[0] = m01.x; mm[1] = m01.y; mm[2] = m23.x; mm[3] = m23.y;
-                om[0] = o01.x; om[1] = o01.y; om[2] = o23.x; om[3] = o23.y;
+            unsigned sv[V];
+            double mm[V], om[V];
+            uint8_t fm[V];
+            if (k0 + V <= ke) {
+                if constexpr (V == 4) {
+                    const uint4 s4 = *reinterpret_cast<const uint4*>(Sin + k0);
+                    const double2 m01 = *reinterpret_cast<const double2*>(st.mu + k0);
+                    const double2 m23 = *reinterpret_cast<const double2*>(st.mu + k0 + 2);
+                    const double2 o01 = *reinterpret_cast<const double2*>(st.omega + k0);
+                    const double2 o23 = *reinterpret_cast<const double2*>(st.omega + k0 + 2);
+                    const unsigned f4 = *reinterpret_cast<const unsigned*>(st.flat + k0);
+                    sv[0] = s4.x; sv[1] = s4.y; sv[2] = s4.z; sv[3] = s4.w;
+                    mm[0] = m01.x; mm[1] = m01.y; mm[2] = m23.x; mm[3] = m23.y;
+                    om[0] = o01.x; om[1] = o01.y; om[2] = o23.x; om[3] = o23.y;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) fm[j] = uint8_t(f4 >> (8 * j));
+                    for (int j = 0; j < V; ++j) fm[j] = uint8_t(f4 >> (8 * j));
+                } else {
+                    const uint2 s2 = *reinterpret_cast<const uint2*>(Sin + k0);
+                    const double2 m01 = *reinterpret_cast<const double2*>(st.mu + k0);
+                    const double2 o01 = *reinterpret_cast<const double2*>(st.omega + k0);
+                    const unsigned f2 = *reinterpret_cast<const unsigned short*>(st.flat + k0);
+                    sv[0] = s2.x; sv[1] = s2.y;
+                    mm[0] = m01.x; mm[1] = m01.y;
+                    om[0] = o01.x; om[1] = o01.y;
+                    fm[0] = uint8_t(f2);
+                    fm[1] = uint8_t(f2 >> 8);
+                }
             } else {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < V; ++j) {
                     const unsigned kj = k0 + j < ke ? k0 + j : krow;
                     sv[j] = Sin[kj];
                     mm[j] = st.mu[kj];
@@ -2110,15 +2293,15 @@ __global__ void __launch_bounds__(256, MINB)
                 }
             }
             const int cnext = 3 * tj1;  // first column of the second group
-            uint8_t vis4[4] = {0, 0, 0, 0};
+            uint8_t vis4[V] = {};
             unsigned surv = 0, mine = 0;  // bit j: element j survives / belongs to this row
             // phase 1 (branch-free over the four elements): membership, R_co's FP64 numerator
             // and denominator, the FP32 quotient
             unsigned memb = 0, flatm = 0, ucol = 0;
-            double num[4], den[4];
-            float qf[4];
+            double num[V], den[V];
+            float qf[V];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) {
+            for (int j = 0; j < V; ++j) {
                 const int c = c0 + j;
                 const bool in = active && c >= 0 && c < g.ec;
                 const bool u = tj1 != tj0 && c >= cnext;  // (selects: no local-memory arrays)
@@ -2135,7 +2318,7 @@ __global__ void __launch_bounds__(256, MINB)
             }
             if constexpr (MODE != 2) {
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < V; ++j) {
                     if (!((mine >> j) & 1u)) continue;
                     const unsigned k = k0 + j;
                     const bool flat = (flatm >> j) & 1u;
@@ -2160,7 +2343,7 @@ __global__ void __launch_bounds__(256, MINB)
                 const float thr_lo = float(thr) - 1e-6f, thr_hi = float(thr) + 1e-6f;
                 unsigned slow = 0;
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
+                for (int j = 0; j < V; ++j) {
                     if (!((memb >> j) & 1u)) continue;
                     const bool flat = (flatm >> j) & 1u, u = (ucol >> j) & 1u;
                     const bool fast = !flat && fabsf(qf[j]) < 0.99f;
@@ -2212,12 +2395,18 @@ __global__ void __launch_bounds__(256, MINB)
                 // (k_sec_rows' FP64 bound test inside the FP32 margin)
                 if (slow) {
 #pragma unroll 1
-                    for (int j = 0; j < 4; ++j) {
+                    for (int j = 0; j < V; ++j) {
                         if (!((slow >> j) & 1u)) continue;
                         const bool flat = (flatm >> j) & 1u, u = (ucol >> j) & 1u;
-                        const double nj = j == 0 ? num[0] : j == 1 ? num[1] : j == 2 ? num[2] : num[3];
-                        const double dj2 = j == 0 ? den[0] : j == 1 ? den[1] : j == 2 ? den[2] : den[3];
-                        const bool fmj = j == 0 ? fm[0] : j == 1 ? fm[1] : j == 2 ? fm[2] : fm[3];
+                        double nj = num[0], dj2 = den[0];
+                        bool fmj = fm[0];
+#pragma unroll
+                        for (int i = 1; i < V; ++i)
+                            if (j == i) {
+                                nj = num[i];
+                                dj2 = den[i];
+                                fmj = fm[i];
+                            }
                         const double val = flat ? 0.0 : dclamp(__ddiv_rn(nj, dj2), -1.0, 1.0);
                         if (val < thr) ++evc;
                         uint8_t vis = 2;
@@ -2255,21 +2444,24 @@ __global__ void __launch_bounds__(256, MINB)
                                 mark_tile(sf.tf, r, c0 + j);
                             }
                         }
-                        if (j == 0) vis4[0] = vis;
-                        else if (j == 1) vis4[1] = vis;
-                        else if (j == 2) vis4[2] = vis;
-                        else vis4[3] = vis;
+#pragma unroll
+                        for (int i = 0; i < V; ++i)
+                            if (j == i) vis4[i] = vis;
                     }
                 }
             }
             if constexpr (MODE == 2) {
-                if (mine == 0xfu) {
-                    *reinterpret_cast<unsigned*>(sf.visits + k0) =
-                        unsigned(vis4[0]) | (unsigned(vis4[1]) << 8) |
-                        (unsigned(vis4[2]) << 16) | (unsigned(vis4[3]) << 24);
+                if (mine == (1u << V) - 1u) {
+                    if constexpr (V == 4)
+                        *reinterpret_cast<unsigned*>(sf.visits + k0) =
+                            unsigned(vis4[0]) | (unsigned(vis4[1]) << 8) |
+                            (unsigned(vis4[2]) << 16) | (unsigned(vis4[3]) << 24);
+                    else
+                        *reinterpret_cast<unsigned short*>(sf.visits + k0) =
+                            (unsigned short)(unsigned(vis4[0]) | (unsigned(vis4[1]) << 8));
                 } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j)
+                    for (int j = 0; j < V; ++j)
                         if ((mine >> j) & 1u) sf.visits[k0 + j] = vis4[j];
                 }
                 if (__any_sync(0xffffffffu, surv != 0u)) {
@@ -2291,7 +2483,7 @@ __global__ void __launch_bounds__(256, MINB)
                         list_full = basepos + tot >= sf.max_locs;
                         unsigned long long pos = basepos + (incl - cnt);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < V; ++j) {
                             if ((surv >> j) & 1u) {
                                 if (pos < sf.max_locs) sf.locs[pos] = make_int2(r, c0 + j);
                                 ++pos;
@@ -2331,6 +2523,397 @@ __global__ void __launch_bounds__(256, MINB)
     egs_tail(dec);
 }
 
+// ---- Fused variant: the walk of k_rco3_s with the member epilogue in the same CTA --------
+//
+// k_rco3_f<NT, HEAD, MODE>: the walk and event scan of k_rco3_s, but instead of storing the
+// eight members' cross sums each thread evaluates them at once (rco_member: R_co, retained
+// count, map / scan 2).  The window statistics of the event's three extent rows over the
+// tile's columns are staged into shared memory by cp.async two events ahead (three buffers,
+// issued after the event barrier so no buffer is overwritten while read), so no E-sized S
+// round trip and no gathers: the group centre's statistics are in the staged middle row.
+// The clipped last group column goes through k_rco3_clip_* + k_rco3_clip_epi.
+constexpr int kRcoStages = 3;
+// (even / multiple of 4 so every staged row stays 16- / 4-byte aligned for cp.async)
+__host__ __device__ constexpr int rco_sc(int G) { return (3 * G + 3) & ~1; }    // doubles per row
+__host__ __device__ constexpr int rco_scf(int G) { return (3 * G + 11) & ~3; }  // flag bytes per row
+__host__ __device__ constexpr size_t rco_stage_bytes(int G) {
+    return size_t(3) * rco_sc(G) * 16 + ((size_t(3) * rco_scf(G) + 15) & ~size_t(15));
+}
+
+template <int NT, bool HEAD, int MODE>
+__global__ void __launch_bounds__(NT, NT == 128 ? 3 : 1)
+    k_rco3_f(const uint8_t* __restrict__ img, int P, int m, int n, Grid g, DevStats st, double mn,
+             double thr, double* __restrict__ map, unsigned long long* __restrict__ n_r, int G,
+             int seg, int tc_reg, int* stop, EgsDecide dec, SecFuse sf) {
+    constexpr int NW = NT / 32;
+    __shared__ unsigned Lb[2][9][NT];
+    __shared__ unsigned Hb[2][HEAD ? 9 : 1][NT];
+    __shared__ unsigned Wb[2][9][NW + 2];
+    extern __shared__ __align__(16) unsigned char rco_stage[];
+    pdl_wait();
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int k0 = int(blockIdx.x) * G;
+    const int ti0 = g.ti_lo + int(blockIdx.y) * seg;
+    const int ti1 = min(ti0 + seg, g.ti_hi);
+    {
+        __shared__ int skip;
+        if (t == 0)
+            skip = (stop && *reinterpret_cast<volatile int*>(stop)) || ti0 >= ti1 || k0 >= tc_reg;
+        __syncthreads();
+        if (skip) {
+            egs_tail(dec);
+            return;
+        }
+    }
+    SecCtx sc;
+    if constexpr (MODE == 2) {
+        const double T = *sf.thr;
+        sc.tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sc.tbf = float(sc.tb);
+        sc.thr_ok = T >= -1.0;
+    }
+    RcoTally tal;
+    bool list_full = false;
+    unsigned long long surv_local = 0;
+    const int k = k0 + t;
+    const int Q = n / 3, R = n - 3 * Q;
+    const unsigned hmask = R == 1 ? 0xffu : 0xffffu;
+    const int sh = (3 * k) & 3;
+    const uint8_t* colp = img + ((3 * k) & ~3);
+    const int cbase = 3 * k0;                                 // first staged column
+    const int ncols = min(3 * G, 3 * tc_reg - cbase);         // staged columns
+    const unsigned strip_end = unsigned(g.row_hi()) * unsigned(g.ec);
+    // ---- window statistics of the event's rows -> stage buffer (cp.async, private copies)
+    auto stage_of = [&](int b) { return rco_stage + size_t(b) * rco_stage_bytes(G); };
+    auto stage_stats = [&](int ti, int b) {
+        unsigned char* sb = stage_of(b);
+        double* smu = reinterpret_cast<double*>(sb);
+        double* som = smu + 3 * rco_sc(G);
+        uint8_t* sfl = reinterpret_cast<uint8_t*>(som + 3 * rco_sc(G));
+        const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1, crr = (r0 + r1) >> 1;
+#pragma unroll 1
+        for (int rr = 0; rr < 3; ++rr) {
+            const int r = crr - 1 + rr;
+            if (r < r0 || r > r1) continue;
+            const unsigned base = unsigned(r) * unsigned(g.ec) + unsigned(cbase);
+            const unsigned lo2 = base & ~1u, lo4 = base & ~3u;
+            const unsigned end = base + unsigned(ncols);
+            const int n2 = int((end - lo2 + 1) >> 1), n4 = int((end - lo4 + 3) >> 2);
+            for (int i = t; i < n2; i += NT) {
+                const unsigned e0 = lo2 + 2 * i;
+                double* dm = smu + rr * rco_sc(G) + 2 * i;
+                double* dq = som + rr * rco_sc(G) + 2 * i;
+                if (e0 + 2 <= strip_end) {
+                    cp_async16(dm, st.mu + e0);
+                    cp_async16(dq, st.omega + e0);
+                } else {
+                    dm[0] = st.mu[e0];
+                    dq[0] = st.omega[e0];
+                }
+            }
+            for (int i = t; i < n4; i += NT) {
+                const unsigned e0 = lo4 + 4 * i;
+                uint8_t* df = sfl + rr * rco_scf(G) + 4 * i;
+                if (e0 + 4 <= strip_end) {
+                    cp_async4(df, st.flat + e0);
+                } else {
+                    for (unsigned e = e0; e < strip_end; ++e) df[e - e0] = st.flat[e];
+                }
+            }
+        }
+        cp_async_commit();
+    };
+    auto ldrow = [&](int x, unsigned& w0, unsigned& w1) {
+        const uint8_t* p = colp + size_t(max(x, 0)) * P;
+        w0 = __ldg(reinterpret_cast<const unsigned*>(p));
+        w1 = __ldg(reinterpret_cast<const unsigned*>(p + 4));
+    };
+    auto words = [&](unsigned w0, unsigned w1, unsigned (&o)[3]) {
+        const unsigned lo = __funnelshift_r(w0, w1, 8 * sh);
+        const unsigned b4 = (w1 >> (8 * sh)) & 0xffu;
+        o[0] = lo & 0x00ffffffu;
+        o[1] = lo >> 8;
+        o[2] = __byte_perm(lo, b4, 0x5432);
+    };
+    unsigned VL[9], VT[9], HL[HEAD ? 9 : 1], HT[HEAD ? 9 : 1];
+#pragma unroll
+    for (int c = 0; c < 9; ++c) {
+        VL[c] = VT[c] = 0u;
+        if constexpr (HEAD) HL[c] = HT[c] = 0u;
+    }
+    unsigned LW[2][3], TW[2][3];
+    auto step = [&](unsigned (&ring)[2][3], unsigned w0, unsigned w1, unsigned* Vb,
+                    unsigned* Hh) {
+        unsigned nw[3];
+        words(w0, w1, nw);
+        const unsigned a = ring[1][1];
+        const unsigned ah = a & hmask;
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            Vb[0 + dj] = __dp4a(a, ring[0][dj], Vb[0 + dj]);
+            Vb[3 + dj] = __dp4a(a, ring[1][dj], Vb[3 + dj]);
+            Vb[6 + dj] = __dp4a(a, nw[dj], Vb[6 + dj]);
+            if constexpr (HEAD) {
+                Hh[0 + dj] = __dp4a(ah, ring[0][dj], Hh[0 + dj]);
+                Hh[3 + dj] = __dp4a(ah, ring[1][dj], Hh[3 + dj]);
+                Hh[6 + dj] = __dp4a(ah, nw[dj], Hh[6 + dj]);
+            }
+        }
+#pragma unroll
+        for (int dj = 0; dj < 3; ++dj) {
+            ring[0][dj] = ring[1][dj];
+            ring[1][dj] = nw[dj];
+        }
+    };
+    // the first two events' statistics in flight during the warm-up
+    stage_stats(ti0, 0);
+    if (ti0 + 1 < ti1) stage_stats(ti0 + 1, 1);
+    else cp_async_commit();
+    int cr = g.center_row(ti0);
+    {
+        unsigned w0, w1;
+        ldrow(cr - 1, w0, w1);
+        words(w0, w1, LW[0]);
+        ldrow(cr, w0, w1);
+        words(w0, w1, LW[1]);
+#pragma unroll
+        for (int j = 0; j < 3; ++j) {
+            TW[0][j] = LW[0][j];
+            TW[1][j] = LW[1][j];
+        }
+        unsigned pw[3][2];
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ldrow(cr + 1 + i, pw[i][0], pw[i][1]);
+        int x = cr;
+#pragma unroll 1
+        for (; x + 3 <= cr + m; x += 3) {
+            unsigned cw[3][2];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                cw[i][0] = pw[i][0];
+                cw[i][1] = pw[i][1];
+            }
+#pragma unroll
+            for (int i = 0; i < 3; ++i) ldrow(x + 4 + i, pw[i][0], pw[i][1]);
+#pragma unroll
+            for (int i = 0; i < 3; ++i) step(LW, cw[i][0], cw[i][1], VL, HL);
+        }
+#pragma unroll 1
+        for (; x < cr + m; ++x) {
+            unsigned w0b, w1b;
+            ldrow(x + 1, w0b, w1b);
+            step(LW, w0b, w1b, VL, HL);
+        }
+    }
+    const bool owner = t < G && k < tc_reg;
+    const int hi = t + Q;
+    const int whi = (hi - 1) >> 5;
+    const int cc = 3 * k + 1;
+    int par = 0, sbuf = 0;
+#pragma unroll 1
+    for (int ti = ti0;;) {
+        const bool more = ti + 1 < ti1;
+        const int crn = more ? g.center_row(ti + 1) : cr;
+        const bool regular = crn - cr == 3;
+        unsigned pl[3][2], pt[3][2];
+        if (more && regular) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                ldrow(cr + m + 1 + i, pl[i][0], pl[i][1]);
+                ldrow(cr + 1 + i, pt[i][0], pt[i][1]);
+            }
+        }
+        // this event's group record (MODE 2)
+        double ra = 0.0, sa = 0.0;
+        bool dg = false, sd = false;
+        if constexpr (MODE == 2) {
+            if (owner) {
+                const size_t gi = size_t(ti) * g.tc + k;
+                ra = __ldg(sf.rho_c + gi);
+                sa = __ldg(sf.sa_c + gi);
+                dg = __ldg(sf.deg_c + gi);
+                sd = sf.seeded ? __ldg(sf.seeded + gi) != 0 : false;
+            }
+        }
+        unsigned x[9], B[9];
+#pragma unroll
+        for (int c = 0; c < 9; ++c) x[c] = B[c] = VL[c] - VT[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, x[c], o);
+                if (lane >= o) x[c] += u;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < 9; ++c) {
+            Lb[par][c][t] = x[c];
+            if constexpr (HEAD) Hb[par][c][t] = HL[c] - HT[c];
+            if (lane == 31) Wb[par][c][wid] = x[c];
+        }
+        cp_async_wait_1();  // this event's statistics (this thread's copies)
+        __syncthreads();    // ... everyone's, and the published sums
+        // two events ahead into the buffer read by the event before this one
+        if (ti + 2 < ti1) stage_stats(ti + 2, sbuf == 0 ? 2 : sbuf - 1);
+        else cp_async_commit();
+        unsigned sbits = 0;
+        int srr[8], scc[8];
+        unsigned evr[3] = {0u, 0u, 0u};  // retained per member row (EgsDecide::rows_out)
+        if (owner) {
+            const unsigned char* sb = stage_of(sbuf);
+            const double* smu = reinterpret_cast<const double*>(sb);
+            const double* som = smu + 3 * rco_sc(G);
+            const uint8_t* sfl = reinterpret_cast<const uint8_t*>(som + 3 * rco_sc(G));
+            const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1;
+            // centre statistics: middle staged row
+            const unsigned cbk = unsigned(cr) * unsigned(g.ec) + unsigned(cbase);
+            const int cci = cc - cbase;
+            const double mc = smu[rco_sc(G) + int(cbk & 1u) + cci];
+            const double oc = som[rco_sc(G) + int(cbk & 1u) + cci];
+            const bool fc = sfl[rco_scf(G) + int(cbk & 3u) + cci];
+            const double mnmc = __dmul_rn(mn, mc);
+            const unsigned kcen = unsigned(cr) * unsigned(g.ec) + unsigned(cc);
+            if constexpr (MODE == 1) map[kcen] = 1.0;  // autocorr.cpp:92-93
+            if constexpr (MODE == 2) sf.visits[kcen] = 0;
+#pragma unroll
+            for (int c = 0; c < 9; ++c) {
+                if (c == 4) continue;
+                const int di = c / 3 - 1, dj = c % 3 - 1;
+                const int r = cr + di;
+                if (r < r0 || r > r1) continue;
+                unsigned S = Lb[par][c][hi - 1] - (x[c] - B[c]);
+                const unsigned wa = Wb[par][c][wid], wb2 = Wb[par][c][wid + 1];
+                S += wid < whi ? wa : 0u;
+                S += wid + 1 < whi ? wb2 : 0u;
+                if constexpr (HEAD) S += Hb[par][c][hi];
+                const int col = cc + dj;
+                const unsigned kk = unsigned(r) * unsigned(g.ec) + unsigned(col);
+                const unsigned rb = unsigned(r) * unsigned(g.ec) + unsigned(cbase);
+                const int rr = di + 1, ci = col - cbase;
+                const double mm = smu[rr * rco_sc(G) + int(rb & 1u) + ci];
+                const double om = som[rr * rco_sc(G) + int(rb & 1u) + ci];
+                const bool fm = sfl[rr * rco_scf(G) + int(rb & 3u) + ci];
+                const unsigned e0 = tal.evc;
+                const bool sv = rco_member<MODE>(tal, r, col, kk, S, mm, om, fm, mnmc, oc, fc, ra,
+                                                 sa, dg, sd, thr, sc, map, sf);
+                evr[rr] += tal.evc - e0;
+                if constexpr (MODE == 2) {
+                    const int slot = c < 4 ? c : c - 1;
+                    sbits |= unsigned(sv) << slot;
+                    srr[slot] = r;
+                    scc[slot] = col;
+                }
+            }
+        }
+        if constexpr (MODE == 2) rco_list<8>(sbits, srr, scc, sf, list_full, surv_local);
+        if (dec.rows_out) {  // CTA-uniform
+#pragma unroll
+            for (int rr = 0; rr < 3; ++rr) {
+                const unsigned d = __reduce_add_sync(0xffffffffu, evr[rr]);
+                if (lane == 0 && d) atomicAdd(dec.rows_out + (cr - 1 + rr), d);
+            }
+        }
+        par ^= 1;
+        sbuf = sbuf == 2 ? 0 : sbuf + 1;
+        if (!more) break;
+        if (regular) {
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                step(LW, pl[i][0], pl[i][1], VL, HL);
+                step(TW, pt[i][0], pt[i][1], VT, HT);
+            }
+        } else {
+#pragma unroll 1
+            for (int xx = cr; xx < crn; ++xx) {
+                unsigned w0, w1;
+                ldrow(xx + m + 1, w0, w1);
+                step(LW, w0, w1, VL, HL);
+                ldrow(xx + 1, w0, w1);
+                step(TW, w0, w1, VT, HT);
+            }
+        }
+        cr = crn;
+        ++ti;
+    }
+    cp_async_wait_all();
+    rco_finish<MODE>(tal, surv_local, n_r, sf, dec);
+}
+
+// The clipped last group column's epilogue (its members' S from k_rco3_clip_sum, compact
+// [group row][6] layout): one thread per (group row, member slot), rco_member as above.
+template <int MODE>
+__global__ void __launch_bounds__(256)
+    k_rco3_clip_epi(Grid g, const unsigned* __restrict__ Sc, DevStats st, double mn, double thr,
+                    double* __restrict__ map, unsigned long long* __restrict__ n_r, EgsDecide dec,
+                    SecFuse sf) {
+    pdl_wait();
+    SecCtx sc;
+    if constexpr (MODE == 2) {
+        const double T = *sf.thr;
+        sc.tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sc.tbf = float(sc.tb);
+        sc.thr_ok = T >= -1.0;
+    }
+    RcoTally tal;
+    bool list_full = false;
+    unsigned long long surv_local = 0;
+    const int kc = g.tc - 1, gc0 = 3 * kc, gc1 = g.ec - 1, ccol = (gc0 + gc1) >> 1;
+    const int wl = gc1 - gc0 + 1;
+    const int items = (g.ti_hi - g.ti_lo) * 6;
+    const int nit = ((items + 31) / 32) * 32;
+    for (int it = blockIdx.x * blockDim.x + threadIdx.x; it - int(threadIdx.x & 31) < nit;
+         it += gridDim.x * blockDim.x) {
+        if (it - int(threadIdx.x & 31) >= items) break;  // warp-uniform
+        bool sv = false;
+        int r = 0, c = 0;
+        if (it < items) {
+            const int ti = g.ti_lo + it / 6, slot = it % 6;
+            const int di = slot / 2 - 1, dj = slot % 2;
+            const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1, cr = (r0 + r1) >> 1;
+            r = cr + di;
+            c = ccol + dj;
+            if (dj < wl && r >= r0 && r <= r1) {
+                const unsigned k = unsigned(r) * unsigned(g.ec) + unsigned(c);
+                if (di == 0 && dj == 0) {
+                    if constexpr (MODE == 1) map[k] = 1.0;
+                    if constexpr (MODE == 2) sf.visits[k] = 0;
+                } else {
+                    const unsigned kcn = unsigned(cr) * unsigned(g.ec) + unsigned(ccol);
+                    const size_t gi = size_t(ti) * g.tc + kc;
+                    const double mnmc = __dmul_rn(mn, st.mu[kcn]);
+                    double ra = 0.0, sa = 0.0;
+                    bool dg = false, sd = false;
+                    if constexpr (MODE == 2) {
+                        ra = sf.rho_c[gi];
+                        sa = sf.sa_c[gi];
+                        dg = sf.deg_c[gi];
+                        sd = sf.seeded ? sf.seeded[gi] != 0 : false;
+                    }
+                    sv = rco_member<MODE>(tal, r, c, k, Sc[size_t(ti - g.ti_lo) * 6 + slot],
+                                          st.mu[k], st.omega[k], st.flat[k] != 0, mnmc,
+                                          st.omega[kcn], st.flat[kcn] != 0, ra, sa, dg, sd, thr,
+                                          sc, map, sf);
+                }
+            }
+        }
+        if constexpr (MODE == 2) rco_list<1>(unsigned(sv), &r, &c, sf, list_full, surv_local);
+    }
+    rco_finish<MODE>(tal, surv_local, n_r, sf, dec);
+}
+
+// TMATCH_RCO3_FUSED=1 selects the single-kernel form (k_rco3_f) for A/B runs.
+// (measured on C5: 4.13 ms fused vs 2.79 ms for the two kernels -- the fused CTA runs 12
+// warps per SM at 168 registers and its eight serial member epilogues per event leave the
+// SM latency-bound; the streaming epilogue runs at twice the occupancy)
+bool rco3_fused() {
+    static bool on = [] {
+        const char* e = std::getenv("TMATCH_RCO3_FUSED");
+        return e ? std::atoi(e) != 0 : false;
+    }();
+    return on;
+}
+
 struct Rco3Geom {
     int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, tc_reg = 0;
 };
@@ -2345,7 +2928,7 @@ bool rco3_enabled() {
     return on;
 }
 
-Rco3Geom rco3_geom(int m, int n, GridDesc gd) {
+Rco3Geom rco3_geom(int m, int n, GridDesc gd, bool fused) {
     Rco3Geom a{};
     if (gd.h != 3 || gd.w != 3) return a;
     static const int force_nt = [] {
@@ -2360,7 +2943,8 @@ Rco3Geom rco3_geom(int m, int n, GridDesc gd) {
     const int Q = n / 3, R = n % 3;
     if (Q < 1 || Q > 65) return a;  // the window's warp totals span at most two warps
     if (gd.ec < 4) return a;        // k_rco_epi: a 4-location chunk wraps at most one row
-    const int nt = force_nt ? force_nt : 256;
+    const int nt = force_nt ? force_nt : (fused ? 128 : 256);
+    const int resident = fused ? (nt == 128 ? 3 : 1) : 2;  // CTAs per SM
     const int G = nt - Q - (R > 0) + 1;
     if (G < 32) return a;
     a.nt = nt;
@@ -2370,7 +2954,7 @@ Rco3Geom rco3_geom(int m, int n, GridDesc gd) {
     const int rows = gd.ti_hi - gd.ti_lo;
     // segments long enough that the m-row warm-up is a small share of the walk, short enough
     // for a few waves of resident CTAs (2 per SM)
-    const int per_wave = std::max(1, (148 * 2) / std::max(1, a.ntiles));
+    const int per_wave = std::max(1, (148 * resident) / std::max(1, a.ntiles));
     int seg = force_seg > 0 ? force_seg : std::max((rows + per_wave - 1) / per_wave, 1);
     if (!force_seg) seg = std::min(seg, std::max(m, 96));
     a.seg = std::max(1, std::min(seg, std::max(rows, 1)));
@@ -2390,18 +2974,95 @@ void launch_rco3_s(const uint8_t* imgp, int pitch, int m, int n, const Grid& g, 
 bool rco3_aligned(GridDesc gd, const DevStats& st, const SecFuse& sf) {
     const size_t kb = size_t(gd.ti_lo) * gd.h * gd.ec;
     auto al = [](const void* p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; };
+    if (rco3_fused())  // k_rco3_f stages pairs / words at even / 4-aligned global indices
+        return al(st.mu, 16) && al(st.omega, 16) && al(st.flat, 4);
     return al(st.mu + kb, 16) && al(st.omega + kb, 16) && al(st.flat + kb, 4) &&
            (!sf.thr || al(sf.visits + kb, 4));
+}
+
+template <int NT, bool HEAD, int MODE>
+void launch_rco3_f1(const uint8_t* imgp, int pitch, int m, int n, const Grid& g, DevStats st,
+                    double mn, double thr, double* map, unsigned long long* n_r, const Rco3Geom& a,
+                    int* stop, cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+    const size_t smem = kRcoStages * rco_stage_bytes(a.G);
+    static size_t attr = 0;
+    if (attr < smem) {
+        cudaFuncSetAttribute(k_rco3_f<NT, HEAD, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             int(smem));
+        attr = smem;
+    }
+    launch_pdl(k_rco3_f<NT, HEAD, MODE>, dim3(a.ntiles, a.nseg), dim3(NT), smem, s, imgp, pitch, m,
+               n, g, st, mn, thr, map, n_r, a.G, a.seg, a.tc_reg, stop, dec, sf);
+}
+
+template <int NT, bool HEAD>
+void launch_rco3_f2(const uint8_t* imgp, int pitch, int m, int n, const Grid& g, DevStats st,
+                    double mn, double thr, double* map, unsigned long long* n_r, const Rco3Geom& a,
+                    int* stop, cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
+    if (sf.thr)
+        launch_rco3_f1<NT, HEAD, 2>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+    else if (map)
+        launch_rco3_f1<NT, HEAD, 1>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+    else
+        launch_rco3_f1<NT, HEAD, 0>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+}
+
+cudaError_t launch_rco3_fused(const uint8_t* imgp, int pitch, int m, int n, GridDesc gd,
+                              DevStats st, double thr, double* map, unsigned long long* n_r,
+                              int* stop, cudaStream_t s, const EgsDecide& dec, const SecFuse& sf,
+                              Rco3Geom a) {
+    const Grid g = to_grid(gd);
+    const double mn = double(m) * double(n);
+    cudaError_t e = cudaSuccess;
+    unsigned *Rp = nullptr, *Sc = nullptr;
+    if (a.tc_reg < gd.tc) {  // the clipped last group column first (no EGS tail on these)
+        const int cc = 3 * (gd.tc - 1), wl = gd.ec - cc;
+        const int x0 = g.center_row(gd.ti_lo), x1 = g.center_row(gd.ti_hi - 1) + m;
+        const int nx = x1 - x0;
+        const int items = (gd.ti_hi - gd.ti_lo) * 6;
+        e = cudaMallocAsync(reinterpret_cast<void**>(&Rp), size_t(6) * nx * sizeof(unsigned), s);
+        if (e == cudaSuccess)
+            e = cudaMallocAsync(reinterpret_cast<void**>(&Sc), size_t(items) * sizeof(unsigned), s);
+        if (e != cudaSuccess) return e;
+        launch_pdl(k_rco3_clip_rows, dim3(std::min((nx + 7) / 8, 148 * 8)), dim3(256), 0, s, imgp,
+                   pitch, n, cc, x0, nx, Rp);
+        launch_pdl(k_rco3_clip_sum, dim3(std::min((items + 255) / 256, 148 * 4)), dim3(256), 0, s,
+                   Rp, m, g, cc, wl, x0, nx, static_cast<unsigned*>(nullptr), Sc);
+        EgsDecide d0{};  // counts only; the decision rides on the main launch
+        const dim3 cg(std::min((items + 255) / 256, 148 * 4));
+        if (sf.thr)
+            launch_pdl(k_rco3_clip_epi<2>, cg, dim3(256), 0, s, g, Sc, st, mn, thr, map, n_r, d0, sf);
+        else if (map)
+            launch_pdl(k_rco3_clip_epi<1>, cg, dim3(256), 0, s, g, Sc, st, mn, thr, map, n_r, d0, sf);
+        else
+            launch_pdl(k_rco3_clip_epi<0>, cg, dim3(256), 0, s, g, Sc, st, mn, thr, map, n_r, d0, sf);
+    }
+    if (a.ntiles > 0) {
+        const bool head = n % 3 != 0;
+        if (a.nt == 128) {
+            if (head) launch_rco3_f2<128, true>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+            else launch_rco3_f2<128, false>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+        } else {
+            if (head) launch_rco3_f2<256, true>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+            else launch_rco3_f2<256, false>(imgp, pitch, m, n, g, st, mn, thr, map, n_r, a, stop, s, dec, sf);
+        }
+    }
+    e = cudaGetLastError();
+    if (Rp) cudaFreeAsync(Rp, s);
+    if (Sc) cudaFreeAsync(Sc, s);
+    return e;
 }
 
 cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc gd, DevStats st,
                         double thr, double* map, unsigned long long* n_r, int* stop,
                         cudaStream_t s, const EgsDecide& dec, const SecFuse& sf) {
-    const Rco3Geom a = rco3_geom(m, n, gd);
+    const Rco3Geom a = rco3_geom(m, n, gd, rco3_fused());
     if (a.nt == 0) return cudaErrorInvalidValue;
     const Grid g = to_grid(gd);
     const int row_lo = g.row_lo(), row_hi = g.row_hi();
     if (row_hi <= row_lo) return cudaSuccess;
+    if (rco3_fused())
+        return launch_rco3_fused(imgp, pitch, m, n, gd, st, thr, map, n_r, stop, s, dec, sf, a);
     const size_t cells = size_t(row_hi - row_lo) * gd.ec;
     unsigned* Sbuf = nullptr;
     cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&Sbuf),
@@ -2429,7 +3090,7 @@ cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc g
                    pitch, n, cc, x0, nx, Rp);
         const int items = (gd.ti_hi - gd.ti_lo) * 6;
         launch_pdl(k_rco3_clip_sum, dim3(std::min((items + 255) / 256, 148 * 4)), dim3(256), 0, s,
-                   Rp, m, g, cc, wl, x0, nx, S);
+                   Rp, m, g, cc, wl, x0, nx, S, static_cast<unsigned*>(nullptr));
     }
     const double mn = double(m) * double(n);
     const int blocks = std::min(row_hi - row_lo, 148 * 8);
@@ -2441,15 +3102,24 @@ cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc g
     auto epi = [&](auto kern) {
         launch_pdl(kern, dim3(blocks), dim3(256), 0, s, g, S, st, mn, thr, map, n_r, stop, dec, sf);
     };
+    static const int vw = [] {  // TMATCH_EPI_V: locations per thread (2 or 4)
+        const char* e = std::getenv("TMATCH_EPI_V");
+        return (e && std::atoi(e) == 2) ? 2 : 4;
+    }();
     const int mode = sf.thr ? 2 : (map ? 1 : 0);
     if (mode == 2) {
-        if (minb == 3) epi(k_rco_epi<2, 3>);
-        else if (minb == 4) epi(k_rco_epi<2, 4>);
-        else epi(k_rco_epi<2, 2>);
+        if (vw == 2) {
+            if (minb == 4) epi(k_rco_epi<2, 4, 2>);
+            else epi(k_rco_epi<2, 3, 2>);
+        } else {
+            if (minb == 4) epi(k_rco_epi<2, 4, 4>);
+            else if (minb == 2) epi(k_rco_epi<2, 2, 4>);
+            else epi(k_rco_epi<2, 3, 4>);
+        }
     } else if (mode == 1) {
-        epi(k_rco_epi<1, 3>);
+        epi(k_rco_epi<1, 3, 4>);
     } else {
-        epi(k_rco_epi<0, 3>);
+        epi(k_rco_epi<0, 3, 4>);
     }
     e = cudaGetLastError();
     cudaFreeAsync(Sbuf, s);
@@ -2770,8 +3440,10 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
         const EgsDecide d = dec ? *dec : EgsDecide{};
         const SecFuse f = fuse ? *fuse : SecFuse{};
         if (decided) *decided = d.ticket != nullptr;
-        if (gd.h == 3 && rco3_enabled() && rco3_geom(m, n, gd).nt > 0 && rco3_aligned(gd, st, f)) {
-            if (launches) *launches = rco3_geom(m, n, gd).tc_reg < gd.tc ? 4 : 2;
+        if (gd.h == 3 && rco3_enabled() && rco3_geom(m, n, gd, rco3_fused()).nt > 0 && rco3_aligned(gd, st, f)) {
+            if (launches)
+                *launches = rco3_geom(m, n, gd, rco3_fused()).tc_reg < gd.tc ? 4
+                            : rco3_fused()                                  ? 1 : 2;
             return launch_rco3(imgp, pitch, m, n, gd, st, retain_threshold, map, n_r, stop, s, d,
                                f);
         }
