@@ -973,9 +973,25 @@ __global__ void __launch_bounds__(NT)
     constexpr int SW = acg_span(NT, H);  // staged bytes per ring row
     constexpr int NCH = SW / 16;
     const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
-    const int dj = int(blockIdx.x) - hr;
-    const int k0 = (int(blockIdx.y) + tile_base) * G;
-    const int zseg = dec.zorder ? dec.zorder[blockIdx.z] : int(blockIdx.z);
+    // Launch order: (dj, tile, segment) with dj fastest.  A count-only candidate with a
+    // segment order (EgsDecide::zorder) runs dj slowest instead, the outer column offsets
+    // first (|dj| = hr members are retained about twice as often as the inner ones: C5,
+    // h = 5: 65 % vs 26-34 %), segments densest first, so its in-kernel rejection comes
+    // after fewer CTAs (any subset count reaching the bound rejects: the test is monotone).
+    int bdj = int(blockIdx.x), btile = int(blockIdx.y), bseg = int(blockIdx.z);
+    if (dec.zorder) {
+        const int ny = int(gridDim.y), nz = int(gridDim.z);
+        const int L = int(blockIdx.x) + int(gridDim.x) * (int(blockIdx.y) + ny * int(blockIdx.z));
+        const int djr = L / (ny * nz), rem = L - djr * (ny * nz);
+        bseg = dec.zorder[rem / ny];
+        btile = rem - (rem / ny) * ny;
+        // rank -> offset: -hr, +hr, -(hr-1), +(hr-1), ..., 0
+        const int mag = hr - (djr >> 1);
+        bdj = hr + ((djr & 1) ? mag : -mag);
+    }
+    const int dj = bdj - hr;
+    const int k0 = (btile + tile_base) * G;
+    const int zseg = bseg;
     const int ti0 = g.ti_lo + zseg * seg;
     const int ti1 = min(ti0 + seg, g.ti_hi);
     {
