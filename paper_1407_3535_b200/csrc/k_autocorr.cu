@@ -1569,11 +1569,14 @@ __global__ void __launch_bounds__(1024)
                 int* __restrict__ order) {
     pdl_wait();
     extern __shared__ unsigned long long segc[];
-    for (int z = threadIdx.x; z < nseg; z += blockDim.x) segc[z] = 0ull;
-    __syncthreads();
-    const int r_lo = ti_lo * h, r_hi = min((ti_lo + nseg * seg) * h, er);
-    for (int r = r_lo + int(threadIdx.x); r < r_hi; r += blockDim.x)
-        if (rows[r]) atomicAdd(&segc[(r / h - ti_lo) / seg], (unsigned long long)rows[r]);
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+    for (int z = wid; z < nseg; z += blockDim.x >> 5) {  // one warp per segment
+        const int r0 = (ti_lo + z * seg) * h, r1 = min((ti_lo + (z + 1) * seg) * h, er);
+        unsigned long long c = 0;
+        for (int r = r0 + lane; r < r1; r += 32) c += rows[r];
+        c = warp_sum(c);
+        if (lane == 0) segc[z] = c;
+    }
     __syncthreads();
     for (int z = threadIdx.x; z < nseg; z += blockDim.x) {
         const unsigned long long c = segc[z];

@@ -10,7 +10,11 @@ import json
 import subprocess
 import sys
 
-PHASE = [("k_acg<3, 256, 0, 1>", "autocorr_sec"), ("k_acg<5, 128", "autocorr_count"),
+# (the kernels of a phase are summed: the two-pass h = 3 R_co is k_rco3_s + k_rco_epi + the
+# clipped-column passes; one search is assumed per report)
+PHASE = [("k_acg<3, 256, 0, 1>", "autocorr_sec"), ("k_rco3_s", "autocorr_sec"),
+         ("k_rco_epi<2", "autocorr_sec"), ("k_rco3_clip", "autocorr_sec"),
+         ("k_acg<5, 128", "autocorr_count"),
          ("k_wstats4", "window_stats"), ("k_tc_corr<1>", "centre_scan"),
          ("k_centre_epi", "centre_scan_epilogue"), ("k_tc_corr<2>", "survivor_eval"),
          ("k_sec_rows_multi", "sec_multi")]
@@ -32,7 +36,8 @@ for r in rows[2:]:
         1e3 if u["gpu__time_duration.sum"] == "msecond" else 1.0)
     res["kernels"][name[:90]] = {"dram_bytes": b, "time_us": t_us}
     for key, ph in PHASE:
-        if key in name and ph not in res["phases"]:
-            res["phases"][ph] = b
+        if key in name:
+            res["phases"][ph] = res["phases"].get(ph, 0.0) + b
+            break
 json.dump(res, open(sys.argv[2], "w"), indent=1)
 print(json.dumps(res["phases"], indent=1))
