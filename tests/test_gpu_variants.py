@@ -2,7 +2,9 @@
 the oracle's bits too.  The switches are read once per process, so every variant runs in
 a subprocess: window statistics, R_co maps and retained counts for h = 3, 5, 7 on four
 image shapes (multi-tile; clipped and unclipped group columns; n % h = 0 and != 0, i.e.
-every packed-walk part layout), compared with the oracle."""
+every packed-walk part layout), compared with the oracle; and one full frozen-policy
+search per shape (the fused R_co + scan-2 path of tm_search) against the oracle's
+`--parallel` match: location, rho bits, eliminated / retained / ops."""
 import os
 import subprocess
 import sys
@@ -35,6 +37,13 @@ for (rows, cols, m, n) in ((150, 1300, 40, 64), (120, 700, 33, 10), (140, 1063, 
         got = ctx.local_autocorrelation(gi, m, n, h, h)
         assert np.array_equal(got, want), ("map", h)
         assert ctx.autocorr_retained(gi, m, n, h, h) == port.retained_count(want, h, h), ("n_r", h)
+    r0, c0 = rows // 3, cols // 2
+    t = img[r0:r0 + m, c0:c0 + n].astype(np.float64)
+    t = np.clip(np.rint(t * 0.9 + 7 + rng.normal(0, 3, t.shape)), 0, 255)
+    got = ctx.search(gi, t, mode="egs", policy="frozen", parallel=True, threads=2)
+    want = port.match(t, img.astype(np.float64), mode="egs", parallel=True)
+    for f in ("best_row", "best_col", "best_rho", "eliminated", "retained", "ops"):
+        assert getattr(got, f) == getattr(want, f), ("search", f, getattr(got, f), getattr(want, f))
     gi.close()
 ctx.close()
 print("ok")
@@ -55,6 +64,14 @@ print("ok")
     {"TMATCH_WSTATS4": "256x4"},
     {"TMATCH_WSTATS4": "128x4"},
     {"TMATCH_WSTATS4": "128x2"},
+    {"TMATCH_RCO3": "0"},
+    {"TMATCH_RCO3": "0", "TMATCH_ACG_PACK": "1"},
+    {"TMATCH_RCO3_FUSED": "1"},
+    {"TMATCH_RCO3_FUSED": "1", "TMATCH_RCO3_NT": "256"},
+    {"TMATCH_RCO3_NT": "128"},
+    {"TMATCH_EPI_V": "2"},
+    {"TMATCH_EPI_MINB": "2"},
+    {"TMATCH_EGS_ORDER": "0"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_kernel_variant_parity(env):
     full = dict(os.environ)
