@@ -2933,6 +2933,102 @@ bool rco3_fused() {
     return on;
 }
 
+// k_rco_epg<MODE, MINB>: pass 2 of the h = 3 R_co with thread = one group's 3-column segment
+// of an extent row (CTA = extent rows, grid-strided): the three locations share the group's
+// centre statistics and record, so nothing is selected per location; S, mu, omega and the
+// flags of the segment are three coalesced scalar loads each (the warp reads 96 consecutive
+// locations).  Same decisions as k_rco_epi (rco_member).
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_rco_epg(Grid g, const unsigned* __restrict__ Sin, DevStats st, double mn, double thr,
+              double* __restrict__ map, unsigned long long* __restrict__ n_r, int* stop,
+              EgsDecide dec, SecFuse sf) {
+    pdl_wait();
+    {
+        __shared__ int skip;
+        if (threadIdx.x == 0) skip = stop && *reinterpret_cast<volatile int*>(stop);
+        __syncthreads();
+        if (skip) {
+            egs_tail(dec);
+            return;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+    SecCtx sc;
+    if constexpr (MODE == 2) {
+        const double T = *sf.thr;
+        sc.tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sc.tbf = float(sc.tb);
+        sc.thr_ok = T >= -1.0;
+    }
+    RcoTally tal;
+    bool list_full = false;
+    unsigned long long surv_local = 0;
+    const int r_lo = g.row_lo(), r_hi = g.row_hi();
+    const int ntj = ((g.tc + 31) / 32) * 32;  // whole warps per row (ballots)
+    for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const unsigned evc_row = tal.evc;
+        const int ti = g.tile_r(r);
+        const int cr = g.center_row(ti);
+        const unsigned krow = unsigned(r) * unsigned(g.ec), kcrow = unsigned(cr) * unsigned(g.ec);
+        const unsigned gbase = unsigned(ti) * unsigned(g.tc);
+        for (int tj = threadIdx.x; tj < ntj; tj += blockDim.x) {
+            const bool active = tj < g.tc;
+            const int tq = active ? tj : 0;
+            const int c0 = 3 * tq, c1 = min(c0 + 3, g.ec) - 1, ccol = (c0 + c1) >> 1;
+            const int nc = c1 - c0 + 1;
+            unsigned sv[3];
+            double mm[3], om[3];
+            bool fm[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const unsigned k = krow + unsigned(c0 + min(j, nc - 1));
+                sv[j] = __ldg(Sin + k);
+                mm[j] = __ldg(st.mu + k);
+                om[j] = __ldg(st.omega + k);
+                fm[j] = __ldg(st.flat + k) != 0;
+            }
+            const unsigned kc = kcrow + unsigned(ccol);
+            const double mc = __ldg(st.mu + kc), oc = __ldg(st.omega + kc);
+            const bool fc = __ldg(st.flat + kc) != 0;
+            double ra = 0.0, sa = 0.0;
+            bool dg = false, sd = false;
+            if constexpr (MODE == 2) {
+                const unsigned gi = gbase + unsigned(tq);
+                ra = __ldg(sf.rho_c + gi);
+                sa = __ldg(sf.sa_c + gi);
+                dg = __ldg(sf.deg_c + gi) != 0;
+                sd = sf.seeded ? __ldg(sf.seeded + gi) != 0 : false;
+            }
+            const double mnmc = __dmul_rn(mn, mc);
+            unsigned sbits = 0;
+            int srr[3], scc[3];
+#pragma unroll
+            for (int j = 0; j < 3; ++j) {
+                const int c = c0 + j;
+                srr[j] = r;
+                scc[j] = c;
+                if (!active || j >= nc) continue;
+                const unsigned k = krow + unsigned(c);
+                if (r == cr && c == ccol) {  // the group's centre (autocorr.cpp:92-93)
+                    if constexpr (MODE == 1) map[k] = 1.0;
+                    if constexpr (MODE == 2) sf.visits[k] = 0;
+                    continue;
+                }
+                const bool s = rco_member<MODE>(tal, r, c, k, sv[j], mm[j], om[j], fm[j], mnmc, oc,
+                                                fc, ra, sa, dg, sd, thr, sc, map, sf);
+                sbits |= unsigned(s) << j;
+            }
+            if constexpr (MODE == 2) rco_list<3>(sbits, srr, scc, sf, list_full, surv_local);
+        }
+        if (dec.rows_out) {  // CTA-uniform
+            const unsigned d = __reduce_add_sync(0xffffffffu, tal.evc - evc_row);
+            if (lane == 0 && d) atomicAdd(dec.rows_out + r, d);
+        }
+    }
+    rco_finish<MODE>(tal, surv_local, n_r, sf, dec);
+}
+
 struct Rco3Geom {
     int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, tc_reg = 0;
 };
@@ -3121,12 +3217,23 @@ cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc g
     auto epi = [&](auto kern) {
         launch_pdl(kern, dim3(blocks), dim3(256), 0, s, g, S, st, mn, thr, map, n_r, stop, dec, sf);
     };
-    static const int vw = [] {  // TMATCH_EPI_V: locations per thread (2 or 4)
-        const char* e = std::getenv("TMATCH_EPI_V");
-        return (e && std::atoi(e) == 2) ? 2 : 4;
+    static const int vw = [] {  // TMATCH_EPI_V: 2 or 4 aligned locations per thread, or 3
+        const char* e = std::getenv("TMATCH_EPI_V");  // (default): one group segment each
+        const int v = e ? std::atoi(e) : 3;
+        return (v == 2 || v == 4) ? v : 3;
     }();
     const int mode = sf.thr ? 2 : (map ? 1 : 0);
-    if (mode == 2) {
+    if (vw == 3) {
+        if (mode == 2) {  // (4 resident CTAs unless TMATCH_EPI_MINB says otherwise)
+            if (minb == 3 && std::getenv("TMATCH_EPI_MINB")) epi(k_rco_epg<2, 3>);
+            else if (minb == 2) epi(k_rco_epg<2, 2>);
+            else epi(k_rco_epg<2, 4>);
+        } else if (mode == 1) {
+            epi(k_rco_epg<1, 3>);
+        } else {
+            epi(k_rco_epg<0, 3>);
+        }
+    } else if (mode == 2) {
         if (vw == 2) {
             if (minb == 4) epi(k_rco_epi<2, 4, 2>);
             else epi(k_rco_epi<2, 3, 2>);
