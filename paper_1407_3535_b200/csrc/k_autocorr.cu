@@ -998,8 +998,13 @@ __global__ void __launch_bounds__(NT)
         // skipped candidate (an earlier decision stopped EGS) or empty block: one read of
         // the flag per block so the exit is uniform
         __shared__ int skip;
+        // phase B after k_rco5_s / k_rco5_cnt: an outer-offset CTA runs only for the tile
+        // holding the clipped last group column (if any), for that group alone
+        const int wlc = g.ec - (g.tc - 1) * W;
+        const bool outer_skip = dec.outer_done && (dj == -hr || dj == hr) &&
+                                !(wlc < W && g.tc - 1 >= k0 && g.tc - 1 < k0 + G);
         if (t == 0) skip = (stop && *reinterpret_cast<volatile int*>(stop)) || ti0 >= ti1 ||
-                           k0 >= g.tc;
+                           k0 >= g.tc || outer_skip;
         __syncthreads();
         if (skip) {
             egs_tail(dec);
@@ -1247,7 +1252,8 @@ __global__ void __launch_bounds__(NT)
     }
     const double mn = double(m) * double(n);
     // this thread's group: members (di, dj) of group column k, all h row offsets
-    const bool owner = t < G && k < g.tc;
+    const bool owner = t < G && k < g.tc &&
+                       !(dec.outer_done && (dj == -hr || dj == hr) && k != g.tc - 1);
     const int gc0 = k * W, gc1 = min(gc0 + W, g.ec) - 1;
     const int cc = (gc0 + gc1) >> 1;
     const int c = cc + dj;
@@ -1589,6 +1595,294 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// ---- Count-only 5x5 candidate, phase A: the outer column offsets in two passes -----------
+//
+// A rejected EGS candidate needs only SOME members whose retained count reaches the
+// rejection bound (the test is monotone in n_r), and the members at dj = +-2 are retained
+// about twice as often as the others (C5: 65 % vs 26-34 %).  Phase A counts exactly those
+// members of the regular group columns: k_rco5_s walks them (thread = group column, the ten
+// offsets di in [-2, 2] x dj = +-2; per row step and offset one dp4a over the first four
+// columns of the block + one IMAD for the fifth, + one masked dp4a for the head when
+// n % 5 != 0) and stores their cross sums; k_rco5_cnt evaluates the retained test
+// (autocorr.cpp:84-88, egs.cpp:12-25) with the in-kernel rejection of k_acg.  If the
+// candidate survives, phase B (k_acg with EgsDecide::outer_done) counts the remaining
+// members -- dj in {-1, 0, 1} and the clipped last column -- and decides on its tail.
+template <int NT, bool HEAD>
+__global__ void __launch_bounds__(NT, NT == 128 ? 3 : 1)
+    k_rco5_s(const uint8_t* __restrict__ img, int P, int m, int n, Grid g,
+             unsigned* __restrict__ Sout, int G, int seg, int tc_reg, const int* __restrict__ stop) {
+    constexpr int NW = NT / 32, NC = 10;
+    __shared__ unsigned Lb[2][NC][NT];
+    __shared__ unsigned Hb[2][HEAD ? NC : 1][NT];
+    __shared__ unsigned Wb[2][NC][NW + 2];
+    pdl_wait();
+    const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+    const int k0 = int(blockIdx.x) * G;
+    const int ti0 = g.ti_lo + int(blockIdx.y) * seg;
+    const int ti1 = min(ti0 + seg, g.ti_hi);
+    if ((stop && *reinterpret_cast<const volatile int*>(stop)) || ti0 >= ti1 || k0 >= tc_reg)
+        return;
+    const int k = k0 + t;
+    const int Q = n / 5, R = n - 5 * Q;
+    const unsigned hmask = R >= 4 ? 0xffffffffu : ((1u << (8 * R)) - 1u);
+    const int sh = (5 * k) & 3;
+    const uint8_t* colp = img + ((5 * k) & ~3);
+    // one row: A = I(x, 5k+2 .. 5k+6), B(-2) = I(x, 5k .. 5k+4), B(+2) = I(x, 5k+4 .. 5k+8)
+    struct Row {
+        unsigned aw, ab, mw, mb, pw, pb;
+    };
+    auto ldrow = [&](int x, unsigned (&w)[3]) {
+        const uint8_t* p = colp + size_t(max(x, 0)) * P;
+        w[0] = __ldg(reinterpret_cast<const unsigned*>(p));
+        w[1] = __ldg(reinterpret_cast<const unsigned*>(p + 4));
+        w[2] = __ldg(reinterpret_cast<const unsigned*>(p + 8));
+    };
+    auto unpack = [&](const unsigned (&w)[3]) {
+        Row r;
+        const unsigned lo = __funnelshift_r(w[0], w[1], 8 * sh);   // bytes 5k   .. 5k+3
+        const unsigned mid = __funnelshift_r(w[1], w[2], 8 * sh);  // bytes 5k+4 .. 5k+7
+        const unsigned top = (w[2] >> (8 * sh)) & 0xffu;           // byte  5k+8
+        r.mw = lo;
+        r.mb = mid & 0xffu;
+        r.pw = mid;
+        r.pb = top;
+        r.aw = __funnelshift_r(lo, mid, 16);  // bytes 5k+2 .. 5k+5
+        r.ab = (mid >> 16) & 0xffu;           // byte  5k+6
+        return r;
+    };
+    unsigned VL[NC], VT[NC], HL[HEAD ? NC : 1], HT[HEAD ? NC : 1];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+        VL[c] = VT[c] = 0u;
+        if constexpr (HEAD) HL[c] = HT[c] = 0u;
+    }
+    Row LR[4], TR[4];  // rows x-2 .. x+1 at the lead / trail position
+    // one row step: A row x (ring[2]), B rows x-2 .. x+2 (ring[0..3], nr)
+    auto step = [&](Row (&ring)[4], const Row& nr, unsigned* Vb, unsigned* Hh) {
+        const unsigned a = ring[2].aw, ab = ring[2].ab, ah = a & hmask;
+#pragma unroll
+        for (int d = 0; d < 5; ++d) {
+            const Row& b = d < 4 ? ring[d] : nr;
+            Vb[2 * d] = __dp4a(a, b.mw, Vb[2 * d]) + ab * b.mb;
+            Vb[2 * d + 1] = __dp4a(a, b.pw, Vb[2 * d + 1]) + ab * b.pb;
+            if constexpr (HEAD) {
+                Hh[2 * d] = __dp4a(ah, b.mw, Hh[2 * d]);
+                Hh[2 * d + 1] = __dp4a(ah, b.pw, Hh[2 * d + 1]);
+            }
+        }
+#pragma unroll
+        for (int i = 0; i < 3; ++i) ring[i] = ring[i + 1];
+        ring[3] = nr;
+    };
+    int cr = g.center_row(ti0);
+    {
+        unsigned w[3];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            ldrow(cr - 2 + i, w);
+            LR[i] = unpack(w);
+            TR[i] = LR[i];
+        }
+        // warm-up: lead rows [cr, cr + m), loads one step ahead
+        unsigned pw[3];
+        ldrow(cr + 2, pw);
+#pragma unroll 1
+        for (int x = cr; x < cr + m; ++x) {
+            const Row nr = unpack(pw);
+            if (x + 1 < cr + m) ldrow(x + 3, pw);
+            step(LR, nr, VL, HL);
+        }
+    }
+    const bool owner = t < G && k < tc_reg;
+    const int hi = t + Q;
+    const int whi = (hi - 1) >> 5;
+    const int cc = 5 * k + 2;
+    int par = 0;
+#pragma unroll 1
+    for (int ti = ti0;;) {
+        const bool more = ti + 1 < ti1;
+        const int crn = more ? g.center_row(ti + 1) : cr;
+        const bool regular = crn - cr == 5;
+        unsigned pl[5][3], pt[5][3];
+        if (more && regular) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                ldrow(cr + m + 2 + i, pl[i]);
+                ldrow(cr + 2 + i, pt[i]);
+            }
+        }
+        unsigned x[NC], B[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) x[c] = B[c] = VL[c] - VT[c];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const unsigned u = __shfl_up_sync(0xffffffffu, x[c], o);
+                if (lane >= o) x[c] += u;
+            }
+        }
+#pragma unroll
+        for (int c = 0; c < NC; ++c) {
+            Lb[par][c][t] = x[c];
+            if constexpr (HEAD) Hb[par][c][t] = HL[c] - HT[c];
+            if (lane == 31) Wb[par][c][wid] = x[c];
+        }
+        __syncthreads();
+        if (owner) {
+            const int r0 = ti * 5, r1 = min(r0 + 5, g.er) - 1;
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int di = c / 2 - 2, dj = (c & 1) ? 2 : -2;
+                const int r = cr + di;
+                if (r < r0 || r > r1) continue;
+                unsigned S = Lb[par][c][hi - 1] - (x[c] - B[c]);
+                const unsigned wa = Wb[par][c][wid], wb2 = Wb[par][c][wid + 1];
+                S += wid < whi ? wa : 0u;
+                S += wid + 1 < whi ? wb2 : 0u;
+                if constexpr (HEAD) S += Hb[par][c][hi];
+                // compact layout [extent row][group column][dj = -2, +2]
+                Sout[(size_t(r - g.row_lo()) * tc_reg + k) * 2 + (c & 1)] = S;
+            }
+        }
+        par ^= 1;
+        if (!more) break;
+        if (regular) {
+#pragma unroll
+            for (int i = 0; i < 5; ++i) {
+                step(LR, unpack(pl[i]), VL, HL);
+                step(TR, unpack(pt[i]), VT, HT);
+            }
+        } else {
+#pragma unroll 1
+            for (int xx = cr; xx < crn; ++xx) {
+                unsigned w[3];
+                ldrow(xx + m + 2, w);
+                step(LR, unpack(w), VL, HL);
+                ldrow(xx + 2, w);
+                step(TR, unpack(w), VT, HT);
+            }
+        }
+        cr = crn;
+        ++ti;
+    }
+}
+
+// Phase A's retained count of the dj = +-2 members of the regular group columns: CTA =
+// extent rows (grid-strided), thread = one group's two outer columns of a row; the CTA's
+// count is flushed every row and the rejection test of k_acg replayed on the running
+// total (sets *stop: later rows, phase B and the decision see it).
+__global__ void __launch_bounds__(256)
+    k_rco5_cnt(Grid g, const unsigned* __restrict__ Sin, DevStats st, double mn, double thr,
+               int tc_reg, unsigned long long* __restrict__ n_r, int* stop,
+               const double* __restrict__ egs_prev, double egs_central, double egs_xi) {
+    pdl_wait();
+    __shared__ unsigned cta_cnt;
+    __shared__ int quit;
+    if (threadIdx.x == 0) {
+        cta_cnt = 0u;
+        quit = *reinterpret_cast<volatile int*>(stop);
+    }
+    __syncthreads();
+    if (quit) return;
+    const int lane = threadIdx.x & 31;
+    const double prev = *egs_prev;
+    const bool can_reject = fabs(prev) <= 1.7976931348623157e308;
+    const int r_lo = g.row_lo(), r_hi = g.row_hi();
+    for (int r = r_lo + blockIdx.x; r < r_hi; r += gridDim.x) {
+        const int ti = g.tile_r(r);
+        const int cr = g.center_row(ti);
+        const unsigned krow = unsigned(r) * unsigned(g.ec), kcrow = unsigned(cr) * unsigned(g.ec);
+        unsigned cnt = 0;
+        const uint2* srow = reinterpret_cast<const uint2*>(Sin) + size_t(r - r_lo) * tc_reg;
+        for (int tj = threadIdx.x; tj < tc_reg; tj += blockDim.x) {
+            const int cc = 5 * tj + 2;
+            const unsigned kc = kcrow + unsigned(cc), km = krow + unsigned(cc - 2),
+                           kp = krow + unsigned(cc + 2);
+            // every load first (independent), then the two retained tests
+            const uint2 sv = __ldg(srow + tj);
+            const double mc = __ldg(st.mu + kc), oc = __ldg(st.omega + kc);
+            const double mm0 = __ldg(st.mu + km), om0 = __ldg(st.omega + km);
+            const double mm1 = __ldg(st.mu + kp), om1 = __ldg(st.omega + kp);
+            const bool fc = __ldg(st.flat + kc) != 0;
+            const bool f0 = fc || __ldg(st.flat + km) != 0, f1 = fc || __ldg(st.flat + kp) != 0;
+            const double mnmc = __dmul_rn(mn, mc);
+            const double n0 = __dsub_rn(double(sv.x), __dmul_rn(mnmc, mm0));
+            const double n1 = __dsub_rn(double(sv.y), __dmul_rn(mnmc, mm1));
+            if (f0 ? 0.0 < thr : retained_below(n0, __dmul_rn(oc, om0), thr)) ++cnt;
+            if (f1 ? 0.0 < thr : retained_below(n1, __dmul_rn(oc, om1), thr)) ++cnt;
+        }
+        cnt = __reduce_add_sync(0xffffffffu, cnt);
+        if (lane == 0 && cnt) atomicAdd(&cta_cnt, cnt);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            const unsigned c = cta_cnt;
+            cta_cnt = 0u;
+            int q = *reinterpret_cast<volatile int*>(stop);
+            if (c) {
+                const unsigned long long tot = atomicAdd(n_r, (unsigned long long)c) + c;
+                const double total = __dadd_rn(__dadd_rn(egs_central, double(tot)), 0.0);
+                if (can_reject && !(__dsub_rn(prev, total) > __dmul_rn(egs_xi, prev))) {
+                    *reinterpret_cast<volatile int*>(stop) = 1;
+                    q = 1;
+                }
+            }
+            quit = q;
+        }
+        __syncthreads();
+        if (quit) return;
+    }
+}
+
+// Phase A launcher (count-only h = 5 with in-kernel rejection): S raster of the outer
+// members, k_rco5_s, k_rco5_cnt.  False: not applicable (phase B then counts everything).
+// TMATCH_RCO5=0 disables it.
+bool rco5_phase_a(const uint8_t* imgp, int pitch, int m, int n, GridDesc gd, DevStats st,
+                  double thr, unsigned long long* n_r, int* stop, const double* egs_prev,
+                  double egs_central, double egs_xi, cudaStream_t s) {
+    static const bool on = [] {
+        const char* e = std::getenv("TMATCH_RCO5");
+        return !(e && std::atoi(e) == 0);
+    }();
+    if (!on || gd.h != 5 || gd.w != 5 || gd.ec < 5) return false;
+    const int Q = n / 5, R = n % 5;
+    constexpr int NT = 128;
+    const int G = NT - Q - (R > 0) + 1;
+    if (Q < 1 || Q > 65 || G < 32) return false;
+    const int tc_reg = gd.ec % 5 == 0 ? gd.tc : gd.tc - 1;
+    if (tc_reg < 1) return false;
+    const int ntiles = (tc_reg + G - 1) / G;
+    const int rows = gd.ti_hi - gd.ti_lo;
+    const int per_wave = std::max(1, (148 * 3) / ntiles);
+    int seg = std::max(1, (rows + per_wave - 1) / per_wave);
+    seg = std::min(seg, std::max(m / 5 + 1, 40));
+    const int nseg = (rows + seg - 1) / seg;
+    const Grid g = to_grid(gd);
+    // (only worth it with several waves of the count kernel: one wave has no order to use;
+    // TMATCH_RCO5_MIN overrides the minimum extent, e.g. 0 for the variant tests)
+    static const double min_extent = [] {
+        const char* e = std::getenv("TMATCH_RCO5_MIN");
+        return e ? std::atof(e) : 3.2e7;
+    }();
+    if (double(gd.er) * double(gd.ec) < min_extent) return false;
+    const size_t cells = size_t(g.row_hi() - g.row_lo()) * tc_reg * 2;
+    unsigned* Sbuf = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void**>(&Sbuf), cells * sizeof(unsigned), s) != cudaSuccess)
+        return false;
+    unsigned* S = Sbuf;  // compact [extent row - row_lo][tc_reg][2]
+    if (R > 0)
+        launch_pdl(k_rco5_s<NT, true>, dim3(ntiles, nseg), dim3(NT), 0, s, imgp, pitch, m, n, g, S,
+                   G, seg, tc_reg, static_cast<const int*>(stop));
+    else
+        launch_pdl(k_rco5_s<NT, false>, dim3(ntiles, nseg), dim3(NT), 0, s, imgp, pitch, m, n, g,
+                   S, G, seg, tc_reg, static_cast<const int*>(stop));
+    const int blocks = std::min(g.row_hi() - g.row_lo(), 148 * 8);
+    launch_pdl(k_rco5_cnt, dim3(blocks), dim3(256), 0, s, g, static_cast<const unsigned*>(S), st,
+               double(m) * double(n), thr, tc_reg, n_r, stop, egs_prev, egs_central, egs_xi);
+    cudaFreeAsync(Sbuf, s);
+    return cudaGetLastError() == cudaSuccess;
+}
+
 struct AcgGeom {
     int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, SW = 0, RR = 0;
     size_t smem = 0;
@@ -1687,6 +1981,13 @@ cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, Gr
     const int t1 = tile_hi < 0 ? a.ntiles : std::min(tile_hi, a.ntiles);
     dim3 grid(gd.w, std::max(0, t1 - tile_lo), a.nseg);
     EgsDecide d = dec;
+    if constexpr (H == 5 && !FUSE) {
+        if (!map && stop && egs_prev && gd.ti_hi > gd.ti_lo && rco5_phase_a(imgp, pitch, m, n, gd,
+                                                                            st, thr, n_r, stop,
+                                                                            egs_prev, egs_central,
+                                                                            egs_xi, s))
+            d.outer_done = 1;
+    }
     int* order = nullptr;
     // (only when the launch runs in several waves: one wave has no order to exploit)
     const long long waves = (long long)grid.x * grid.y * grid.z / std::max(1, 148 * occ);

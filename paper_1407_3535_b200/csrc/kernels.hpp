@@ -125,6 +125,9 @@ struct EgsDecide {
     unsigned* rows_out = nullptr;
     const unsigned* rows_in = nullptr;
     const int* zorder = nullptr;
+    // phase B of a two-phase count-only candidate (k_autocorr.cu, k_rco5_s): the members at
+    // dj = +-hr of the regular group columns are already counted
+    int outer_done = 0;
 };
 
 // Scan 2 fused into the R_co launch of the predicted group size (tm_search): scan 1 and the

@@ -72,6 +72,8 @@ print("ok")
     {"TMATCH_EPI_V": "2"},
     {"TMATCH_EPI_MINB": "2"},
     {"TMATCH_EGS_ORDER": "0"},
+    {"TMATCH_RCO5_MIN": "0"},
+    {"TMATCH_RCO5": "0"},
 ], ids=lambda e: ",".join(f"{k}={v}" for k, v in e.items()) or "default")
 def test_kernel_variant_parity(env):
     full = dict(os.environ)
