@@ -1834,6 +1834,10 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// launches made by launch_acg_f beside k_acg itself (phase A, k_seg_order): reported by
+// autocorr_u8_fused for the context's launch count
+thread_local int g_acg_extra = 0;
+
 // Phase A launcher (count-only h = 5 with in-kernel rejection): S raster of the outer
 // members, k_rco5_s, k_rco5_cnt.  False: not applicable (phase B then counts everything).
 // TMATCH_RCO5=0 disables it.
@@ -1985,8 +1989,10 @@ cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, Gr
         if (!map && stop && egs_prev && gd.ti_hi > gd.ti_lo && rco5_phase_a(imgp, pitch, m, n, gd,
                                                                             st, thr, n_r, stop,
                                                                             egs_prev, egs_central,
-                                                                            egs_xi, s))
+                                                                            egs_xi, s)) {
             d.outer_done = 1;
+            g_acg_extra += 2;
+        }
     }
     int* order = nullptr;
     // (only when the launch runs in several waves: one wave has no order to exploit)
@@ -1998,6 +2004,7 @@ cudaError_t launch_acg_f(const uint8_t* imgp, int pitch, int q, int m, int n, Gr
         launch_pdl(k_seg_order, dim3(1), dim3(1024), size_t(a.nseg) * 8, s, dec.rows_in, gd.er,
                    gd.h, gd.ti_lo, a.seg, a.nseg, order);
         d.zorder = order;
+        ++g_acg_extra;
     }
     if (gd.ti_hi > gd.ti_lo && grid.y > 0)
         launch_pdl(k_acg<H, NT, NP, FUSE>, grid, dim3(NT), a.smem, s, imgp, pitch, q, m, n,
@@ -3874,6 +3881,13 @@ cudaError_t autocorr_u8_fused(const uint8_t* img, int p, int q, int m, int n, Gr
             return launch_rco3(imgp, pitch, m, n, gd, st, retain_threshold, map, n_r, stop, s, d,
                                f);
         }
+        g_acg_extra = 0;
+        struct Extra {  // k_acg's extra launches into *launches on every return below
+            int* out;
+            ~Extra() {
+                if (out) *out += g_acg_extra;
+            }
+        } extra{launches};
         if (gd.h == 3)
             return launch_acg<3>(imgp, pitch, q, m, n, gd, st, retain_threshold, map, n_r, stop,
                                  egs_prev, egs_central, egs_xi, s, d, f);
