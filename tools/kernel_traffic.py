@@ -13,7 +13,9 @@ import sys
 # (the kernels of a phase are summed: the two-pass h = 3 R_co is k_rco3_s + k_rco_epi + the
 # clipped-column passes; one search is assumed per report)
 PHASE = [("k_acg<3, 256, 0, 1>", "autocorr_sec"), ("k_rco3_s", "autocorr_sec"),
-         ("k_rco_epi<2", "autocorr_sec"), ("k_rco3_clip", "autocorr_sec"),
+         ("k_rco_epi<2", "autocorr_sec"), ("k_rco_epg<2", "autocorr_sec"),
+         ("k_rco3_clip", "autocorr_sec"), ("k_rco5_s", "autocorr_count"),
+         ("k_rco5_cnt", "autocorr_count"), ("k_seg_order", "autocorr_count"),
          ("k_acg<5, 128", "autocorr_count"),
          ("k_wstats4", "window_stats"), ("k_tc_corr<1>", "centre_scan"),
          ("k_centre_epi", "centre_scan_epilogue"), ("k_tc_corr<2>", "survivor_eval"),
