@@ -3337,6 +3337,118 @@ __global__ void __launch_bounds__(256, MINB)
     rco_finish<MODE>(tal, surv_local, n_r, sf, dec);
 }
 
+// k_rco_epg9<MODE, MINB>: pass 2 with thread = one whole 3x3 group (CTA = group rows,
+// grid-strided; threads over the group columns): its three rows' S / mu / omega / flags are
+// coalesced loads along each row, the centre's statistics come from the middle row's own
+// loads (no gather of the centre row by the rows above and below it) and the group record is
+// read once for nine locations.  Same decisions as k_rco_epg (rco_member).
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB)
+    k_rco_epg9(Grid g, const unsigned* __restrict__ Sin, DevStats st, double mn, double thr,
+               double* __restrict__ map, unsigned long long* __restrict__ n_r, int* stop,
+               EgsDecide dec, SecFuse sf) {
+    pdl_wait();
+    {
+        __shared__ int skip;
+        if (threadIdx.x == 0) skip = stop && *reinterpret_cast<volatile int*>(stop);
+        __syncthreads();
+        if (skip) {
+            egs_tail(dec);
+            return;
+        }
+    }
+    const int lane = threadIdx.x & 31;
+    SecCtx sc;
+    if constexpr (MODE == 2) {
+        const double T = *sf.thr;
+        sc.tb = dclamp(dmin(T, 1.0), -1.0, 1.0);
+        sc.tbf = float(sc.tb);
+        sc.thr_ok = T >= -1.0;
+    }
+    RcoTally tal;
+    bool list_full = false;
+    unsigned long long surv_local = 0;
+    const int ntj = ((g.tc + 31) / 32) * 32;  // whole warps (ballots)
+    for (int ti = g.ti_lo + blockIdx.x; ti < g.ti_hi; ti += gridDim.x) {
+        const int r0 = ti * 3, r1 = min(r0 + 3, g.er) - 1, cr = (r0 + r1) >> 1;
+        const int nr = r1 - r0 + 1, rc = cr - r0;  // rows of the group row, centre's row slot
+        const unsigned gbase = unsigned(ti) * unsigned(g.tc);
+        unsigned evr[3] = {0u, 0u, 0u};
+        for (int tj = threadIdx.x; tj < ntj; tj += blockDim.x) {
+            const bool active = tj < g.tc;
+            const int tq = active ? tj : 0;
+            const int c0 = 3 * tq, c1 = min(c0 + 3, g.ec) - 1, ccol = (c0 + c1) >> 1;
+            const int nc = c1 - c0 + 1, jc = ccol - c0;
+            unsigned sv[3][3];
+            double mm[3][3], om[3][3];
+            bool fm[3][3];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const unsigned krow = unsigned(r0 + min(i, nr - 1)) * unsigned(g.ec);
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const unsigned k = krow + unsigned(c0 + min(j, nc - 1));
+                    sv[i][j] = __ldg(Sin + k);
+                    mm[i][j] = __ldg(st.mu + k);
+                    om[i][j] = __ldg(st.omega + k);
+                    fm[i][j] = __ldg(st.flat + k) != 0;
+                }
+            }
+            double ra = 0.0, sa = 0.0;
+            bool dg = false, sd = false;
+            if constexpr (MODE == 2) {
+                const unsigned gi = gbase + unsigned(tq);
+                ra = __ldg(sf.rho_c + gi);
+                sa = __ldg(sf.sa_c + gi);
+                dg = __ldg(sf.deg_c + gi) != 0;
+                sd = sf.seeded ? __ldg(sf.seeded + gi) != 0 : false;
+            }
+            // the centre's statistics from the loaded rows (selects: no local-memory arrays)
+            auto pick = [&](const double (&a)[3][3]) {
+                const double r0v = jc == 1 ? a[0][1] : a[0][0];
+                const double r1v = jc == 1 ? a[1][1] : a[1][0];
+                return rc == 1 ? r1v : r0v;
+            };
+            const double mc = pick(mm), oc = pick(om);
+            const bool fc = rc == 1 ? (jc == 1 ? fm[1][1] : fm[1][0]) : (jc == 1 ? fm[0][1] : fm[0][0]);
+            const double mnmc = __dmul_rn(mn, mc);
+            unsigned sbits = 0;
+            int srr[9], scc[9];
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+#pragma unroll
+                for (int j = 0; j < 3; ++j) {
+                    const int r = r0 + i, c = c0 + j;
+                    srr[3 * i + j] = r;
+                    scc[3 * i + j] = c;
+                    if (!active || i >= nr || j >= nc) continue;
+                    const unsigned k = unsigned(r) * unsigned(g.ec) + unsigned(c);
+                    if (i == rc && j == jc) {  // the group's centre (autocorr.cpp:92-93)
+                        if constexpr (MODE == 1) map[k] = 1.0;
+                        if constexpr (MODE == 2) sf.visits[k] = 0;
+                        continue;
+                    }
+                    const unsigned e0 = tal.evc;
+                    const bool s = rco_member<MODE>(tal, r, c, k, sv[i][j], mm[i][j], om[i][j],
+                                                    fm[i][j], mnmc, oc, fc, ra, sa, dg, sd, thr,
+                                                    sc, map, sf);
+                    evr[i] += tal.evc - e0;
+                    sbits |= unsigned(s) << (3 * i + j);
+                }
+            }
+            if constexpr (MODE == 2) rco_list<9>(sbits, srr, scc, sf, list_full, surv_local);
+        }
+        if (dec.rows_out) {  // CTA-uniform
+#pragma unroll
+            for (int i = 0; i < 3; ++i) {
+                const unsigned d = __reduce_add_sync(0xffffffffu, evr[i]);
+                if (lane == 0 && d && i < nr) atomicAdd(dec.rows_out + r0 + i, d);
+            }
+        }
+    }
+    rco_finish<MODE>(tal, surv_local, n_r, sf, dec);
+}
+
 struct Rco3Geom {
     int nt = 0, G = 0, ntiles = 0, seg = 0, nseg = 0, tc_reg = 0;
 };
@@ -3525,13 +3637,32 @@ cudaError_t launch_rco3(const uint8_t* imgp, int pitch, int m, int n, GridDesc g
     auto epi = [&](auto kern) {
         launch_pdl(kern, dim3(blocks), dim3(256), 0, s, g, S, st, mn, thr, map, n_r, stop, dec, sf);
     };
-    static const int vw = [] {  // TMATCH_EPI_V: 2 or 4 aligned locations per thread, or 3
-        const char* e = std::getenv("TMATCH_EPI_V");  // (default): one group segment each
-        const int v = e ? std::atoi(e) : 3;
-        return (v == 2 || v == 4) ? v : 3;
+    // TMATCH_EPI_V: 2 or 4 aligned locations per thread, 3: one group segment (default on
+    // small extents: C2 37 vs 43 us), 9: one whole group (default on large ones: C5 1.51 vs
+    // 1.61 ms -- 2 CTAs/SM at 128 registers want many group rows)
+    static const int vw_env = [] {
+        const char* e = std::getenv("TMATCH_EPI_V");
+        const int v = e ? std::atoi(e) : 0;
+        return (v == 2 || v == 4 || v == 3 || v == 9) ? v : 0;
     }();
+    const int vw = vw_env ? vw_env : (double(gd.er) * double(gd.ec) > 3.2e7 ? 9 : 3);
     const int mode = sf.thr ? 2 : (map ? 1 : 0);
-    if (vw == 3) {
+    if (vw == 9) {
+        auto epi9 = [&](auto kern) {
+            const int gblocks = std::min(gd.ti_hi - gd.ti_lo, 148 * 8);
+            launch_pdl(kern, dim3(gblocks), dim3(256), 0, s, g, S, st, mn, thr, map, n_r, stop, dec,
+                       sf);
+        };
+        if (mode == 2) {
+            if (minb == 3 && std::getenv("TMATCH_EPI_MINB")) epi9(k_rco_epg9<2, 3>);
+            else if (minb == 4) epi9(k_rco_epg9<2, 4>);
+            else epi9(k_rco_epg9<2, 2>);
+        } else if (mode == 1) {
+            epi9(k_rco_epg9<1, 2>);
+        } else {
+            epi9(k_rco_epg9<0, 2>);
+        }
+    } else if (vw == 3) {
         if (mode == 2) {  // (4 resident CTAs unless TMATCH_EPI_MINB says otherwise)
             if (minb == 3 && std::getenv("TMATCH_EPI_MINB")) epi(k_rco_epg<2, 3>);
             else if (minb == 2) epi(k_rco_epg<2, 2>);

@@ -70,6 +70,8 @@ print("ok")
     {"TMATCH_RCO3_FUSED": "1", "TMATCH_RCO3_NT": "256"},
     {"TMATCH_RCO3_NT": "128"},
     {"TMATCH_EPI_V": "2"},
+    {"TMATCH_EPI_V": "4"},
+    {"TMATCH_EPI_V": "9"},
     {"TMATCH_EPI_MINB": "2"},
     {"TMATCH_EGS_ORDER": "0"},
     {"TMATCH_RCO5_MIN": "0"},
