@@ -47,6 +47,10 @@ for d in range(-hr, hr + 1):
     tot += cnt
     print(f"dj={d:+d} retained {cnt} ({cnt / max(1, (dj == d).sum() * er):.3f} of its locations)")
 print("total", tot)
+for d in range(-hr, hr + 1):
+    sel = ret[di == d, :]
+    cnt = int(sel.sum()) - (int(((dj[None, :] == 0) & sel).sum()) if d == 0 else 0)
+    print(f"di={d:+d} retained {cnt} ({cnt / max(1, (di == d).sum() * ec):.3f} of its locations)")
 for order in ([-2, -1, 0, 1, 2], [-2, 2, -1, 1, 0]):
     cum, work = 0, 0
     for d in order:
