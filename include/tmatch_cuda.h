@@ -302,6 +302,10 @@ int tm_strip_fused_finish(tm_ctx* ctx, tm_strip_part* out);
 int64_t tm_ctx_launch_count(const tm_ctx* ctx);
 /* tm_search h_e predictions (the fused scan-2 path ran on the accepted size / did not). */
 int tm_ctx_search_stats(const tm_ctx* ctx, int64_t* fused_hits, int64_t* fused_misses);
+/* Split tensor-core screening of non-integer images (detail.hpp:32-51 bracketed on three
+ * byte planes, see k_tc.cu): locations bracketed / locations re-evaluated by the FP64
+ * replica since the context was created. */
+int tm_ctx_split_stats(const tm_ctx* ctx, int64_t* screened, int64_t* exact);
 /* The context's CUDA stream (cudaStream_t) for callers that time or order work on it. */
 void* tm_ctx_stream(tm_ctx* ctx);
 /* Per-phase device timing with CUDA events on the context stream (off by default). */

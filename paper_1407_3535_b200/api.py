@@ -228,6 +228,13 @@ class Context:
         N.check(N.lib().tm_ctx_search_stats(self.h, C.byref(h), C.byref(m)))
         return {"fused_hits": h.value, "fused_misses": m.value}
 
+    def split_stats(self) -> dict:
+        """Split tensor-core screening of non-integer images: locations bracketed on the
+        tensor cores / re-evaluated exactly by the FP64 replica."""
+        a, b = C.c_int64(), C.c_int64()
+        N.check(N.lib().tm_ctx_split_stats(self.h, C.byref(a), C.byref(b)))
+        return {"screened": a.value, "exact": b.value}
+
     def set_profiling(self, enable=True):
         N.check(N.lib().tm_ctx_set_profiling(self.h, int(bool(enable))))
 

@@ -262,6 +262,9 @@ struct tm_ctx {
     DBuf<int2> locs, seed_locs;
     DBuf<uint8_t> seq_deg, seeded, deg_c, visits;
     DBuf<double> rho_c, surface, dotbuf;
+    DBuf<float> ub_surface;  // split screening: upper bounds of rho
+    bool tc_split = true;    // TMATCH_TC_SPLIT=0: non-integer images stay on the FP64 replica
+    int64_t split_screened = 0, split_exact = 0;  // locations bracketed / re-evaluated exactly
     DBuf<float> tf;
     DBuf<double> td;
     // the template ctx->tf / ctx->td hold (upload_template skips identical re-uploads);
@@ -429,6 +432,12 @@ struct tm_image {
     DBuf<uint8_t> u8p;
     int u8p_pitch = 0;
     int u8p_rows = 0;
+    // non-integer images: the three byte planes of floor(v * 2^16) for the split
+    // tensor-core screening (k_tc.cu, "split planes"); split_ok = every pixel in [0, 256)
+    DBuf<uint8_t> split;
+    int split_pitch = 0;
+    size_t split_stride = 0;
+    bool have_split = false, split_ok = false;
     // Row-strip image (tm_image_create_strip_u8): only image rows [row_lo, row_hi) hold
     // pixels (the rank's strip + halo); window statistics cover the extent rows whose
     // windows lie inside them; prefix_noise comes from the allreduced global q_total.
@@ -645,6 +654,7 @@ void compute_ws(tm_ctx* ctx, tm_image* img, int m, int n, WS& ws) {
 // recomputed in place by the next get_ws).
 void invalidate_ws(tm_image* img) {
     for (auto& kv : img->ws_cache) kv.second->valid = false;
+    img->have_split = false;
 }
 
 WS& get_ws(tm_ctx* ctx, tm_image* img, int m, int n) {
@@ -800,6 +810,33 @@ const uint8_t* tc_image(tm_ctx* ctx, tm_image* img, int ec) {
     return img->u8p.p;
 }
 
+// Non-integer image + integer template: the byte planes for the split tensor-core
+// screening, made on first use.  False when a pixel lies outside [0, 256) (FP64 replica).
+bool split_path(tm_ctx* ctx, tm_image* img, const Tmpl& T) {
+    if (!ctx->tc || !ctx->tc_split || img->integer || !T.integer || T.ts.flat) return false;
+    if (img->row_lo != 0 || img->row_hi < img->p) return false;  // strip images: 8-bit only
+    if (!tmk::tc_supported(T.m, T.n) || tmk::tc_plan(T.m, T.n, 1, kTcSmemBudget).nch == 0)
+        return false;
+    if (!img->have_split) {
+        const int pitch = tmk::tc_pitch(img->q, img->q);
+        const int rows = img->p + tmk::kU8PadRows;
+        img->split_stride = size_t(rows) * pitch;
+        img->split.ensure(img->split_stride * tmk::kTcSplitPlanes);
+        int* bad = reinterpret_cast<int*>(ctx->counters.p + 34);
+        CK(cudaMemsetAsync(bad, 0, sizeof(int), ctx->s));
+        CK(tmk::tc_split_image(img->f64.p, img->p, img->q, img->split.p, pitch, rows,
+                               img->split_stride, bad, ctx->s));
+        ctx->add(1);
+        int hbad = 0;
+        CK(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->s));
+        CK(cudaStreamSynchronize(ctx->s));
+        img->split_pitch = pitch;
+        img->have_split = true;
+        img->split_ok = hbad == 0;
+    }
+    return img->split_ok;
+}
+
 // Bands of up to `rmax` output rows r0 + sr*k; a list of rows with irregular spacing
 // becomes single-row bands.
 std::vector<tmk::TcBand> tc_bands(const std::vector<int>& rows, const std::vector<int>& yi, int sr,
@@ -835,9 +872,10 @@ struct RowSet {
     }
 };
 
-TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, int sr) {
+TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, int sr,
+                   int band_rows = 16) {
     const std::vector<long long> key = {T.m, T.n, sr, ws.ec, rs.kind, rs.lo, rs.hi,
-                                        rs.kind ? rs.g.er : 0, rs.kind ? rs.g.h : 0};
+                                        rs.kind ? rs.g.er : 0, rs.kind ? rs.g.h : 0, band_rows};
     auto it = ctx->tc_geo.find(key);
     if (it != ctx->tc_geo.end()) return *it->second;
     if (ctx->tc_geo.size() > 64) ctx->tc_geo.clear();
@@ -850,8 +888,9 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, i
     // rows per band: the fewest waves of 148 persistent CTAs with <= 16 rows per band, then
     // bands as equal as possible so every CTA gets the same number of tiles
     const size_t work = rows.size() * size_t(geo->ntc);
-    const size_t waves = std::max<size_t>(1, (work + 148 * 16 - 1) / (148 * 16));
-    int rmax = int(std::min<size_t>(16, std::max<size_t>(1, (work + 148 * waves - 1) / (148 * waves))));
+    const size_t br = size_t(band_rows);
+    const size_t waves = std::max<size_t>(1, (work + 148 * br - 1) / (148 * br));
+    int rmax = int(std::min<size_t>(br, std::max<size_t>(1, (work + 148 * waves - 1) / (148 * waves))));
     const std::vector<tmk::TcBand> bands = tc_bands(rows, yi, sr, rmax);
     geo->nbands = int(bands.size());
     geo->bands.ensure(bands.size());
@@ -874,7 +913,8 @@ TcGeo& tc_geometry(tm_ctx* ctx, const WS& ws, const Tmpl& T, const RowSet& rs, i
 // Runs the tensor-core kernel over `rows` (group-row indices `yi`) -> partials, returns #.
 int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet& rs, int sr,
            tmk::TcTask task, const int** rows_dev = nullptr, bool side_build = false) {
-    TcGeo& geo = tc_geometry(ctx, ws, T, rs, sr);
+    const bool split = task.mode >= 3;
+    TcGeo& geo = tc_geometry(ctx, ws, T, rs, sr, split ? tmk::kTcSplitRows : 16);
     HT("tc_geo");
     const tmk::TcPlan& plan = geo.plan;
     if (side_build && ctx->tc_b.cap >= plan.total_bytes) {
@@ -890,8 +930,19 @@ int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet
     }
     HT("build_b");
     tmk::TcJob job{};
-    job.imgp = tc_image(ctx, img, ws.ec);
-    job.pitch = img->u8p_pitch;
+    if (split) {
+        // error model of the split (k_tc.cu): truncation < 2^-16 per pixel, times sum(T);
+        // the reference's sequential FP64 sum is within gamma_mn of the true dot
+        job.imgp = img->split.p;
+        job.pitch = img->split_pitch;
+        job.plane_stride = img->split_stride;
+        job.scr_delta = T.ts.mn * T.ts.mu * (1.0 + 1e-9) / 65536.0;
+        job.scr_gamma = (T.ts.mn + 4.0) * 2.220446049250313e-16;
+        task.kp = tmk::kTcSplitRows;
+    } else {
+        job.imgp = tc_image(ctx, img, ws.ec);
+        job.pitch = img->u8p_pitch;
+    }
     job.bglob = ctx->tc_b.p;
     job.plan = plan;
     job.ts = T.ts;
@@ -2040,6 +2091,42 @@ tmk::CellH refine(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, int l
     return c;
 }
 
+// brute_force_match on a non-integer image: bracket rho everywhere with the split
+// tensor-core pass, list the locations whose upper bound reaches the largest lower bound,
+// evaluate those with the FP64 replica (window_dot order) -> cells[2].  False: the list
+// overflowed or nothing was non-flat (the caller runs the dense FP64 replica instead).
+bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
+    const int er = ws.er, ec = ws.ec;
+    const size_t E = size_t(er) * ec;
+    RowSet rs;
+    rs.lo = 0;
+    rs.hi = er;
+    tmk::TcTask task{};
+    task.mode = 3;
+    task.c_lim = ec;
+    task.c_last = -1;
+    ctx->ub_surface.ensure(E);
+    task.out_ub = ctx->ub_surface.p;
+    ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
+    const int np = tc_run(ctx, img, ws, T, rs, 1, task);
+    reduce_to(ctx, np, 3);  // cells[3].rho = the largest lower bound
+    const size_t cap = std::min<size_t>(E, size_t(1) << 20);
+    ctx->locs.ensure(cap);
+    unsigned long long* cnt = ctx->counters.p + 35;
+    CK(cudaMemsetAsync(cnt, 0, 8, ctx->s));
+    CK(tmk::tc_screen_compact(ctx->ub_surface.p, er, ec, ctx->cells.p + 3, ctx->locs.p, cnt, cap,
+                              ctx->s));
+    ctx->add(1);
+    unsigned long long n = 0;
+    CK(cudaMemcpyAsync(&n, cnt, 8, cudaMemcpyDeviceToHost, ctx->s));
+    CK(cudaStreamSynchronize(ctx->s));
+    if (n == 0 || n > cap) return false;
+    ctx->split_screened += (long long)E;
+    ctx->split_exact += (long long)n;
+    eval_list(ctx, img, ws, T, ctx->locs.p, cnt, int(cap), nullptr, nullptr, 2);
+    return true;
+}
+
 // brute_force_match (stats.cpp:156-213)
 tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface_host) {
     const int m = T.m, n = T.n;
@@ -2089,6 +2176,8 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
         CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &np, ctx->s));
         ctx->add(1);
         reduce_to(ctx, np, 2);
+    } else if (!surface && split_path(ctx, img, T) && brute_split(ctx, img, ws, T)) {
+        // screened on the tensor cores, the near-maximal locations re-evaluated exactly
     } else {
         ctx->partials.ensure(kListBlocks);
         CK(tmk::corr_dense_f64(job, surface, ctx->partials.p, kListBlocks, ctx->s));
@@ -2294,6 +2383,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         if (const char* e = std::getenv("TMATCH_AUTOCORR")) ctx->ac_fused = std::strcmp(e, "colwalk") != 0;
         if (const char* e = std::getenv("TMATCH_WSTATS")) ctx->ws4 = std::strcmp(e, "column") != 0;
         if (const char* e = std::getenv("TMATCH_TC")) ctx->tc = std::strcmp(e, "0") != 0;
+        if (const char* e = std::getenv("TMATCH_TC_SPLIT")) ctx->tc_split = std::strcmp(e, "0") != 0;
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
         cudaMemPool_t pool;
@@ -2311,8 +2401,8 @@ int tm_ctx_create(int device, tm_ctx** out) {
         CK(cudaEventCreateWithFlags(&ctx->ev_egs, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_b0, cudaEventDisableTiming));
         CK(cudaEventCreateWithFlags(&ctx->ev_b1, cudaEventDisableTiming));
-        ctx->counters.ensure(32);
-        CK(cudaMemsetAsync(ctx->counters.p, 0, 32 * sizeof(unsigned long long), ctx->s));
+        ctx->counters.ensure(40);
+        CK(cudaMemsetAsync(ctx->counters.p, 0, 40 * sizeof(unsigned long long), ctx->s));
         ctx->cells.ensure(8);
         ctx->thr.ensure(2);
         ctx->tally.ensure(1);
@@ -2336,6 +2426,13 @@ int tm_ctx_search_stats(const tm_ctx* ctx, int64_t* fused_hits, int64_t* fused_m
     if (!ctx || !fused_hits || !fused_misses) return TM_EINVAL;
     *fused_hits = ctx->fused_hits;
     *fused_misses = ctx->fused_misses;
+    return TM_OK;
+}
+
+int tm_ctx_split_stats(const tm_ctx* ctx, int64_t* screened, int64_t* exact) {
+    if (!ctx || !screened || !exact) return TM_EINVAL;
+    *screened = ctx->split_screened;
+    *exact = ctx->split_exact;
     return TM_OK;
 }
 

@@ -330,14 +330,77 @@ __device__ __forceinline__ double dot_f64(const CorrJob& job, int r, int c) {
     return acc;
 }
 
+// The same sum by a whole CTA, for SHORT lists (a single thread's replay of m*n dependent
+// loads takes ~1 ms at 128x128): the products t*I are independent, only the additions must
+// run in window_dot's order.  Warps 1.. fill a shared-memory chunk of products (rounded once,
+// like the reference's pt[j] * pi[j]) while thread 0 adds the previous chunk in sequence.
+// Returns the dot in thread 0.
+constexpr int kF64Chunk = 2048;
+__device__ double dot_f64_cta(const CorrJob& job, int r, int c, double (*buf)[kF64Chunk]) {
+    const int total = job.m * job.n;
+    const int nch = (total + kF64Chunk - 1) / kF64Chunk;
+    const int tid = threadIdx.x;
+    auto fill = [&](int k, int first, int step) {
+        const int e0 = k * kF64Chunk, e1 = min(total, e0 + kF64Chunk);
+        for (int e = e0 + first; e < e1; e += step) {
+            const int i = e / job.n, j = e - i * job.n;
+            buf[k & 1][e - e0] =
+                __dmul_rn(job.td[e], job.imgd[size_t(r + i) * job.q + c + j]);
+        }
+    };
+    fill(0, tid, blockDim.x);
+    __syncthreads();
+    double acc = 0.0;
+    for (int k = 0; k < nch; ++k) {
+        if (tid >= 32) {
+            if (k + 1 < nch) fill(k + 1, tid - 32, blockDim.x - 32);
+        } else if (tid == 0) {
+            const double* b = buf[k & 1];
+            const int cnt = min(kF64Chunk, total - k * kF64Chunk);
+            int e = 0;
+            for (; e + 8 <= cnt; e += 8) {
+                double v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) v[u] = b[e + u];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) acc = __dadd_rn(acc, v[u]);
+            }
+            for (; e < cnt; ++e) acc = __dadd_rn(acc, b[e]);
+        }
+        __syncthreads();
+    }
+    return acc;
+}
+
 __global__ void __launch_bounds__(256)
     k_list_f64(CorrJob job, const int2* __restrict__ locs, const unsigned long long* count,
                int max_count, double* out_rho, uint8_t* out_deg, CellH* partials,
                int rho_by_loc) {
     __shared__ Cell scratch[8];
+    __shared__ double prod[2][kF64Chunk];
     const long long nloc = min((long long)*count, (long long)max_count);
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
+    if (nloc <= 4ll * gridDim.x) {  // short list: one CTA per location
+        for (long long li = blockIdx.x; li < nloc; li += gridDim.x) {
+            const int2 rc = locs[li];
+            const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
+            const bool wflat = job.st.flat[kk];
+            const bool deg = ts.flat || wflat;
+            const double dot = deg ? 0.0 : dot_f64_cta(job, rc.x, rc.y, prod);  // block-uniform
+            if (threadIdx.x == 0) {
+                const double rho =
+                    deg ? 0.0 : zncc_epilogue(dot, ts, job.st.mu[kk], job.st.omega[kk], wflat);
+                if (out_rho) out_rho[rho_by_loc ? kk : li] = rho;
+                if (out_deg) out_deg[li] = deg;
+                const Cell cand = make_cell(rc.x, rc.y, rho, deg);
+                if (better(cand, best)) best = cand;
+            }
+        }
+        best = block_best(best, scratch);
+        if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
+        return;
+    }
     for (long long li = blockIdx.x * (long long)blockDim.x + threadIdx.x; li < nloc;
          li += (long long)gridDim.x * blockDim.x) {
         const int2 rc = locs[li];

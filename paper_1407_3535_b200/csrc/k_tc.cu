@@ -25,6 +25,19 @@
 //   warp 1      TMEM allocation; one elected thread issues the MMAs and commits.
 //   warps 2..5  epilogue: tcgen05.ld of the exact s32 dots, FP64 ZNCC, argmax / outputs;
 //               re-zero the TMEM buffer and hand it back (double buffered).
+//
+// Split planes (MODE 3; the north star's "3x" tensor-core variant for non-integer search
+// images, e.g. OptA's blurred image).  A pixel v in [0, 256) is cut into three bytes of
+// floor(v * 2^16) (tc_split_image); each plane runs the same Toeplitz MMA chains against
+// the same B into its own TMEM slots, so  dot_a = D0 + D1/2^8 + D2/2^16  is an EXACT
+// integer combination with  0 <= dot_true - dot_a < 2^-16 * sum(T).  kind::i8 slices are
+// used instead of 3xTF32 because the s32 accumulation has no rounding at all (a rigorous
+// radius; 3xTF32 accumulates in FP32, ~K*2^-24) and the i8 pipe has 4x the TF32 peak.
+// The reference's FP64 window_dot (detail.hpp:32-41) rounds in sequence and cannot be
+// reproduced by any re-associated sum, so this mode SCREENS: it brackets every rho
+// (detail.hpp:45-51 evaluated on the bracketed dot), keeps the largest lower bound and
+// lists the few locations whose upper bound reaches it; those are evaluated exactly by the
+// FP64 replica (k_list_f64).  Results stay bit-identical to the reference.
 #include <algorithm>
 #include <cstdio>
 #include <vector>
@@ -130,6 +143,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
     pdl_wait();
     extern __shared__ __align__(1024) uint8_t sm[];
     const TcPlan& P = job.plan;
+    constexpr int NPL = MODE >= 3 ? kTcSplitPlanes : 1;  // image planes per output row
     // a ring stage holds kRows consecutive scheduled image rows (kRows slots of a_slot bytes):
     // one expect_tx, one full-wait and one commit per stage instead of per row
     constexpr int kRows = 4;
@@ -218,6 +232,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     }
                     const int4* sc = sched + task.sched_off[ch];
                     const int ns = task.sched_len[ch];
+                    for (int pl = 0; pl < NPL; ++pl)
                     for (int e0 = 0; e0 < ns; e0 += kRows) {
                         int dx[kRows];
                         int nr = 0;  // rows are in k_lo order: the valid ones are a prefix
@@ -237,7 +252,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                             mbar_expect_tx(full + s, uint32_t(nr * P.a_bytes));
                             for (int j = 0; j < nr; ++j)
                                 bulk_g2s(sA + (size_t(s) * kRows + j) * P.a_slot,
-                                         job.imgp + size_t(bd.r0 + dx[j]) * job.pitch + c0,
+                                         job.imgp + (NPL > 1 ? size_t(pl) * job.plane_stride : size_t(0)) +
+                                             size_t(bd.r0 + dx[j]) * job.pitch + c0,
                                          uint32_t(P.a_bytes), full + s);
                         }
                         ++it;
@@ -288,6 +304,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                 const int4* sc = sched + task.sched_off[ch];
                 const int ns = task.sched_len[ch];
                 // one ring stage = up to kRows scheduled rows: one wait, their MMAs, one commit
+                for (int pl = 0; pl < NPL; ++pl)
                 for (int e0 = 0; e0 < ns; e0 += kRows) {
                     int4 rows[kRows];
                     int nr = 0;
@@ -309,7 +326,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                         uint64_t ad = a_desc0 + uint64_t(uint32_t(s * kRows + j) * slot16);
                         uint64_t bdsc = b_desc0 + uint64_t(uint32_t(rows[j].w) * entry16);
                         const uint32_t idesc = idesc0 | (uint32_t(k_hi - rows[j].y + 1) << 18);
-                        const uint32_t d = dbase + uint32_t(16 * rows[j].y);
+                        const uint32_t d =
+                            dbase + uint32_t(16 * (rows[j].y + (NPL > 1 ? pl * task.kp : 0)));
                         for (int ks = 0; ks < ksteps; ++ks) {
                             asm volatile(
                                 "{\n .reg .pred e, acc;\n elect.sync _|e, 0xffffffff;\n"
@@ -379,7 +397,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
             // MODE 1: which of the 16 columns are group centres (constant over the tile)
             uint32_t cmask = 0;
             int tj0 = 0, ph_last = -1;
-            if (MODE == 1) {
+            if (MODE == 1 || MODE == 4) {
                 const int d0 = cb - task.cbase;
                 int first = d0 <= 0 ? -d0 : (d0 % task.cstep == 0 ? 0 : task.cstep - d0 % task.cstep);
                 tj0 = (cb + first - task.cbase) / task.cstep;
@@ -399,16 +417,64 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                 tmem_ld16(addr, v);
                 tmem_zero16(addr);
                 const int r = bd.r0 + bd.sr * k;
-                if (MODE == 1) {
+                if (MODE == 3) {
+                    // split planes: v = plane 0 (integer parts); planes 1, 2 sit kp and 2 kp
+                    // slots further.  dot_a is exact; the bracket of the reference's rho:
+                    //   dot_ref in [dot_a (1 - gamma), (dot_a + delta)(1 + gamma)]
+                    uint32_t v1[16], v2[16];
+                    tmem_ld16(addr + uint32_t(16 * task.kp), v1);
+                    tmem_zero16(addr + uint32_t(16 * task.kp));
+                    tmem_ld16(addr + uint32_t(32 * task.kp), v2);
+                    tmem_zero16(addr + uint32_t(32 * task.kp));
+                    const size_t rb = size_t(r) * st.ec + cb;
+                    const double tmean = __dmul_rn(ts.mn, ts.mu);
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) {
+                        if (!((cmask >> ph) & 1u)) continue;
+                        const size_t kk = rb + ph;
+                        if (st.flat[kk]) {
+                            task.out_ub[kk] = -2.0f;
+                            continue;
+                        }
+                        const double dot_a = double(int(v[ph])) + double(int(v1[ph])) * 0.00390625 +
+                                             double(int(v2[ph])) * 0.0000152587890625;
+                        const double half = 0.5 * job.scr_delta;
+                        const double rad = half + job.scr_gamma * (dot_a + job.scr_delta);
+                        const double den = __dmul_rn(ts.omega, st.omega[kk]);
+                        const double num = (dot_a + half) - __dmul_rn(tmean, st.mu[kk]);
+                        const double rho_m = num / den;
+                        const double e = (rad / den) * 1.000001 + 1e-14 + fabs(rho_m) * 1e-14;
+                        const double lb = dclamp(rho_m - e, -1.0, 1.0);
+                        const double ub = dclamp(rho_m + e, -1.0, 1.0);
+                        task.out_ub[kk] = __double2float_ru(ub);
+                        const Cell cand = make_cell(r, cb + ph, lb, false);
+                        if (better(cand, best)) best = cand;
+                    }
+                    continue;
+                }
+                if (MODE == 1 || MODE == 4) {
                     // centres: the exact dot goes to a compact per-group array; the FP64
-                    // epilogue runs in k_centre_epi (coalesced statistics loads)
+                    // epilogue runs in k_centre_epi (coalesced statistics loads).  MODE 4
+                    // (split planes): dot_a = D0 + D1/2^8 + D2/2^16, exact in FP64; the
+                    // bracket is taken by k_split_centre_epi.
+                    uint32_t v1[16], v2[16];
+                    if (MODE == 4) {
+                        tmem_ld16(addr + uint32_t(16 * task.kp), v1);
+                        tmem_zero16(addr + uint32_t(16 * task.kp));
+                        tmem_ld16(addr + uint32_t(32 * task.kp), v2);
+                        tmem_zero16(addr + uint32_t(32 * task.kp));
+                    }
                     double* row_out = task.out_rho + size_t(bd.yi0 + k) * task.tc;
                     int tj = tj0;
 #pragma unroll
                     for (int ph = 0; ph < 16; ++ph) {
-                        if (ph == ph_last) row_out[task.tc - 1] = double(int(v[ph]));
+                        double d = double(int(v[ph]));
+                        if (MODE == 4)
+                            d = d + double(int(v1[ph])) * 0.00390625 +
+                                double(int(v2[ph])) * 0.0000152587890625;
+                        if (ph == ph_last) row_out[task.tc - 1] = d;
                         if (!((cmask >> ph) & 1u)) continue;
-                        row_out[tj++] = double(int(v[ph]));
+                        row_out[tj++] = d;
                     }
                     continue;
                 }
@@ -532,6 +598,205 @@ __global__ void k_tc_pitch(const uint8_t* __restrict__ img, int p, int q, uint8_
     }
 }
 
+// floor(v * 2^16) of a non-integer image cut into three byte planes (16-byte pitched, zero
+// padded like k_tc_pitch): plane 0 = integer part, planes 1, 2 = the next two bytes.
+__global__ void k_tc_split(const double* __restrict__ img, int p, int q, uint8_t* __restrict__ out,
+                           int pitch, int rows, size_t plane_stride, int* __restrict__ bad) {
+    const int cpr = pitch >> 4;
+    const size_t total = size_t(rows) * cpr;
+    int any_bad = 0;
+    for (size_t i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < total;
+         i += size_t(gridDim.x) * blockDim.x) {
+        const int r = int(i / cpr), c = int(i - size_t(r) * cpr) << 4;
+        unsigned w[3][4] = {};
+        if (r < p && c < q) {
+            const double* src = img + size_t(r) * q + c;
+            const int nb = min(16, q - c);
+            for (int b = 0; b < nb; ++b) {
+                const double v = __ldg(src + b);
+                if (!(v >= 0.0 && v < 256.0)) {
+                    any_bad = 1;
+                    continue;
+                }
+                const unsigned u = __double2uint_rd(v * 65536.0);  // exact scaling
+                w[0][b >> 2] |= (u >> 16) << (8 * (b & 3));
+                w[1][b >> 2] |= ((u >> 8) & 255u) << (8 * (b & 3));
+                w[2][b >> 2] |= (u & 255u) << (8 * (b & 3));
+            }
+        }
+#pragma unroll
+        for (int pl = 0; pl < 3; ++pl)
+            *reinterpret_cast<uint4*>(out + pl * plane_stride + size_t(r) * pitch + c) =
+                make_uint4(w[pl][0], w[pl][1], w[pl][2], w[pl][3]);
+    }
+    if (any_bad) atomicOr(bad, 1);
+}
+
+// Locations whose upper bound reaches the largest lower bound (any order: the exact
+// evaluation that follows reduces with better_candidate's total order).
+__global__ void k_tc_screen_compact(const float* __restrict__ ub, int er, int ec,
+                                    const CellH* __restrict__ best, int2* __restrict__ locs,
+                                    unsigned long long* __restrict__ count,
+                                    unsigned long long max_count) {
+    pdl_wait();
+    const double lim = best->rho;
+    const size_t E = size_t(er) * ec;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+         k += size_t(gridDim.x) * blockDim.x) {
+        const float u = __ldg(ub + k);
+        if (u >= -1.5f && double(u) >= lim) {
+            const unsigned long long at = atomicAdd(count, 1ull);
+            if (at < max_count) locs[at] = make_int2(int(k / size_t(ec)), int(k % size_t(ec)));
+        }
+    }
+}
+
+// ---- split centre scan (scan 1 of a search on a non-integer image) ----------------------
+// The bracket of one rho from the exact split dot (same model as MODE 3 of k_tc_corr).
+__device__ __forceinline__ void split_bracket(double dot_a, const SplitModel& sm, const TStats& ts,
+                                              double mu_w, double omega_w, double& rho_m,
+                                              double& e) {
+    const double half = 0.5 * sm.delta;
+    const double rad = half + sm.gamma * (dot_a + sm.delta);
+    const double den = __dmul_rn(ts.omega, omega_w);
+    const double num = (dot_a + half) - __dmul_rn(__dmul_rn(ts.mn, ts.mu), mu_w);
+    rho_m = num / den;
+    e = (rad / den) * 1.000001 + 1e-14 + fabs(rho_m) * 1e-14;
+}
+
+// Per centre: provisional rho_c = clamp(rho_m), radius rad_c (0 = exact), deg_c; partials =
+// the best LOWER bound among non-degenerate centres (or the first degenerate centre).
+__global__ void __launch_bounds__(256)
+    k_split_centre_epi(Grid g, const double* __restrict__ dot, DevStats st, TStatsH tsh,
+                       SplitModel sm, double* __restrict__ rho_c, double* __restrict__ rad_c,
+                       uint8_t* __restrict__ deg_c, CellH* partials) {
+    pdl_wait();
+    __shared__ Cell scratch[8];
+    const TStats ts = TStats{tsh.mu, tsh.omega, tsh.mn, tsh.flat};
+    const size_t G = size_t(g.tr) * g.tc;
+    Cell best = no_cell();
+    for (size_t gi = blockIdx.x * size_t(blockDim.x) + threadIdx.x; gi < G;
+         gi += size_t(gridDim.x) * blockDim.x) {
+        const int ti = int(gi / size_t(g.tc)), tj = int(gi - size_t(ti) * g.tc);
+        const int r = g.center_row(ti), c = g.center_col(tj);
+        const size_t kk = size_t(r) * g.ec + c;
+        if (st.flat[kk]) {
+            rho_c[gi] = 0.0;
+            rad_c[gi] = 0.0;
+            deg_c[gi] = 1;
+            const Cell cand = make_cell(r, c, 0.0, true);
+            if (better(cand, best)) best = cand;
+            continue;
+        }
+        double rho_m, e;
+        split_bracket(dot[gi], sm, ts, st.mu[kk], st.omega[kk], rho_m, e);
+        rho_c[gi] = dclamp(rho_m, -1.0, 1.0);
+        rad_c[gi] = e;
+        deg_c[gi] = 0;
+        const Cell cand = make_cell(r, c, dclamp(rho_m - e, -1.0, 1.0), false);
+        if (better(cand, best)) best = cand;
+    }
+    best = block_best(best, scratch);
+    if (threadIdx.x == 0)
+        partials[blockIdx.x] = CellH{best.rho, best.row, best.col, best.flags};
+}
+
+__device__ __forceinline__ void split_append(int2* locs, int* gidx, unsigned long long* count,
+                                             int r, int c, size_t gi) {
+    const unsigned long long at = atomicAdd(count, 1ull);
+    locs[at] = make_int2(r, c);  // capacity G: a centre is listed at most once per pass
+    gidx[at] = int(gi);
+}
+
+// Centres that still need their exact rho.  mode 0: the candidates for the best centre
+// (upper bound >= the largest lower bound in *lim; a degenerate *lim lists that centre
+// alone).  mode 1: the seeding decision rho_c >= thr - margin (k_seed_members) is not
+// settled by the bracket.
+__global__ void __launch_bounds__(256)
+    k_split_pick(Grid g, const double* __restrict__ rho_c, const double* __restrict__ rad_c,
+                 const uint8_t* __restrict__ deg_c, int mode, const CellH* __restrict__ lim,
+                 const double* __restrict__ thr, double margin, int2* locs, int* gidx,
+                 unsigned long long* count) {
+    pdl_wait();
+    const size_t G = size_t(g.tr) * g.tc;
+    for (size_t gi = blockIdx.x * size_t(blockDim.x) + threadIdx.x; gi < G;
+         gi += size_t(gridDim.x) * blockDim.x) {
+        const int ti = int(gi / size_t(g.tc)), tj = int(gi - size_t(ti) * g.tc);
+        const int r = g.center_row(ti), c = g.center_col(tj);
+        bool pick = false;
+        if (mode == 0) {
+            if (lim->flags & 2)
+                pick = (lim->flags & 1) && lim->row == r && lim->col == c;
+            else
+                pick = !deg_c[gi] && rho_c[gi] + rad_c[gi] >= lim->rho;
+        } else {
+            const double e = rad_c[gi];
+            const double x = *thr - margin;
+            pick = e > 0.0 && !deg_c[gi] && fabs(rho_c[gi] - x) <= e + 1e-12;
+        }
+        if (pick) split_append(locs, gidx, count, r, c, gi);
+    }
+}
+
+// Exact values back into the per-group arrays.
+__global__ void k_split_scatter(const double* __restrict__ rho, const int* __restrict__ gidx,
+                                const unsigned long long* __restrict__ count,
+                                double* __restrict__ rho_c, double* __restrict__ rad_c) {
+    pdl_wait();
+    const unsigned long long n = *count;
+    for (unsigned long long i = blockIdx.x * size_t(blockDim.x) + threadIdx.x; i < n;
+         i += size_t(gridDim.x) * blockDim.x) {
+        rho_c[gidx[i]] = rho[i];
+        rad_c[gidx[i]] = 0.0;
+    }
+}
+
+// Groups whose members' bound test (k_sec_rows: sec_holds(min(T, 1), rho_c, R_co),
+// bounds.cpp:41-46) is not settled by the centre's bracket [rho - e, rho + e].  The bound
+// rho*R + sqrt(1 - rho^2) sqrt(1 - R^2) is monotone in rho on either side of rho = R, so its
+// range over the bracket is spanned by the endpoint values unless R lies inside; brackets
+// reaching |rho| ~ 1 (where the FP64 square root amplifies rounding) are listed outright.
+__global__ void __launch_bounds__(256)
+    k_split_sec_uncertain(Grid g, const double* __restrict__ map, const double* __restrict__ rho_c,
+                          const double* __restrict__ rad_c, const uint8_t* __restrict__ deg_c,
+                          const uint8_t* __restrict__ flat, const double* __restrict__ thr_ptr,
+                          const uint8_t* __restrict__ seeded, uint8_t* __restrict__ gflag,
+                          int2* locs, int* gidx, unsigned long long* count) {
+    pdl_wait();
+    const double T = *thr_ptr;
+    if (!(T >= -1.0)) return;  // nothing is eliminated: no decision depends on rho_c
+    const double tb = dmin(T, 1.0);
+    const size_t E = size_t(g.er) * g.ec;
+    for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
+         k += size_t(gridDim.x) * blockDim.x) {
+        int r, c;
+        g.rc(k, r, c);
+        const int ti = g.tile_r(r), tj = g.tile_c(c);
+        const size_t gi = size_t(ti) * g.tc + tj;
+        const double e = rad_c[gi];
+        if (e == 0.0 || deg_c[gi] || gflag[gi]) continue;
+        if (seeded && seeded[gi]) continue;
+        const int cr = g.center_row(ti), cc = g.center_col(tj);
+        if ((cr == r && cc == c) || flat[k]) continue;
+        const double a = rho_c[gi];
+        const double lo = a - e, hi = a + e;
+        const double b = dclamp(map[k], -1.0, 1.0);
+        bool unsure = hi >= 0.9999995 || lo <= -0.9999995 || (b >= lo && b <= hi);
+        if (!unsure) {
+            const double f_lo = __dadd_rn(__dmul_rn(lo, b), half_gap(lo, b));
+            const double f_hi = __dadd_rn(__dmul_rn(hi, b), half_gap(hi, b));
+            const double fmax = dmax(f_lo, f_hi), fmin = dmin(f_lo, f_hi);
+            unsure = !(tb >= fmax + 1e-12 || tb < fmin - 1e-12);
+        }
+        if (unsure) {
+            // one listing per group: byte flags claimed through a 32-bit atomicOr
+            const unsigned bit = 1u << (8 * unsigned(gi & 3));
+            const unsigned old = atomicOr(reinterpret_cast<unsigned*>(gflag) + (gi >> 2), bit);
+            if (!(old & bit)) split_append(locs, gidx, count, cr, cc, gi);
+        }
+    }
+}
+
 }  // namespace
 
 namespace {
@@ -648,6 +913,57 @@ cudaError_t tc_pitch_image(const uint8_t* img, int p, int q, uint8_t* out, int p
     return cudaGetLastError();
 }
 
+cudaError_t tc_split_image(const double* img, int p, int q, uint8_t* out, int pitch, int rows,
+                           size_t plane_stride, int* bad, cudaStream_t s) {
+    const size_t chunks = size_t(rows) * (pitch / 16);
+    const int blocks = int(std::min<size_t>((chunks + 255) / 256, 148 * 8));
+    k_tc_split<<<blocks, 256, 0, s>>>(img, p, q, out, pitch, rows, plane_stride, bad);
+    return cudaGetLastError();
+}
+
+cudaError_t tc_screen_compact(const float* ub, int er, int ec, const CellH* best, int2* locs,
+                              unsigned long long* count, unsigned long long max_count,
+                              cudaStream_t s) {
+    launch_pdl(k_tc_screen_compact, dim3(148 * 8), dim3(256), 0, s, ub, er, ec, best, locs, count,
+               max_count);
+    return cudaGetLastError();
+}
+
+cudaError_t split_centre_epilogue(GridDesc g, const double* dot, DevStats st, TStatsH ts,
+                                  SplitModel sm, double* rho_c, double* rad_c, uint8_t* deg_c,
+                                  CellH* partials, int n_partials, cudaStream_t s) {
+    launch_pdl(k_split_centre_epi, dim3(n_partials), dim3(256), 0, s, to_grid(g), dot, st, ts, sm,
+               rho_c, rad_c, deg_c, partials);
+    return cudaGetLastError();
+}
+
+cudaError_t split_pick(GridDesc g, const double* rho_c, const double* rad_c, const uint8_t* deg_c,
+                       int mode, const CellH* lim, const double* thr, double margin, int2* locs,
+                       int* gidx, unsigned long long* count, cudaStream_t s) {
+    const size_t G = size_t(g.tr) * g.tc;
+    const int blocks = int(std::min<size_t>((G + 255) / 256, 148 * 8));
+    launch_pdl(k_split_pick, dim3(blocks), dim3(256), 0, s, to_grid(g), rho_c, rad_c, deg_c, mode,
+               lim, thr, margin, locs, gidx, count);
+    return cudaGetLastError();
+}
+
+cudaError_t split_scatter(const double* rho, const int* gidx, const unsigned long long* count,
+                          double* rho_c, double* rad_c, cudaStream_t s) {
+    launch_pdl(k_split_scatter, dim3(64), dim3(256), 0, s, rho, gidx, count, rho_c, rad_c);
+    return cudaGetLastError();
+}
+
+cudaError_t split_sec_uncertain(GridDesc g, const double* map, const double* rho_c,
+                                const double* rad_c, const uint8_t* deg_c, const uint8_t* flat,
+                                const double* thr, const uint8_t* seeded, uint8_t* gflag,
+                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s) {
+    const size_t E = size_t(g.er) * g.ec;
+    const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 8));
+    launch_pdl(k_split_sec_uncertain, dim3(blocks), dim3(256), 0, s, to_grid(g), map, rho_c, rad_c,
+               deg_c, flat, thr, seeded, gflag, locs, gidx, count);
+    return cudaGetLastError();
+}
+
 cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& plan, uint8_t* out,
                        cudaStream_t s, const int* gate) {
     dim3 grid(64, plan.nch);
@@ -662,18 +978,22 @@ cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* 
     *nparts = grid;
     const size_t smem = job.plan.smem;
     cudaError_t e = cudaSuccess;
-    static size_t attr_set[3] = {0, 0, 0};
-    if (task.mode < 0 || task.mode > 2) return cudaErrorInvalidValue;
+    static size_t attr_set[5] = {0, 0, 0, 0, 0};
+    if (task.mode < 0 || task.mode > 4) return cudaErrorInvalidValue;
     if (attr_set[task.mode] < smem) {
         const void* fn = task.mode == 0 ? (const void*)k_tc_corr<0>
-                        : task.mode == 1 ? (const void*)k_tc_corr<1> : (const void*)k_tc_corr<2>;
+                        : task.mode == 1 ? (const void*)k_tc_corr<1>
+                        : task.mode == 2 ? (const void*)k_tc_corr<2>
+                        : task.mode == 3 ? (const void*)k_tc_corr<3> : (const void*)k_tc_corr<4>;
         cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem));
         attr_set[task.mode] = smem;
     }
     switch (task.mode) {
         case 0: launch_pdl(k_tc_corr<0>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
         case 1: launch_pdl(k_tc_corr<1>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
-        default: launch_pdl(k_tc_corr<2>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
+        case 2: launch_pdl(k_tc_corr<2>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
+        case 3: launch_pdl(k_tc_corr<3>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
+        default: launch_pdl(k_tc_corr<4>, dim3(grid), dim3(kTcThreads), smem, s, job, task, partials); break;
     }
     e = cudaGetLastError();
     return e;

@@ -466,6 +466,10 @@ struct TcPlan {  // B arrangement + shared-memory plan for one (template size, r
 struct TcJob {
     const uint8_t* imgp;  // pitched 8-bit image (tc_pitch), zero padded
     int pitch;
+    // split modes (3, 4): three byte planes of a non-integer image (tc_split_image), plane
+    // pl at imgp + pl*plane_stride; scr_delta / scr_gamma: the error model of tc_split.
+    size_t plane_stride = 0;
+    double scr_delta = 0.0, scr_gamma = 0.0;
     const uint8_t* bglob;  // tc_build_b output
     TcPlan plan;
     TStatsH ts;
@@ -477,7 +481,11 @@ struct TcBand {  // output rows r0 + sr*k, k < cnt (cnt <= 16); yi0 = group row 
 struct TcTask {
     const TcBand* bands;
     int nbands, ntc;  // tiles = bands x 2048-column tiles
-    int mode;         // 0 dense (out_rho = surface), 1 centres, 2 dense masked (mask == 2)
+    int mode;         // 0 dense (out_rho = surface), 1 centres, 2 dense masked (mask == 2),
+                      // 3 dense screening of a split (non-integer) image: out_ub = upper
+                      // bounds of rho, partials = the largest lower bound
+    int kp;           // split modes: TMEM slot stride between planes (rows per band <= kp)
+    float* out_ub;    // mode 3: upper bound of rho per location (-2 at flat windows)
     int c_lim;        // modes 0/2: output columns < c_lim
     int cbase, cstep, nc, tc;  // mode 1: centre columns cbase + cstep*tj, tj < nc; tc = row stride
     int c_last;                // mode 1: clipped last group's centre column (tj = tc-1) or -1
@@ -510,5 +518,34 @@ cudaError_t tc_build_b(const float* tf, int npad, int m, int n, const TcPlan& pl
                        const int* gate = nullptr);
 cudaError_t tc_corr(const TcJob& job, const TcTask& task, CellH* partials, int* nparts,
                     cudaStream_t s);
+// Split (non-integer image) variant, see k_tc.cu "split planes".  tc_split_image writes the
+// three zero-padded byte planes of floor(v * 2^16) and raises *bad when a pixel lies outside
+// [0, 256); tc_screen_compact lists the locations whose upper bound reaches the largest
+// lower bound (best->rho); count may exceed max_count (the caller then falls back).
+struct SplitModel {  // dot_ref in [dot_a (1 - gamma), (dot_a + delta)(1 + gamma)]
+    double delta, gamma;
+};
+// Split centre scan (scan 1 on a non-integer image): brackets per centre, the centres whose
+// exact rho is still needed (best-centre candidates, undecided seeding / bound tests), and
+// the exact values scattered back.  Lists have capacity G; gflag = (G + 3) & ~3 zeroed bytes.
+cudaError_t split_centre_epilogue(GridDesc g, const double* dot, DevStats st, TStatsH ts,
+                                  SplitModel sm, double* rho_c, double* rad_c, uint8_t* deg_c,
+                                  CellH* partials, int n_partials, cudaStream_t s);
+cudaError_t split_pick(GridDesc g, const double* rho_c, const double* rad_c, const uint8_t* deg_c,
+                       int mode, const CellH* lim, const double* thr, double margin, int2* locs,
+                       int* gidx, unsigned long long* count, cudaStream_t s);
+cudaError_t split_scatter(const double* rho, const int* gidx, const unsigned long long* count,
+                          double* rho_c, double* rad_c, cudaStream_t s);
+cudaError_t split_sec_uncertain(GridDesc g, const double* map, const double* rho_c,
+                                const double* rad_c, const uint8_t* deg_c, const uint8_t* flat,
+                                const double* thr, const uint8_t* seeded, uint8_t* gflag,
+                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s);
+constexpr int kTcSplitPlanes = 3;
+constexpr int kTcSplitRows = 5;  // rows per band: 3 planes x 5 rows <= 16 TMEM slots
+cudaError_t tc_split_image(const double* img, int p, int q, uint8_t* out, int pitch, int rows,
+                           size_t plane_stride, int* bad, cudaStream_t s);
+cudaError_t tc_screen_compact(const float* ub, int er, int ec, const CellH* best, int2* locs,
+                              unsigned long long* count, unsigned long long max_count,
+                              cudaStream_t s);
 
 }  // namespace tmk

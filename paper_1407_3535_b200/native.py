@@ -112,6 +112,7 @@ SIGNATURES = {
     "tm_image_set_noise_floor": (C.c_int, [_P, _P, C.c_uint64]),
     "tm_ctx_launch_count": (C.c_int64, [_P]),
     "tm_ctx_search_stats": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
+    "tm_ctx_split_stats": (C.c_int, [_P, C.POINTER(C.c_int64), C.POINTER(C.c_int64)]),
     "tm_ctx_stream": (C.c_void_p, [_P]),
     "tm_ctx_set_profiling": (C.c_int, [_P, C.c_int]),
     "tm_ctx_phase_times": (C.c_int, [_P, C.c_char_p, C.c_size_t]),

@@ -1,0 +1,114 @@
+"""Split tensor-core screening of NON-INTEGER search images (k_tc.cu "split planes").
+
+The reference evaluates window_dot (detail.hpp:32-41) on FP64 pixels in sequence; the
+B200 path brackets every rho on three byte planes with tcgen05 kind::i8 and re-evaluates
+only the locations that can still win with the FP64 replica.  The bar is the same as
+everywhere else: results bit-identical to the oracle (which is pinned to the reference).
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+from conftest import RESULT_KEYS, assert_same_result
+
+pytestmark = pytest.mark.gpu
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _image(rng, p, q, smooth=True):
+    base = np.cumsum(np.cumsum(rng.normal(size=(p, q)), 0), 1) if smooth else rng.normal(size=(p, q))
+    return np.clip(np.rint((base - base.min()) / (np.ptp(base) + 1e-9) * 255), 0, 255)
+
+
+def _template(rng, img, m, n, noise=3.0):
+    p, q = img.shape
+    r0, c0 = int(rng.integers(0, p - m + 1)), int(rng.integers(0, q - n + 1))
+    return np.clip(np.rint(img[r0:r0 + m, c0:c0 + n] * 1.1 - 5 + rng.normal(0, noise, (m, n))),
+                   0, 255)
+
+
+SHAPES = [(96, 96, 16, 16), (70, 131, 33, 31), (128, 96, 17, 64), (40, 2100, 8, 8),
+          (300, 260, 64, 64), (61, 61, 5, 3)]
+
+
+@pytest.mark.parametrize("idx", range(len(SHAPES)))
+def test_brute_on_blurred_image_equals_oracle(ctx, port, idx):
+    p, q, m, n = SHAPES[idx]
+    rng = np.random.default_rng(100 + idx)
+    img = _image(rng, p, q, smooth=idx % 2 == 0)
+    if idx == 2:
+        img[10:60, 5:50] = 77.0  # flat windows (degenerate locations never win)
+    t = _template(rng, img, m, n)
+    blurred = port.blur(img)
+    assert np.any(blurred != np.rint(blurred))
+    g = ctx.image(blurred)
+    assert not g.is_integer
+    s0 = ctx.split_stats()
+    a = ctx.brute_force_match(t, g)
+    s1 = ctx.split_stats()
+    b = port.brute(t, blurred)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+    E = (p - m + 1) * (q - n + 1)
+    assert s1["screened"] - s0["screened"] == E, "the split tensor-core pass did not run"
+    assert 1 <= s1["exact"] - s0["exact"] <= max(16, E // 50)
+
+
+def test_brute_ties_and_near_ties(ctx, port):
+    """Exact duplicates of the best window: better_candidate's (row, col) order decides, so
+    every tied location must survive the screening."""
+    rng = np.random.default_rng(5)
+    img = _image(rng, 90, 120)
+    blurred = port.blur(img)
+    patch = blurred[20:36, 30:46].copy()
+    for (r, c) in ((50, 70), (3, 100), (70, 2)):
+        blurred[r:r + 16, c:c + 16] = patch
+    t = np.clip(np.rint(patch), 0, 255)
+    a = ctx.brute_force_match(t, ctx.image(blurred))
+    b = port.brute(t, blurred)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+    # a copy that differs by less than the screening radius
+    blurred[50, 70] += 2.0 ** -20
+    a = ctx.brute_force_match(t, ctx.image(blurred))
+    b = port.brute(t, blurred)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+
+
+def test_out_of_range_and_flat_fall_back(ctx, port):
+    rng = np.random.default_rng(9)
+    img = _image(rng, 64, 64)
+    t = _template(rng, img, 9, 9)
+    for f in (lambda x: x * 1.5 + 0.25, lambda x: x - 40.5):  # pixels >= 256 / negative
+        im2 = f(port.blur(img))
+        s0 = ctx.split_stats()
+        a = ctx.brute_force_match(t, ctx.image(im2))
+        assert ctx.split_stats() == s0  # FP64 replica
+        assert_same_result(a, port.brute(t, im2), keys=RESULT_KEYS[:-1])
+    flat = np.full((40, 40), 12.25)
+    a = ctx.brute_force_match(t, ctx.image(flat))
+    assert_same_result(a, port.brute(t, flat), keys=RESULT_KEYS[:-1])
+
+
+def test_split_switch_off_is_the_fp64_replica():
+    code = (
+        "import numpy as np\n"
+        "from oracle.binding import Oracle\n"
+        "from paper_1407_3535_b200 import api\n"
+        "rng = np.random.default_rng(3)\n"
+        "img = np.clip(np.rint(rng.normal(128, 40, (80, 80))), 0, 255)\n"
+        "port = Oracle('port')\n"
+        "b = port.blur(img)\n"
+        "t = np.clip(np.rint(b[10:26, 20:36]), 0, 255)\n"
+        "with api.Context(0) as ctx:\n"
+        "    a = ctx.brute_force_match(t, ctx.image(b))\n"
+        "    assert ctx.split_stats() == {'screened': 0, 'exact': 0}\n"
+        "    o = port.brute(t, b)\n"
+        "    assert (a.best_row, a.best_col, a.best_rho) == (o.best_row, o.best_col, o.best_rho)\n"
+        "print('ok')\n")
+    env = dict(os.environ, TMATCH_TC_SPLIT="0", PYTHONPATH=ROOT)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True,
+                         text=True, timeout=600)
+    assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
