@@ -263,6 +263,13 @@ struct tm_ctx {
     DBuf<uint8_t> seq_deg, seeded, deg_c, visits;
     DBuf<double> rho_c, surface, dotbuf;
     DBuf<float> ub_surface;  // split screening: upper bounds of rho
+    // split centre scan: bracket radius per group (0 = rho_c exact), the centres picked for
+    // the exact replay (location, group index, exact rho) and the per-group listed flags
+    DBuf<double> rad_c, split_rho;
+    DBuf<int2> split_locs;
+    DBuf<int> split_gidx;
+    DBuf<uint8_t> split_flag;
+    int64_t split_centres = 0;  // centres bracketed by the split centre scan
     bool tc_split = true;    // TMATCH_TC_SPLIT=0: non-integer images stay on the FP64 replica
     int64_t split_screened = 0, split_exact = 0;  // locations bracketed / re-evaluated exactly
     DBuf<float> tf;
@@ -810,6 +817,14 @@ const uint8_t* tc_image(tm_ctx* ctx, tm_image* img, int ec) {
     return img->u8p.p;
 }
 
+// Error model of the split planes (k_tc.cu): the truncation is < 2^-16 per pixel, i.e.
+// < 2^-16 * sum(T) per dot; the reference's sequential FP64 sum of m*n non-negative products
+// (detail.hpp:32-41) is within gamma_{mn} of the true dot (twice the textbook bound here).
+tmk::SplitModel split_model(const Tmpl& T) {
+    return tmk::SplitModel{T.ts.mn * T.ts.mu * (1.0 + 1e-9) / 65536.0,
+                           (T.ts.mn + 4.0) * 2.220446049250313e-16};
+}
+
 // Non-integer image + integer template: the byte planes for the split tensor-core
 // screening, made on first use.  False when a pixel lies outside [0, 256) (FP64 replica).
 bool split_path(tm_ctx* ctx, tm_image* img, const Tmpl& T) {
@@ -936,8 +951,9 @@ int tc_run(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, const RowSet
         job.imgp = img->split.p;
         job.pitch = img->split_pitch;
         job.plane_stride = img->split_stride;
-        job.scr_delta = T.ts.mn * T.ts.mu * (1.0 + 1e-9) / 65536.0;
-        job.scr_gamma = (T.ts.mn + 4.0) * 2.220446049250313e-16;
+        const tmk::SplitModel sm = split_model(T);
+        job.scr_delta = sm.delta;
+        job.scr_gamma = sm.gamma;
         task.kp = tmk::kTcSplitRows;
     } else {
         job.imgp = tc_image(ctx, img, ws.ec);
@@ -1208,6 +1224,105 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
     CK(cudaStreamSynchronize(ctx->s));
     eval_list(ctx, img, ws, T, ctx->seed_locs.p, ctx->counters.p + 4, int(GS), ctx->rho_c.p + off,
               ctx->deg_c.p + off, 0, op);
+}
+
+// ---- scan 1 on a non-integer image through the split planes ---------------------------
+// Frozen / seeded policies only: every decision that reads rho_c (best centre, seeding,
+// members' bound tests) is either settled by the centre's bracket or the centre is
+// re-evaluated by the FP64 replica first, so counts, visit codes and results equal the
+// all-exact path's.  (The sequential replay re-tests members at a moving threshold and
+// keeps the exact scan.)
+bool split_centres_ok(tm_ctx* ctx, tm_image* img, const Tmpl& T, const tmk::GridDesc& g) {
+    return g.h <= tmk::kTcMaxClasses && g.ti_lo == 0 && g.ti_hi == g.tr &&
+           split_path(ctx, img, T) && tmk::tc_plan(T.m, T.n, g.h, kTcSmemBudget).nch > 0;
+}
+
+// The centres listed in split_locs / split_gidx (count on the device) -> exact rho by the
+// FP64 replica, scattered into rho_c (radius 0); their best -> cells[slot] (+ op).
+void split_exact(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, size_t G,
+                 unsigned long long* cnt, int slot, const tmk::ReduceOp* op = nullptr) {
+    eval_list(ctx, img, ws, T, ctx->split_locs.p, cnt, int(std::min<size_t>(G, INT_MAX)),
+              ctx->split_rho.p, nullptr, slot, op);
+    CK(tmk::split_scatter(ctx->split_rho.p, ctx->split_gidx.p, cnt, ctx->rho_c.p, ctx->rad_c.p,
+                          ctx->s));
+    ctx->add(1);
+}
+
+void centre_scan_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                       const tmk::GridDesc& g, const tmk::ReduceOp* op) {
+    const size_t G = size_t(g.tr) * g.tc;
+    ctx->sa_ready = false;
+    ctx->rho_c.ensure(G);
+    ctx->deg_c.ensure(G);
+    ctx->rad_c.ensure(G);
+    ctx->dotbuf.ensure(G);
+    ctx->split_rho.ensure(G);
+    ctx->split_locs.ensure(G);
+    ctx->split_gidx.ensure(G);
+    ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
+    unsigned long long* cnt = ctx->counters.p + 35;
+    {
+        Phase ph(ctx, "centre_scan");
+        RowSet rs;
+        rs.kind = 1;
+        rs.lo = 0;
+        rs.hi = g.tr;
+        rs.g = g;
+        const bool clipped = size_t(g.tc) * g.w > size_t(g.ec);
+        tmk::TcTask task{};
+        task.mode = 4;
+        task.cbase = g.w / 2;
+        task.cstep = g.w;
+        task.nc = clipped ? g.tc - 1 : g.tc;
+        task.tc = g.tc;
+        task.c_last = clipped ? centre_col_h(g, g.tc - 1) : -1;
+        task.out_rho = ctx->dotbuf.p;
+        tc_run(ctx, img, ws, T, rs, g.h, task);
+        const int n1 = int(std::min<size_t>(kListBlocks, (G + 255) / 256));
+        CK(tmk::split_centre_epilogue(g, ctx->dotbuf.p, ws.dev(), T.ts, split_model(T),
+                                      ctx->rho_c.p, ctx->rad_c.p, ctx->deg_c.p, ctx->partials.p,
+                                      n1, ctx->s));
+        ctx->add(1);
+        reduce_to(ctx, n1, 3);  // cells[3]: the largest lower bound
+        CK(cudaMemsetAsync(cnt, 0, 8, ctx->s));
+        CK(tmk::split_pick(g, ctx->rho_c.p, ctx->rad_c.p, ctx->deg_c.p, 0, ctx->cells.p + 3,
+                           ctx->thr.p, 0.0, ctx->split_locs.p, ctx->split_gidx.p, cnt, ctx->s));
+        ctx->add(1);
+    }
+    ctx->split_centres += (long long)G;
+    split_exact(ctx, img, ws, T, G, cnt, 0, op);  // exact best centre -> cells[0], threshold
+}
+
+// Seeded policy: centres whose seeding decision (rho_c >= thr - margin, k_seed_members) the
+// bracket leaves open get their exact rho first.
+void split_refine_seeding(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                          const tmk::GridDesc& g, double margin) {
+    const size_t G = size_t(g.tr) * g.tc;
+    unsigned long long* cnt = ctx->counters.p + 35;
+    CK(cudaMemsetAsync(cnt, 0, 8, ctx->s));
+    CK(tmk::split_pick(g, ctx->rho_c.p, ctx->rad_c.p, ctx->deg_c.p, 1, ctx->cells.p + 3,
+                       ctx->thr.p, margin, ctx->split_locs.p, ctx->split_gidx.p, cnt, ctx->s));
+    ctx->add(1);
+    split_exact(ctx, img, ws, T, G, cnt, 3);
+}
+
+// Scan 2: groups with a member whose bound test the centre's bracket leaves open.
+void split_refine_bounds(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                         const tmk::GridDesc& g, const double* map, const uint8_t* seeded) {
+    const size_t G = size_t(g.tr) * g.tc;
+    unsigned long long* cnt = ctx->counters.p + 35;
+    const size_t fl = (G + 3) & ~size_t(3);
+    ctx->split_flag.ensure(fl);
+    CK(cudaMemsetAsync(ctx->split_flag.p, 0, fl, ctx->s));
+    CK(cudaMemsetAsync(cnt, 0, 8, ctx->s));
+    {
+        Phase ph(ctx, "split_bounds");
+        CK(tmk::split_sec_uncertain(g, map, ctx->rho_c.p, ctx->rad_c.p, ctx->deg_c.p, ws.fl.p,
+                                    ctx->thr.p, seeded, ctx->split_flag.p, ctx->split_locs.p,
+                                    ctx->split_gidx.p, cnt, ctx->s));
+        ctx->add(1);
+    }
+    split_exact(ctx, img, ws, T, G, cnt, 3);
 }
 
 // Speculative centre scan for tm_search: the B build and the tensor-core centre dots for a
@@ -1901,12 +2016,18 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     // the centre reduction also bootstraps the threshold (matcher.cpp:121-125) and zeroes
     // the seeding counters and the scan-2 tally
     const uint8_t* seeded = nullptr;
+    bool split_c = false;  // scan 1 bracketed on the split planes (non-integer image)
     if (!in.prescanned) {
     const tmk::ReduceOp op_init = centre_op(ctx, P);
-    centre_scan(ctx, img, ws, T, g, &op_init);
+    split_c = !seq && split_centres_ok(ctx, img, T, g);
+    if (split_c)
+        centre_scan_split(ctx, img, ws, T, g, &op_init);
+    else
+        centre_scan(ctx, img, ws, T, g, &op_init);
     HT("centre_scan");
 
     if (policy == TM_POLICY_SEEDED) {
+        if (split_c) split_refine_seeding(ctx, img, ws, T, g, P.seed_margin);
         const unsigned long long max_groups = 256;
         const unsigned long long max_locs = max_groups * (unsigned long long)(g.h * g.w);
         ctx->seed_locs.ensure(max_locs);
@@ -1929,6 +2050,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     ctx->visits.ensure(E);
     uint8_t* visits = ctx->visits.p;
     ctx->locs.ensure(E);
+    if (split_c) split_refine_bounds(ctx, img, ws, T, g, in.map, seeded);
     if (!in.prescanned) {
         Phase ph(ctx, "sec_compact");
         ctx->sa_c.ensure(G);
@@ -2431,7 +2553,7 @@ int tm_ctx_search_stats(const tm_ctx* ctx, int64_t* fused_hits, int64_t* fused_m
 
 int tm_ctx_split_stats(const tm_ctx* ctx, int64_t* screened, int64_t* exact) {
     if (!ctx || !screened || !exact) return TM_EINVAL;
-    *screened = ctx->split_screened;
+    *screened = ctx->split_screened + ctx->split_centres;
     *exact = ctx->split_exact;
     return TM_OK;
 }

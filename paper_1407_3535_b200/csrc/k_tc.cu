@@ -49,6 +49,10 @@ namespace tmk {
 
 namespace {
 
+Grid to_grid(GridDesc d) {
+    return Grid::make(d.er, d.ec, d.h, d.w, d.tr, d.tc, d.ti_lo, d.ti_hi);
+}
+
 constexpr int kTcThreads = 320;  // producer, MMA, 8 epilogue warps
 constexpr int kTcMaxStages = 64;
 constexpr int kTcBarBytes = 2048;  // barriers + TMEM slot at the start of shared memory

@@ -112,3 +112,66 @@ def test_split_switch_off_is_the_fp64_replica():
     out = subprocess.run([sys.executable, "-c", code], env=env, cwd=ROOT, capture_output=True,
                          text=True, timeout=600)
     assert out.returncode == 0 and "ok" in out.stdout, out.stderr[-2000:]
+
+
+# ---- scan 1 on the split planes (transitive search of a non-integer image) ---------------
+SEARCH_SHAPES = [(96, 96, 16, 16, 3, 3), (70, 131, 33, 31, 5, 5), (128, 96, 17, 64, 3, 5),
+                 (40, 2100, 8, 8, 3, 3), (300, 260, 64, 64, 5, 5), (61, 61, 5, 3, 7, 3),
+                 (200, 180, 24, 24, 1, 1)]
+
+
+@pytest.mark.parametrize("idx", range(len(SEARCH_SHAPES)))
+def test_frozen_search_on_blurred_image_equals_oracle(ctx, port, idx):
+    """Frozen policy (the reference's --parallel scan): counts, visit codes, threshold and
+    result bit-identical to the oracle, with scan 1 bracketed on the tensor cores."""
+    p, q, m, n, h, w = SEARCH_SHAPES[idx]
+    rng = np.random.default_rng(200 + idx)
+    img = _image(rng, p, q, smooth=idx % 2 == 0)
+    if idx == 2:
+        img[10:60, 5:50] = 77.0  # flat windows: degenerate centres and flat members
+    t = _template(rng, img, m, n, noise=1.0 + idx)
+    blurred = port.blur(img)
+    amap = port.local_autocorrelation(blurred, m, n, h, w)
+    g = ctx.image(blurred)
+    s0 = ctx.split_stats()
+    for init in (None, 0.5):
+        a, va = ctx.transitive_search(t, g, amap, h, w, parallel=True, threads=3,
+                                      record_visits=True, init_threshold=init)
+        b, vb = port.transitive_search(t, blurred, amap, h, w, parallel=True, threads=3,
+                                       visits=True, init_threshold=init)
+        np.testing.assert_array_equal(va, vb)
+        assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+    er, ec = p - m + 1, q - n + 1
+    G = -(-er // h) * -(-ec // w)
+    if G > 1:
+        assert ctx.split_stats()["screened"] - s0["screened"] == 2 * G, "split centre scan did not run"
+
+
+@pytest.mark.parametrize("idx", [0, 1, 4])
+def test_seeded_search_on_blurred_image(ctx, port, idx):
+    """Seeded policy: same argmax / rho as brute force, sound eliminations, consistent counts."""
+    p, q, m, n, h, w = SEARCH_SHAPES[idx]
+    rng = np.random.default_rng(300 + idx)
+    img = _image(rng, p, q)
+    t = _template(rng, img, m, n)
+    blurred = port.blur(img)
+    amap = port.local_autocorrelation(blurred, m, n, h, w)
+    b, surface = port.brute(t, blurred, surface=True)
+    a, vis = ctx.transitive_search(t, ctx.image(blurred), amap, h, w, policy="seeded",
+                                   record_visits=True)
+    assert (a.best_row, a.best_col, a.best_rho) == (b.best_row, b.best_col, b.best_rho)
+    assert np.all(surface[vis == 1] <= a.final_threshold + 1e-9)
+    assert a.eliminated + a.retained + a.centers == b.ops
+
+
+def test_opta_match_with_blur_uses_split_planes(ctx, port):
+    """match(mode=opta) whose optimised image is blurred (kappa > 0): prepare + frozen run
+    equal to the oracle, scan 1 on the split planes."""
+    rng = np.random.default_rng(17)
+    img = _image(rng, 160, 160, smooth=False)
+    t = _template(rng, img, 16, 16, noise=2.0)
+    s0 = ctx.split_stats()
+    a, va = ctx.match(t, img, mode="opta", parallel=True, threads=3, record_visits=True)
+    b, vb = port.match(t, img, mode="opta", parallel=True, threads=3, visits=True)
+    np.testing.assert_array_equal(va, vb)
+    assert_same_result(a, b)
