@@ -328,7 +328,8 @@ def roofline(phases, wl, res, pk, fp64_search=False):
       autocorr_u8    p*q + 25 B per location (R_co map written)
       autocorr_count p*q + 17 B per location (count-only EGS candidate, stops early)
       sec_compact    10 B per location (map 8 + flat 1 + visit 1)
-      centre_scan    2*m*n ops per group centre (tcgen05 kind::i8)
+      centre_scan    2*m*n ops per group centre (tcgen05 kind::i8); x 3 planes on a
+                     non-integer search image (split variant)
     """
     p, q = wl.image.shape
     m, n = wl.templates[0].pixels.shape
@@ -350,8 +351,15 @@ def roofline(phases, wl, res, pk, fp64_search=False):
         "centre_scan": ("tensor", 2.0 * m * n * G,
                         "k_tc_build_b + k_tc_corr<1> + k_centre_epi (tcgen05 kind::i8)"),
     }
-    if fp64_search:  # OptA with kappa > 0: the search image is non-integer (FP64 replica
-        defs.pop("centre_scan")  # kernels, no tensor-core / i8 roofline)
+    if fp64_search:
+        # OptA with kappa > 0: the search image is non-integer.  Scan 1 runs on the three
+        # byte planes of the split tensor-core variant (DESIGN 4.3a: 3 x 2*m*n integer ops
+        # per centre, the exact FP64 replays of undecided centres included in the phase);
+        # the window statistics are FP64 replica kernels (no u8 roofline).
+        defs["centre_scan"] = ("tensor", 3 * 2.0 * m * n * G,
+                               "k_tc_build_b + k_tc_corr<4> + k_split_centre_epi + k_split_pick "
+                               "+ k_list_f64 (tcgen05 kind::i8 on three byte planes, bracketed "
+                               "rho_c, exact replay of the undecided centres)")
         defs.pop("window_stats")
     rows = []
     for name, v in phases.items():
@@ -608,6 +616,9 @@ def run_b200(args):
                     "elim_pct": r.elim_pct, "eliminated": r.eliminated, "retained": r.retained,
                     "centers": r.centers, "ops": r.ops} for r in res[:4]],
         "h_e": info["h"], "kappa": info["kappa"],
+        # non-integer search images (OptA, kappa > 0): centres / locations bracketed on the
+        # tensor cores by the split-plane variant since the context was created
+        "split_planes": ctx.split_stats(),
         "elimination_pct": statistics.mean(r.elim_pct for r in res),
         "parity": {"full_size_vs_reference": parity, "cpu_sample_vs_reference": sample_parity},
         "frozen": frozen,

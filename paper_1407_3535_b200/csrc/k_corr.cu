@@ -381,7 +381,7 @@ __global__ void __launch_bounds__(256)
     const long long nloc = min((long long)*count, (long long)max_count);
     const TStats ts = to_ts(job.ts);
     Cell best = no_cell();
-    if (nloc <= 4ll * gridDim.x) {  // short list: one CTA per location
+    if (nloc <= 16ll * gridDim.x) {  // short list: one CTA per location
         for (long long li = blockIdx.x; li < nloc; li += gridDim.x) {
             const int2 rc = locs[li];
             const size_t kk = size_t(rc.x) * job.st.ec + rc.y;
