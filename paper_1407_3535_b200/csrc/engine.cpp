@@ -1227,11 +1227,11 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 }
 
 // ---- scan 1 on a non-integer image through the split planes ---------------------------
-// Frozen / seeded policies only: every decision that reads rho_c (best centre, seeding,
-// members' bound tests) is either settled by the centre's bracket or the centre is
-// re-evaluated by the FP64 replica first, so counts, visit codes and results equal the
-// all-exact path's.  (The sequential replay re-tests members at a moving threshold and
-// keeps the exact scan.)
+// Every decision that reads rho_c (best centre, seeding, members' bound tests) is either
+// settled by the centre's bracket or the centre is re-evaluated by the FP64 replica first,
+// so counts, visit codes and results equal the all-exact path's.  Sequential policy: the
+// running threshold only rises from scan 1's, so members certainly eliminated at it stay
+// eliminated; every other member's group gets its exact rho_c (the replay re-tests them).
 bool split_centres_ok(tm_ctx* ctx, tm_image* img, const Tmpl& T, const tmk::GridDesc& g) {
     return g.h <= tmk::kTcMaxClasses && g.ti_lo == 0 && g.ti_hi == g.tr &&
            split_path(ctx, img, T) && tmk::tc_plan(T.m, T.n, g.h, kTcSmemBudget).nch > 0;
@@ -1308,7 +1308,8 @@ void split_refine_seeding(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& 
 
 // Scan 2: groups with a member whose bound test the centre's bracket leaves open.
 void split_refine_bounds(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
-                         const tmk::GridDesc& g, const double* map, const uint8_t* seeded) {
+                         const tmk::GridDesc& g, const double* map, const uint8_t* seeded,
+                         bool moving) {
     const size_t G = size_t(g.tr) * g.tc;
     unsigned long long* cnt = ctx->counters.p + 35;
     const size_t fl = (G + 3) & ~size_t(3);
@@ -1319,7 +1320,7 @@ void split_refine_bounds(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T
         Phase ph(ctx, "split_bounds");
         CK(tmk::split_sec_uncertain(g, map, ctx->rho_c.p, ctx->rad_c.p, ctx->deg_c.p, ws.fl.p,
                                     ctx->thr.p, seeded, ctx->split_flag.p, ctx->split_locs.p,
-                                    ctx->split_gidx.p, cnt, ctx->s));
+                                    ctx->split_gidx.p, cnt, ctx->s, moving ? 1 : 0));
         ctx->add(1);
     }
     split_exact(ctx, img, ws, T, G, cnt, 3);
@@ -1869,6 +1870,9 @@ struct SearchIn {
 // Scan-2 survivors (listed in ctx->locs, marked 2 in ctx->visits) -> cells[2].  Dense
 // survivor sets run the band kernel masked by the visit map; sparse ones one warp per
 // location.  rho_loc (optional, extent-sized) receives rho by location.
+bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                 const uint8_t* mask = nullptr);
+
 void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
                     const tmk::GridDesc& g, unsigned long long survivors, double* rho_loc,
                     const tmk::TileFlags* tflags = nullptr) {
@@ -1923,6 +1927,13 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         }
         reduce_to(ctx, np, 2);
     } else if (survivors > 0) {
+        // non-integer image, many survivors whose rho only matters for the argmax (frozen /
+        // seeded): bracket them all on the split planes (masked by the visit codes) and
+        // replay the few that can still win
+        if (!rho_loc && survivors > std::max<unsigned long long>(16 * kListBlocks, E / 64) &&
+            g.ti_lo == 0 && g.ti_hi == g.tr && split_path(ctx, img, T) &&
+            brute_split(ctx, img, ws, T, visits))
+            return;
         const tmk::CorrJob job = make_job(ctx, img, ws, T);
         ctx->partials.ensure(kListBlocks);
         {
@@ -2019,7 +2030,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     bool split_c = false;  // scan 1 bracketed on the split planes (non-integer image)
     if (!in.prescanned) {
     const tmk::ReduceOp op_init = centre_op(ctx, P);
-    split_c = !seq && split_centres_ok(ctx, img, T, g);
+    split_c = split_centres_ok(ctx, img, T, g);
     if (split_c)
         centre_scan_split(ctx, img, ws, T, g, &op_init);
     else
@@ -2050,7 +2061,7 @@ tm_match_result search(tm_ctx* ctx, const SearchIn& in, const Tmpl& T,
     ctx->visits.ensure(E);
     uint8_t* visits = ctx->visits.p;
     ctx->locs.ensure(E);
-    if (split_c) split_refine_bounds(ctx, img, ws, T, g, in.map, seeded);
+    if (split_c) split_refine_bounds(ctx, img, ws, T, g, in.map, seeded, seq);
     if (!in.prescanned) {
         Phase ph(ctx, "sec_compact");
         ctx->sa_c.ensure(G);
@@ -2217,7 +2228,10 @@ tmk::CellH refine(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T, int l
 // tensor-core pass, list the locations whose upper bound reaches the largest lower bound,
 // evaluate those with the FP64 replica (window_dot order) -> cells[2].  False: the list
 // overflowed or nothing was non-flat (the caller runs the dense FP64 replica instead).
-bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
+// mask: only the locations with mask == 2 compete (scan-2 survivors of a frozen / seeded
+// search).
+bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
+                 const uint8_t* mask) {
     const int er = ws.er, ec = ws.ec;
     const size_t E = size_t(er) * ec;
     RowSet rs;
@@ -2227,16 +2241,17 @@ bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
     task.mode = 3;
     task.c_lim = ec;
     task.c_last = -1;
+    task.mask = mask;
     ctx->ub_surface.ensure(E);
     task.out_ub = ctx->ub_surface.p;
     ctx->partials.ensure(size_t(148 + kListBlocks) + 1);
     const int np = tc_run(ctx, img, ws, T, rs, 1, task);
     reduce_to(ctx, np, 3);  // cells[3].rho = the largest lower bound
     const size_t cap = std::min<size_t>(E, size_t(1) << 20);
-    ctx->locs.ensure(cap);
+    ctx->split_locs.ensure(cap);
     unsigned long long* cnt = ctx->counters.p + 35;
     CK(cudaMemsetAsync(cnt, 0, 8, ctx->s));
-    CK(tmk::tc_screen_compact(ctx->ub_surface.p, er, ec, ctx->cells.p + 3, ctx->locs.p, cnt, cap,
+    CK(tmk::tc_screen_compact(ctx->ub_surface.p, er, ec, ctx->cells.p + 3, ctx->split_locs.p, cnt, cap,
                               ctx->s));
     ctx->add(1);
     unsigned long long n = 0;
@@ -2245,7 +2260,7 @@ bool brute_split(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T) {
     if (n == 0 || n > cap) return false;
     ctx->split_screened += (long long)E;
     ctx->split_exact += (long long)n;
-    eval_list(ctx, img, ws, T, ctx->locs.p, cnt, int(cap), nullptr, nullptr, 2);
+    eval_list(ctx, img, ws, T, ctx->split_locs.p, cnt, int(cap), nullptr, nullptr, 2);
     return true;
 }
 

@@ -436,7 +436,8 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     for (int ph = 0; ph < 16; ++ph) {
                         if (!((cmask >> ph) & 1u)) continue;
                         const size_t kk = rb + ph;
-                        if (st.flat[kk]) {
+                        // masked (scan-2 survivors only): the other locations never compete
+                        if (st.flat[kk] || (task.mask && task.mask[kk] != 2)) {
                             task.out_ub[kk] = -2.0f;
                             continue;
                         }
@@ -760,15 +761,18 @@ __global__ void k_split_scatter(const double* __restrict__ rho, const int* __res
 // rho*R + sqrt(1 - rho^2) sqrt(1 - R^2) is monotone in rho on either side of rho = R, so its
 // range over the bracket is spanned by the endpoint values unless R lies inside; brackets
 // reaching |rho| ~ 1 (where the FP64 square root amplifies rounding) are listed outright.
+// A non-finite / below -1 threshold eliminates nothing at T; with a moving threshold those
+// members are re-tested later, so every bracketed group is listed.
 __global__ void __launch_bounds__(256)
     k_split_sec_uncertain(Grid g, const double* __restrict__ map, const double* __restrict__ rho_c,
                           const double* __restrict__ rad_c, const uint8_t* __restrict__ deg_c,
                           const uint8_t* __restrict__ flat, const double* __restrict__ thr_ptr,
                           const uint8_t* __restrict__ seeded, uint8_t* __restrict__ gflag,
-                          int2* locs, int* gidx, unsigned long long* count) {
+                          int2* locs, int* gidx, unsigned long long* count, int moving) {
     pdl_wait();
     const double T = *thr_ptr;
-    if (!(T >= -1.0)) return;  // nothing is eliminated: no decision depends on rho_c
+    if (!(T >= -1.0) && !moving) return;  // nothing is eliminated: no decision reads rho_c
+    const bool none = !(T >= -1.0);
     const double tb = dmin(T, 1.0);
     const size_t E = size_t(g.er) * g.ec;
     for (size_t k = blockIdx.x * size_t(blockDim.x) + threadIdx.x; k < E;
@@ -785,12 +789,15 @@ __global__ void __launch_bounds__(256)
         const double a = rho_c[gi];
         const double lo = a - e, hi = a + e;
         const double b = dclamp(map[k], -1.0, 1.0);
-        bool unsure = hi >= 0.9999995 || lo <= -0.9999995 || (b >= lo && b <= hi);
+        bool unsure = none || hi >= 0.9999995 || lo <= -0.9999995 || (b >= lo && b <= hi);
         if (!unsure) {
             const double f_lo = __dadd_rn(__dmul_rn(lo, b), half_gap(lo, b));
             const double f_hi = __dadd_rn(__dmul_rn(hi, b), half_gap(hi, b));
             const double fmax = dmax(f_lo, f_hi), fmin = dmin(f_lo, f_hi);
-            unsure = !(tb >= fmax + 1e-12 || tb < fmin - 1e-12);
+            // moving (sequential policy): the threshold only rises from T, so a member
+            // certainly eliminated now stays eliminated; every other member may be re-tested
+            // at a later threshold and needs the exact rho_c
+            unsure = !(tb >= fmax + 1e-12 || (!moving && tb < fmin - 1e-12));
         }
         if (unsure) {
             // one listing per group: byte flags claimed through a 32-bit atomicOr
@@ -960,11 +967,12 @@ cudaError_t split_scatter(const double* rho, const int* gidx, const unsigned lon
 cudaError_t split_sec_uncertain(GridDesc g, const double* map, const double* rho_c,
                                 const double* rad_c, const uint8_t* deg_c, const uint8_t* flat,
                                 const double* thr, const uint8_t* seeded, uint8_t* gflag,
-                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s) {
+                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s,
+                                int moving) {
     const size_t E = size_t(g.er) * g.ec;
     const int blocks = int(std::min<size_t>((E + 255) / 256, 148 * 8));
     launch_pdl(k_split_sec_uncertain, dim3(blocks), dim3(256), 0, s, to_grid(g), map, rho_c, rad_c,
-               deg_c, flat, thr, seeded, gflag, locs, gidx, count);
+               deg_c, flat, thr, seeded, gflag, locs, gidx, count, moving);
     return cudaGetLastError();
 }
 

@@ -483,7 +483,8 @@ struct TcTask {
     int nbands, ntc;  // tiles = bands x 2048-column tiles
     int mode;         // 0 dense (out_rho = surface), 1 centres, 2 dense masked (mask == 2),
                       // 3 dense screening of a split (non-integer) image: out_ub = upper
-                      // bounds of rho, partials = the largest lower bound
+                      // bounds of rho, partials = the largest lower bound (mask != null:
+                      // only locations with mask == 2 compete), 4 centres of a split image
     int kp;           // split modes: TMEM slot stride between planes (rows per band <= kp)
     float* out_ub;    // mode 3: upper bound of rho per location (-2 at flat windows)
     int c_lim;        // modes 0/2: output columns < c_lim
@@ -539,7 +540,8 @@ cudaError_t split_scatter(const double* rho, const int* gidx, const unsigned lon
 cudaError_t split_sec_uncertain(GridDesc g, const double* map, const double* rho_c,
                                 const double* rad_c, const uint8_t* deg_c, const uint8_t* flat,
                                 const double* thr, const uint8_t* seeded, uint8_t* gflag,
-                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s);
+                                int2* locs, int* gidx, unsigned long long* count, cudaStream_t s,
+                                int moving = 0);
 constexpr int kTcSplitPlanes = 3;
 constexpr int kTcSplitRows = 5;  // rows per band: 3 planes x 5 rows <= 16 TMEM slots
 cudaError_t tc_split_image(const double* img, int p, int q, uint8_t* out, int pitch, int rows,

@@ -121,9 +121,10 @@ SEARCH_SHAPES = [(96, 96, 16, 16, 3, 3), (70, 131, 33, 31, 5, 5), (128, 96, 17, 
 
 
 @pytest.mark.parametrize("idx", range(len(SEARCH_SHAPES)))
-def test_frozen_search_on_blurred_image_equals_oracle(ctx, port, idx):
-    """Frozen policy (the reference's --parallel scan): counts, visit codes, threshold and
-    result bit-identical to the oracle, with scan 1 bracketed on the tensor cores."""
+def test_search_on_blurred_image_equals_oracle(ctx, port, idx):
+    """Both reference policies (--parallel frozen scan, default sequential scan): counts,
+    visit codes, threshold and result bit-identical to the oracle, with scan 1 bracketed on
+    the tensor cores."""
     p, q, m, n, h, w = SEARCH_SHAPES[idx]
     rng = np.random.default_rng(200 + idx)
     img = _image(rng, p, q, smooth=idx % 2 == 0)
@@ -133,18 +134,21 @@ def test_frozen_search_on_blurred_image_equals_oracle(ctx, port, idx):
     blurred = port.blur(img)
     amap = port.local_autocorrelation(blurred, m, n, h, w)
     g = ctx.image(blurred)
-    s0 = ctx.split_stats()
-    for init in (None, 0.5):
-        a, va = ctx.transitive_search(t, g, amap, h, w, parallel=True, threads=3,
-                                      record_visits=True, init_threshold=init)
-        b, vb = port.transitive_search(t, blurred, amap, h, w, parallel=True, threads=3,
-                                       visits=True, init_threshold=init)
-        np.testing.assert_array_equal(va, vb)
-        assert_same_result(a, b, keys=RESULT_KEYS[:-1])
     er, ec = p - m + 1, q - n + 1
     G = -(-er // h) * -(-ec // w)
-    if G > 1:
-        assert ctx.split_stats()["screened"] - s0["screened"] == 2 * G, "split centre scan did not run"
+    # parallel=True: frozen threshold; parallel=False: the reference's default sequential scan
+    # (running threshold), replayed exactly -- both with scan 1 on the split planes
+    for par in (True, False):
+        for init in (None, 0.5):
+            s0 = ctx.split_stats()
+            a, va = ctx.transitive_search(t, g, amap, h, w, parallel=par, threads=3,
+                                          record_visits=True, init_threshold=init)
+            b, vb = port.transitive_search(t, blurred, amap, h, w, parallel=par, threads=3,
+                                           visits=True, init_threshold=init)
+            np.testing.assert_array_equal(va, vb, err_msg=f"par={par} init={init}")
+            assert_same_result(a, b, keys=RESULT_KEYS[:-1], msg=f"par={par} init={init}")
+            assert ctx.split_stats()["screened"] - s0["screened"] == G, \
+                "split centre scan did not run"
 
 
 @pytest.mark.parametrize("idx", [0, 1, 4])
@@ -175,3 +179,31 @@ def test_opta_match_with_blur_uses_split_planes(ctx, port):
     b, vb = port.match(t, img, mode="opta", parallel=True, threads=3, visits=True)
     np.testing.assert_array_equal(va, vb)
     assert_same_result(a, b)
+
+
+def test_many_survivors_are_bracketed_then_replayed(ctx, port):
+    """Weak elimination (a template without a true match) under the frozen policy: the
+    survivors' rho only matter for the argmax, so they are bracketed by one masked split pass
+    and the near-maximal ones replayed -- same result, counts and visit codes."""
+    rng = np.random.default_rng(77)
+    img = _image(rng, 400, 380)
+    blurred = port.blur(img)
+    t = np.clip(np.rint(rng.normal(128, 50, (16, 16))), 0, 255)
+    h = w = 3
+    amap = port.local_autocorrelation(blurred, 16, 16, h, w)
+    g = ctx.image(blurred)
+    E = (400 - 15) * (380 - 15)
+    G = -(-(400 - 15) // h) * -(-(380 - 15) // w)
+    for policy in ("frozen", "seeded"):
+        s0 = ctx.split_stats()
+        a, va = ctx.transitive_search(t, g, amap, h, w, policy=policy, record_visits=True)
+        if policy == "frozen":
+            b, vb = port.transitive_search(t, blurred, amap, h, w, parallel=True, threads=3,
+                                           visits=True)
+            np.testing.assert_array_equal(va, vb)
+            assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+            assert a.retained > max(9472, E // 64), "workload does not reach the split pass"
+            assert ctx.split_stats()["screened"] - s0["screened"] == G + E
+        else:
+            bb = port.brute(t, blurred)
+            assert (a.best_row, a.best_col, a.best_rho) == (bb.best_row, bb.best_col, bb.best_rho)
