@@ -147,7 +147,8 @@ def test_search_on_blurred_image_equals_oracle(ctx, port, idx):
                                            visits=True, init_threshold=init)
             np.testing.assert_array_equal(va, vb, err_msg=f"par={par} init={init}")
             assert_same_result(a, b, keys=RESULT_KEYS[:-1], msg=f"par={par} init={init}")
-            assert ctx.split_stats()["screened"] - s0["screened"] == G, \
+            # G centres (+ E when a large survivor set took the masked split pass)
+            assert ctx.split_stats()["screened"] - s0["screened"] in (G, G + er * ec), \
                 "split centre scan did not run"
 
 
