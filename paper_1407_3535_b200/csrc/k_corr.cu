@@ -837,9 +837,15 @@ __global__ void __launch_bounds__(256)
                 }
                 if (in && sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
             }
-            if (__any_sync(0xffffffffu, (smask | fmask) != 0u)) {  // warp-uniform, rare
+            // templates with a survivor / kept flat member in this warp (warp-uniform mask):
+            // only those are visited (weak templates of a batch keep most warps busy here,
+            // the others never)
+            unsigned todo = __reduce_or_sync(0xffffffffu, smask | fmask);
+            {
 #pragma unroll 1
-                for (int k = 0; k < sm.K; ++k) {
+                while (todo) {
+                    const int k = __ffs(todo) - 1;
+                    todo &= todo - 1u;
                     const bool fk = (fmask >> k) & 1u, sk = (smask >> k) & 1u;
                     const unsigned bfl = __ballot_sync(0xffffffffu, fk);
                     if (bfl) {
