@@ -602,6 +602,9 @@ def run_b200(args):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "weak",
+        # spread of the K timed steps (value uses the mean, as the contract says)
+        "ms_per_step_min": min(times), "ms_per_step_median": statistics.median(times),
+        "ms_per_step_max": max(times),
         "vs_baseline": None,
         "dtype": "u8 (s32 tensor-core dots, u32 window / cross sums), f64 epilogues",
         "data": "synthetic (seeded bit-deterministic 1/f^beta generator, SURVEY 8d)",

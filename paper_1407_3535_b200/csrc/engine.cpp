@@ -285,6 +285,10 @@ struct tm_ctx {
     DBuf<unsigned> egs_rows;  // per-extent-row retained counts of a batch's first candidate
     bool sa_ready = false;  // sa_c filled by this search's centre epilogue
     float2* batch_rec = nullptr;  // run_batch: the centre epilogue also writes the records
+    // run_batch: the centres' window statistics gathered once per batch (compact, per group)
+    DBuf<double> cs_mu, cs_om;
+    DBuf<uint8_t> cs_fl;
+    bool batch_cs = false;
     Pinned pin_tf, pin_td, pin_rows, pin_locs, pin_cnt, pin_egs;
     // row-strip search protocol state (tm_strip_search_*)
     struct StripState {
@@ -1115,9 +1119,11 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
             tc_run(ctx, img, ws, T, rs, g.h, task, &rows_dev, side_b);
             n1 = std::min(kListBlocks, int((size_t(nstrip) * g.tc + 255) / 256));
             const tmk::TailReduce tail = tail_to(ctx, n1 + n2, 0, op);  // n2 = 0 here
+            const tmk::CentreStats cs{ctx->cs_mu.p, ctx->cs_om.p, ctx->cs_fl.p};
             CK(tmk::centre_epilogue(job, g, rows_dev, wr, g.w, g.tc, 0, ctx->dotbuf.p,
                                     ctx->rho_c.p, ctx->deg_c.p, ctx->partials.p, n1, ctx->s,
-                                    task.c_last, &tail, nullptr, ctx->sa_c.p, ctx->batch_rec));
+                                    task.c_last, &tail, nullptr, ctx->sa_c.p, ctx->batch_rec,
+                                    ctx->batch_cs ? &cs : nullptr));
             HT("centre_epi");
             ctx->add(1);
         }
@@ -3056,13 +3062,22 @@ void run_batch(tm_ctx* ctx, tm_prep* prep, tm_image* img, const double* tmpls, i
 
     // 1. scan 1 (+ seeding) per template; the tensor-core centre epilogue writes the
     //    template's batch records directly, the seeding marks its seeded groups in them
+    //    (the centres' window statistics are gathered once for the whole batch)
+    ctx->cs_mu.ensure(G);
+    ctx->cs_om.ensure(G);
+    ctx->cs_fl.ensure(G);
+    CK(tmk::gather_centre_stats(g, ws.dev(),
+                                tmk::CentreStats{ctx->cs_mu.p, ctx->cs_om.p, ctx->cs_fl.p}, s));
+    ctx->add(1);
     for (int k = 0; k < K; ++k) {
         const Tmpl& T = Ts[k];
         const tmk::ReduceOp op_init = centre_op(ctx, P);
         float2* recs = B.rec.p + size_t(k) * G;
         ctx->batch_rec = recs;
+        ctx->batch_cs = true;
         centre_scan(ctx, simg, ws, T, g, &op_init);
         ctx->batch_rec = nullptr;
+        ctx->batch_cs = false;
         const bool recs_written = ctx->sa_ready;  // (the tensor-core epilogue ran)
         if (!ctx->sa_ready) {  // (the tensor-core epilogue writes it; keep the invariant)
             CK(tmk::sqrt_gap(ctx->rho_c.p, ctx->sa_c.p, G, s));

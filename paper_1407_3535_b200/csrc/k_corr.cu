@@ -207,7 +207,7 @@ __global__ void __launch_bounds__(256)
     k_centre_epi(CorrJob job, Grid g, const int* __restrict__ rows, int cbase, int sw, int nc,
                  int col0, const double* __restrict__ dot, double* rho_c, uint8_t* deg_c,
                  CellH* partials, int c_last, TailReduce tail, const int* __restrict__ gate,
-                 double* __restrict__ sa_out, float2* __restrict__ rec_out) {
+                 double* __restrict__ sa_out, float2* __restrict__ rec_out, CentreStats cs) {
     pdl_wait();
     if (gate && !*gate) return;  // speculative launch not confirmed (every block: no ticket)
     __shared__ Cell scratch[8];
@@ -223,8 +223,12 @@ __global__ void __launch_bounds__(256)
         const int c = (c_last >= 0 && col0 + k == g.tc - 1) ? c_last : cbase + k * sw;
         const size_t gi = size_t(g.ti_lo + yi) * g.tc + col0 + k;
         const size_t kk = size_t(r) * job.st.ec + c;
-        const bool wflat = job.st.flat[kk];
-        const double rho = zncc_epilogue(dot[gi], ts, job.st.mu[kk], job.st.omega[kk], wflat);
+        // a template batch reads the centres' statistics from compact per-group arrays
+        // (gathered once for all templates: coalesced 17 B instead of ~51 B of sectors)
+        const bool wflat = cs.mu ? cs.fl[gi] != 0 : job.st.flat[kk] != 0;
+        const double mu_w = cs.mu ? cs.mu[gi] : job.st.mu[kk];
+        const double om_w = cs.mu ? cs.om[gi] : job.st.omega[kk];
+        const double rho = zncc_epilogue(dot[gi], ts, mu_w, om_w, wflat);
         const bool deg = ts.flat || wflat;
         rho_c[gi] = rho;
         deg_c[gi] = deg;
@@ -241,6 +245,22 @@ __global__ void __launch_bounds__(256)
     best = block_best(best, scratch);
     if (threadIdx.x == 0) store_partial(best, partials, blockIdx.x);
     tail_reduce(tail, scratch);
+}
+
+// The window statistics of every group centre, compacted per group (template batches).
+__global__ void __launch_bounds__(256)
+    k_gather_centre_stats(Grid g, DevStats st, double* __restrict__ mu_c,
+                          double* __restrict__ om_c, uint8_t* __restrict__ fl_c) {
+    pdl_wait();
+    const size_t G0 = size_t(g.ti_lo) * g.tc, G1 = size_t(g.ti_hi) * g.tc;
+    for (size_t gi = G0 + blockIdx.x * size_t(blockDim.x) + threadIdx.x; gi < G1;
+         gi += size_t(gridDim.x) * blockDim.x) {
+        const int ti = int(gi / size_t(g.tc)), tj = int(gi - size_t(ti) * g.tc);
+        const size_t kk = size_t(g.center_row(ti)) * st.ec + g.center_col(tj);
+        mu_c[gi] = st.mu[kk];
+        om_c[gi] = st.omega[kk];
+        fl_c[gi] = st.flat[kk];
+    }
 }
 
 // ---- sparse: one warp per location ----------------------------------------------------
@@ -1141,10 +1161,17 @@ cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last,
                             const TailReduce* tail, const int* gate, double* sa_out,
-                            float2* rec_out) {
+                            float2* rec_out, const CentreStats* cs) {
     launch_pdl(k_centre_epi, dim3(n_partials), dim3(256), 0, s, job, to_grid(g), rows, cbase, sw,
                nc, col0, dot, rho_c, deg_c, partials, c_last, tail ? *tail : TailReduce{}, gate,
-               sa_out, rec_out);
+               sa_out, rec_out, cs ? *cs : CentreStats{});
+    return cudaGetLastError();
+}
+
+cudaError_t gather_centre_stats(GridDesc g, DevStats st, CentreStats out, cudaStream_t s) {
+    const size_t G = size_t(g.ti_hi - g.ti_lo) * g.tc;
+    launch_pdl(k_gather_centre_stats, dim3(int(std::min<size_t>((G + 255) / 256, 148 * 8))),
+               dim3(256), 0, s, to_grid(g), st, out.mu, out.om, out.fl);
     return cudaGetLastError();
 }
 

@@ -371,12 +371,19 @@ cudaError_t corr_dense_f64(const CorrJob& job, double* surface, CellH* partials,
                            cudaStream_t s);
 
 // Epilogue of a K-split centre scan (rho/deg from the accumulated dots + argmax partials).
+struct CentreStats {  // window statistics of the group centres, one entry per group
+    double* mu = nullptr;
+    double* om = nullptr;
+    uint8_t* fl = nullptr;
+};
 cudaError_t centre_epilogue(const CorrJob& job, GridDesc g, const int* rows, int cbase, int sw,
                             int nc, int col0, const double* dot, double* rho_c, uint8_t* deg_c,
                             CellH* partials, int n_partials, cudaStream_t s, int c_last = -1,
                             const TailReduce* tail = nullptr, const int* gate = nullptr,
                             double* sa_out = nullptr,
-                            float2* rec_out = nullptr);
+                            float2* rec_out = nullptr, const CentreStats* cs = nullptr);
+// cs[gi] = statistics at group gi's centre (a template batch gathers them once)
+cudaError_t gather_centre_stats(GridDesc g, DevStats st, CentreStats out, cudaStream_t s);
 // rho_c[i*tc + col] = rho[i] (clipped last centre column after a list evaluation).
 cudaError_t scatter_column(const double* rho, const uint8_t* deg, int n, int tc, int col,
                            double* rho_c, uint8_t* deg_c, cudaStream_t s);
