@@ -56,6 +56,12 @@ Grid to_grid(GridDesc d) {
 constexpr int kTcThreads = 320;  // producer, MMA, 8 epilogue warps
 constexpr int kTcMaxStages = 64;
 constexpr int kTcBarBytes = 2048;  // barriers + TMEM slot at the start of shared memory
+constexpr int kTcSchedBytes = 16 * 1024;  // staged row schedule
+// Epilogue staging: a warp's 512 output columns of one row (window statistics, visit codes)
+// are loaded coalesced and transposed through shared memory to the TMEM layout (lane a owns
+// columns 16a..16a+15); 17-element lane pitch = conflict-free both ways.
+constexpr int kEpiWarpDoubles = 512 + 32;
+constexpr int kEpiBytes = 8 * kEpiWarpDoubles * 8;
 constexpr int kTcCols = 2048;  // output columns per tile (M=128 rows x 16 phases)
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -196,7 +202,7 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
-    const bool sched_smem = task.sched_total * 16 <= P.header - kTcBarBytes;
+    const bool sched_smem = task.sched_total * 16 <= kTcSchedBytes;
     if (sched_smem)
         for (int i = tid; i < task.sched_total; i += blockDim.x) ssched[i] = __ldg(task.sched + i);
     const int4* sched = sched_smem ? ssched : task.sched;
@@ -390,6 +396,11 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
         const TStats ts = TStats{job.ts.mu, job.ts.omega, job.ts.mn, job.ts.flat};
         const DevStats st = job.st;
         Cell best = no_cell();
+        // dense modes without a rho surface: FP32 pre-test against the thread's exact best
+        const bool can_skip = (MODE == 0 || MODE == 2) && !task.out_rho && !(task.dbg_flags & 4);
+        bool best_ok = false;
+        float best_f = -INFINITY;
+        const double tmean = __dmul_rn(ts.mn, ts.mu);  // detail.hpp:49 mn * ts.mu
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             if (!tile_on(t)) continue;
@@ -431,7 +442,6 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     tmem_ld16(addr + uint32_t(32 * task.kp), v2);
                     tmem_zero16(addr + uint32_t(32 * task.kp));
                     const size_t rb = size_t(r) * st.ec + cb;
-                    const double tmean = __dmul_rn(ts.mn, ts.mu);
 #pragma unroll
                     for (int ph = 0; ph < 16; ++ph) {
                         if (!((cmask >> ph) & 1u)) continue;
@@ -484,37 +494,125 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     continue;
                 }
                 const size_t rb = size_t(r) * st.ec + cb;
-                // MODE 2: the visit codes first -- only the (rare) survivors' statistics are
-                // loaded; a thread whose 16 columns hold none skips the row
+                const size_t rowb = size_t(r) * st.ec;
+                const int cw = c0 + 512 * q4;  // the warp's first column (lane: cw + 16*lane)
+                double* wd = reinterpret_cast<double*>(sm + kTcBarBytes + kTcSchedBytes) +
+                             size_t(ew) * kEpiWarpDoubles;
+                uint8_t* wb = reinterpret_cast<uint8_t*>(wd);
+                // MODE 2: the visit codes first (coalesced, transposed through shared memory);
+                // a warp whose 512 columns hold no survivor skips the row
                 uint32_t on2 = cmask;
+                bool staged = true;
                 if (MODE == 2) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int idx = j * 32 + lane, col = cw + idx;
+                        wb[idx + (idx >> 4)] = col < task.c_lim ? __ldg(task.mask + rowb + col)
+                                                                : uint8_t(0);
+                    }
+                    __syncwarp();
                     on2 = 0u;
 #pragma unroll
                     for (int ph = 0; ph < 16; ++ph)
-                        if (((cmask >> ph) & 1u) && task.mask[rb + ph] == 2) on2 |= 1u << ph;
-                    if (!on2) continue;
+                        if (((cmask >> ph) & 1u) && wb[17 * lane + ph] == 2) on2 |= 1u << ph;
+                    __syncwarp();
+                    const unsigned nsurv = __reduce_add_sync(0xffffffffu, unsigned(__popc(on2)));
+                    if (nsurv == 0u) continue;
+                    staged = nsurv >= 96u;  // sparse rows: gather only the survivors' statistics
                 }
-                // all loads first (independent, predicated), then the FP64 epilogues
                 uint8_t fl[16];
                 double mu[16], om[16];
+                if (staged) {
+                    // the warp's 512 columns of flat / mu / omega: coalesced loads (all issued
+                    // first), then one array at a time through the warp's staging buffer
+                    uint8_t gf[16];
+                    double gm[16], go[16];
 #pragma unroll
-                for (int ph = 0; ph < 16; ++ph) {
-                    const bool on = (on2 >> ph) & 1u;
-                    const size_t kk = on ? rb + ph : 0;
-                    fl[ph] = on ? st.flat[kk] : uint8_t(1);
-                    mu[ph] = on ? st.mu[kk] : 0.0;
-                    om[ph] = on ? st.omega[kk] : 0.0;
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = cw + j * 32 + lane;
+                        const bool in = col < task.c_lim;
+                        const size_t kk = in ? rowb + col : rowb;
+                        gf[j] = in ? __ldg(st.flat + kk) : uint8_t(1);
+                        gm[j] = in ? __ldg(st.mu + kk) : 0.0;
+                        go[j] = in ? __ldg(st.omega + kk) : 0.0;
+                    }
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int idx = j * 32 + lane;
+                        wb[idx + (idx >> 4)] = gf[j];
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) fl[ph] = wb[17 * lane + ph];
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int idx = j * 32 + lane;
+                        wd[idx + (idx >> 4)] = gm[j];
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) mu[ph] = wd[17 * lane + ph];
+                    __syncwarp();
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int idx = j * 32 + lane;
+                        wd[idx + (idx >> 4)] = go[j];
+                    }
+                    __syncwarp();
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) om[ph] = wd[17 * lane + ph];
+                    __syncwarp();
+                } else {
+                    // all loads first (independent, predicated), then the FP64 epilogues
+#pragma unroll
+                    for (int ph = 0; ph < 16; ++ph) {
+                        const bool on = (on2 >> ph) & 1u;
+                        const size_t kk = on ? rb + ph : 0;
+                        fl[ph] = on ? st.flat[kk] : uint8_t(1);
+                        mu[ph] = on ? st.mu[kk] : 0.0;
+                        om[ph] = on ? st.omega[kk] : 0.0;
+                    }
                 }
 #pragma unroll
                 for (int ph = 0; ph < 16; ++ph) {
                     if (!((on2 >> ph) & 1u)) continue;
                     const int c = cb + ph;
                     const bool wflat = fl[ph];
+                    if (can_skip && best_ok) {
+                        // argmax only: a location whose FP32 quotient is below the warp's
+                        // best (non-degenerate, exact) rho by more than the quotient's error
+                        // (< 1e-6 for |q| < 2; margin 2e-5) cannot win -- no FP64 division
+                        if (wflat) continue;
+                        const double num =
+                            __dsub_rn(double(int(v[ph])), __dmul_rn(tmean, mu[ph]));
+                        const float q = __fdividef(__double2float_rn(num),
+                                                   __double2float_rn(__dmul_rn(ts.omega, om[ph])));
+                        if (fabsf(q) < 2.f && q + 2e-5f < best_f) continue;
+                    }
                     const double rho = zncc_epilogue(double(int(v[ph])), ts, mu[ph], om[ph], wflat);
                     const bool deg = ts.flat || wflat;
                     if (task.out_rho) task.out_rho[rb + ph] = rho;
                     const Cell cand = make_cell(r, c, rho, deg);
-                    if (better(cand, best)) best = cand;
+                    if (better(cand, best)) {
+                        best = cand;
+                        if (!deg) {
+                            best_ok = true;
+                            best_f = fmaxf(best_f, __double2float_rd(rho));
+                        }
+                    }
+                }
+                if (can_skip) {
+                    // the pre-test limit is shared by the warp after every row (any exact
+                    // non-degenerate rho found so far bounds the final maximum from below)
+                    const int bits = __float_as_int(best_ok ? best_f : -INFINITY);
+                    const int key = bits >= 0 ? bits : bits ^ 0x7fffffff;  // order-preserving
+                    const int top = __reduce_max_sync(0xffffffffu, key);
+                    const float lim = __int_as_float(top >= 0 ? top : top ^ 0x7fffffff);
+                    if (lim > -INFINITY) {
+                        best_ok = true;
+                        best_f = lim;
+                    }
                 }
             }
             asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
@@ -849,7 +947,7 @@ TcPlan tc_plan(int m, int n, int sr, size_t smem_budget) {
     P.a_slot = (P.a_bytes + 127) / 128 * 128;
     // header: barriers + up to 16 KB of staged row schedule; at least 16 ring stages; B
     // gets the rest (the ring grows back into what B leaves)
-    P.header = kTcBarBytes + 16 * 1024;
+    P.header = kTcBarBytes + kTcSchedBytes + kEpiBytes;
     const size_t fixed = size_t(16) * P.a_slot + P.header;
     const size_t entry = size_t(16) * P.kx;
     const int per_chunk = int((smem_budget - fixed) / entry);
