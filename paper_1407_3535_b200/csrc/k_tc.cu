@@ -527,14 +527,26 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                     // first), then one array at a time through the warp's staging buffer
                     uint8_t gf[16];
                     double gm[16], go[16];
+                    // row pointers at this lane's first column: element j is 32*j further
+                    const uint8_t* pf = st.flat + rowb + cw + lane;
+                    const double* pm = st.mu + rowb + cw + lane;
+                    const double* po = st.omega + rowb + cw + lane;
+                    const int left = task.c_lim - cw - lane;  // columns j with 32*j < left exist
+                    if (left > 480) {  // warp-uniform for all but the last column tile
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = cw + j * 32 + lane;
-                        const bool in = col < task.c_lim;
-                        const size_t kk = in ? rowb + col : rowb;
-                        gf[j] = in ? __ldg(st.flat + kk) : uint8_t(1);
-                        gm[j] = in ? __ldg(st.mu + kk) : 0.0;
-                        go[j] = in ? __ldg(st.omega + kk) : 0.0;
+                        for (int j = 0; j < 16; ++j) {
+                            gf[j] = __ldg(pf + 32 * j);
+                            gm[j] = __ldg(pm + 32 * j);
+                            go[j] = __ldg(po + 32 * j);
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            const bool in = 32 * j < left;
+                            gf[j] = in ? __ldg(pf + 32 * j) : uint8_t(1);
+                            gm[j] = in ? __ldg(pm + 32 * j) : 0.0;
+                            go[j] = in ? __ldg(po + 32 * j) : 0.0;
+                        }
                     }
 #pragma unroll
                     for (int j = 0; j < 16; ++j) {
@@ -574,22 +586,30 @@ __global__ void __launch_bounds__(kTcThreads, 1) k_tc_corr(TcJob job, TcTask tas
                         om[ph] = on ? st.omega[kk] : 0.0;
                     }
                 }
+                uint32_t need = on2;
+                if (can_skip && best_ok) {
+                    // argmax only: a location whose FP32 quotient is below the warp's best
+                    // (non-degenerate, exact) rho by more than the quotient's error (< 1e-6
+                    // for |q| < 2; margin 2e-5) cannot win -- no FP64 division.  Branch-free:
+                    // the locations that still need the exact epilogue are collected in a mask
+                    uint32_t skip = 0u;
 #pragma unroll
-                for (int ph = 0; ph < 16; ++ph) {
-                    if (!((on2 >> ph) & 1u)) continue;
-                    const int c = cb + ph;
-                    const bool wflat = fl[ph];
-                    if (can_skip && best_ok) {
-                        // argmax only: a location whose FP32 quotient is below the warp's
-                        // best (non-degenerate, exact) rho by more than the quotient's error
-                        // (< 1e-6 for |q| < 2; margin 2e-5) cannot win -- no FP64 division
-                        if (wflat) continue;
+                    for (int ph = 0; ph < 16; ++ph) {
                         const double num =
                             __dsub_rn(double(int(v[ph])), __dmul_rn(tmean, mu[ph]));
                         const float q = __fdividef(__double2float_rn(num),
                                                    __double2float_rn(__dmul_rn(ts.omega, om[ph])));
-                        if (fabsf(q) < 2.f && q + 2e-5f < best_f) continue;
+                        const bool sk = fl[ph] != 0 || (fabsf(q) < 2.f && q + 2e-5f < best_f);
+                        skip |= (sk ? 1u : 0u) << ph;
                     }
+                    need &= ~skip;
+                }
+                if (need)
+#pragma unroll
+                for (int ph = 0; ph < 16; ++ph) {
+                    if (!((need >> ph) & 1u)) continue;
+                    const int c = cb + ph;
+                    const bool wflat = fl[ph];
                     const double rho = zncc_epilogue(double(int(v[ph])), ts, mu[ph], om[ph], wflat);
                     const bool deg = ts.flat || wflat;
                     if (task.out_rho) task.out_rho[rb + ph] = rho;
