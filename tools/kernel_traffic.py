@@ -14,6 +14,7 @@ import sys
 # clipped-column passes; one search is assumed per report)
 PHASE = [("k_acg<3, 256, 0, 1>", "autocorr_sec"), ("k_rco3_s", "autocorr_sec"),
          ("k_rco_epi<2", "autocorr_sec"), ("k_rco_epg<2", "autocorr_sec"),
+         ("k_rco_epg9<2", "autocorr_sec"),
          ("k_rco3_clip", "autocorr_sec"), ("k_rco5_s", "autocorr_count"),
          ("k_rco5_cnt", "autocorr_count"), ("k_seg_order", "autocorr_count"),
          ("k_acg<5, 128", "autocorr_count"),
