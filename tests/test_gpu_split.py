@@ -208,3 +208,20 @@ def test_many_survivors_are_bracketed_then_replayed(ctx, port):
         else:
             bb = port.brute(t, blurred)
             assert (a.best_row, a.best_col, a.best_rho) == (bb.best_row, bb.best_col, bb.best_rho)
+
+
+def test_candidate_list_overflow_falls_back_to_the_replica(ctx, port):
+    """A periodic non-integer image whose template matches exactly at every second row and
+    column: more than 2^20 tied candidates survive the screening, the list overflows and the
+    dense FP64 replica decides (first tie in (row, col) order, as better_candidate says)."""
+    cell = np.array([[10.25, 200.5], [77.75, 31.125]])
+    img = np.tile(cell, (1050, 1050))
+    t = np.tile(np.array([[10.0, 200.0], [78.0, 31.0]]), (8, 8))
+    g = ctx.image(img)
+    assert not g.is_integer
+    s0 = ctx.split_stats()
+    a = ctx.brute_force_match(t, g)
+    assert ctx.split_stats()["exact"] == s0["exact"], "expected the overflow fallback"
+    b = port.brute(t, img)
+    assert_same_result(a, b, keys=RESULT_KEYS[:-1])
+    assert (a.best_row, a.best_col) == (0, 0)
