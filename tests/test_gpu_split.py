@@ -225,3 +225,12 @@ def test_candidate_list_overflow_falls_back_to_the_replica(ctx, port):
     b = port.brute(t, img)
     assert_same_result(a, b, keys=RESULT_KEYS[:-1])
     assert (a.best_row, a.best_col) == (0, 0)
+
+
+def test_randomised_differential_sample():
+    """A short run of tools/split_fuzz.py (random non-integer images, every policy, visit maps
+    and all result fields against the oracle)."""
+    out = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "split_fuzz.py"), "60", "5"],
+                         cwd=ROOT, env=dict(os.environ, PYTHONPATH=ROOT), capture_output=True,
+                         text=True, timeout=900)
+    assert out.returncode == 0 and "0 mismatching" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
