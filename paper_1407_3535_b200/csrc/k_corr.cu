@@ -833,30 +833,43 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
             for (int k = 0; k < KP; ++k)
                 rec[k] = k < sm.K ? __ldg(sm.rec + size_t(k) * sm.G + gi) : make_float2(0.f, -2.f);
-            unsigned smask = 0u, fmask = 0u;  // survivors / kept flat members, bit k
+            // member: seeded group -> kept (evaluated already); else eliminated iff the bound
+            // holds (FP32 with a 4e-6 margin, FP64 inside it); kept flat members are not
+            // listed (rho 0 without a dot).  Branch-free per template: bit masks of the
+            // certain eliminations, of the templates inside the margin (decided exactly after
+            // the loop; rare) and of the seeded groups.
+            unsigned el = 0u, amb = 0u, sd = 0u;
+            const bool testable = member && !fv;
 #pragma unroll
             for (int k = 0; k < KP; ++k) {
-                if (k >= sm.K) break;
-                // member: seeded group -> kept (evaluated already); else eliminated iff the
-                // bound holds (FP32 with a 4e-6 margin, FP64 inside it); kept flat members
-                // are not listed (rho 0 without a dot)
-                uint8_t vis = member ? 2 : 0;
-                if (member && rec[k].y != -2.f && !fv && rec[k].y >= 0.f && ((thr_ok >> k) & 1u)) {
-                    const float f = fmaf(rec[k].x, bf, rec[k].y * sq);
-                    const bool el = tbf[k] >= f + 4e-6f ||
-                                    (tbf[k] >= f - 4e-6f &&
-                                     sec_exact_multi(sm, k, size_t(k) * sm.G + gi, b, x));
-                    if (el) {
-                        vis = 1;
-                        ++n_elim[k];
-                    }
-                }
-                if (vis == 2 && rec[k].y != -2.f) {
-                    if (fv) fmask |= 1u << k;
-                    else smask |= 1u << k;
-                }
-                if (in && sm.visits) sm.visits[size_t(k) * sm.E + kk] = vis;
+                const float ry = rec[k].y;  // -1 degenerate centre, -2 seeded group (or k >= K)
+                const float f = fmaf(rec[k].x, bf, ry * sq);
+                const bool t = testable && ry >= 0.f && ((thr_ok >> k) & 1u);
+                const bool sure = tbf[k] >= f + 4e-6f;
+                const bool maybe = !sure && tbf[k] >= f - 4e-6f;
+                el |= (t && sure ? 1u : 0u) << k;
+                amb |= (t && maybe ? 1u : 0u) << k;
+                sd |= (ry == -2.f ? 1u : 0u) << k;
             }
+            while (amb) {  // inside the FP32 margin: the exact FP64 bound test
+                const int k = __ffs(amb) - 1;
+                amb &= amb - 1u;
+                if (sec_exact_multi(sm, k, size_t(k) * sm.G + gi, b, x)) el |= 1u << k;
+            }
+            const unsigned kmask = sm.K >= 32 ? 0xffffffffu : (1u << sm.K) - 1u;
+            const unsigned listed = member ? (~el & ~sd & kmask) : 0u;  // kept, not seeded
+            const unsigned smask = fv ? 0u : listed, fmask = fv ? listed : 0u;
+            if (in && sm.visits) {
+                uint8_t* vp = sm.visits + kk;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    if (k >= sm.K) break;
+                    *vp = member ? (((el >> k) & 1u) ? uint8_t(1) : uint8_t(2)) : uint8_t(0);
+                    vp += sm.E;
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KP; ++k) n_elim[k] += (el >> k) & 1u;
             // templates with a survivor / kept flat member in this warp (warp-uniform mask):
             // only those are visited (weak templates of a batch keep most warps busy here,
             // the others never)
