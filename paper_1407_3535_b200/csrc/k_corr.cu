@@ -847,9 +847,9 @@ __global__ void __launch_bounds__(256)
                 const bool t = testable && ry >= 0.f && ((thr_ok >> k) & 1u);
                 const bool sure = tbf[k] >= f + 4e-6f;
                 const bool maybe = !sure && tbf[k] >= f - 4e-6f;
-                el |= (t && sure ? 1u : 0u) << k;
-                amb |= (t && maybe ? 1u : 0u) << k;
-                sd |= (ry == -2.f ? 1u : 0u) << k;
+                if (t && sure) el |= 1u << k;  // (predicated ORs with an immediate)
+                if (t && maybe) amb |= 1u << k;
+                if (ry == -2.f) sd |= 1u << k;
             }
             while (amb) {  // inside the FP32 margin: the exact FP64 bound test
                 const int k = __ffs(amb) - 1;
@@ -861,10 +861,11 @@ __global__ void __launch_bounds__(256)
             const unsigned smask = fv ? 0u : listed, fmask = fv ? listed : 0u;
             if (in && sm.visits) {
                 uint8_t* vp = sm.visits + kk;
+                const unsigned base = member ? 2u : 0u;  // el is 0 for a non-member
 #pragma unroll
                 for (int k = 0; k < KP; ++k) {
                     if (k >= sm.K) break;
-                    *vp = member ? (((el >> k) & 1u) ? uint8_t(1) : uint8_t(2)) : uint8_t(0);
+                    *vp = uint8_t(base - ((el >> k) & 1u));  // 2 kept, 1 eliminated, 0 centre
                     vp += sm.E;
                 }
             }
