@@ -1,7 +1,9 @@
 """Randomised differential check of the split-plane paths against the oracle.
 
     python tools/split_fuzz.py [cases] [seed]        (FUZZ_INTEGER=1: 8-bit images -> the
-                                                      kind::i8 passes and their FP32 pre-test)
+                                                      kind::i8 passes and their FP32 pre-test;
+                                                      FUZZ_LARGE=1: wide images, half the
+                                                      templates without a match)
 
 Non-integer images of random shape / smoothness / contrast (near-flat patches, values at
 both ends of [0, 256), exact duplicates of the best window), integer templates; brute force
@@ -23,6 +25,8 @@ KEYS = ("best_row", "best_col", "best_rho", "best_degenerate", "final_threshold"
 
 def make_case(rng):
     p, q = int(rng.integers(24, 220)), int(rng.integers(24, 260))
+    if os.environ.get("FUZZ_LARGE") == "1":  # several 2048-column tiles, dense survivor rows
+        p, q = int(rng.integers(300, 700)), int(rng.integers(1800, 2700))
     m, n = int(rng.integers(2, min(p, 70))), int(rng.integers(2, min(q, 70)))
     kind = rng.integers(0, 4)
     if kind == 0:
@@ -49,6 +53,8 @@ def make_case(rng):
     r0, c0 = int(rng.integers(0, p - m + 1)), int(rng.integers(0, q - n + 1))
     t = np.clip(np.rint(img[r0:r0 + m, c0:c0 + n] * rng.uniform(0.8, 1.2) +
                         rng.uniform(-10, 10) + rng.normal(0, rng.uniform(0, 6), (m, n))), 0, 255)
+    if os.environ.get("FUZZ_LARGE") == "1" and rng.random() < 0.5:
+        t = np.clip(np.rint(rng.normal(128, 50, (m, n))), 0, 255)  # no match: weak elimination
     if rng.random() < 0.25:  # plant an exact duplicate of the cut window
         r1, c1 = int(rng.integers(0, p - m + 1)), int(rng.integers(0, q - n + 1))
         img[r1:r1 + m, c1:c1 + n] = img[r0:r0 + m, c0:c0 + n]
