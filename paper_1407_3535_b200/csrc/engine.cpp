@@ -270,7 +270,9 @@ struct tm_ctx {
     DBuf<int> split_gidx;
     DBuf<uint8_t> split_flag;
     int64_t split_centres = 0;  // centres bracketed by the split centre scan
-    bool tc_split = true;    // TMATCH_TC_SPLIT=0: non-integer images stay on the FP64 replica
+    // TMATCH_TC_SPLIT: 0 = non-integer images stay on the FP64 replica, 1 (default) = split
+    // planes when the pass is large enough to pay for their fixed cost, 2 = always
+    int tc_split = 1;
     int64_t split_screened = 0, split_exact = 0;  // locations bracketed / re-evaluated exactly
     DBuf<float> tf;
     DBuf<double> td;
@@ -831,8 +833,12 @@ tmk::SplitModel split_model(const Tmpl& T) {
 
 // Non-integer image + integer template: the byte planes for the split tensor-core
 // screening, made on first use.  False when a pixel lies outside [0, 256) (FP64 replica).
-bool split_path(tm_ctx* ctx, tm_image* img, const Tmpl& T) {
-    if (!ctx->tc || !ctx->tc_split || img->integer || !T.integer || T.ts.flat) return false;
+// work = multiply-adds of the pass, min_work = the size below which the FP64 replica is as
+// fast (measured: brute force crosses over near 256^2 x 32^2, scan 1 near 5,000 centres of
+// 32^2; tools/tiny_split_probe.py).
+bool split_path(tm_ctx* ctx, tm_image* img, const Tmpl& T, double work, double min_work) {
+    if (!ctx->tc || ctx->tc_split <= 0 || img->integer || !T.integer || T.ts.flat) return false;
+    if (ctx->tc_split == 1 && work < min_work) return false;
     if (img->row_lo != 0 || img->row_hi < img->p) return false;  // strip images: 8-bit only
     if (!tmk::tc_supported(T.m, T.n) || tmk::tc_plan(T.m, T.n, 1, kTcSmemBudget).nch == 0)
         return false;
@@ -1239,8 +1245,10 @@ void centre_scan(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
 // running threshold only rises from scan 1's, so members certainly eliminated at it stay
 // eliminated; every other member's group gets its exact rho_c (the replay re-tests them).
 bool split_centres_ok(tm_ctx* ctx, tm_image* img, const Tmpl& T, const tmk::GridDesc& g) {
+    const double work = double(g.tr) * g.tc * T.m * T.n;
     return g.h <= tmk::kTcMaxClasses && g.ti_lo == 0 && g.ti_hi == g.tr &&
-           split_path(ctx, img, T) && tmk::tc_plan(T.m, T.n, g.h, kTcSmemBudget).nch > 0;
+           split_path(ctx, img, T, work, 2097152.0) &&
+           tmk::tc_plan(T.m, T.n, g.h, kTcSmemBudget).nch > 0;
 }
 
 // The centres listed in split_locs / split_gidx (count on the device) -> exact rho by the
@@ -1937,7 +1945,8 @@ void eval_survivors(tm_ctx* ctx, tm_image* img, const WS& ws, const Tmpl& T,
         // seeded): bracket them all on the split planes (masked by the visit codes) and
         // replay the few that can still win
         if (!rho_loc && survivors > std::max<unsigned long long>(16 * kListBlocks, E / 64) &&
-            g.ti_lo == 0 && g.ti_hi == g.tr && split_path(ctx, img, T) &&
+            g.ti_lo == 0 && g.ti_hi == g.tr &&
+            split_path(ctx, img, T, double(E) * T.m * T.n, 67108864.0) &&
             brute_split(ctx, img, ws, T, visits))
             return;
         const tmk::CorrJob job = make_job(ctx, img, ws, T);
@@ -2319,7 +2328,8 @@ tm_match_result brute(tm_ctx* ctx, tm_image* img, const Tmpl& T, double* surface
         CK(tmk::corr_band(band_job(ctx, img, job), t, ctx->partials.p, &np, ctx->s));
         ctx->add(1);
         reduce_to(ctx, np, 2);
-    } else if (!surface && split_path(ctx, img, T) && brute_split(ctx, img, ws, T)) {
+    } else if (!surface && split_path(ctx, img, T, double(E) * T.m * T.n, 67108864.0) &&
+               brute_split(ctx, img, ws, T)) {
         // screened on the tensor cores, the near-maximal locations re-evaluated exactly
     } else {
         ctx->partials.ensure(kListBlocks);
@@ -2526,7 +2536,7 @@ int tm_ctx_create(int device, tm_ctx** out) {
         if (const char* e = std::getenv("TMATCH_AUTOCORR")) ctx->ac_fused = std::strcmp(e, "colwalk") != 0;
         if (const char* e = std::getenv("TMATCH_WSTATS")) ctx->ws4 = std::strcmp(e, "column") != 0;
         if (const char* e = std::getenv("TMATCH_TC")) ctx->tc = std::strcmp(e, "0") != 0;
-        if (const char* e = std::getenv("TMATCH_TC_SPLIT")) ctx->tc_split = std::strcmp(e, "0") != 0;
+        if (const char* e = std::getenv("TMATCH_TC_SPLIT")) ctx->tc_split = std::atoi(e);
         CK(cudaSetDevice(device));
         CK(cudaStreamCreateWithFlags(&ctx->s, cudaStreamNonBlocking));
         cudaMemPool_t pool;

@@ -19,6 +19,24 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
+@pytest.fixture(scope="module")
+def ctx():
+    """A context with the split planes forced (TMATCH_TC_SPLIT=2): by default passes below a
+    work threshold stay on the FP64 replica, and these tests use small images."""
+    from paper_1407_3535_b200 import api
+    old = os.environ.get("TMATCH_TC_SPLIT")
+    os.environ["TMATCH_TC_SPLIT"] = "2"
+    try:
+        c = api.Context(0)
+    finally:
+        if old is None:
+            os.environ.pop("TMATCH_TC_SPLIT", None)
+        else:
+            os.environ["TMATCH_TC_SPLIT"] = old
+    yield c
+    c.close()
+
+
 def _image(rng, p, q, smooth=True):
     base = np.cumsum(np.cumsum(rng.normal(size=(p, q)), 0), 1) if smooth else rng.normal(size=(p, q))
     return np.clip(np.rint((base - base.min()) / (np.ptp(base) + 1e-9) * 255), 0, 255)
@@ -234,3 +252,19 @@ def test_randomised_differential_sample():
                          cwd=ROOT, env=dict(os.environ, PYTHONPATH=ROOT), capture_output=True,
                          text=True, timeout=900)
     assert out.returncode == 0 and "0 mismatching" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
+
+
+def test_default_threshold_keeps_tiny_passes_on_the_replica(port):
+    """Default mode (TMATCH_TC_SPLIT unset): a 96x96 search stays on the FP64 replica (faster
+    there), a 600x600 one takes the split planes; both equal the oracle."""
+    from paper_1407_3535_b200 import api
+    rng = np.random.default_rng(4)
+    with api.Context(0) as c:
+        for size, m, expect_split in ((96, 16, False), (600, 32, True)):
+            img = _image(rng, size, size)
+            blurred = port.blur(img)
+            t = _template(rng, img, m, m)
+            s0 = c.split_stats()
+            a = c.brute_force_match(t, c.image(blurred))
+            assert_same_result(a, port.brute(t, blurred), keys=RESULT_KEYS[:-1])
+            assert (c.split_stats()["screened"] > s0["screened"]) == expect_split

@@ -19,6 +19,8 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from oracle.binding import Oracle  # noqa: E402  (checker only)
 from paper_1407_3535_b200 import api  # noqa: E402
 
+os.environ.setdefault("TMATCH_TC_SPLIT", "2")  # force the split planes on small images too
+
 KEYS = ("best_row", "best_col", "best_rho", "best_degenerate", "final_threshold", "centers",
         "eliminated", "retained", "ops")
 
